@@ -1,0 +1,179 @@
+/*
+ * gscache.h -- C ABI of the B200-native GSCache hot path: real-time fitting and querying of
+ * the multi-level 3D-Gaussian path-space radiance cache of arXiv 2507.19718.
+ *
+ * PAPER.md lines are cited as P:<line>; SURVEY.md 8(c) readings as C1..C8 / A1..A19 and
+ * restated in DESIGN.md.  The paper exposes its cache "via a C-style API" (sec.3.7);
+ * these are the calls of its problem statement: the renderer supplies attenuated radiance
+ * samples with their path length (P:9, sec.3.5) and reads the cache back.
+ *
+ * Conventions
+ *  - Pointers marked "host or device" may point to either; the library detects the kind with
+ *    cudaPointerGetAttributes and stages host data through its own pinned buffers.
+ *  - Ownership: all buffers passed in stay owned by the caller and must stay valid until
+ *    the work enqueued on `stream` completes.  The library owns parameters, AdamW state,
+ *    evaluation records, grids, culling lists and scratch (cudaMalloc at create/reserve).
+ *  - Errors: argument errors return GC_ERR_ARG with no side effect.  Data problems are not
+ *    errors: non-finite samples, path_len <= 0 and non-finite gradients are dropped and
+ *    counted in gc_fit_stats.  Asynchronous CUDA/NCCL failures are sticky and
+ *    returned by the next call.  No C++ exception crosses the ABI.  gc_last_error()
+ *    returns a thread-local message for the last non-OK status.
+ *  - Streams: every call enqueues work on `stream` (NULL = legacy default stream) and
+ *    returns; calls on one handle are stream-ordered and not thread-safe.  gc_fit and
+ *    gc_query are CUDA-graph capturable once gc_reserve has sized the scratch.
+ *  - There is no CPU fallback: without a usable sm_100 device gc_create fails.
+ */
+#ifndef GSCACHE_H_
+#define GSCACHE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gc_cache_s* gc_cache;      /* opaque, library-owned */
+typedef void* gc_stream;                  /* a cudaStream_t */
+
+typedef enum {
+  GC_OK = 0, GC_ERR_ARG = 1, GC_ERR_STATE = 2, GC_ERR_CUDA = 3, GC_ERR_OOM = 4,
+  GC_ERR_NCCL = 5, GC_ERR_UNSUPPORTED = 6
+} gc_status;
+
+/* parameter groups, paper order (App. B) */
+enum { GC_POS = 0, GC_ROT = 1, GC_COLOR = 2, GC_SCALE = 3, GC_OPACITY = 4, GC_NGROUPS = 5,
+       GC_MAX_LEVELS = 16 };
+
+typedef struct {
+  float lr[GC_NGROUPS];            /* 1.16e-3, 1e-3, 1.25e-2, 0, 1.5e-1         (sec.4.1)   */
+  float weight_decay[GC_NGROUPS];  /* 0, 1e-2, 1e-2, 1e-2, 1e-2  AdamW lambda  (A13)      */
+  float beta1, beta2, adam_eps;    /* 0.9, 0.999, 1e-8                          (A13)             */
+  float hdr_eps;                   /* 0.01                                      (Eq. 4)     */
+  int loss_grad_mode;              /* 0 = stop-gradient denominator (A10), 1 = full quotient      */
+  int lr_schedule;                 /* 1 = Eq. 5 eta_t = eta_0/(1+ln t), 0 = constant      */
+  float cutoff_sigma;              /* tau = 3 Mahalanobis cut-off (A3); INFINITY = dense          */
+  float init_opacity;              /* 0.1 ("similar to Kerbl"; A5)                           */
+  float init_scale_factor;         /* 0.5 ("scales ... to 50%")                              */
+  float init_zcap;                 /* 2.0 ("z-score greater than 2")                         */
+  int cells_per_axis[GC_MAX_LEVELS]; /* culling grid resolution; 0 = auto rule (C8)             */
+} gc_hparams;
+
+/* Per-call statistics.  Written asynchronously: valid once the stream has synchronised. */
+typedef struct {
+  int64_t n_in;                    /* samples passed in                                          */
+  int64_t n_valid;                 /* samples with path_len >= 1 and finite pos/rgb (C2)         */
+  int64_t n_dropped;               /* n_in - n_valid                                             */
+  int64_t step;                    /* schedule counter t used by this call (0 = no-op call)      */
+  int64_t nonfinite_grads;         /* raw gradient elements skipped by AdamW (C6)                */
+  int64_t n_pairs;                 /* contributing (sample, Gaussian) pairs, Q <= tau^2          */
+  int64_t n_candidates;            /* (sample, Gaussian) pairs tested via the culling lists      */
+  int64_t count[GC_MAX_LEVELS];    /* k_l: valid samples per level (global under DP)             */
+  double loss[GC_MAX_LEVELS];      /* L_l of Eq. 4 / C4, before this call's update               */
+} gc_fit_stats;
+
+/* Raw parameters of one level in the paper's layout, row-major per Gaussian. */
+typedef struct {
+  int64_t count;
+  float* position;                 /* [N][3]                                                     */
+  float* rotation;                 /* [N][4] quaternion (w,x,y,z), stored unnormalised (A6)      */
+  float* color;                    /* [N][3] raw colour; activation max(0,c) (A4)                */
+  float* log_scale;                /* [N][3]                                                     */
+  float* opacity_logit;            /* [N][1]; activation sigmoid (A5)                            */
+} gc_level_params;
+
+/* Fills the paper defaults listed above. */
+void gc_default_hparams(gc_hparams* hp);
+
+/* Create a cache of `levels` levels (1..16) on CUDA device `device`.
+ *  counts [levels] (host): Gaussians per level, non-increasing, counts[0] = N0 (sec.3.2:
+ *    "replicated and logarithmically sub-sampled for each level"; explicit counts, A9).
+ *  init_pos, init_rgb [N0][3] (host or device): initial point cloud (positions and albedo,
+ *    P:72).  Level 0 takes the points in caller order; level l >= 1 takes the first counts[l]
+ *    points of the permutation pi = stable argsort(splitmix64(seed + i)) (nested subsets, C7).
+ *  init_log_scale [N0][3] (host or device) or NULL: NULL computes Eq. 2 per level:
+ *    s_i = min(mu_N + zcap sigma_N, max(mean 3-NN distance, 1e-6 diag)) * factor, isotropic.
+ *  Rotation (1,0,0,0), opacity logit ln(p/(1-p)), colour = albedo, AdamW moments 0, t = 0.
+ *  hp: NULL = defaults.  On success *out receives the handle.  Synchronises the device. */
+gc_status gc_create(int levels, const int64_t* counts, const float* init_pos,
+                    const float* init_rgb, const float* init_log_scale, uint64_t seed,
+                    const gc_hparams* hp, int device, gc_cache* out);
+
+gc_status gc_destroy(gc_cache c);
+
+/* Pre-size scratch for batches of up to S_fit fit samples and S_query query points, so that
+ * later gc_fit/gc_query calls never allocate (required before CUDA-graph capture). */
+gc_status gc_reserve(gc_cache c, int64_t S_fit, int64_t S_query);
+
+/* One optimisation step on a batch of S renderer samples (sec.3.5, sec.3.6):
+ *  pos [S][3] f32, path_len [S] i32, rgb [S][3] f32 (host or device).  Level of a sample
+ *  l = min(n, L) - 1 (C2).  Evaluates each sample's level mixture (C3), the HDR loss Eq. 4
+ *  averaged per level over 3 k_l (C4), back-propagates into all 14 raw parameters (C5) and
+ *  takes one AdamW step with eta_g(t) (C6).  A level with k_l = 0 skips its step; a batch
+ *  with no valid sample is a no-op (t not advanced).  stats (host, nullable) is filled when
+ *  the stream reaches the end of this call's work. */
+gc_status gc_fit(gc_cache c, const float* pos, const int32_t* path_len, const float* rgb,
+                 int64_t S, gc_stream stream, gc_fit_stats* stats);
+
+/* Cache lookup (sec.3.1, sec.3.4): out_rgb[i] = yhat_l(x_i) (C3) for S points.
+ *  pos [S][3] f32 (host or device); path_len [S] i32 (host or device) or NULL, in which case
+ *  `level` in [0, L) is used for every point.  Points with path_len <= 0 or non-finite
+ *  position get 0.  out_rgb [S][3] f32 (host or device), caller order.  Never mutates. */
+gc_status gc_query(gc_cache c, const float* pos, const int32_t* path_len, int level, int64_t S,
+                   float* out_rgb, gc_stream stream);
+
+/* Copy out (gc_params) / in (gc_set_params) the raw parameters of one level in the paper's
+ * layout.  dst/src arrays: host or device, `count` must equal the level's size.
+ * gc_set_params rebuilds the level's evaluation records and culling lists; reset_adam != 0
+ * zeroes its AdamW moments and per-level step counter. */
+gc_status gc_params(gc_cache c, int level, gc_level_params* dst, gc_stream stream);
+gc_status gc_set_params(gc_cache c, int level, const gc_level_params* src, int reset_adam,
+                        gc_stream stream);
+
+/* Viewport / scene change: the next stepping gc_fit uses t = 1 again. */
+gc_status gc_reset_schedule(gc_cache c);
+
+/* Culling grid of a level (C8): cell c_a = clamp(floor((x_a - origin_a) * inv_cell_a), 0,
+ * dims_a - 1); linear cell id (c_z * dims_y + c_y) * dims_x + c_x.  Fixed at create. */
+gc_status gc_grid(gc_cache c, int level, double origin[3], double inv_cell[3], int32_t dims[3]);
+
+/* Number of levels and per-level Gaussian counts (host array of GC_MAX_LEVELS). */
+gc_status gc_info(gc_cache c, int* levels, int64_t* counts);
+
+/* Multi-GPU data parallelism (north star; none in the paper): every rank calls gc_fit
+ * with its own shard; one NCCL all-reduce (sum) of the per-level coefficient gradients and
+ * level statistics per step makes every replica take the identical AdamW step.
+ * nccl_uid: 128-byte ncclUniqueId produced by rank 0 (gc_nccl_unique_id) and broadcast by
+ * the caller.  mode: 0 = data parallel.  world == 1 detaches. */
+gc_status gc_nccl_unique_id(void* uid128);
+gc_status gc_set_comm(gc_cache c, const void* nccl_uid, int rank, int world, int mode);
+
+/* ---- debug / parity exports (not on the hot path) ---------------------------------- */
+
+/* Enable (1) / disable (0) recording of the raw 14-parameter gradients of each gc_fit. */
+gc_status gc_debug_enable_grads(gc_cache c, int enable);
+/* Raw gradients d(sum_l L_l)/d(theta) of the last gc_fit (C5), in gc_level_params layout. */
+gc_status gc_debug_grads(gc_cache c, int level, gc_level_params* dst, gc_stream stream);
+/* Culling lists of one level (C8): offsets [cells+1] (level-local, host), idx (host, cap
+ * entries, level-local Gaussian indices, each cell's list ascending).  *n = total entries.
+ * Returns GC_ERR_ARG (with *n set) if cap is too small.  Synchronises the stream. */
+gc_status gc_debug_cull(gc_cache c, int level, int32_t* offsets, int32_t* idx, int64_t cap,
+                        int64_t* n, gc_stream stream);
+/* Level assignment of the last gc_fit's samples (C2), caller order, -1 = dropped.  level_of
+ * [S] (host or device), S = that call's S. */
+gc_status gc_debug_levels(gc_cache c, int32_t* level_of, gc_stream stream);
+
+/* Per-kernel device timing (CUDA events on the call's stream), for bench.py's roofline.
+ * enable != 0 records events around every kernel of gc_fit / gc_query. */
+gc_status gc_profile_enable(gc_cache c, int enable);
+/* Accumulated milliseconds and launch counts per named kernel since the last reset; names
+ * are written as a ';'-separated list into `names` (cap bytes).  Synchronises the device. */
+gc_status gc_profile_read(gc_cache c, char* names, int64_t cap, double* ms, int64_t* launches,
+                          int max_kernels, int* n_kernels, int reset);
+
+const char* gc_last_error(void);
+const char* gc_status_string(gc_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSCACHE_H_ */

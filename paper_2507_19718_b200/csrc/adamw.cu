@@ -1,0 +1,220 @@
+// adamw.cu -- per-call level statistics, the Eq. 5 schedule scalars, and the fused
+// normalise + chain rule + AdamW + next-step record/cull-count kernel (A6).
+#include "common.cuh"
+#include "kernels.h"
+#include "record.cuh"
+
+namespace gsc {
+
+constexpr int kPart = kMaxL + 2;
+
+
+// One block: sums the fwd/bwd per-block partials, derives k_l from the binned cell offsets.
+__global__ void __launch_bounds__(256) k_stats(const double* __restrict__ partial, int nblocks,
+                                               const uint32_t* __restrict__ cell_start, LevelGeom g,
+                                               int64_t S, LvlStats* lvl) {
+  __shared__ double red[8];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int col = 0; col < kPart; ++col) {
+    double acc = 0.0;
+    for (int b = t; b < nblocks; b += 256) acc += partial[(int64_t)b * kPart + col];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (t == 0) {
+      double s = 0.0;
+      for (int k = 0; k < 8; ++k) s += red[k];
+      if (col < kMaxL) lvl->loss_sum[col] = s;
+      else if (col == kMaxL) lvl->n_pairs = s;
+      else lvl->n_cand = s;
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    double tot = 0.0;
+    for (int l = 0; l < kMaxL; ++l) {
+      double c = 0.0;
+      if (l < g.L) c = (double)(cell_start[g.coff[l + 1]] - cell_start[g.coff[l]]);
+      lvl->count[l] = c;
+      tot += c;
+    }
+    lvl->n_valid = tot;
+    lvl->n_in = (double)S;
+  }
+}
+
+struct StepHP {
+  float lr[GC_NGROUPS]; float beta1, beta2; int schedule; int L;
+};
+
+// One thread: Eq. 5 schedule, per-level skip (A12), bias corrections, stats.
+__global__ void k_step_scalars(const LvlStats* __restrict__ lvl, DevState* st, StepHP hp,
+                               gc_fit_stats* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double tot = 0.0;
+  for (int l = 0; l < hp.L; ++l) tot += lvl->count[l];
+  const int stepped = tot > 0.0;
+  st->stepped = stepped;
+  st->nonfinite = 0ull;
+  if (stepped) st->t += 1;
+  const double t = (double)st->t;
+  for (int k = 0; k < GC_NGROUPS; ++k)
+    st->eta[k] = hp.schedule ? (float)((double)hp.lr[k] / (1.0 + log(t))) : hp.lr[k];
+  for (int l = 0; l < kMaxL; ++l) {
+    const double k = l < hp.L ? lvl->count[l] : 0.0;
+    const int act = stepped && k > 0.0;
+    st->active[l] = act;
+    if (act) st->adam_step[l] += 1;
+    const double n = (double)st->adam_step[l];
+    st->bc1[l] = (float)(1.0 - pow((double)hp.beta1, n));
+    st->bc2[l] = (float)(1.0 - pow((double)hp.beta2, n));
+    st->inv3k[l] = act ? (float)(1.0 / (3.0 * k)) : 0.f;
+    out->count[l] = (int64_t)k;
+    out->loss[l] = k > 0.0 ? lvl->loss_sum[l] / (3.0 * k) : 0.0;
+  }
+  out->n_in = (int64_t)lvl->n_in;
+  out->n_valid = (int64_t)lvl->n_valid;
+  out->n_dropped = (int64_t)(lvl->n_in - lvl->n_valid);
+  out->step = stepped ? st->t : 0;
+  out->nonfinite_grads = 0;
+  out->n_pairs = (int64_t)lvl->n_pairs;
+  out->n_candidates = (int64_t)lvl->n_cand;
+}
+
+struct AdamHP {
+  float wd[GC_NGROUPS]; float beta1, beta2, eps; double tau;
+};
+
+__device__ __forceinline__ int group_of(int k) { return k < 3 ? 0 : (k < 7 ? 1 : (k < 10 ? 2 : (k < 13 ? 3 : 4))); }
+
+// Chain rule (C5) from the 12 coefficient gradients (dmu, packed dA, dv) to 14 raw grads.
+__device__ void chain_rule(const float p[kNP], const float cg[12], float out[kNP]) {
+  const float qw0 = p[P_Q], qx0 = p[P_Q + 1], qy0 = p[P_Q + 2], qz0 = p[P_Q + 3];
+  const float n2 = qw0 * qw0 + qx0 * qx0 + qy0 * qy0 + qz0 * qz0;
+  const bool deg = n2 < 1e-24f;
+  float qn = sqrtf(n2), w = 1.f, x = 0.f, y = 0.f, z = 0.f;
+  if (!deg) { w = qw0 / qn; x = qx0 / qn; y = qy0 / qn; z = qz0 / qn; }
+  float R[3][3];
+  R[0][0] = 1.f - 2.f * (y * y + z * z); R[0][1] = 2.f * (x * y - w * z); R[0][2] = 2.f * (x * z + w * y);
+  R[1][0] = 2.f * (x * y + w * z); R[1][1] = 1.f - 2.f * (x * x + z * z); R[1][2] = 2.f * (y * z - w * x);
+  R[2][0] = 2.f * (x * z - w * y); R[2][1] = 2.f * (y * z + w * x); R[2][2] = 1.f - 2.f * (x * x + y * y);
+  const float D[3] = {expf(-2.f * p[P_S]), expf(-2.f * p[P_S + 1]), expf(-2.f * p[P_S + 2])};
+  const float G[3][3] = {{cg[3], cg[6], cg[7]}, {cg[6], cg[4], cg[8]}, {cg[7], cg[8], cg[5]}};
+  out[0] = cg[0]; out[1] = cg[1]; out[2] = cg[2];
+  // GR = G R ; M_kk = (R^T G R)_kk ; dR = 2 G R D
+  float GR[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) GR[a][b] = G[a][0] * R[0][b] + G[a][1] * R[1][b] + G[a][2] * R[2][b];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float Mkk = R[0][k] * GR[0][k] + R[1][k] * GR[1][k] + R[2][k] * GR[2][k];
+    out[P_S + k] = -2.f * D[k] * Mkk;
+  }
+  if (deg) {
+    out[3] = out[4] = out[5] = out[6] = 0.f;
+  } else {
+    float dR[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) dR[a][b] = 2.f * GR[a][b] * D[b];
+    // dR/dq_hat (C5) contracted with dR
+    const float dw = 2.f * (-z * dR[0][1] + y * dR[0][2] + z * dR[1][0] - x * dR[1][2] - y * dR[2][0] + x * dR[2][1]);
+    const float dx = 2.f * (y * dR[0][1] + z * dR[0][2] + y * dR[1][0] - 2.f * x * dR[1][1] - w * dR[1][2] +
+                            z * dR[2][0] + w * dR[2][1] - 2.f * x * dR[2][2]);
+    const float dy = 2.f * (-2.f * y * dR[0][0] + x * dR[0][1] + w * dR[0][2] + x * dR[1][0] + z * dR[1][2] -
+                            w * dR[2][0] + z * dR[2][1] - 2.f * y * dR[2][2]);
+    const float dz = 2.f * (-2.f * z * dR[0][0] - w * dR[0][1] + x * dR[0][2] + w * dR[1][0] - 2.f * z * dR[1][1] +
+                            y * dR[1][2] + x * dR[2][0] + y * dR[2][1]);
+    const float dot = w * dw + x * dx + y * dy + z * dz;
+    out[3] = (dw - w * dot) / qn; out[4] = (dx - x * dot) / qn;
+    out[5] = (dy - y * dot) / qn; out[6] = (dz - z * dot) / qn;
+  }
+  const float wo = 1.f / (1.f + expf(-p[P_O]));
+  const float c0 = fmaxf(p[P_C], 0.f), c1 = fmaxf(p[P_C + 1], 0.f), c2 = fmaxf(p[P_C + 2], 0.f);
+  const float dwo = cg[9] * c0 + cg[10] * c1 + cg[11] * c2;
+  out[P_O] = dwo * wo * (1.f - wo);
+  out[P_C] = p[P_C] > 0.f ? wo * cg[9] : 0.f;
+  out[P_C + 1] = p[P_C + 1] > 0.f ? wo * cg[10] : 0.f;
+  out[P_C + 2] = p[P_C + 2] > 0.f ? wo * cg[11] : 0.f;
+}
+
+__global__ void __launch_bounds__(256) k_adamw(int64_t G, float* __restrict__ P, float* __restrict__ M,
+                                               float* __restrict__ V, float* __restrict__ grad,
+                                               float4* rec, uint4* range, uint32_t* csr_count,
+                                               float* dbg, const DevState* __restrict__ st, AdamHP hp,
+                                               LevelGeom g, gc_fit_stats* out) {
+  unsigned long long bad = 0;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < G; j += (int64_t)gridDim.x * blockDim.x) {
+    const int l = level_of_gaussian(g, j);
+    float p[kNP];
+#pragma unroll
+    for (int k = 0; k < kNP; ++k) p[k] = P[k * G + j];
+    float4* gp = reinterpret_cast<float4*>(grad + 12 * j);
+    const float4 c0 = gp[0], c1 = gp[1], c2 = gp[2];
+    const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+    gp[0] = zero; gp[1] = zero; gp[2] = zero;
+    const bool act = st->active[l] != 0;
+    if (act || dbg) {
+      const float s = st->inv3k[l];
+      const float cg[12] = {c0.x * s, c0.y * s, c0.z * s, c0.w * s, c1.x * s, c1.y * s,
+                            c1.z * s, c1.w * s, c2.x * s, c2.y * s, c2.z * s, c2.w * s};
+      float raw[kNP];
+      chain_rule(p, cg, raw);
+      if (dbg) {
+#pragma unroll
+        for (int k = 0; k < kNP; ++k) dbg[k * G + j] = raw[k];
+      }
+      if (act) {
+        const float bc1 = st->bc1[l], bc2 = st->bc2[l];
+#pragma unroll
+        for (int k = 0; k < kNP; ++k) {
+          const float gk = raw[k];
+          if (!isfinite(gk)) { ++bad; continue; }
+          const int grp = group_of(k);
+          const float eta = st->eta[grp];
+          float m = M[k * G + j], v = V[k * G + j];
+          float pk = p[k] * (1.f - eta * hp.wd[grp]);
+          m = hp.beta1 * m + (1.f - hp.beta1) * gk;
+          v = hp.beta2 * v + (1.f - hp.beta2) * gk * gk;
+          pk = pk - eta * (m / bc1) / (sqrtf(v / bc2) + hp.eps);
+          M[k * G + j] = m; V[k * G + j] = v; P[k * G + j] = pk; p[k] = pk;
+        }
+      }
+    }
+    record_and_count(j, p, hp.tau, g, rec, range, csr_count);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(reinterpret_cast<unsigned long long*>(&out->nonfinite_grads), bad);
+}
+
+void launch_stats(const double* partial, int nblocks, const uint32_t* cell_start,
+                  const LevelGeom& g, int64_t S, LvlStats* lvl, cudaStream_t s, Profiler* prof) {
+  ProfScope ps(prof, "stats", s);
+  k_stats<<<1, 256, 0, s>>>(partial, nblocks, cell_start, g, S, lvl);
+}
+
+void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp, int L,
+                         gc_fit_stats* dev_stats, cudaStream_t s) {
+  StepHP h;
+  for (int k = 0; k < GC_NGROUPS; ++k) h.lr[k] = hp.lr[k];
+  h.beta1 = hp.beta1; h.beta2 = hp.beta2; h.schedule = hp.lr_schedule; h.L = L;
+  k_step_scalars<<<1, 32, 0, s>>>(lvl, st, h, dev_stats);
+}
+
+void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, float4* rec, uint4* range,
+                  uint32_t* csr_count, float* dbg_grad, DevState* st, const gc_hparams& hp,
+                  const LevelGeom& g, gc_fit_stats* dev_stats, cudaStream_t s, Profiler* prof) {
+  ProfScope ps(prof, "adamw_record_cull", s);
+  AdamHP h;
+  for (int k = 0; k < GC_NGROUPS; ++k) h.wd[k] = hp.weight_decay[k];
+  h.beta1 = hp.beta1; h.beta2 = hp.beta2; h.eps = hp.adam_eps; h.tau = (double)hp.cutoff_sigma;
+  int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((G + 255) / 256, 148 * 8));
+  k_adamw<<<blocks, 256, 0, s>>>(G, P, M, V, grad, rec, range, csr_count, dbg_grad, st, h, g, dev_stats);
+}
+
+}  // namespace gsc

@@ -1,0 +1,684 @@
+// api.cu -- the C ABI of include/gscache.h: handle, validation, memory, stream-ordered
+// orchestration of the kernels, statistics, debug exports and NCCL data parallelism.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace gsc;
+
+static thread_local std::string g_err;
+
+static gc_status fail(gc_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(e_ == cudaErrorMemoryAllocation ? GC_ERR_OOM : GC_ERR_CUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                          \
+  } while (0)
+
+#define NK(call)                                                                              \
+  do {                                                                                        \
+    ncclResult_t r_ = (call);                                                                 \
+    if (r_ != ncclSuccess) return fail(GC_ERR_NCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
+  } while (0)
+
+template <class T>
+static cudaError_t dalloc(T** p, size_t n) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc((void**)p, n * sizeof(T));
+  return e;
+}
+
+struct Scratch {
+  int64_t cap = 0;
+  uint32_t *key = nullptr, *rank = nullptr, *bidx = nullptr;
+  float *bx = nullptr, *by = nullptr, *bz = nullptr, *br = nullptr, *bg = nullptr, *bb = nullptr;
+  uint32_t *cell_count = nullptr, *cell_start = nullptr, *totals = nullptr;
+  uint2* tiles = nullptr;
+  WorkItem* work = nullptr;
+  float *in_pos = nullptr, *in_rgb = nullptr, *out = nullptr;
+  int32_t* in_len = nullptr;
+  void release() {
+    void* ps[] = {key, rank, bidx, bx, by, bz, br, bg, bb, cell_count, cell_start, totals, tiles, work,
+                  in_pos, in_rgb, out, in_len};
+    for (void* p : ps) if (p) cudaFree(p);
+    *this = Scratch();
+  }
+};
+
+struct StatsPayload { gc_fit_stats* dst; const gc_fit_stats* src; };
+
+struct gc_cache_s {
+  int device = 0, sms = 148;
+  LevelGeom geom{};
+  int L = 0;
+  int64_t G = 0, NC = 0;
+  int64_t counts[kMaxL] = {0};
+  gc_hparams hp{};
+  float *P = nullptr, *M = nullptr, *V = nullptr, *grad = nullptr, *dbg = nullptr;
+  float4* rec = nullptr;
+  uint4* range = nullptr;
+  uint32_t *csr_count = nullptr, *csr_off = nullptr, *csr_cursor = nullptr, *csr_totals = nullptr;
+  int32_t* csr_idx = nullptr;
+  uint2* csr_tiles = nullptr;
+  uint32_t csr_cap = 0;
+  DevState* st = nullptr;
+  LvlStats* lvl = nullptr;
+  gc_fit_stats* dstats = nullptr;
+  gc_fit_stats* hstats = nullptr;   // pinned staging
+  double* partial = nullptr;
+  int fb_grid = 0, q_grid = 0;
+  bool dbg_on = false;
+  Scratch fit, qry;
+  int64_t last_fit_S = -1;
+  std::vector<StatsPayload*> payloads;
+  size_t payload_next = 0;
+  Profiler prof;
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  float* pack_tmp = nullptr;
+  int64_t pack_cap = 0;
+};
+
+// ------------------------------------------------------------------------- helpers
+static bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  return cs != cudaStreamCaptureStatusNone;
+}
+
+static gc_status check_sticky(gc_cache c) {
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(GC_ERR_CUDA, "asynchronous CUDA error: %s", cudaGetErrorString(e));
+  }
+  return GC_OK;
+}
+
+static gc_status ensure_scratch(gc_cache c, Scratch& sc, int64_t S, bool fit, cudaStream_t s) {
+  if (sc.cap >= S && sc.cell_count) return GC_OK;
+  if (capturing(s)) return fail(GC_ERR_STATE, "scratch too small during graph capture; call gc_reserve first");
+  CK(cudaDeviceSynchronize());
+  sc.release();
+  int64_t cap = std::max<int64_t>(S, 1024);
+  int64_t ntiles = (c->NC + kScanTile - 1) / kScanTile;
+  int64_t work_cap = cap / kCH + std::min<int64_t>(cap, c->NC) + 2;
+  CK(dalloc(&sc.key, cap)); CK(dalloc(&sc.rank, cap));
+  CK(dalloc(&sc.bx, cap)); CK(dalloc(&sc.by, cap)); CK(dalloc(&sc.bz, cap));
+  if (fit) { CK(dalloc(&sc.br, cap)); CK(dalloc(&sc.bg, cap)); CK(dalloc(&sc.bb, cap)); }
+  else CK(dalloc(&sc.bidx, cap));
+  CK(dalloc(&sc.cell_count, c->NC)); CK(dalloc(&sc.cell_start, c->NC + 1));
+  CK(dalloc(&sc.tiles, ntiles)); CK(dalloc(&sc.totals, 4));
+  CK(dalloc(&sc.work, work_cap));
+  sc.cap = cap;
+  return GC_OK;
+}
+
+static gc_status ensure_staging(Scratch& sc, bool need_pos, bool need_len, bool need_rgb, bool need_out) {
+  if (need_pos && !sc.in_pos) CK(dalloc(&sc.in_pos, 3 * sc.cap));
+  if (need_len && !sc.in_len) CK(dalloc(&sc.in_len, sc.cap));
+  if (need_rgb && !sc.in_rgb) CK(dalloc(&sc.in_rgb, 3 * sc.cap));
+  if (need_out && !sc.out) CK(dalloc(&sc.out, 3 * sc.cap));
+  return GC_OK;
+}
+
+static gc_status rebuild_csr(gc_cache c, cudaStream_t s, bool recompute_records) {
+  if (recompute_records) {
+    CK(cudaMemsetAsync(c->csr_count, 0, sizeof(uint32_t) * c->NC, s));
+    launch_record_cull(c->G, c->P, (double)c->hp.cutoff_sigma, c->geom, c->rec, c->range, c->csr_count, s);
+  }
+  launch_scan(c->csr_count, c->NC, 0, c->csr_tiles, c->csr_totals, c->csr_off, c->csr_cursor, nullptr,
+              c->geom, s, &c->prof);
+  launch_cull_emit(c->G, c->range, c->geom, c->csr_cursor, c->csr_idx, c->csr_cap, c->st, s, &c->prof);
+  CK(cudaGetLastError());
+  return GC_OK;
+}
+
+static void CUDART_CB stats_cb(void* arg) {
+  StatsPayload* p = (StatsPayload*)arg;
+  memcpy(p->dst, p->src, sizeof(gc_fit_stats));
+}
+
+static gc_status emit_stats(gc_cache c, gc_fit_stats* user, cudaStream_t s) {
+  if (!user) return GC_OK;
+  CK(cudaMemcpyAsync(c->hstats, c->dstats, sizeof(gc_fit_stats), cudaMemcpyDeviceToHost, s));
+  StatsPayload* p;
+  if (capturing(s)) {
+    p = new StatsPayload{user, c->hstats};
+    c->payloads.push_back(p);          // owned by the handle for the graph's lifetime
+  } else {
+    const size_t ring = 64;
+    if (c->payloads.size() < ring) c->payloads.push_back(new StatsPayload{});
+    p = c->payloads[c->payload_next++ % std::min(c->payloads.size(), ring)];
+    p->dst = user; p->src = c->hstats;
+  }
+  CK(cudaLaunchHostFunc(s, stats_cb, p));
+  return GC_OK;
+}
+
+// ---------------------------------------------------------------------------- ABI
+extern "C" {
+
+const char* gc_last_error(void) { return g_err.c_str(); }
+
+const char* gc_status_string(gc_status s) {
+  switch (s) {
+    case GC_OK: return "GC_OK";
+    case GC_ERR_ARG: return "GC_ERR_ARG";
+    case GC_ERR_STATE: return "GC_ERR_STATE";
+    case GC_ERR_CUDA: return "GC_ERR_CUDA";
+    case GC_ERR_OOM: return "GC_ERR_OOM";
+    case GC_ERR_NCCL: return "GC_ERR_NCCL";
+    case GC_ERR_UNSUPPORTED: return "GC_ERR_UNSUPPORTED";
+  }
+  return "?";
+}
+
+void gc_default_hparams(gc_hparams* hp) {
+  if (!hp) return;
+  memset(hp, 0, sizeof *hp);
+  const float lr[GC_NGROUPS] = {1.16e-3f, 1e-3f, 1.25e-2f, 0.f, 1.5e-1f};
+  const float wd[GC_NGROUPS] = {0.f, 1e-2f, 1e-2f, 1e-2f, 1e-2f};
+  for (int k = 0; k < GC_NGROUPS; ++k) { hp->lr[k] = lr[k]; hp->weight_decay[k] = wd[k]; }
+  hp->beta1 = 0.9f; hp->beta2 = 0.999f; hp->adam_eps = 1e-8f; hp->hdr_eps = 0.01f;
+  hp->loss_grad_mode = 0; hp->lr_schedule = 1; hp->cutoff_sigma = 3.f; hp->init_opacity = 0.1f;
+  hp->init_scale_factor = 0.5f; hp->init_zcap = 2.f;
+}
+
+static uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+static gc_status create_impl(gc_cache c, const int64_t* counts, const float* init_pos,
+                             const float* init_rgb, const float* init_log_scale, uint64_t seed) {
+  CK(cudaSetDevice(c->device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, c->device));
+  if (prop.major < 10) return fail(GC_ERR_UNSUPPORTED, "device %d is sm_%d%d; libgscache is built for sm_100a only", c->device, prop.major, prop.minor);
+  c->sms = prop.multiProcessorCount;
+  const int L = c->L;
+  const int64_t N0 = counts[0];
+  c->geom.L = L;
+  c->geom.goff[0] = 0;
+  for (int l = 0; l < L; ++l) { c->counts[l] = counts[l]; c->geom.goff[l + 1] = c->geom.goff[l] + counts[l]; }
+  for (int l = L; l < kMaxL; ++l) c->geom.goff[l + 1] = c->geom.goff[L];
+  const int64_t G = c->G = c->geom.goff[L];
+
+  // permutation pi = stable argsort(splitmix64(seed + i)) (C7), source index of every Gaussian
+  std::vector<std::pair<uint64_t, int64_t>> kv((size_t)N0);
+  for (int64_t i = 0; i < N0; ++i) kv[i] = {splitmix64(seed + (uint64_t)i), i};
+  std::stable_sort(kv.begin(), kv.end(), [](const std::pair<uint64_t, int64_t>& a, const std::pair<uint64_t, int64_t>& b) { return a.first < b.first; });
+  std::vector<int64_t> src((size_t)G);
+  for (int l = 0; l < L; ++l)
+    for (int64_t i = 0; i < counts[l]; ++i) src[c->geom.goff[l] + i] = (l == 0) ? i : kv[i].second;
+
+  cudaStream_t s = 0;
+  CK(dalloc(&c->P, kNP * G)); CK(dalloc(&c->M, kNP * G)); CK(dalloc(&c->V, kNP * G));
+  CK(cudaMemset(c->M, 0, sizeof(float) * kNP * G)); CK(cudaMemset(c->V, 0, sizeof(float) * kNP * G));
+  CK(dalloc(&c->rec, 3 * G)); CK(dalloc(&c->grad, 12 * G)); CK(dalloc(&c->range, G));
+  CK(cudaMemset(c->grad, 0, sizeof(float) * 12 * G));
+  CK(dalloc(&c->st, 1)); CK(cudaMemset(c->st, 0, sizeof(DevState)));
+  CK(dalloc(&c->lvl, 1)); CK(dalloc(&c->dstats, 1)); CK(cudaMemset(c->dstats, 0, sizeof(gc_fit_stats)));
+  CK(cudaHostAlloc((void**)&c->hstats, sizeof(gc_fit_stats), cudaHostAllocDefault));
+
+  // inputs (host or device)
+  float *dpos = nullptr, *drgb = nullptr, *dls = nullptr;
+  int64_t* dsrc = nullptr;
+  CK(dalloc(&dpos, 3 * N0)); CK(dalloc(&drgb, 3 * N0)); CK(dalloc(&dsrc, G));
+  CK(cudaMemcpy(dpos, init_pos, sizeof(float) * 3 * N0, cudaMemcpyDefault));
+  CK(cudaMemcpy(drgb, init_rgb, sizeof(float) * 3 * N0, cudaMemcpyDefault));
+  if (init_log_scale) { CK(dalloc(&dls, 3 * N0)); CK(cudaMemcpy(dls, init_log_scale, sizeof(float) * 3 * N0, cudaMemcpyDefault)); }
+  CK(cudaMemcpy(dsrc, src.data(), sizeof(int64_t) * G, cudaMemcpyHostToDevice));
+  const double p0 = (double)c->hp.init_opacity;
+  const float logit = (float)std::log(p0 / (1.0 - p0));
+  launch_gather_init(N0, dpos, drgb, dls, dsrc, G, c->P, logit, s);
+  CK(cudaGetLastError());
+  if (!init_log_scale) {   // Eq. 2 per level
+    double *dbar = nullptr, *capfl = nullptr;
+    CK(dalloc(&dbar, N0)); CK(dalloc(&capfl, 2));
+    for (int l = 0; l < L; ++l)
+      launch_eq2_level(c->P, G, c->geom.goff[l], counts[l], dbar, capfl, (double)c->hp.init_zcap,
+                       (double)c->hp.init_scale_factor, c->P, s);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    cudaFree(dbar); cudaFree(capfl);
+  }
+  CK(cudaDeviceSynchronize());
+  cudaFree(dpos); cudaFree(drgb); cudaFree(dsrc); if (dls) cudaFree(dls);
+
+  // culling grids (C8 auto rule, host fp64): level AABB + 5% of its diagonal; cell edge =
+  // 2 tau mean(e^s); dims = clamp(ceil(extent/edge), 1, 512), total cells <= 2^22 per level.
+  std::vector<float> hp_((size_t)kNP * G);
+  CK(cudaMemcpy(hp_.data(), c->P, sizeof(float) * kNP * G, cudaMemcpyDeviceToHost));
+  c->geom.coff[0] = 0;
+  const double tau = (double)c->hp.cutoff_sigma;
+  for (int l = 0; l < L; ++l) {
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY}, ms = 0.0;
+    for (int64_t j = c->geom.goff[l]; j < c->geom.goff[l + 1]; ++j) {
+      for (int a = 0; a < 3; ++a) {
+        double v = hp_[(size_t)(P_MU + a) * G + j];
+        lo[a] = std::min(lo[a], v); hi[a] = std::max(hi[a], v);
+      }
+      ms += (std::exp((double)hp_[(size_t)P_S * G + j]) + std::exp((double)hp_[(size_t)(P_S + 1) * G + j]) +
+             std::exp((double)hp_[(size_t)(P_S + 2) * G + j])) / 3.0;
+    }
+    ms /= (double)std::max<int64_t>(1, counts[l]);
+    double diag = std::sqrt((hi[0] - lo[0]) * (hi[0] - lo[0]) + (hi[1] - lo[1]) * (hi[1] - lo[1]) + (hi[2] - lo[2]) * (hi[2] - lo[2]));
+    double ext[3];
+    for (int a = 0; a < 3; ++a) {
+      double pad = 0.05 * diag + 1e-6;
+      lo[a] -= pad; hi[a] += pad;
+      ext[a] = hi[a] - lo[a];
+    }
+    int32_t dims[3];
+    const int fixed = c->hp.cells_per_axis[l];
+    if (fixed > 0) {
+      for (int a = 0; a < 3; ++a) dims[a] = std::min(fixed, 4096);
+    } else {
+      double edge = std::isfinite(tau) ? 2.0 * tau * ms : INFINITY;
+      if (!(edge > 0.0)) edge = INFINITY;
+      for (int it = 0; it < 200; ++it) {
+        int64_t prod = 1;
+        for (int a = 0; a < 3; ++a) {
+          double d = std::isfinite(edge) ? std::ceil(ext[a] / edge) : 1.0;
+          dims[a] = (int32_t)std::max(1.0, std::min(512.0, d));
+          prod *= dims[a];
+        }
+        if (prod <= (int64_t)1 << 22) break;
+        edge *= 1.25;
+      }
+    }
+    for (int a = 0; a < 3; ++a) {
+      c->geom.origin[l][a] = lo[a];
+      c->geom.dims[l][a] = dims[a];
+      c->geom.inv_cell[l][a] = (double)dims[a] / ext[a];
+    }
+    c->geom.coff[l + 1] = c->geom.coff[l] + (int64_t)dims[0] * dims[1] * dims[2];
+  }
+  for (int l = L; l < kMaxL; ++l) c->geom.coff[l + 1] = c->geom.coff[L];
+  c->NC = c->geom.coff[L];
+  if (c->NC >= (int64_t)1 << 31) return fail(GC_ERR_ARG, "culling grid too large (%lld cells)", (long long)c->NC);
+
+  // records + culling lists; exact size of the first CSR sets the list capacity
+  CK(dalloc(&c->csr_count, c->NC)); CK(dalloc(&c->csr_off, c->NC + 1)); CK(dalloc(&c->csr_cursor, c->NC));
+  CK(dalloc(&c->csr_tiles, (c->NC + kScanTile - 1) / kScanTile)); CK(dalloc(&c->csr_totals, 4));
+  CK(cudaMemset(c->csr_count, 0, sizeof(uint32_t) * c->NC));
+  launch_record_cull(G, c->P, tau, c->geom, c->rec, c->range, c->csr_count, s);
+  launch_scan(c->csr_count, c->NC, 0, c->csr_tiles, c->csr_totals, c->csr_off, c->csr_cursor, nullptr, c->geom, s, nullptr);
+  CK(cudaGetLastError());
+  uint32_t total = 0;
+  CK(cudaMemcpy(&total, c->csr_totals, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  uint64_t cap = std::max<uint64_t>(4ull * total, (uint64_t)total + (1u << 20));
+  cap = std::min<uint64_t>(cap, 0x7FFFFFFFull);
+  c->csr_cap = (uint32_t)cap;
+  CK(dalloc(&c->csr_idx, c->csr_cap));
+  launch_cull_emit(G, c->range, c->geom, c->csr_cursor, c->csr_idx, c->csr_cap, c->st, s, nullptr);
+  CK(cudaGetLastError());
+
+  c->fb_grid = fwdbwd_grid();
+  c->q_grid = query_grid();
+  CK(dalloc(&c->partial, (size_t)c->fb_grid * (kMaxL + 2)));
+  CK(cudaDeviceSynchronize());
+  return GC_OK;
+}
+
+static void destroy_impl(gc_cache c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  void* ps[] = {c->P, c->M, c->V, c->grad, c->dbg, c->rec, c->range, c->csr_count, c->csr_off, c->csr_cursor,
+                c->csr_totals, c->csr_idx, c->csr_tiles, c->st, c->lvl, c->dstats, c->partial, c->pack_tmp};
+  for (void* p : ps) if (p) cudaFree(p);
+  if (c->hstats) cudaFreeHost(c->hstats);
+  c->fit.release();
+  c->qry.release();
+  for (auto* p : c->payloads) delete p;
+  if (c->comm) ncclCommDestroy(c->comm);
+  delete c;
+}
+
+gc_status gc_create(int levels, const int64_t* counts, const float* init_pos, const float* init_rgb,
+                    const float* init_log_scale, uint64_t seed, const gc_hparams* hp, int device,
+                    gc_cache* out) {
+  if (!out) return fail(GC_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (levels < 1 || levels > GC_MAX_LEVELS) return fail(GC_ERR_ARG, "levels must be in [1, %d]", GC_MAX_LEVELS);
+  if (!counts || !init_pos || !init_rgb) return fail(GC_ERR_ARG, "counts/init_pos/init_rgb must not be NULL");
+  for (int l = 0; l < levels; ++l) {
+    if (counts[l] < 1) return fail(GC_ERR_ARG, "counts[%d] < 1", l);
+    if (l > 0 && counts[l] > counts[l - 1]) return fail(GC_ERR_ARG, "counts must be non-increasing");
+  }
+  int64_t G = 0;
+  for (int l = 0; l < levels; ++l) G += counts[l];
+  if (G >= (int64_t)1 << 31) return fail(GC_ERR_ARG, "too many Gaussians");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return fail(GC_ERR_UNSUPPORTED, "no CUDA device %d (libgscache has no CPU fallback)", device);
+  }
+  gc_cache c = new gc_cache_s();
+  c->device = device;
+  c->L = levels;
+  if (hp) c->hp = *hp; else gc_default_hparams(&c->hp);
+  if (!(c->hp.cutoff_sigma > 0.f)) { delete c; return fail(GC_ERR_ARG, "cutoff_sigma must be > 0"); }
+  gc_status st = create_impl(c, counts, init_pos, init_rgb, init_log_scale, seed);
+  if (st != GC_OK) { std::string e = g_err; destroy_impl(c); g_err = e; return st; }
+  *out = c;
+  return GC_OK;
+}
+
+gc_status gc_destroy(gc_cache c) {
+  if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  destroy_impl(c);
+  return GC_OK;
+}
+
+gc_status gc_reserve(gc_cache c, int64_t S_fit, int64_t S_query) {
+  if (!c || S_fit < 0 || S_query < 0) return fail(GC_ERR_ARG, "bad arguments");
+  CK(cudaSetDevice(c->device));
+  if (S_fit > 0) { gc_status s = ensure_scratch(c, c->fit, S_fit, true, 0); if (s) return s; }
+  if (S_query > 0) { gc_status s = ensure_scratch(c, c->qry, S_query, false, 0); if (s) return s; }
+  if (S_fit > 0) { gc_status s = ensure_staging(c->fit, true, true, true, false); if (s) return s; }
+  if (S_query > 0) { gc_status s = ensure_staging(c->qry, true, true, false, true); if (s) return s; }
+  return GC_OK;
+}
+
+gc_status gc_fit(gc_cache c, const float* pos, const int32_t* path_len, const float* rgb, int64_t S,
+                 gc_stream stream, gc_fit_stats* stats) {
+  if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  if (S < 0 || S >= ((int64_t)1 << 31)) return fail(GC_ERR_ARG, "S out of range");
+  if (S > 0 && (!pos || !path_len || !rgb)) return fail(GC_ERR_ARG, "NULL sample pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->device));
+  if (gc_status e = check_sticky(c)) return e;
+  if (gc_status e = ensure_scratch(c, c->fit, std::max<int64_t>(S, 1), true, s)) return e;
+  Scratch& F = c->fit;
+  if (S > 0) {
+    const bool hpos = !is_device_ptr(pos), hlen = !is_device_ptr(path_len), hrgb = !is_device_ptr(rgb);
+    if (hpos || hlen || hrgb) {
+      if (capturing(s) && (!F.in_pos || !F.in_len || !F.in_rgb)) return fail(GC_ERR_STATE, "staging not reserved before capture");
+      if (gc_status e = ensure_staging(F, hpos, hlen, hrgb, false)) return e;
+      if (hpos) { CK(cudaMemcpyAsync(F.in_pos, pos, sizeof(float) * 3 * S, cudaMemcpyHostToDevice, s)); pos = F.in_pos; }
+      if (hlen) { CK(cudaMemcpyAsync(F.in_len, path_len, sizeof(int32_t) * S, cudaMemcpyHostToDevice, s)); path_len = F.in_len; }
+      if (hrgb) { CK(cudaMemcpyAsync(F.in_rgb, rgb, sizeof(float) * 3 * S, cudaMemcpyHostToDevice, s)); rgb = F.in_rgb; }
+    }
+  }
+  IngestBufs b{F.key, F.rank, F.cell_count, F.bx, F.by, F.bz, F.br, F.bg, F.bb, nullptr};
+  CK(cudaMemsetAsync(F.cell_count, 0, sizeof(uint32_t) * c->NC, s));
+  if (S > 0) launch_keys(pos, path_len, rgb, -1, S, c->geom, b, s, &c->prof);
+  launch_scan(F.cell_count, c->NC, kCH, F.tiles, F.totals, F.cell_start, nullptr, F.work, c->geom, s, &c->prof);
+  if (S > 0) launch_scatter(pos, rgb, S, F.cell_start, b, s, &c->prof);
+  FitArgs fa;
+  fa.work = F.work; fa.n_work = F.totals + 1; fa.csr_off = c->csr_off; fa.csr_idx = c->csr_idx; fa.rec = c->rec;
+  fa.bx = F.bx; fa.by = F.by; fa.bz = F.bz; fa.br = F.br; fa.bg = F.bg; fa.bb = F.bb;
+  fa.grad = c->grad; fa.partial = c->partial;
+  const float tau = c->hp.cutoff_sigma;
+  fa.tau2 = tau * tau; fa.hdr_eps = c->hp.hdr_eps; fa.mode = c->hp.loss_grad_mode; fa.L = c->L;
+  launch_fwdbwd(fa, c->fb_grid, s, &c->prof);
+  launch_stats(c->partial, c->fb_grid, F.cell_start, c->geom, S, c->lvl, s, &c->prof);
+  if (c->comm && c->world > 1) {   // data parallel: one sum over ranks of grads + level stats
+    NK(ncclGroupStart());
+    NK(ncclAllReduce(c->grad, c->grad, (size_t)12 * c->G, ncclFloat32, ncclSum, c->comm, s));
+    NK(ncclAllReduce(c->lvl, c->lvl, sizeof(LvlStats) / sizeof(double), ncclFloat64, ncclSum, c->comm, s));
+    NK(ncclGroupEnd());
+  }
+  launch_step_scalars(c->lvl, c->st, c->hp, c->L, c->dstats, s);
+  CK(cudaMemsetAsync(c->csr_count, 0, sizeof(uint32_t) * c->NC, s));
+  launch_adamw(c->G, c->P, c->M, c->V, c->grad, c->rec, c->range, c->csr_count, c->dbg_on ? c->dbg : nullptr,
+               c->st, c->hp, c->geom, c->dstats, s, &c->prof);
+  if (gc_status e = rebuild_csr(c, s, false)) return e;
+  if (gc_status e = emit_stats(c, stats, s)) return e;
+  CK(cudaGetLastError());
+  c->last_fit_S = S;
+  return GC_OK;
+}
+
+gc_status gc_query(gc_cache c, const float* pos, const int32_t* path_len, int level, int64_t S,
+                   float* out_rgb, gc_stream stream) {
+  if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  if (S < 0 || S >= ((int64_t)1 << 31)) return fail(GC_ERR_ARG, "S out of range");
+  if (S > 0 && (!pos || !out_rgb)) return fail(GC_ERR_ARG, "NULL pointer");
+  if (!path_len && (level < 0 || level >= c->L)) return fail(GC_ERR_ARG, "level %d not in [0, %d)", level, c->L);
+  if (S == 0) return GC_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->device));
+  if (gc_status e = check_sticky(c)) return e;
+  if (gc_status e = ensure_scratch(c, c->qry, S, false, s)) return e;
+  Scratch& Q = c->qry;
+  const bool hpos = !is_device_ptr(pos), hlen = path_len && !is_device_ptr(path_len), hout = !is_device_ptr(out_rgb);
+  if (hpos || hlen || hout) {
+    if (capturing(s) && (!Q.in_pos || !Q.in_len || !Q.out)) return fail(GC_ERR_STATE, "staging not reserved before capture");
+    if (gc_status e = ensure_staging(Q, hpos, hlen, false, hout)) return e;
+    if (hpos) { CK(cudaMemcpyAsync(Q.in_pos, pos, sizeof(float) * 3 * S, cudaMemcpyHostToDevice, s)); pos = Q.in_pos; }
+    if (hlen) { CK(cudaMemcpyAsync(Q.in_len, path_len, sizeof(int32_t) * S, cudaMemcpyHostToDevice, s)); path_len = Q.in_len; }
+  }
+  float* dout = hout ? Q.out : out_rgb;
+  IngestBufs b{Q.key, Q.rank, Q.cell_count, Q.bx, Q.by, Q.bz, nullptr, nullptr, nullptr, Q.bidx};
+  CK(cudaMemsetAsync(Q.cell_count, 0, sizeof(uint32_t) * c->NC, s));
+  launch_keys_query(pos, path_len, path_len ? -1 : level, S, c->geom, b, dout, s, &c->prof);
+  launch_scan(Q.cell_count, c->NC, kCH, Q.tiles, Q.totals, Q.cell_start, nullptr, Q.work, c->geom, s, &c->prof);
+  launch_scatter(pos, nullptr, S, Q.cell_start, b, s, &c->prof);
+  QueryArgs qa;
+  qa.work = Q.work; qa.n_work = Q.totals + 1; qa.csr_off = c->csr_off; qa.csr_idx = c->csr_idx; qa.rec = c->rec;
+  qa.bx = Q.bx; qa.by = Q.by; qa.bz = Q.bz; qa.bidx = Q.bidx; qa.out = dout;
+  const float tau = c->hp.cutoff_sigma;
+  qa.tau2 = tau * tau;
+  launch_query(qa, c->q_grid, s, &c->prof);
+  if (hout) CK(cudaMemcpyAsync(out_rgb, dout, sizeof(float) * 3 * S, cudaMemcpyDeviceToHost, s));
+  CK(cudaGetLastError());
+  return GC_OK;
+}
+
+static gc_status level_io(gc_cache c, int level, gc_level_params* p, bool out, const float* planes,
+                          cudaStream_t s) {
+  if (!c || !p || level < 0 || level >= c->L) return fail(GC_ERR_ARG, "bad level or NULL");
+  const int64_t n = c->counts[level];
+  if (p->count != n) return fail(GC_ERR_ARG, "count %lld != level size %lld", (long long)p->count, (long long)n);
+  if (!p->position || !p->rotation || !p->color || !p->log_scale || !p->opacity_logit) return fail(GC_ERR_ARG, "NULL field");
+  CK(cudaSetDevice(c->device));
+  if (c->pack_cap < kNP * n) {
+    CK(cudaDeviceSynchronize());
+    if (c->pack_tmp) cudaFree(c->pack_tmp);
+    CK(dalloc(&c->pack_tmp, kNP * n));
+    c->pack_cap = kNP * n;
+  }
+  float* t = c->pack_tmp;
+  float* f[5] = {p->position, p->rotation, p->color, p->log_scale, p->opacity_logit};
+  const int64_t off[5] = {0, 3 * n, 7 * n, 10 * n, 13 * n}, w[5] = {3, 4, 3, 3, 1};
+  if (out) {
+    launch_pack(planes, c->G, c->geom.goff[level], n, t, s);
+    for (int k = 0; k < 5; ++k) CK(cudaMemcpyAsync(f[k], t + off[k], sizeof(float) * w[k] * n, cudaMemcpyDefault, s));
+  } else {
+    for (int k = 0; k < 5; ++k) CK(cudaMemcpyAsync(t + off[k], f[k], sizeof(float) * w[k] * n, cudaMemcpyDefault, s));
+    launch_unpack(t, c->G, c->geom.goff[level], n, c->P, s);
+  }
+  CK(cudaGetLastError());
+  return GC_OK;
+}
+
+gc_status gc_params(gc_cache c, int level, gc_level_params* dst, gc_stream stream) {
+  if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  return level_io(c, level, dst, true, c->P, (cudaStream_t)stream);
+}
+
+gc_status gc_set_params(gc_cache c, int level, const gc_level_params* src, int reset_adam, gc_stream stream) {
+  if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  cudaStream_t s = (cudaStream_t)stream;
+  gc_level_params tmp = *src;
+  if (gc_status e = level_io(c, level, &tmp, false, nullptr, s)) return e;
+  if (reset_adam) {
+    const int64_t n = c->counts[level], b = c->geom.goff[level];
+    for (int k = 0; k < kNP; ++k) {
+      CK(cudaMemsetAsync(c->M + k * c->G + b, 0, sizeof(float) * n, s));
+      CK(cudaMemsetAsync(c->V + k * c->G + b, 0, sizeof(float) * n, s));
+    }
+    CK(cudaMemsetAsync(&c->st->adam_step[level], 0, sizeof(long long), s));
+  }
+  return rebuild_csr(c, s, true);
+}
+
+gc_status gc_reset_schedule(gc_cache c) {
+  if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemsetAsync(&c->st->t, 0, sizeof(long long), 0));
+  CK(cudaDeviceSynchronize());
+  return GC_OK;
+}
+
+gc_status gc_grid(gc_cache c, int level, double origin[3], double inv_cell[3], int32_t dims[3]) {
+  if (!c || level < 0 || level >= c->L || !origin || !inv_cell || !dims) return fail(GC_ERR_ARG, "bad arguments");
+  for (int a = 0; a < 3; ++a) {
+    origin[a] = c->geom.origin[level][a]; inv_cell[a] = c->geom.inv_cell[level][a]; dims[a] = c->geom.dims[level][a];
+  }
+  return GC_OK;
+}
+
+gc_status gc_info(gc_cache c, int* levels, int64_t* counts) {
+  if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  if (levels) *levels = c->L;
+  if (counts) for (int l = 0; l < GC_MAX_LEVELS; ++l) counts[l] = l < c->L ? c->counts[l] : 0;
+  return GC_OK;
+}
+
+gc_status gc_nccl_unique_id(void* uid128) {
+  if (!uid128) return fail(GC_ERR_ARG, "NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  NK(ncclGetUniqueId((ncclUniqueId*)uid128));
+  return GC_OK;
+}
+
+gc_status gc_set_comm(gc_cache c, const void* nccl_uid, int rank, int world, int mode) {
+  if (!c || world < 1 || rank < 0 || rank >= world) return fail(GC_ERR_ARG, "bad rank/world");
+  if (mode != 0) return fail(GC_ERR_UNSUPPORTED, "only mode 0 (data parallel) is implemented");
+  CK(cudaSetDevice(c->device));
+  CK(cudaDeviceSynchronize());
+  if (c->comm) { ncclCommDestroy(c->comm); c->comm = nullptr; }
+  c->rank = rank; c->world = world;
+  if (world == 1) return GC_OK;
+  if (!nccl_uid) return fail(GC_ERR_ARG, "NULL nccl_uid");
+  ncclUniqueId id;
+  memcpy(&id, nccl_uid, sizeof id);
+  NK(ncclCommInitRank(&c->comm, world, id, rank));
+  return GC_OK;
+}
+
+gc_status gc_debug_enable_grads(gc_cache c, int enable) {
+  if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  CK(cudaSetDevice(c->device));
+  if (enable && !c->dbg) { CK(dalloc(&c->dbg, kNP * c->G)); CK(cudaMemset(c->dbg, 0, sizeof(float) * kNP * c->G)); }
+  c->dbg_on = enable != 0;
+  return GC_OK;
+}
+
+gc_status gc_debug_grads(gc_cache c, int level, gc_level_params* dst, gc_stream stream) {
+  if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  if (!c->dbg) return fail(GC_ERR_STATE, "gradient recording not enabled (gc_debug_enable_grads)");
+  return level_io(c, level, dst, true, c->dbg, (cudaStream_t)stream);
+}
+
+gc_status gc_debug_cull(gc_cache c, int level, int32_t* offsets, int32_t* idx, int64_t cap, int64_t* n,
+                        gc_stream stream) {
+  if (!c || level < 0 || level >= c->L || !offsets || !n) return fail(GC_ERR_ARG, "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->device));
+  const int64_t c0 = c->geom.coff[level], nc = c->geom.coff[level + 1] - c0;
+  std::vector<uint32_t> off((size_t)nc + 1);
+  CK(cudaMemcpyAsync(off.data(), c->csr_off + c0, sizeof(uint32_t) * (nc + 1), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int64_t total = (int64_t)off[nc] - off[0];
+  *n = total;
+  for (int64_t k = 0; k <= nc; ++k) offsets[k] = (int32_t)(off[k] - off[0]);
+  if (!idx || cap < total) return fail(GC_ERR_ARG, "idx capacity %lld < %lld", (long long)cap, (long long)total);
+  std::vector<int32_t> h((size_t)std::max<int64_t>(total, 1));
+  CK(cudaMemcpyAsync(h.data(), c->csr_idx + off[0], sizeof(int32_t) * total, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int64_t g0 = c->geom.goff[level];
+  for (int64_t k = 0; k < nc; ++k) {
+    std::sort(h.begin() + offsets[k], h.begin() + offsets[k + 1]);
+    for (int64_t e = offsets[k]; e < offsets[k + 1]; ++e) idx[e] = (int32_t)(h[e] - g0);
+  }
+  return GC_OK;
+}
+
+gc_status gc_debug_levels(gc_cache c, int32_t* level_of, gc_stream stream) {
+  if (!c || !level_of) return fail(GC_ERR_ARG, "bad arguments");
+  if (c->last_fit_S < 0) return fail(GC_ERR_STATE, "no gc_fit yet");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->device));
+  const int64_t S = c->last_fit_S;
+  if (S == 0) return GC_OK;
+  if (is_device_ptr(level_of)) { launch_levels_of(c->fit.key, S, c->geom, level_of, s); }
+  else {
+    int32_t* d = nullptr;
+    CK(dalloc(&d, S));
+    launch_levels_of(c->fit.key, S, c->geom, d, s);
+    CK(cudaMemcpyAsync(level_of, d, sizeof(int32_t) * S, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    cudaFree(d);
+  }
+  CK(cudaGetLastError());
+  return GC_OK;
+}
+
+gc_status gc_profile_enable(gc_cache c, int enable) {
+  if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  c->prof.enabled = enable != 0;
+  return GC_OK;
+}
+
+gc_status gc_profile_read(gc_cache c, char* names, int64_t cap, double* ms, int64_t* launches,
+                          int max_kernels, int* n_kernels, int reset) {
+  if (!c || !names || !ms || !launches || !n_kernels) return fail(GC_ERR_ARG, "bad arguments");
+  CK(cudaSetDevice(c->device));
+  CK(cudaDeviceSynchronize());
+  c->prof.flush();
+  std::string all;
+  int k = 0;
+  for (auto& kv : c->prof.acc) {
+    if (k >= max_kernels) break;
+    if (k) all += ";";
+    all += kv.first;
+    ms[k] = kv.second.first;
+    launches[k] = kv.second.second;
+    ++k;
+  }
+  *n_kernels = k;
+  if ((int64_t)all.size() + 1 > cap) return fail(GC_ERR_ARG, "names buffer too small");
+  memcpy(names, all.c_str(), all.size() + 1);
+  if (reset) c->prof.acc.clear();
+  return GC_OK;
+}
+
+}  // extern "C"

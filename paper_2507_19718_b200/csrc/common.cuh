@@ -1,0 +1,121 @@
+// common.cuh -- internal types and device helpers of libgscache (sm_100a only).
+// Not part of the ABI; see include/gscache.h and DESIGN.md.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gscache.h"
+
+namespace gsc {
+
+constexpr int kMaxL = GC_MAX_LEVELS;
+constexpr int kNP = 14;              // raw floats per Gaussian
+constexpr int kCH = 256;             // samples per work item == threads of the fwd/bwd block
+constexpr int kTG = 256;             // Gaussians per shared-memory tile
+constexpr int kScanTile = 2048;      // 256 threads x 8 items
+constexpr uint32_t kInvalidKey = 0xFFFFFFFFu;
+
+// Plane index of raw parameter column k in the SoA parameter store (paper order).
+enum { P_MU = 0, P_Q = 3, P_C = 7, P_S = 10, P_O = 13 };
+
+// Per-level geometry, passed by value to kernels (fixed at create).
+struct LevelGeom {
+  int L;
+  int64_t goff[kMaxL + 1];           // Gaussian offsets of each level in the global arrays
+  int64_t coff[kMaxL + 1];           // cell offsets of each level's grid in the global cell ids
+  double origin[kMaxL][3];
+  double inv_cell[kMaxL][3];
+  int32_t dims[kMaxL][3];
+};
+
+// Device-resident optimizer / schedule state (persistent across calls; graph friendly).
+struct DevState {
+  long long t;                       // Eq. 5 counter: stepping fits since create / reset
+  long long adam_step[kMaxL];        // per-level AdamW bias-correction counters (A12)
+  float eta[GC_NGROUPS];             // eta_g(t) of the current step
+  float bc1[kMaxL], bc2[kMaxL];      // 1 - beta^step per level (current step)
+  float inv3k[kMaxL];                // 1 / (3 k_l) (0 when the level is skipped)
+  int active[kMaxL];                 // level takes a step this call
+  int stepped;                       // this call stepped (>= 1 valid sample)
+  unsigned long long nonfinite;      // non-finite gradient elements skipped (this call)
+  unsigned int csr_total;            // culling-list entries of the current CSR
+  unsigned int csr_overflow;         // sticky: a rebuild exceeded the list capacity
+};
+
+// Per-call level statistics; summed over ranks under data parallelism (all doubles so a
+// single NCCL all-reduce covers them).
+struct LvlStats {
+  double count[kMaxL];
+  double loss_sum[kMaxL];            // sum over samples of sum_ch (x-y)^2/(y+eps)^2
+  double n_pairs, n_cand, n_valid, n_in;
+};
+
+// Work item of the binned sample stream: samples [start, start+count) of cell `cell`.
+struct WorkItem { int cell, start, count, level; };
+
+__device__ __forceinline__ int level_of_cell(const LevelGeom& g, int64_t cell) {
+  int l = 0;
+#pragma unroll 1
+  for (int k = 1; k < g.L; ++k) l += (cell >= g.coff[k]);
+  return l;
+}
+
+__device__ __forceinline__ int level_of_gaussian(const LevelGeom& g, int64_t j) {
+  int l = 0;
+#pragma unroll 1
+  for (int k = 1; k < g.L; ++k) l += (j >= g.goff[k]);
+  return l;
+}
+
+// C8 clamp of a floored cell coordinate (NaN / -inf -> 0, large -> dims-1).
+__device__ __forceinline__ int32_t clampcell(double f, int32_t dim) {
+  if (!(f >= 0.0)) return 0;
+  if (f > (double)(dim - 1)) return dim - 1;
+  return (int32_t)f;
+}
+
+// Sample cell (C8), fp64 without contraction: floor((x - origin) * inv_cell).
+__device__ __forceinline__ int64_t sample_cell(const LevelGeom& g, int l, float x, float y, float z) {
+  int32_t c0 = clampcell(floor(__dmul_rn(__dsub_rn((double)x, g.origin[l][0]), g.inv_cell[l][0])), g.dims[l][0]);
+  int32_t c1 = clampcell(floor(__dmul_rn(__dsub_rn((double)y, g.origin[l][1]), g.inv_cell[l][1])), g.dims[l][1]);
+  int32_t c2 = clampcell(floor(__dmul_rn(__dsub_rn((double)z, g.origin[l][2]), g.inv_cell[l][2])), g.dims[l][2]);
+  return g.coff[l] + ((int64_t)c2 * g.dims[l][1] + c1) * g.dims[l][0] + c0;
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Vector reduction into global memory (sm_90+): REDG.E.ADD.F32x4.
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b),
+               "f"(c), "f"(d)
+               : "memory");
+}
+
+// Mahalanobis form Q = d^T A d of a packed symmetric A (A00,A11,A22,A01,A02,A12), with the
+// operation order fixed by explicit intrinsics so that every kernel takes the same cut-off
+// decision for the same pair.  Also returns t = A d.
+struct Rec {
+  float mx, my, mz, a00, a11, a22, a01, a02, a12, v0, v1, v2;
+};
+
+__device__ __forceinline__ float quad_form(const Rec& r, float x, float y, float z, float& dx,
+                                           float& dy, float& dz, float& tx, float& ty, float& tz) {
+  dx = __fsub_rn(x, r.mx);
+  dy = __fsub_rn(y, r.my);
+  dz = __fsub_rn(z, r.mz);
+  tx = __fmaf_rn(r.a02, dz, __fmaf_rn(r.a01, dy, __fmul_rn(r.a00, dx)));
+  ty = __fmaf_rn(r.a12, dz, __fmaf_rn(r.a11, dy, __fmul_rn(r.a01, dx)));
+  tz = __fmaf_rn(r.a22, dz, __fmaf_rn(r.a12, dy, __fmul_rn(r.a02, dx)));
+  return __fmaf_rn(dz, tz, __fmaf_rn(dy, ty, __fmul_rn(dx, tx)));
+}
+
+__device__ __forceinline__ Rec load_rec(const float4* rec, int64_t j) {
+  float4 p = __ldg(rec + 3 * j), q = __ldg(rec + 3 * j + 1), s = __ldg(rec + 3 * j + 2);
+  return Rec{p.x, p.y, p.z, p.w, q.x, q.y, q.z, q.w, s.x, s.y, s.z, s.w};
+}
+
+}  // namespace gsc

@@ -1,0 +1,194 @@
+// cull_scan.cu -- evaluation records (A2), exact conservative culling (C8) and the
+// three-phase tiled exclusive scan used for both the sample bins and the culling CSR.
+#include "common.cuh"
+#include "kernels.h"
+#include "record.cuh"
+
+namespace gsc {
+
+__global__ void k_record_cull(int64_t G, const float* __restrict__ P, double tau, LevelGeom g,
+                              float4* rec, uint4* range, uint32_t* csr_count) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < G; j += (int64_t)gridDim.x * blockDim.x) {
+    float p[kNP];
+#pragma unroll
+    for (int k = 0; k < kNP; ++k) p[k] = P[k * G + j];
+    record_and_count(j, p, tau, g, rec, range, csr_count);
+  }
+}
+
+// Fill the culling lists: each Gaussian appends its global index to every cell of its range.
+// The order inside a cell is atomic order (unspecified); gc_debug_cull sorts on export.
+__global__ void k_cull_emit(int64_t G, const uint4* __restrict__ range, LevelGeom g,
+                            uint32_t* cursor, int32_t* idx, uint32_t cap, DevState* st) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < G; j += (int64_t)gridDim.x * blockDim.x) {
+    uint4 r = range[j];
+    int l = level_of_gaussian(g, j);
+    int32_t lx = r.x & 0xFFFF, hx = r.x >> 16, ly = r.y & 0xFFFF, hy = r.y >> 16, lz = r.z & 0xFFFF, hz = r.z >> 16;
+    const int64_t dx = g.dims[l][0], dy = g.dims[l][1];
+    for (int32_t cz = lz; cz <= hz; ++cz)
+      for (int32_t cy = ly; cy <= hy; ++cy)
+        for (int32_t cx = lx; cx <= hx; ++cx) {
+          uint32_t pos = atomicAdd(cursor + g.coff[l] + ((int64_t)cz * dy + cy) * dx + cx, 1u);
+          if (pos < cap) idx[pos] = (int32_t)j;
+          else atomicOr(&st->csr_overflow, 1u);
+        }
+  }
+}
+
+// ---------------------------------------------------------------------------- scan
+// Block-wide exclusive scan of (a, b) pairs, 256 threads (8 warps).
+__device__ __forceinline__ uint2 block_excl_scan(uint2 v, uint2& total) {
+  __shared__ uint2 wsum[8];
+  __shared__ uint2 tot_s;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint2 inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t a = __shfl_up_sync(0xffffffffu, inc.x, o), b = __shfl_up_sync(0xffffffffu, inc.y, o);
+    if (lane >= o) { inc.x += a; inc.y += b; }
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    uint2 w = lane < 8 ? wsum[lane] : make_uint2(0, 0);
+    uint2 wi = w;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      uint32_t a = __shfl_up_sync(0xffffffffu, wi.x, o), b = __shfl_up_sync(0xffffffffu, wi.y, o);
+      if (lane >= o) { wi.x += a; wi.y += b; }
+    }
+    if (lane < 8) wsum[lane] = make_uint2(wi.x - w.x, wi.y - w.y);
+    if (lane == 7) tot_s = wi;
+  }
+  __syncthreads();
+  uint2 base = wsum[warp];
+  total = tot_s;
+  __syncthreads();
+  return make_uint2(base.x + inc.x - v.x, base.y + inc.y - v.y);
+}
+
+__device__ __forceinline__ void load8(const uint32_t* cnt, int64_t n, int64_t base, uint32_t c[8]) {
+  if (base + 8 <= n && ((base & 3) == 0)) {
+    uint4 a = *reinterpret_cast<const uint4*>(cnt + base), b = *reinterpret_cast<const uint4*>(cnt + base + 4);
+    c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w; c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k] = (base + k < n) ? cnt[base + k] : 0u;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_scan_reduce(const uint32_t* __restrict__ cnt, int64_t n, int ch, uint2* tile_sums) {
+  int64_t base = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 8;
+  uint32_t c[8];
+  load8(cnt, n, base, c);
+  uint2 s = make_uint2(0, 0);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) { s.x += c[k]; if (ch) s.y += (c[k] + ch - 1) / ch; }
+  uint2 total;
+  block_excl_scan(s, total);
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+}
+
+// Single block: in-place exclusive scan of the tile sums; totals[0..1] = grand totals.
+__global__ void __launch_bounds__(1024) k_scan_tiles(uint2* tile_sums, int ntiles, uint32_t* totals) {
+  __shared__ uint2 carry_s;
+  __shared__ uint2 wsum[32];
+  if (threadIdx.x == 0) carry_s = make_uint2(0, 0);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int b = 0; b < ntiles; b += 1024) {
+    int i = b + threadIdx.x;
+    uint2 v = i < ntiles ? tile_sums[i] : make_uint2(0, 0);
+    uint2 inc = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t a = __shfl_up_sync(0xffffffffu, inc.x, o), c = __shfl_up_sync(0xffffffffu, inc.y, o);
+      if (lane >= o) { inc.x += a; inc.y += c; }
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      uint2 w = wsum[lane], wi = w;
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t a = __shfl_up_sync(0xffffffffu, wi.x, o), c = __shfl_up_sync(0xffffffffu, wi.y, o);
+        if (lane >= o) { wi.x += a; wi.y += c; }
+      }
+      wsum[lane] = make_uint2(wi.x - w.x, wi.y - w.y);
+    }
+    __syncthreads();
+    uint2 carry = carry_s;
+    uint2 ex = make_uint2(carry.x + wsum[warp].x + inc.x - v.x, carry.y + wsum[warp].y + inc.y - v.y);
+    if (i < ntiles) tile_sums[i] = ex;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry_s = make_uint2(ex.x + v.x, ex.y + v.y);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { totals[0] = carry_s.x; totals[1] = carry_s.y; }
+}
+
+// Down-sweep: exclusive offsets (and an optional copy used as atomic cursors); with ch > 0,
+// one WorkItem per chunk of <= ch samples of every non-empty cell.
+__global__ void __launch_bounds__(256) k_scan_down(const uint32_t* __restrict__ cnt, int64_t n, int ch,
+                                                   const uint2* __restrict__ tile_prefix,
+                                                   uint32_t* excl, uint32_t* excl_copy,
+                                                   WorkItem* work, LevelGeom g) {
+  int64_t base = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 8;
+  uint32_t c[8];
+  load8(cnt, n, base, c);
+  uint2 s = make_uint2(0, 0);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) { s.x += c[k]; if (ch) s.y += (c[k] + ch - 1) / ch; }
+  uint2 total;
+  uint2 ex = block_excl_scan(s, total);
+  uint2 tp = tile_prefix[blockIdx.x];
+  uint32_t off = tp.x + ex.x, woff = tp.y + ex.y;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    int64_t i = base + k;
+    if (i < n) {
+      excl[i] = off;
+      if (excl_copy) excl_copy[i] = off;
+      if (ch && c[k]) {
+        int lvl = level_of_cell(g, i);
+        for (uint32_t q = 0; q * ch < c[k]; ++q)
+          work[woff++] = WorkItem{(int)i, (int)(off + q * ch), (int)min((uint32_t)ch, c[k] - q * ch), lvl};
+      }
+      off += c[k];
+    }
+    if (i == n - 1) excl[n] = off;
+  }
+}
+
+void launch_scan(const uint32_t* cnt, int64_t n, int ch, uint2* tile_sums, uint32_t* totals,
+                 uint32_t* excl, uint32_t* excl_copy, WorkItem* work, const LevelGeom& g,
+                 cudaStream_t s, Profiler* prof) {
+  int ntiles = (int)((n + kScanTile - 1) / kScanTile);
+  {
+    ProfScope ps(prof, "scan_reduce", s);
+    k_scan_reduce<<<ntiles, 256, 0, s>>>(cnt, n, ch, tile_sums);
+  }
+  {
+    ProfScope ps(prof, "scan_tiles", s);
+    k_scan_tiles<<<1, 1024, 0, s>>>(tile_sums, ntiles, totals);
+  }
+  {
+    ProfScope ps(prof, "scan_down", s);
+    k_scan_down<<<ntiles, 256, 0, s>>>(cnt, n, ch, tile_sums, excl, excl_copy, work, g);
+  }
+}
+
+void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& g, float4* rec,
+                        uint4* range, uint32_t* csr_count, cudaStream_t s) {
+  int blocks = (int)std::min<int64_t>((G + 255) / 256, 148 * 16);
+  if (blocks < 1) blocks = 1;
+  k_record_cull<<<blocks, 256, 0, s>>>(G, P, tau, g, rec, range, csr_count);
+}
+
+void launch_cull_emit(int64_t G, const uint4* range, const LevelGeom& g, uint32_t* cursor,
+                      int32_t* idx, uint32_t cap, DevState* st, cudaStream_t s, Profiler* prof) {
+  ProfScope ps(prof, "cull_emit", s);
+  int blocks = (int)std::min<int64_t>((G + 255) / 256, 148 * 16);
+  if (blocks < 1) blocks = 1;
+  k_cull_emit<<<blocks, 256, 0, s>>>(G, range, g, cursor, idx, cap, st);
+}
+
+}  // namespace gsc

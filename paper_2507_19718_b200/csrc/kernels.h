@@ -1,0 +1,124 @@
+// kernels.h -- host-side launchers of libgscache's kernels and the per-kernel profiler.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace gsc {
+
+// CUDA-event timing of named kernels on their launch stream (bench.py roofline).
+struct Profiler {
+  bool enabled = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  std::map<std::string, std::pair<double, long long>> acc;   // name -> (ms, launches)
+
+  cudaEvent_t get() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  void flush() {  // caller synchronised
+    for (auto& p : pending) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, p.second.first, p.second.second) == cudaSuccess) {
+        auto& a = acc[p.first];
+        a.first += ms;
+        a.second += 1;
+      }
+      pool.push_back(p.second.first);
+      pool.push_back(p.second.second);
+    }
+    pending.clear();
+  }
+  ~Profiler() {
+    for (auto& p : pending) { cudaEventDestroy(p.second.first); cudaEventDestroy(p.second.second); }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
+struct ProfScope {
+  Profiler* p; const char* name; cudaStream_t s; cudaEvent_t a = nullptr, b = nullptr;
+  ProfScope(Profiler* p_, const char* n, cudaStream_t s_) : p(p_), name(n), s(s_) {
+    if (p && p->enabled) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(s, &cs);
+      if (cs == cudaStreamCaptureStatusNone) { a = p->get(); b = p->get(); cudaEventRecord(a, s); }
+    }
+  }
+  ~ProfScope() {
+    if (a) { cudaEventRecord(b, s); p->pending.push_back({name, {a, b}}); }
+  }
+};
+
+// cull_scan.cu
+void launch_scan(const uint32_t* cnt, int64_t n, int ch, uint2* tile_sums, uint32_t* totals,
+                 uint32_t* excl, uint32_t* excl_copy, WorkItem* work, const LevelGeom& g,
+                 cudaStream_t s, Profiler* prof);
+void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& g, float4* rec,
+                        uint4* range, uint32_t* csr_count, cudaStream_t s);
+void launch_cull_emit(int64_t G, const uint4* range, const LevelGeom& g, uint32_t* cursor,
+                      int32_t* idx, uint32_t cap, DevState* st, cudaStream_t s, Profiler* prof);
+
+// ingest.cu
+struct IngestBufs {
+  uint32_t* key;        // [S] global cell id or kInvalidKey
+  uint32_t* rank;       // [S] arrival rank inside the cell
+  uint32_t* cell_count; // [NC]
+  float* bx; float* by; float* bz;          // [S] binned positions
+  float* br; float* bg; float* bb;          // [S] binned targets (fit only)
+  uint32_t* bidx;       // [S] original sample index (query only)
+};
+void launch_keys(const float* pos, const int32_t* len, const float* rgb, int level_fixed,
+                 int64_t S, const LevelGeom& g, IngestBufs b, cudaStream_t s, Profiler* prof);
+void launch_keys_query(const float* pos, const int32_t* len, int level_fixed, int64_t S,
+                       const LevelGeom& g, IngestBufs b, float* out, cudaStream_t s, Profiler* prof);
+void launch_scatter(const float* pos, const float* rgb, int64_t S, const uint32_t* cell_start,
+                    IngestBufs b, cudaStream_t s, Profiler* prof);
+void launch_levels_of(const uint32_t* key, int64_t S, const LevelGeom& g, int32_t* out,
+                      cudaStream_t s);
+
+// fwdbwd.cu
+struct FitArgs {
+  const WorkItem* work; const uint32_t* n_work;
+  const uint32_t* csr_off; const int32_t* csr_idx; const float4* rec;
+  const float* bx; const float* by; const float* bz; const float* br; const float* bg; const float* bb;
+  float* grad;          // [G][12]
+  double* partial;      // [grid][kMaxL + 2]: per-block loss sums, pairs, candidates
+  float tau2, hdr_eps; int mode; int L;
+};
+int fwdbwd_grid();
+void launch_fwdbwd(const FitArgs& a, int grid, cudaStream_t s, Profiler* prof);
+struct QueryArgs {
+  const WorkItem* work; const uint32_t* n_work;
+  const uint32_t* csr_off; const int32_t* csr_idx; const float4* rec;
+  const float* bx; const float* by; const float* bz; const uint32_t* bidx;
+  float* out; float tau2;
+};
+int query_grid();
+void launch_query(const QueryArgs& a, int grid, cudaStream_t s, Profiler* prof);
+
+// adamw.cu
+void launch_stats(const double* partial, int nblocks, const uint32_t* cell_start,
+                  const LevelGeom& g, int64_t S, LvlStats* lvl, cudaStream_t s, Profiler* prof);
+void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp, int L,
+                         gc_fit_stats* dev_stats, cudaStream_t s);
+void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, float4* rec, uint4* range,
+                  uint32_t* csr_count, float* dbg_grad, DevState* st, const gc_hparams& hp,
+                  const LevelGeom& g, gc_fit_stats* dev_stats, cudaStream_t s, Profiler* prof);
+
+// create.cu
+void launch_gather_init(int64_t N0, const float* pos, const float* rgb, const float* log_scale,
+                        const int64_t* src, int64_t G, float* P, float opacity_logit, cudaStream_t s);
+void launch_eq2_level(const float* P, int64_t G, int64_t base, int64_t n, double* dbar, double* capfl,
+                      double zcap, double factor, float* Pw, cudaStream_t s);
+void launch_pack(const float* P, int64_t G, int64_t base, int64_t n, float* out14, cudaStream_t s);
+void launch_unpack(const float* in14, int64_t G, int64_t base, int64_t n, float* P, cudaStream_t s);
+
+}  // namespace gsc

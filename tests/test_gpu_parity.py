@@ -1,0 +1,365 @@
+"""CUDA path vs the fp64 oracle, element by element, through the C ABI (-m gpu).
+
+Tolerances (BASELINE.json north_star; SURVEY.md 8(c) "parity tolerances"):
+  forward   |dy| <= 1e-5 |y| + 1e-7 max|y|, except samples with a pair on the cut-off
+            boundary (|Q - tau^2| <= 1e-4 tau^2, reading A3), which get v e^{-tau^2/2} extra;
+  gradients per (level, group) ||dg|| / ||g|| <= 1e-4;
+  loss after 100 fit steps within 1 %;
+  parameter layout, level assignment and culling lists bit-exact.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workload
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+F32 = lambda v: float(np.float32(v))  # noqa: E731
+
+
+@pytest.fixture(scope="module")
+def gsc():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2507_19718_b200 as m
+    assert torch.cuda.is_available()
+    return m
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def make_cfg1(gsc, counts=(4096, 1024, 256), seed=7, hp=None, log_scale=None):
+    pos, alb = workload.init_cloud(1)
+    pos, alb = pos[:counts[0]], alb[:counts[0]]
+    c = gsc.GSCache(list(counts), cuda(pos), cuda(alb), init_log_scale=log_scale, seed=seed,
+                    hparams=hp)
+    return c, pos, alb
+
+
+def rows(c):
+    return np.concatenate([c.params_rows(l) for l in range(c.L)]).astype(np.float64)
+
+
+def check_forward(y, yo, P, goff, x, lv, tau=3.0, what=""):
+    """Element tolerance + A3 boundary allowance computed by brute force for failures."""
+    y, yo = np.asarray(y, np.float64), np.asarray(yo, np.float64)
+    tol = 1e-5 * np.abs(yo) + 1e-7 * max(np.abs(yo).max(), 1e-30)
+    bad = np.nonzero((np.abs(y - yo) > tol).any(axis=1))[0]
+    amb_count = 0
+    for i in bad:
+        l = lv[i]
+        assert l >= 0, (what, i)
+        _, _, amb, na = oracle.eval_brute(P[goff[l]:goff[l + 1]], x[i:i + 1].astype(np.float64),
+                                          tau=tau, amb_rel=1e-4)
+        assert na[0] > 0, (what, "sample", i, y[i], yo[i])
+        assert np.all(np.abs(y[i] - yo[i]) <= tol[i] + amb[0] * (1 + 1e-6)), (what, i)
+        amb_count += 1
+    assert amb_count <= max(3, len(y) // 10000), (what, amb_count)
+    return amb_count
+
+
+# ----------------------------------------------------------------------- create (C7)
+def test_create_layout_bit_exact(gsc):
+    c, pos, alb = make_cfg1(gsc)
+    P = rows(c)
+    Po = oracle.create([4096, 1024, 256], pos.astype(np.float64), alb.astype(np.float64), seed=7,
+                       init_opacity=F32(0.1), zcap=2.0, factor=0.5)
+    Po32 = Po.astype(np.float32).astype(np.float64)
+    np.testing.assert_array_equal(P[:, 0:10], Po32[:, 0:10])       # pos, rot, colour
+    np.testing.assert_array_equal(P[:, 13], Po32[:, 13])           # opacity logit
+    ulp = np.abs(P[:, 10:13].astype(np.float32).view(np.int32) - Po32[:, 10:13].astype(np.float32).view(np.int32))
+    assert ulp.max() <= 2, ulp.max()                                 # Eq. 2 log-scales
+
+
+def test_create_with_given_scales_exact(gsc):
+    pos, alb = workload.init_cloud(1)
+    ls = np.log(np.random.default_rng(1).uniform(0.01, 0.03, (4096, 3))).astype(np.float32)
+    c = gsc.GSCache([4096, 512], pos, alb, init_log_scale=ls, seed=11)   # host pointers
+    Po = oracle.create([4096, 512], pos, alb, init_log_scale=ls.astype(np.float64), seed=11,
+                       init_opacity=F32(0.1))
+    np.testing.assert_array_equal(rows(c), Po.astype(np.float32).astype(np.float64))
+
+
+def test_set_params_roundtrip_and_reset(gsc):
+    c, _, _ = make_cfg1(gsc)
+    r = np.random.default_rng(2)
+    P1 = c.params_rows(1)
+    P1[:, 3:7] = r.normal(size=(1024, 4))
+    P1[:, 10:13] += r.normal(scale=0.2, size=(1024, 3))
+    c.set_params_rows(1, P1, reset_adam=True)
+    np.testing.assert_array_equal(c.params_rows(1), P1.astype(np.float32))
+
+
+# -------------------------------------------------------------------- culling (C8)
+def _check_csr(c, P):
+    for l in range(c.L):
+        o, ic, d = c.grid(l)
+        Pl = P[c.goff[l]:c.goff[l + 1]]
+        rng = oracle.cull_ranges(Pl, 3.0, o, ic, d)
+        off_o, idx_o = oracle.build_csr(rng, d)
+        off_g, idx_g = c.debug_cull(l)
+        np.testing.assert_array_equal(off_g.astype(np.int64), off_o)
+        np.testing.assert_array_equal(idx_g, idx_o)
+
+
+def test_culling_lists_bit_exact_at_create_and_after_steps(gsc):
+    c, _, _ = make_cfg1(gsc)
+    _check_csr(c, rows(c))
+    for f in range(3):
+        x, ln, rgb = workload.fit_batch(1, frame=f, S=65536)
+        c.fit(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    _check_csr(c, rows(c))
+    # rotated / anisotropic Gaussians through set_params
+    r = np.random.default_rng(3)
+    P0 = c.params_rows(0)
+    P0[:, 3:7] = r.normal(size=(4096, 4)).astype(np.float32)
+    P0[:, 10:13] += r.uniform(-0.5, 0.7, (4096, 3)).astype(np.float32)
+    c.set_params_rows(0, P0)
+    _check_csr(c, rows(c))
+
+
+# ---------------------------------------------------------------- levels (C2)
+def test_level_assignment_bit_exact(gsc):
+    c, _, _ = make_cfg1(gsc)
+    x, ln, rgb = workload.fit_batch(1, S=50_000)
+    r = np.random.default_rng(4)
+    ln = r.integers(-3, 9, len(ln)).astype(np.int32)
+    x[r.integers(0, len(x), 50), r.integers(0, 3, 50)] = np.nan
+    x[r.integers(0, len(x), 50), 0] = np.inf
+    rgb[r.integers(0, len(x), 50), r.integers(0, 3, 50)] = np.nan
+    c.fit(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    lg = c.debug_levels(len(x))
+    lo = oracle.level_of(ln, 3, x.astype(np.float64), rgb.astype(np.float64))
+    np.testing.assert_array_equal(lg, lo)
+
+
+# ---------------------------------------------------------------- query (C3)
+@pytest.mark.parametrize("level_mode", ["per_sample", "fixed"])
+def test_query_parity_cfg1(gsc, level_mode):
+    c, _, _ = make_cfg1(gsc)
+    P = rows(c)
+    x, ln = workload.query_batch(1)
+    if level_mode == "fixed":
+        y = c.query(cuda(x), None, level=1).cpu().numpy()
+        yo, lv, _ = oracle.query(c.goff, P, x.astype(np.float64), None, level=1, grids=c.grids())
+    else:
+        y = c.query(cuda(x), cuda(ln)).cpu().numpy()
+        yo, lv, _ = oracle.query(c.goff, P, x.astype(np.float64), ln, grids=c.grids())
+    assert np.abs(yo).max() > 0
+    check_forward(y, yo, P, c.goff, x, lv, what="query")
+
+
+def test_query_invalid_points_and_ragged_sizes(gsc):
+    c, _, _ = make_cfg1(gsc, counts=(4096, 700, 33))
+    P = rows(c)
+    for S in (1, 31, 257, 5000):
+        x, ln = workload.query_batch(1, frame=S, S=S)
+        ln[::7] = 0
+        x[::11, 1] = np.nan
+        y = c.query(x, ln)                                         # host buffers
+        xo = x.astype(np.float64)
+        yo, lv, _ = oracle.query(c.goff, P, xo, ln, grids=c.grids())
+        assert np.all(y[lv < 0] == 0)
+        ok = lv >= 0
+        check_forward(y[ok], yo[ok], P, c.goff, x[ok], lv[ok], what=f"S={S}")
+
+
+def test_query_dense_no_cutoff(gsc):
+    """tau = INFINITY: every Gaussian of the level contributes (dense evaluator)."""
+    pos, alb, ls = workload.cfg0_lattice()
+    hp = gsc.default_hparams(cutoff_sigma=float("inf"))
+    c = gsc.GSCache([64, 16], pos, alb, init_log_scale=ls, seed=1, hparams=hp)
+    P = rows(c)
+    x, _ = workload.cfg0_samples(3000)
+    ln = np.random.default_rng(5).integers(1, 3, 3000).astype(np.int32)
+    y = c.query(x, ln)
+    yo, lv, npairs = oracle.query(c.goff, P, x.astype(np.float64), ln, tau=np.inf)
+    assert npairs == 3000 * 64 - (ln == 2).sum() * 48
+    check_forward(y, yo, P, c.goff, x, lv, tau=np.inf, what="dense")
+
+
+# ------------------------------------------------------------- gradients (C5)
+@pytest.mark.parametrize("mode", [0, 1])
+def test_gradient_parity(gsc, mode):
+    hp = gsc.default_hparams(loss_grad_mode=mode)
+    c, _, _ = make_cfg1(gsc, hp=hp)
+    r = np.random.default_rng(6)
+    P0 = c.params_rows(0)                                          # give level 0 rotations/anisotropy
+    P0[:, 3:7] = r.normal(size=(4096, 4)).astype(np.float32)
+    P0[:, 10:13] += r.uniform(-0.3, 0.3, (4096, 3)).astype(np.float32)
+    c.set_params_rows(0, P0)
+    P = rows(c)
+    c.debug_enable_grads(True)
+    x, ln, rgb = workload.fit_batch(1)
+    st = c.fit(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    g = np.concatenate([c.debug_grads_rows(l) for l in range(3)]).astype(np.float64)
+    ro = oracle.loss_grad(c.goff, P, x.astype(np.float64), ln, rgb.astype(np.float64),
+                          mode=mode, grids=c.grids())
+    go = ro["grad"]
+    for l in range(3):
+        assert st.count[l] == ro["count"][l]
+        assert abs(st.loss[l] - ro["loss"][l]) <= 1e-4 * ro["loss"][l]
+        sl = slice(c.goff[l], c.goff[l + 1])
+        for name, cs in oracle.GROUP_SLICES.items():
+            a, b = g[sl, cs], go[sl, cs]
+            nb = np.linalg.norm(b)
+            if name == "rotation" and l > 0:                        # isotropic levels: dq = 0
+                assert np.linalg.norm(a) <= 1e-4 * np.linalg.norm(go[sl]) + 1e-12
+                continue
+            assert nb > 0, (l, name)
+            assert np.linalg.norm(a - b) / nb <= 1e-4, (l, name, np.linalg.norm(a - b) / nb)
+    assert st.n_pairs == ro["npairs"] or abs(st.n_pairs - ro["npairs"]) <= 1e-4 * ro["npairs"]
+
+
+# ----------------------------------------------------------- optimizer (C6)
+def test_first_step_matches_oracle_update(gsc):
+    """One AdamW step (C6) from identical parameters: updates agree wherever the gradient is
+    not at the eps / fp32-rounding level (there Adam's first step is +-eta * sign(g))."""
+    c, _, _ = make_cfg1(gsc)
+    P = rows(c)
+    x, ln, rgb = workload.fit_batch(1, frame=3)
+    c.fit(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    oc = oracle.OracleCache([4096, 1024, 256], P, grids=c.grids())
+    go = oc.fit(x.astype(np.float64), ln, rgb.astype(np.float64))["grad"]
+    P1 = rows(c)
+    eta = np.array([1.16e-3] * 3 + [1e-3] * 4 + [1.25e-2] * 3 + [0.0] * 3 + [1.5e-1])
+    strong = np.abs(go) > 1e-3 * np.abs(go).max(axis=0, keepdims=True)
+    err = np.abs((P1 - P) - (oc.P - P))
+    assert np.all(err[strong] <= 1e-3 * eta[np.nonzero(strong)[1]] + 4e-7 * (1 + np.abs(P[strong])))
+    assert np.all(err <= 2.0 * eta[None, :] + 4e-7 * (1 + np.abs(P)))
+
+
+def test_empty_batch_and_all_invalid_are_noops(gsc):
+    c, _, _ = make_cfg1(gsc)
+    P = rows(c)
+    st = c.fit(np.zeros((0, 3), np.float32), np.zeros(0, np.int32), np.zeros((0, 3), np.float32))
+    torch.cuda.synchronize()
+    assert st.step == 0 and st.n_valid == 0
+    x, ln, rgb = workload.fit_batch(1, S=1000)
+    st = c.fit(cuda(x), cuda(np.zeros_like(ln)), cuda(rgb))
+    torch.cuda.synchronize()
+    assert st.step == 0 and st.n_dropped == 1000
+    np.testing.assert_array_equal(rows(c), P)
+    st = c.fit(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    assert st.step == 1                                            # schedule starts at t = 1
+
+
+def test_level_skip_and_schedule_reset(gsc):
+    c, _, _ = make_cfg1(gsc)
+    P = rows(c)
+    x, ln, rgb = workload.fit_batch(1, S=20000)
+    ln[:] = 1
+    st = c.fit(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    P1 = rows(c)
+    np.testing.assert_array_equal(P1[4096:], P[4096:])           # levels 1, 2 skipped (A12)
+    assert st.count[1] == 0 and st.step == 1
+    st = c.fit(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    assert st.step == 2
+    c.reset_schedule()
+    st = c.fit(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    assert st.step == 1
+
+
+# ------------------------------------------------------- whole fit (100 steps)
+def _run_curve(c, oc, batches, steps):
+    lg, lo = [], []
+    for s in range(steps):
+        x, ln, rgb = batches(s)
+        st = c.fit(cuda(x), cuda(ln), cuda(rgb))
+        torch.cuda.synchronize()
+        lg.append(sum(st.loss[:c.L]))
+        lo.append(oc.fit(x.astype(np.float64), ln, rgb.astype(np.float64))["loss"].sum())
+    return np.array(lg), np.array(lo)
+
+
+def test_cfg0_recovery_100_steps_loss_parity(gsc):
+    """BASELINE configs[0]: 64 Gaussians, 4096 clean samples of a known mixture, 100 steps."""
+    pos, alb, ls = workload.cfg0_lattice()
+    hp = gsc.default_hparams(lr_schedule=0)
+    c = gsc.GSCache([64], pos, alb, init_log_scale=ls, seed=1, hparams=hp)
+    P0 = rows(c)
+    dmu, col = workload.cfg0_truth_perturbation()
+    T = P0.copy()
+    T[:, 0:3] += dmu
+    T[:, 7:10] = col
+    x, ln = workload.cfg0_samples()
+    y, _ = oracle.eval_brute(T, x.astype(np.float64))
+    y = y.astype(np.float32)
+    oc = oracle.OracleCache([64], P0, hp=dict(lr_schedule=0))
+    lg, lo = _run_curve(c, oc, lambda s: (x, ln, y), 100)
+    assert abs(lg[-1] - lo[-1]) <= 0.01 * lo[-1], (lg[-1], lo[-1])
+    np.testing.assert_allclose(lg, lo, rtol=0.01)
+    assert lg[-1] <= 1e-3 * lg[0]
+
+
+def test_cfg1_noisy_100_steps_loss_parity(gsc):
+    """BASELINE configs[1] (3 levels 4096/1024/256, noisy samples): loss at step 100 within 1 %."""
+    c, _, _ = make_cfg1(gsc)
+    oc = oracle.OracleCache([4096, 1024, 256], rows(c), grids=c.grids())
+    S = 65536
+    lg, lo = _run_curve(c, oc, lambda s: workload.fit_batch(1, frame=s, S=S), 100)
+    assert abs(lg[-1] - lo[-1]) <= 0.01 * lo[-1], (lg[-1], lo[-1])
+    np.testing.assert_allclose(lg, lo, rtol=0.01)
+
+
+# ------------------------------------------------------------ full size, sampled
+def test_cfg2_full_size_sampled(gsc):
+    """configs[2] at full size in bench.py's launch configuration: fit + full-frame query;
+    sampled query outputs against per-point brute force; level counts exact."""
+    pos, alb = workload.init_cloud(2)
+    counts = workload.CONFIGS[2]["counts"]
+    c = gsc.GSCache(counts, cuda(pos), cuda(alb), seed=2)
+    x, ln, rgb = workload.fit_batch(2)
+    xq, lq = workload.query_batch(2)
+    c.reserve(len(x), len(xq))
+    P = rows(c)
+    y = c.query(cuda(xq), cuda(lq)).cpu().numpy()
+    st = c.fit(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    idx = np.random.default_rng(7).choice(len(xq), 3000, replace=False)
+    yo, lv, _ = oracle.query(c.goff, P, xq[idx].astype(np.float64), lq[idx])
+    check_forward(y[idx], yo, P, c.goff, xq[idx], lv, what="cfg2 sampled")
+    lvl = oracle.level_of(ln, 4, x.astype(np.float64), rgb.astype(np.float64))
+    for l in range(4):
+        assert st.count[l] == int((lvl == l).sum())
+    assert st.n_valid + st.n_dropped == len(x)
+    assert np.isfinite(st.loss[:4]).all() and st.n_pairs > 0
+
+
+def test_cuda_graph_replay_matches_eager(gsc):
+    c1, _, _ = make_cfg1(gsc)
+    c2, _, _ = make_cfg1(gsc)
+    x, ln, rgb = workload.fit_batch(1, S=65536)
+    xq, lq = workload.query_batch(1, S=65536)
+    X, LN, RGB, XQ, LQ = map(cuda, (x, ln, rgb, xq, lq))
+    out = torch.empty((65536, 3), device="cuda")
+    for c in (c1, c2):
+        c.reserve(65536, 65536)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        c2.query(XQ, LQ, out=out, stream=s)        # warm-up outside capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        c2.query(XQ, LQ, out=out, stream=s)
+        c2.fit(X, LN, RGB, stream=s)
+    for _ in range(3):
+        c1.query(XQ, LQ)
+        c1.fit(X, LN, RGB)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(rows(c2), rows(c1), rtol=1e-5, atol=1e-6)
