@@ -47,6 +47,8 @@ def rows(c):
 def check_forward(y, yo, P, goff, x, lv, tau=3.0, what=""):
     """Element tolerance + A3 boundary allowance computed by brute force for failures."""
     y, yo = np.asarray(y, np.float64), np.asarray(yo, np.float64)
+    if y.size == 0:
+        return 0
     tol = 1e-5 * np.abs(yo) + 1e-7 * max(np.abs(yo).max(), 1e-30)
     bad = np.nonzero((np.abs(y - yo) > tol).any(axis=1))[0]
     amb_count = 0
