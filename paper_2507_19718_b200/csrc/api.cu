@@ -52,15 +52,15 @@ static cudaError_t dalloc(T** p, size_t n) {
 
 struct Scratch {
   int64_t cap = 0;
-  uint32_t *key = nullptr, *rank = nullptr, *bidx = nullptr;
-  float *bx = nullptr, *by = nullptr, *bz = nullptr, *br = nullptr, *bg = nullptr, *bb = nullptr;
+  uint32_t *key = nullptr, *rank = nullptr;
+  float4* bin = nullptr;
   uint32_t *cell_count = nullptr, *cell_start = nullptr, *totals = nullptr;
   uint2* tiles = nullptr;
   WorkItem* work = nullptr;
   float *in_pos = nullptr, *in_rgb = nullptr, *out = nullptr;
   int32_t* in_len = nullptr;
   void release() {
-    void* ps[] = {key, rank, bidx, bx, by, bz, br, bg, bb, cell_count, cell_start, totals, tiles, work,
+    void* ps[] = {key, rank, bin, cell_count, cell_start, totals, tiles, work,
                   in_pos, in_rgb, out, in_len};
     for (void* p : ps) if (p) cudaFree(p);
     *this = Scratch();
@@ -133,9 +133,7 @@ static gc_status ensure_scratch(gc_cache c, Scratch& sc, int64_t S, bool fit, cu
   int64_t ntiles = (c->NC + kScanTile - 1) / kScanTile;
   int64_t work_cap = cap / kCH + std::min<int64_t>(cap, c->NC) + 2;
   CK(dalloc(&sc.key, cap)); CK(dalloc(&sc.rank, cap));
-  CK(dalloc(&sc.bx, cap)); CK(dalloc(&sc.by, cap)); CK(dalloc(&sc.bz, cap));
-  if (fit) { CK(dalloc(&sc.br, cap)); CK(dalloc(&sc.bg, cap)); CK(dalloc(&sc.bb, cap)); }
-  else CK(dalloc(&sc.bidx, cap));
+  CK(dalloc(&sc.bin, (fit ? 2 : 1) * cap));
   CK(dalloc(&sc.cell_count, c->NC)); CK(dalloc(&sc.cell_start, c->NC + 1));
   CK(dalloc(&sc.tiles, ntiles)); CK(dalloc(&sc.totals, 4));
   CK(dalloc(&sc.work, work_cap));
@@ -435,14 +433,14 @@ gc_status gc_fit(gc_cache c, const float* pos, const int32_t* path_len, const fl
       if (hrgb) { CK(cudaMemcpyAsync(F.in_rgb, rgb, sizeof(float) * 3 * S, cudaMemcpyHostToDevice, s)); rgb = F.in_rgb; }
     }
   }
-  IngestBufs b{F.key, F.rank, F.cell_count, F.bx, F.by, F.bz, F.br, F.bg, F.bb, nullptr};
+  IngestBufs b{F.key, F.rank, F.cell_count, F.bin};
   CK(cudaMemsetAsync(F.cell_count, 0, sizeof(uint32_t) * c->NC, s));
   if (S > 0) launch_keys(pos, path_len, rgb, -1, S, c->geom, b, s, &c->prof);
   launch_scan(F.cell_count, c->NC, kCH, F.tiles, F.totals, F.cell_start, nullptr, F.work, c->geom, s, &c->prof);
   if (S > 0) launch_scatter(pos, rgb, S, F.cell_start, b, s, &c->prof);
   FitArgs fa;
   fa.work = F.work; fa.n_work = F.totals + 1; fa.csr_off = c->csr_off; fa.csr_idx = c->csr_idx; fa.rec = c->rec;
-  fa.bx = F.bx; fa.by = F.by; fa.bz = F.bz; fa.br = F.br; fa.bg = F.bg; fa.bb = F.bb;
+  fa.bin = F.bin;
   fa.grad = c->grad; fa.partial = c->partial;
   const float tau = c->hp.cutoff_sigma;
   fa.tau2 = tau * tau; fa.hdr_eps = c->hp.hdr_eps; fa.mode = c->hp.loss_grad_mode; fa.L = c->L;
@@ -485,14 +483,14 @@ gc_status gc_query(gc_cache c, const float* pos, const int32_t* path_len, int le
     if (hlen) { CK(cudaMemcpyAsync(Q.in_len, path_len, sizeof(int32_t) * S, cudaMemcpyHostToDevice, s)); path_len = Q.in_len; }
   }
   float* dout = hout ? Q.out : out_rgb;
-  IngestBufs b{Q.key, Q.rank, Q.cell_count, Q.bx, Q.by, Q.bz, nullptr, nullptr, nullptr, Q.bidx};
+  IngestBufs b{Q.key, Q.rank, Q.cell_count, Q.bin};
   CK(cudaMemsetAsync(Q.cell_count, 0, sizeof(uint32_t) * c->NC, s));
   launch_keys_query(pos, path_len, path_len ? -1 : level, S, c->geom, b, dout, s, &c->prof);
   launch_scan(Q.cell_count, c->NC, kCH, Q.tiles, Q.totals, Q.cell_start, nullptr, Q.work, c->geom, s, &c->prof);
   launch_scatter(pos, nullptr, S, Q.cell_start, b, s, &c->prof);
   QueryArgs qa;
   qa.work = Q.work; qa.n_work = Q.totals + 1; qa.csr_off = c->csr_off; qa.csr_idx = c->csr_idx; qa.rec = c->rec;
-  qa.bx = Q.bx; qa.by = Q.by; qa.bz = Q.bz; qa.bidx = Q.bidx; qa.out = dout;
+  qa.bin = Q.bin; qa.out = dout;
   const float tau = c->hp.cutoff_sigma;
   qa.tau2 = tau * tau;
   launch_query(qa, c->q_grid, s, &c->prof);

@@ -10,8 +10,7 @@ namespace gsc {
 
 constexpr int kMaxL = GC_MAX_LEVELS;
 constexpr int kNP = 14;              // raw floats per Gaussian
-constexpr int kCH = 256;             // samples per work item == threads of the fwd/bwd block
-constexpr int kTG = 256;             // Gaussians per shared-memory tile
+constexpr int kCH = 32;              // samples per work item == one warp of the fwd/bwd kernels
 constexpr int kScanTile = 2048;      // 256 threads x 8 items
 constexpr uint32_t kInvalidKey = 0xFFFFFFFFu;
 

@@ -1,77 +1,109 @@
 // fwdbwd.cu -- the fused forward + HDR loss + backward kernel of gc_fit (A4) and the
-// forward-only lookup kernel of gc_query (A7).
+// forward-only lookup kernel of gc_query (A7).  Warp-centric: no block barriers.
 //
-// One persistent CTA of 256 threads walks the work list; a work item is <= 256 samples of
-// one (level, cell) bin.  The cell's culling list (C8) is gathered into shared memory as
-// 48-byte evaluation records, 256 Gaussians per tile.
-//   pass 1 (thread = sample): yhat = sum v_j e^{-Q/2} over the staged Gaussians with
-//          Q <= tau^2 (C3), the Eq. 4 loss and g = dL/dyhat (C4, unnormalised; the 1/(3k_l)
-//          factor is applied by the optimizer once k_l is known globally, C9);
-//   pass 2 (thread = Gaussian x sample-split): the 12 coefficient-gradient terms of C5
-//          accumulated in registers over the shared-memory samples, merged across the K
-//          sample splits with __shfl_xor_sync, then 3 x red.global.add.v4.f32 per
-//          (Gaussian, work item) that touched any sample -- never shared-memory float atomics.
+// A work item is <= 32 binned samples of one (level, cell) bin; one warp owns it.  The
+// cell's culling list (C8) is staged into the warp's shared memory 32 evaluation records
+// (48 B each) at a time.
+//   pass 1 (lane = sample): yhat = sum v_j e^{-Q/2} over the candidates with Q <= tau^2 (C3),
+//          with the warp ballot of every candidate kept as a 32-bit sample mask; the Eq. 4
+//          loss and g = dL/dyhat (C4, unnormalised -- the 1/(3 k_l) factor is applied by the
+//          optimizer once k_l is known globally, C9).
+//   pass 2 (lane = contributing pair): the masks are expanded into a candidate-major pair list;
+//          each lane evaluates the 12 coefficient-gradient terms of C5 for one pair, a
+//          segmented warp-shuffle scan merges the pairs of each Gaussian, and the segment's last
+//          lane issues 3 x red.global.add.v4.f32.  Work is proportional to contributing pairs,
+//          every lane busy; never shared-memory float atomics (a CAS loop on sm_100a).
 #include "common.cuh"
 #include "kernels.h"
 
 namespace gsc {
 
 constexpr int kPart = kMaxL + 2;
-constexpr float kNegHalfLog2e = -0.72134752044448170f;   // -0.5 * log2(e)
+constexpr int kWarps = 8;                                 // warps per CTA
+constexpr int kMaskCap = 256;                             // candidate masks kept per warp
+constexpr float kNegHalfLog2e = -0.72134752044448170f;    // -0.5 * log2(e)
 
-__global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
-  __shared__ float4 s_r0[kTG], s_r1[kTG], s_r2[kTG];
-  __shared__ int s_gid[kTG];
-  __shared__ float s_x[kCH], s_y[kCH], s_z[kCH], s_g0[kCH], s_g1[kCH], s_g2[kCH];
-  __shared__ float s_wl[8];
-  __shared__ int s_wp[8];
-  __shared__ double s_loss[kMaxL];
-  __shared__ unsigned long long s_pairs, s_cand;
+struct ChunkSmem {
+  float4 r0[32], r1[32], r2[32];   // staged records of one 32-candidate chunk
+  int gid[32];
+};
 
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  if (t < kMaxL) s_loss[t] = 0.0;
-  if (t == 0) { s_pairs = 0ull; s_cand = 0ull; }
+struct WarpSmem : ChunkSmem {
+  float4 sxg[32];                  // sample x, y, z, g0
+  float2 sg[32];                   // sample g1, g2
+  uint32_t mask[kMaskCap];         // per candidate: ballot of the warp's samples inside
+  uint16_t pairs[32 * 32];         // (candidate << 5) | sample, candidate-major
+};
+
+__device__ __forceinline__ Rec rec_from(const ChunkSmem& w, int k) {
+  const float4 p = w.r0[k], q = w.r1[k], r = w.r2[k];
+  return Rec{p.x, p.y, p.z, p.w, q.x, q.y, q.z, q.w, r.x, r.y, r.z, r.w};
+}
+
+__device__ __forceinline__ void stage_chunk(ChunkSmem& w, const int32_t* __restrict__ csr_idx,
+                                            const float4* __restrict__ rec, int base, int kc, int lane) {
+  if (lane < kc) {
+    const int gid = __ldg(csr_idx + base + lane);
+    w.gid[lane] = gid;
+    w.r0[lane] = __ldg(rec + 3 * gid); w.r1[lane] = __ldg(rec + 3 * gid + 1); w.r2[lane] = __ldg(rec + 3 * gid + 2);
+  }
+  __syncwarp();
+}
+
+// Sample-parallel evaluation of one staged chunk: accumulates yhat, returns nothing; the
+// ballot of candidate k is stored to masks[k] (if non-null).
+__device__ __forceinline__ void eval_chunk(const ChunkSmem& w, int kc, bool act, float x, float y, float z,
+                                           float tau2, float& y0, float& y1, float& y2, int& np,
+                                           uint32_t* masks, int lane) {
+#pragma unroll 2
+  for (int k = 0; k < kc; ++k) {
+    const Rec g = rec_from(w, k);
+    float dx, dy, dz, tx, ty, tz;
+    const float Q = quad_form(g, x, y, z, dx, dy, dz, tx, ty, tz);
+    const bool in = act && Q <= tau2;
+    const uint32_t m = __ballot_sync(0xffffffffu, in);
+    if (masks && lane == 0) masks[k] = m;
+    if (m) {
+      if (in) {
+        const float e = ex2_approx(Q * kNegHalfLog2e);
+        y0 = fmaf(g.v0, e, y0); y1 = fmaf(g.v1, e, y1); y2 = fmaf(g.v2, e, y2);
+        ++np;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(256, 3) k_fwdbwd(FitArgs a) {
+  __shared__ WarpSmem sm[kWarps];
+  __shared__ double s_loss[kWarps][kMaxL];
+  __shared__ unsigned long long s_cnt[kWarps][2];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WarpSmem& w = sm[wid];
+  if (lane < kMaxL) s_loss[wid][lane] = 0.0;
+  unsigned long long pairs_acc = 0, cand_acc = 0;
   const uint32_t n_work = *a.n_work;
   const float tau2 = a.tau2, eps = a.hdr_eps;
+  const uint32_t gw = blockIdx.x * kWarps + wid, nw = gridDim.x * kWarps;
 
-  for (uint32_t w = blockIdx.x; w < n_work; w += gridDim.x) {
-    const WorkItem wi = a.work[w];
-    const int lo = (int)a.csr_off[wi.cell];
-    const int C = (int)a.csr_off[wi.cell + 1] - lo;
-    const int n = wi.count;
-    const bool act = t < n;
+  for (uint32_t it = gw; it < n_work; it += nw) {
+    const WorkItem wi = a.work[it];
+    const int lo = (int)__ldg(a.csr_off + wi.cell);
+    const int C = (int)__ldg(a.csr_off + wi.cell + 1) - lo;
+    const bool act = lane < wi.count;
     float x = 0.f, y = 0.f, z = 0.f, xr = 0.f, xg = 0.f, xb = 0.f;
     if (act) {
-      const int si = wi.start + t;
-      x = a.bx[si]; y = a.by[si]; z = a.bz[si];
-      xr = a.br[si]; xg = a.bg[si]; xb = a.bb[si];
+      const float4 p = __ldcs(a.bin + 2 * (int64_t)(wi.start + lane));
+      const float4 q = __ldcs(a.bin + 2 * (int64_t)(wi.start + lane) + 1);
+      x = p.x; y = p.y; z = p.z; xr = p.w; xg = q.x; xb = q.y;
     }
-    // ---------------- pass 1: thread = sample
+    // ---------------- pass 1
     float y0 = 0.f, y1 = 0.f, y2 = 0.f;
     int np = 0;
-    for (int tb = 0; tb < C; tb += kTG) {
-      const int Ct = min(kTG, C - tb);
-      __syncthreads();
-      if (t < Ct) {
-        const int gid = a.csr_idx[lo + tb + t];
-        s_gid[t] = gid;
-        s_r0[t] = __ldg(a.rec + 3 * gid); s_r1[t] = __ldg(a.rec + 3 * gid + 1); s_r2[t] = __ldg(a.rec + 3 * gid + 2);
-      }
-      __syncthreads();
-      if (act) {
-#pragma unroll 4
-        for (int k = 0; k < Ct; ++k) {
-          const float4 p = s_r0[k], q = s_r1[k], r = s_r2[k];
-          const Rec g{p.x, p.y, p.z, p.w, q.x, q.y, q.z, q.w, r.x, r.y, r.z, r.w};
-          float dx, dy, dz, tx, ty, tz;
-          const float Q = quad_form(g, x, y, z, dx, dy, dz, tx, ty, tz);
-          if (Q <= tau2) {
-            const float e = ex2_approx(Q * kNegHalfLog2e);
-            y0 = fmaf(g.v0, e, y0); y1 = fmaf(g.v1, e, y1); y2 = fmaf(g.v2, e, y2);
-            ++np;
-          }
-        }
-      }
+    for (int cb = 0; cb < C; cb += 32) {
+      const int kc = min(32, C - cb);
+      stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane);
+      eval_chunk(w, kc, act, x, y, z, tau2, y0, y1, y2, np, cb + 32 <= kMaskCap ? w.mask + cb : nullptr, lane);
     }
     // ---------------- Eq. 4 loss and dL/dyhat (unnormalised)
     float g0 = 0.f, g1 = 0.f, g2 = 0.f, ls = 0.f;
@@ -86,138 +118,150 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
         g2 = -2.f * r2 * (xb + eps) * i2 / d2;
       }
     }
-    __syncthreads();
-    s_x[t] = x; s_y[t] = y; s_z[t] = z; s_g0[t] = g0; s_g1[t] = g1; s_g2[t] = g2;
+    w.sxg[lane] = make_float4(x, y, z, g0);
+    w.sg[lane] = make_float2(g1, g2);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       ls += __shfl_xor_sync(0xffffffffu, ls, o);
       np += __shfl_xor_sync(0xffffffffu, np, o);
     }
-    if (lane == 0) { s_wl[warp] = ls; s_wp[warp] = np; }
-    __syncthreads();
-    if (t == 0) {
-      float bl = 0.f; int bp = 0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) { bl += s_wl[k]; bp += s_wp[k]; }
-      s_loss[wi.level] += (double)bl;
-      s_pairs += (unsigned long long)bp;
-      s_cand += (unsigned long long)n * (unsigned long long)C;
-    }
-    // ---------------- pass 2: thread = (Gaussian jj, sample split sp)
-    for (int tb = 0; tb < C; tb += kTG) {
-      const int Ct = min(kTG, C - tb);
-      if (C > kTG) {
-        __syncthreads();
-        if (t < Ct) {
-          const int gid = a.csr_idx[lo + tb + t];
-          s_gid[t] = gid;
-          s_r0[t] = __ldg(a.rec + 3 * gid); s_r1[t] = __ldg(a.rec + 3 * gid + 1); s_r2[t] = __ldg(a.rec + 3 * gid + 2);
-        }
-        __syncthreads();
+    if (lane == 0) s_loss[wid][wi.level] += (double)ls;
+    pairs_acc += (unsigned)np;
+    cand_acc += (unsigned long long)wi.count * (unsigned long long)C;
+    if (np == 0) { __syncwarp(); continue; }
+    __syncwarp();
+    // ---------------- pass 2: contributing pairs, candidate-major
+    for (int cb = 0; cb < C; cb += 32) {
+      const int kc = min(32, C - cb);
+      if (C > 32) stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane);
+      uint32_t mk;
+      if (cb + 32 <= kMaskCap) {
+        mk = lane < kc ? w.mask[cb + lane] : 0u;
+      } else {                         // re-derive the ballots exactly as pass 1 did
+        float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+        int tn = 0;
+        eval_chunk(w, kc, act, x, y, z, tau2, t0, t1, t2, tn, w.mask, lane);
+        mk = lane < kc ? w.mask[lane] : 0u;
       }
-      // K = number of sample splits per Gaussian: largest power of two with K * Ct <= 256, K <= 32
-      int logK = 0;
-      while (logK < 5 && (Ct << (logK + 1)) <= kCH) ++logK;
-      const int K = 1 << logK;
-      const int jj = t >> logK, sp = t & (K - 1);
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f, a6 = 0.f, a7 = 0.f,
-            a8 = 0.f, a9 = 0.f, a10 = 0.f, a11 = 0.f;
-      bool touched = false;
-      if (jj < Ct) {
-        const float4 p = s_r0[jj], q = s_r1[jj], r = s_r2[jj];
-        const Rec g{p.x, p.y, p.z, p.w, q.x, q.y, q.z, q.w, r.x, r.y, r.z, r.w};
-        for (int s = sp; s < n; s += K) {
+      const int cnt = __popc(mk);
+      int off = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, off, o);
+        if (lane >= o) off += v;
+      }
+      const int total = __shfl_sync(0xffffffffu, off, 31);
+      if (total == 0) continue;
+      off -= cnt;
+      for (uint32_t b = mk; b; b &= b - 1) w.pairs[off++] = (uint16_t)((lane << 5) | (__ffs(b) - 1));
+      __syncwarp();
+      for (int p0 = 0; p0 < total; p0 += 32) {
+        const int p = p0 + lane;
+        const bool valid = p < total;
+        int k = 32 + lane;              // unique key for idle lanes: own segment
+        float v[12];
+#pragma unroll
+        for (int q = 0; q < 12; ++q) v[q] = 0.f;
+        if (valid) {
+          const uint32_t e16 = w.pairs[p];
+          k = e16 >> 5;
+          const int s = e16 & 31;
+          const Rec g = rec_from(w, k);
+          const float4 sx = w.sxg[s];
+          const float2 sg = w.sg[s];
           float dx, dy, dz, tx, ty, tz;
-          const float Q = quad_form(g, s_x[s], s_y[s], s_z[s], dx, dy, dz, tx, ty, tz);
-          if (Q <= tau2) {
-            const float e = ex2_approx(Q * kNegHalfLog2e);
-            const float c0 = s_g0[s], c1 = s_g1[s], c2 = s_g2[s];
-            const float he = (c0 * g.v0 + c1 * g.v1 + c2 * g.v2) * e;
-            a0 = fmaf(he, tx, a0); a1 = fmaf(he, ty, a1); a2 = fmaf(he, tz, a2);   // d mu
-            const float k = -0.5f * he;
-            const float kx = k * dx, ky = k * dy, kz = k * dz;
-            a3 = fmaf(kx, dx, a3); a4 = fmaf(ky, dy, a4); a5 = fmaf(kz, dz, a5);   // dA00 dA11 dA22
-            a6 = fmaf(kx, dy, a6); a7 = fmaf(kx, dz, a7); a8 = fmaf(ky, dz, a8);   // dA01 dA02 dA12
-            a9 = fmaf(c0, e, a9); a10 = fmaf(c1, e, a10); a11 = fmaf(c2, e, a11);  // d v
-            touched = true;
+          const float Q = quad_form(g, sx.x, sx.y, sx.z, dx, dy, dz, tx, ty, tz);
+          const float e = ex2_approx(Q * kNegHalfLog2e);
+          const float he = (sx.w * g.v0 + sg.x * g.v1 + sg.y * g.v2) * e;
+          v[0] = he * tx; v[1] = he * ty; v[2] = he * tz;                 // d mu
+          const float kk = -0.5f * he;
+          const float kx = kk * dx, ky = kk * dy, kz = kk * dz;
+          v[3] = kx * dx; v[4] = ky * dy; v[5] = kz * dz;                 // dA00 dA11 dA22
+          v[6] = kx * dy; v[7] = kx * dz; v[8] = ky * dz;                 // dA01 dA02 dA12
+          v[9] = sx.w * e; v[10] = sg.x * e; v[11] = sg.y * e;            // d v
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, k);
+        const int head = __ffs(peers) - 1, tail = 31 - __clz(peers);
+        // segmented inclusive scan (segments are contiguous: pairs are candidate-major);
+        // stops as soon as no segment is longer than the current stride
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const bool need = lane - o >= head;
+          if (!__any_sync(0xffffffffu, need)) break;
+#pragma unroll
+          for (int q = 0; q < 12; ++q) {
+            const float t = __shfl_up_sync(0xffffffffu, v[q], o);
+            if (need) v[q] += t;
           }
         }
+        if (valid && lane == tail) {
+          float* gp = a.grad + 12 * (int64_t)w.gid[k];
+          red_add_v4(gp, v[0], v[1], v[2], v[3]);
+          red_add_v4(gp + 4, v[4], v[5], v[6], v[7]);
+          red_add_v4(gp + 8, v[8], v[9], v[10], v[11]);
+        }
       }
-      for (int o = K >> 1; o > 0; o >>= 1) {
-        a0 += __shfl_xor_sync(0xffffffffu, a0, o); a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-        a2 += __shfl_xor_sync(0xffffffffu, a2, o); a3 += __shfl_xor_sync(0xffffffffu, a3, o);
-        a4 += __shfl_xor_sync(0xffffffffu, a4, o); a5 += __shfl_xor_sync(0xffffffffu, a5, o);
-        a6 += __shfl_xor_sync(0xffffffffu, a6, o); a7 += __shfl_xor_sync(0xffffffffu, a7, o);
-        a8 += __shfl_xor_sync(0xffffffffu, a8, o); a9 += __shfl_xor_sync(0xffffffffu, a9, o);
-        a10 += __shfl_xor_sync(0xffffffffu, a10, o); a11 += __shfl_xor_sync(0xffffffffu, a11, o);
-        touched = touched | (bool)__shfl_xor_sync(0xffffffffu, (int)touched, o);
-      }
-      if (sp == 0 && jj < Ct && touched) {
-        float* gp = a.grad + 12 * (int64_t)s_gid[jj];
-        red_add_v4(gp, a0, a1, a2, a3);
-        red_add_v4(gp + 4, a4, a5, a6, a7);
-        red_add_v4(gp + 8, a8, a9, a10, a11);
-      }
+      __syncwarp();
     }
   }
+  if (lane == 0) { s_cnt[wid][0] = pairs_acc; s_cnt[wid][1] = cand_acc; }
   __syncthreads();
   double* part = a.partial + (int64_t)blockIdx.x * kPart;
-  if (t < kMaxL) part[t] = s_loss[t];
-  if (t == 0) { part[kMaxL] = (double)s_pairs; part[kMaxL + 1] = (double)s_cand; }
+  if (threadIdx.x < kMaxL) {
+    double s = 0.0;
+    for (int q = 0; q < kWarps; ++q) s += s_loss[q][threadIdx.x];
+    part[threadIdx.x] = s;
+  }
+  if (threadIdx.x == 0) {
+    unsigned long long p = 0, c = 0;
+    for (int q = 0; q < kWarps; ++q) { p += s_cnt[q][0]; c += s_cnt[q][1]; }
+    part[kMaxL] = (double)p;
+    part[kMaxL + 1] = (double)c;
+  }
 }
 
 __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
-  __shared__ float4 s_r0[kTG], s_r1[kTG], s_r2[kTG];
-  const int t = threadIdx.x;
+  __shared__ ChunkSmem sm[kWarps];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  ChunkSmem& w = sm[wid];
   const uint32_t n_work = *a.n_work;
   const float tau2 = a.tau2;
-  for (uint32_t w = blockIdx.x; w < n_work; w += gridDim.x) {
-    const WorkItem wi = a.work[w];
-    const int lo = (int)a.csr_off[wi.cell];
-    const int C = (int)a.csr_off[wi.cell + 1] - lo;
-    const bool act = t < wi.count;
+  const uint32_t gw = blockIdx.x * kWarps + wid, nw = gridDim.x * kWarps;
+  for (uint32_t it = gw; it < n_work; it += nw) {
+    const WorkItem wi = a.work[it];
+    const int lo = (int)__ldg(a.csr_off + wi.cell);
+    const int C = (int)__ldg(a.csr_off + wi.cell + 1) - lo;
+    const bool act = lane < wi.count;
     float x = 0.f, y = 0.f, z = 0.f;
-    if (act) { const int si = wi.start + t; x = a.bx[si]; y = a.by[si]; z = a.bz[si]; }
+    uint32_t idx = 0;
+    if (act) {
+      const float4 p = __ldcs(a.bin + wi.start + lane);
+      x = p.x; y = p.y; z = p.z; idx = __float_as_uint(p.w);
+    }
     float y0 = 0.f, y1 = 0.f, y2 = 0.f;
-    for (int tb = 0; tb < C; tb += kTG) {
-      const int Ct = min(kTG, C - tb);
-      __syncthreads();
-      if (t < Ct) {
-        const int gid = a.csr_idx[lo + tb + t];
-        s_r0[t] = __ldg(a.rec + 3 * gid); s_r1[t] = __ldg(a.rec + 3 * gid + 1); s_r2[t] = __ldg(a.rec + 3 * gid + 2);
-      }
-      __syncthreads();
-      if (act) {
-#pragma unroll 4
-        for (int k = 0; k < Ct; ++k) {
-          const float4 p = s_r0[k], q = s_r1[k], r = s_r2[k];
-          const Rec g{p.x, p.y, p.z, p.w, q.x, q.y, q.z, q.w, r.x, r.y, r.z, r.w};
-          float dx, dy, dz, tx, ty, tz;
-          const float Q = quad_form(g, x, y, z, dx, dy, dz, tx, ty, tz);
-          if (Q <= tau2) {
-            const float e = ex2_approx(Q * kNegHalfLog2e);
-            y0 = fmaf(g.v0, e, y0); y1 = fmaf(g.v1, e, y1); y2 = fmaf(g.v2, e, y2);
-          }
-        }
-      }
+    int np = 0;
+    for (int cb = 0; cb < C; cb += 32) {
+      const int kc = min(32, C - cb);
+      stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane);
+      eval_chunk(w, kc, act, x, y, z, tau2, y0, y1, y2, np, nullptr, lane);
     }
     if (act) {
-      const uint32_t i = a.bidx[wi.start + t];
-      a.out[3 * (int64_t)i] = y0; a.out[3 * (int64_t)i + 1] = y1; a.out[3 * (int64_t)i + 2] = y2;
+      __stcs(a.out + 3 * (int64_t)idx, y0); __stcs(a.out + 3 * (int64_t)idx + 1, y1);
+      __stcs(a.out + 3 * (int64_t)idx + 2, y2);
     }
   }
 }
 
-static int persistent_grid(const void* fn) {
+static int persistent_grid(const void* fn, size_t smem) {
   int dev = 0, sms = 148, per = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 256, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 256, smem);
   return sms * std::max(per, 1);
 }
 
-int fwdbwd_grid() { static int g = persistent_grid((const void*)k_fwdbwd); return g; }
-int query_grid() { static int g = persistent_grid((const void*)k_query); return g; }
+int fwdbwd_grid() { static int g = persistent_grid((const void*)k_fwdbwd, 0); return g; }
+int query_grid() { static int g = persistent_grid((const void*)k_query, 0); return g; }
 
 void launch_fwdbwd(const FitArgs& a, int grid, cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "fwdbwd", s);

@@ -1,56 +1,101 @@
 // ingest.cu -- SoA sample ingest binned by (level, cell): validation and level assignment
 // (C2; sec.3.5 per-level path buffers), fp64 cell keys (C8), a counting sort
-// whose histogram ranks come from warp-aggregated atomics, and the scatter into planar bins.
+// whose ranks come from warp-aggregated atomics, and the scatter into cell-major bins of
+// full 32-byte sectors.  Each thread handles kU samples with all loads issued up front
+// (memory-level parallelism: the kernels are latency-bound otherwise).
 #include "common.cuh"
 #include "kernels.h"
 
 namespace gsc {
 
+constexpr int kU = 4;   // samples per thread per iteration
+
 __global__ void __launch_bounds__(256) k_keys(const float* __restrict__ pos, const int32_t* __restrict__ len,
                                               const float* __restrict__ rgb, int level_fixed, int64_t S,
                                               LevelGeom g, IngestBufs b, float* out_zero) {
   const int lane = threadIdx.x & 31;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  // warp-uniform trip count so that __match_any_sync sees full warps
-  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < S; i0 += stride) {
-    int64_t i = i0 + lane;
-    bool ok = i < S;
-    uint32_t key = kInvalidKey;
-    if (ok) {
-      float x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
-      ok = isfinite(x) && isfinite(y) && isfinite(z);
-      int l = level_fixed;
-      if (level_fixed < 0) {
-        int n = len[i];
-        ok = ok && n >= 1;
-        l = min(n, g.L) - 1;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i0 = warp * 32 * kU; i0 < S; i0 += nwarps * 32 * kU) {
+    float x[kU], y[kU], z[kU], c[kU][3];
+    int n[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = i0 + u * 32 + lane;
+      if (i < S) {
+        x[u] = __ldcs(pos + 3 * i); y[u] = __ldcs(pos + 3 * i + 1); z[u] = __ldcs(pos + 3 * i + 2);
+        n[u] = level_fixed < 0 ? __ldcs(len + i) : 1;
+        if (rgb) { c[u][0] = __ldcs(rgb + 3 * i); c[u][1] = __ldcs(rgb + 3 * i + 1); c[u][2] = __ldcs(rgb + 3 * i + 2); }
+      } else {
+        x[u] = y[u] = z[u] = 0.f; n[u] = 0;
       }
-      if (rgb) ok = ok && isfinite(rgb[3 * i]) && isfinite(rgb[3 * i + 1]) && isfinite(rgb[3 * i + 2]);
-      if (ok) key = (uint32_t)sample_cell(g, l, x, y, z);
-      else if (out_zero) { out_zero[3 * i] = 0.f; out_zero[3 * i + 1] = 0.f; out_zero[3 * i + 2] = 0.f; }
     }
-    unsigned peers = __match_any_sync(0xffffffffu, key);
-    uint32_t rank = 0;
-    if (key != kInvalidKey) {
-      int leader = __ffs(peers) - 1;
-      uint32_t base = 0;
-      if (lane == leader) base = atomicAdd(b.cell_count + key, (uint32_t)__popc(peers));
-      base = __shfl_sync(peers, base, leader);
-      rank = base + __popc(peers & ((1u << lane) - 1u));
+    uint32_t key[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = i0 + u * 32 + lane;
+      bool ok = i < S && isfinite(x[u]) && isfinite(y[u]) && isfinite(z[u]);
+      int l = level_fixed;
+      if (level_fixed < 0) { ok = ok && n[u] >= 1; l = min(n[u], g.L) - 1; }
+      if (rgb) ok = ok && isfinite(c[u][0]) && isfinite(c[u][1]) && isfinite(c[u][2]);
+      key[u] = ok ? (uint32_t)sample_cell(g, l, x[u], y[u], z[u]) : kInvalidKey;
+      if (!ok && out_zero && i < S) { out_zero[3 * i] = 0.f; out_zero[3 * i + 1] = 0.f; out_zero[3 * i + 2] = 0.f; }
     }
-    if (i < S) { b.key[i] = key; b.rank[i] = rank; }
+    uint32_t rank[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const unsigned peers = __match_any_sync(0xffffffffu, key[u]);
+      rank[u] = 0;
+      if (key[u] != kInvalidKey) {
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(b.cell_count + key[u], (uint32_t)__popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        rank[u] = base + __popc(peers & ((1u << lane) - 1u));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = i0 + u * 32 + lane;
+      if (i < S) { b.key[i] = key[u]; b.rank[i] = rank[u]; }
+    }
   }
 }
 
 __global__ void __launch_bounds__(256) k_scatter(const float* __restrict__ pos, const float* __restrict__ rgb,
                                                  int64_t S, const uint32_t* __restrict__ cell_start, IngestBufs b) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t key = b.key[i];
-    if (key == kInvalidKey) continue;
-    uint32_t d = cell_start[key] + b.rank[i];
-    b.bx[d] = pos[3 * i]; b.by[d] = pos[3 * i + 1]; b.bz[d] = pos[3 * i + 2];
-    if (rgb) { b.br[d] = rgb[3 * i]; b.bg[d] = rgb[3 * i + 1]; b.bb[d] = rgb[3 * i + 2]; }
-    if (b.bidx) b.bidx[d] = (uint32_t)i;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (t >> 5) * 32 * kU + (t & 31); i0 < S; i0 += T * kU) {
+    uint32_t key[kU], rank[kU], d[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = i0 + u * 32;
+      key[u] = i < S ? __ldcs(b.key + i) : kInvalidKey;
+      rank[u] = i < S ? __ldcs(b.rank + i) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) d[u] = key[u] != kInvalidKey ? __ldg(cell_start + key[u]) + rank[u] : 0u;
+    float v[kU][6];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = i0 + u * 32;
+      if (key[u] != kInvalidKey) {
+        v[u][0] = __ldcs(pos + 3 * i); v[u][1] = __ldcs(pos + 3 * i + 1); v[u][2] = __ldcs(pos + 3 * i + 2);
+        if (rgb) { v[u][3] = __ldcs(rgb + 3 * i); v[u][4] = __ldcs(rgb + 3 * i + 1); v[u][5] = __ldcs(rgb + 3 * i + 2); }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (key[u] == kInvalidKey) continue;
+      const int64_t i = i0 + u * 32;
+      if (rgb) {
+        b.bin[2 * (int64_t)d[u]] = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
+        b.bin[2 * (int64_t)d[u] + 1] = make_float4(v[u][4], v[u][5], 0.f, 0.f);
+      } else {
+        b.bin[d[u]] = make_float4(v[u][0], v[u][1], v[u][2], __uint_as_float((uint32_t)i));
+      }
+    }
   }
 }
 
@@ -62,7 +107,7 @@ __global__ void k_levels_of(const uint32_t* key, int64_t S, LevelGeom g, int32_t
 }
 
 static int grid_for(int64_t n, int per_sm = 8) {
-  int64_t b = (n + 255) / 256;
+  int64_t b = (n + 256 * kU - 1) / (256 * kU);
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * per_sm));
 }
 

@@ -71,9 +71,8 @@ struct IngestBufs {
   uint32_t* key;        // [S] global cell id or kInvalidKey
   uint32_t* rank;       // [S] arrival rank inside the cell
   uint32_t* cell_count; // [NC]
-  float* bx; float* by; float* bz;          // [S] binned positions
-  float* br; float* bg; float* bb;          // [S] binned targets (fit only)
-  uint32_t* bidx;       // [S] original sample index (query only)
+  float4* bin;          // binned samples, cell-major: fit 2 x float4 (x,y,z,r | g,b,-,-),
+                        // query 1 x float4 (x,y,z, original index as bits)
 };
 void launch_keys(const float* pos, const int32_t* len, const float* rgb, int level_fixed,
                  int64_t S, const LevelGeom& g, IngestBufs b, cudaStream_t s, Profiler* prof);
@@ -88,7 +87,7 @@ void launch_levels_of(const uint32_t* key, int64_t S, const LevelGeom& g, int32_
 struct FitArgs {
   const WorkItem* work; const uint32_t* n_work;
   const uint32_t* csr_off; const int32_t* csr_idx; const float4* rec;
-  const float* bx; const float* by; const float* bz; const float* br; const float* bg; const float* bb;
+  const float4* bin;
   float* grad;          // [G][12]
   double* partial;      // [grid][kMaxL + 2]: per-block loss sums, pairs, candidates
   float tau2, hdr_eps; int mode; int L;
@@ -98,7 +97,7 @@ void launch_fwdbwd(const FitArgs& a, int grid, cudaStream_t s, Profiler* prof);
 struct QueryArgs {
   const WorkItem* work; const uint32_t* n_work;
   const uint32_t* csr_off; const int32_t* csr_idx; const float4* rec;
-  const float* bx; const float* by; const float* bz; const uint32_t* bidx;
+  const float4* bin;
   float* out; float tau2;
 };
 int query_grid();
