@@ -20,7 +20,8 @@ namespace gsc {
 
 constexpr int kPart = kMaxL + 2;
 constexpr int kWarps = 8;                                 // warps per CTA
-constexpr int kMaskCap = 256;                             // candidate masks kept per warp
+constexpr int kPairCap = 512;                             // recorded (sample, Gaussian) pairs per warp
+constexpr int kMaxChunks = 64;                            // recorded chunks per work item (C <= 2048)
 constexpr float kNegHalfLog2e = -0.72134752044448170f;    // -0.5 * log2(e)
 
 struct ChunkSmem {
@@ -31,8 +32,9 @@ struct ChunkSmem {
 struct WarpSmem : ChunkSmem {
   float4 sxg[32];                  // sample x, y, z, g0
   float2 sg[32];                   // sample g1, g2
-  uint32_t mask[kMaskCap];         // per candidate: ballot of the warp's samples inside
-  uint16_t pairs[32 * 32];         // (candidate << 5) | sample, candidate-major
+  uint16_t pkey[kPairCap];         // (candidate-in-chunk << 5) | sample, chunk- then candidate-major
+  float pe[kPairCap];              // e = exp(-Q/2) of the pair, as pass 1 computed it
+  uint16_t cend[kMaxChunks];       // end offset of every chunk's pairs
 };
 
 __device__ __forceinline__ Rec rec_from(const ChunkSmem& w, int k) {
@@ -42,6 +44,7 @@ __device__ __forceinline__ Rec rec_from(const ChunkSmem& w, int k) {
 
 __device__ __forceinline__ void stage_chunk(ChunkSmem& w, const int32_t* __restrict__ csr_idx,
                                             const float4* __restrict__ rec, int base, int kc, int lane) {
+  __syncwarp();
   if (lane < kc) {
     const int gid = __ldg(csr_idx + base + lane);
     w.gid[lane] = gid;
@@ -50,11 +53,14 @@ __device__ __forceinline__ void stage_chunk(ChunkSmem& w, const int32_t* __restr
   __syncwarp();
 }
 
-// Sample-parallel evaluation of one staged chunk: accumulates yhat, returns nothing; the
-// ballot of candidate k is stored to masks[k] (if non-null).
+// Sample-parallel evaluation of one staged chunk (lane = sample).  Accumulates yhat and, if
+// `rec` is given, appends every inside pair (k, lane, e) at pbase + rank among the ballot
+// (candidate-major), up to `cap` entries; pbase advances by the ballot's popcount.
+template <bool kRecord>
 __device__ __forceinline__ void eval_chunk(const ChunkSmem& w, int kc, bool act, float x, float y, float z,
                                            float tau2, float& y0, float& y1, float& y2, int& np,
-                                           uint32_t* masks, int lane) {
+                                           uint16_t* pkey, float* pe, int& pbase, int cap, int lane) {
+  const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll 2
   for (int k = 0; k < kc; ++k) {
     const Rec g = rec_from(w, k);
@@ -62,13 +68,69 @@ __device__ __forceinline__ void eval_chunk(const ChunkSmem& w, int kc, bool act,
     const float Q = quad_form(g, x, y, z, dx, dy, dz, tx, ty, tz);
     const bool in = act && Q <= tau2;
     const uint32_t m = __ballot_sync(0xffffffffu, in);
-    if (masks && lane == 0) masks[k] = m;
     if (m) {
       if (in) {
         const float e = ex2_approx(Q * kNegHalfLog2e);
         y0 = fmaf(g.v0, e, y0); y1 = fmaf(g.v1, e, y1); y2 = fmaf(g.v2, e, y2);
         ++np;
+        if (kRecord) {
+          const int pos = pbase + __popc(m & lt);
+          if (pos < cap) { pkey[pos] = (uint16_t)((k << 5) | lane); pe[pos] = e; }
+        }
       }
+      if (kRecord) pbase += __popc(m);
+    }
+  }
+  __syncwarp();
+}
+
+// Gradient terms of pairs [p0, p1) of the staged chunk (lane = pair): 12 coefficient
+// gradients (C5), a <= 2-level segmented shuffle scan over each Gaussian's run of pairs,
+// then red.global.add.v4.f32 from every 4th lane of a run counted from its end.
+__device__ __forceinline__ void chunk_pairs_bwd(const WarpSmem& w, int p0, int p1, float* __restrict__ grad,
+                                                int lane) {
+  for (int pb = p0; pb < p1; pb += 32) {
+    const int p = pb + lane;
+    const bool valid = p < p1;
+    int k = 32 + lane;                 // idle lanes form their own segments
+    float v[12];
+#pragma unroll
+    for (int q = 0; q < 12; ++q) v[q] = 0.f;
+    if (valid) {
+      const uint32_t key = w.pkey[p];
+      const float e = w.pe[p];
+      k = key >> 5;
+      const int s = key & 31;
+      const Rec g = rec_from(w, k);
+      const float4 sx = w.sxg[s];
+      const float2 sg = w.sg[s];
+      float dx, dy, dz, tx, ty, tz;
+      quad_form(g, sx.x, sx.y, sx.z, dx, dy, dz, tx, ty, tz);
+      const float he = (sx.w * g.v0 + sg.x * g.v1 + sg.y * g.v2) * e;
+      v[0] = he * tx; v[1] = he * ty; v[2] = he * tz;                 // d mu
+      const float kk = -0.5f * he;
+      const float kx = kk * dx, ky = kk * dy, kz = kk * dz;
+      v[3] = kx * dx; v[4] = ky * dy; v[5] = kz * dz;                 // dA00 dA11 dA22
+      v[6] = kx * dy; v[7] = kx * dz; v[8] = ky * dz;                 // dA01 dA02 dA12
+      v[9] = sx.w * e; v[10] = sg.x * e; v[11] = sg.y * e;            // d v
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, k);
+    const int head = __ffs(peers) - 1, tail = 31 - __clz(peers);
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      const bool need = lane - o >= head;
+      if (!__any_sync(0xffffffffu, need)) break;
+#pragma unroll
+      for (int q = 0; q < 12; ++q) {
+        const float t = __shfl_up_sync(0xffffffffu, v[q], o);
+        if (need) v[q] += t;
+      }
+    }
+    if (valid && ((tail - lane) & 3) == 0) {
+      float* gp = grad + 12 * (int64_t)w.gid[k];
+      red_add_v4(gp, v[0], v[1], v[2], v[3]);
+      red_add_v4(gp + 4, v[4], v[5], v[6], v[7]);
+      red_add_v4(gp + 8, v[8], v[9], v[10], v[11]);
     }
   }
   __syncwarp();
@@ -97,14 +159,17 @@ __global__ void __launch_bounds__(256, 3) k_fwdbwd(FitArgs a) {
       const float4 q = __ldcs(a.bin + 2 * (int64_t)(wi.start + lane) + 1);
       x = p.x; y = p.y; z = p.z; xr = p.w; xg = q.x; xb = q.y;
     }
-    // ---------------- pass 1
+    // ---------------- pass 1 (records the inside pairs while they fit)
     float y0 = 0.f, y1 = 0.f, y2 = 0.f;
-    int np = 0;
-    for (int cb = 0; cb < C; cb += 32) {
+    int np = 0, pbase = 0;
+    const bool chunks_fit = C <= 32 * kMaxChunks;
+    for (int cb = 0, c = 0; cb < C; cb += 32, ++c) {
       const int kc = min(32, C - cb);
       stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane);
-      eval_chunk(w, kc, act, x, y, z, tau2, y0, y1, y2, np, cb + 32 <= kMaskCap ? w.mask + cb : nullptr, lane);
+      eval_chunk<true>(w, kc, act, x, y, z, tau2, y0, y1, y2, np, w.pkey, w.pe, pbase, kPairCap, lane);
+      if (lane == 0 && c < kMaxChunks) w.cend[c] = (uint16_t)min(pbase, 0xFFFF);
     }
+    const bool recorded = chunks_fit && pbase <= kPairCap;
     // ---------------- Eq. 4 loss and dL/dyhat (unnormalised)
     float g0 = 0.f, g1 = 0.f, g2 = 0.f, ls = 0.f;
     if (act) {
@@ -128,80 +193,43 @@ __global__ void __launch_bounds__(256, 3) k_fwdbwd(FitArgs a) {
     if (lane == 0) s_loss[wid][wi.level] += (double)ls;
     pairs_acc += (unsigned)np;
     cand_acc += (unsigned long long)wi.count * (unsigned long long)C;
-    if (np == 0) { __syncwarp(); continue; }
     __syncwarp();
-    // ---------------- pass 2: contributing pairs, candidate-major
-    for (int cb = 0; cb < C; cb += 32) {
-      const int kc = min(32, C - cb);
-      if (C > 32) stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane);
-      uint32_t mk;
-      if (cb + 32 <= kMaskCap) {
-        mk = lane < kc ? w.mask[cb + lane] : 0u;
-      } else {                         // re-derive the ballots exactly as pass 1 did
-        float t0 = 0.f, t1 = 0.f, t2 = 0.f;
-        int tn = 0;
-        eval_chunk(w, kc, act, x, y, z, tau2, t0, t1, t2, tn, w.mask, lane);
-        mk = lane < kc ? w.mask[lane] : 0u;
+    if (np == 0) continue;
+    // ---------------- pass 2
+    if (recorded) {
+      int pstart = 0;
+      for (int cb = 0, c = 0; cb < C; cb += 32, ++c) {
+        const int pend = w.cend[c];
+        if (pend == pstart) continue;
+        if (C > 32) stage_chunk(w, a.csr_idx, a.rec, lo + cb, min(32, C - cb), lane);
+        chunk_pairs_bwd(w, pstart, pend, a.grad, lane);
+        pstart = pend;
       }
-      const int cnt = __popc(mk);
-      int off = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, off, o);
-        if (lane >= o) off += v;
-      }
-      const int total = __shfl_sync(0xffffffffu, off, 31);
-      if (total == 0) continue;
-      off -= cnt;
-      for (uint32_t b = mk; b; b &= b - 1) w.pairs[off++] = (uint16_t)((lane << 5) | (__ffs(b) - 1));
-      __syncwarp();
-      for (int p0 = 0; p0 < total; p0 += 32) {
-        const int p = p0 + lane;
-        const bool valid = p < total;
-        int k = 32 + lane;              // unique key for idle lanes: own segment
-        float v[12];
-#pragma unroll
-        for (int q = 0; q < 12; ++q) v[q] = 0.f;
-        if (valid) {
-          const uint32_t e16 = w.pairs[p];
-          k = e16 >> 5;
-          const int s = e16 & 31;
+    } else {
+      // rare dense case: re-derive each chunk's pairs exactly as pass 1 did, in batches
+      for (int cb = 0; cb < C; cb += 32) {
+        const int kc = min(32, C - cb);
+        stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane);
+        const uint32_t lt = (1u << lane) - 1u;
+        int pb = 0;
+        for (int k = 0; k < kc; ++k) {
           const Rec g = rec_from(w, k);
-          const float4 sx = w.sxg[s];
-          const float2 sg = w.sg[s];
           float dx, dy, dz, tx, ty, tz;
-          const float Q = quad_form(g, sx.x, sx.y, sx.z, dx, dy, dz, tx, ty, tz);
-          const float e = ex2_approx(Q * kNegHalfLog2e);
-          const float he = (sx.w * g.v0 + sg.x * g.v1 + sg.y * g.v2) * e;
-          v[0] = he * tx; v[1] = he * ty; v[2] = he * tz;                 // d mu
-          const float kk = -0.5f * he;
-          const float kx = kk * dx, ky = kk * dy, kz = kk * dz;
-          v[3] = kx * dx; v[4] = ky * dy; v[5] = kz * dz;                 // dA00 dA11 dA22
-          v[6] = kx * dy; v[7] = kx * dz; v[8] = ky * dz;                 // dA01 dA02 dA12
-          v[9] = sx.w * e; v[10] = sg.x * e; v[11] = sg.y * e;            // d v
-        }
-        const unsigned peers = __match_any_sync(0xffffffffu, k);
-        const int head = __ffs(peers) - 1, tail = 31 - __clz(peers);
-        // segmented inclusive scan (segments are contiguous: pairs are candidate-major);
-        // stops as soon as no segment is longer than the current stride
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const bool need = lane - o >= head;
-          if (!__any_sync(0xffffffffu, need)) break;
-#pragma unroll
-          for (int q = 0; q < 12; ++q) {
-            const float t = __shfl_up_sync(0xffffffffu, v[q], o);
-            if (need) v[q] += t;
+          const float Q = quad_form(g, x, y, z, dx, dy, dz, tx, ty, tz);
+          const bool in = act && Q <= tau2;
+          const uint32_t m = __ballot_sync(0xffffffffu, in);
+          if (!m) continue;
+          if (pb + 32 > kPairCap) { chunk_pairs_bwd(w, 0, pb, a.grad, lane); pb = 0; }
+          if (in) {
+            const int pos = pb + __popc(m & lt);
+            w.pkey[pos] = (uint16_t)((k << 5) | lane);
+            w.pe[pos] = ex2_approx(Q * kNegHalfLog2e);
           }
+          pb += __popc(m);
+          __syncwarp();
         }
-        if (valid && lane == tail) {
-          float* gp = a.grad + 12 * (int64_t)w.gid[k];
-          red_add_v4(gp, v[0], v[1], v[2], v[3]);
-          red_add_v4(gp + 4, v[4], v[5], v[6], v[7]);
-          red_add_v4(gp + 8, v[8], v[9], v[10], v[11]);
-        }
+        chunk_pairs_bwd(w, 0, pb, a.grad, lane);
       }
-      __syncwarp();
     }
   }
   if (lane == 0) { s_cnt[wid][0] = pairs_acc; s_cnt[wid][1] = cand_acc; }
@@ -239,11 +267,11 @@ __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
       x = p.x; y = p.y; z = p.z; idx = __float_as_uint(p.w);
     }
     float y0 = 0.f, y1 = 0.f, y2 = 0.f;
-    int np = 0;
+    int np = 0, pb = 0;
     for (int cb = 0; cb < C; cb += 32) {
       const int kc = min(32, C - cb);
       stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane);
-      eval_chunk(w, kc, act, x, y, z, tau2, y0, y1, y2, np, nullptr, lane);
+      eval_chunk<false>(w, kc, act, x, y, z, tau2, y0, y1, y2, np, nullptr, nullptr, pb, 0, lane);
     }
     if (act) {
       __stcs(a.out + 3 * (int64_t)idx, y0); __stcs(a.out + 3 * (int64_t)idx + 1, y1);

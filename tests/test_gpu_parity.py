@@ -365,3 +365,33 @@ def test_cuda_graph_replay_matches_eager(gsc):
         g.replay()
     torch.cuda.synchronize()
     np.testing.assert_allclose(rows(c2), rows(c1), rtol=1e-5, atol=1e-6)
+
+
+def test_gradient_parity_dense_no_cutoff(gsc):
+    """tau = INFINITY: every (sample, Gaussian) pair contributes, so the per-warp pair list
+    overflows and the kernel's re-derivation path runs; gradients must still match."""
+    pos, alb, ls = workload.cfg0_lattice()
+    hp = gsc.default_hparams(cutoff_sigma=float("inf"))
+    c = gsc.GSCache([64, 16], pos, alb, init_log_scale=ls, seed=1, hparams=hp)
+    r = np.random.default_rng(8)
+    P0 = c.params_rows(0)
+    P0[:, 3:7] = r.normal(size=(64, 4)).astype(np.float32)
+    P0[:, 10:13] += r.uniform(-0.3, 0.3, (64, 3)).astype(np.float32)
+    c.set_params_rows(0, P0)
+    P = rows(c)
+    c.debug_enable_grads(True)
+    x, _ = workload.cfg0_samples(3000)
+    ln = r.integers(1, 3, 3000).astype(np.int32)
+    rgb = r.uniform(0, 2, (3000, 3)).astype(np.float32)
+    st = c.fit(x, ln, rgb)
+    torch.cuda.synchronize()
+    g = np.concatenate([c.debug_grads_rows(l) for l in range(2)]).astype(np.float64)
+    ro = oracle.loss_grad(c.goff, P, x.astype(np.float64), ln, rgb.astype(np.float64), tau=np.inf)
+    assert st.n_pairs == ro["npairs"]
+    for l in range(2):
+        sl = slice(c.goff[l], c.goff[l + 1])
+        for name, cs in oracle.GROUP_SLICES.items():
+            a, b = g[sl, cs], ro["grad"][sl, cs]
+            if name == "rotation" and l > 0:
+                continue
+            assert np.linalg.norm(a - b) <= 1e-4 * np.linalg.norm(b), (l, name)
