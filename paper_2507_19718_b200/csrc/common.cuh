@@ -10,7 +10,7 @@ namespace gsc {
 
 constexpr int kMaxL = GC_MAX_LEVELS;
 constexpr int kNP = 14;              // raw floats per Gaussian
-constexpr int kCH = 32;              // samples per work item == one warp of the fwd/bwd kernels
+constexpr int kCH = 64;              // samples per work item: one warp, two samples per lane
 constexpr int kScanTile = 2048;      // 256 threads x 8 items
 constexpr uint32_t kInvalidKey = 0xFFFFFFFFu;
 
@@ -94,27 +94,8 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
                : "memory");
 }
 
-// Mahalanobis form Q = d^T A d of a packed symmetric A (A00,A11,A22,A01,A02,A12), with the
-// operation order fixed by explicit intrinsics so that every kernel takes the same cut-off
-// decision for the same pair.  Also returns t = A d.
-struct Rec {
-  float mx, my, mz, a00, a11, a22, a01, a02, a12, v0, v1, v2;
-};
-
-__device__ __forceinline__ float quad_form(const Rec& r, float x, float y, float z, float& dx,
-                                           float& dy, float& dz, float& tx, float& ty, float& tz) {
-  dx = __fsub_rn(x, r.mx);
-  dy = __fsub_rn(y, r.my);
-  dz = __fsub_rn(z, r.mz);
-  tx = __fmaf_rn(r.a02, dz, __fmaf_rn(r.a01, dy, __fmul_rn(r.a00, dx)));
-  ty = __fmaf_rn(r.a12, dz, __fmaf_rn(r.a11, dy, __fmul_rn(r.a01, dx)));
-  tz = __fmaf_rn(r.a22, dz, __fmaf_rn(r.a12, dy, __fmul_rn(r.a02, dx)));
-  return __fmaf_rn(dz, tz, __fmaf_rn(dy, ty, __fmul_rn(dx, tx)));
-}
-
-__device__ __forceinline__ Rec load_rec(const float4* rec, int64_t j) {
-  float4 p = __ldg(rec + 3 * j), q = __ldg(rec + 3 * j + 1), s = __ldg(rec + 3 * j + 2);
-  return Rec{p.x, p.y, p.z, p.w, q.x, q.y, q.z, q.w, s.x, s.y, s.z, s.w};
-}
+// Evaluation record (48 B, 3 x float4): the upper-triangular Cholesky factor U of
+// A = Sigma^-1 = U^T U (Q = |U (x - mu)|^2), the mean mu and the amplitude v = w max(0, c):
+//   r0 = (U00, U01, U02, U11)  r1 = (U12, U22, mu_x, mu_y)  r2 = (mu_z, v0, v1, v2)
 
 }  // namespace gsc

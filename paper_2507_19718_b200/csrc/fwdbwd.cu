@@ -1,18 +1,19 @@
 // fwdbwd.cu -- the fused forward + HDR loss + backward kernel of gc_fit (A4) and the
 // forward-only lookup kernel of gc_query (A7).  Warp-centric: no block barriers.
 //
-// A work item is <= 32 binned samples of one (level, cell) bin; one warp owns it.  The
-// cell's culling list (C8) is staged into the warp's shared memory 32 evaluation records
-// (48 B each) at a time.
-//   pass 1 (lane = sample): yhat = sum v_j e^{-Q/2} over the candidates with Q <= tau^2 (C3),
-//          with the warp ballot of every candidate kept as a 32-bit sample mask; the Eq. 4
-//          loss and g = dL/dyhat (C4, unnormalised -- the 1/(3 k_l) factor is applied by the
-//          optimizer once k_l is known globally, C9).
-//   pass 2 (lane = contributing pair): the masks are expanded into a candidate-major pair list;
-//          each lane evaluates the 12 coefficient-gradient terms of C5 for one pair, a
-//          segmented warp-shuffle scan merges the pairs of each Gaussian, and the segment's last
-//          lane issues 3 x red.global.add.v4.f32.  Work is proportional to contributing pairs,
-//          every lane busy; never shared-memory float atomics (a CAS loop on sm_100a).
+// A work item is <= 64 binned samples of one (level, cell) bin; one warp owns it, every lane
+// two samples (s = lane, lane + 32) so that each staged candidate feeds two evaluations.
+// The cell's culling list (C8) is staged into the warp's shared memory 32 candidates at a
+// time, recentred on the item's first sample.
+//   pass 1 (lane = sample pair): yhat = sum v_j e^{-Q/2} over the candidates with
+//          Q <= tau^2 (C3); every inside pair (candidate, sample, e) is appended to a
+//          candidate-major pair list (ballot + popc ranks); the Eq. 4 loss and g = dL/dyhat
+//          (C4, unnormalised -- the 1/(3 k_l) factor is applied by the optimizer once k_l is
+//          known globally, C9).
+//   pass 2 (lane = contributing pair): the 12 coefficient-gradient terms of C5 per pair, a
+//          <= 2-level segmented warp-shuffle scan over each Gaussian's run of pairs, and
+//          red.global.add.v4.f32 from every 4th lane of a run.  Work is proportional to the
+//          contributing pairs; never shared-memory float atomics (a CAS loop on sm_100a).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -20,65 +21,99 @@ namespace gsc {
 
 constexpr int kPart = kMaxL + 2;
 constexpr int kWarps = 8;                                 // warps per CTA
-constexpr int kPairCap = 512;                             // recorded (sample, Gaussian) pairs per warp
+constexpr int kPairCap = 768;                             // recorded (sample, Gaussian) pairs per warp
 constexpr int kMaxChunks = 64;                            // recorded chunks per work item (C <= 2048)
 constexpr float kNegHalfLog2e = -0.72134752044448170f;    // -0.5 * log2(e)
+static_assert(kCH == 64, "two samples per lane");
 
+// Staged candidate (64 B in shared memory), relative to the work item's reference point
+// x_ref (its first sample): c = U (mu - x_ref), so that for x' = x - x_ref
+//   w = U x' - c = U (x - mu),  Q = |w|^2   (9 FMA per pair; recentring keeps fp32 exact enough)
 struct ChunkSmem {
-  float4 r0[32], r1[32], r2[32];   // staged records of one 32-candidate chunk
-  int gid[32];
+  float4 r0[32];                   // U00 U01 U02 U11
+  float4 r1[32];                   // U12 U22 -c0 -c1
+  float4 r2[32];                   // -c2 v0 v1 v2
+  float4 r3[32];                   // mu - x_ref, gid (as bits)
 };
 
 struct WarpSmem : ChunkSmem {
-  float4 sxg[32];                  // sample x, y, z, g0
-  float2 sg[32];                   // sample g1, g2
-  uint16_t pkey[kPairCap];         // (candidate-in-chunk << 5) | sample, chunk- then candidate-major
+  float4 sxg[64];                  // sample x', y', z', g0
+  float2 sg[64];                   // sample g1, g2
+  uint16_t pkey[kPairCap];         // (candidate-in-chunk << 6) | sample, chunk- then candidate-major
   float pe[kPairCap];              // e = exp(-Q/2) of the pair, as pass 1 computed it
   uint16_t cend[kMaxChunks];       // end offset of every chunk's pairs
 };
 
-__device__ __forceinline__ Rec rec_from(const ChunkSmem& w, int k) {
+struct Cand { float u00, u01, u02, u11, u12, u22, nc0, nc1, nc2, v0, v1, v2; };
+
+__device__ __forceinline__ Cand cand_from(const ChunkSmem& w, int k) {
   const float4 p = w.r0[k], q = w.r1[k], r = w.r2[k];
-  return Rec{p.x, p.y, p.z, p.w, q.x, q.y, q.z, q.w, r.x, r.y, r.z, r.w};
+  return Cand{p.x, p.y, p.z, p.w, q.x, q.y, q.z, q.w, r.x, r.y, r.z, r.w};
+}
+
+// w = U x' - c and Q = |w|^2, with the operation order fixed (identical in every pass).
+__device__ __forceinline__ float cand_q(const Cand& g, float x, float y, float z, float& w0, float& w1, float& w2) {
+  w0 = __fmaf_rn(g.u02, z, __fmaf_rn(g.u01, y, __fmaf_rn(g.u00, x, g.nc0)));
+  w1 = __fmaf_rn(g.u12, z, __fmaf_rn(g.u11, y, g.nc1));
+  w2 = __fmaf_rn(g.u22, z, g.nc2);
+  return __fmaf_rn(w2, w2, __fmaf_rn(w1, w1, __fmul_rn(w0, w0)));
 }
 
 __device__ __forceinline__ void stage_chunk(ChunkSmem& w, const int32_t* __restrict__ csr_idx,
-                                            const float4* __restrict__ rec, int base, int kc, int lane) {
+                                            const float4* __restrict__ rec, int base, int kc, int lane,
+                                            float xr, float yr, float zr) {
   __syncwarp();
   if (lane < kc) {
     const int gid = __ldg(csr_idx + base + lane);
-    w.gid[lane] = gid;
-    w.r0[lane] = __ldg(rec + 3 * gid); w.r1[lane] = __ldg(rec + 3 * gid + 1); w.r2[lane] = __ldg(rec + 3 * gid + 2);
+    const float4 p = __ldg(rec + 3 * gid), q = __ldg(rec + 3 * gid + 1), r = __ldg(rec + 3 * gid + 2);
+    const float m0 = q.z - xr, m1 = q.w - yr, m2 = r.x - zr;
+    const float c0 = fmaf(p.z, m2, fmaf(p.y, m1, p.x * m0));
+    const float c1 = fmaf(q.x, m2, p.w * m1);
+    const float c2 = q.y * m2;
+    w.r0[lane] = p;
+    w.r1[lane] = make_float4(q.x, q.y, -c0, -c1);
+    w.r2[lane] = make_float4(-c2, r.y, r.z, r.w);
+    w.r3[lane] = make_float4(m0, m1, m2, __int_as_float(gid));
   }
   __syncwarp();
 }
 
-// Sample-parallel evaluation of one staged chunk (lane = sample).  Accumulates yhat and, if
-// `rec` is given, appends every inside pair (k, lane, e) at pbase + rank among the ballot
-// (candidate-major), up to `cap` entries; pbase advances by the ballot's popcount.
+// Two samples per lane (a = lane, b = lane + 32; inactive samples carry x' = NaN, never
+// inside).  Accumulates yhat and, if kRecord, appends every inside pair at pbase + its rank
+// (candidate-major; sample a's before sample b's), up to `cap`; pbase advances regardless.
 template <bool kRecord>
-__device__ __forceinline__ void eval_chunk(const ChunkSmem& w, int kc, bool act, float x, float y, float z,
-                                           float tau2, float& y0, float& y1, float& y2, int& np,
+__device__ __forceinline__ void eval_chunk(const ChunkSmem& w, int kc, const float (&xa)[3], const float (&xb)[3],
+                                           float tau2, float (&ya)[3], float (&yb)[3], int& np,
                                            uint16_t* pkey, float* pe, int& pbase, int cap, int lane) {
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll 2
   for (int k = 0; k < kc; ++k) {
-    const Rec g = rec_from(w, k);
-    float dx, dy, dz, tx, ty, tz;
-    const float Q = quad_form(g, x, y, z, dx, dy, dz, tx, ty, tz);
-    const bool in = act && Q <= tau2;
-    const uint32_t m = __ballot_sync(0xffffffffu, in);
-    if (m) {
-      if (in) {
-        const float e = ex2_approx(Q * kNegHalfLog2e);
-        y0 = fmaf(g.v0, e, y0); y1 = fmaf(g.v1, e, y1); y2 = fmaf(g.v2, e, y2);
+    const Cand g = cand_from(w, k);
+    float w0, w1, w2;
+    const float Qa = cand_q(g, xa[0], xa[1], xa[2], w0, w1, w2);
+    const float Qb = cand_q(g, xb[0], xb[1], xb[2], w0, w1, w2);
+    const bool ina = Qa <= tau2, inb = Qb <= tau2;
+    const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = __ballot_sync(0xffffffffu, inb);
+    if (ma | mb) {
+      if (ina) {
+        const float e = ex2_approx(Qa * kNegHalfLog2e);
+        ya[0] = fmaf(g.v0, e, ya[0]); ya[1] = fmaf(g.v1, e, ya[1]); ya[2] = fmaf(g.v2, e, ya[2]);
         ++np;
         if (kRecord) {
-          const int pos = pbase + __popc(m & lt);
-          if (pos < cap) { pkey[pos] = (uint16_t)((k << 5) | lane); pe[pos] = e; }
+          const int pos = pbase + __popc(ma & lt);
+          if (pos < cap) { pkey[pos] = (uint16_t)((k << 6) | lane); pe[pos] = e; }
         }
       }
-      if (kRecord) pbase += __popc(m);
+      if (inb) {
+        const float e = ex2_approx(Qb * kNegHalfLog2e);
+        yb[0] = fmaf(g.v0, e, yb[0]); yb[1] = fmaf(g.v1, e, yb[1]); yb[2] = fmaf(g.v2, e, yb[2]);
+        ++np;
+        if (kRecord) {
+          const int pos = pbase + __popc(ma) + __popc(mb & lt);
+          if (pos < cap) { pkey[pos] = (uint16_t)((k << 6) | (lane + 32)); pe[pos] = e; }
+        }
+      }
+      if (kRecord) pbase += __popc(ma) + __popc(mb);
     }
   }
   __syncwarp();
@@ -96,16 +131,23 @@ __device__ __forceinline__ void chunk_pairs_bwd(const WarpSmem& w, int p0, int p
     float v[12];
 #pragma unroll
     for (int q = 0; q < 12; ++q) v[q] = 0.f;
+    int gid = 0;
     if (valid) {
       const uint32_t key = w.pkey[p];
       const float e = w.pe[p];
-      k = key >> 5;
-      const int s = key & 31;
-      const Rec g = rec_from(w, k);
+      k = key >> 6;
+      const int s = key & 63;
+      const Cand g = cand_from(w, k);
+      const float4 mu = w.r3[k];
+      gid = __float_as_int(mu.w);
       const float4 sx = w.sxg[s];
       const float2 sg = w.sg[s];
-      float dx, dy, dz, tx, ty, tz;
-      quad_form(g, sx.x, sx.y, sx.z, dx, dy, dz, tx, ty, tz);
+      float w0, w1, w2;
+      cand_q(g, sx.x, sx.y, sx.z, w0, w1, w2);
+      const float tx = g.u00 * w0;                                   // t = A d = U^T w
+      const float ty = fmaf(g.u11, w1, g.u01 * w0);
+      const float tz = fmaf(g.u22, w2, fmaf(g.u12, w1, g.u02 * w0));
+      const float dx = sx.x - mu.x, dy = sx.y - mu.y, dz = sx.z - mu.z;
       const float he = (sx.w * g.v0 + sg.x * g.v1 + sg.y * g.v2) * e;
       v[0] = he * tx; v[1] = he * ty; v[2] = he * tz;                 // d mu
       const float kk = -0.5f * he;
@@ -127,7 +169,7 @@ __device__ __forceinline__ void chunk_pairs_bwd(const WarpSmem& w, int p0, int p
       }
     }
     if (valid && ((tail - lane) & 3) == 0) {
-      float* gp = grad + 12 * (int64_t)w.gid[k];
+      float* gp = grad + 12 * (int64_t)gid;
       red_add_v4(gp, v[0], v[1], v[2], v[3]);
       red_add_v4(gp + 4, v[4], v[5], v[6], v[7]);
       red_add_v4(gp + 8, v[8], v[9], v[10], v[11]);
@@ -136,8 +178,30 @@ __device__ __forceinline__ void chunk_pairs_bwd(const WarpSmem& w, int p0, int p
   __syncwarp();
 }
 
+__device__ __forceinline__ void load_pos(const float4* __restrict__ bin, int stride, int start, int count, int s,
+                                         float (&x)[3], float4& p) {
+  if (s < count) {
+    p = __ldcs(bin + stride * (int64_t)(start + s));
+    x[0] = p.x; x[1] = p.y; x[2] = p.z;
+  } else {
+    x[0] = x[1] = x[2] = __int_as_float(0x7fffffff);     // NaN: never inside
+    p = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+__device__ __forceinline__ void hdr_grad(int mode, float eps, const float (&y)[3], const float (&t)[3],
+                                         float (&g)[3], float& ls) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const float d = y[c] + eps, r = t[c] - y[c], i = 1.f / (d * d);
+    ls += r * r * i;
+    g[c] = mode == 0 ? -2.f * r * i : -2.f * r * (t[c] + eps) * i / d;
+  }
+}
+
 __global__ void __launch_bounds__(256, 3) k_fwdbwd(FitArgs a) {
-  __shared__ WarpSmem sm[kWarps];
+  extern __shared__ __align__(16) unsigned char dsm[];
+  WarpSmem* sm = reinterpret_cast<WarpSmem*>(dsm);
   __shared__ double s_loss[kWarps][kMaxL];
   __shared__ unsigned long long s_cnt[kWarps][2];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -152,39 +216,41 @@ __global__ void __launch_bounds__(256, 3) k_fwdbwd(FitArgs a) {
     const WorkItem wi = a.work[it];
     const int lo = (int)__ldg(a.csr_off + wi.cell);
     const int C = (int)__ldg(a.csr_off + wi.cell + 1) - lo;
-    const bool act = lane < wi.count;
-    float x = 0.f, y = 0.f, z = 0.f, xr = 0.f, xg = 0.f, xb = 0.f;
-    if (act) {
-      const float4 p = __ldcs(a.bin + 2 * (int64_t)(wi.start + lane));
+    float xa[3], xb[3], ta[3] = {0.f, 0.f, 0.f}, tb[3] = {0.f, 0.f, 0.f};
+    float4 pa, pb4;
+    load_pos(a.bin, 2, wi.start, wi.count, lane, xa, pa);
+    load_pos(a.bin, 2, wi.start, wi.count, lane + 32, xb, pb4);
+    if (lane < wi.count) {
       const float4 q = __ldcs(a.bin + 2 * (int64_t)(wi.start + lane) + 1);
-      x = p.x; y = p.y; z = p.z; xr = p.w; xg = q.x; xb = q.y;
+      ta[0] = pa.w; ta[1] = q.x; ta[2] = q.y;
     }
+    if (lane + 32 < wi.count) {
+      const float4 q = __ldcs(a.bin + 2 * (int64_t)(wi.start + lane + 32) + 1);
+      tb[0] = pb4.w; tb[1] = q.x; tb[2] = q.y;
+    }
+    const float xref = __shfl_sync(0xffffffffu, xa[0], 0), yref = __shfl_sync(0xffffffffu, xa[1], 0),
+                zref = __shfl_sync(0xffffffffu, xa[2], 0);
+    xa[0] -= xref; xa[1] -= yref; xa[2] -= zref;            // NaN stays NaN
+    xb[0] -= xref; xb[1] -= yref; xb[2] -= zref;
     // ---------------- pass 1 (records the inside pairs while they fit)
-    float y0 = 0.f, y1 = 0.f, y2 = 0.f;
+    float ya[3] = {0.f, 0.f, 0.f}, yb[3] = {0.f, 0.f, 0.f};
     int np = 0, pbase = 0;
     const bool chunks_fit = C <= 32 * kMaxChunks;
     for (int cb = 0, c = 0; cb < C; cb += 32, ++c) {
       const int kc = min(32, C - cb);
-      stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane);
-      eval_chunk<true>(w, kc, act, x, y, z, tau2, y0, y1, y2, np, w.pkey, w.pe, pbase, kPairCap, lane);
+      stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref);
+      eval_chunk<true>(w, kc, xa, xb, tau2, ya, yb, np, w.pkey, w.pe, pbase, kPairCap, lane);
       if (lane == 0 && c < kMaxChunks) w.cend[c] = (uint16_t)min(pbase, 0xFFFF);
     }
     const bool recorded = chunks_fit && pbase <= kPairCap;
     // ---------------- Eq. 4 loss and dL/dyhat (unnormalised)
-    float g0 = 0.f, g1 = 0.f, g2 = 0.f, ls = 0.f;
-    if (act) {
-      const float d0 = y0 + eps, d1 = y1 + eps, d2 = y2 + eps;
-      const float r0 = xr - y0, r1 = xg - y1, r2 = xb - y2;
-      const float i0 = 1.f / (d0 * d0), i1 = 1.f / (d1 * d1), i2 = 1.f / (d2 * d2);
-      ls = r0 * r0 * i0 + r1 * r1 * i1 + r2 * r2 * i2;
-      if (a.mode == 0) { g0 = -2.f * r0 * i0; g1 = -2.f * r1 * i1; g2 = -2.f * r2 * i2; }
-      else {
-        g0 = -2.f * r0 * (xr + eps) * i0 / d0; g1 = -2.f * r1 * (xg + eps) * i1 / d1;
-        g2 = -2.f * r2 * (xb + eps) * i2 / d2;
-      }
-    }
-    w.sxg[lane] = make_float4(x, y, z, g0);
-    w.sg[lane] = make_float2(g1, g2);
+    float ga[3] = {0.f, 0.f, 0.f}, gb[3] = {0.f, 0.f, 0.f}, ls = 0.f;
+    if (lane < wi.count) hdr_grad(a.mode, eps, ya, ta, ga, ls);
+    if (lane + 32 < wi.count) hdr_grad(a.mode, eps, yb, tb, gb, ls);
+    w.sxg[lane] = make_float4(xa[0], xa[1], xa[2], ga[0]);
+    w.sg[lane] = make_float2(ga[1], ga[2]);
+    w.sxg[lane + 32] = make_float4(xb[0], xb[1], xb[2], gb[0]);
+    w.sg[lane + 32] = make_float2(gb[1], gb[2]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       ls += __shfl_xor_sync(0xffffffffu, ls, o);
@@ -201,31 +267,37 @@ __global__ void __launch_bounds__(256, 3) k_fwdbwd(FitArgs a) {
       for (int cb = 0, c = 0; cb < C; cb += 32, ++c) {
         const int pend = w.cend[c];
         if (pend == pstart) continue;
-        if (C > 32) stage_chunk(w, a.csr_idx, a.rec, lo + cb, min(32, C - cb), lane);
+        if (C > 32) stage_chunk(w, a.csr_idx, a.rec, lo + cb, min(32, C - cb), lane, xref, yref, zref);
         chunk_pairs_bwd(w, pstart, pend, a.grad, lane);
         pstart = pend;
       }
     } else {
       // rare dense case: re-derive each chunk's pairs exactly as pass 1 did, in batches
+      const uint32_t lt = (1u << lane) - 1u;
       for (int cb = 0; cb < C; cb += 32) {
         const int kc = min(32, C - cb);
-        stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane);
-        const uint32_t lt = (1u << lane) - 1u;
+        stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref);
         int pb = 0;
         for (int k = 0; k < kc; ++k) {
-          const Rec g = rec_from(w, k);
-          float dx, dy, dz, tx, ty, tz;
-          const float Q = quad_form(g, x, y, z, dx, dy, dz, tx, ty, tz);
-          const bool in = act && Q <= tau2;
-          const uint32_t m = __ballot_sync(0xffffffffu, in);
-          if (!m) continue;
-          if (pb + 32 > kPairCap) { chunk_pairs_bwd(w, 0, pb, a.grad, lane); pb = 0; }
-          if (in) {
-            const int pos = pb + __popc(m & lt);
-            w.pkey[pos] = (uint16_t)((k << 5) | lane);
-            w.pe[pos] = ex2_approx(Q * kNegHalfLog2e);
+          const Cand g = cand_from(w, k);
+          float w0, w1, w2;
+          const float Qa = cand_q(g, xa[0], xa[1], xa[2], w0, w1, w2);
+          const float Qb = cand_q(g, xb[0], xb[1], xb[2], w0, w1, w2);
+          const bool ina = Qa <= tau2, inb = Qb <= tau2;
+          const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = __ballot_sync(0xffffffffu, inb);
+          if (!(ma | mb)) continue;
+          if (pb + 64 > kPairCap) { chunk_pairs_bwd(w, 0, pb, a.grad, lane); pb = 0; }
+          if (ina) {
+            const int pos = pb + __popc(ma & lt);
+            w.pkey[pos] = (uint16_t)((k << 6) | lane);
+            w.pe[pos] = ex2_approx(Qa * kNegHalfLog2e);
           }
-          pb += __popc(m);
+          if (inb) {
+            const int pos = pb + __popc(ma) + __popc(mb & lt);
+            w.pkey[pos] = (uint16_t)((k << 6) | (lane + 32));
+            w.pe[pos] = ex2_approx(Qb * kNegHalfLog2e);
+          }
+          pb += __popc(ma) + __popc(mb);
           __syncwarp();
         }
         chunk_pairs_bwd(w, 0, pb, a.grad, lane);
@@ -259,26 +331,33 @@ __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
     const WorkItem wi = a.work[it];
     const int lo = (int)__ldg(a.csr_off + wi.cell);
     const int C = (int)__ldg(a.csr_off + wi.cell + 1) - lo;
-    const bool act = lane < wi.count;
-    float x = 0.f, y = 0.f, z = 0.f;
-    uint32_t idx = 0;
-    if (act) {
-      const float4 p = __ldcs(a.bin + wi.start + lane);
-      x = p.x; y = p.y; z = p.z; idx = __float_as_uint(p.w);
-    }
-    float y0 = 0.f, y1 = 0.f, y2 = 0.f;
-    int np = 0, pb = 0;
+    float xa[3], xb[3];
+    float4 pa, pb4;
+    load_pos(a.bin, 1, wi.start, wi.count, lane, xa, pa);
+    load_pos(a.bin, 1, wi.start, wi.count, lane + 32, xb, pb4);
+    const float xref = __shfl_sync(0xffffffffu, xa[0], 0), yref = __shfl_sync(0xffffffffu, xa[1], 0),
+                zref = __shfl_sync(0xffffffffu, xa[2], 0);
+    xa[0] -= xref; xa[1] -= yref; xa[2] -= zref;
+    xb[0] -= xref; xb[1] -= yref; xb[2] -= zref;
+    float ya[3] = {0.f, 0.f, 0.f}, yb[3] = {0.f, 0.f, 0.f};
+    int np = 0, pbase = 0;
     for (int cb = 0; cb < C; cb += 32) {
       const int kc = min(32, C - cb);
-      stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane);
-      eval_chunk<false>(w, kc, act, x, y, z, tau2, y0, y1, y2, np, nullptr, nullptr, pb, 0, lane);
+      stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref);
+      eval_chunk<false>(w, kc, xa, xb, tau2, ya, yb, np, nullptr, nullptr, pbase, 0, lane);
     }
-    if (act) {
-      __stcs(a.out + 3 * (int64_t)idx, y0); __stcs(a.out + 3 * (int64_t)idx + 1, y1);
-      __stcs(a.out + 3 * (int64_t)idx + 2, y2);
+    if (lane < wi.count) {
+      const int64_t i = __float_as_uint(pa.w);
+      __stcs(a.out + 3 * i, ya[0]); __stcs(a.out + 3 * i + 1, ya[1]); __stcs(a.out + 3 * i + 2, ya[2]);
+    }
+    if (lane + 32 < wi.count) {
+      const int64_t i = __float_as_uint(pb4.w);
+      __stcs(a.out + 3 * i, yb[0]); __stcs(a.out + 3 * i + 1, yb[1]); __stcs(a.out + 3 * i + 2, yb[2]);
     }
   }
 }
+
+constexpr size_t kFwdBwdSmem = sizeof(WarpSmem) * kWarps;
 
 static int persistent_grid(const void* fn, size_t smem) {
   int dev = 0, sms = 148, per = 1;
@@ -288,12 +367,18 @@ static int persistent_grid(const void* fn, size_t smem) {
   return sms * std::max(per, 1);
 }
 
-int fwdbwd_grid() { static int g = persistent_grid((const void*)k_fwdbwd, 0); return g; }
+int fwdbwd_grid() {
+  static int g = [] {
+    cudaFuncSetAttribute(k_fwdbwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdBwdSmem);
+    return persistent_grid((const void*)k_fwdbwd, kFwdBwdSmem);
+  }();
+  return g;
+}
 int query_grid() { static int g = persistent_grid((const void*)k_query, 0); return g; }
 
 void launch_fwdbwd(const FitArgs& a, int grid, cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "fwdbwd", s);
-  k_fwdbwd<<<grid, 256, 0, s>>>(a);
+  k_fwdbwd<<<grid, 256, kFwdBwdSmem, s>>>(a);
 }
 
 void launch_query(const QueryArgs& a, int grid, cudaStream_t s, Profiler* prof) {

@@ -11,26 +11,32 @@ static __device__ const double kT8[8] = {
     0x1.6a09e667f3bcdp+0, 0x1.8ace5422aa0dcp+0, 0x1.ae89f995ad3aep+0, 0x1.d5818dcfba488p+0};
 constexpr double kK8 = 0x1.71547652b82fep+3;   // 8 log2(e)
 
-// Record of one Gaussian from its raw parameters (C1): mu, A = R diag(e^-2s) R^T, v = w max(0,c).
+// Record of one Gaussian from its raw parameters (C1): A = R diag(e^-2s) R^T is formed and
+// Cholesky-factored in fp64 (A = U^T U), stored in fp32 with mu and v = w max(0, c).
 __device__ __forceinline__ void make_record(const float p[kNP], float4 out[3]) {
-  float w = p[P_Q], x = p[P_Q + 1], y = p[P_Q + 2], z = p[P_Q + 3];
-  float n2 = w * w + x * x + y * y + z * z;
-  if (n2 < 1e-24f) { w = 1.f; x = y = z = 0.f; }
-  else { float inv = rsqrtf(n2); inv = inv * (1.5f - 0.5f * n2 * inv * inv); w *= inv; x *= inv; y *= inv; z *= inv; }
-  float R[3][3];
-  R[0][0] = 1.f - 2.f * (y * y + z * z); R[0][1] = 2.f * (x * y - w * z); R[0][2] = 2.f * (x * z + w * y);
-  R[1][0] = 2.f * (x * y + w * z); R[1][1] = 1.f - 2.f * (x * x + z * z); R[1][2] = 2.f * (y * z - w * x);
-  R[2][0] = 2.f * (x * z - w * y); R[2][1] = 2.f * (y * z + w * x); R[2][2] = 1.f - 2.f * (x * x + y * y);
-  float D0 = expf(-2.f * p[P_S]), D1 = expf(-2.f * p[P_S + 1]), D2 = expf(-2.f * p[P_S + 2]);
-  float A[3][3];
+  double w = p[P_Q], x = p[P_Q + 1], y = p[P_Q + 2], z = p[P_Q + 3];
+  const double n2 = w * w + x * x + y * y + z * z;
+  if (n2 < 1e-24) { w = 1.0; x = y = z = 0.0; }
+  else { const double n = sqrt(n2); w /= n; x /= n; y /= n; z /= n; }
+  double R[3][3];
+  R[0][0] = 1.0 - 2.0 * (y * y + z * z); R[0][1] = 2.0 * (x * y - w * z); R[0][2] = 2.0 * (x * z + w * y);
+  R[1][0] = 2.0 * (x * y + w * z); R[1][1] = 1.0 - 2.0 * (x * x + z * z); R[1][2] = 2.0 * (y * z - w * x);
+  R[2][0] = 2.0 * (x * z - w * y); R[2][1] = 2.0 * (y * z + w * x); R[2][2] = 1.0 - 2.0 * (x * x + y * y);
+  const double D0 = exp(-2.0 * (double)p[P_S]), D1 = exp(-2.0 * (double)p[P_S + 1]), D2 = exp(-2.0 * (double)p[P_S + 2]);
+  double A[3][3];
 #pragma unroll
   for (int a = 0; a < 3; ++a)
 #pragma unroll
     for (int b = a; b < 3; ++b) A[a][b] = R[a][0] * R[b][0] * D0 + R[a][1] * R[b][1] * D1 + R[a][2] * R[b][2] * D2;
-  float wo = 1.f / (1.f + expf(-p[P_O]));
-  out[0] = make_float4(p[P_MU], p[P_MU + 1], p[P_MU + 2], A[0][0]);
-  out[1] = make_float4(A[1][1], A[2][2], A[0][1], A[0][2]);
-  out[2] = make_float4(A[1][2], wo * fmaxf(p[P_C], 0.f), wo * fmaxf(p[P_C + 1], 0.f), wo * fmaxf(p[P_C + 2], 0.f));
+  const double U00 = sqrt(A[0][0]);
+  const double U01 = A[0][1] / U00, U02 = A[0][2] / U00;
+  const double U11 = sqrt(fmax(A[1][1] - U01 * U01, 1e-300));
+  const double U12 = (A[1][2] - U01 * U02) / U11;
+  const double U22 = sqrt(fmax(A[2][2] - U02 * U02 - U12 * U12, 1e-300));
+  const float wo = 1.f / (1.f + expf(-p[P_O]));
+  out[0] = make_float4((float)U00, (float)U01, (float)U02, (float)U11);
+  out[1] = make_float4((float)U12, (float)U22, p[P_MU], p[P_MU + 1]);
+  out[2] = make_float4(p[P_MU + 2], wo * fmaxf(p[P_C], 0.f), wo * fmaxf(p[P_C + 1], 0.f), wo * fmaxf(p[P_C + 2], 0.f));
 }
 
 // C8 cell range of one Gaussian, fp64 with explicitly rounded + - * / sqrt only.
