@@ -58,6 +58,19 @@ class gc_fit_stats(C.Structure):
                     loss=list(self.loss)[:L])
 
 
+def pinned_stats() -> "gc_fit_stats":
+    """A gc_fit_stats in page-locked host memory (the library then copies the statistics
+    with one cudaMemcpyAsync instead of a host callback); falls back to pageable memory."""
+    try:
+        import torch
+        buf = torch.empty(C.sizeof(gc_fit_stats), dtype=torch.uint8).pin_memory()
+        st = gc_fit_stats.from_address(buf.data_ptr())
+        st._buf = buf
+        return st
+    except Exception:
+        return gc_fit_stats()
+
+
 class gc_level_params(C.Structure):
     _fields_ = [("count", C.c_int64), ("position", C.c_void_p), ("rotation", C.c_void_p),
                 ("color", C.c_void_p), ("log_scale", C.c_void_p), ("opacity_logit", C.c_void_p)]
@@ -193,7 +206,7 @@ class GSCache:
         self.h = h
         self.device = device
         self.goff = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
-        self._stats = gc_fit_stats()
+        self._stats = pinned_stats()
 
     def __del__(self):
         h = getattr(self, "h", None)

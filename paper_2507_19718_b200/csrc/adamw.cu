@@ -9,38 +9,29 @@ namespace gsc {
 constexpr int kPart = kMaxL + 2;
 
 
-// One block: sums the fwd/bwd per-block partials, derives k_l from the binned cell offsets.
-__global__ void __launch_bounds__(256) k_stats(const double* __restrict__ partial, int nblocks,
-                                               const uint32_t* __restrict__ cell_start, LevelGeom g,
-                                               int64_t S, LvlStats* lvl) {
-  __shared__ double red[8];
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  for (int col = 0; col < kPart; ++col) {
-    double acc = 0.0;
-    for (int b = t; b < nblocks; b += 256) acc += partial[(int64_t)b * kPart + col];
+// One block, one warp per column: sums the fwd/bwd per-block partials; k_l from the binned
+// cell offsets at the level boundaries.
+__global__ void __launch_bounds__(kPart * 32) k_stats(const double* __restrict__ partial, int nblocks,
+                                                      const uint32_t* __restrict__ cell_start, LevelGeom g,
+                                                      int64_t S, LvlStats* lvl) {
+  const int lane = threadIdx.x & 31, col = threadIdx.x >> 5;
+  double acc = 0.0;
+  for (int b = lane; b < nblocks; b += 32) acc += __ldg(partial + (int64_t)b * kPart + col);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) red[warp] = acc;
-    __syncthreads();
-    if (t == 0) {
-      double s = 0.0;
-      for (int k = 0; k < 8; ++k) s += red[k];
-      if (col < kMaxL) lvl->loss_sum[col] = s;
-      else if (col == kMaxL) lvl->n_pairs = s;
-      else lvl->n_cand = s;
-    }
-    __syncthreads();
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) {
+    if (col < kMaxL) lvl->loss_sum[col] = acc;
+    else if (col == kMaxL) lvl->n_pairs = acc;
+    else lvl->n_cand = acc;
   }
-  if (t == 0) {
-    double tot = 0.0;
-    for (int l = 0; l < kMaxL; ++l) {
-      double c = 0.0;
-      if (l < g.L) c = (double)(cell_start[g.coff[l + 1]] - cell_start[g.coff[l]]);
-      lvl->count[l] = c;
-      tot += c;
-    }
-    lvl->n_valid = tot;
-    lvl->n_in = (double)S;
+  if (col == 0) {
+    double c = 0.0;
+    if (lane < g.L) c = (double)(cell_start[g.coff[lane + 1]] - cell_start[g.coff[lane]]);
+    if (lane < kMaxL) lvl->count[lane] = c;
+    double tot = c;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (lane == 0) { lvl->n_valid = tot; lvl->n_in = (double)S; }
   }
 }
 
@@ -195,7 +186,7 @@ __global__ void __launch_bounds__(256) k_adamw(int64_t G, float* __restrict__ P,
 void launch_stats(const double* partial, int nblocks, const uint32_t* cell_start,
                   const LevelGeom& g, int64_t S, LvlStats* lvl, cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "stats", s);
-  k_stats<<<1, 256, 0, s>>>(partial, nblocks, cell_start, g, S, lvl);
+  k_stats<<<1, kPart * 32, 0, s>>>(partial, nblocks, cell_start, g, S, lvl);
 }
 
 void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp, int L,

@@ -135,6 +135,7 @@ static gc_status ensure_scratch(gc_cache c, Scratch& sc, int64_t S, bool fit, cu
   CK(dalloc(&sc.key, cap)); CK(dalloc(&sc.rank, cap));
   CK(dalloc(&sc.bin, (fit ? 2 : 1) * cap));
   CK(dalloc(&sc.cell_count, c->NC)); CK(dalloc(&sc.cell_start, c->NC + 1));
+  CK(cudaMemset(sc.cell_count, 0, sizeof(uint32_t) * c->NC));   // kept zero by the scan
   CK(dalloc(&sc.tiles, ntiles)); CK(dalloc(&sc.totals, 4));
   CK(dalloc(&sc.work, work_cap));
   sc.cap = cap;
@@ -151,7 +152,6 @@ static gc_status ensure_staging(Scratch& sc, bool need_pos, bool need_len, bool 
 
 static gc_status rebuild_csr(gc_cache c, cudaStream_t s, bool recompute_records) {
   if (recompute_records) {
-    CK(cudaMemsetAsync(c->csr_count, 0, sizeof(uint32_t) * c->NC, s));
     launch_record_cull(c->G, c->P, (double)c->hp.cutoff_sigma, c->geom, c->rec, c->range, c->csr_count, s);
   }
   launch_scan(c->csr_count, c->NC, 0, c->csr_tiles, c->csr_totals, c->csr_off, c->csr_cursor, nullptr,
@@ -166,8 +166,18 @@ static void CUDART_CB stats_cb(void* arg) {
   memcpy(p->dst, p->src, sizeof(gc_fit_stats));
 }
 
+static bool is_pinned_host(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return a.type == cudaMemoryTypeHost;
+}
+
 static gc_status emit_stats(gc_cache c, gc_fit_stats* user, cudaStream_t s) {
   if (!user) return GC_OK;
+  if (is_pinned_host(user)) {          // page-locked: one async copy, no host callback
+    CK(cudaMemcpyAsync(user, c->dstats, sizeof(gc_fit_stats), cudaMemcpyDeviceToHost, s));
+    return GC_OK;
+  }
   CK(cudaMemcpyAsync(c->hstats, c->dstats, sizeof(gc_fit_stats), cudaMemcpyDeviceToHost, s));
   StatsPayload* p;
   if (capturing(s)) {
@@ -434,7 +444,6 @@ gc_status gc_fit(gc_cache c, const float* pos, const int32_t* path_len, const fl
     }
   }
   IngestBufs b{F.key, F.rank, F.cell_count, F.bin};
-  CK(cudaMemsetAsync(F.cell_count, 0, sizeof(uint32_t) * c->NC, s));
   if (S > 0) launch_keys(pos, path_len, rgb, -1, S, c->geom, b, s, &c->prof);
   launch_scan(F.cell_count, c->NC, kCH, F.tiles, F.totals, F.cell_start, nullptr, F.work, c->geom, s, &c->prof);
   if (S > 0) launch_scatter(pos, rgb, S, F.cell_start, b, s, &c->prof);
@@ -453,7 +462,6 @@ gc_status gc_fit(gc_cache c, const float* pos, const int32_t* path_len, const fl
     NK(ncclGroupEnd());
   }
   launch_step_scalars(c->lvl, c->st, c->hp, c->L, c->dstats, s);
-  CK(cudaMemsetAsync(c->csr_count, 0, sizeof(uint32_t) * c->NC, s));
   launch_adamw(c->G, c->P, c->M, c->V, c->grad, c->rec, c->range, c->csr_count, c->dbg_on ? c->dbg : nullptr,
                c->st, c->hp, c->geom, c->dstats, s, &c->prof);
   if (gc_status e = rebuild_csr(c, s, false)) return e;
@@ -484,7 +492,6 @@ gc_status gc_query(gc_cache c, const float* pos, const int32_t* path_len, int le
   }
   float* dout = hout ? Q.out : out_rgb;
   IngestBufs b{Q.key, Q.rank, Q.cell_count, Q.bin};
-  CK(cudaMemsetAsync(Q.cell_count, 0, sizeof(uint32_t) * c->NC, s));
   launch_keys_query(pos, path_len, path_len ? -1 : level, S, c->geom, b, dout, s, &c->prof);
   launch_scan(Q.cell_count, c->NC, kCH, Q.tiles, Q.totals, Q.cell_start, nullptr, Q.work, c->geom, s, &c->prof);
   launch_scatter(pos, nullptr, S, Q.cell_start, b, s, &c->prof);

@@ -89,57 +89,36 @@ __global__ void __launch_bounds__(256) k_scan_reduce(const uint32_t* __restrict_
   if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
 }
 
-// Single block: in-place exclusive scan of the tile sums; totals[0..1] = grand totals.
-__global__ void __launch_bounds__(1024) k_scan_tiles(uint2* tile_sums, int ntiles, uint32_t* totals) {
-  __shared__ uint2 carry_s;
-  __shared__ uint2 wsum[32];
-  if (threadIdx.x == 0) carry_s = make_uint2(0, 0);
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int b = 0; b < ntiles; b += 1024) {
-    int i = b + threadIdx.x;
-    uint2 v = i < ntiles ? tile_sums[i] : make_uint2(0, 0);
-    uint2 inc = v;
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t a = __shfl_up_sync(0xffffffffu, inc.x, o), c = __shfl_up_sync(0xffffffffu, inc.y, o);
-      if (lane >= o) { inc.x += a; inc.y += c; }
-    }
-    if (lane == 31) wsum[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-      uint2 w = wsum[lane], wi = w;
-      for (int o = 1; o < 32; o <<= 1) {
-        uint32_t a = __shfl_up_sync(0xffffffffu, wi.x, o), c = __shfl_up_sync(0xffffffffu, wi.y, o);
-        if (lane >= o) { wi.x += a; wi.y += c; }
-      }
-      wsum[lane] = make_uint2(wi.x - w.x, wi.y - w.y);
-    }
-    __syncthreads();
-    uint2 carry = carry_s;
-    uint2 ex = make_uint2(carry.x + wsum[warp].x + inc.x - v.x, carry.y + wsum[warp].y + inc.y - v.y);
-    if (i < ntiles) tile_sums[i] = ex;
-    __syncthreads();
-    if (threadIdx.x == 1023) carry_s = make_uint2(ex.x + v.x, ex.y + v.y);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) { totals[0] = carry_s.x; totals[1] = carry_s.y; }
-}
-
-// Down-sweep: exclusive offsets (and an optional copy used as atomic cursors); with ch > 0,
-// one WorkItem per chunk of <= ch samples of every non-empty cell.
-__global__ void __launch_bounds__(256) k_scan_down(const uint32_t* __restrict__ cnt, int64_t n, int ch,
-                                                   const uint2* __restrict__ tile_prefix,
-                                                   uint32_t* excl, uint32_t* excl_copy,
+// Down-sweep (reduce-then-scan without a middle pass): every tile sums the tile totals
+// before it itself, scans its 2048 counts, writes the exclusive offsets (and an optional
+// copy used as atomic cursors) and, with ch > 0, one WorkItem per chunk of <= ch samples of
+// every non-empty cell.  The counts are zeroed after reading (ready for the next call), and
+// the last tile publishes the grand totals.
+__global__ void __launch_bounds__(256) k_scan_down(uint32_t* __restrict__ cnt, int64_t n, int ch,
+                                                   const uint2* __restrict__ tile_sums, int ntiles,
+                                                   uint32_t* totals, uint32_t* excl, uint32_t* excl_copy,
                                                    WorkItem* work, LevelGeom g) {
+  uint2 pre = make_uint2(0, 0), dummy;
+  for (int j = threadIdx.x; j < (int)blockIdx.x; j += 256) {
+    const uint2 t = __ldg(tile_sums + j);
+    pre.x += t.x; pre.y += t.y;
+  }
+  block_excl_scan(pre, dummy);
+  const uint2 tp = dummy;
   int64_t base = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 8;
   uint32_t c[8];
   load8(cnt, n, base, c);
+  if (base + 8 <= n && ((base & 3) == 0)) {
+    *reinterpret_cast<uint4*>(cnt + base) = make_uint4(0, 0, 0, 0);
+    *reinterpret_cast<uint4*>(cnt + base + 4) = make_uint4(0, 0, 0, 0);
+  } else {
+    for (int k = 0; k < 8; ++k) if (base + k < n) cnt[base + k] = 0u;
+  }
   uint2 s = make_uint2(0, 0);
 #pragma unroll
   for (int k = 0; k < 8; ++k) { s.x += c[k]; if (ch) s.y += (c[k] + ch - 1) / ch; }
   uint2 total;
   uint2 ex = block_excl_scan(s, total);
-  uint2 tp = tile_prefix[blockIdx.x];
   uint32_t off = tp.x + ex.x, woff = tp.y + ex.y;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
@@ -156,9 +135,10 @@ __global__ void __launch_bounds__(256) k_scan_down(const uint32_t* __restrict__ 
     }
     if (i == n - 1) excl[n] = off;
   }
+  if (blockIdx.x == ntiles - 1 && threadIdx.x == 0) { totals[0] = tp.x + total.x; totals[1] = tp.y + total.y; }
 }
 
-void launch_scan(const uint32_t* cnt, int64_t n, int ch, uint2* tile_sums, uint32_t* totals,
+void launch_scan(uint32_t* cnt, int64_t n, int ch, uint2* tile_sums, uint32_t* totals,
                  uint32_t* excl, uint32_t* excl_copy, WorkItem* work, const LevelGeom& g,
                  cudaStream_t s, Profiler* prof) {
   int ntiles = (int)((n + kScanTile - 1) / kScanTile);
@@ -167,12 +147,8 @@ void launch_scan(const uint32_t* cnt, int64_t n, int ch, uint2* tile_sums, uint3
     k_scan_reduce<<<ntiles, 256, 0, s>>>(cnt, n, ch, tile_sums);
   }
   {
-    ProfScope ps(prof, "scan_tiles", s);
-    k_scan_tiles<<<1, 1024, 0, s>>>(tile_sums, ntiles, totals);
-  }
-  {
     ProfScope ps(prof, "scan_down", s);
-    k_scan_down<<<ntiles, 256, 0, s>>>(cnt, n, ch, tile_sums, excl, excl_copy, work, g);
+    k_scan_down<<<ntiles, 256, 0, s>>>(cnt, n, ch, tile_sums, ntiles, totals, excl, excl_copy, work, g);
   }
 }
 

@@ -58,7 +58,7 @@ struct ProfScope {
 };
 
 // cull_scan.cu
-void launch_scan(const uint32_t* cnt, int64_t n, int ch, uint2* tile_sums, uint32_t* totals,
+void launch_scan(uint32_t* cnt, int64_t n, int ch, uint2* tile_sums, uint32_t* totals,
                  uint32_t* excl, uint32_t* excl_copy, WorkItem* work, const LevelGeom& g,
                  cudaStream_t s, Profiler* prof);
 void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& g, float4* rec,
