@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(kPart * 32) k_stats(const double* __restrict__
   }
   if (col == 0) {
     double c = 0.0;
-    if (lane < g.L) c = (double)(cell_start[g.coff[lane + 1]] - cell_start[g.coff[lane]]);
+    if (lane < g.L) c = (double)(cell_start[g.coff[lane + 1] * kRep] - cell_start[g.coff[lane] * kRep]);
     if (lane < kMaxL) lvl->count[lane] = c;
     double tot = c;
 #pragma unroll
@@ -161,19 +161,23 @@ __global__ void __launch_bounds__(256) k_adamw(int64_t G, float* __restrict__ P,
       }
       if (act) {
         const float bc1 = st->bc1[l], bc2 = st->bc2[l];
+        float m[kNP], v[kNP];
+#pragma unroll
+        for (int k = 0; k < kNP; ++k) { m[k] = M[k * G + j]; v[k] = V[k * G + j]; }   // all loads in flight
 #pragma unroll
         for (int k = 0; k < kNP; ++k) {
           const float gk = raw[k];
-          if (!isfinite(gk)) { ++bad; continue; }
+          const bool ok = isfinite(gk);
+          bad += !ok;
           const int grp = group_of(k);
           const float eta = st->eta[grp];
-          float m = M[k * G + j], v = V[k * G + j];
-          float pk = p[k] * (1.f - eta * hp.wd[grp]);
-          m = hp.beta1 * m + (1.f - hp.beta1) * gk;
-          v = hp.beta2 * v + (1.f - hp.beta2) * gk * gk;
-          pk = pk - eta * (m / bc1) / (sqrtf(v / bc2) + hp.eps);
-          M[k * G + j] = m; V[k * G + j] = v; P[k * G + j] = pk; p[k] = pk;
+          const float mk = hp.beta1 * m[k] + (1.f - hp.beta1) * gk;
+          const float vk = hp.beta2 * v[k] + (1.f - hp.beta2) * gk * gk;
+          const float pk = p[k] * (1.f - eta * hp.wd[grp]) - eta * (mk / bc1) / (sqrtf(vk / bc2) + hp.eps);
+          if (ok) { m[k] = mk; v[k] = vk; p[k] = pk; }
         }
+#pragma unroll
+        for (int k = 0; k < kNP; ++k) { M[k * G + j] = m[k]; V[k * G + j] = v[k]; P[k * G + j] = p[k]; }
       }
     }
     record_and_count(j, p, hp.tau, g, rec, range, csr_count);

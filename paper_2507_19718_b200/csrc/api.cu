@@ -130,12 +130,13 @@ static gc_status ensure_scratch(gc_cache c, Scratch& sc, int64_t S, bool fit, cu
   CK(cudaDeviceSynchronize());
   sc.release();
   int64_t cap = std::max<int64_t>(S, 1024);
-  int64_t ntiles = (c->NC + kScanTile - 1) / kScanTile;
+  const int64_t nbins = c->NC * kRep;                 // replicated per-cell counters
+  int64_t ntiles = (nbins + kScanTile - 1) / kScanTile;
   int64_t work_cap = cap / kCH + std::min<int64_t>(cap, c->NC) + 2;
   CK(dalloc(&sc.key, cap)); CK(dalloc(&sc.rank, cap));
   CK(dalloc(&sc.bin, (fit ? 2 : 1) * cap));
-  CK(dalloc(&sc.cell_count, c->NC)); CK(dalloc(&sc.cell_start, c->NC + 1));
-  CK(cudaMemset(sc.cell_count, 0, sizeof(uint32_t) * c->NC));   // kept zero by the scan
+  CK(dalloc(&sc.cell_count, nbins)); CK(dalloc(&sc.cell_start, nbins + 1));
+  CK(cudaMemset(sc.cell_count, 0, sizeof(uint32_t) * nbins));   // kept zero by the scan
   CK(dalloc(&sc.tiles, ntiles)); CK(dalloc(&sc.totals, 4));
   CK(dalloc(&sc.work, work_cap));
   sc.cap = cap;
@@ -445,7 +446,7 @@ gc_status gc_fit(gc_cache c, const float* pos, const int32_t* path_len, const fl
   }
   IngestBufs b{F.key, F.rank, F.cell_count, F.bin};
   if (S > 0) launch_keys(pos, path_len, rgb, -1, S, c->geom, b, s, &c->prof);
-  launch_scan(F.cell_count, c->NC, kCH, F.tiles, F.totals, F.cell_start, nullptr, F.work, c->geom, s, &c->prof);
+  launch_scan(F.cell_count, c->NC * kRep, kCH, F.tiles, F.totals, F.cell_start, nullptr, F.work, c->geom, s, &c->prof);
   if (S > 0) launch_scatter(pos, rgb, S, F.cell_start, b, s, &c->prof);
   FitArgs fa;
   fa.work = F.work; fa.n_work = F.totals + 1; fa.csr_off = c->csr_off; fa.csr_idx = c->csr_idx; fa.rec = c->rec;
@@ -493,7 +494,7 @@ gc_status gc_query(gc_cache c, const float* pos, const int32_t* path_len, int le
   float* dout = hout ? Q.out : out_rgb;
   IngestBufs b{Q.key, Q.rank, Q.cell_count, Q.bin};
   launch_keys_query(pos, path_len, path_len ? -1 : level, S, c->geom, b, dout, s, &c->prof);
-  launch_scan(Q.cell_count, c->NC, kCH, Q.tiles, Q.totals, Q.cell_start, nullptr, Q.work, c->geom, s, &c->prof);
+  launch_scan(Q.cell_count, c->NC * kRep, kCH, Q.tiles, Q.totals, Q.cell_start, nullptr, Q.work, c->geom, s, &c->prof);
   launch_scatter(pos, nullptr, S, Q.cell_start, b, s, &c->prof);
   QueryArgs qa;
   qa.work = Q.work; qa.n_work = Q.totals + 1; qa.csr_off = c->csr_off; qa.csr_idx = c->csr_idx; qa.rec = c->rec;

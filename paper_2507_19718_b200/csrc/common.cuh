@@ -12,6 +12,7 @@ constexpr int kMaxL = GC_MAX_LEVELS;
 constexpr int kNP = 14;              // raw floats per Gaussian
 constexpr int kCH = 64;              // samples per work item: one warp, two samples per lane
 constexpr int kScanTile = 2048;      // 256 threads x 8 items
+constexpr int kRep = 8;              // replicated per-cell sample counters (hot-cell atomics / 8)
 constexpr uint32_t kInvalidKey = 0xFFFFFFFFu;
 
 // Plane index of raw parameter column k in the SoA parameter store (paper order).

@@ -77,13 +77,21 @@ __device__ __forceinline__ void load8(const uint32_t* cnt, int64_t n, int64_t ba
   }
 }
 
+// ch > 0: sample bins, whose counts come as kRep replicas per cell (one thread's 8 items =
+// one cell, so that work items of <= ch samples are cut per cell); ch == 0: plain counts.
+__device__ __forceinline__ uint2 sum8(const uint32_t c[8], int ch) {
+  uint2 s = make_uint2(0, 0);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s.x += c[k];
+  if (ch) s.y = (s.x + ch - 1) / ch;
+  return s;
+}
+
 __global__ void __launch_bounds__(256) k_scan_reduce(const uint32_t* __restrict__ cnt, int64_t n, int ch, uint2* tile_sums) {
   int64_t base = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 8;
   uint32_t c[8];
   load8(cnt, n, base, c);
-  uint2 s = make_uint2(0, 0);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) { s.x += c[k]; if (ch) s.y += (c[k] + ch - 1) / ch; }
+  const uint2 s = sum8(c, ch);
   uint2 total;
   block_excl_scan(s, total);
   if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
@@ -114,23 +122,22 @@ __global__ void __launch_bounds__(256) k_scan_down(uint32_t* __restrict__ cnt, i
   } else {
     for (int k = 0; k < 8; ++k) if (base + k < n) cnt[base + k] = 0u;
   }
-  uint2 s = make_uint2(0, 0);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) { s.x += c[k]; if (ch) s.y += (c[k] + ch - 1) / ch; }
+  const uint2 s = sum8(c, ch);
   uint2 total;
   uint2 ex = block_excl_scan(s, total);
   uint32_t off = tp.x + ex.x, woff = tp.y + ex.y;
+  if (ch && s.x) {                       // one cell per thread (kRep replicas)
+    const int64_t cell = base / kRep;
+    const int lvl = level_of_cell(g, cell);
+    for (uint32_t q = 0; q * ch < s.x; ++q)
+      work[woff++] = WorkItem{(int)cell, (int)(off + q * ch), (int)min((uint32_t)ch, s.x - q * ch), lvl};
+  }
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     int64_t i = base + k;
     if (i < n) {
       excl[i] = off;
       if (excl_copy) excl_copy[i] = off;
-      if (ch && c[k]) {
-        int lvl = level_of_cell(g, i);
-        for (uint32_t q = 0; q * ch < c[k]; ++q)
-          work[woff++] = WorkItem{(int)i, (int)(off + q * ch), (int)min((uint32_t)ch, c[k] - q * ch), lvl};
-      }
       off += c[k];
     }
     if (i == n - 1) excl[n] = off;

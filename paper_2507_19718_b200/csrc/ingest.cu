@@ -8,7 +8,7 @@
 
 namespace gsc {
 
-constexpr int kU = 4;   // samples per thread per iteration
+constexpr int kU = 8;   // samples per thread per iteration
 
 __global__ void __launch_bounds__(256) k_keys(const float* __restrict__ pos, const int32_t* __restrict__ len,
                                               const float* __restrict__ rgb, int level_fixed, int64_t S,
@@ -41,18 +41,25 @@ __global__ void __launch_bounds__(256) k_keys(const float* __restrict__ pos, con
       key[u] = ok ? (uint32_t)sample_cell(g, l, x[u], y[u], z[u]) : kInvalidKey;
       if (!ok && out_zero && i < S) { out_zero[3 * i] = 0.f; out_zero[3 * i + 1] = 0.f; out_zero[3 * i + 2] = 0.f; }
     }
+    // all kU warp-aggregated atomics are issued before any result is consumed; counter
+    // replica r = (i >> 5) % kRep spreads a hot cell's arrivals over kRep addresses (the
+    // same-address L2 atomic rate, ~55 M/s, otherwise serialises a 4k-sample cell for 70 us)
+    unsigned peers[kU];
+    uint32_t base[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) peers[u] = __match_any_sync(0xffffffffu, key[u]);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      base[u] = 0;
+      const uint32_t r = (uint32_t)(((i0 + u * 32) >> 5) & (kRep - 1));
+      if (key[u] != kInvalidKey && lane == __ffs(peers[u]) - 1)
+        base[u] = atomicAdd(b.cell_count + (size_t)key[u] * kRep + r, (uint32_t)__popc(peers[u]));
+    }
     uint32_t rank[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const unsigned peers = __match_any_sync(0xffffffffu, key[u]);
-      rank[u] = 0;
-      if (key[u] != kInvalidKey) {
-        const int leader = __ffs(peers) - 1;
-        uint32_t base = 0;
-        if (lane == leader) base = atomicAdd(b.cell_count + key[u], (uint32_t)__popc(peers));
-        base = __shfl_sync(peers, base, leader);
-        rank[u] = base + __popc(peers & ((1u << lane) - 1u));
-      }
+      const uint32_t bb = __shfl_sync(0xffffffffu, base[u], __ffs(peers[u]) - 1);
+      rank[u] = key[u] != kInvalidKey ? bb + __popc(peers[u] & ((1u << lane) - 1u)) : 0u;
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
@@ -75,7 +82,10 @@ __global__ void __launch_bounds__(256) k_scatter(const float* __restrict__ pos, 
       rank[u] = i < S ? __ldcs(b.rank + i) : 0u;
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) d[u] = key[u] != kInvalidKey ? __ldg(cell_start + key[u]) + rank[u] : 0u;
+    for (int u = 0; u < kU; ++u)
+      d[u] = key[u] != kInvalidKey
+                 ? __ldg(cell_start + (size_t)key[u] * kRep + (((i0 + u * 32) >> 5) & (kRep - 1))) + rank[u]
+                 : 0u;
     float v[kU][6];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {

@@ -22,7 +22,7 @@ __device__ __forceinline__ void make_record(const float p[kNP], float4 out[3]) {
   R[0][0] = 1.0 - 2.0 * (y * y + z * z); R[0][1] = 2.0 * (x * y - w * z); R[0][2] = 2.0 * (x * z + w * y);
   R[1][0] = 2.0 * (x * y + w * z); R[1][1] = 1.0 - 2.0 * (x * x + z * z); R[1][2] = 2.0 * (y * z - w * x);
   R[2][0] = 2.0 * (x * z - w * y); R[2][1] = 2.0 * (y * z + w * x); R[2][2] = 1.0 - 2.0 * (x * x + y * y);
-  const double D0 = exp(-2.0 * (double)p[P_S]), D1 = exp(-2.0 * (double)p[P_S + 1]), D2 = exp(-2.0 * (double)p[P_S + 2]);
+  const double D0 = expf(-2.f * p[P_S]), D1 = expf(-2.f * p[P_S + 1]), D2 = expf(-2.f * p[P_S + 2]);
   double A[3][3];
 #pragma unroll
   for (int a = 0; a < 3; ++a)
