@@ -110,7 +110,8 @@ gc_status gc_reserve(gc_cache c, int64_t S_fit, int64_t S_query);
  *  averaged per level over 3 k_l (C4), back-propagates into all 14 raw parameters (C5) and
  *  takes one AdamW step with eta_g(t) (C6).  A level with k_l = 0 skips its step; a batch
  *  with no valid sample is a no-op (t not advanced).  stats (host, nullable) is filled when
- *  the stream reaches the end of this call's work. */
+ *  the stream reaches the end of this call's work: page-locked memory receives one
+ *  cudaMemcpyAsync, pageable memory a copy made by a stream host callback. */
 gc_status gc_fit(gc_cache c, const float* pos, const int32_t* path_len, const float* rgb,
                  int64_t S, gc_stream stream, gc_fit_stats* stats);
 
@@ -143,7 +144,9 @@ gc_status gc_info(gc_cache c, int* levels, int64_t* counts);
  * with its own shard; one NCCL all-reduce (sum) of the per-level coefficient gradients and
  * level statistics per step makes every replica take the identical AdamW step.
  * nccl_uid: 128-byte ncclUniqueId produced by rank 0 (gc_nccl_unique_id) and broadcast by
- * the caller.  mode: 0 = data parallel.  world == 1 detaches. */
+ * the caller.  mode: 0 = data parallel (1 = level-sharded: GC_ERR_UNSUPPORTED for now).
+ * nccl_uid == NULL with world == 1 detaches; a uid with world == 1 builds a one-rank
+ * communicator (the all-reduce then runs as an identity, used to test the path). */
 gc_status gc_nccl_unique_id(void* uid128);
 gc_status gc_set_comm(gc_cache c, const void* nccl_uid, int rank, int world, int mode);
 

@@ -456,7 +456,7 @@ gc_status gc_fit(gc_cache c, const float* pos, const int32_t* path_len, const fl
   fa.tau2 = tau * tau; fa.hdr_eps = c->hp.hdr_eps; fa.mode = c->hp.loss_grad_mode; fa.L = c->L;
   launch_fwdbwd(fa, c->fb_grid, s, &c->prof);
   launch_stats(c->partial, c->fb_grid, F.cell_start, c->geom, S, c->lvl, s, &c->prof);
-  if (c->comm && c->world > 1) {   // data parallel: one sum over ranks of grads + level stats
+  if (c->comm) {                   // data parallel: one sum over ranks of grads + level stats
     NK(ncclGroupStart());
     NK(ncclAllReduce(c->grad, c->grad, (size_t)12 * c->G, ncclFloat32, ncclSum, c->comm, s));
     NK(ncclAllReduce(c->lvl, c->lvl, sizeof(LvlStats) / sizeof(double), ncclFloat64, ncclSum, c->comm, s));
@@ -592,8 +592,10 @@ gc_status gc_set_comm(gc_cache c, const void* nccl_uid, int rank, int world, int
   CK(cudaDeviceSynchronize());
   if (c->comm) { ncclCommDestroy(c->comm); c->comm = nullptr; }
   c->rank = rank; c->world = world;
-  if (world == 1) return GC_OK;
-  if (!nccl_uid) return fail(GC_ERR_ARG, "NULL nccl_uid");
+  if (!nccl_uid) {
+    if (world == 1) return GC_OK;     // detach
+    return fail(GC_ERR_ARG, "NULL nccl_uid");
+  }
   ncclUniqueId id;
   memcpy(&id, nccl_uid, sizeof id);
   NK(ncclCommInitRank(&c->comm, world, id, rank));

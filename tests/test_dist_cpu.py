@@ -1,0 +1,119 @@
+"""Data-parallel semantics on CPU with torch.distributed gloo, world_size 2 (no GPU).
+
+C9: the P-rank step equals the 1-rank step on the concatenated batch because the
+library sums the UNNORMALISED per-level coefficient gradients and the level counts over the
+ranks and normalises by the global 3 k_l afterwards.  Here each rank computes its shard's
+contribution with the fp64 oracle, the ranks all-reduce over gloo exactly what the library
+all-reduces over NCCL, and the result must equal the oracle on the whole batch.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import workload
+from paper_2507_19718_b200.dist import shard_range
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _problem():
+    r = np.random.default_rng(21)
+    G = (40, 12)
+    P = np.zeros((sum(G), 14))
+    P[:, 0:3] = r.uniform(-0.6, 0.6, (sum(G), 3))
+    P[:, 3:7] = r.normal(size=(sum(G), 4))
+    P[:, 7:10] = r.uniform(0.3, 2, (sum(G), 3))
+    P[:, 10:13] = np.log(r.uniform(0.1, 0.3, (sum(G), 3)))
+    P[:, 13] = r.uniform(-1, 1, sum(G))
+    x = r.uniform(-0.7, 0.7, (3001, 3))
+    ln = r.integers(0, 4, 3001).astype(np.int32)
+    rgb = r.uniform(0, 3, (3001, 3))
+    return [0, G[0], G[0] + G[1]], P, x, ln, rgb
+
+
+def _worker(rank, world, port, out):
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    goff, P, x, ln, rgb = _problem()
+    lo, hi = shard_range(len(x), rank, world)
+    res = oracle.loss_grad(goff, P, x[lo:hi], ln[lo:hi], rgb[lo:hi], mode=1)
+    k = res["count"].astype(np.float64)
+    # unnormalise (the library never normalises before the all-reduce)
+    g = res["grad"].copy()
+    for l in range(2):
+        g[goff[l]:goff[l + 1]] *= 3 * k[l]
+    ls = res["loss"] * 3 * k
+    buf = torch.from_numpy(np.concatenate([g.ravel(), ls, k]))
+    dist.all_reduce(buf)                      # what gc_fit all-reduces over NCCL
+    b = buf.numpy()
+    G = len(P)
+    gsum, lsum, ksum = b[:G * 14].reshape(G, 14), b[G * 14:G * 14 + 2], b[G * 14 + 2:]
+    for l in range(2):
+        gsum[goff[l]:goff[l + 1]] /= 3 * ksum[l]
+    out[rank] = (gsum, lsum / (3 * ksum), ksum)
+    dist.destroy_process_group()
+
+
+def test_dp_decomposition_equals_single_rank_gloo():
+    world = 2
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.start_processes(_worker, args=(world, port, out), nprocs=world, join=True,
+                           start_method="fork")
+        res = dict(out)
+    goff, P, x, ln, rgb = _problem()
+    full = oracle.loss_grad(goff, P, x, ln, rgb, mode=1)
+    for r in range(world):
+        g, loss, k = res[r]
+        np.testing.assert_array_equal(k, full["count"])
+        np.testing.assert_allclose(loss, full["loss"], rtol=1e-12)
+        np.testing.assert_allclose(g, full["grad"], rtol=1e-10, atol=1e-14)
+    np.testing.assert_array_equal(res[0][0], res[1][0])    # replicas stay identical
+
+
+def test_shard_range_covers_exactly():
+    for n in (0, 1, 7, 1000, 2_073_600):
+        for world in (1, 2, 3, 8):
+            spans = [shard_range(n, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+            sizes = [b - a for a, b in spans]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def _uid_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2507_19718_b200.dist import exchange_unique_id
+    out[rank] = exchange_unique_id()
+    dist.destroy_process_group()
+
+
+def test_nccl_unique_id_exchange_over_gloo():
+    """The communicator bootstrap: rank 0's ncclUniqueId reaches every rank unchanged."""
+    from paper_2507_19718_b200 import build
+    build.build()
+    world = 2
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        try:
+            mp.start_processes(_uid_worker, args=(world, port, out), nprocs=world, join=True,
+                               start_method="fork")
+        except Exception as e:  # ncclGetUniqueId needs a network interface; report, don't hide
+            pytest.skip(f"ncclGetUniqueId unavailable here: {e}")
+        res = dict(out)
+    assert len(res[0]) == 128 and res[0] == res[1] and any(res[0])

@@ -395,3 +395,20 @@ def test_gradient_parity_dense_no_cutoff(gsc):
             if name == "rotation" and l > 0:
                 continue
             assert np.linalg.norm(a - b) <= 1e-4 * np.linalg.norm(b), (l, name)
+
+
+def test_data_parallel_one_rank_nccl_path_is_identity(gsc):
+    """The DP path (NCCL all-reduce of gradients + level stats inside gc_fit) on a one-rank
+    communicator must reproduce the plain path bit for bit (sum over one rank)."""
+    c1, _, _ = make_cfg1(gsc)
+    c2, _, _ = make_cfg1(gsc)
+    c2.set_comm(gsc.nccl_unique_id(), 0, 1)
+    for f in range(3):
+        x, ln, rgb = workload.fit_batch(1, frame=f, S=50_000)
+        s1 = c1.fit(cuda(x), cuda(ln), cuda(rgb))
+        torch.cuda.synchronize()
+        l1 = list(s1.loss[:3])
+        s2 = c2.fit(cuda(x), cuda(ln), cuda(rgb))
+        torch.cuda.synchronize()
+        assert list(s2.loss[:3]) == l1
+    np.testing.assert_array_equal(rows(c1), rows(c2))
