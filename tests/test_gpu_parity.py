@@ -399,7 +399,8 @@ def test_gradient_parity_dense_no_cutoff(gsc):
 
 def test_data_parallel_one_rank_nccl_path_is_identity(gsc):
     """The DP path (NCCL all-reduce of gradients + level stats inside gc_fit) on a one-rank
-    communicator must reproduce the plain path bit for bit (sum over one rank)."""
+    communicator must reproduce the plain path (sum over one rank; float atomics make the
+    gradient summation order, hence the last bits, run-dependent)."""
     c1, _, _ = make_cfg1(gsc)
     c2, _, _ = make_cfg1(gsc)
     c2.set_comm(gsc.nccl_unique_id(), 0, 1)
@@ -410,5 +411,5 @@ def test_data_parallel_one_rank_nccl_path_is_identity(gsc):
         l1 = list(s1.loss[:3])
         s2 = c2.fit(cuda(x), cuda(ln), cuda(rgb))
         torch.cuda.synchronize()
-        assert list(s2.loss[:3]) == l1
-    np.testing.assert_array_equal(rows(c1), rows(c2))
+        np.testing.assert_allclose(list(s2.loss[:3]), l1, rtol=1e-6)
+    np.testing.assert_allclose(rows(c1), rows(c2), rtol=1e-5, atol=1e-6)
