@@ -171,24 +171,35 @@ def sample_cell(x, origin, inv_cell, dims):
 
 
 def cull_ranges(P, tau, origin, inv_cell, dims):
+    """C8: per-Gaussian inclusive cell ranges [G][6] and bounding-sphere radii^2 [G]."""
     P = _d(P).reshape(-1, NP)
     o, ic, dm = _d(origin), _d(inv_cell), _i32(dims)
     rng = np.empty((len(P), 6), np.int32)
+    r2 = np.empty(len(P), np.float64)
     lib().orc_cull_ranges(C.c_int64(len(P)), _p(P, np.float64), C.c_double(tau), _p(o, np.float64),
-                          _p(ic, np.float64), _p(dm, np.int32), _p(rng, np.int32))
-    return rng
+                          _p(ic, np.float64), _p(dm, np.int32), _p(rng, np.int32), _p(r2, np.float64))
+    return rng, r2
 
 
-def build_csr(rng, dims):
-    rng, dm = _i32(rng).reshape(-1, 6), _i32(dims)
+def build_csr(P, rng, r2, origin, inv_cell, dims):
+    """C8 culling lists (cell -> ascending level-local Gaussian indices)."""
+    P, rng, r2 = _d(P).reshape(-1, NP), _i32(rng).reshape(-1, 6), _d(r2)
+    o, ic, dm = _d(origin), _d(inv_cell), _i32(dims)
     cells = int(dm[0]) * int(dm[1]) * int(dm[2])
     off = np.empty(cells + 1, np.int64)
-    n = lib().orc_build_csr(C.c_int64(len(rng)), _p(rng, np.int32), _p(dm, np.int32),
-                            _p(off, np.int64), None)
+    args = (C.c_int64(len(rng)), _p(P, np.float64), _p(rng, np.int32), _p(r2, np.float64),
+            _p(o, np.float64), _p(ic, np.float64), _p(dm, np.int32), _p(off, np.int64))
+    n = lib().orc_build_csr(*args, None)
     idx = np.empty(max(n, 1), np.int32)
-    lib().orc_build_csr(C.c_int64(len(rng)), _p(rng, np.int32), _p(dm, np.int32),
-                        _p(off, np.int64), _p(idx, np.int32))
+    lib().orc_build_csr(*args, _p(idx, np.int32))
     return off, idx[:n]
+
+
+def csr_for(P, tau, grid):
+    """Convenience: the C8 lists of one level for grid = (origin, inv_cell, dims)."""
+    o, ic, d = grid
+    rng, r2 = cull_ranges(P, tau, o, ic, d)
+    return build_csr(P, rng, r2, o, ic, d)
 
 
 def _grids(grids, L):

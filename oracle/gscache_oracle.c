@@ -275,11 +275,17 @@ void orc_q_matrix(int64_t G, const double* P, int64_t S, const double* x, double
 
 /* ------------------------------------------------ exact conservative culling (C8) */
 
-/* Upper bounds of 2^(r/8), r = 0..7: the smallest doubles >= 2^(r/8). */
-static const double orc_T8[8] = {
-  0x1.0000000000000p+0, 0x1.172b83c7d517bp+0, 0x1.306fe0a31b716p+0, 0x1.4bfdad5362a28p+0,
-  0x1.6a09e667f3bcdp+0, 0x1.8ace5422aa0dcp+0, 0x1.ae89f995ad3aep+0, 0x1.d5818dcfba488p+0};
-static const double orc_K8 = 0x1.71547652b82fep+3; /* 8*log2(e) */
+/* Upper bounds of 2^(r/32), r = 0..31: the smallest doubles >= 2^(r/32) (C8). */
+static const double orc_T32[32] = {
+  0x1.0000000000000p+0, 0x1.059b0d3158575p+0, 0x1.0b5586cf98910p+0, 0x1.11301d0125b51p+0,
+  0x1.172b83c7d517bp+0, 0x1.1d4873168b9abp+0, 0x1.2387a6e756239p+0, 0x1.29e9df51fdee2p+0,
+  0x1.306fe0a31b716p+0, 0x1.371a7373aa9cbp+0, 0x1.3dea64c123423p+0, 0x1.44e086061892ep+0,
+  0x1.4bfdad5362a28p+0, 0x1.5342b569d4f82p+0, 0x1.5ab07dd48542ap+0, 0x1.6247eb03a5585p+0,
+  0x1.6a09e667f3bcdp+0, 0x1.71f75e8ec5f74p+0, 0x1.7a11473eb0187p+0, 0x1.82589994cce13p+0,
+  0x1.8ace5422aa0dcp+0, 0x1.93737b0cdc5e5p+0, 0x1.9c49182a3f091p+0, 0x1.a5503b23e255dp+0,
+  0x1.ae89f995ad3aep+0, 0x1.b7f76f2fb5e47p+0, 0x1.c199bdd85529dp+0, 0x1.cb720dcef906ap+0,
+  0x1.d5818dcfba488p+0, 0x1.dfc97337b9b5fp+0, 0x1.ea4afa2a490dap+0, 0x1.f50765b6e4541p+0};
+static const double orc_K32 = 0x1.71547652b82fep+5; /* 32*log2(e) */
 
 static int32_t orc_clampcell(double f, int32_t dim) {
   if (!(f >= 0.0)) return 0;                 /* also catches -inf */
@@ -293,62 +299,96 @@ void orc_sample_cell(const double* x, const double* origin, const double* inv_ce
   for (int a = 0; a < 3; ++a) c3[a] = orc_clampcell(floor((x[a] - origin[a]) * inv_cell[a]), dims[a]);
 }
 
-/* Per-Gaussian inclusive cell range [lo, hi] per axis.  Only + - * / sqrt floor ceil ldexp. */
+/* C8 per Gaussian: inclusive cell range [lo, hi] per axis (the AABB of the tau-ellipsoid
+ * bounded with U_b >= e^{s_b}) and r2 = tau^2 max_b U_b^2, the squared radius of a sphere
+ * containing the ellipsoid.  Only + - * / sqrt floor ceil ldexp; written order, no FMA.
+ * U_b = ldexp(T32[r], Q) with k_b = ceil(s_b * 32 log2 e) + 1, Q = floor(k_b/32), r = k_b - 32Q,
+ * so U_b / e^{s_b} lies in (2^{1/32}, 2^{2/32}]. */
 void orc_cull_ranges(int64_t G, const double* P, double tau, const double* origin,
-                     const double* inv_cell, const int32_t* dims, int32_t* rng /*[G][6]*/) {
+                     const double* inv_cell, const int32_t* dims, int32_t* rng /*[G][6]*/,
+                     double* r2 /*[G] or NULL*/) {
   for (int64_t j = 0; j < G; ++j) {
     const double* p = P + j * NP;
-    double qh[4], qn, R[3][3], U[3];
+    double qh[4], qn, R[3][3], U2[3];
     int deg;
     orc_qnorm(p + 3, qh, &qn, &deg);
     orc_rot(qh, R);
     for (int b = 0; b < 3; ++b) {
-      double sk = p[10 + b] * orc_K8;          /* clamp keeps the int conversion defined;   */
-      if (!(sk >= -8000.0)) sk = (sk != sk) ? 8000.0 : -8000.0;   /* NaN -> huge extent  */
-      if (sk > 8000.0) sk = 8000.0;
+      double sk = p[10 + b] * orc_K32;          /* clamp keeps the int conversion defined   */
+      if (!(sk >= -32000.0)) sk = (sk != sk) ? 32000.0 : -32000.0;   /* NaN -> huge extent */
+      if (sk > 32000.0) sk = 32000.0;
       int32_t k = (int32_t)ceil(sk) + 1;
-      int32_t Qe = (k >= 0) ? k / 8 : -((-k + 7) / 8);   /* floor(k/8) */
-      int32_t r = k - 8 * Qe;
-      U[b] = ldexp(orc_T8[r], Qe);
+      int32_t Qe = (k >= 0) ? k / 32 : -((-k + 31) / 32);   /* floor(k/32) */
+      int32_t r = k - 32 * Qe;
+      double U = ldexp(orc_T32[r], Qe);
+      U2[b] = U * U;
     }
     for (int a = 0; a < 3; ++a) {
-      double s0 = R[a][0] * R[a][0] * (U[0] * U[0]);
-      double s1 = R[a][1] * R[a][1] * (U[1] * U[1]);
-      double s2 = R[a][2] * R[a][2] * (U[2] * U[2]);
+      double s0 = R[a][0] * R[a][0] * U2[0];
+      double s1 = R[a][1] * R[a][1] * U2[1];
+      double s2 = R[a][2] * R[a][2] * U2[2];
       double h = tau * sqrt((s0 + s1) + s2);
       double flo = floor(((p[a] - h) - origin[a]) * inv_cell[a]);
       double fhi = floor(((p[a] + h) - origin[a]) * inv_cell[a]);
       rng[6 * j + a] = orc_clampcell(flo, dims[a]);
       rng[6 * j + 3 + a] = orc_clampcell(fhi, dims[a]);
     }
+    if (r2) {
+      double um = U2[0];
+      if (U2[1] > um) um = U2[1];
+      if (U2[2] > um) um = U2[2];
+      r2[j] = (tau * tau) * um;
+    }
   }
 }
 
-/* CSR cell -> ascending Gaussian indices (local to the level).  offsets: [cells+1].
- * If idx == NULL only offsets are produced (returns total entries). */
-int64_t orc_build_csr(int64_t G, const int32_t* rng, const int32_t* dims, int64_t* offsets,
-                      int32_t* idx) {
+/* Is cell c (per-axis indices) within the sphere |x - mu|^2 <= r2 of a Gaussian?  Squared
+ * distance from mu to the cell's box; border cells extend to infinity outwards (samples
+ * outside the grid clamp into them, A17). */
+int orc_cell_hit(const double* mu, double r2, const int32_t* c, const double* origin,
+                 const double* inv_cell, const int32_t* dims) {
+  double D2 = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    double lo = c[a] == 0 ? -INFINITY : origin[a] + (double)c[a] / inv_cell[a];
+    double hi = c[a] == dims[a] - 1 ? INFINITY : origin[a] + (double)(c[a] + 1) / inv_cell[a];
+    double d = mu[a] < lo ? lo - mu[a] : (mu[a] > hi ? mu[a] - hi : 0.0);
+    D2 = D2 + d * d;
+  }
+  return D2 <= r2;
+}
+
+/* CSR cell -> ascending Gaussian indices (local to the level): Gaussian j is listed in every
+ * cell of its range that passes orc_cell_hit.  offsets: [cells+1].  If idx == NULL only the
+ * offsets are produced (returns total entries). */
+int64_t orc_build_csr(int64_t G, const double* P, const int32_t* rng, const double* r2,
+                      const double* origin, const double* inv_cell, const int32_t* dims,
+                      int64_t* offsets, int32_t* idx) {
   int64_t cells = (int64_t)dims[0] * dims[1] * dims[2];
   for (int64_t c = 0; c <= cells; ++c) offsets[c] = 0;
-  for (int64_t j = 0; j < G; ++j) {
-    const int32_t* r = rng + 6 * j;
-    for (int32_t z = r[2]; z <= r[5]; ++z)
-      for (int32_t y = r[1]; y <= r[4]; ++y)
-        for (int32_t x = r[0]; x <= r[3]; ++x)
-          offsets[((int64_t)z * dims[1] + y) * dims[0] + x + 1] += 1;
+  for (int pass = 0; pass < 2; ++pass) {
+    int64_t* cur = NULL;
+    if (pass == 1) {
+      if (!idx) break;
+      for (int64_t c = 0; c < cells; ++c) offsets[c + 1] += offsets[c];
+      cur = (int64_t*)malloc(sizeof(int64_t) * (size_t)(cells > 0 ? cells : 1));
+      for (int64_t c = 0; c < cells; ++c) cur[c] = offsets[c];
+    }
+    for (int64_t j = 0; j < G; ++j) {
+      const int32_t* r = rng + 6 * j;
+      const double* mu = P + j * NP;
+      int32_t c3[3];
+      for (c3[2] = r[2]; c3[2] <= r[5]; ++c3[2])
+        for (c3[1] = r[1]; c3[1] <= r[4]; ++c3[1])
+          for (c3[0] = r[0]; c3[0] <= r[3]; ++c3[0]) {
+            if (!orc_cell_hit(mu, r2[j], c3, origin, inv_cell, dims)) continue;
+            int64_t cell = ((int64_t)c3[2] * dims[1] + c3[1]) * dims[0] + c3[0];
+            if (pass == 0) offsets[cell + 1] += 1;
+            else idx[cur[cell]++] = (int32_t)j;
+          }
+    }
+    if (cur) free(cur);
   }
-  for (int64_t c = 0; c < cells; ++c) offsets[c + 1] += offsets[c];
-  if (!idx) return offsets[cells];
-  int64_t* cur = (int64_t*)malloc(sizeof(int64_t) * (size_t)(cells > 0 ? cells : 1));
-  for (int64_t c = 0; c < cells; ++c) cur[c] = offsets[c];
-  for (int64_t j = 0; j < G; ++j) {
-    const int32_t* r = rng + 6 * j;
-    for (int32_t z = r[2]; z <= r[5]; ++z)
-      for (int32_t y = r[1]; y <= r[4]; ++y)
-        for (int32_t x = r[0]; x <= r[3]; ++x)
-          idx[cur[((int64_t)z * dims[1] + y) * dims[0] + x]++] = (int32_t)j;
-  }
-  free(cur);
+  if (!idx) for (int64_t c = 0; c < cells; ++c) offsets[c + 1] += offsets[c];
   return offsets[cells];
 }
 
@@ -364,11 +404,13 @@ static int orc_csr_make(int64_t G, const double* P, double tau, const double* or
                         const double* inv_cell, const int32_t* dims, orc_csr* c) {
   c->cells = (int64_t)dims[0] * dims[1] * dims[2];
   c->rng = (int32_t*)malloc(sizeof(int32_t) * 6 * (size_t)(G > 0 ? G : 1));
+  double* r2 = (double*)malloc(sizeof(double) * (size_t)(G > 0 ? G : 1));
   c->off = (int64_t*)malloc(sizeof(int64_t) * (size_t)(c->cells + 1));
-  orc_cull_ranges(G, P, tau, origin, inv_cell, dims, c->rng);
-  int64_t n = orc_build_csr(G, c->rng, dims, c->off, NULL);
+  orc_cull_ranges(G, P, tau, origin, inv_cell, dims, c->rng, r2);
+  int64_t n = orc_build_csr(G, P, c->rng, r2, origin, inv_cell, dims, c->off, NULL);
   c->idx = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
-  orc_build_csr(G, c->rng, dims, c->off, c->idx);
+  orc_build_csr(G, P, c->rng, r2, origin, inv_cell, dims, c->off, c->idx);
+  free(r2);
   return 0;
 }
 static void orc_csr_free(orc_csr* c) { free(c->rng); free(c->off); free(c->idx); }

@@ -135,7 +135,7 @@ __device__ void chain_rule(const float p[kNP], const float cg[12], float out[kNP
 
 __global__ void __launch_bounds__(256) k_adamw(int64_t G, float* __restrict__ P, float* __restrict__ M,
                                                float* __restrict__ V, float* __restrict__ grad,
-                                               float4* rec, uint4* range, uint32_t* csr_count,
+                                               float4* rec, uint4* range, double* rad2, uint32_t* csr_count,
                                                float* dbg, const DevState* __restrict__ st, AdamHP hp,
                                                LevelGeom g, gc_fit_stats* out) {
   unsigned long long bad = 0;
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(256) k_adamw(int64_t G, float* __restrict__ P,
         for (int k = 0; k < kNP; ++k) { M[k * G + j] = m[k]; V[k * G + j] = v[k]; P[k * G + j] = p[k]; }
       }
     }
-    record_and_count(j, p, hp.tau, g, rec, range, csr_count);
+    record_and_count(j, p, hp.tau, g, rec, range, rad2, csr_count);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
@@ -202,14 +202,14 @@ void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp
 }
 
 void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, float4* rec, uint4* range,
-                  uint32_t* csr_count, float* dbg_grad, DevState* st, const gc_hparams& hp,
+                  double* rad2, uint32_t* csr_count, float* dbg_grad, DevState* st, const gc_hparams& hp,
                   const LevelGeom& g, gc_fit_stats* dev_stats, cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "adamw_record_cull", s);
   AdamHP h;
   for (int k = 0; k < GC_NGROUPS; ++k) h.wd[k] = hp.weight_decay[k];
   h.beta1 = hp.beta1; h.beta2 = hp.beta2; h.eps = hp.adam_eps; h.tau = (double)hp.cutoff_sigma;
   int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((G + 255) / 256, 148 * 8));
-  k_adamw<<<blocks, 256, 0, s>>>(G, P, M, V, grad, rec, range, csr_count, dbg_grad, st, h, g, dev_stats);
+  k_adamw<<<blocks, 256, 0, s>>>(G, P, M, V, grad, rec, range, rad2, csr_count, dbg_grad, st, h, g, dev_stats);
 }
 
 }  // namespace gsc

@@ -79,6 +79,7 @@ struct gc_cache_s {
   float *P = nullptr, *M = nullptr, *V = nullptr, *grad = nullptr, *dbg = nullptr;
   float4* rec = nullptr;
   uint4* range = nullptr;
+  double* rad2 = nullptr;
   uint32_t *csr_count = nullptr, *csr_off = nullptr, *csr_cursor = nullptr, *csr_totals = nullptr;
   int32_t* csr_idx = nullptr;
   uint2* csr_tiles = nullptr;
@@ -153,11 +154,11 @@ static gc_status ensure_staging(Scratch& sc, bool need_pos, bool need_len, bool 
 
 static gc_status rebuild_csr(gc_cache c, cudaStream_t s, bool recompute_records) {
   if (recompute_records) {
-    launch_record_cull(c->G, c->P, (double)c->hp.cutoff_sigma, c->geom, c->rec, c->range, c->csr_count, s);
+    launch_record_cull(c->G, c->P, (double)c->hp.cutoff_sigma, c->geom, c->rec, c->range, c->rad2, c->csr_count, s);
   }
   launch_scan(c->csr_count, c->NC, 0, c->csr_tiles, c->csr_totals, c->csr_off, c->csr_cursor, nullptr,
               c->geom, s, &c->prof);
-  launch_cull_emit(c->G, c->range, c->geom, c->csr_cursor, c->csr_idx, c->csr_cap, c->st, s, &c->prof);
+  launch_cull_emit(c->G, c->range, c->rad2, c->P, c->geom, c->csr_cursor, c->csr_idx, c->csr_cap, c->st, s, &c->prof);
   CK(cudaGetLastError());
   return GC_OK;
 }
@@ -256,7 +257,7 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
   cudaStream_t s = 0;
   CK(dalloc(&c->P, kNP * G)); CK(dalloc(&c->M, kNP * G)); CK(dalloc(&c->V, kNP * G));
   CK(cudaMemset(c->M, 0, sizeof(float) * kNP * G)); CK(cudaMemset(c->V, 0, sizeof(float) * kNP * G));
-  CK(dalloc(&c->rec, 3 * G)); CK(dalloc(&c->grad, 12 * G)); CK(dalloc(&c->range, G));
+  CK(dalloc(&c->rec, 3 * G)); CK(dalloc(&c->grad, 12 * G)); CK(dalloc(&c->range, G)); CK(dalloc(&c->rad2, G));
   CK(cudaMemset(c->grad, 0, sizeof(float) * 12 * G));
   CK(dalloc(&c->st, 1)); CK(cudaMemset(c->st, 0, sizeof(DevState)));
   CK(dalloc(&c->lvl, 1)); CK(dalloc(&c->dstats, 1)); CK(cudaMemset(c->dstats, 0, sizeof(gc_fit_stats)));
@@ -344,7 +345,7 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
   CK(dalloc(&c->csr_count, c->NC)); CK(dalloc(&c->csr_off, c->NC + 1)); CK(dalloc(&c->csr_cursor, c->NC));
   CK(dalloc(&c->csr_tiles, (c->NC + kScanTile - 1) / kScanTile)); CK(dalloc(&c->csr_totals, 4));
   CK(cudaMemset(c->csr_count, 0, sizeof(uint32_t) * c->NC));
-  launch_record_cull(G, c->P, tau, c->geom, c->rec, c->range, c->csr_count, s);
+  launch_record_cull(G, c->P, tau, c->geom, c->rec, c->range, c->rad2, c->csr_count, s);
   launch_scan(c->csr_count, c->NC, 0, c->csr_tiles, c->csr_totals, c->csr_off, c->csr_cursor, nullptr, c->geom, s, nullptr);
   CK(cudaGetLastError());
   uint32_t total = 0;
@@ -353,7 +354,7 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
   cap = std::min<uint64_t>(cap, 0x7FFFFFFFull);
   c->csr_cap = (uint32_t)cap;
   CK(dalloc(&c->csr_idx, c->csr_cap));
-  launch_cull_emit(G, c->range, c->geom, c->csr_cursor, c->csr_idx, c->csr_cap, c->st, s, nullptr);
+  launch_cull_emit(G, c->range, c->rad2, c->P, c->geom, c->csr_cursor, c->csr_idx, c->csr_cap, c->st, s, nullptr);
   CK(cudaGetLastError());
 
   c->fb_grid = fwdbwd_grid();
@@ -367,7 +368,7 @@ static void destroy_impl(gc_cache c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  void* ps[] = {c->P, c->M, c->V, c->grad, c->dbg, c->rec, c->range, c->csr_count, c->csr_off, c->csr_cursor,
+  void* ps[] = {c->P, c->M, c->V, c->grad, c->dbg, c->rec, c->range, c->rad2, c->csr_count, c->csr_off, c->csr_cursor,
                 c->csr_totals, c->csr_idx, c->csr_tiles, c->st, c->lvl, c->dstats, c->partial, c->pack_tmp};
   for (void* p : ps) if (p) cudaFree(p);
   if (c->hstats) cudaFreeHost(c->hstats);
@@ -463,7 +464,7 @@ gc_status gc_fit(gc_cache c, const float* pos, const int32_t* path_len, const fl
     NK(ncclGroupEnd());
   }
   launch_step_scalars(c->lvl, c->st, c->hp, c->L, c->dstats, s);
-  launch_adamw(c->G, c->P, c->M, c->V, c->grad, c->rec, c->range, c->csr_count, c->dbg_on ? c->dbg : nullptr,
+  launch_adamw(c->G, c->P, c->M, c->V, c->grad, c->rec, c->range, c->rad2, c->csr_count, c->dbg_on ? c->dbg : nullptr,
                c->st, c->hp, c->geom, c->dstats, s, &c->prof);
   if (gc_status e = rebuild_csr(c, s, false)) return e;
   if (gc_status e = emit_stats(c, stats, s)) return e;

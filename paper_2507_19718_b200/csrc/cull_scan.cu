@@ -7,31 +7,32 @@
 namespace gsc {
 
 __global__ void k_record_cull(int64_t G, const float* __restrict__ P, double tau, LevelGeom g,
-                              float4* rec, uint4* range, uint32_t* csr_count) {
+                              float4* rec, uint4* range, double* rad2, uint32_t* csr_count) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < G; j += (int64_t)gridDim.x * blockDim.x) {
     float p[kNP];
 #pragma unroll
     for (int k = 0; k < kNP; ++k) p[k] = P[k * G + j];
-    record_and_count(j, p, tau, g, rec, range, csr_count);
+    record_and_count(j, p, tau, g, rec, range, rad2, csr_count);
   }
 }
 
 // Fill the culling lists: each Gaussian appends its global index to every cell of its range.
 // The order inside a cell is atomic order (unspecified); gc_debug_cull sorts on export.
-__global__ void k_cull_emit(int64_t G, const uint4* __restrict__ range, LevelGeom g,
-                            uint32_t* cursor, int32_t* idx, uint32_t cap, DevState* st) {
+__global__ void k_cull_emit(int64_t G, const uint4* __restrict__ range, const double* __restrict__ rad2,
+                            const float* __restrict__ P, LevelGeom g, uint32_t* cursor, int32_t* idx,
+                            uint32_t cap, DevState* st) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < G; j += (int64_t)gridDim.x * blockDim.x) {
     uint4 r = range[j];
+    const double r2 = rad2[j];
+    const double m0 = P[P_MU * G + j], m1 = P[(P_MU + 1) * G + j], m2 = P[(P_MU + 2) * G + j];
     int l = level_of_gaussian(g, j);
-    int32_t lx = r.x & 0xFFFF, hx = r.x >> 16, ly = r.y & 0xFFFF, hy = r.y >> 16, lz = r.z & 0xFFFF, hz = r.z >> 16;
-    const int64_t dx = g.dims[l][0], dy = g.dims[l][1];
-    for (int32_t cz = lz; cz <= hz; ++cz)
-      for (int32_t cy = ly; cy <= hy; ++cy)
-        for (int32_t cx = lx; cx <= hx; ++cx) {
-          uint32_t pos = atomicAdd(cursor + g.coff[l] + ((int64_t)cz * dy + cy) * dx + cx, 1u);
-          if (pos < cap) idx[pos] = (int32_t)j;
-          else atomicOr(&st->csr_overflow, 1u);
-        }
+    const int32_t lo[3] = {(int32_t)(r.x & 0xFFFF), (int32_t)(r.y & 0xFFFF), (int32_t)(r.z & 0xFFFF)};
+    const int32_t hi[3] = {(int32_t)(r.x >> 16), (int32_t)(r.y >> 16), (int32_t)(r.z >> 16)};
+    for_each_cell(lo, hi, m0, m1, m2, r2, g, l, [&](int64_t cell) {
+      const uint32_t pos = atomicAdd(cursor + cell, 1u);
+      if (pos < cap) idx[pos] = (int32_t)j;
+      else atomicOr(&st->csr_overflow, 1u);
+    });
   }
 }
 
@@ -160,18 +161,18 @@ void launch_scan(uint32_t* cnt, int64_t n, int ch, uint2* tile_sums, uint32_t* t
 }
 
 void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& g, float4* rec,
-                        uint4* range, uint32_t* csr_count, cudaStream_t s) {
+                        uint4* range, double* rad2, uint32_t* csr_count, cudaStream_t s) {
   int blocks = (int)std::min<int64_t>((G + 255) / 256, 148 * 16);
   if (blocks < 1) blocks = 1;
-  k_record_cull<<<blocks, 256, 0, s>>>(G, P, tau, g, rec, range, csr_count);
+  k_record_cull<<<blocks, 256, 0, s>>>(G, P, tau, g, rec, range, rad2, csr_count);
 }
 
-void launch_cull_emit(int64_t G, const uint4* range, const LevelGeom& g, uint32_t* cursor,
-                      int32_t* idx, uint32_t cap, DevState* st, cudaStream_t s, Profiler* prof) {
+void launch_cull_emit(int64_t G, const uint4* range, const double* rad2, const float* P, const LevelGeom& g,
+                      uint32_t* cursor, int32_t* idx, uint32_t cap, DevState* st, cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "cull_emit", s);
   int blocks = (int)std::min<int64_t>((G + 255) / 256, 148 * 16);
   if (blocks < 1) blocks = 1;
-  k_cull_emit<<<blocks, 256, 0, s>>>(G, range, g, cursor, idx, cap, st);
+  k_cull_emit<<<blocks, 256, 0, s>>>(G, range, rad2, P, g, cursor, idx, cap, st);
 }
 
 }  // namespace gsc

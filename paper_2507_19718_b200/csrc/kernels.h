@@ -62,9 +62,9 @@ void launch_scan(uint32_t* cnt, int64_t n, int ch, uint2* tile_sums, uint32_t* t
                  uint32_t* excl, uint32_t* excl_copy, WorkItem* work, const LevelGeom& g,
                  cudaStream_t s, Profiler* prof);
 void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& g, float4* rec,
-                        uint4* range, uint32_t* csr_count, cudaStream_t s);
-void launch_cull_emit(int64_t G, const uint4* range, const LevelGeom& g, uint32_t* cursor,
-                      int32_t* idx, uint32_t cap, DevState* st, cudaStream_t s, Profiler* prof);
+                        uint4* range, double* rad2, uint32_t* csr_count, cudaStream_t s);
+void launch_cull_emit(int64_t G, const uint4* range, const double* rad2, const float* P, const LevelGeom& g,
+                      uint32_t* cursor, int32_t* idx, uint32_t cap, DevState* st, cudaStream_t s, Profiler* prof);
 
 // ingest.cu
 struct IngestBufs {
@@ -109,7 +109,7 @@ void launch_stats(const double* partial, int nblocks, const uint32_t* cell_start
 void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp, int L,
                          gc_fit_stats* dev_stats, cudaStream_t s);
 void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, float4* rec, uint4* range,
-                  uint32_t* csr_count, float* dbg_grad, DevState* st, const gc_hparams& hp,
+                  double* rad2, uint32_t* csr_count, float* dbg_grad, DevState* st, const gc_hparams& hp,
                   const LevelGeom& g, gc_fit_stats* dev_stats, cudaStream_t s, Profiler* prof);
 
 // create.cu

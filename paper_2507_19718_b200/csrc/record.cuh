@@ -5,11 +5,17 @@
 
 namespace gsc {
 
-// Upper bounds of 2^(r/8): the smallest doubles >= 2^(r/8) (C8; hex literals of the spec).
-static __device__ const double kT8[8] = {
-    0x1.0000000000000p+0, 0x1.172b83c7d517bp+0, 0x1.306fe0a31b716p+0, 0x1.4bfdad5362a28p+0,
-    0x1.6a09e667f3bcdp+0, 0x1.8ace5422aa0dcp+0, 0x1.ae89f995ad3aep+0, 0x1.d5818dcfba488p+0};
-constexpr double kK8 = 0x1.71547652b82fep+3;   // 8 log2(e)
+// Upper bounds of 2^(r/32): the smallest doubles >= 2^(r/32) (C8; hex literals of the spec).
+static __device__ const double kT32[32] = {
+    0x1.0000000000000p+0, 0x1.059b0d3158575p+0, 0x1.0b5586cf98910p+0, 0x1.11301d0125b51p+0,
+    0x1.172b83c7d517bp+0, 0x1.1d4873168b9abp+0, 0x1.2387a6e756239p+0, 0x1.29e9df51fdee2p+0,
+    0x1.306fe0a31b716p+0, 0x1.371a7373aa9cbp+0, 0x1.3dea64c123423p+0, 0x1.44e086061892ep+0,
+    0x1.4bfdad5362a28p+0, 0x1.5342b569d4f82p+0, 0x1.5ab07dd48542ap+0, 0x1.6247eb03a5585p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.71f75e8ec5f74p+0, 0x1.7a11473eb0187p+0, 0x1.82589994cce13p+0,
+    0x1.8ace5422aa0dcp+0, 0x1.93737b0cdc5e5p+0, 0x1.9c49182a3f091p+0, 0x1.a5503b23e255dp+0,
+    0x1.ae89f995ad3aep+0, 0x1.b7f76f2fb5e47p+0, 0x1.c199bdd85529dp+0, 0x1.cb720dcef906ap+0,
+    0x1.d5818dcfba488p+0, 0x1.dfc97337b9b5fp+0, 0x1.ea4afa2a490dap+0, 0x1.f50765b6e4541p+0};
+constexpr double kK32 = 0x1.71547652b82fep+5;   // 32 log2(e)
 
 // Record of one Gaussian from its raw parameters (C1): A = R diag(e^-2s) R^T is formed and
 // Cholesky-factored in fp64 (A = U^T U), stored in fp32 with mu and v = w max(0, c).
@@ -39,9 +45,11 @@ __device__ __forceinline__ void make_record(const float p[kNP], float4 out[3]) {
   out[2] = make_float4(p[P_MU + 2], wo * fmaxf(p[P_C], 0.f), wo * fmaxf(p[P_C + 1], 0.f), wo * fmaxf(p[P_C + 2], 0.f));
 }
 
-// C8 cell range of one Gaussian, fp64 with explicitly rounded + - * / sqrt only.
+// C8 cell range of one Gaussian (AABB of its tau-ellipsoid, bounded with U_b >= e^{s_b}) and
+// r2 = tau^2 max_b U_b^2; fp64 with explicitly rounded + - * / sqrt only (no FMA, no exp), in
+// the order the oracle writes them, so both produce the same integers.
 __device__ __forceinline__ void cull_range(const float p[kNP], double tau, const LevelGeom& g, int l,
-                           int32_t lo[3], int32_t hi[3]) {
+                                           int32_t lo[3], int32_t hi[3], double& r2) {
   double w = p[P_Q], x = p[P_Q + 1], y = p[P_Q + 2], z = p[P_Q + 3];
   double n2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(w, w), __dmul_rn(x, x)), __dmul_rn(y, y)), __dmul_rn(z, z));
   if (n2 < 1e-24) { w = 1.0; x = 0.0; y = 0.0; z = 0.0; }
@@ -62,12 +70,12 @@ __device__ __forceinline__ void cull_range(const float p[kNP], double tau, const
   double U2[3];
 #pragma unroll
   for (int b = 0; b < 3; ++b) {
-    double sk = __dmul_rn((double)p[P_S + b], kK8);
-    if (!(sk >= -8000.0)) sk = (sk != sk) ? 8000.0 : -8000.0;
-    if (sk > 8000.0) sk = 8000.0;
+    double sk = __dmul_rn((double)p[P_S + b], kK32);
+    if (!(sk >= -32000.0)) sk = (sk != sk) ? 32000.0 : -32000.0;
+    if (sk > 32000.0) sk = 32000.0;
     int32_t k = (int32_t)ceil(sk) + 1;
-    int32_t Qe = (k >= 0) ? k / 8 : -((-k + 7) / 8);
-    double U = ldexp(kT8[k - 8 * Qe], Qe);
+    int32_t Qe = (k >= 0) ? k / 32 : -((-k + 31) / 32);
+    double U = ldexp(kT32[k - 32 * Qe], Qe);
     U2[b] = __dmul_rn(U, U);
   }
 #pragma unroll
@@ -80,24 +88,63 @@ __device__ __forceinline__ void cull_range(const float p[kNP], double tau, const
     lo[a] = clampcell(floor(__dmul_rn(__dsub_rn(__dsub_rn(mu, h), g.origin[l][a]), g.inv_cell[l][a])), g.dims[l][a]);
     hi[a] = clampcell(floor(__dmul_rn(__dsub_rn(__dadd_rn(mu, h), g.origin[l][a]), g.inv_cell[l][a])), g.dims[l][a]);
   }
+  double um = U2[0];
+  if (U2[1] > um) um = U2[1];
+  if (U2[2] > um) um = U2[2];
+  r2 = __dmul_rn(__dmul_rn(tau, tau), um);
+}
+
+// Cell membership (C8): squared distance from mu to the cell's box <= r2; border cells reach
+// to infinity outwards (A17).  The oracle's orc_cell_hit computes, per axis,
+// d_a = dist(mu_a, [o_a + c_a/inv_a, o_a + (c_a+1)/inv_a]) and D2 = (d_x^2 + d_y^2) + d_z^2;
+// the same per-axis terms are tabulated here once per Gaussian (bit-identical doubles).
+__device__ __forceinline__ double axis_d2(double mu, int32_t c, const LevelGeom& g, int l, int a) {
+  const double lo = c == 0 ? -INFINITY : __dadd_rn(g.origin[l][a], __ddiv_rn((double)c, g.inv_cell[l][a]));
+  const double hi = c == g.dims[l][a] - 1 ? INFINITY
+                                          : __dadd_rn(g.origin[l][a], __ddiv_rn((double)(c + 1), g.inv_cell[l][a]));
+  const double d = mu < lo ? __dsub_rn(lo, mu) : (mu > hi ? __dsub_rn(mu, hi) : 0.0);
+  return __dmul_rn(d, d);
+}
+
+constexpr int kAxisTab = 8;
+
+// Visit every listed cell of one Gaussian: f(cell_linear_index).
+template <class F>
+__device__ __forceinline__ void for_each_cell(const int32_t lo[3], const int32_t hi[3], double m0, double m1,
+                                              double m2, double r2, const LevelGeom& g, int l, F&& f) {
+  const int64_t dx = g.dims[l][0], dy = g.dims[l][1];
+  const bool tab = hi[0] - lo[0] < kAxisTab && hi[1] - lo[1] < kAxisTab && hi[2] - lo[2] < kAxisTab;
+  double tx[kAxisTab], ty[kAxisTab];
+  if (tab) {
+    for (int32_t c = lo[0]; c <= hi[0]; ++c) tx[c - lo[0]] = axis_d2(m0, c, g, l, 0);
+    for (int32_t c = lo[1]; c <= hi[1]; ++c) ty[c - lo[1]] = axis_d2(m1, c, g, l, 1);
+  }
+  for (int32_t cz = lo[2]; cz <= hi[2]; ++cz) {
+    const double dz2 = axis_d2(m2, cz, g, l, 2);
+    for (int32_t cy = lo[1]; cy <= hi[1]; ++cy) {
+      const double dy2 = tab ? ty[cy - lo[1]] : axis_d2(m1, cy, g, l, 1);
+      for (int32_t cx = lo[0]; cx <= hi[0]; ++cx) {
+        const double dx2 = tab ? tx[cx - lo[0]] : axis_d2(m0, cx, g, l, 0);
+        if (__dadd_rn(__dadd_rn(dx2, dy2), dz2) <= r2) f(g.coff[l] + ((int64_t)cz * dy + cy) * dx + cx);
+      }
+    }
+  }
 }
 
 __device__ __forceinline__ void record_and_count(int64_t j, const float p[kNP], double tau, const LevelGeom& g,
-                                 float4* rec, uint4* range, uint32_t* csr_count) {
+                                                 float4* rec, uint4* range, double* rad2, uint32_t* csr_count) {
   float4 r[3];
   make_record(p, r);
   rec[3 * j] = r[0]; rec[3 * j + 1] = r[1]; rec[3 * j + 2] = r[2];
-  int l = level_of_gaussian(g, j);
+  const int l = level_of_gaussian(g, j);
   int32_t lo[3], hi[3];
-  cull_range(p, tau, g, l, lo, hi);
-  uint32_t cnt = (uint32_t)(hi[0] - lo[0] + 1) * (uint32_t)(hi[1] - lo[1] + 1) * (uint32_t)(hi[2] - lo[2] + 1);
+  double r2;
+  cull_range(p, tau, g, l, lo, hi, r2);
   range[j] = make_uint4((uint32_t)lo[0] | ((uint32_t)hi[0] << 16), (uint32_t)lo[1] | ((uint32_t)hi[1] << 16),
-                        (uint32_t)lo[2] | ((uint32_t)hi[2] << 16), cnt);
-  const int64_t dx = g.dims[l][0], dy = g.dims[l][1];
-  for (int32_t cz = lo[2]; cz <= hi[2]; ++cz)
-    for (int32_t cy = lo[1]; cy <= hi[1]; ++cy)
-      for (int32_t cx = lo[0]; cx <= hi[0]; ++cx)
-        atomicAdd(csr_count + g.coff[l] + ((int64_t)cz * dy + cy) * dx + cx, 1u);
+                        (uint32_t)lo[2] | ((uint32_t)hi[2] << 16), 0u);
+  rad2[j] = r2;
+  for_each_cell(lo, hi, (double)p[P_MU], (double)p[P_MU + 1], (double)p[P_MU + 2], r2, g, l,
+                [&](int64_t cell) { atomicAdd(csr_count + cell, 1u); });
 }
 
 }  // namespace gsc

@@ -101,8 +101,7 @@ def _check_csr(c, P):
     for l in range(c.L):
         o, ic, d = c.grid(l)
         Pl = P[c.goff[l]:c.goff[l + 1]]
-        rng = oracle.cull_ranges(Pl, 3.0, o, ic, d)
-        off_o, idx_o = oracle.build_csr(rng, d)
+        off_o, idx_o = oracle.csr_for(Pl, 3.0, (o, ic, d))
         off_g, idx_g = c.debug_cull(l)
         np.testing.assert_array_equal(off_g.astype(np.int64), off_o)
         np.testing.assert_array_equal(idx_g, idx_o)

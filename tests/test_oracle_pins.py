@@ -391,8 +391,7 @@ def test_culling_contains_every_supported_pair(cells):
     P = rand_params(40, r)
     P[:, 10:13] = np.log(r.uniform(0.03, 0.2, (40, 3)))
     origin, inv, dims = _grid_for(P, cells)
-    rng = oracle.cull_ranges(P, 3.0, origin, inv, dims)
-    off, idx = oracle.build_csr(rng, dims)
+    off, idx = oracle.csr_for(P, 3.0, (origin, inv, dims))
     x = np.concatenate([r.uniform(-0.9, 0.9, (3000, 3)),
                         P[:, 0:3] + r.normal(scale=0.1, size=(40, 3))])
     Q = oracle.q_matrix(P, x)
@@ -431,17 +430,38 @@ def test_culled_evaluator_equals_brute_force():
 
 
 def test_cull_bound_is_transcendental_free_and_tight():
-    """C8: the exp-free bound U_b exceeds e^{s_b} by a factor in (2^{1/8}, 2^{2/8}]."""
+    """C8: the exp-free bound U_b exceeds e^{s_b} by a factor in (2^{1/32}, 2^{2/32}]."""
     P = np.zeros((1, 14)); P[0, 3] = 1.0
     n = 2_000_000_000                                        # 1e-7 cells: resolution << h
     inv = n / 200.0
     for s in np.linspace(-6, 1, 57):
         P[0, 10:13] = s
-        rng = oracle.cull_ranges(P, 1.0, np.zeros(3) - 100.0, np.full(3, inv),
-                                 np.full(3, n, np.int32))
+        rng, r2 = oracle.cull_ranges(P, 1.0, np.zeros(3) - 100.0, np.full(3, inv),
+                                     np.full(3, n, np.int32))
         h = (rng[0, 3] - rng[0, 0] + 1) / (2 * inv)          # half extent in world units
         ratio = h / np.exp(s)
-        assert 2 ** 0.125 * (1 - 1e-4) < ratio < 2 ** 0.25 * (1 + 1e-4), (s, ratio)
+        assert 2 ** (1 / 32) * (1 - 1e-4) < ratio < 2 ** (2 / 32) * (1 + 1e-4), (s, ratio)
+        assert 2 ** (1 / 32) < np.sqrt(r2[0]) / np.exp(s) <= 2 ** (2 / 32)
+
+
+def test_cell_sphere_test_prunes_aabb_corners():
+    """C8 list membership = AABB range AND sphere-box test: strictly fewer entries than the
+    AABB alone for an isotropic Gaussian straddling cells, and never losing a covered cell."""
+    P = np.zeros((1, 14)); P[0, 3] = 1.0; P[0, 10:13] = np.log(0.1)
+    P[0, 0:3] = [0.5, 0.5, 0.5]                             # at a cell corner
+    grid = (np.zeros(3) - 1.0, np.full(3, 10.0), np.full(3, 20, np.int32))   # edge 0.1
+    rng, r2 = oracle.cull_ranges(P, 3.0, *grid)
+    aabb = np.prod(rng[0, 3:] - rng[0, :3] + 1)
+    off, idx = oracle.build_csr(P, rng, r2, *grid)
+    assert 0 < len(idx) < aabb
+    # every cell containing a point of the tau-sphere is listed
+    r = np.random.default_rng(13)
+    u = r.normal(size=(20000, 3)); u /= np.linalg.norm(u, axis=1, keepdims=True)
+    pts = P[0, 0:3] + u * 0.3 * r.uniform(0, 1, (20000, 1)) ** (1 / 3)
+    c = oracle.sample_cell(pts, *grid)
+    lin = (c[:, 2] * 20 + c[:, 1]) * 20 + c[:, 0]
+    listed = {cell for cell in range(8000) if off[cell + 1] > off[cell]}
+    assert set(lin.tolist()) <= listed
 
 
 # ----------------------------------------------------- whole-fit pins (oracle)
