@@ -143,7 +143,10 @@ __global__ void __launch_bounds__(256) k_scan_down(uint32_t* __restrict__ cnt, i
     }
     if (i == n - 1) excl[n] = off;
   }
-  if (blockIdx.x == ntiles - 1 && threadIdx.x == 0) { totals[0] = tp.x + total.x; totals[1] = tp.y + total.y; }
+  if (blockIdx.x == ntiles - 1 && threadIdx.x == 0) {
+    totals[0] = tp.x + total.x; totals[1] = tp.y + total.y;
+    totals[2] = 0u;                    // dynamic work counter of the consumer kernel
+  }
 }
 
 void launch_scan(uint32_t* cnt, int64_t n, int ch, uint2* tile_sums, uint32_t* totals,

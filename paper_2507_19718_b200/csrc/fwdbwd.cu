@@ -21,7 +21,7 @@ namespace gsc {
 
 constexpr int kPart = kMaxL + 2;
 constexpr int kWarps = 8;                                 // warps per CTA
-constexpr int kPairCap = 768;                             // recorded (sample, Gaussian) pairs per warp
+constexpr int kPairCap = 512;                             // recorded (sample, Gaussian) pairs per warp
 constexpr int kMaxChunks = 64;                            // recorded chunks per work item (C <= 2048)
 constexpr float kNegHalfLog2e = -0.72134752044448170f;    // -0.5 * log2(e)
 static_assert(kCH == 64, "two samples per lane");
@@ -199,7 +199,7 @@ __device__ __forceinline__ void hdr_grad(int mode, float eps, const float (&y)[3
   }
 }
 
-__global__ void __launch_bounds__(256, 3) k_fwdbwd(FitArgs a) {
+__global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
   extern __shared__ __align__(16) unsigned char dsm[];
   WarpSmem* sm = reinterpret_cast<WarpSmem*>(dsm);
   __shared__ double s_loss[kWarps][kMaxL];
@@ -208,11 +208,15 @@ __global__ void __launch_bounds__(256, 3) k_fwdbwd(FitArgs a) {
   WarpSmem& w = sm[wid];
   if (lane < kMaxL) s_loss[wid][lane] = 0.0;
   unsigned long long pairs_acc = 0, cand_acc = 0;
-  const uint32_t n_work = *a.n_work;
+  const uint32_t n_work = a.n_work[0];
+  uint32_t* next = const_cast<uint32_t*>(a.n_work) + 1;   // dynamic work counter (zeroed by the scan)
   const float tau2 = a.tau2, eps = a.hdr_eps;
-  const uint32_t gw = blockIdx.x * kWarps + wid, nw = gridDim.x * kWarps;
 
-  for (uint32_t it = gw; it < n_work; it += nw) {
+  for (;;) {
+    uint32_t it = 0;
+    if (lane == 0) it = atomicAdd(next, 1u);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= n_work) break;
     const WorkItem wi = a.work[it];
     const int lo = (int)__ldg(a.csr_off + wi.cell);
     const int C = (int)__ldg(a.csr_off + wi.cell + 1) - lo;
@@ -324,10 +328,14 @@ __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
   __shared__ ChunkSmem sm[kWarps];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   ChunkSmem& w = sm[wid];
-  const uint32_t n_work = *a.n_work;
+  const uint32_t n_work = a.n_work[0];
+  uint32_t* next = const_cast<uint32_t*>(a.n_work) + 1;   // dynamic work counter (zeroed by the scan)
   const float tau2 = a.tau2;
-  const uint32_t gw = blockIdx.x * kWarps + wid, nw = gridDim.x * kWarps;
-  for (uint32_t it = gw; it < n_work; it += nw) {
+  for (;;) {
+    uint32_t it = 0;
+    if (lane == 0) it = atomicAdd(next, 1u);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= n_work) break;
     const WorkItem wi = a.work[it];
     const int lo = (int)__ldg(a.csr_off + wi.cell);
     const int C = (int)__ldg(a.csr_off + wi.cell + 1) - lo;
