@@ -26,7 +26,10 @@ __global__ void __launch_bounds__(kPart * 32) k_stats(const double* __restrict__
   }
   if (col == 0) {
     double c = 0.0;
-    if (lane < g.L) c = (double)(cell_start[g.coff[lane + 1] * kRep] - cell_start[g.coff[lane] * kRep]);
+    // start of cell c in the replica-major offsets: replica 0 row; the end sentinel at kRep*NC
+    const int64_t nc = g.coff[g.L];
+    auto at = [&](int64_t cc) { return cell_start[cc == nc ? nc * kRep : cc]; };
+    if (lane < g.L) c = (double)(at(g.coff[lane + 1]) - at(g.coff[lane]));
     if (lane < kMaxL) lvl->count[lane] = c;
     double tot = c;
 #pragma unroll

@@ -445,7 +445,7 @@ gc_status gc_fit(gc_cache c, const float* pos, const int32_t* path_len, const fl
       if (hrgb) { CK(cudaMemcpyAsync(F.in_rgb, rgb, sizeof(float) * 3 * S, cudaMemcpyHostToDevice, s)); rgb = F.in_rgb; }
     }
   }
-  IngestBufs b{F.key, F.rank, F.cell_count, F.bin};
+  IngestBufs b{F.key, F.rank, F.cell_count, F.bin, c->NC};
   if (S > 0) launch_keys(pos, path_len, rgb, -1, S, c->geom, b, s, &c->prof);
   launch_scan(F.cell_count, c->NC * kRep, kCH, F.tiles, F.totals, F.cell_start, nullptr, F.work, c->geom, s, &c->prof);
   if (S > 0) launch_scatter(pos, rgb, S, F.cell_start, b, s, &c->prof);
@@ -493,7 +493,7 @@ gc_status gc_query(gc_cache c, const float* pos, const int32_t* path_len, int le
     if (hlen) { CK(cudaMemcpyAsync(Q.in_len, path_len, sizeof(int32_t) * S, cudaMemcpyHostToDevice, s)); path_len = Q.in_len; }
   }
   float* dout = hout ? Q.out : out_rgb;
-  IngestBufs b{Q.key, Q.rank, Q.cell_count, Q.bin};
+  IngestBufs b{Q.key, Q.rank, Q.cell_count, Q.bin, c->NC};
   launch_keys_query(pos, path_len, path_len ? -1 : level, S, c->geom, b, dout, s, &c->prof);
   launch_scan(Q.cell_count, c->NC * kRep, kCH, Q.tiles, Q.totals, Q.cell_start, nullptr, Q.work, c->geom, s, &c->prof);
   launch_scatter(pos, nullptr, S, Q.cell_start, b, s, &c->prof);

@@ -88,10 +88,26 @@ __device__ __forceinline__ uint2 sum8(const uint32_t c[8], int ch) {
   return s;
 }
 
+// Sample-bin counters are replica-major ([kRep][NC]: the replicas of a cell live in different
+// L2 lines, so a hot cell's atomics spread over slices); a scan thread owns the kRep
+// replicas of one cell, visiting cells in order.  Plain counters: 8 consecutive entries.
+__device__ __forceinline__ int64_t entry(int ch, int64_t n, int64_t base, int k) {
+  if (!ch) return base + k;
+  const int64_t nc = n / kRep;
+  return (int64_t)k * nc + base / kRep;    // base / kRep = this thread's cell
+}
+
+__device__ __forceinline__ void load_counts(const uint32_t* cnt, int64_t n, int ch, int64_t base, uint32_t c[8]) {
+  if (!ch) { load8(cnt, n, base, c); return; }
+  const int64_t cell = base / kRep, nc = n / kRep;
+#pragma unroll
+  for (int k = 0; k < kRep; ++k) c[k] = cell < nc ? cnt[(int64_t)k * nc + cell] : 0u;
+}
+
 __global__ void __launch_bounds__(256) k_scan_reduce(const uint32_t* __restrict__ cnt, int64_t n, int ch, uint2* tile_sums) {
   int64_t base = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 8;
   uint32_t c[8];
-  load8(cnt, n, base, c);
+  load_counts(cnt, n, ch, base, c);
   const uint2 s = sum8(c, ch);
   uint2 total;
   block_excl_scan(s, total);
@@ -116,12 +132,13 @@ __global__ void __launch_bounds__(256) k_scan_down(uint32_t* __restrict__ cnt, i
   const uint2 tp = dummy;
   int64_t base = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 8;
   uint32_t c[8];
-  load8(cnt, n, base, c);
-  if (base + 8 <= n && ((base & 3) == 0)) {
+  load_counts(cnt, n, ch, base, c);
+  if (!ch && base + 8 <= n && ((base & 3) == 0)) {
     *reinterpret_cast<uint4*>(cnt + base) = make_uint4(0, 0, 0, 0);
     *reinterpret_cast<uint4*>(cnt + base + 4) = make_uint4(0, 0, 0, 0);
-  } else {
-    for (int k = 0; k < 8; ++k) if (base + k < n) cnt[base + k] = 0u;
+  } else if (base < n) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { const int64_t e = entry(ch, n, base, k); if (e < n && base + k < n) cnt[e] = 0u; }
   }
   const uint2 s = sum8(c, ch);
   uint2 total;
@@ -137,8 +154,9 @@ __global__ void __launch_bounds__(256) k_scan_down(uint32_t* __restrict__ cnt, i
   for (int k = 0; k < 8; ++k) {
     int64_t i = base + k;
     if (i < n) {
-      excl[i] = off;
-      if (excl_copy) excl_copy[i] = off;
+      const int64_t e = entry(ch, n, base, k);
+      excl[e] = off;
+      if (excl_copy) excl_copy[e] = off;
       off += c[k];
     }
     if (i == n - 1) excl[n] = off;

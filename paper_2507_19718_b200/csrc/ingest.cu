@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(256) k_keys(const float* __restrict__ pos, con
       base[u] = 0;
       const uint32_t r = (uint32_t)(((i0 + u * 32) >> 5) & (kRep - 1));
       if (key[u] != kInvalidKey && lane == __ffs(peers[u]) - 1)
-        base[u] = atomicAdd(b.cell_count + (size_t)key[u] * kRep + r, (uint32_t)__popc(peers[u]));
+        base[u] = atomicAdd(b.cell_count + (size_t)r * b.nc + key[u], (uint32_t)__popc(peers[u]));
     }
     uint32_t rank[kU];
 #pragma unroll
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(256) k_scatter(const float* __restrict__ pos, 
 #pragma unroll
     for (int u = 0; u < kU; ++u)
       d[u] = key[u] != kInvalidKey
-                 ? __ldg(cell_start + (size_t)key[u] * kRep + (((i0 + u * 32) >> 5) & (kRep - 1))) + rank[u]
+                 ? __ldg(cell_start + (size_t)(((i0 + u * 32) >> 5) & (kRep - 1)) * b.nc + key[u]) + rank[u]
                  : 0u;
     float v[kU][6];
 #pragma unroll

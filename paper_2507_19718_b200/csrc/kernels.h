@@ -73,6 +73,7 @@ struct IngestBufs {
   uint32_t* cell_count; // [NC]
   float4* bin;          // binned samples, cell-major: fit 2 x float4 (x,y,z,r | g,b,-,-),
                         // query 1 x float4 (x,y,z, original index as bits)
+  int64_t nc;           // cells (counters are replica-major [kRep][nc])
 };
 void launch_keys(const float* pos, const int32_t* len, const float* rgb, int level_fixed,
                  int64_t S, const LevelGeom& g, IngestBufs b, cudaStream_t s, Profiler* prof);
