@@ -8,11 +8,22 @@
 
 namespace gsc {
 
-constexpr int kU = 8;   // samples per thread per iteration
+constexpr int kU = 4;   // samples per thread per iteration
 
-__global__ void __launch_bounds__(256) k_keys(const float* __restrict__ pos, const int32_t* __restrict__ len,
-                                              const float* __restrict__ rgb, int level_fixed, int64_t S,
-                                              LevelGeom g, IngestBufs b, float* out_zero) {
+__global__ void __launch_bounds__(256, 5) k_keys(const float* __restrict__ pos, const int32_t* __restrict__ len,
+                                                 const float* __restrict__ rgb, int level_fixed, int64_t S,
+                                                 LevelGeom g, IngestBufs b, float* out_zero) {
+  // per-level grid in shared memory: indexed by a runtime level, the kernel-parameter copy
+  // would go through dynamically indexed constant loads
+  __shared__ double s_org[kMaxL][3], s_inv[kMaxL][3];
+  __shared__ int32_t s_dim[kMaxL][3];
+  __shared__ int64_t s_coff[kMaxL];
+  if (threadIdx.x < kMaxL * 3) {
+    const int l = threadIdx.x / 3, a = threadIdx.x % 3;
+    s_org[l][a] = g.origin[l][a]; s_inv[l][a] = g.inv_cell[l][a]; s_dim[l][a] = g.dims[l][a];
+    if (a == 0) s_coff[l] = g.coff[l];
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -38,7 +49,14 @@ __global__ void __launch_bounds__(256) k_keys(const float* __restrict__ pos, con
       int l = level_fixed;
       if (level_fixed < 0) { ok = ok && n[u] >= 1; l = min(n[u], g.L) - 1; }
       if (rgb) ok = ok && isfinite(c[u][0]) && isfinite(c[u][1]) && isfinite(c[u][2]);
-      key[u] = ok ? (uint32_t)sample_cell(g, l, x[u], y[u], z[u]) : kInvalidKey;
+      if (ok) {
+        const int32_t c0 = clampcell(floor(__dmul_rn(__dsub_rn((double)x[u], s_org[l][0]), s_inv[l][0])), s_dim[l][0]);
+        const int32_t c1 = clampcell(floor(__dmul_rn(__dsub_rn((double)y[u], s_org[l][1]), s_inv[l][1])), s_dim[l][1]);
+        const int32_t c2 = clampcell(floor(__dmul_rn(__dsub_rn((double)z[u], s_org[l][2]), s_inv[l][2])), s_dim[l][2]);
+        key[u] = (uint32_t)(s_coff[l] + ((int64_t)c2 * s_dim[l][1] + c1) * s_dim[l][0] + c0);
+      } else {
+        key[u] = kInvalidKey;
+      }
       if (!ok && out_zero && i < S) { out_zero[3 * i] = 0.f; out_zero[3 * i + 1] = 0.f; out_zero[3 * i + 2] = 0.f; }
     }
     // all kU warp-aggregated atomics are issued before any result is consumed; counter
@@ -69,7 +87,7 @@ __global__ void __launch_bounds__(256) k_keys(const float* __restrict__ pos, con
   }
 }
 
-__global__ void __launch_bounds__(256) k_scatter(const float* __restrict__ pos, const float* __restrict__ rgb,
+__global__ void __launch_bounds__(256, 4) k_scatter(const float* __restrict__ pos, const float* __restrict__ rgb,
                                                  int64_t S, const uint32_t* __restrict__ cell_start, IngestBufs b) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t T = (int64_t)gridDim.x * blockDim.x;
@@ -116,7 +134,7 @@ __global__ void k_levels_of(const uint32_t* key, int64_t S, LevelGeom g, int32_t
   }
 }
 
-static int grid_for(int64_t n, int per_sm = 8) {
+static int grid_for(int64_t n, int per_sm = 12) {
   int64_t b = (n + 256 * kU - 1) / (256 * kU);
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * per_sm));
 }
