@@ -343,14 +343,15 @@ void orc_cull_ranges(int64_t G, const double* P, double tau, const double* origi
 }
 
 /* Is cell c (per-axis indices) within the sphere |x - mu|^2 <= r2 of a Gaussian?  Squared
- * distance from mu to the cell's box; border cells extend to infinity outwards (samples
- * outside the grid clamp into them, A17). */
+ * distance from mu to the cell's box [o + c*e, o + (c+1)*e] with e = 1/inv_cell; border
+ * cells extend to infinity outwards (samples outside the grid clamp into them, A17). */
 int orc_cell_hit(const double* mu, double r2, const int32_t* c, const double* origin,
                  const double* inv_cell, const int32_t* dims) {
   double D2 = 0.0;
   for (int a = 0; a < 3; ++a) {
-    double lo = c[a] == 0 ? -INFINITY : origin[a] + (double)c[a] / inv_cell[a];
-    double hi = c[a] == dims[a] - 1 ? INFINITY : origin[a] + (double)(c[a] + 1) / inv_cell[a];
+    double e = 1.0 / inv_cell[a];
+    double lo = c[a] == 0 ? -INFINITY : origin[a] + (double)c[a] * e;
+    double hi = c[a] == dims[a] - 1 ? INFINITY : origin[a] + (double)(c[a] + 1) * e;
     double d = mu[a] < lo ? lo - mu[a] : (mu[a] > hi ? mu[a] - hi : 0.0);
     D2 = D2 + d * d;
   }

@@ -136,7 +136,7 @@ __device__ void chain_rule(const float p[kNP], const float cg[12], float out[kNP
   out[P_C + 2] = p[P_C + 2] > 0.f ? wo * cg[11] : 0.f;
 }
 
-__global__ void __launch_bounds__(256) k_adamw(int64_t G, float* __restrict__ P, float* __restrict__ M,
+__global__ void __launch_bounds__(256, 3) k_adamw(int64_t G, float* __restrict__ P, float* __restrict__ M,
                                                float* __restrict__ V, float* __restrict__ grad,
                                                float4* rec, uint4* range, double* rad2, uint32_t* csr_count,
                                                float* dbg, const DevState* __restrict__ st, AdamHP hp,
