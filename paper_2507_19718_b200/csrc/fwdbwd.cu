@@ -59,21 +59,83 @@ __device__ __forceinline__ float cand_q(const Cand& g, float x, float y, float z
   return __fmaf_rn(w2, w2, __fmaf_rn(w1, w1, __fmul_rn(w0, w0)));
 }
 
-__device__ __forceinline__ void stage_chunk(ChunkSmem& w, const int32_t* __restrict__ csr_idx,
+// Stages one chunk and returns (warp-uniformly) whether every candidate is isotropic
+// (U = u I, exact for equal log-scales; the paper's setting).  Isotropic chunks use the
+// layout r0 = (mu - x_ref, tau^2/u^2), r1 = (-0.5 log2e u^2, v), r2.x = u^2, r3 as usual;
+// general chunks r0..r2 as documented on ChunkSmem.
+__device__ __forceinline__ bool stage_chunk(ChunkSmem& w, const int32_t* __restrict__ csr_idx,
                                             const float4* __restrict__ rec, int base, int kc, int lane,
-                                            float xr, float yr, float zr) {
+                                            float xr, float yr, float zr, float tau2) {
   __syncwarp();
+  float4 p = make_float4(0.f, 0.f, 0.f, 0.f), q = p, r = p;
+  int gid = 0;
   if (lane < kc) {
-    const int gid = __ldg(csr_idx + base + lane);
-    const float4 p = __ldg(rec + 3 * gid), q = __ldg(rec + 3 * gid + 1), r = __ldg(rec + 3 * gid + 2);
+    gid = __ldg(csr_idx + base + lane);
+    p = __ldg(rec + 3 * gid); q = __ldg(rec + 3 * gid + 1); r = __ldg(rec + 3 * gid + 2);
+  }
+  const bool iso = __all_sync(0xffffffffu, lane >= kc || (p.y == 0.f && p.z == 0.f && q.x == 0.f &&
+                                                           p.x == p.w && p.w == q.y));
+  if (lane < kc) {
     const float m0 = q.z - xr, m1 = q.w - yr, m2 = r.x - zr;
-    const float c0 = fmaf(p.z, m2, fmaf(p.y, m1, p.x * m0));
-    const float c1 = fmaf(q.x, m2, p.w * m1);
-    const float c2 = q.y * m2;
-    w.r0[lane] = p;
-    w.r1[lane] = make_float4(q.x, q.y, -c0, -c1);
-    w.r2[lane] = make_float4(-c2, r.y, r.z, r.w);
+    if (iso) {
+      const float u2 = p.x * p.x;
+      w.r0[lane] = make_float4(m0, m1, m2, tau2 / u2);
+      w.r1[lane] = make_float4(kNegHalfLog2e * u2, r.y, r.z, r.w);
+      w.r2[lane] = make_float4(u2, 0.f, 0.f, 0.f);
+    } else {
+      const float c0 = fmaf(p.z, m2, fmaf(p.y, m1, p.x * m0));
+      const float c1 = fmaf(q.x, m2, p.w * m1);
+      const float c2 = q.y * m2;
+      w.r0[lane] = p;
+      w.r1[lane] = make_float4(q.x, q.y, -c0, -c1);
+      w.r2[lane] = make_float4(-c2, r.y, r.z, r.w);
+    }
     w.r3[lane] = make_float4(m0, m1, m2, __int_as_float(gid));
+  }
+  __syncwarp();
+  return iso;
+}
+
+// Isotropic test value s = |x' - m|^2 (operation order fixed: every pass agrees).
+__device__ __forceinline__ float iso_s(const float (&x)[3], const float4& c) {
+  const float dx = __fsub_rn(x[0], c.x), dy = __fsub_rn(x[1], c.y), dz = __fsub_rn(x[2], c.z);
+  return __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+}
+
+// Isotropic chunk: s = |x' - m|^2 <= tau^2/u^2, e = 2^{-0.5 log2e u^2 s} (7 ops per test).
+template <bool kRecord>
+__device__ __forceinline__ void eval_chunk_iso(const ChunkSmem& w, int kc, const float (&xa)[3], const float (&xb)[3],
+                                               float (&ya)[3], float (&yb)[3], uint16_t* pkey, float* pe,
+                                               int& pbase, int cap, int lane) {
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll 2
+  for (int k = 0; k < kc; ++k) {
+    const float4 c = w.r0[k], f = w.r1[k];
+    const float sa = iso_s(xa, c), sb = iso_s(xb, c);
+    const bool ina = sa <= c.w, inb = sb <= c.w;
+    if (!kRecord) {
+      if (__any_sync(0xffffffffu, ina || inb)) {
+        if (ina) { const float e = ex2_approx(f.x * sa); ya[0] = fmaf(f.y, e, ya[0]); ya[1] = fmaf(f.z, e, ya[1]); ya[2] = fmaf(f.w, e, ya[2]); }
+        if (inb) { const float e = ex2_approx(f.x * sb); yb[0] = fmaf(f.y, e, yb[0]); yb[1] = fmaf(f.z, e, yb[1]); yb[2] = fmaf(f.w, e, yb[2]); }
+      }
+      continue;
+    }
+    const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = __ballot_sync(0xffffffffu, inb);
+    if (ma | mb) {
+      if (ina) {
+        const float e = ex2_approx(f.x * sa);
+        ya[0] = fmaf(f.y, e, ya[0]); ya[1] = fmaf(f.z, e, ya[1]); ya[2] = fmaf(f.w, e, ya[2]);
+        const int pos = pbase + __popc(ma & lt);
+        if (pos < cap) { pkey[pos] = (uint16_t)((k << 6) | lane); pe[pos] = e; }
+      }
+      if (inb) {
+        const float e = ex2_approx(f.x * sb);
+        yb[0] = fmaf(f.y, e, yb[0]); yb[1] = fmaf(f.z, e, yb[1]); yb[2] = fmaf(f.w, e, yb[2]);
+        const int pos = pbase + __popc(ma) + __popc(mb & lt);
+        if (pos < cap) { pkey[pos] = (uint16_t)((k << 6) | (lane + 32)); pe[pos] = e; }
+      }
+      pbase += __popc(ma) + __popc(mb);
+    }
   }
   __syncwarp();
 }
@@ -83,7 +145,7 @@ __device__ __forceinline__ void stage_chunk(ChunkSmem& w, const int32_t* __restr
 // (candidate-major; sample a's before sample b's), up to `cap`; pbase advances regardless.
 template <bool kRecord>
 __device__ __forceinline__ void eval_chunk(const ChunkSmem& w, int kc, const float (&xa)[3], const float (&xb)[3],
-                                           float tau2, float (&ya)[3], float (&yb)[3], int& np,
+                                           float tau2, float (&ya)[3], float (&yb)[3],
                                            uint16_t* pkey, float* pe, int& pbase, int cap, int lane) {
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll 2
@@ -93,12 +155,18 @@ __device__ __forceinline__ void eval_chunk(const ChunkSmem& w, int kc, const flo
     const float Qa = cand_q(g, xa[0], xa[1], xa[2], w0, w1, w2);
     const float Qb = cand_q(g, xb[0], xb[1], xb[2], w0, w1, w2);
     const bool ina = Qa <= tau2, inb = Qb <= tau2;
+    if (!kRecord) {
+      if (__any_sync(0xffffffffu, ina || inb)) {
+        if (ina) { const float e = ex2_approx(Qa * kNegHalfLog2e); ya[0] = fmaf(g.v0, e, ya[0]); ya[1] = fmaf(g.v1, e, ya[1]); ya[2] = fmaf(g.v2, e, ya[2]); }
+        if (inb) { const float e = ex2_approx(Qb * kNegHalfLog2e); yb[0] = fmaf(g.v0, e, yb[0]); yb[1] = fmaf(g.v1, e, yb[1]); yb[2] = fmaf(g.v2, e, yb[2]); }
+      }
+      continue;
+    }
     const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = __ballot_sync(0xffffffffu, inb);
     if (ma | mb) {
       if (ina) {
         const float e = ex2_approx(Qa * kNegHalfLog2e);
         ya[0] = fmaf(g.v0, e, ya[0]); ya[1] = fmaf(g.v1, e, ya[1]); ya[2] = fmaf(g.v2, e, ya[2]);
-        ++np;
         if (kRecord) {
           const int pos = pbase + __popc(ma & lt);
           if (pos < cap) { pkey[pos] = (uint16_t)((k << 6) | lane); pe[pos] = e; }
@@ -107,7 +175,6 @@ __device__ __forceinline__ void eval_chunk(const ChunkSmem& w, int kc, const flo
       if (inb) {
         const float e = ex2_approx(Qb * kNegHalfLog2e);
         yb[0] = fmaf(g.v0, e, yb[0]); yb[1] = fmaf(g.v1, e, yb[1]); yb[2] = fmaf(g.v2, e, yb[2]);
-        ++np;
         if (kRecord) {
           const int pos = pbase + __popc(ma) + __popc(mb & lt);
           if (pos < cap) { pkey[pos] = (uint16_t)((k << 6) | (lane + 32)); pe[pos] = e; }
@@ -123,7 +190,7 @@ __device__ __forceinline__ void eval_chunk(const ChunkSmem& w, int kc, const flo
 // gradients (C5), a <= 2-level segmented shuffle scan over each Gaussian's run of pairs,
 // then red.global.add.v4.f32 from every 4th lane of a run counted from its end.
 __device__ __forceinline__ void chunk_pairs_bwd(const WarpSmem& w, int p0, int p1, float* __restrict__ grad,
-                                                int lane) {
+                                                int lane, bool iso) {
   for (int pb = p0; pb < p1; pb += 32) {
     const int p = pb + lane;
     const bool valid = p < p1;
@@ -137,18 +204,27 @@ __device__ __forceinline__ void chunk_pairs_bwd(const WarpSmem& w, int p0, int p
       const float e = w.pe[p];
       k = key >> 6;
       const int s = key & 63;
-      const Cand g = cand_from(w, k);
       const float4 mu = w.r3[k];
       gid = __float_as_int(mu.w);
       const float4 sx = w.sxg[s];
       const float2 sg = w.sg[s];
-      float w0, w1, w2;
-      cand_q(g, sx.x, sx.y, sx.z, w0, w1, w2);
-      const float tx = g.u00 * w0;                                   // t = A d = U^T w
-      const float ty = fmaf(g.u11, w1, g.u01 * w0);
-      const float tz = fmaf(g.u22, w2, fmaf(g.u12, w1, g.u02 * w0));
       const float dx = sx.x - mu.x, dy = sx.y - mu.y, dz = sx.z - mu.z;
-      const float he = (sx.w * g.v0 + sg.x * g.v1 + sg.y * g.v2) * e;
+      float tx, ty, tz, v0, v1, v2;
+      if (iso) {                                                     // t = A d = u^2 d
+        const float u2 = w.r2[k].x;
+        const float4 f = w.r1[k];
+        tx = u2 * dx; ty = u2 * dy; tz = u2 * dz;
+        v0 = f.y; v1 = f.z; v2 = f.w;
+      } else {                                                       // t = A d = U^T w
+        const Cand g = cand_from(w, k);
+        float w0, w1, w2;
+        cand_q(g, sx.x, sx.y, sx.z, w0, w1, w2);
+        tx = g.u00 * w0;
+        ty = fmaf(g.u11, w1, g.u01 * w0);
+        tz = fmaf(g.u22, w2, fmaf(g.u12, w1, g.u02 * w0));
+        v0 = g.v0; v1 = g.v1; v2 = g.v2;
+      }
+      const float he = (sx.w * v0 + sg.x * v1 + sg.y * v2) * e;
       v[0] = he * tx; v[1] = he * ty; v[2] = he * tz;                 // d mu
       const float kk = -0.5f * he;
       const float kx = kk * dx, ky = kk * dy, kz = kk * dz;
@@ -238,14 +314,17 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
     xb[0] -= xref; xb[1] -= yref; xb[2] -= zref;
     // ---------------- pass 1 (records the inside pairs while they fit)
     float ya[3] = {0.f, 0.f, 0.f}, yb[3] = {0.f, 0.f, 0.f};
-    int np = 0, pbase = 0;
+    int pbase = 0;
+    bool iso = false;
     const bool chunks_fit = C <= 32 * kMaxChunks;
     for (int cb = 0, c = 0; cb < C; cb += 32, ++c) {
       const int kc = min(32, C - cb);
-      stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref);
-      eval_chunk<true>(w, kc, xa, xb, tau2, ya, yb, np, w.pkey, w.pe, pbase, kPairCap, lane);
+      iso = stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref, tau2);
+      if (iso) eval_chunk_iso<true>(w, kc, xa, xb, ya, yb, w.pkey, w.pe, pbase, kPairCap, lane);
+      else eval_chunk<true>(w, kc, xa, xb, tau2, ya, yb, w.pkey, w.pe, pbase, kPairCap, lane);
       if (lane == 0 && c < kMaxChunks) w.cend[c] = (uint16_t)min(pbase, 0xFFFF);
     }
+    const int np = pbase;                        // inside pairs of the item (warp-uniform)
     const bool recorded = chunks_fit && pbase <= kPairCap;
     // ---------------- Eq. 4 loss and dL/dyhat (unnormalised)
     float ga[3] = {0.f, 0.f, 0.f}, gb[3] = {0.f, 0.f, 0.f}, ls = 0.f;
@@ -256,10 +335,7 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
     w.sxg[lane + 32] = make_float4(xb[0], xb[1], xb[2], gb[0]);
     w.sg[lane + 32] = make_float2(gb[1], gb[2]);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      ls += __shfl_xor_sync(0xffffffffu, ls, o);
-      np += __shfl_xor_sync(0xffffffffu, np, o);
-    }
+    for (int o = 16; o > 0; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
     if (lane == 0) s_loss[wid][wi.level] += (double)ls;
     pairs_acc += (unsigned)np;
     cand_acc += (unsigned long long)wi.count * (unsigned long long)C;
@@ -271,8 +347,8 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
       for (int cb = 0, c = 0; cb < C; cb += 32, ++c) {
         const int pend = w.cend[c];
         if (pend == pstart) continue;
-        if (C > 32) stage_chunk(w, a.csr_idx, a.rec, lo + cb, min(32, C - cb), lane, xref, yref, zref);
-        chunk_pairs_bwd(w, pstart, pend, a.grad, lane);
+        if (C > 32) iso = stage_chunk(w, a.csr_idx, a.rec, lo + cb, min(32, C - cb), lane, xref, yref, zref, tau2);
+        chunk_pairs_bwd(w, pstart, pend, a.grad, lane, iso);
         pstart = pend;
       }
     } else {
@@ -280,31 +356,41 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
       const uint32_t lt = (1u << lane) - 1u;
       for (int cb = 0; cb < C; cb += 32) {
         const int kc = min(32, C - cb);
-        stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref);
+        const bool ci = stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref, tau2);
         int pb = 0;
         for (int k = 0; k < kc; ++k) {
-          const Cand g = cand_from(w, k);
-          float w0, w1, w2;
-          const float Qa = cand_q(g, xa[0], xa[1], xa[2], w0, w1, w2);
-          const float Qb = cand_q(g, xb[0], xb[1], xb[2], w0, w1, w2);
-          const bool ina = Qa <= tau2, inb = Qb <= tau2;
+          float Qa, Qb, ea, eb;                    // same arithmetic as eval_chunk[_iso]
+          bool ina, inb;
+          if (ci) {
+            const float4 cc = w.r0[k], f = w.r1[k];
+            Qa = iso_s(xa, cc); Qb = iso_s(xb, cc);
+            ina = Qa <= cc.w; inb = Qb <= cc.w;
+            ea = ex2_approx(f.x * Qa); eb = ex2_approx(f.x * Qb);
+          } else {
+            const Cand g = cand_from(w, k);
+            float w0, w1, w2;
+            Qa = cand_q(g, xa[0], xa[1], xa[2], w0, w1, w2);
+            Qb = cand_q(g, xb[0], xb[1], xb[2], w0, w1, w2);
+            ina = Qa <= tau2; inb = Qb <= tau2;
+            ea = ex2_approx(Qa * kNegHalfLog2e); eb = ex2_approx(Qb * kNegHalfLog2e);
+          }
           const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = __ballot_sync(0xffffffffu, inb);
           if (!(ma | mb)) continue;
-          if (pb + 64 > kPairCap) { chunk_pairs_bwd(w, 0, pb, a.grad, lane); pb = 0; }
+          if (pb + 64 > kPairCap) { chunk_pairs_bwd(w, 0, pb, a.grad, lane, ci); pb = 0; }
           if (ina) {
             const int pos = pb + __popc(ma & lt);
             w.pkey[pos] = (uint16_t)((k << 6) | lane);
-            w.pe[pos] = ex2_approx(Qa * kNegHalfLog2e);
+            w.pe[pos] = ea;
           }
           if (inb) {
             const int pos = pb + __popc(ma) + __popc(mb & lt);
             w.pkey[pos] = (uint16_t)((k << 6) | (lane + 32));
-            w.pe[pos] = ex2_approx(Qb * kNegHalfLog2e);
+            w.pe[pos] = eb;
           }
           pb += __popc(ma) + __popc(mb);
           __syncwarp();
         }
-        chunk_pairs_bwd(w, 0, pb, a.grad, lane);
+        chunk_pairs_bwd(w, 0, pb, a.grad, lane, ci);
       }
     }
   }
@@ -348,11 +434,13 @@ __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
     xa[0] -= xref; xa[1] -= yref; xa[2] -= zref;
     xb[0] -= xref; xb[1] -= yref; xb[2] -= zref;
     float ya[3] = {0.f, 0.f, 0.f}, yb[3] = {0.f, 0.f, 0.f};
-    int np = 0, pbase = 0;
+    int pbase = 0;
     for (int cb = 0; cb < C; cb += 32) {
       const int kc = min(32, C - cb);
-      stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref);
-      eval_chunk<false>(w, kc, xa, xb, tau2, ya, yb, np, nullptr, nullptr, pbase, 0, lane);
+      if (stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref, tau2))
+        eval_chunk_iso<false>(w, kc, xa, xb, ya, yb, nullptr, nullptr, pbase, 0, lane);
+      else
+        eval_chunk<false>(w, kc, xa, xb, tau2, ya, yb, nullptr, nullptr, pbase, 0, lane);
     }
     if (lane < wi.count) {
       const int64_t i = __float_as_uint(pa.w);

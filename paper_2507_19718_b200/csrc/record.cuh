@@ -34,11 +34,17 @@ __device__ __forceinline__ void make_record(const float p[kNP], float4 out[3]) {
   for (int a = 0; a < 3; ++a)
 #pragma unroll
     for (int b = a; b < 3; ++b) A[a][b] = R[a][0] * R[b][0] * D0 + R[a][1] * R[b][1] * D1 + R[a][2] * R[b][2] * D2;
-  const double U00 = sqrt(A[0][0]);
-  const double U01 = A[0][1] / U00, U02 = A[0][2] / U00;
-  const double U11 = sqrt(fmax(A[1][1] - U01 * U01, 1e-300));
-  const double U12 = (A[1][2] - U01 * U02) / U11;
-  const double U22 = sqrt(fmax(A[2][2] - U02 * U02 - U12 * U12, 1e-300));
+  double U00 = sqrt(A[0][0]);
+  double U01 = A[0][1] / U00, U02 = A[0][2] / U00;
+  double U11 = sqrt(fmax(A[1][1] - U01 * U01, 1e-300));
+  double U12 = (A[1][2] - U01 * U02) / U11;
+  double U22 = sqrt(fmax(A[2][2] - U02 * U02 - U12 * U12, 1e-300));
+  if (p[P_S] == p[P_S + 1] && p[P_S + 1] == p[P_S + 2]) {
+    // isotropic: A = e^{-2s} R R^T = e^{-2s} I exactly, U = e^{-s} I (the rotation drops
+    // out); with the paper's scale LR of 0 and isotropic Eq. 2 init every Gaussian stays here
+    U00 = U11 = U22 = sqrt(D0);
+    U01 = U02 = U12 = 0.0;
+  }
   const float wo = 1.f / (1.f + expf(-p[P_O]));
   out[0] = make_float4((float)U00, (float)U01, (float)U02, (float)U11);
   out[1] = make_float4((float)U12, (float)U22, p[P_MU], p[P_MU + 1]);
