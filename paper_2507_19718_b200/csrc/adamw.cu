@@ -16,6 +16,7 @@ __global__ void __launch_bounds__(kPart * 32) k_stats(const double* __restrict__
                                                       int64_t S, LvlStats* lvl) {
   const int lane = threadIdx.x & 31, col = threadIdx.x >> 5;
   double acc = 0.0;
+#pragma unroll 8
   for (int b = lane; b < nblocks; b += 32) acc += __ldg(partial + (int64_t)b * kPart + col);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -42,38 +43,47 @@ struct StepHP {
   float lr[GC_NGROUPS]; float beta1, beta2; int schedule; int L;
 };
 
-// One thread: Eq. 5 schedule, per-level skip (A12), bias corrections, stats.
+// One warp: Eq. 5 schedule, per-level skip (A12), bias corrections, stats.  Lane l
+// owns level l; beta^step is a running product (no pow on the critical path).
 __global__ void k_step_scalars(const LvlStats* __restrict__ lvl, DevState* st, StepHP hp,
                                gc_fit_stats* out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int lane = threadIdx.x;
   double tot = 0.0;
   for (int l = 0; l < hp.L; ++l) tot += lvl->count[l];
   const int stepped = tot > 0.0;
-  st->stepped = stepped;
-  st->nonfinite = 0ull;
-  if (stepped) st->t += 1;
-  const double t = (double)st->t;
-  for (int k = 0; k < GC_NGROUPS; ++k)
-    st->eta[k] = hp.schedule ? (float)((double)hp.lr[k] / (1.0 + log(t))) : hp.lr[k];
-  for (int l = 0; l < kMaxL; ++l) {
+  const long long t = st->t + stepped;
+  __syncwarp();
+  if (lane < GC_NGROUPS)
+    st->eta[lane] = hp.schedule ? (float)((double)hp.lr[lane] / (1.0 + log((double)t))) : hp.lr[lane];
+  if (lane < kMaxL) {
+    const int l = lane;
     const double k = l < hp.L ? lvl->count[l] : 0.0;
     const int act = stepped && k > 0.0;
     st->active[l] = act;
-    if (act) st->adam_step[l] += 1;
-    const double n = (double)st->adam_step[l];
-    st->bc1[l] = (float)(1.0 - pow((double)hp.beta1, n));
-    st->bc2[l] = (float)(1.0 - pow((double)hp.beta2, n));
+    double p1 = st->b1pow[l], p2 = st->b2pow[l];
+    if (act) {
+      st->adam_step[l] += 1;
+      p1 *= (double)hp.beta1; p2 *= (double)hp.beta2;
+      st->b1pow[l] = p1; st->b2pow[l] = p2;
+    }
+    st->bc1[l] = (float)(1.0 - p1);
+    st->bc2[l] = (float)(1.0 - p2);
     st->inv3k[l] = act ? (float)(1.0 / (3.0 * k)) : 0.f;
     out->count[l] = (int64_t)k;
     out->loss[l] = k > 0.0 ? lvl->loss_sum[l] / (3.0 * k) : 0.0;
   }
-  out->n_in = (int64_t)lvl->n_in;
-  out->n_valid = (int64_t)lvl->n_valid;
-  out->n_dropped = (int64_t)(lvl->n_in - lvl->n_valid);
-  out->step = stepped ? st->t : 0;
-  out->nonfinite_grads = 0;
-  out->n_pairs = (int64_t)lvl->n_pairs;
-  out->n_candidates = (int64_t)lvl->n_cand;
+  if (lane == 0) {
+    st->stepped = stepped;
+    st->nonfinite = 0ull;
+    st->t = t;
+    out->n_in = (int64_t)lvl->n_in;
+    out->n_valid = (int64_t)lvl->n_valid;
+    out->n_dropped = (int64_t)(lvl->n_in - lvl->n_valid);
+    out->step = stepped ? t : 0;
+    out->nonfinite_grads = 0;
+    out->n_pairs = (int64_t)lvl->n_pairs;
+    out->n_candidates = (int64_t)lvl->n_cand;
+  }
 }
 
 struct AdamHP {

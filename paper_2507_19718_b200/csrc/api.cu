@@ -260,6 +260,12 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
   CK(dalloc(&c->rec, 3 * G)); CK(dalloc(&c->grad, 12 * G)); CK(dalloc(&c->range, G)); CK(dalloc(&c->rad2, G));
   CK(cudaMemset(c->grad, 0, sizeof(float) * 12 * G));
   CK(dalloc(&c->st, 1)); CK(cudaMemset(c->st, 0, sizeof(DevState)));
+  {
+    DevState h0;
+    memset(&h0, 0, sizeof h0);
+    for (int l = 0; l < kMaxL; ++l) { h0.b1pow[l] = 1.0; h0.b2pow[l] = 1.0; }
+    CK(cudaMemcpy(c->st, &h0, sizeof h0, cudaMemcpyHostToDevice));
+  }
   CK(dalloc(&c->lvl, 1)); CK(dalloc(&c->dstats, 1)); CK(cudaMemset(c->dstats, 0, sizeof(gc_fit_stats)));
   CK(cudaHostAlloc((void**)&c->hstats, sizeof(gc_fit_stats), cudaHostAllocDefault));
 
@@ -552,6 +558,9 @@ gc_status gc_set_params(gc_cache c, int level, const gc_level_params* src, int r
       CK(cudaMemsetAsync(c->V + k * c->G + b, 0, sizeof(float) * n, s));
     }
     CK(cudaMemsetAsync(&c->st->adam_step[level], 0, sizeof(long long), s));
+    static const double one = 1.0;   // beta^0 (pageable source: the copy completes before return)
+    CK(cudaMemcpyAsync(&c->st->b1pow[level], &one, sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(&c->st->b2pow[level], &one, sizeof(double), cudaMemcpyHostToDevice, s));
   }
   return rebuild_csr(c, s, true);
 }

@@ -32,6 +32,7 @@ struct LevelGeom {
 struct DevState {
   long long t;                       // Eq. 5 counter: stepping fits since create / reset
   long long adam_step[kMaxL];        // per-level AdamW bias-correction counters (A12)
+  double b1pow[kMaxL], b2pow[kMaxL]; // beta^adam_step, kept as running products
   float eta[GC_NGROUPS];             // eta_g(t) of the current step
   float bc1[kMaxL], bc2[kMaxL];      // 1 - beta^step per level (current step)
   float inv3k[kMaxL];                // 1 / (3 k_l) (0 when the level is skipped)
