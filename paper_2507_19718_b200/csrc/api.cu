@@ -340,6 +340,7 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
       c->geom.origin[l][a] = lo[a];
       c->geom.dims[l][a] = dims[a];
       c->geom.inv_cell[l][a] = (double)dims[a] / ext[a];
+      c->geom.edge[l][a] = 1.0 / c->geom.inv_cell[l][a];
     }
     c->geom.coff[l + 1] = c->geom.coff[l] + (int64_t)dims[0] * dims[1] * dims[2];
   }
@@ -461,15 +462,21 @@ gc_status gc_fit(gc_cache c, const float* pos, const int32_t* path_len, const fl
   fa.grad = c->grad; fa.partial = c->partial;
   const float tau = c->hp.cutoff_sigma;
   fa.tau2 = tau * tau; fa.hdr_eps = c->hp.hdr_eps; fa.mode = c->hp.loss_grad_mode; fa.L = c->L;
+  const bool dp = c->comm != nullptr;
+  fa.fused = 0;   // last-CTA stats tail: measured 16 us slower than the two small kernels; off
+  fa.cell_start = F.cell_start; fa.S = S; fa.lvl = c->lvl; fa.st = c->st; fa.dstats = c->dstats;
+  fa.geom = c->geom;
+  for (int k = 0; k < GC_NGROUPS; ++k) fa.shp.lr[k] = c->hp.lr[k];
+  fa.shp.beta1 = c->hp.beta1; fa.shp.beta2 = c->hp.beta2; fa.shp.schedule = c->hp.lr_schedule; fa.shp.L = c->L;
   launch_fwdbwd(fa, c->fb_grid, s, &c->prof);
-  launch_stats(c->partial, c->fb_grid, F.cell_start, c->geom, S, c->lvl, s, &c->prof);
-  if (c->comm) {                   // data parallel: one sum over ranks of grads + level stats
+  if (!fa.fused) launch_stats(c->partial, c->fb_grid, F.cell_start, c->geom, S, c->lvl, s, &c->prof);
+  if (dp) {                         // data parallel: one sum over ranks of grads + level stats
     NK(ncclGroupStart());
     NK(ncclAllReduce(c->grad, c->grad, (size_t)12 * c->G, ncclFloat32, ncclSum, c->comm, s));
     NK(ncclAllReduce(c->lvl, c->lvl, sizeof(LvlStats) / sizeof(double), ncclFloat64, ncclSum, c->comm, s));
     NK(ncclGroupEnd());
   }
-  launch_step_scalars(c->lvl, c->st, c->hp, c->L, c->dstats, s);
+  if (!fa.fused) launch_step_scalars(c->lvl, c->st, c->hp, c->L, c->dstats, s);
   launch_adamw(c->G, c->P, c->M, c->V, c->grad, c->rec, c->range, c->rad2, c->csr_count, c->dbg_on ? c->dbg : nullptr,
                c->st, c->hp, c->geom, c->dstats, s, &c->prof);
   if (gc_status e = rebuild_csr(c, s, false)) return e;

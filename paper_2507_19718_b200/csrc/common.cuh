@@ -25,6 +25,7 @@ struct LevelGeom {
   int64_t coff[kMaxL + 1];           // cell offsets of each level's grid in the global cell ids
   double origin[kMaxL][3];
   double inv_cell[kMaxL][3];
+  double edge[kMaxL][3];             // 1.0 / inv_cell (IEEE division on the host, as the oracle)
   int32_t dims[kMaxL][3];
 };
 
@@ -41,6 +42,7 @@ struct DevState {
   unsigned long long nonfinite;      // non-finite gradient elements skipped (this call)
   unsigned int csr_total;            // culling-list entries of the current CSR
   unsigned int csr_overflow;         // sticky: a rebuild exceeded the list capacity
+  unsigned int done;                 // CTA completion counter of the fused fwd/bwd tail
 };
 
 // Per-call level statistics; summed over ranks under data parallelism (all doubles so a

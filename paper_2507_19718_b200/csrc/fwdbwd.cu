@@ -16,10 +16,10 @@
 //          contributing pairs; never shared-memory float atomics (a CAS loop on sm_100a).
 #include "common.cuh"
 #include "kernels.h"
+#include "stats.cuh"
 
 namespace gsc {
 
-constexpr int kPart = kMaxL + 2;
 constexpr int kWarps = 8;                                 // warps per CTA
 constexpr int kPairCap = 512;                             // recorded (sample, Gaussian) pairs per warp
 constexpr int kMaxChunks = 64;                            // recorded chunks per work item (C <= 2048)
@@ -408,6 +408,20 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
     part[kMaxL] = (double)p;
     part[kMaxL + 1] = (double)c;
   }
+  if (!a.fused) return;
+  // single GPU: the last CTA to finish reduces the statistics and takes the step scalars
+  // (saves two dependent launches; under data parallelism an all-reduce sits in between)
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&a.st->done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  stats_reduce(a.partial, gridDim.x, a.cell_start, a.geom, a.S, a.lvl, wid, kWarps, lane);
+  __syncthreads();
+  if (wid == 0) step_scalars_warp(a.lvl, a.st, a.shp, a.dstats, lane);
+  if (threadIdx.x == 0) a.st->done = 0u;
 }
 
 __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "stats.cuh"
 
 namespace gsc {
 
@@ -92,6 +93,9 @@ struct FitArgs {
   float* grad;          // [G][12]
   double* partial;      // [grid][kMaxL + 2]: per-block loss sums, pairs, candidates
   float tau2, hdr_eps; int mode; int L;
+  // fused statistics + step scalars in the last CTA (single GPU)
+  int fused; const uint32_t* cell_start; int64_t S; LvlStats* lvl; DevState* st; StepHP shp;
+  gc_fit_stats* dstats; LevelGeom geom;
 };
 int fwdbwd_grid();
 void launch_fwdbwd(const FitArgs& a, int grid, cudaStream_t s, Profiler* prof);

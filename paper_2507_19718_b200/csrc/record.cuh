@@ -105,7 +105,7 @@ __device__ __forceinline__ void cull_range(const float p[kNP], double tau, const
 // d_a = dist(mu_a, [o_a + c_a e_a, o_a + (c_a+1) e_a]), e_a = 1/inv_a, D2 = (d_x^2 + d_y^2) + d_z^2;
 // the same per-axis terms are tabulated here once per Gaussian (bit-identical doubles).
 __device__ __forceinline__ double axis_d2(double mu, int32_t c, const LevelGeom& g, int l, int a) {
-  const double e = __ddiv_rn(1.0, g.inv_cell[l][a]);      // cell edge (same rounding as the oracle)
+  const double e = g.edge[l][a];                          // 1.0 / inv_cell (same rounding as the oracle)
   const double lo = c == 0 ? -INFINITY : __dadd_rn(g.origin[l][a], __dmul_rn((double)c, e));
   const double hi = c == g.dims[l][a] - 1 ? INFINITY : __dadd_rn(g.origin[l][a], __dmul_rn((double)(c + 1), e));
   const double d = mu < lo ? __dsub_rn(lo, mu) : (mu > hi ? __dsub_rn(mu, hi) : 0.0);
