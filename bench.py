@@ -176,7 +176,7 @@ def run_ours(args):
     S = c["S"]
     pos, alb = workload.init_cloud(cfg)
     cache = gsc.GSCache(counts, torch.from_numpy(pos).to(dev), torch.from_numpy(alb).to(dev),
-                        seed=cfg, device=local)
+                        seed=cfg, device=local, hparams=dict(cell_edge_scale=args.cell_scale))
     if world > 1:
         uid = [gsc.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -368,6 +368,7 @@ def main():
     ap.add_argument("--cpu-samples", type=int, default=200_000)
     ap.add_argument("--ref-samples", type=int, default=100_000)
     ap.add_argument("--clock-window", type=float, default=2.0)
+    ap.add_argument("--cell-scale", type=float, default=1.0, help="culling-grid cell edge multiplier")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -56,6 +56,7 @@ typedef struct {
   float init_scale_factor;         /* 0.5 ("scales ... to 50%")                              */
   float init_zcap;                 /* 2.0 ("z-score greater than 2")                         */
   int cells_per_axis[GC_MAX_LEVELS]; /* culling grid resolution; 0 = auto rule (C8)             */
+  float cell_edge_scale;           /* auto rule: cell edge = scale * 2 tau mean(e^s); default 1     */
 } gc_hparams;
 
 /* Per-call statistics.  Written asynchronously: valid once the stream has synchronised. */

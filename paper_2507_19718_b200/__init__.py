@@ -42,7 +42,7 @@ class gc_hparams(C.Structure):
                 ("hdr_eps", C.c_float), ("loss_grad_mode", C.c_int), ("lr_schedule", C.c_int),
                 ("cutoff_sigma", C.c_float), ("init_opacity", C.c_float),
                 ("init_scale_factor", C.c_float), ("init_zcap", C.c_float),
-                ("cells_per_axis", C.c_int * MAX_LEVELS)]
+                ("cells_per_axis", C.c_int * MAX_LEVELS), ("cell_edge_scale", C.c_float)]
 
 
 class gc_fit_stats(C.Structure):

@@ -221,7 +221,7 @@ void gc_default_hparams(gc_hparams* hp) {
   for (int k = 0; k < GC_NGROUPS; ++k) { hp->lr[k] = lr[k]; hp->weight_decay[k] = wd[k]; }
   hp->beta1 = 0.9f; hp->beta2 = 0.999f; hp->adam_eps = 1e-8f; hp->hdr_eps = 0.01f;
   hp->loss_grad_mode = 0; hp->lr_schedule = 1; hp->cutoff_sigma = 3.f; hp->init_opacity = 0.1f;
-  hp->init_scale_factor = 0.5f; hp->init_zcap = 2.f;
+  hp->init_scale_factor = 0.5f; hp->init_zcap = 2.f; hp->cell_edge_scale = 1.f;
 }
 
 static uint64_t splitmix64(uint64_t x) {
@@ -323,7 +323,8 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
     if (fixed > 0) {
       for (int a = 0; a < 3; ++a) dims[a] = std::min(fixed, 4096);
     } else {
-      double edge = std::isfinite(tau) ? 2.0 * tau * ms : INFINITY;
+      const double esc = c->hp.cell_edge_scale > 0.f ? (double)c->hp.cell_edge_scale : 1.0;
+      double edge = std::isfinite(tau) ? esc * 2.0 * tau * ms : INFINITY;
       if (!(edge > 0.0)) edge = INFINITY;
       for (int it = 0; it < 200; ++it) {
         int64_t prod = 1;
