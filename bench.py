@@ -270,11 +270,18 @@ def run_ours(args):
     top = max(prof, key=lambda k: prof[k][0])
     n_pairs, n_cand = int(st.n_pairs), int(st.n_candidates)
     pk, pk_kind = peaks()
+    traffic = None
+    try:   # per-launch DRAM bytes of the dominant kernel from the committed ncu capture
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            traffic = json.load(f).get("gsc::k_" + top)
+    except Exception:
+        pass
     if top == "fwdbwd":
         flops = (n_pairs / world) * FLOPS_PER_PAIR + n_valid_local * FLOPS_PER_SAMPLE
         achieved = flops / (kernel_ms[top] * 1e-3) / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP32_PEAK_TFLOPS, "traffic": None, "kernel": top,
+                "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic, "kernel": top,
+                "traffic_source": "profiles/r01_traffic.json (ncu dram__bytes_read+write per launch)",
                 "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (B200_PROFILING.md counts/clock)",
                 "algorithmic": f"{FLOPS_PER_PAIR:.0f} flop/contributing pair + {FLOPS_PER_SAMPLE:.0f}/sample"}
     else:
