@@ -123,6 +123,19 @@ gc_status gc_fit(gc_cache c, const float* pos, const int32_t* path_len, const fl
 gc_status gc_query(gc_cache c, const float* pos, const int32_t* path_len, int level, int64_t S,
                    float* out_rgb, gc_stream stream);
 
+/* Cache lookup with the renderer-side epilogue (next-row f3): for every valid point i
+ *   out_rgb[i] = unbiased_rgb[i]                        if unbiased_rgb[i] != 0 (any channel):
+ *                natural termination keeps a path's own non-zero radiance (sec.3.3.1);
+ *              = yhat_l(x_i) * attenuation[i] / beta[i]  otherwise: Eq. 3, the cached
+ *                radiance times the path throughput prod sigma_k divided by the cascaded
+ *                cache-miss probability beta_{n-1} (sec.3.4.2).
+ *  attenuation [S][3] (NULL = 1), beta [S] (NULL = 1), unbiased_rgb [S][3] (NULL = none): host
+ *  or device.  Points with path_len <= 0 or non-finite position get 0.  Same evaluator and
+ *  binning as gc_query. */
+gc_status gc_query_radiance(gc_cache c, const float* pos, const int32_t* path_len, int level,
+                            int64_t S, const float* attenuation, const float* beta,
+                            const float* unbiased_rgb, float* out_rgb, gc_stream stream);
+
 /* Copy out (gc_params) / in (gc_set_params) the raw parameters of one level in the paper's
  * layout.  dst/src arrays: host or device, `count` must equal the level's size.
  * gc_set_params rebuilds the level's evaluation records and culling lists; reset_adam != 0

@@ -229,6 +229,22 @@ def query(goff, P, x, length=None, level=-1, tau=3.0, grids=None):
     return y, lv, npairs.value
 
 
+def query_radiance(yhat, attenuation=None, beta=None, unbiased_rgb=None):
+    """Renderer epilogue of a cache hit (next-row f3): natural termination keeps a path's own
+    non-zero radiance (sec.3.3.1); otherwise Eq. 3 (sec.3.4.2)
+    L_hat = L_n * prod(sigma) / beta_{n-1}.  fp64, elementwise."""
+    y = _d(yhat).reshape(-1, 3).copy()
+    if attenuation is not None:
+        y = y * _d(attenuation).reshape(-1, 3)
+    if beta is not None:
+        y = y / _d(beta).reshape(-1, 1)
+    if unbiased_rgb is not None:
+        u = _d(unbiased_rgb).reshape(-1, 3)
+        hit = np.any(u != 0.0, axis=1)
+        y[hit] = u[hit]
+    return y
+
+
 def level_of(length, L, x, rgb=None):
     x = _d(x).reshape(-1, 3)
     rgb = None if rgb is None else _d(rgb).reshape(-1, 3)

@@ -24,6 +24,7 @@ STATUS = {0: "GC_OK", 1: "GC_ERR_ARG", 2: "GC_ERR_STATE", 3: "GC_ERR_CUDA", 4: "
 
 # Symbols include/gscache.h declares (checked by tests/test_abi.py).
 EXPORTS = ["gc_default_hparams", "gc_create", "gc_destroy", "gc_reserve", "gc_fit", "gc_query",
+           "gc_query_radiance",
            "gc_params", "gc_set_params", "gc_reset_schedule", "gc_grid", "gc_info",
            "gc_nccl_unique_id", "gc_set_comm", "gc_debug_enable_grads", "gc_debug_grads",
            "gc_debug_cull", "gc_debug_levels", "gc_profile_enable", "gc_profile_read",
@@ -94,6 +95,7 @@ def lib():
             "gc_reserve": (i32, [vp, i64, i64]),
             "gc_fit": (i32, [vp, vp, vp, vp, i64, vp, vp]),
             "gc_query": (i32, [vp, vp, vp, i32, i64, vp, vp]),
+            "gc_query_radiance": (i32, [vp, vp, vp, i32, i64, vp, vp, vp, vp, vp]),
             "gc_params": (i32, [vp, i32, vp, vp]),
             "gc_set_params": (i32, [vp, i32, vp, i32, vp]),
             "gc_reset_schedule": (i32, [vp]),
@@ -250,6 +252,29 @@ class GSCache:
         n = _Buf(path_len, np.int32)
         _check(lib().gc_query(self.h, p.ptr, n.ptr, int(level), S, o.ptr, _stream_ptr(stream)))
         self._keep_q = (p, n, o)
+        return out
+
+    def query_radiance(self, pos, path_len=None, level=-1, attenuation=None, beta=None,
+                       unbiased_rgb=None, out=None, stream=None):
+        """gc_query_radiance: lookup + natural-termination substitution + Eq. 3 scaling."""
+        p = _Buf(pos, np.float32)
+        S = p.n // 3
+        if out is None:
+            try:
+                import torch
+                if isinstance(pos, torch.Tensor):
+                    out = torch.empty((S, 3), dtype=torch.float32, device=pos.device)
+            except ImportError:
+                pass
+            if out is None:
+                out = np.empty((S, 3), np.float32)
+        o = _Buf(out, np.float32, writable=True)
+        n = _Buf(path_len, np.int32)
+        at, be, un = (_Buf(attenuation, np.float32), _Buf(beta, np.float32),
+                      _Buf(unbiased_rgb, np.float32))
+        _check(lib().gc_query_radiance(self.h, p.ptr, n.ptr, int(level), S, at.ptr, be.ptr, un.ptr,
+                                       o.ptr, _stream_ptr(stream)))
+        self._keep_q = (p, n, o, at, be, un)
         return out
 
     # ------------------------------------------------------------ params I/O

@@ -487,8 +487,24 @@ gc_status gc_fit(gc_cache c, const float* pos, const int32_t* path_len, const fl
   return GC_OK;
 }
 
+static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_len, int level, int64_t S,
+                            const float* att, const float* beta, const float* unb, float* out_rgb,
+                            gc_stream stream);
+
 gc_status gc_query(gc_cache c, const float* pos, const int32_t* path_len, int level, int64_t S,
                    float* out_rgb, gc_stream stream) {
+  return query_impl(c, pos, path_len, level, S, nullptr, nullptr, nullptr, out_rgb, stream);
+}
+
+gc_status gc_query_radiance(gc_cache c, const float* pos, const int32_t* path_len, int level,
+                            int64_t S, const float* attenuation, const float* beta,
+                            const float* unbiased_rgb, float* out_rgb, gc_stream stream) {
+  return query_impl(c, pos, path_len, level, S, attenuation, beta, unbiased_rgb, out_rgb, stream);
+}
+
+static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_len, int level, int64_t S,
+                            const float* att, const float* beta, const float* unb, float* out_rgb,
+                            gc_stream stream) {
   if (!c) return fail(GC_ERR_ARG, "NULL handle");
   if (S < 0 || S >= ((int64_t)1 << 31)) return fail(GC_ERR_ARG, "S out of range");
   if (S > 0 && (!pos || !out_rgb)) return fail(GC_ERR_ARG, "NULL pointer");
@@ -514,10 +530,24 @@ gc_status gc_query(gc_cache c, const float* pos, const int32_t* path_len, int le
   QueryArgs qa;
   qa.work = Q.work; qa.n_work = Q.totals + 1; qa.csr_off = c->csr_off; qa.csr_idx = c->csr_idx; qa.rec = c->rec;
   qa.bin = Q.bin; qa.out = dout;
+  // epilogue inputs: device pointers are used in place, host ones staged once per call
+  const float* ep[3] = {att, beta, unb};
+  const int64_t epn[3] = {3 * S, S, 3 * S};
+  float* epd[3] = {nullptr, nullptr, nullptr};
+  for (int k = 0; k < 3; ++k) {
+    if (!ep[k]) continue;
+    if (is_device_ptr(ep[k])) { epd[k] = const_cast<float*>(ep[k]); continue; }
+    if (capturing(s)) return fail(GC_ERR_STATE, "host epilogue buffers cannot be captured");
+    CK(dalloc(&epd[k], epn[k]));
+    CK(cudaMemcpyAsync(epd[k], ep[k], sizeof(float) * epn[k], cudaMemcpyHostToDevice, s));
+  }
+  qa.att = epd[0]; qa.beta = epd[1]; qa.unb = epd[2];
   const float tau = c->hp.cutoff_sigma;
   qa.tau2 = tau * tau;
   launch_query(qa, c->q_grid, s, &c->prof);
   if (hout) CK(cudaMemcpyAsync(out_rgb, dout, sizeof(float) * 3 * S, cudaMemcpyDeviceToHost, s));
+  for (int k = 0; k < 3; ++k)
+    if (epd[k] && epd[k] != ep[k]) { CK(cudaStreamSynchronize(s)); cudaFree(epd[k]); }
   CK(cudaGetLastError());
   return GC_OK;
 }

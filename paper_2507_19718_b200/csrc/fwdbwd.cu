@@ -424,6 +424,20 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
   if (threadIdx.x == 0) a.st->done = 0u;
 }
 
+// Output of one query in caller order, with the optional renderer epilogue (f3): natural
+// termination keeps a non-zero unbiased radiance; otherwise Eq. 3,
+// yhat * attenuation / beta.
+__device__ __forceinline__ void query_out(const QueryArgs& a, int64_t i, const float (&y)[3]) {
+  float o0 = y[0], o1 = y[1], o2 = y[2];
+  if (a.att) { o0 *= a.att[3 * i]; o1 *= a.att[3 * i + 1]; o2 *= a.att[3 * i + 2]; }
+  if (a.beta) { const float ib = 1.f / a.beta[i]; o0 *= ib; o1 *= ib; o2 *= ib; }
+  if (a.unb) {
+    const float u0 = a.unb[3 * i], u1 = a.unb[3 * i + 1], u2 = a.unb[3 * i + 2];
+    if (u0 != 0.f || u1 != 0.f || u2 != 0.f) { o0 = u0; o1 = u1; o2 = u2; }
+  }
+  __stcs(a.out + 3 * i, o0); __stcs(a.out + 3 * i + 1, o1); __stcs(a.out + 3 * i + 2, o2);
+}
+
 __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
   __shared__ ChunkSmem sm[kWarps];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -456,14 +470,8 @@ __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
       else
         eval_chunk<false>(w, kc, xa, xb, tau2, ya, yb, nullptr, nullptr, pbase, 0, lane);
     }
-    if (lane < wi.count) {
-      const int64_t i = __float_as_uint(pa.w);
-      __stcs(a.out + 3 * i, ya[0]); __stcs(a.out + 3 * i + 1, ya[1]); __stcs(a.out + 3 * i + 2, ya[2]);
-    }
-    if (lane + 32 < wi.count) {
-      const int64_t i = __float_as_uint(pb4.w);
-      __stcs(a.out + 3 * i, yb[0]); __stcs(a.out + 3 * i + 1, yb[1]); __stcs(a.out + 3 * i + 2, yb[2]);
-    }
+    if (lane < wi.count) query_out(a, __float_as_uint(pa.w), ya);
+    if (lane + 32 < wi.count) query_out(a, __float_as_uint(pb4.w), yb);
   }
 }
 

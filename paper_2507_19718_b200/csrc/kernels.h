@@ -104,6 +104,7 @@ struct QueryArgs {
   const uint32_t* csr_off; const int32_t* csr_idx; const float4* rec;
   const float4* bin;
   float* out; float tau2;
+  const float* att; const float* beta; const float* unb;   // optional f3 epilogue (caller order)
 };
 int query_grid();
 void launch_query(const QueryArgs& a, int grid, cudaStream_t s, Profiler* prof);

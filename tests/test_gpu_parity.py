@@ -412,3 +412,24 @@ def test_data_parallel_one_rank_nccl_path_is_identity(gsc):
         torch.cuda.synchronize()
         np.testing.assert_allclose(list(s2.loss[:3]), l1, rtol=1e-6)
     np.testing.assert_allclose(rows(c1), rows(c2), rtol=1e-5, atol=1e-6)
+
+
+def test_query_radiance_epilogue(gsc):
+    """gc_query_radiance: natural-termination substitution + Eq. 3."""
+    c, _, _ = make_cfg1(gsc)
+    P = rows(c)
+    x, ln = workload.query_batch(1, S=20000)
+    r = np.random.default_rng(9)
+    att = r.uniform(0.1, 1.0, (20000, 3)).astype(np.float32)
+    beta = r.uniform(0.2, 1.0, 20000).astype(np.float32)
+    unb = np.where(r.random((20000, 1)) < 0.3, r.uniform(0.1, 5, (20000, 3)), 0.0).astype(np.float32)
+    y = c.query_radiance(cuda(x), cuda(ln), attenuation=cuda(att), beta=cuda(beta),
+                         unbiased_rgb=cuda(unb)).cpu().numpy()
+    yo, lv, _ = oracle.query(c.goff, P, x.astype(np.float64), ln, grids=c.grids())
+    want = oracle.query_radiance(yo, att, beta, unb)
+    hit = np.any(unb != 0, axis=1)
+    np.testing.assert_array_equal(y[hit], unb[hit])
+    miss = ~hit
+    check_forward(y[miss] / (att[miss] / beta[miss, None]), yo[miss], P, c.goff, x[miss], lv[miss],
+                  what="radiance")
+    np.testing.assert_allclose(y[miss], want[miss], rtol=2e-5, atol=1e-7 * np.abs(want).max())

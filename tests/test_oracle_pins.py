@@ -518,3 +518,20 @@ def test_noise2noise_fixed_point(mode):
     else:
         np.testing.assert_allclose(ratio, 1.0, atol=0.05)
         assert np.all(np.mean(ys, 0) / Lt > 4.0)
+
+
+def test_query_radiance_epilogue_special_cases():
+    """Eq. 3: L_hat = L_n prod(sigma)/beta_{n-1}; beta = 1 and prod(sigma) = 1 reduce
+    to the cached value; a cache miss probability beta halves -> radiance doubles; natural
+    termination keeps a non-zero unbiased sample and only then."""
+    y = np.array([[1.0, 2.0, 3.0], [0.5, 0.0, 4.0], [2.0, 2.0, 2.0]])
+    np.testing.assert_array_equal(oracle.query_radiance(y), y)
+    np.testing.assert_array_equal(oracle.query_radiance(y, np.ones((3, 3)), np.ones(3)), y)
+    np.testing.assert_allclose(oracle.query_radiance(y, beta=np.full(3, 0.5)), 2 * y)
+    att = np.array([[0.5, 0.25, 1.0]] * 3)
+    np.testing.assert_allclose(oracle.query_radiance(y, att), y * att)
+    unb = np.array([[0.0, 0.0, 0.0], [0.0, 1e-3, 0.0], [7.0, 0.0, 0.0]])
+    out = oracle.query_radiance(y, att, np.full(3, 0.8), unb)
+    np.testing.assert_allclose(out[0], y[0] * att[0] / 0.8)
+    np.testing.assert_array_equal(out[1], unb[1])
+    np.testing.assert_array_equal(out[2], unb[2])
