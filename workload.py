@@ -10,7 +10,8 @@ radii U[0.15,0.35], thickness 0.03) plus one slab |z-0.1|<0.02, |x|,|y|<0.8.  A 
 structure chosen proportionally to its area, a uniform point on it, plus N(0, 0.01^2)
 jitter -- the first-collision points of delta tracking on iso-structures (sec.3.2).
 
-Radiance per level (two small lights): L_l(x) = 0.5^l sum_m E_m/(|x-p_m|^2+rho_l^2),
+Radiance per level (two small lights): L_l(x) = 0.5^l sum_m E_m/(|x-p_m|^2+rho_l^2)
+(E scaled so that L is O(0.1-1)),
 rho_l = 0.1+0.3 l.  Noisy MC sample: xhat = L B Z / p with B~Bernoulli(p=0.25),
 Z = exp(0.5 N - 0.125) shared by the channels, so E[xhat] = L (unbiased).
 Path lengths: geometric(0.5) (n=1 w.p. 1/2, ...), 5 % of fit samples carry n=0 (dropped).
@@ -28,8 +29,14 @@ CONFIGS = {
             S=16_777_216, steps=50),
 }
 
-LIGHTS = [(np.array([1.5, 1.0, 0.5]), np.array([8.0, 7.0, 6.0])),
-          (np.array([-1.2, 1.4, -0.8]), np.array([2.0, 3.0, 5.0]))]
+# light powers scaled so that attenuated radiance is O(0.1-1), the range the paper's learning
+# rates adapt to within tens of frames
+LIGHTS = [(np.array([1.5, 1.0, 0.5]), np.array([8.0, 7.0, 6.0]) / 8),
+          (np.array([-1.2, 1.4, -0.8]), np.array([2.0, 3.0, 5.0]) / 8)]
+# cfg3's mid-run "light / transfer-function change": light 1 moves and brightens x1.5,
+# higher-order levels dim x0.7
+LIGHTS_CHANGED = [(np.array([-0.5, 1.5, 1.5]), np.array([12.0, 10.5, 9.0]) / 8),
+                  (np.array([-1.2, 1.4, -0.8]), np.array([2.0, 3.0, 5.0]) / 8)]
 
 
 def rng_for(cfg: int, stream: int = 0) -> np.random.Generator:
@@ -67,14 +74,17 @@ class Scene:
         return np.clip(out, -1.0, 1.0), self.albedo[k]
 
 
-def radiance(x: np.ndarray, level: np.ndarray) -> np.ndarray:
+def radiance(x: np.ndarray, level: np.ndarray, changed: bool = False) -> np.ndarray:
     """Synthetic ground-truth attenuated radiance of path-length level `level` at x."""
     rho2 = (0.1 + 0.3 * level.astype(np.float64)) ** 2
     out = np.zeros((len(x), 3))
-    for p, E in LIGHTS:
+    for p, E in (LIGHTS_CHANGED if changed else LIGHTS):
         d2 = ((x - p) ** 2).sum(1)
         out += E[None, :] / (d2 + rho2)[:, None]
-    return out * (0.5 ** level.astype(np.float64))[:, None]
+    out *= (0.5 ** level.astype(np.float64))[:, None]
+    if changed:
+        out *= np.where(level >= 1, 0.7, 1.0)[:, None]
+    return out
 
 
 def path_lengths(n: int, L: int, r: np.random.Generator, p_zero: float = 0.05) -> np.ndarray:
@@ -93,7 +103,7 @@ def init_cloud(cfg: int):
 
 
 def fit_batch(cfg: int, frame: int = 0, S: int | None = None, morton: bool = False,
-              light_scale: float = 1.0):
+              light_scale: float = 1.0, changed: bool = False):
     """One frame of noisy renderer samples: pos f32[S][3], len i32[S], rgb f32[S][3]."""
     c = CONFIGS[cfg]
     S = c["S"] if S is None else S
@@ -103,7 +113,7 @@ def fit_batch(cfg: int, frame: int = 0, S: int | None = None, morton: bool = Fal
     pos, _ = sc.points(S, r)
     ln = path_lengths(S, L, r)
     lvl = np.clip(np.minimum(ln, L) - 1, 0, None)
-    Lx = radiance(pos, lvl) * light_scale
+    Lx = radiance(pos, lvl, changed) * light_scale
     B = (r.random(S) < 0.25).astype(np.float64)
     Z = np.exp(0.5 * r.normal(size=S) - 0.125)
     rgb = Lx * (B * Z / 0.25)[:, None]
