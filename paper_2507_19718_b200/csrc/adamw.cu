@@ -79,54 +79,53 @@ __device__ void chain_rule(const float p[kNP], const float cg[12], float out[kNP
   out[P_C + 2] = p[P_C + 2] > 0.f ? wo * cg[11] : 0.f;
 }
 
+// Fused normalise + chain rule + AdamW of one Gaussian per thread (A6); zeroes the gradient
+// slots it consumes.  The next step's evaluation record and culling counts are emitted by
+// k_record_cull right after (split so both kernels stay spill-free and latency-hidden).
 __global__ void __launch_bounds__(256, 3) k_adamw(int64_t G, float* __restrict__ P, float* __restrict__ M,
-                                               float* __restrict__ V, float* __restrict__ grad,
-                                               float4* rec, uint4* range, double* rad2, uint32_t* csr_count,
-                                               float* dbg, const DevState* __restrict__ st, AdamHP hp,
-                                               LevelGeom g, gc_fit_stats* out) {
+                                                  float* __restrict__ V, float* __restrict__ grad,
+                                                  float* dbg, const DevState* __restrict__ st, AdamHP hp,
+                                                  LevelGeom g, gc_fit_stats* out) {
   unsigned long long bad = 0;
+  float eta[GC_NGROUPS], dec[GC_NGROUPS];
+#pragma unroll
+  for (int k = 0; k < GC_NGROUPS; ++k) { eta[k] = st->eta[k]; dec[k] = 1.f - eta[k] * hp.wd[k]; }
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < G; j += (int64_t)gridDim.x * blockDim.x) {
     const int l = level_of_gaussian(g, j);
-    float p[kNP];
-#pragma unroll
-    for (int k = 0; k < kNP; ++k) p[k] = P[k * G + j];
+    const bool act = st->active[l] != 0;
     float4* gp = reinterpret_cast<float4*>(grad + 12 * j);
     const float4 c0 = gp[0], c1 = gp[1], c2 = gp[2];
     const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
     gp[0] = zero; gp[1] = zero; gp[2] = zero;
-    const bool act = st->active[l] != 0;
-    if (act || dbg) {
-      const float s = st->inv3k[l];
-      const float cg[12] = {c0.x * s, c0.y * s, c0.z * s, c0.w * s, c1.x * s, c1.y * s,
-                            c1.z * s, c1.w * s, c2.x * s, c2.y * s, c2.z * s, c2.w * s};
-      float raw[kNP];
-      chain_rule(p, cg, raw);
-      if (dbg) {
+    if (!act && !dbg) continue;
+    float p[kNP];
 #pragma unroll
-        for (int k = 0; k < kNP; ++k) dbg[k * G + j] = raw[k];
-      }
-      if (act) {
-        const float bc1 = st->bc1[l], bc2 = st->bc2[l];
-        float m[kNP], v[kNP];
+    for (int k = 0; k < kNP; ++k) p[k] = P[k * G + j];
+    const float s = st->inv3k[l];
+    const float cg[12] = {c0.x * s, c0.y * s, c0.z * s, c0.w * s, c1.x * s, c1.y * s,
+                          c1.z * s, c1.w * s, c2.x * s, c2.y * s, c2.z * s, c2.w * s};
+    float raw[kNP];
+    chain_rule(p, cg, raw);
+    if (dbg) {
 #pragma unroll
-        for (int k = 0; k < kNP; ++k) { m[k] = M[k * G + j]; v[k] = V[k * G + j]; }   // all loads in flight
-#pragma unroll
-        for (int k = 0; k < kNP; ++k) {
-          const float gk = raw[k];
-          const bool ok = isfinite(gk);
-          bad += !ok;
-          const int grp = group_of(k);
-          const float eta = st->eta[grp];
-          const float mk = hp.beta1 * m[k] + (1.f - hp.beta1) * gk;
-          const float vk = hp.beta2 * v[k] + (1.f - hp.beta2) * gk * gk;
-          const float pk = p[k] * (1.f - eta * hp.wd[grp]) - eta * (mk / bc1) / (sqrtf(vk / bc2) + hp.eps);
-          if (ok) { m[k] = mk; v[k] = vk; p[k] = pk; }
-        }
-#pragma unroll
-        for (int k = 0; k < kNP; ++k) { M[k * G + j] = m[k]; V[k * G + j] = v[k]; P[k * G + j] = p[k]; }
-      }
+      for (int k = 0; k < kNP; ++k) dbg[k * G + j] = raw[k];
     }
-    record_and_count(j, p, hp.tau, g, rec, range, rad2, csr_count);
+    if (!act) continue;
+    const float ibc1 = 1.f / st->bc1[l], ibc2 = 1.f / st->bc2[l];
+    float m[kNP], v[kNP];
+#pragma unroll
+    for (int k = 0; k < kNP; ++k) { m[k] = M[k * G + j]; v[k] = V[k * G + j]; }   // all loads in flight
+#pragma unroll
+    for (int k = 0; k < kNP; ++k) {
+      const int grp = k < 3 ? 0 : (k < 7 ? 1 : (k < 10 ? 2 : (k < 13 ? 3 : 4)));   // constant after unroll
+      const float gk = raw[k];
+      const bool ok = isfinite(gk);
+      bad += !ok;
+      const float mk = hp.beta1 * m[k] + (1.f - hp.beta1) * gk;
+      const float vk = hp.beta2 * v[k] + (1.f - hp.beta2) * gk * gk;
+      const float pk = p[k] * dec[grp] - eta[grp] * (mk * ibc1) / (sqrtf(vk * ibc2) + hp.eps);
+      if (ok) { M[k * G + j] = mk; V[k * G + j] = vk; P[k * G + j] = pk; }
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
@@ -150,12 +149,18 @@ void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp
 void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, float4* rec, uint4* range,
                   double* rad2, uint32_t* csr_count, float* dbg_grad, DevState* st, const gc_hparams& hp,
                   const LevelGeom& g, gc_fit_stats* dev_stats, cudaStream_t s, Profiler* prof) {
-  ProfScope ps(prof, "adamw_record_cull", s);
   AdamHP h;
   for (int k = 0; k < GC_NGROUPS; ++k) h.wd[k] = hp.weight_decay[k];
   h.beta1 = hp.beta1; h.beta2 = hp.beta2; h.eps = hp.adam_eps; h.tau = (double)hp.cutoff_sigma;
-  int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((G + 255) / 256, 148 * 8));
-  k_adamw<<<blocks, 256, 0, s>>>(G, P, M, V, grad, rec, range, rad2, csr_count, dbg_grad, st, h, g, dev_stats);
+  {
+    ProfScope ps(prof, "adamw", s);
+    int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((G + 255) / 256, 148 * 8));
+    k_adamw<<<blocks, 256, 0, s>>>(G, P, M, V, grad, dbg_grad, st, h, g, dev_stats);
+  }
+  {
+    ProfScope ps(prof, "record_cull", s);
+    launch_record_cull(G, P, h.tau, g, rec, range, rad2, csr_count, s);
+  }
 }
 
 }  // namespace gsc

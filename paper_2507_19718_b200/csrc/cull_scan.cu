@@ -28,6 +28,34 @@ __global__ void k_cull_emit(int64_t G, const uint4* __restrict__ range, const do
     int l = level_of_gaussian(g, j);
     const int32_t lo[3] = {(int32_t)(r.x & 0xFFFF), (int32_t)(r.y & 0xFFFF), (int32_t)(r.z & 0xFFFF)};
     const int32_t hi[3] = {(int32_t)(r.x >> 16), (int32_t)(r.y >> 16), (int32_t)(r.z >> 16)};
+    const int32_t nx = hi[0] - lo[0] + 1, ny = hi[1] - lo[1] + 1, nz = hi[2] - lo[2] + 1;
+    if (nx <= 3 && ny <= 3 && nz <= 3) {
+      // common case (a range spans <= 3 cells per axis at the auto cell size): all cursor
+      // atomics of the Gaussian are issued before any result is used
+      const int64_t dx = g.dims[l][0], dy = g.dims[l][1];
+      double tx[3], ty[3], tz[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        tx[c] = c < nx ? axis_d2(m0, lo[0] + c, g, l, 0) : 0.0;
+        ty[c] = c < ny ? axis_d2(m1, lo[1] + c, g, l, 1) : 0.0;
+        tz[c] = c < nz ? axis_d2(m2, lo[2] + c, g, l, 2) : 0.0;
+      }
+      uint32_t pos[27];
+#pragma unroll
+      for (int q = 0; q < 27; ++q) {
+        const int qx = q % 3, qy = (q / 3) % 3, qz = q / 9;
+        pos[q] = 0xFFFFFFFFu;
+        if (qx < nx && qy < ny && qz < nz && __dadd_rn(__dadd_rn(tx[qx], ty[qy]), tz[qz]) <= r2)
+          pos[q] = atomicAdd(cursor + g.coff[l] + ((int64_t)(lo[2] + qz) * dy + (lo[1] + qy)) * dx + (lo[0] + qx), 1u);
+      }
+#pragma unroll
+      for (int q = 0; q < 27; ++q) {
+        if (pos[q] == 0xFFFFFFFFu) continue;
+        if (pos[q] < cap) idx[pos[q]] = (int32_t)j;
+        else atomicOr(&st->csr_overflow, 1u);
+      }
+      continue;
+    }
     for_each_cell(lo, hi, m0, m1, m2, r2, g, l, [&](int64_t cell) {
       const uint32_t pos = atomicAdd(cursor + cell, 1u);
       if (pos < cap) idx[pos] = (int32_t)j;

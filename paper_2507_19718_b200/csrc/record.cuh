@@ -20,6 +20,16 @@ constexpr double kK32 = 0x1.71547652b82fep+5;   // 32 log2(e)
 // Record of one Gaussian from its raw parameters (C1): A = R diag(e^-2s) R^T is formed and
 // Cholesky-factored in fp64 (A = U^T U), stored in fp32 with mu and v = w max(0, c).
 __device__ __forceinline__ void make_record(const float p[kNP], float4 out[3]) {
+  const float wo = 1.f / (1.f + expf(-p[P_O]));
+  out[2] = make_float4(p[P_MU + 2], wo * fmaxf(p[P_C], 0.f), wo * fmaxf(p[P_C + 1], 0.f), wo * fmaxf(p[P_C + 2], 0.f));
+  if (p[P_S] == p[P_S + 1] && p[P_S + 1] == p[P_S + 2]) {
+    // isotropic: A = e^{-2s} R R^T = e^{-2s} I exactly, U = e^{-s} I (the rotation drops out);
+    // with the paper's scale LR of 0 and isotropic Eq. 2 init every Gaussian stays here
+    const float u = expf(-p[P_S]);
+    out[0] = make_float4(u, 0.f, 0.f, u);
+    out[1] = make_float4(0.f, u, p[P_MU], p[P_MU + 1]);
+    return;
+  }
   double w = p[P_Q], x = p[P_Q + 1], y = p[P_Q + 2], z = p[P_Q + 3];
   const double n2 = w * w + x * x + y * y + z * z;
   if (n2 < 1e-24) { w = 1.0; x = y = z = 0.0; }
@@ -34,21 +44,13 @@ __device__ __forceinline__ void make_record(const float p[kNP], float4 out[3]) {
   for (int a = 0; a < 3; ++a)
 #pragma unroll
     for (int b = a; b < 3; ++b) A[a][b] = R[a][0] * R[b][0] * D0 + R[a][1] * R[b][1] * D1 + R[a][2] * R[b][2] * D2;
-  double U00 = sqrt(A[0][0]);
-  double U01 = A[0][1] / U00, U02 = A[0][2] / U00;
-  double U11 = sqrt(fmax(A[1][1] - U01 * U01, 1e-300));
-  double U12 = (A[1][2] - U01 * U02) / U11;
-  double U22 = sqrt(fmax(A[2][2] - U02 * U02 - U12 * U12, 1e-300));
-  if (p[P_S] == p[P_S + 1] && p[P_S + 1] == p[P_S + 2]) {
-    // isotropic: A = e^{-2s} R R^T = e^{-2s} I exactly, U = e^{-s} I (the rotation drops
-    // out); with the paper's scale LR of 0 and isotropic Eq. 2 init every Gaussian stays here
-    U00 = U11 = U22 = sqrt(D0);
-    U01 = U02 = U12 = 0.0;
-  }
-  const float wo = 1.f / (1.f + expf(-p[P_O]));
+  const double U00 = sqrt(A[0][0]);
+  const double U01 = A[0][1] / U00, U02 = A[0][2] / U00;
+  const double U11 = sqrt(fmax(A[1][1] - U01 * U01, 1e-300));
+  const double U12 = (A[1][2] - U01 * U02) / U11;
+  const double U22 = sqrt(fmax(A[2][2] - U02 * U02 - U12 * U12, 1e-300));
   out[0] = make_float4((float)U00, (float)U01, (float)U02, (float)U11);
   out[1] = make_float4((float)U12, (float)U22, p[P_MU], p[P_MU + 1]);
-  out[2] = make_float4(p[P_MU + 2], wo * fmaxf(p[P_C], 0.f), wo * fmaxf(p[P_C + 1], 0.f), wo * fmaxf(p[P_C + 2], 0.f));
 }
 
 // C8 cell range of one Gaussian (AABB of its tau-ellipsoid, bounded with U_b >= e^{s_b}) and
