@@ -106,10 +106,18 @@ def run_reference(args):
     c = workload.CONFIGS[cfg]
     pos, alb = workload.init_cloud(cfg)
     counts = c["counts"]
-    # Eq. 2 brute-force kNN of the oracle is O(N^2); scales of the oracle's own create at
-    # the sample size are not timed -- supply isotropic scales from the level spacing.
-    ls = np.full((counts[0], 3), np.log(0.5 * 2.0 / counts[0] ** (1 / 3)))
-    P = oracle.create(counts, pos.astype(np.float64), alb.astype(np.float64), ls, seed=cfg)
+    # untimed setup: the oracle's create with Eq. 2 scales per level; the 3-NN means come from
+    # scipy's k-d tree (the oracle's O(N^2) brute force would take minutes at 65k points),
+    # then oracle.eq2_from_dbar applies Eq. 2 itself.
+    from scipy.spatial import cKDTree
+    P = oracle.create(counts, pos.astype(np.float64), alb.astype(np.float64),
+                      np.zeros((counts[0], 3)), seed=cfg)
+    goff = np.concatenate([[0], np.cumsum(counts)])
+    for l in range(len(counts)):
+        pts = P[goff[l]:goff[l + 1], 0:3]
+        d, _ = cKDTree(pts).query(pts, k=4)
+        s_ = oracle.eq2_from_dbar(d[:, 1:].mean(1), oracle.diag(pts))
+        P[goff[l]:goff[l + 1], 10:13] = np.log(s_)[:, None]
     grids = auto_grids(P, counts)
     oc = oracle.OracleCache(counts, P, grids=grids)
     n = args.ref_samples
