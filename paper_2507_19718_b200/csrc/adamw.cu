@@ -11,11 +11,13 @@ namespace gsc {
 __global__ void __launch_bounds__(kPart * 32) k_stats(const double* __restrict__ partial, int nblocks,
                                                       const uint32_t* __restrict__ cell_start, LevelGeom g,
                                                       int64_t S, LvlStats* lvl) {
+  pdl_enter();
   stats_reduce(partial, nblocks, cell_start, g, S, lvl, threadIdx.x >> 5, kPart, threadIdx.x & 31);
 }
 
 __global__ void k_step_scalars(const LvlStats* __restrict__ lvl, DevState* st, StepHP hp,
                                gc_fit_stats* out) {
+  pdl_enter();
   step_scalars_warp(lvl, st, hp, out, threadIdx.x);
 }
 
@@ -86,6 +88,7 @@ __global__ void __launch_bounds__(256, 3) k_adamw(int64_t G, float* __restrict__
                                                   float* __restrict__ V, float* __restrict__ grad,
                                                   float* dbg, const DevState* __restrict__ st, AdamHP hp,
                                                   LevelGeom g, gc_fit_stats* out) {
+  pdl_enter();
   unsigned long long bad = 0;
   float eta[GC_NGROUPS], dec[GC_NGROUPS];
 #pragma unroll
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(256, 3) k_adamw(int64_t G, float* __restrict__
 void launch_stats(const double* partial, int nblocks, const uint32_t* cell_start,
                   const LevelGeom& g, int64_t S, LvlStats* lvl, cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "stats", s);
-  k_stats<<<1, kPart * 32, 0, s>>>(partial, nblocks, cell_start, g, S, lvl);
+  launch_pdl(k_stats, dim3(1), dim3(kPart * 32), 0, s, partial, nblocks, cell_start, g, S, lvl);
 }
 
 void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp, int L,
@@ -143,7 +146,7 @@ void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp
   StepHP h;
   for (int k = 0; k < GC_NGROUPS; ++k) h.lr[k] = hp.lr[k];
   h.beta1 = hp.beta1; h.beta2 = hp.beta2; h.schedule = hp.lr_schedule; h.L = L;
-  k_step_scalars<<<1, 32, 0, s>>>(lvl, st, h, dev_stats);
+  launch_pdl(k_step_scalars, dim3(1), dim3(32), 0, s, lvl, st, h, dev_stats);
 }
 
 void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, float4* rec, uint4* range,
@@ -155,7 +158,7 @@ void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, float4* 
   {
     ProfScope ps(prof, "adamw", s);
     int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((G + 255) / 256, 148 * 8));
-    k_adamw<<<blocks, 256, 0, s>>>(G, P, M, V, grad, dbg_grad, st, h, g, dev_stats);
+    launch_pdl(k_adamw, dim3(blocks), dim3(256), 0, s, G, P, M, V, grad, dbg_grad, (const DevState*)st, h, g, dev_stats);
   }
   {
     ProfScope ps(prof, "record_cull", s);

@@ -85,6 +85,14 @@ __device__ __forceinline__ int64_t sample_cell(const LevelGeom& g, int l, float 
   return g.coff[l] + ((int64_t)c2 * g.dims[l][1] + c1) * g.dims[l][0] + c0;
 }
 
+// Programmatic dependent launch: every hot-path kernel waits for its predecessor's memory at
+// its top and immediately allows its own successor to be scheduled (the successor's CTAs then
+// sit in griddepcontrol.wait while this grid drains, hiding the launch gap).
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

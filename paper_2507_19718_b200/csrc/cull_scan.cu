@@ -8,6 +8,7 @@ namespace gsc {
 
 __global__ void k_record_cull(int64_t G, const float* __restrict__ P, double tau, LevelGeom g,
                               float4* rec, uint4* range, double* rad2, uint32_t* csr_count) {
+  pdl_enter();
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < G; j += (int64_t)gridDim.x * blockDim.x) {
     float p[kNP];
 #pragma unroll
@@ -21,6 +22,7 @@ __global__ void k_record_cull(int64_t G, const float* __restrict__ P, double tau
 __global__ void k_cull_emit(int64_t G, const uint4* __restrict__ range, const double* __restrict__ rad2,
                             const float* __restrict__ P, LevelGeom g, uint32_t* cursor, int32_t* idx,
                             uint32_t cap, DevState* st) {
+  pdl_enter();
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < G; j += (int64_t)gridDim.x * blockDim.x) {
     uint4 r = range[j];
     const double r2 = rad2[j];
@@ -133,6 +135,7 @@ __device__ __forceinline__ void load_counts(const uint32_t* cnt, int64_t n, int 
 }
 
 __global__ void __launch_bounds__(256) k_scan_reduce(const uint32_t* __restrict__ cnt, int64_t n, int ch, uint2* tile_sums) {
+  pdl_enter();
   int64_t base = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 8;
   uint32_t c[8];
   load_counts(cnt, n, ch, base, c);
@@ -151,6 +154,7 @@ __global__ void __launch_bounds__(256) k_scan_down(uint32_t* __restrict__ cnt, i
                                                    const uint2* __restrict__ tile_sums, int ntiles,
                                                    uint32_t* totals, uint32_t* excl, uint32_t* excl_copy,
                                                    WorkItem* work, LevelGeom g) {
+  pdl_enter();
   uint2 pre = make_uint2(0, 0), dummy;
   for (int j = threadIdx.x; j < (int)blockIdx.x; j += 256) {
     const uint2 t = __ldg(tile_sums + j);
@@ -201,11 +205,11 @@ void launch_scan(uint32_t* cnt, int64_t n, int ch, uint2* tile_sums, uint32_t* t
   int ntiles = (int)((n + kScanTile - 1) / kScanTile);
   {
     ProfScope ps(prof, "scan_reduce", s);
-    k_scan_reduce<<<ntiles, 256, 0, s>>>(cnt, n, ch, tile_sums);
+    launch_pdl(k_scan_reduce, dim3(ntiles), dim3(256), 0, s, (const uint32_t*)cnt, n, ch, tile_sums);
   }
   {
     ProfScope ps(prof, "scan_down", s);
-    k_scan_down<<<ntiles, 256, 0, s>>>(cnt, n, ch, tile_sums, ntiles, totals, excl, excl_copy, work, g);
+    launch_pdl(k_scan_down, dim3(ntiles), dim3(256), 0, s, cnt, n, ch, (const uint2*)tile_sums, ntiles, totals, excl, excl_copy, work, g);
   }
 }
 
@@ -213,7 +217,7 @@ void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& 
                         uint4* range, double* rad2, uint32_t* csr_count, cudaStream_t s) {
   int blocks = (int)std::min<int64_t>((G + 255) / 256, 148 * 16);
   if (blocks < 1) blocks = 1;
-  k_record_cull<<<blocks, 256, 0, s>>>(G, P, tau, g, rec, range, rad2, csr_count);
+  launch_pdl(k_record_cull, dim3(blocks), dim3(256), 0, s, G, P, tau, g, rec, range, rad2, csr_count);
 }
 
 void launch_cull_emit(int64_t G, const uint4* range, const double* rad2, const float* P, const LevelGeom& g,
@@ -221,7 +225,7 @@ void launch_cull_emit(int64_t G, const uint4* range, const double* rad2, const f
   ProfScope ps(prof, "cull_emit", s);
   int blocks = (int)std::min<int64_t>((G + 255) / 256, 148 * 16);
   if (blocks < 1) blocks = 1;
-  k_cull_emit<<<blocks, 256, 0, s>>>(G, range, rad2, P, g, cursor, idx, cap, st);
+  launch_pdl(k_cull_emit, dim3(blocks), dim3(256), 0, s, G, range, rad2, P, g, cursor, idx, cap, st);
 }
 
 }  // namespace gsc

@@ -276,6 +276,7 @@ __device__ __forceinline__ void hdr_grad(int mode, float eps, const float (&y)[3
 }
 
 __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char dsm[];
   WarpSmem* sm = reinterpret_cast<WarpSmem*>(dsm);
   __shared__ double s_loss[kWarps][kMaxL];
@@ -439,6 +440,7 @@ __device__ __forceinline__ void query_out(const QueryArgs& a, int64_t i, const f
 }
 
 __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
+  pdl_enter();
   __shared__ ChunkSmem sm[kWarps];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   ChunkSmem& w = sm[wid];
@@ -496,12 +498,12 @@ int query_grid() { static int g = persistent_grid((const void*)k_query, 0); retu
 
 void launch_fwdbwd(const FitArgs& a, int grid, cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "fwdbwd", s);
-  k_fwdbwd<<<grid, 256, kFwdBwdSmem, s>>>(a);
+  launch_pdl(k_fwdbwd, dim3(grid), dim3(256), kFwdBwdSmem, s, a);
 }
 
 void launch_query(const QueryArgs& a, int grid, cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "query_fwd", s);
-  k_query<<<grid, 256, 0, s>>>(a);
+  launch_pdl(k_query, dim3(grid), dim3(256), 0, s, a);
 }
 
 }  // namespace gsc

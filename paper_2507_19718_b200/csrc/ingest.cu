@@ -13,6 +13,7 @@ constexpr int kU = 4;   // samples per thread per iteration
 __global__ void __launch_bounds__(256, 5) k_keys(const float* __restrict__ pos, const int32_t* __restrict__ len,
                                                  const float* __restrict__ rgb, int level_fixed, int64_t S,
                                                  LevelGeom g, IngestBufs b, float* out_zero) {
+  pdl_enter();
   // per-level grid in shared memory: indexed by a runtime level, the kernel-parameter copy
   // would go through dynamically indexed constant loads
   __shared__ double s_org[kMaxL][3], s_inv[kMaxL][3];
@@ -89,6 +90,7 @@ __global__ void __launch_bounds__(256, 5) k_keys(const float* __restrict__ pos, 
 
 __global__ void __launch_bounds__(256, 4) k_scatter(const float* __restrict__ pos, const float* __restrict__ rgb,
                                                  int64_t S, const uint32_t* __restrict__ cell_start, IngestBufs b) {
+  pdl_enter();
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t T = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i0 = (t >> 5) * 32 * kU + (t & 31); i0 < S; i0 += T * kU) {
@@ -142,19 +144,19 @@ static int grid_for(int64_t n, int per_sm = 12) {
 void launch_keys(const float* pos, const int32_t* len, const float* rgb, int level_fixed,
                  int64_t S, const LevelGeom& g, IngestBufs b, cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "ingest_keys", s);
-  k_keys<<<grid_for(S), 256, 0, s>>>(pos, len, rgb, level_fixed, S, g, b, nullptr);
+  launch_pdl(k_keys, dim3(grid_for(S)), dim3(256), 0, s, pos, len, rgb, level_fixed, S, g, b, (float*)nullptr);
 }
 
 void launch_keys_query(const float* pos, const int32_t* len, int level_fixed, int64_t S,
                        const LevelGeom& g, IngestBufs b, float* out, cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "query_keys", s);
-  k_keys<<<grid_for(S), 256, 0, s>>>(pos, len, nullptr, level_fixed, S, g, b, out);
+  launch_pdl(k_keys, dim3(grid_for(S)), dim3(256), 0, s, pos, len, (const float*)nullptr, level_fixed, S, g, b, out);
 }
 
 void launch_scatter(const float* pos, const float* rgb, int64_t S, const uint32_t* cell_start,
                     IngestBufs b, cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, rgb ? "ingest_scatter" : "query_scatter", s);
-  k_scatter<<<grid_for(S), 256, 0, s>>>(pos, rgb, S, cell_start, b);
+  launch_pdl(k_scatter, dim3(grid_for(S)), dim3(256), 0, s, pos, rgb, S, cell_start, b);
 }
 
 void launch_levels_of(const uint32_t* key, int64_t S, const LevelGeom& g, int32_t* out, cudaStream_t s) {
