@@ -463,6 +463,7 @@ gc_status gc_fit(gc_cache c, const float* pos, const int32_t* path_len, const fl
   fa.grad = c->grad; fa.partial = c->partial;
   const float tau = c->hp.cutoff_sigma;
   fa.tau2 = tau * tau; fa.hdr_eps = c->hp.hdr_eps; fa.mode = c->hp.loss_grad_mode; fa.L = c->L;
+  fa.lite = (c->hp.lr[GC_SCALE] == 0.f && !c->dbg_on) ? 1 : 0;
   const bool dp = c->comm != nullptr;
   fa.fused = 0;   // last-CTA stats tail: measured 16 us slower than the two small kernels; off
   fa.cell_start = F.cell_start; fa.S = S; fa.lvl = c->lvl; fa.st = c->st; fa.dstats = c->dstats;

@@ -189,15 +189,20 @@ __device__ __forceinline__ void eval_chunk(const ChunkSmem& w, int kc, const flo
 // Gradient terms of pairs [p0, p1) of the staged chunk (lane = pair): 12 coefficient
 // gradients (C5), a <= 2-level segmented shuffle scan over each Gaussian's run of pairs,
 // then red.global.add.v4.f32 from every 4th lane of a run counted from its end.
-__device__ __forceinline__ void chunk_pairs_bwd(const WarpSmem& w, int p0, int p1, float* __restrict__ grad,
-                                                int lane, bool iso) {
+// kLite (isotropic chunk, scale group frozen with lr 0, no gradient export): the 6 dA terms
+// only feed dL/ds, whose update is frozen, and dL/dq, which is exactly 0 for isotropic
+// Gaussians -- so only d mu and d v are accumulated (dead work skipped, not approximated).
+template <bool kLite>
+__device__ __forceinline__ void chunk_pairs_bwd_impl(const WarpSmem& w, int p0, int p1, float* __restrict__ grad,
+                                                     int lane, bool iso) {
+  constexpr int NV = kLite ? 6 : 12;
   for (int pb = p0; pb < p1; pb += 32) {
     const int p = pb + lane;
     const bool valid = p < p1;
     int k = 32 + lane;                 // idle lanes form their own segments
-    float v[12];
+    float v[NV];
 #pragma unroll
-    for (int q = 0; q < 12; ++q) v[q] = 0.f;
+    for (int q = 0; q < NV; ++q) v[q] = 0.f;
     int gid = 0;
     if (valid) {
       const uint32_t key = w.pkey[p];
@@ -226,11 +231,15 @@ __device__ __forceinline__ void chunk_pairs_bwd(const WarpSmem& w, int p0, int p
       }
       const float he = (sx.w * v0 + sg.x * v1 + sg.y * v2) * e;
       v[0] = he * tx; v[1] = he * ty; v[2] = he * tz;                 // d mu
-      const float kk = -0.5f * he;
-      const float kx = kk * dx, ky = kk * dy, kz = kk * dz;
-      v[3] = kx * dx; v[4] = ky * dy; v[5] = kz * dz;                 // dA00 dA11 dA22
-      v[6] = kx * dy; v[7] = kx * dz; v[8] = ky * dz;                 // dA01 dA02 dA12
-      v[9] = sx.w * e; v[10] = sg.x * e; v[11] = sg.y * e;            // d v
+      if constexpr (kLite) {
+        v[3] = sx.w * e; v[4] = sg.x * e; v[5] = sg.y * e;            // d v
+      } else {
+        const float kk = -0.5f * he;
+        const float kx = kk * dx, ky = kk * dy, kz = kk * dz;
+        v[3] = kx * dx; v[4] = ky * dy; v[5] = kz * dz;               // dA00 dA11 dA22
+        v[6] = kx * dy; v[7] = kx * dz; v[8] = ky * dz;               // dA01 dA02 dA12
+        v[9] = sx.w * e; v[10] = sg.x * e; v[11] = sg.y * e;          // d v
+      }
     }
     const unsigned peers = __match_any_sync(0xffffffffu, k);
     const int head = __ffs(peers) - 1, tail = 31 - __clz(peers);
@@ -239,19 +248,30 @@ __device__ __forceinline__ void chunk_pairs_bwd(const WarpSmem& w, int p0, int p
       const bool need = lane - o >= head;
       if (!__any_sync(0xffffffffu, need)) break;
 #pragma unroll
-      for (int q = 0; q < 12; ++q) {
+      for (int q = 0; q < NV; ++q) {
         const float t = __shfl_up_sync(0xffffffffu, v[q], o);
         if (need) v[q] += t;
       }
     }
     if (valid && ((tail - lane) & 3) == 0) {
       float* gp = grad + 12 * (int64_t)gid;
-      red_add_v4(gp, v[0], v[1], v[2], v[3]);
-      red_add_v4(gp + 4, v[4], v[5], v[6], v[7]);
-      red_add_v4(gp + 8, v[8], v[9], v[10], v[11]);
+      if constexpr (kLite) {
+        red_add_v4(gp, v[0], v[1], v[2], 0.f);
+        red_add_v4(gp + 8, 0.f, v[3], v[4], v[5]);
+      } else {
+        red_add_v4(gp, v[0], v[1], v[2], v[3]);
+        red_add_v4(gp + 4, v[4], v[5], v[6], v[7]);
+        red_add_v4(gp + 8, v[8], v[9], v[10], v[11]);
+      }
     }
   }
   __syncwarp();
+}
+
+__device__ __forceinline__ void chunk_pairs_bwd(const WarpSmem& w, int p0, int p1, float* __restrict__ grad,
+                                                int lane, bool iso, bool lite_ok) {
+  if (iso && lite_ok) chunk_pairs_bwd_impl<true>(w, p0, p1, grad, lane, true);
+  else chunk_pairs_bwd_impl<false>(w, p0, p1, grad, lane, iso);
 }
 
 __device__ __forceinline__ void load_pos(const float4* __restrict__ bin, int stride, int start, int count, int s,
@@ -349,7 +369,7 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
         const int pend = w.cend[c];
         if (pend == pstart) continue;
         if (C > 32) iso = stage_chunk(w, a.csr_idx, a.rec, lo + cb, min(32, C - cb), lane, xref, yref, zref, tau2);
-        chunk_pairs_bwd(w, pstart, pend, a.grad, lane, iso);
+        chunk_pairs_bwd(w, pstart, pend, a.grad, lane, iso, a.lite);
         pstart = pend;
       }
     } else {
@@ -377,7 +397,7 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
           }
           const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = __ballot_sync(0xffffffffu, inb);
           if (!(ma | mb)) continue;
-          if (pb + 64 > kPairCap) { chunk_pairs_bwd(w, 0, pb, a.grad, lane, ci); pb = 0; }
+          if (pb + 64 > kPairCap) { chunk_pairs_bwd(w, 0, pb, a.grad, lane, ci, a.lite); pb = 0; }
           if (ina) {
             const int pos = pb + __popc(ma & lt);
             w.pkey[pos] = (uint16_t)((k << 6) | lane);
@@ -391,7 +411,7 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
           pb += __popc(ma) + __popc(mb);
           __syncwarp();
         }
-        chunk_pairs_bwd(w, 0, pb, a.grad, lane, ci);
+        chunk_pairs_bwd(w, 0, pb, a.grad, lane, ci, a.lite);
       }
     }
   }

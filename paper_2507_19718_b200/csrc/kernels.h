@@ -107,6 +107,7 @@ struct FitArgs {
   float* grad;          // [G][12]
   double* partial;      // [grid][kMaxL + 2]: per-block loss sums, pairs, candidates
   float tau2, hdr_eps; int mode; int L;
+  int lite;             // scale group frozen (lr 0) and no gradient export: skip dA on isotropic chunks
   // fused statistics + step scalars in the last CTA (single GPU)
   int fused; const uint32_t* cell_start; int64_t S; LvlStats* lvl; DevState* st; StepHP shp;
   gc_fit_stats* dstats; LevelGeom geom;
