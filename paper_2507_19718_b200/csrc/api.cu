@@ -138,7 +138,10 @@ static gc_status ensure_scratch(gc_cache c, Scratch& sc, int64_t S, bool fit, cu
   CK(dalloc(&sc.bin, (fit ? 2 : 1) * cap));
   CK(dalloc(&sc.cell_count, nbins)); CK(dalloc(&sc.cell_start, nbins + 1));
   CK(cudaMemset(sc.cell_count, 0, sizeof(uint32_t) * nbins));   // kept zero by the scan
-  CK(dalloc(&sc.tiles, ntiles)); CK(dalloc(&sc.totals, 4));
+  (void)ntiles;
+  CK(dalloc(&sc.tiles, scan_state_words(nbins)));
+  CK(cudaMemset(sc.tiles, 0, sizeof(uint2) * scan_state_words(nbins)));
+  CK(dalloc(&sc.totals, 4));
   CK(dalloc(&sc.work, work_cap));
   sc.cap = cap;
   return GC_OK;
@@ -351,7 +354,9 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
 
   // records + culling lists; exact size of the first CSR sets the list capacity
   CK(dalloc(&c->csr_count, c->NC)); CK(dalloc(&c->csr_off, c->NC + 1)); CK(dalloc(&c->csr_cursor, c->NC));
-  CK(dalloc(&c->csr_tiles, (c->NC + kScanTile - 1) / kScanTile)); CK(dalloc(&c->csr_totals, 4));
+  CK(dalloc(&c->csr_tiles, scan_state_words(c->NC)));
+  CK(cudaMemset(c->csr_tiles, 0, sizeof(uint2) * scan_state_words(c->NC)));
+  CK(dalloc(&c->csr_totals, 4));
   CK(cudaMemset(c->csr_count, 0, sizeof(uint32_t) * c->NC));
   launch_record_cull(G, c->P, tau, c->geom, c->rec, c->range, c->rad2, c->csr_count, s);
   launch_scan(c->csr_count, c->NC, 0, c->csr_tiles, c->csr_totals, c->csr_off, c->csr_cursor, nullptr, c->geom, s, nullptr);

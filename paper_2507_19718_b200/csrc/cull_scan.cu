@@ -134,35 +134,44 @@ __device__ __forceinline__ void load_counts(const uint32_t* cnt, int64_t n, int 
   for (int k = 0; k < kRep; ++k) c[k] = cell < nc ? cnt[(int64_t)k * nc + cell] : 0u;
 }
 
-__global__ void __launch_bounds__(256) k_scan_reduce(const uint32_t* __restrict__ cnt, int64_t n, int ch, uint2* tile_sums) {
-  pdl_enter();
-  int64_t base = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 8;
-  uint32_t c[8];
-  load_counts(cnt, n, ch, base, c);
-  const uint2 s = sum8(c, ch);
-  uint2 total;
-  block_excl_scan(s, total);
-  if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+
+// Single-pass scan with decoupled look-back.  Tiles are taken in ticket order (so every
+// predecessor is already running); a tile publishes its aggregate, warp 0 walks back over
+// its predecessors 32 at a time until it meets an inclusive prefix, publishes its own
+// inclusive prefix, and the block then writes the exclusive offsets (and an optional copy
+// used as atomic cursors) and, with ch > 0, one WorkItem per chunk of <= ch samples of every
+// non-empty cell.  The counts are zeroed after reading (ready for the next call) and the last
+// tile publishes the grand totals.  Tile status words (flag:2 | chunks:31 | count:31) are
+// ping-ponged between two arrays by a launch parity, each tile clearing its slot in the
+// array the next launch will use.
+__device__ __forceinline__ unsigned long long st_pack(uint32_t f, uint2 v) {
+  return ((unsigned long long)f << 62) | ((unsigned long long)(v.y & 0x7FFFFFFFu) << 31) | (v.x & 0x7FFFFFFFu);
+}
+__device__ __forceinline__ uint32_t st_flag(unsigned long long w) { return (uint32_t)(w >> 62); }
+__device__ __forceinline__ uint2 st_val(unsigned long long w) {
+  return make_uint2((uint32_t)(w & 0x7FFFFFFFu), (uint32_t)((w >> 31) & 0x7FFFFFFFu));
 }
 
-// Down-sweep (reduce-then-scan without a middle pass): every tile sums the tile totals
-// before it itself, scans its 2048 counts, writes the exclusive offsets (and an optional
-// copy used as atomic cursors) and, with ch > 0, one WorkItem per chunk of <= ch samples of
-// every non-empty cell.  The counts are zeroed after reading (ready for the next call), and
-// the last tile publishes the grand totals.
-__global__ void __launch_bounds__(256) k_scan_down(uint32_t* __restrict__ cnt, int64_t n, int ch,
-                                                   const uint2* __restrict__ tile_sums, int ntiles,
-                                                   uint32_t* totals, uint32_t* excl, uint32_t* excl_copy,
-                                                   WorkItem* work, LevelGeom g) {
+__global__ void __launch_bounds__(256) k_scan(uint32_t* __restrict__ cnt, int64_t n, int ch,
+                                              unsigned long long* state, uint32_t* ctl, int ntiles,
+                                              uint32_t* totals, uint32_t* excl, uint32_t* excl_copy,
+                                              WorkItem* work, LevelGeom g) {
   pdl_enter();
-  uint2 pre = make_uint2(0, 0), dummy;
-  for (int j = threadIdx.x; j < (int)blockIdx.x; j += 256) {
-    const uint2 t = __ldg(tile_sums + j);
-    pre.x += t.x; pre.y += t.y;
+  __shared__ int s_tile;
+  __shared__ uint32_t s_par;
+  __shared__ uint2 s_prefix;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    s_par = *(volatile uint32_t*)(ctl + 1);
+    __threadfence();
+    s_tile = (int)atomicAdd(ctl, 1u);
   }
-  block_excl_scan(pre, dummy);
-  const uint2 tp = dummy;
-  int64_t base = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 8;
+  __syncthreads();
+  const int tile = s_tile;
+  const uint32_t par = s_par;
+  unsigned long long* cur = state + (size_t)par * ntiles;
+  unsigned long long* nxt = state + (size_t)(par ^ 1u) * ntiles;
+  int64_t base = (int64_t)tile * kScanTile + threadIdx.x * 8;
   uint32_t c[8];
   load_counts(cnt, n, ch, base, c);
   if (!ch && base + 8 <= n && ((base & 3) == 0)) {
@@ -174,7 +183,38 @@ __global__ void __launch_bounds__(256) k_scan_down(uint32_t* __restrict__ cnt, i
   }
   const uint2 s = sum8(c, ch);
   uint2 total;
-  uint2 ex = block_excl_scan(s, total);
+  const uint2 ex = block_excl_scan(s, total);
+  if (warp == 0) {
+    uint2 prefix = make_uint2(0, 0);
+    if (tile == 0) {
+      if (lane == 0) atomicExch(cur, st_pack(2u, total));
+    } else {
+      if (lane == 0) atomicExch(cur + tile, st_pack(1u, total));
+      int j = tile - 1;
+      for (;;) {
+        const int idx = j - lane;
+        unsigned long long w = st_pack(2u, make_uint2(0, 0));   // before tile 0: inclusive 0
+        if (idx >= 0) {
+          do { w = *(volatile unsigned long long*)(cur + idx); } while (st_flag(w) == 0u);
+        }
+        const uint32_t inc = __ballot_sync(0xffffffffu, st_flag(w) == 2u);
+        const int stop = inc ? __ffs(inc) - 1 : 32;
+        uint2 v = lane <= stop ? st_val(w) : make_uint2(0, 0);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+          v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+        }
+        prefix.x += v.x; prefix.y += v.y;
+        if (inc) break;
+        j -= 32;
+      }
+      if (lane == 0) atomicExch(cur + tile, st_pack(2u, make_uint2(prefix.x + total.x, prefix.y + total.y)));
+    }
+    if (lane == 0) { s_prefix = prefix; nxt[tile] = 0ull; }
+  }
+  __syncthreads();
+  const uint2 tp = s_prefix;
   uint32_t off = tp.x + ex.x, woff = tp.y + ex.y;
   if (ch && s.x) {                       // one cell per thread (kRep replicas)
     const int64_t cell = base / kRep;
@@ -193,24 +233,24 @@ __global__ void __launch_bounds__(256) k_scan_down(uint32_t* __restrict__ cnt, i
     }
     if (i == n - 1) excl[n] = off;
   }
-  if (blockIdx.x == ntiles - 1 && threadIdx.x == 0) {
+  if (tile == ntiles - 1 && threadIdx.x == 0) {
     totals[0] = tp.x + total.x; totals[1] = tp.y + total.y;
     totals[2] = 0u;                    // dynamic work counter of the consumer kernel
+    ctl[0] = 0u;                       // tickets of the next launch
+    ctl[1] = par ^ 1u;                 // every block of this launch has read the parity
   }
 }
 
-void launch_scan(uint32_t* cnt, int64_t n, int ch, uint2* tile_sums, uint32_t* totals,
+int scan_state_words(int64_t n) { return (int)(2 * ((n + kScanTile - 1) / kScanTile) + 2); }
+
+void launch_scan(uint32_t* cnt, int64_t n, int ch, uint2* state, uint32_t* totals,
                  uint32_t* excl, uint32_t* excl_copy, WorkItem* work, const LevelGeom& g,
                  cudaStream_t s, Profiler* prof) {
-  int ntiles = (int)((n + kScanTile - 1) / kScanTile);
-  {
-    ProfScope ps(prof, "scan_reduce", s);
-    launch_pdl(k_scan_reduce, dim3(ntiles), dim3(256), 0, s, (const uint32_t*)cnt, n, ch, tile_sums);
-  }
-  {
-    ProfScope ps(prof, "scan_down", s);
-    launch_pdl(k_scan_down, dim3(ntiles), dim3(256), 0, s, cnt, n, ch, (const uint2*)tile_sums, ntiles, totals, excl, excl_copy, work, g);
-  }
+  const int ntiles = (int)((n + kScanTile - 1) / kScanTile);
+  unsigned long long* st = reinterpret_cast<unsigned long long*>(state);
+  uint32_t* ctl = reinterpret_cast<uint32_t*>(st + 2 * ntiles);
+  ProfScope ps(prof, "scan", s);
+  launch_pdl(k_scan, dim3(ntiles), dim3(256), 0, s, cnt, n, ch, st, ctl, ntiles, totals, excl, excl_copy, work, g);
 }
 
 void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& g, float4* rec,

@@ -73,7 +73,8 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 }
 
 // cull_scan.cu
-void launch_scan(uint32_t* cnt, int64_t n, int ch, uint2* tile_sums, uint32_t* totals,
+int scan_state_words(int64_t n);   // uint2 words of look-back state for an n-entry scan (zeroed)
+void launch_scan(uint32_t* cnt, int64_t n, int ch, uint2* state, uint32_t* totals,
                  uint32_t* excl, uint32_t* excl_copy, WorkItem* work, const LevelGeom& g,
                  cudaStream_t s, Profiler* prof);
 void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& g, float4* rec,
