@@ -200,10 +200,14 @@ def run_ours(args):
     cache.reserve(S, S)
     stream = torch.cuda.Stream(device=dev)
 
-    def step(f, s_):
-        x, ln, rgb, xq, lq = frames[f]
-        cache.query(xq, lq, out=outq, stream=s_)
+    def frame_call(x, ln, rgb, xq, lq, out, s_):
+        if args.fused:                      # one binning pass for both sample sets
+            return cache.fit_query(x, ln, rgb, xq, lq, out=out, stream=s_)[1]
+        cache.query(xq, lq, out=out, stream=s_)
         return cache.fit(x, ln, rgb, stream=s_)
+
+    def step(f, s_):
+        return frame_call(*frames[f], outq, s_)
 
     # warm-up (eager), then capture one CUDA graph per rotating frame
     with torch.cuda.stream(stream):
@@ -302,16 +306,12 @@ def run_ours(args):
     e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         for w in range(2):
-            x, ln, rgb, xq, lq = hx[w % R]
-            cache.query(xq, lq, out=hout, stream=stream)
-            cache.fit(x, ln, rgb, stream=stream)
+            frame_call(*hx[w % R], hout, stream)
     barrier()
     e4.record(stream)
     with torch.cuda.stream(stream):
         for k in range(args.steps):
-            x, ln, rgb, xq, lq = hx[k % R]
-            cache.query(xq, lq, out=hout, stream=stream)
-            cache.fit(x, ln, rgb, stream=stream)
+            frame_call(*hx[k % R], hout, stream)
     e5.record(stream)
     barrier()
     ms_e2e = torch.tensor([e4.elapsed_time(e5) / args.steps], dtype=torch.float64, device=dev)
@@ -334,7 +334,8 @@ def run_ours(args):
             "config": {"workload": c["name"], "levels": len(counts), "counts": counts,
                        "S_fit_per_gpu": S, "S_query_per_gpu": S, "parallelism": f"dp{world}",
                        "l2": f"{R} rotating device-resident frames ({R * in_bytes / 1e6:.0f} MB) > 126 MB L2",
-                       "cuda_graph": not args.no_graph},
+                       "cuda_graph": not args.no_graph,
+                       "frame_call": "gc_fit_query" if args.fused else "gc_query + gc_fit"},
             "queries_per_s": S * world / (ms_step * 1e-3),
             "pairs_per_sample": n_pairs / max(n_valid, 1),
             "candidates_per_sample": n_cand / max(n_valid, 1),
@@ -379,6 +380,8 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--fused", action="store_true",
+                    help="time the fused gc_fit_query frame call instead of gc_query + gc_fit")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=200_000)
     ap.add_argument("--ref-samples", type=int, default=100_000)

@@ -102,7 +102,9 @@ gc_status gc_create(int levels, const int64_t* counts, const float* init_pos,
 gc_status gc_destroy(gc_cache c);
 
 /* Pre-size scratch for batches of up to S_fit fit samples and S_query query points, so that
- * later gc_fit/gc_query calls never allocate (required before CUDA-graph capture). */
+ * later gc_fit / gc_query / gc_fit_query(S_fit, S_query) calls never allocate (required
+ * before CUDA-graph capture).  The fit scratch is sized for S_fit + S_query so that the
+ * fused call fits. */
 gc_status gc_reserve(gc_cache c, int64_t S_fit, int64_t S_query);
 
 /* One optimisation step on a batch of S renderer samples (sec.3.5, sec.3.6):
@@ -115,6 +117,21 @@ gc_status gc_reserve(gc_cache c, int64_t S_fit, int64_t S_query);
  *  cudaMemcpyAsync, pageable memory a copy made by a stream host callback. */
 gc_status gc_fit(gc_cache c, const float* pos, const int32_t* path_len, const float* rgb,
                  int64_t S, gc_stream stream, gc_fit_stats* stats);
+
+/* One frame of the real-time loop in one call (sec.3.7): the S_q cache
+ * lookups of the frame are answered from the parameters as they are BEFORE this call's
+ * optimisation step (the frame's renderer reads the cache fitted through the previous
+ * frame), then the S fit samples take the step exactly as gc_fit.  Results equal gc_query
+ * followed by gc_fit up to fp32 summation rounding; the two sample sets share one binning
+ * pass and one staging of every cell's culling list.
+ *  pos/path_len/rgb/S: as gc_fit.  qpos [S_q][3] f32, qlen [S_q] i32 or NULL (then `qlevel`
+ *  for every lookup), attenuation/beta/unbiased_rgb: the gc_query_radiance epilogue (each
+ *  NULL = none), out_rgb [S_q][3]: caller order; all host or device.  Lookups with
+ *  qlen <= 0 or non-finite position get 0.  stats as gc_fit (fit samples only). */
+gc_status gc_fit_query(gc_cache c, const float* pos, const int32_t* path_len, const float* rgb,
+                       int64_t S, const float* qpos, const int32_t* qlen, int qlevel, int64_t S_q,
+                       const float* attenuation, const float* beta, const float* unbiased_rgb,
+                       float* out_rgb, gc_stream stream, gc_fit_stats* stats);
 
 /* Cache lookup (sec.3.1, sec.3.4): out_rgb[i] = yhat_l(x_i) (C3) for S points.
  *  pos [S][3] f32 (host or device); path_len [S] i32 (host or device) or NULL, in which case

@@ -24,7 +24,7 @@ STATUS = {0: "GC_OK", 1: "GC_ERR_ARG", 2: "GC_ERR_STATE", 3: "GC_ERR_CUDA", 4: "
 
 # Symbols include/gscache.h declares (checked by tests/test_abi.py).
 EXPORTS = ["gc_default_hparams", "gc_create", "gc_destroy", "gc_reserve", "gc_fit", "gc_query",
-           "gc_query_radiance",
+           "gc_query_radiance", "gc_fit_query",
            "gc_params", "gc_set_params", "gc_reset_schedule", "gc_grid", "gc_info",
            "gc_nccl_unique_id", "gc_set_comm", "gc_debug_enable_grads", "gc_debug_grads",
            "gc_debug_cull", "gc_debug_levels", "gc_profile_enable", "gc_profile_read",
@@ -96,6 +96,7 @@ def lib():
             "gc_fit": (i32, [vp, vp, vp, vp, i64, vp, vp]),
             "gc_query": (i32, [vp, vp, vp, i32, i64, vp, vp]),
             "gc_query_radiance": (i32, [vp, vp, vp, i32, i64, vp, vp, vp, vp, vp]),
+            "gc_fit_query": (i32, [vp, vp, vp, vp, i64, vp, vp, i32, i64, vp, vp, vp, vp, vp, vp]),
             "gc_params": (i32, [vp, i32, vp, vp]),
             "gc_set_params": (i32, [vp, i32, vp, i32, vp]),
             "gc_reset_schedule": (i32, [vp]),
@@ -176,6 +177,19 @@ class _Buf:
         self.n = a.size
 
 
+def _out_like(pos, S, out):
+    """`out` or a new [S][3] float32 array on `pos`'s device."""
+    if out is not None:
+        return out
+    try:
+        import torch
+        if isinstance(pos, torch.Tensor):
+            return torch.empty((S, 3), dtype=torch.float32, device=pos.device)
+    except ImportError:
+        pass
+    return np.empty((S, 3), np.float32)
+
+
 def _stream_ptr(stream):
     if stream is None:
         try:
@@ -235,19 +249,32 @@ class GSCache:
         self._keep = (p, n, r)
         return st
 
+    def fit_query(self, pos, path_len, rgb, qpos, qlen=None, qlevel=-1, attenuation=None,
+                  beta=None, unbiased_rgb=None, out=None, stream=None,
+                  stats: gc_fit_stats | None = None):
+        """gc_fit_query: the frame's lookups (pre-step parameters) + one fit step.  Returns
+        (out, stats)."""
+        p, n, r = _Buf(pos, np.float32), _Buf(path_len, np.int32), _Buf(rgb, np.float32)
+        S = n.n if n.n >= 0 else p.n // 3
+        qp = _Buf(qpos, np.float32)
+        Sq = qp.n // 3
+        out = _out_like(qpos, Sq, out)
+        o = _Buf(out, np.float32, writable=True)
+        qn = _Buf(qlen, np.int32)
+        at, be, un = (_Buf(attenuation, np.float32), _Buf(beta, np.float32),
+                      _Buf(unbiased_rgb, np.float32))
+        st = self._stats if stats is None else stats
+        _check(lib().gc_fit_query(self.h, p.ptr, n.ptr, r.ptr, S, qp.ptr, qn.ptr, int(qlevel), Sq,
+                                  at.ptr, be.ptr, un.ptr, o.ptr, _stream_ptr(stream), C.addressof(st)))
+        self._keep = (p, n, r)
+        self._keep_q = (qp, qn, o, at, be, un)
+        return out, st
+
     def query(self, pos, path_len=None, level=-1, out=None, stream=None):
         """Cache lookup; returns `out` (allocated like `pos` if None)."""
         p = _Buf(pos, np.float32)
         S = p.n // 3
-        if out is None:
-            try:
-                import torch
-                if isinstance(pos, torch.Tensor):
-                    out = torch.empty((S, 3), dtype=torch.float32, device=pos.device)
-            except ImportError:
-                pass
-            if out is None:
-                out = np.empty((S, 3), np.float32)
+        out = _out_like(pos, S, out)
         o = _Buf(out, np.float32, writable=True)
         n = _Buf(path_len, np.int32)
         _check(lib().gc_query(self.h, p.ptr, n.ptr, int(level), S, o.ptr, _stream_ptr(stream)))
@@ -259,15 +286,7 @@ class GSCache:
         """gc_query_radiance: lookup + natural-termination substitution + Eq. 3 scaling."""
         p = _Buf(pos, np.float32)
         S = p.n // 3
-        if out is None:
-            try:
-                import torch
-                if isinstance(pos, torch.Tensor):
-                    out = torch.empty((S, 3), dtype=torch.float32, device=pos.device)
-            except ImportError:
-                pass
-            if out is None:
-                out = np.empty((S, 3), np.float32)
+        out = _out_like(pos, S, out)
         o = _Buf(out, np.float32, writable=True)
         n = _Buf(path_len, np.int32)
         at, be, un = (_Buf(attenuation, np.float32), _Buf(beta, np.float32),
@@ -402,6 +421,11 @@ def gc_create(counts, init_pos, init_rgb, init_log_scale=None, seed=0, hparams=N
 
 def gc_fit(cache: GSCache, pos, path_len, rgb, stream=None):
     return cache.fit(pos, path_len, rgb, stream)
+
+
+def gc_fit_query(cache: GSCache, pos, path_len, rgb, qpos, qlen=None, qlevel=-1, out=None,
+                 stream=None):
+    return cache.fit_query(pos, path_len, rgb, qpos, qlen, qlevel, out=out, stream=stream)
 
 
 def gc_query(cache: GSCache, pos, path_len=None, level=-1, out=None, stream=None):

@@ -8,11 +8,15 @@
 namespace gsc {
 
 
-__global__ void __launch_bounds__(kPart * 32) k_stats(const double* __restrict__ partial, int nblocks,
+constexpr int kStatsWarps = 16;
+
+__global__ void __launch_bounds__(kStatsWarps * 32) k_stats(const double* __restrict__ partial, int nblocks,
                                                       const uint32_t* __restrict__ cell_start, LevelGeom g,
                                                       int64_t S, LvlStats* lvl) {
   pdl_enter();
-  stats_reduce(partial, nblocks, cell_start, g, S, lvl, threadIdx.x >> 5, kPart, threadIdx.x & 31);
+  stats_reduce(partial, nblocks, cell_start, g, S, lvl, threadIdx.x >> 5, kStatsWarps, threadIdx.x & 31);
+  __syncthreads();
+  if (threadIdx.x == 0) stats_totals(lvl, g, S, lvl);
 }
 
 __global__ void k_step_scalars(const LvlStats* __restrict__ lvl, DevState* st, StepHP hp,
@@ -138,7 +142,7 @@ __global__ void __launch_bounds__(256, 3) k_adamw(int64_t G, float* __restrict__
 void launch_stats(const double* partial, int nblocks, const uint32_t* cell_start,
                   const LevelGeom& g, int64_t S, LvlStats* lvl, cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "stats", s);
-  launch_pdl(k_stats, dim3(1), dim3(kPart * 32), 0, s, partial, nblocks, cell_start, g, S, lvl);
+  launch_pdl(k_stats, dim3(1), dim3(kStatsWarps * 32), 0, s, partial, nblocks, cell_start, g, S, lvl);
 }
 
 void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp, int L,

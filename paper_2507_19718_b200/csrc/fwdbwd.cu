@@ -62,7 +62,8 @@ __device__ __forceinline__ float cand_q(const Cand& g, float x, float y, float z
 // Stages one chunk and returns (warp-uniformly) whether every candidate is isotropic
 // (U = u I, exact for equal log-scales; the paper's setting).  Isotropic chunks use the
 // layout r0 = (mu - x_ref, tau^2/u^2), r1 = (-0.5 log2e u^2, v), r2.x = u^2, r3 as usual;
-// general chunks r0..r2 as documented on ChunkSmem.
+// general chunks r0..r2 as documented on ChunkSmem.  (The expanded form g|x'|^2 + g|m|^2 -
+// 2g x'.m saves 2 ops per test but its cancellation costs ~1e-5 relative: measured, rejected.)
 __device__ __forceinline__ bool stage_chunk(ChunkSmem& w, const int32_t* __restrict__ csr_idx,
                                             const float4* __restrict__ rec, int base, int kc, int lane,
                                             float xr, float yr, float zr, float tau2) {
@@ -103,10 +104,14 @@ __device__ __forceinline__ float iso_s(const float (&x)[3], const float4& c) {
 }
 
 // Isotropic chunk: s = |x' - m|^2 <= tau^2/u^2, e = 2^{-0.5 log2e u^2 s} (7 ops per test).
+// Branch-free: e is computed for every lane and zeroed outside (MUFU has the slack; a
+// divergent inside block costs more issue slots than it saves).  Record positions are
+// clamped to cap - 1: an overflowing item is re-derived by the caller, so the clobbered
+// last slot is never read.
 template <bool kRecord>
 __device__ __forceinline__ void eval_chunk_iso(const ChunkSmem& w, int kc, const float (&xa)[3], const float (&xb)[3],
                                                float (&ya)[3], float (&yb)[3], uint16_t* pkey, float* pe,
-                                               int& pbase, int cap, int lane) {
+                                               int& pbase, int cap, int lane, uint32_t fa = ~0u, uint32_t fb = ~0u) {
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll 2
   for (int k = 0; k < kc; ++k) {
@@ -114,27 +119,24 @@ __device__ __forceinline__ void eval_chunk_iso(const ChunkSmem& w, int kc, const
     const float sa = iso_s(xa, c), sb = iso_s(xb, c);
     const bool ina = sa <= c.w, inb = sb <= c.w;
     if (!kRecord) {
-      if (__any_sync(0xffffffffu, ina || inb)) {
-        if (ina) { const float e = ex2_approx(f.x * sa); ya[0] = fmaf(f.y, e, ya[0]); ya[1] = fmaf(f.z, e, ya[1]); ya[2] = fmaf(f.w, e, ya[2]); }
-        if (inb) { const float e = ex2_approx(f.x * sb); yb[0] = fmaf(f.y, e, yb[0]); yb[1] = fmaf(f.z, e, yb[1]); yb[2] = fmaf(f.w, e, yb[2]); }
-      }
+      const float xa_ = ex2_approx(f.x * sa), xb_ = ex2_approx(f.x * sb);
+      const float ea = ina ? xa_ : 0.f, eb = inb ? xb_ : 0.f;
+      ya[0] = fmaf(f.y, ea, ya[0]); ya[1] = fmaf(f.z, ea, ya[1]); ya[2] = fmaf(f.w, ea, ya[2]);
+      yb[0] = fmaf(f.y, eb, yb[0]); yb[1] = fmaf(f.z, eb, yb[1]); yb[2] = fmaf(f.w, eb, yb[2]);
       continue;
     }
-    const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = __ballot_sync(0xffffffffu, inb);
-    if (ma | mb) {
-      if (ina) {
-        const float e = ex2_approx(f.x * sa);
-        ya[0] = fmaf(f.y, e, ya[0]); ya[1] = fmaf(f.z, e, ya[1]); ya[2] = fmaf(f.w, e, ya[2]);
-        const int pos = pbase + __popc(ma & lt);
-        if (pos < cap) { pkey[pos] = (uint16_t)((k << 6) | lane); pe[pos] = e; }
-      }
-      if (inb) {
-        const float e = ex2_approx(f.x * sb);
-        yb[0] = fmaf(f.y, e, yb[0]); yb[1] = fmaf(f.z, e, yb[1]); yb[2] = fmaf(f.w, e, yb[2]);
-        const int pos = pbase + __popc(ma) + __popc(mb & lt);
-        if (pos < cap) { pkey[pos] = (uint16_t)((k << 6) | (lane + 32)); pe[pos] = e; }
-      }
-      pbase += __popc(ma) + __popc(mb);
+    const uint32_t ia = __ballot_sync(0xffffffffu, ina), ib = __ballot_sync(0xffffffffu, inb);
+    if (ia | ib) {
+      const uint32_t ma = ia & fa, mb = ib & fb;      // pairs of fitted samples only
+      const float xa_ = ex2_approx(f.x * sa), xb_ = ex2_approx(f.x * sb);
+      const float ea = ina ? xa_ : 0.f, eb = inb ? xb_ : 0.f;
+      ya[0] = fmaf(f.y, ea, ya[0]); ya[1] = fmaf(f.z, ea, ya[1]); ya[2] = fmaf(f.w, ea, ya[2]);
+      yb[0] = fmaf(f.y, eb, yb[0]); yb[1] = fmaf(f.z, eb, yb[1]); yb[2] = fmaf(f.w, eb, yb[2]);
+      const int na = __popc(ma);
+      const int pa = min(pbase + __popc(ma & lt), cap - 1), pb = min(pbase + na + __popc(mb & lt), cap - 1);
+      if ((ma >> lane) & 1u) { pkey[pa] = (uint16_t)((k << 6) | lane); pe[pa] = ea; }
+      if ((mb >> lane) & 1u) { pkey[pb] = (uint16_t)((k << 6) | (lane + 32)); pe[pb] = eb; }
+      pbase += na + __popc(mb);
     }
   }
   __syncwarp();
@@ -146,7 +148,8 @@ __device__ __forceinline__ void eval_chunk_iso(const ChunkSmem& w, int kc, const
 template <bool kRecord>
 __device__ __forceinline__ void eval_chunk(const ChunkSmem& w, int kc, const float (&xa)[3], const float (&xb)[3],
                                            float tau2, float (&ya)[3], float (&yb)[3],
-                                           uint16_t* pkey, float* pe, int& pbase, int cap, int lane) {
+                                           uint16_t* pkey, float* pe, int& pbase, int cap, int lane,
+                                           uint32_t fa = ~0u, uint32_t fb = ~0u) {
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll 2
   for (int k = 0; k < kc; ++k) {
@@ -156,31 +159,24 @@ __device__ __forceinline__ void eval_chunk(const ChunkSmem& w, int kc, const flo
     const float Qb = cand_q(g, xb[0], xb[1], xb[2], w0, w1, w2);
     const bool ina = Qa <= tau2, inb = Qb <= tau2;
     if (!kRecord) {
-      if (__any_sync(0xffffffffu, ina || inb)) {
-        if (ina) { const float e = ex2_approx(Qa * kNegHalfLog2e); ya[0] = fmaf(g.v0, e, ya[0]); ya[1] = fmaf(g.v1, e, ya[1]); ya[2] = fmaf(g.v2, e, ya[2]); }
-        if (inb) { const float e = ex2_approx(Qb * kNegHalfLog2e); yb[0] = fmaf(g.v0, e, yb[0]); yb[1] = fmaf(g.v1, e, yb[1]); yb[2] = fmaf(g.v2, e, yb[2]); }
-      }
+      const float xa_ = ex2_approx(Qa * kNegHalfLog2e), xb_ = ex2_approx(Qb * kNegHalfLog2e);
+      const float ea = ina ? xa_ : 0.f, eb = inb ? xb_ : 0.f;
+      ya[0] = fmaf(g.v0, ea, ya[0]); ya[1] = fmaf(g.v1, ea, ya[1]); ya[2] = fmaf(g.v2, ea, ya[2]);
+      yb[0] = fmaf(g.v0, eb, yb[0]); yb[1] = fmaf(g.v1, eb, yb[1]); yb[2] = fmaf(g.v2, eb, yb[2]);
       continue;
     }
-    const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = __ballot_sync(0xffffffffu, inb);
-    if (ma | mb) {
-      if (ina) {
-        const float e = ex2_approx(Qa * kNegHalfLog2e);
-        ya[0] = fmaf(g.v0, e, ya[0]); ya[1] = fmaf(g.v1, e, ya[1]); ya[2] = fmaf(g.v2, e, ya[2]);
-        if (kRecord) {
-          const int pos = pbase + __popc(ma & lt);
-          if (pos < cap) { pkey[pos] = (uint16_t)((k << 6) | lane); pe[pos] = e; }
-        }
-      }
-      if (inb) {
-        const float e = ex2_approx(Qb * kNegHalfLog2e);
-        yb[0] = fmaf(g.v0, e, yb[0]); yb[1] = fmaf(g.v1, e, yb[1]); yb[2] = fmaf(g.v2, e, yb[2]);
-        if (kRecord) {
-          const int pos = pbase + __popc(ma) + __popc(mb & lt);
-          if (pos < cap) { pkey[pos] = (uint16_t)((k << 6) | (lane + 32)); pe[pos] = e; }
-        }
-      }
-      if (kRecord) pbase += __popc(ma) + __popc(mb);
+    const uint32_t ia = __ballot_sync(0xffffffffu, ina), ib = __ballot_sync(0xffffffffu, inb);
+    if (ia | ib) {
+      const uint32_t ma = ia & fa, mb = ib & fb;      // pairs of fitted samples only
+      const float xa_ = ex2_approx(Qa * kNegHalfLog2e), xb_ = ex2_approx(Qb * kNegHalfLog2e);
+      const float ea = ina ? xa_ : 0.f, eb = inb ? xb_ : 0.f;
+      ya[0] = fmaf(g.v0, ea, ya[0]); ya[1] = fmaf(g.v1, ea, ya[1]); ya[2] = fmaf(g.v2, ea, ya[2]);
+      yb[0] = fmaf(g.v0, eb, yb[0]); yb[1] = fmaf(g.v1, eb, yb[1]); yb[2] = fmaf(g.v2, eb, yb[2]);
+      const int na = __popc(ma);
+      const int pa = min(pbase + __popc(ma & lt), cap - 1), pb = min(pbase + na + __popc(mb & lt), cap - 1);
+      if ((ma >> lane) & 1u) { pkey[pa] = (uint16_t)((k << 6) | lane); pe[pa] = ea; }
+      if ((mb >> lane) & 1u) { pkey[pb] = (uint16_t)((k << 6) | (lane + 32)); pe[pb] = eb; }
+      pbase += na + __popc(mb);
     }
   }
   __syncwarp();
@@ -295,15 +291,34 @@ __device__ __forceinline__ void hdr_grad(int mode, float eps, const float (&y)[3
   }
 }
 
+// Output of one query in caller order, with the optional renderer epilogue (f3): natural
+// termination keeps a non-zero unbiased radiance (P:87-90); otherwise Eq. 3 (P:162),
+// yhat * attenuation / beta.
+__device__ __forceinline__ void query_out(float* out, const float* att, const float* beta, const float* unb,
+                                          int64_t i, const float (&y)[3]) {
+  float o0 = y[0], o1 = y[1], o2 = y[2];
+  if (att) { o0 *= att[3 * i]; o1 *= att[3 * i + 1]; o2 *= att[3 * i + 2]; }
+  if (beta) { const float ib = 1.f / beta[i]; o0 *= ib; o1 *= ib; o2 *= ib; }
+  if (unb) {
+    const float u0 = unb[3 * i], u1 = unb[3 * i + 1], u2 = unb[3 * i + 2];
+    if (u0 != 0.f || u1 != 0.f || u2 != 0.f) { o0 = u0; o1 = u1; o2 = u2; }
+  }
+  __stcs(out + 3 * i, o0); __stcs(out + 3 * i + 1, o1); __stcs(out + 3 * i + 2, o2);
+}
+
+// kQ: lookups ride along in the bins (gc_fit_query); instantiated apart so that gc_fit's
+// kernel carries no query bookkeeping.
+template <bool kQ>
 __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
   pdl_enter();
   extern __shared__ __align__(16) unsigned char dsm[];
   WarpSmem* sm = reinterpret_cast<WarpSmem*>(dsm);
   __shared__ double s_loss[kWarps][kMaxL];
   __shared__ unsigned long long s_cnt[kWarps][2];
+  __shared__ uint32_t s_nfit[kWarps][kMaxL];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpSmem& w = sm[wid];
-  if (lane < kMaxL) s_loss[wid][lane] = 0.0;
+  if (lane < kMaxL) { s_loss[wid][lane] = 0.0; s_nfit[wid][lane] = 0u; }
   unsigned long long pairs_acc = 0, cand_acc = 0;
   const uint32_t n_work = a.n_work[0];
   uint32_t* next = const_cast<uint32_t*>(a.n_work) + 1;   // dynamic work counter (zeroed by the scan)
@@ -321,18 +336,38 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
     float4 pa, pb4;
     load_pos(a.bin, 2, wi.start, wi.count, lane, xa, pa);
     load_pos(a.bin, 2, wi.start, wi.count, lane + 32, xb, pb4);
+    bool fita = false, fitb = false;              // fitted sample (else a query riding along, q.z = 1)
     if (lane < wi.count) {
       const float4 q = __ldcs(a.bin + 2 * (int64_t)(wi.start + lane) + 1);
       ta[0] = pa.w; ta[1] = q.x; ta[2] = q.y;
+      fita = !kQ || q.z == 0.f;
     }
     if (lane + 32 < wi.count) {
       const float4 q = __ldcs(a.bin + 2 * (int64_t)(wi.start + lane + 32) + 1);
       tb[0] = pb4.w; tb[1] = q.x; tb[2] = q.y;
+      fitb = !kQ || q.z == 0.f;
     }
+    const uint32_t fa = kQ ? __ballot_sync(0xffffffffu, fita) : ~0u;
+    const uint32_t fb = kQ ? __ballot_sync(0xffffffffu, fitb) : ~0u;
+    const int nfit = kQ ? __popc(fa) + __popc(fb) : wi.count;
     const float xref = __shfl_sync(0xffffffffu, xa[0], 0), yref = __shfl_sync(0xffffffffu, xa[1], 0),
                 zref = __shfl_sync(0xffffffffu, xa[2], 0);
     xa[0] -= xref; xa[1] -= yref; xa[2] -= zref;            // NaN stays NaN
     xb[0] -= xref; xb[1] -= yref; xb[2] -= zref;
+    if (kQ && nfit == 0) {                      // lookups only: gc_query's forward pass
+      float ya[3] = {0.f, 0.f, 0.f}, yb[3] = {0.f, 0.f, 0.f};
+      int pbase = 0;
+      for (int cb = 0; cb < C; cb += 32) {
+        const int kc = min(32, C - cb);
+        if (stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref, tau2))
+          eval_chunk_iso<false>(w, kc, xa, xb, ya, yb, nullptr, nullptr, pbase, 0, lane);
+        else
+          eval_chunk<false>(w, kc, xa, xb, tau2, ya, yb, nullptr, nullptr, pbase, 0, lane);
+      }
+      if (lane < wi.count) query_out(a.out, a.att, a.beta, a.unb, __float_as_uint(pa.w), ya);
+      if (lane + 32 < wi.count) query_out(a.out, a.att, a.beta, a.unb, __float_as_uint(pb4.w), yb);
+      continue;
+    }
     // ---------------- pass 1 (records the inside pairs while they fit)
     float ya[3] = {0.f, 0.f, 0.f}, yb[3] = {0.f, 0.f, 0.f};
     int pbase = 0;
@@ -341,25 +376,27 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
     for (int cb = 0, c = 0; cb < C; cb += 32, ++c) {
       const int kc = min(32, C - cb);
       iso = stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref, tau2);
-      if (iso) eval_chunk_iso<true>(w, kc, xa, xb, ya, yb, w.pkey, w.pe, pbase, kPairCap, lane);
-      else eval_chunk<true>(w, kc, xa, xb, tau2, ya, yb, w.pkey, w.pe, pbase, kPairCap, lane);
+      if (iso) eval_chunk_iso<true>(w, kc, xa, xb, ya, yb, w.pkey, w.pe, pbase, kPairCap, lane, fa, fb);
+      else eval_chunk<true>(w, kc, xa, xb, tau2, ya, yb, w.pkey, w.pe, pbase, kPairCap, lane, fa, fb);
       if (lane == 0 && c < kMaxChunks) w.cend[c] = (uint16_t)min(pbase, 0xFFFF);
     }
     const int np = pbase;                        // inside pairs of the item (warp-uniform)
     const bool recorded = chunks_fit && pbase <= kPairCap;
     // ---------------- Eq. 4 loss and dL/dyhat (unnormalised)
     float ga[3] = {0.f, 0.f, 0.f}, gb[3] = {0.f, 0.f, 0.f}, ls = 0.f;
-    if (lane < wi.count) hdr_grad(a.mode, eps, ya, ta, ga, ls);
-    if (lane + 32 < wi.count) hdr_grad(a.mode, eps, yb, tb, gb, ls);
+    if (fita) hdr_grad(a.mode, eps, ya, ta, ga, ls);
+    else if (kQ && lane < wi.count) query_out(a.out, a.att, a.beta, a.unb, __float_as_uint(pa.w), ya);
+    if (fitb) hdr_grad(a.mode, eps, yb, tb, gb, ls);
+    else if (kQ && lane + 32 < wi.count) query_out(a.out, a.att, a.beta, a.unb, __float_as_uint(pb4.w), yb);
     w.sxg[lane] = make_float4(xa[0], xa[1], xa[2], ga[0]);
     w.sg[lane] = make_float2(ga[1], ga[2]);
     w.sxg[lane + 32] = make_float4(xb[0], xb[1], xb[2], gb[0]);
     w.sg[lane + 32] = make_float2(gb[1], gb[2]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
-    if (lane == 0) s_loss[wid][wi.level] += (double)ls;
+    if (lane == 0) { s_loss[wid][wi.level] += (double)ls; s_nfit[wid][wi.level] += (uint32_t)nfit; }
     pairs_acc += (unsigned)np;
-    cand_acc += (unsigned long long)wi.count * (unsigned long long)C;
+    cand_acc += (unsigned long long)nfit * (unsigned long long)C;
     __syncwarp();
     if (np == 0) continue;
     // ---------------- pass 2
@@ -395,15 +432,15 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
             ina = Qa <= tau2; inb = Qb <= tau2;
             ea = ex2_approx(Qa * kNegHalfLog2e); eb = ex2_approx(Qb * kNegHalfLog2e);
           }
-          const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = __ballot_sync(0xffffffffu, inb);
+          const uint32_t ma = __ballot_sync(0xffffffffu, ina) & fa, mb = __ballot_sync(0xffffffffu, inb) & fb;
           if (!(ma | mb)) continue;
           if (pb + 64 > kPairCap) { chunk_pairs_bwd(w, 0, pb, a.grad, lane, ci, a.lite); pb = 0; }
-          if (ina) {
+          if ((ma >> lane) & 1u) {
             const int pos = pb + __popc(ma & lt);
             w.pkey[pos] = (uint16_t)((k << 6) | lane);
             w.pe[pos] = ea;
           }
-          if (inb) {
+          if ((mb >> lane) & 1u) {
             const int pos = pb + __popc(ma) + __popc(mb & lt);
             w.pkey[pos] = (uint16_t)((k << 6) | (lane + 32));
             w.pe[pos] = eb;
@@ -420,14 +457,16 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
   double* part = a.partial + (int64_t)blockIdx.x * kPart;
   if (threadIdx.x < kMaxL) {
     double s = 0.0;
-    for (int q = 0; q < kWarps; ++q) s += s_loss[q][threadIdx.x];
+    unsigned long long n = 0;
+    for (int q = 0; q < kWarps; ++q) { s += s_loss[q][threadIdx.x]; n += s_nfit[q][threadIdx.x]; }
     part[threadIdx.x] = s;
+    part[kMaxL + threadIdx.x] = (double)n;
   }
   if (threadIdx.x == 0) {
     unsigned long long p = 0, c = 0;
     for (int q = 0; q < kWarps; ++q) { p += s_cnt[q][0]; c += s_cnt[q][1]; }
-    part[kMaxL] = (double)p;
-    part[kMaxL + 1] = (double)c;
+    part[2 * kMaxL] = (double)p;
+    part[2 * kMaxL + 1] = (double)c;
   }
   if (!a.fused) return;
   // single GPU: the last CTA to finish reduces the statistics and takes the step scalars
@@ -441,22 +480,10 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
   __threadfence();
   stats_reduce(a.partial, gridDim.x, a.cell_start, a.geom, a.S, a.lvl, wid, kWarps, lane);
   __syncthreads();
+  if (threadIdx.x == 0) stats_totals(a.lvl, a.geom, a.S, a.lvl);
+  __syncthreads();
   if (wid == 0) step_scalars_warp(a.lvl, a.st, a.shp, a.dstats, lane);
   if (threadIdx.x == 0) a.st->done = 0u;
-}
-
-// Output of one query in caller order, with the optional renderer epilogue (f3): natural
-// termination keeps a non-zero unbiased radiance (P:87-90); otherwise Eq. 3 (P:162),
-// yhat * attenuation / beta.
-__device__ __forceinline__ void query_out(const QueryArgs& a, int64_t i, const float (&y)[3]) {
-  float o0 = y[0], o1 = y[1], o2 = y[2];
-  if (a.att) { o0 *= a.att[3 * i]; o1 *= a.att[3 * i + 1]; o2 *= a.att[3 * i + 2]; }
-  if (a.beta) { const float ib = 1.f / a.beta[i]; o0 *= ib; o1 *= ib; o2 *= ib; }
-  if (a.unb) {
-    const float u0 = a.unb[3 * i], u1 = a.unb[3 * i + 1], u2 = a.unb[3 * i + 2];
-    if (u0 != 0.f || u1 != 0.f || u2 != 0.f) { o0 = u0; o1 = u1; o2 = u2; }
-  }
-  __stcs(a.out + 3 * i, o0); __stcs(a.out + 3 * i + 1, o1); __stcs(a.out + 3 * i + 2, o2);
 }
 
 __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
@@ -492,8 +519,8 @@ __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
       else
         eval_chunk<false>(w, kc, xa, xb, tau2, ya, yb, nullptr, nullptr, pbase, 0, lane);
     }
-    if (lane < wi.count) query_out(a, __float_as_uint(pa.w), ya);
-    if (lane + 32 < wi.count) query_out(a, __float_as_uint(pb4.w), yb);
+    if (lane < wi.count) query_out(a.out, a.att, a.beta, a.unb, __float_as_uint(pa.w), ya);
+    if (lane + 32 < wi.count) query_out(a.out, a.att, a.beta, a.unb, __float_as_uint(pb4.w), yb);
   }
 }
 
@@ -509,8 +536,10 @@ static int persistent_grid(const void* fn, size_t smem) {
 
 int fwdbwd_grid() {
   static int g = [] {
-    cudaFuncSetAttribute(k_fwdbwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdBwdSmem);
-    return persistent_grid((const void*)k_fwdbwd, kFwdBwdSmem);
+    cudaFuncSetAttribute(k_fwdbwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdBwdSmem);
+    cudaFuncSetAttribute(k_fwdbwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdBwdSmem);
+    return std::min(persistent_grid((const void*)k_fwdbwd<false>, kFwdBwdSmem),
+                    persistent_grid((const void*)k_fwdbwd<true>, kFwdBwdSmem));
   }();
   return g;
 }
@@ -518,7 +547,8 @@ int query_grid() { static int g = persistent_grid((const void*)k_query, 0); retu
 
 void launch_fwdbwd(const FitArgs& a, int grid, cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "fwdbwd", s);
-  launch_pdl(k_fwdbwd, dim3(grid), dim3(256), kFwdBwdSmem, s, a);
+  if (a.out) launch_pdl(k_fwdbwd<true>, dim3(grid), dim3(256), kFwdBwdSmem, s, a);
+  else launch_pdl(k_fwdbwd<false>, dim3(grid), dim3(256), kFwdBwdSmem, s, a);
 }
 
 void launch_query(const QueryArgs& a, int grid, cudaStream_t s, Profiler* prof) {

@@ -6,15 +6,16 @@
 
 namespace gsc {
 
-constexpr int kPart = kMaxL + 2;     // per-CTA partial: loss sums [kMaxL], pairs, candidates
+// per-CTA partial of k_fwdbwd: loss sums [kMaxL], fitted-sample counts [kMaxL], pairs, candidates
+constexpr int kPart = 2 * kMaxL + 2;
 
 struct StepHP {
   float lr[GC_NGROUPS]; float beta1, beta2; int schedule; int L;
 };
 
-// Sums the per-CTA partials (one warp per column, columns strided over nwarps warps) and
-// derives k_l from the binned cell offsets at the level boundaries.
-__device__ __forceinline__ void stats_reduce(const double* partial, int nblocks, const uint32_t* cell_start,
+// Sums the per-CTA partials (one warp per column, columns strided over nwarps warps): loss
+// sums, k_l (valid fitted samples per level) and the pair / candidate counters.
+__device__ __forceinline__ void stats_reduce(const double* partial, int nblocks, const uint32_t* /*unused*/,
                                              const LevelGeom& g, int64_t S, LvlStats* lvl, int warp,
                                              int nwarps, int lane) {
   for (int col = warp; col < kPart; col += nwarps) {
@@ -25,22 +26,18 @@ __device__ __forceinline__ void stats_reduce(const double* partial, int nblocks,
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) {
       if (col < kMaxL) lvl->loss_sum[col] = acc;
-      else if (col == kMaxL) lvl->n_pairs = acc;
+      else if (col < 2 * kMaxL) lvl->count[col - kMaxL] = col - kMaxL < g.L ? acc : 0.0;
+      else if (col == 2 * kMaxL) lvl->n_pairs = acc;
       else lvl->n_cand = acc;
     }
   }
-  if (warp == 0) {
-    double c = 0.0;
-    // start of cell c in the replica-major offsets: replica-0 row; end sentinel at kRep * NC
-    const int64_t nc = g.coff[g.L];
-    auto at = [&](int64_t cc) { return __ldcg(cell_start + (cc == nc ? nc * kRep : cc)); };
-    if (lane < g.L) c = (double)(at(g.coff[lane + 1]) - at(g.coff[lane]));
-    if (lane < kMaxL) lvl->count[lane] = c;
-    double tot = c;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    if (lane == 0) { lvl->n_valid = tot; lvl->n_in = (double)S; }
-  }
+}
+
+__device__ __forceinline__ void stats_totals(const LvlStats* lvl, const LevelGeom& g, int64_t S, LvlStats* out) {
+  double tot = 0.0;
+  for (int l = 0; l < g.L; ++l) tot += lvl->count[l];
+  out->n_valid = tot;
+  out->n_in = (double)S;
 }
 
 // One warp: Eq. 5 schedule, per-level skip (A12), bias corrections, stats.  Lane l

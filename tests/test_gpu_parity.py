@@ -471,3 +471,107 @@ def test_cfg3_adaptation_after_light_change():
     assert all(curves[True][f] <= curves[False][f] for f in after)  # reset adapts faster
     rec = {r: min([f for f in after if curves[r][f] <= e_pre] or [10 ** 9]) for r in (True, False)}
     assert rec[True] <= rec[False]
+
+
+# ------------------------------------------- fused frame call (lookups + fit step)
+def _aniso_cfg1(gsc, hp=None):
+    c, _, _ = make_cfg1(gsc, hp=hp)
+    r = np.random.default_rng(6)
+    P0 = c.params_rows(0)
+    P0[:, 3:7] = r.normal(size=(4096, 4)).astype(np.float32)
+    P0[:, 10:13] += r.uniform(-0.3, 0.3, (4096, 3)).astype(np.float32)
+    c.set_params_rows(0, P0)
+    return c
+
+
+def test_fit_query_lookups_and_gradients(gsc):
+    """gc_fit_query: lookups use the pre-step parameters (C3 vs oracle.query), the fit part
+    is gc_fit's (C4/C5 vs oracle.loss_grad), invalid lookups get 0."""
+    c = _aniso_cfg1(gsc)
+    P = rows(c)
+    c.debug_enable_grads(True)
+    x, ln, rgb = workload.fit_batch(1)
+    xq, lq = workload.query_batch(1, frame=4)
+    lq[::13] = 0
+    xq[::17, 0] = np.nan
+    y, st = c.fit_query(cuda(x), cuda(ln), cuda(rgb), cuda(xq), cuda(lq))
+    torch.cuda.synchronize()
+    y = y.cpu().numpy()
+    yo, lv, _ = oracle.query(c.goff, P, xq.astype(np.float64), lq, grids=c.grids())
+    assert np.all(y[lv < 0] == 0) and (lv < 0).sum() > 0
+    ok = lv >= 0
+    check_forward(y[ok], yo[ok], P, c.goff, xq[ok], lv[ok], what="fit_query lookups")
+    g = np.concatenate([c.debug_grads_rows(l) for l in range(3)]).astype(np.float64)
+    ro = oracle.loss_grad(c.goff, P, x.astype(np.float64), ln, rgb.astype(np.float64), grids=c.grids())
+    for l in range(3):
+        assert st.count[l] == ro["count"][l]
+        assert abs(st.loss[l] - ro["loss"][l]) <= 1e-4 * ro["loss"][l]
+        sl = slice(c.goff[l], c.goff[l + 1])
+        for name, cs in oracle.GROUP_SLICES.items():
+            a, b = g[sl, cs], ro["grad"][sl, cs]
+            if name == "rotation" and l > 0:
+                assert np.linalg.norm(a) <= 1e-4 * np.linalg.norm(ro["grad"][sl]) + 1e-12
+                continue
+            assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-4, (l, name)
+    assert st.step == 1 and st.n_in == len(x)
+
+
+def test_fit_query_equals_query_then_fit(gsc):
+    """Same step as gc_query followed by gc_fit (lite path: isotropic, scales frozen)."""
+    c1, _, _ = make_cfg1(gsc)
+    c2, _, _ = make_cfg1(gsc)
+    for frame in range(3):
+        x, ln, rgb = workload.fit_batch(1, frame=frame, S=100_000)
+        xq, lq = workload.query_batch(1, frame=frame, S=50_000)
+        y1, s1 = c1.fit_query(cuda(x), cuda(ln), cuda(rgb), cuda(xq), cuda(lq))
+        torch.cuda.synchronize()
+        l1 = list(s1.loss[:3]); n1 = list(s1.count[:3])
+        y2 = c2.query(cuda(xq), cuda(lq))
+        s2 = c2.fit(cuda(x), cuda(ln), cuda(rgb))
+        torch.cuda.synchronize()
+        np.testing.assert_allclose(y1.cpu().numpy(), y2.cpu().numpy(), rtol=2e-5, atol=1e-7)
+        assert n1 == list(s2.count[:3])
+        np.testing.assert_allclose(l1, list(s2.loss[:3]), rtol=2e-5)
+    np.testing.assert_allclose(rows(c1), rows(c2), rtol=1e-4, atol=2e-5)
+
+
+@pytest.mark.parametrize("S_fit,S_q", [(0, 300), (257, 1), (5000, 33), (1, 4097)])
+def test_fit_query_ragged_host_buffers_and_epilogue(gsc, S_fit, S_q):
+    c, _, _ = make_cfg1(gsc, counts=(4096, 700, 33))
+    P = rows(c)
+    x, ln, rgb = workload.fit_batch(1, frame=S_fit, S=max(S_fit, 1))
+    x, ln, rgb = x[:S_fit], ln[:S_fit], rgb[:S_fit]
+    xq, lq = workload.query_batch(1, frame=S_q, S=S_q)
+    r = np.random.default_rng(S_q)
+    att = r.uniform(0.1, 1.0, (S_q, 3)).astype(np.float32)
+    beta = r.uniform(0.2, 1.0, S_q).astype(np.float32)
+    y, st = c.fit_query(x, ln, rgb, xq, lq, attenuation=att, beta=beta)     # host buffers
+    torch.cuda.synchronize()
+    yo, lv, _ = oracle.query(c.goff, P, xq.astype(np.float64), lq, grids=c.grids())
+    check_forward(y / (att / beta[:, None]), yo, P, c.goff, xq, lv, what=f"{S_fit},{S_q}")
+    assert st.n_in == S_fit and st.step == (1 if (ln > 0).any() else 0)
+
+
+def test_fit_query_graph_replay_matches_eager(gsc):
+    c1, _, _ = make_cfg1(gsc)
+    c2, _, _ = make_cfg1(gsc)
+    x, ln, rgb = [cuda(a) for a in workload.fit_batch(1, S=60_000)]
+    xq, lq = [cuda(a) for a in workload.query_batch(1, S=30_000)]
+    c2.reserve(60_000, 30_000)
+    out = torch.empty((30_000, 3), device="cuda")
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        c2.fit_query(x, ln, rgb, xq, lq, out=out, stream=st)        # warm (allocations done)
+    torch.cuda.synchronize()
+    c1.fit_query(x, ln, rgb, xq, lq)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        c2.fit_query(x, ln, rgb, xq, lq, out=out, stream=st)
+    for _ in range(3):
+        y1, _ = c1.fit_query(x, ln, rgb, xq, lq)
+        g.replay()
+        torch.cuda.synchronize()
+        # bin order inside a cell and gradient atomics are unordered: fp32 rounding only
+        np.testing.assert_allclose(y1.cpu().numpy(), out.cpu().numpy(), rtol=2e-5, atol=1e-7)
+    np.testing.assert_allclose(rows(c1), rows(c2), rtol=1e-5, atol=1e-6)
