@@ -8,15 +8,21 @@
 namespace gsc {
 
 
-constexpr int kStatsWarps = 16;
+constexpr int kStatsWarps = 32;
 
+// Level statistics of the call; with do_step (single GPU: no all-reduce in between) warp 0
+// then takes the step scalars in the same launch.
 __global__ void __launch_bounds__(kStatsWarps * 32) k_stats(const double* __restrict__ partial, int nblocks,
                                                       const uint32_t* __restrict__ cell_start, LevelGeom g,
-                                                      int64_t S, LvlStats* lvl) {
+                                                      int64_t S, LvlStats* lvl, int do_step, DevState* st,
+                                                      StepHP hp, gc_fit_stats* out) {
   pdl_enter();
   stats_reduce(partial, nblocks, cell_start, g, S, lvl, threadIdx.x >> 5, kStatsWarps, threadIdx.x & 31);
   __syncthreads();
   if (threadIdx.x == 0) stats_totals(lvl, g, S, lvl);
+  if (!do_step) return;
+  __syncthreads();
+  if (threadIdx.x < 32) step_scalars_warp(lvl, st, hp, out, threadIdx.x);
 }
 
 __global__ void k_step_scalars(const LvlStats* __restrict__ lvl, DevState* st, StepHP hp,
@@ -139,18 +145,24 @@ __global__ void __launch_bounds__(256, 3) k_adamw(int64_t G, float* __restrict__
   if ((threadIdx.x & 31) == 0 && bad) atomicAdd(reinterpret_cast<unsigned long long*>(&out->nonfinite_grads), bad);
 }
 
-void launch_stats(const double* partial, int nblocks, const uint32_t* cell_start,
-                  const LevelGeom& g, int64_t S, LvlStats* lvl, cudaStream_t s, Profiler* prof) {
+static StepHP step_hp(const gc_hparams& hp, int L) {
+  StepHP h;
+  for (int k = 0; k < GC_NGROUPS; ++k) h.lr[k] = hp.lr[k];
+  h.beta1 = hp.beta1; h.beta2 = hp.beta2; h.schedule = hp.lr_schedule; h.L = L;
+  return h;
+}
+
+void launch_stats(const double* partial, int nblocks, const uint32_t* cell_start, const LevelGeom& g, int64_t S,
+                  LvlStats* lvl, bool with_step, DevState* st, const gc_hparams& hp, int L,
+                  gc_fit_stats* dev_stats, cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "stats", s);
-  launch_pdl(k_stats, dim3(1), dim3(kStatsWarps * 32), 0, s, partial, nblocks, cell_start, g, S, lvl);
+  launch_pdl(k_stats, dim3(1), dim3(kStatsWarps * 32), 0, s, partial, nblocks, cell_start, g, S, lvl,
+             with_step ? 1 : 0, st, step_hp(hp, L), dev_stats);
 }
 
 void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp, int L,
                          gc_fit_stats* dev_stats, cudaStream_t s) {
-  StepHP h;
-  for (int k = 0; k < GC_NGROUPS; ++k) h.lr[k] = hp.lr[k];
-  h.beta1 = hp.beta1; h.beta2 = hp.beta2; h.schedule = hp.lr_schedule; h.L = L;
-  launch_pdl(k_step_scalars, dim3(1), dim3(32), 0, s, lvl, st, h, dev_stats);
+  launch_pdl(k_step_scalars, dim3(1), dim3(32), 0, s, lvl, st, step_hp(hp, L), dev_stats);
 }
 
 void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, float4* rec, uint4* range,

@@ -540,14 +540,16 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
   fa.shp.beta1 = c->hp.beta1; fa.shp.beta2 = c->hp.beta2; fa.shp.schedule = c->hp.lr_schedule; fa.shp.L = c->L;
   launch_fwdbwd(fa, c->fb_grid, s, &c->prof);
   if (hout) CK(cudaMemcpyAsync(out_rgb, dout, sizeof(float) * 3 * S_q, cudaMemcpyDeviceToHost, s));
-  if (!fa.fused) launch_stats(c->partial, c->fb_grid, F.cell_start, c->geom, S, c->lvl, s, &c->prof);
+  if (!fa.fused)                    // single GPU: the step scalars ride in the same launch
+    launch_stats(c->partial, c->fb_grid, F.cell_start, c->geom, S, c->lvl, !dp, c->st, c->hp, c->L, c->dstats, s,
+                 &c->prof);
   if (dp) {                         // data parallel: one sum over ranks of grads + level stats
     NK(ncclGroupStart());
     NK(ncclAllReduce(c->grad, c->grad, (size_t)12 * c->G, ncclFloat32, ncclSum, c->comm, s));
     NK(ncclAllReduce(c->lvl, c->lvl, sizeof(LvlStats) / sizeof(double), ncclFloat64, ncclSum, c->comm, s));
     NK(ncclGroupEnd());
   }
-  if (!fa.fused) launch_step_scalars(c->lvl, c->st, c->hp, c->L, c->dstats, s);
+  if (!fa.fused && dp) launch_step_scalars(c->lvl, c->st, c->hp, c->L, c->dstats, s);
   launch_adamw(c->G, c->P, c->M, c->V, c->grad, c->rec, c->range, c->rad2, c->csr_count, c->dbg_on ? c->dbg : nullptr,
                c->st, c->hp, c->geom, c->dstats, s, &c->prof);
   if (gc_status e = rebuild_csr(c, s, false)) return e;

@@ -137,7 +137,7 @@ __device__ __forceinline__ void load_counts(const uint32_t* cnt, int64_t n, int 
 
 // Single-pass scan with decoupled look-back.  Tiles are taken in ticket order (so every
 // predecessor is already running); a tile publishes its aggregate, warp 0 walks back over
-// its predecessors 32 at a time until it meets an inclusive prefix, publishes its own
+// its predecessors 256 at a time until it meets an inclusive prefix, publishes its own
 // inclusive prefix, and the block then writes the exclusive offsets (and an optional copy
 // used as atomic cursors) and, with ch > 0, one WorkItem per chunk of <= ch samples of every
 // non-empty cell.  The counts are zeroed after reading (ready for the next call) and the last
@@ -190,16 +190,34 @@ __global__ void __launch_bounds__(256) k_scan(uint32_t* __restrict__ cnt, int64_
       if (lane == 0) atomicExch(cur, st_pack(2u, total));
     } else {
       if (lane == 0) atomicExch(cur + tile, st_pack(1u, total));
+      // each round covers 256 predecessors (8 per lane, lane L owns j-8L .. j-8L-7, all
+      // loads in flight together): a tile walks back over a few rounds at most, even when
+      // every predecessor has only published its aggregate
       int j = tile - 1;
       for (;;) {
-        const int idx = j - lane;
-        unsigned long long w = st_pack(2u, make_uint2(0, 0));   // before tile 0: inclusive 0
-        if (idx >= 0) {
-          do { w = *(volatile unsigned long long*)(cur + idx); } while (st_flag(w) == 0u);
+        unsigned long long w[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int idx = j - 8 * lane - q;
+          w[q] = idx >= 0 ? *(volatile unsigned long long*)(cur + idx) : st_pack(2u, make_uint2(0, 0));
         }
-        const uint32_t inc = __ballot_sync(0xffffffffu, st_flag(w) == 2u);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int idx = j - 8 * lane - q;
+          while (st_flag(w[q]) == 0u) w[q] = *(volatile unsigned long long*)(cur + idx);
+        }
+        int qs = 8;                              // first inclusive prefix of this lane
+#pragma unroll
+        for (int q = 7; q >= 0; --q) if (st_flag(w[q]) == 2u) qs = q;
+        const uint32_t inc = __ballot_sync(0xffffffffu, qs < 8);
         const int stop = inc ? __ffs(inc) - 1 : 32;
-        uint2 v = lane <= stop ? st_val(w) : make_uint2(0, 0);
+        uint2 v = make_uint2(0, 0);
+        if (lane <= stop) {
+          const int qe = lane < stop ? 7 : qs;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (q <= qe) { const uint2 t = st_val(w[q]); v.x += t.x; v.y += t.y; }
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
@@ -207,7 +225,7 @@ __global__ void __launch_bounds__(256) k_scan(uint32_t* __restrict__ cnt, int64_
         }
         prefix.x += v.x; prefix.y += v.y;
         if (inc) break;
-        j -= 32;
+        j -= 256;
       }
       if (lane == 0) atomicExch(cur + tile, st_pack(2u, make_uint2(prefix.x + total.x, prefix.y + total.y)));
     }

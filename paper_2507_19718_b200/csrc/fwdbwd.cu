@@ -454,19 +454,20 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
   }
   if (lane == 0) { s_cnt[wid][0] = pairs_acc; s_cnt[wid][1] = cand_acc; }
   __syncthreads();
-  double* part = a.partial + (int64_t)blockIdx.x * kPart;
+  double* part = a.partial + blockIdx.x;               // column-major [kPart][gridDim.x]
+  const int64_t cs = gridDim.x;
   if (threadIdx.x < kMaxL) {
     double s = 0.0;
     unsigned long long n = 0;
     for (int q = 0; q < kWarps; ++q) { s += s_loss[q][threadIdx.x]; n += s_nfit[q][threadIdx.x]; }
-    part[threadIdx.x] = s;
-    part[kMaxL + threadIdx.x] = (double)n;
+    part[threadIdx.x * cs] = s;
+    part[(kMaxL + threadIdx.x) * cs] = (double)n;
   }
   if (threadIdx.x == 0) {
     unsigned long long p = 0, c = 0;
     for (int q = 0; q < kWarps; ++q) { p += s_cnt[q][0]; c += s_cnt[q][1]; }
-    part[2 * kMaxL] = (double)p;
-    part[2 * kMaxL + 1] = (double)c;
+    part[2 * kMaxL * cs] = (double)p;
+    part[(2 * kMaxL + 1) * cs] = (double)c;
   }
   if (!a.fused) return;
   // single GPU: the last CTA to finish reduces the statistics and takes the step scalars

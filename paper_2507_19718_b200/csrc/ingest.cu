@@ -10,7 +10,7 @@ namespace gsc {
 
 constexpr int kU = 4;   // samples per thread per iteration
 
-__global__ void __launch_bounds__(256, 5) k_keys(const float* __restrict__ pos, const int32_t* __restrict__ len,
+__global__ void __launch_bounds__(256, 4) k_keys(const float* __restrict__ pos, const int32_t* __restrict__ len,
                                                  const float* __restrict__ rgb, int level_fixed, int64_t S,
                                                  LevelGeom g, IngestBufs b, float* out_zero) {
   pdl_enter();

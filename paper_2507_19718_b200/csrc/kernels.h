@@ -130,8 +130,9 @@ int query_grid();
 void launch_query(const QueryArgs& a, int grid, cudaStream_t s, Profiler* prof);
 
 // adamw.cu
-void launch_stats(const double* partial, int nblocks, const uint32_t* cell_start,
-                  const LevelGeom& g, int64_t S, LvlStats* lvl, cudaStream_t s, Profiler* prof);
+void launch_stats(const double* partial, int nblocks, const uint32_t* cell_start, const LevelGeom& g, int64_t S,
+                  LvlStats* lvl, bool with_step, DevState* st, const gc_hparams& hp, int L,
+                  gc_fit_stats* dev_stats, cudaStream_t s, Profiler* prof);
 void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp, int L,
                          gc_fit_stats* dev_stats, cudaStream_t s);
 void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, float4* rec, uint4* range,

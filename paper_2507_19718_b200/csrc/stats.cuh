@@ -13,15 +13,22 @@ struct StepHP {
   float lr[GC_NGROUPS]; float beta1, beta2; int schedule; int L;
 };
 
-// Sums the per-CTA partials (one warp per column, columns strided over nwarps warps): loss
-// sums, k_l (valid fitted samples per level) and the pair / candidate counters.
+// Sums the per-CTA partials, stored column-major ([kPart][nblocks]: a column is contiguous),
+// one warp per column with columns strided over nwarps warps: loss sums, k_l (valid fitted
+// samples per level) and the pair / candidate counters.  Fixed summation order.
 __device__ __forceinline__ void stats_reduce(const double* partial, int nblocks, const uint32_t* /*unused*/,
                                              const LevelGeom& g, int64_t S, LvlStats* lvl, int warp,
                                              int nwarps, int lane) {
   for (int col = warp; col < kPart; col += nwarps) {
-    double acc = 0.0;
-#pragma unroll 8
-    for (int b = lane; b < nblocks; b += 32) acc += __ldcg(partial + (int64_t)b * kPart + col);
+    const double* p = partial + (int64_t)col * nblocks;
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    int b = lane;
+    for (; b + 96 < nblocks; b += 128) {       // four independent loads in flight per lane
+#pragma unroll
+      for (int q = 0; q < 4; ++q) a[q] += __ldcg(p + b + 32 * q);
+    }
+    for (; b < nblocks; b += 32) a[0] += __ldcg(p + b);
+    double acc = (a[0] + a[1]) + (a[2] + a[3]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) {
