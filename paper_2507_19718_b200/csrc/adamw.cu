@@ -8,16 +8,15 @@
 namespace gsc {
 
 
-constexpr int kStatsWarps = 32;
+constexpr int kStatsThreads = ((kSlots * kPart + 31) / 32) * 32;
 
 // Level statistics of the call; with do_step (single GPU: no all-reduce in between) warp 0
 // then takes the step scalars in the same launch.
-__global__ void __launch_bounds__(kStatsWarps * 32) k_stats(const double* __restrict__ partial, int nblocks,
-                                                      const uint32_t* __restrict__ cell_start, LevelGeom g,
-                                                      int64_t S, LvlStats* lvl, int do_step, DevState* st,
-                                                      StepHP hp, gc_fit_stats* out) {
+__global__ void __launch_bounds__(kStatsThreads) k_stats(double* __restrict__ partial, LevelGeom g, int64_t S,
+                                                         LvlStats* lvl, int do_step, DevState* st, StepHP hp,
+                                                         gc_fit_stats* out) {
   pdl_enter();
-  stats_reduce(partial, nblocks, cell_start, g, S, lvl, threadIdx.x >> 5, kStatsWarps, threadIdx.x & 31);
+  stats_reduce(partial, g, lvl);
   __syncthreads();
   if (threadIdx.x == 0) stats_totals(lvl, g, S, lvl);
   if (!do_step) return;
@@ -152,12 +151,11 @@ static StepHP step_hp(const gc_hparams& hp, int L) {
   return h;
 }
 
-void launch_stats(const double* partial, int nblocks, const uint32_t* cell_start, const LevelGeom& g, int64_t S,
-                  LvlStats* lvl, bool with_step, DevState* st, const gc_hparams& hp, int L,
-                  gc_fit_stats* dev_stats, cudaStream_t s, Profiler* prof) {
+void launch_stats(double* partial, const LevelGeom& g, int64_t S, LvlStats* lvl, bool with_step, DevState* st,
+                  const gc_hparams& hp, int L, gc_fit_stats* dev_stats, cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "stats", s);
-  launch_pdl(k_stats, dim3(1), dim3(kStatsWarps * 32), 0, s, partial, nblocks, cell_start, g, S, lvl,
-             with_step ? 1 : 0, st, step_hp(hp, L), dev_stats);
+  launch_pdl(k_stats, dim3(1), dim3(kStatsThreads), 0, s, partial, g, S, lvl, with_step ? 1 : 0, st,
+             step_hp(hp, L), dev_stats);
 }
 
 void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp, int L,

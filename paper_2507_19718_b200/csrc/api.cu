@@ -373,7 +373,8 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
 
   c->fb_grid = fwdbwd_grid();
   c->q_grid = query_grid();
-  CK(dalloc(&c->partial, (size_t)c->fb_grid * kPart));
+  CK(dalloc(&c->partial, (size_t)kSlots * kPart));
+  CK(cudaMemset(c->partial, 0, sizeof(double) * kSlots * kPart));
   CK(cudaDeviceSynchronize());
   return GC_OK;
 }
@@ -533,23 +534,17 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
   fa.tau2 = tau * tau; fa.hdr_eps = c->hp.hdr_eps; fa.mode = c->hp.loss_grad_mode; fa.L = c->L;
   fa.lite = (c->hp.lr[GC_SCALE] == 0.f && !c->dbg_on) ? 1 : 0;
   const bool dp = c->comm != nullptr;
-  fa.fused = 0;   // last-CTA stats tail: measured 16 us slower than the two small kernels; off
-  fa.cell_start = F.cell_start; fa.S = S; fa.lvl = c->lvl; fa.st = c->st; fa.dstats = c->dstats;
-  fa.geom = c->geom;
-  for (int k = 0; k < GC_NGROUPS; ++k) fa.shp.lr[k] = c->hp.lr[k];
-  fa.shp.beta1 = c->hp.beta1; fa.shp.beta2 = c->hp.beta2; fa.shp.schedule = c->hp.lr_schedule; fa.shp.L = c->L;
   launch_fwdbwd(fa, c->fb_grid, s, &c->prof);
   if (hout) CK(cudaMemcpyAsync(out_rgb, dout, sizeof(float) * 3 * S_q, cudaMemcpyDeviceToHost, s));
-  if (!fa.fused)                    // single GPU: the step scalars ride in the same launch
-    launch_stats(c->partial, c->fb_grid, F.cell_start, c->geom, S, c->lvl, !dp, c->st, c->hp, c->L, c->dstats, s,
-                 &c->prof);
+  // single GPU: the step scalars ride in the statistics launch
+  launch_stats(c->partial, c->geom, S, c->lvl, !dp, c->st, c->hp, c->L, c->dstats, s, &c->prof);
   if (dp) {                         // data parallel: one sum over ranks of grads + level stats
     NK(ncclGroupStart());
     NK(ncclAllReduce(c->grad, c->grad, (size_t)12 * c->G, ncclFloat32, ncclSum, c->comm, s));
     NK(ncclAllReduce(c->lvl, c->lvl, sizeof(LvlStats) / sizeof(double), ncclFloat64, ncclSum, c->comm, s));
     NK(ncclGroupEnd());
   }
-  if (!fa.fused && dp) launch_step_scalars(c->lvl, c->st, c->hp, c->L, c->dstats, s);
+  if (dp) launch_step_scalars(c->lvl, c->st, c->hp, c->L, c->dstats, s);
   launch_adamw(c->G, c->P, c->M, c->V, c->grad, c->rec, c->range, c->rad2, c->csr_count, c->dbg_on ? c->dbg : nullptr,
                c->st, c->hp, c->geom, c->dstats, s, &c->prof);
   if (gc_status e = rebuild_csr(c, s, false)) return e;

@@ -42,7 +42,7 @@ struct DevState {
   unsigned long long nonfinite;      // non-finite gradient elements skipped (this call)
   unsigned int csr_total;            // culling-list entries of the current CSR
   unsigned int csr_overflow;         // sticky: a rebuild exceeded the list capacity
-  unsigned int done;                 // CTA completion counter of the fused fwd/bwd tail
+  unsigned int done;                 // (unused, kept for layout)
 };
 
 // Per-call level statistics; summed over ranks under data parallelism (all doubles so a

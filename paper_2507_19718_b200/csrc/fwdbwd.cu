@@ -454,37 +454,22 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
   }
   if (lane == 0) { s_cnt[wid][0] = pairs_acc; s_cnt[wid][1] = cand_acc; }
   __syncthreads();
-  double* part = a.partial + blockIdx.x;               // column-major [kPart][gridDim.x]
-  const int64_t cs = gridDim.x;
+  // per-CTA partials go into kSlots slotted fp64 accumulators (slot = CTA mod kSlots: a few
+  // dozen same-address reductions each), read and re-zeroed by k_stats
+  double* part = a.partial + (int64_t)(blockIdx.x % kSlots) * kPart;
   if (threadIdx.x < kMaxL) {
     double s = 0.0;
     unsigned long long n = 0;
     for (int q = 0; q < kWarps; ++q) { s += s_loss[q][threadIdx.x]; n += s_nfit[q][threadIdx.x]; }
-    part[threadIdx.x * cs] = s;
-    part[(kMaxL + threadIdx.x) * cs] = (double)n;
+    if (s != 0.0) atomicAdd(part + threadIdx.x, s);
+    if (n) atomicAdd(part + kMaxL + threadIdx.x, (double)n);
   }
   if (threadIdx.x == 0) {
     unsigned long long p = 0, c = 0;
     for (int q = 0; q < kWarps; ++q) { p += s_cnt[q][0]; c += s_cnt[q][1]; }
-    part[2 * kMaxL * cs] = (double)p;
-    part[(2 * kMaxL + 1) * cs] = (double)c;
+    if (p) atomicAdd(part + 2 * kMaxL, (double)p);
+    if (c) atomicAdd(part + 2 * kMaxL + 1, (double)c);
   }
-  if (!a.fused) return;
-  // single GPU: the last CTA to finish reduces the statistics and takes the step scalars
-  // (saves two dependent launches; under data parallelism an all-reduce sits in between)
-  __shared__ bool s_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&a.st->done, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  stats_reduce(a.partial, gridDim.x, a.cell_start, a.geom, a.S, a.lvl, wid, kWarps, lane);
-  __syncthreads();
-  if (threadIdx.x == 0) stats_totals(a.lvl, a.geom, a.S, a.lvl);
-  __syncthreads();
-  if (wid == 0) step_scalars_warp(a.lvl, a.st, a.shp, a.dstats, lane);
-  if (threadIdx.x == 0) a.st->done = 0u;
 }
 
 __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {

@@ -113,9 +113,7 @@ struct FitArgs {
   double* partial;      // [grid][kMaxL + 2]: per-block loss sums, pairs, candidates
   float tau2, hdr_eps; int mode; int L;
   int lite;             // scale group frozen (lr 0) and no gradient export: skip dA on isotropic chunks
-  // fused statistics + step scalars in the last CTA (single GPU)
-  int fused; const uint32_t* cell_start; int64_t S; LvlStats* lvl; DevState* st; StepHP shp;
-  gc_fit_stats* dstats; LevelGeom geom;
+
 };
 int fwdbwd_grid();
 void launch_fwdbwd(const FitArgs& a, int grid, cudaStream_t s, Profiler* prof);
@@ -130,9 +128,8 @@ int query_grid();
 void launch_query(const QueryArgs& a, int grid, cudaStream_t s, Profiler* prof);
 
 // adamw.cu
-void launch_stats(const double* partial, int nblocks, const uint32_t* cell_start, const LevelGeom& g, int64_t S,
-                  LvlStats* lvl, bool with_step, DevState* st, const gc_hparams& hp, int L,
-                  gc_fit_stats* dev_stats, cudaStream_t s, Profiler* prof);
+void launch_stats(double* partial, const LevelGeom& g, int64_t S, LvlStats* lvl, bool with_step, DevState* st,
+                  const gc_hparams& hp, int L, gc_fit_stats* dev_stats, cudaStream_t s, Profiler* prof);
 void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp, int L,
                          gc_fit_stats* dev_stats, cudaStream_t s);
 void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, float4* rec, uint4* range,

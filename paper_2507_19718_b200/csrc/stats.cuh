@@ -1,42 +1,39 @@
 // stats.cuh -- per-call level statistics and the step scalars (Eq. 5 schedule, per-level
-// AdamW skip and bias corrections).  Device functions shared by the standalone kernels (data
-// parallel: an all-reduce runs between them) and the last CTA of k_fwdbwd (single GPU).
+// AdamW skip and bias corrections).  Device functions of k_stats (single GPU: both in one
+// launch) and k_step_scalars (data parallel: the all-reduce runs between them).
 #pragma once
 #include "common.cuh"
 
 namespace gsc {
 
-// per-CTA partial of k_fwdbwd: loss sums [kMaxL], fitted-sample counts [kMaxL], pairs, candidates
+// partials of k_fwdbwd: loss sums [kMaxL], fitted-sample counts [kMaxL], pairs, candidates;
+// accumulated into kSlots slots [kSlots][kPart] (zero between calls)
 constexpr int kPart = 2 * kMaxL + 2;
+constexpr int kSlots = 16;
 
 struct StepHP {
   float lr[GC_NGROUPS]; float beta1, beta2; int schedule; int L;
 };
 
-// Sums the per-CTA partials, stored column-major ([kPart][nblocks]: a column is contiguous),
-// one warp per column with columns strided over nwarps warps: loss sums, k_l (valid fitted
-// samples per level) and the pair / candidate counters.  Fixed summation order.
-__device__ __forceinline__ void stats_reduce(const double* partial, int nblocks, const uint32_t* /*unused*/,
-                                             const LevelGeom& g, int64_t S, LvlStats* lvl, int warp,
-                                             int nwarps, int lane) {
-  for (int col = warp; col < kPart; col += nwarps) {
-    const double* p = partial + (int64_t)col * nblocks;
-    double a[4] = {0.0, 0.0, 0.0, 0.0};
-    int b = lane;
-    for (; b + 96 < nblocks; b += 128) {       // four independent loads in flight per lane
+// Sums the kSlots slotted partials per column in a fixed order and re-zeroes the slots (one
+// CTA of >= kSlots * kPart threads): loss sums, k_l (valid fitted samples per level) and the
+// pair / candidate counters.
+__device__ __forceinline__ void stats_reduce(double* partial, const LevelGeom& g, LvlStats* lvl) {
+  __shared__ double s_v[kSlots][kPart];
+  const int t = threadIdx.x;
+  if (t < kSlots * kPart) {
+    s_v[t / kPart][t % kPart] = __ldcg(partial + t);
+    partial[t] = 0.0;
+  }
+  __syncthreads();
+  if (t < kPart) {
+    double acc = 0.0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) a[q] += __ldcg(p + b + 32 * q);
-    }
-    for (; b < nblocks; b += 32) a[0] += __ldcg(p + b);
-    double acc = (a[0] + a[1]) + (a[2] + a[3]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) {
-      if (col < kMaxL) lvl->loss_sum[col] = acc;
-      else if (col < 2 * kMaxL) lvl->count[col - kMaxL] = col - kMaxL < g.L ? acc : 0.0;
-      else if (col == 2 * kMaxL) lvl->n_pairs = acc;
-      else lvl->n_cand = acc;
-    }
+    for (int q = 0; q < kSlots; ++q) acc += s_v[q][t];
+    if (t < kMaxL) lvl->loss_sum[t] = acc;
+    else if (t < 2 * kMaxL) lvl->count[t - kMaxL] = t - kMaxL < g.L ? acc : 0.0;
+    else if (t == 2 * kMaxL) lvl->n_pairs = acc;
+    else lvl->n_cand = acc;
   }
 }
 
