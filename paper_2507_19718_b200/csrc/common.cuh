@@ -11,7 +11,8 @@ namespace gsc {
 constexpr int kMaxL = GC_MAX_LEVELS;
 constexpr int kNP = 14;              // raw floats per Gaussian
 constexpr int kCH = 64;              // samples per work item: one warp, two samples per lane
-constexpr int kScanTile = 2048;      // 256 threads x 8 items
+constexpr int kScanThreads = 1024;   // one scan tile per CTA: 1024 threads x 8 items
+constexpr int kScanTile = 8 * kScanThreads;
 constexpr int kRep = 8;              // replicated per-cell sample counters (hot-cell atomics / 8)
 constexpr uint32_t kInvalidKey = 0xFFFFFFFFu;
 

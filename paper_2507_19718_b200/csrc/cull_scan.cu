@@ -67,9 +67,10 @@ __global__ void k_cull_emit(int64_t G, const uint4* __restrict__ range, const do
 }
 
 // ---------------------------------------------------------------------------- scan
-// Block-wide exclusive scan of (a, b) pairs, 256 threads (8 warps).
+// Block-wide exclusive scan of (a, b) pairs, kScanThreads threads.
 __device__ __forceinline__ uint2 block_excl_scan(uint2 v, uint2& total) {
-  __shared__ uint2 wsum[8];
+  constexpr int kW = kScanThreads / 32;
+  __shared__ uint2 wsum[kW];
   __shared__ uint2 tot_s;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint2 inc = v;
@@ -81,15 +82,15 @@ __device__ __forceinline__ uint2 block_excl_scan(uint2 v, uint2& total) {
   if (lane == 31) wsum[warp] = inc;
   __syncthreads();
   if (warp == 0) {
-    uint2 w = lane < 8 ? wsum[lane] : make_uint2(0, 0);
+    uint2 w = lane < kW ? wsum[lane] : make_uint2(0, 0);
     uint2 wi = w;
 #pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
+    for (int o = 1; o < kW; o <<= 1) {
       uint32_t a = __shfl_up_sync(0xffffffffu, wi.x, o), b = __shfl_up_sync(0xffffffffu, wi.y, o);
       if (lane >= o) { wi.x += a; wi.y += b; }
     }
-    if (lane < 8) wsum[lane] = make_uint2(wi.x - w.x, wi.y - w.y);
-    if (lane == 7) tot_s = wi;
+    if (lane < kW) wsum[lane] = make_uint2(wi.x - w.x, wi.y - w.y);
+    if (lane == kW - 1) tot_s = wi;
   }
   __syncthreads();
   uint2 base = wsum[warp];
@@ -152,7 +153,7 @@ __device__ __forceinline__ uint2 st_val(unsigned long long w) {
   return make_uint2((uint32_t)(w & 0x7FFFFFFFu), (uint32_t)((w >> 31) & 0x7FFFFFFFu));
 }
 
-__global__ void __launch_bounds__(256) k_scan(uint32_t* __restrict__ cnt, int64_t n, int ch,
+__global__ void __launch_bounds__(kScanThreads) k_scan(uint32_t* __restrict__ cnt, int64_t n, int ch,
                                               unsigned long long* state, uint32_t* ctl, int ntiles,
                                               uint32_t* totals, uint32_t* excl, uint32_t* excl_copy,
                                               WorkItem* work, LevelGeom g) {
@@ -268,7 +269,7 @@ void launch_scan(uint32_t* cnt, int64_t n, int ch, uint2* state, uint32_t* total
   unsigned long long* st = reinterpret_cast<unsigned long long*>(state);
   uint32_t* ctl = reinterpret_cast<uint32_t*>(st + 2 * ntiles);
   ProfScope ps(prof, "scan", s);
-  launch_pdl(k_scan, dim3(ntiles), dim3(256), 0, s, cnt, n, ch, st, ctl, ntiles, totals, excl, excl_copy, work, g);
+  launch_pdl(k_scan, dim3(ntiles), dim3(kScanThreads), 0, s, cnt, n, ch, st, ctl, ntiles, totals, excl, excl_copy, work, g);
 }
 
 void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& g, float4* rec,

@@ -553,10 +553,13 @@ def test_fit_query_ragged_host_buffers_and_epilogue(gsc, S_fit, S_q):
 
 
 def test_fit_query_graph_replay_matches_eager(gsc):
+    """A captured gc_fit_query replays correctly: every replay's lookups match the oracle on
+    the parameters it started from, and the trajectory matches eager calls."""
     c1, _, _ = make_cfg1(gsc)
     c2, _, _ = make_cfg1(gsc)
-    x, ln, rgb = [cuda(a) for a in workload.fit_batch(1, S=60_000)]
-    xq, lq = [cuda(a) for a in workload.query_batch(1, S=30_000)]
+    xh, lh, rh = workload.fit_batch(1, S=60_000)
+    xqh, lqh = workload.query_batch(1, S=30_000)
+    x, ln, rgb, xq, lq = map(cuda, (xh, lh, rh, xqh, lqh))
     c2.reserve(60_000, 30_000)
     out = torch.empty((30_000, 3), device="cuda")
     st = torch.cuda.Stream()
@@ -569,9 +572,11 @@ def test_fit_query_graph_replay_matches_eager(gsc):
     with torch.cuda.graph(g, stream=st):
         c2.fit_query(x, ln, rgb, xq, lq, out=out, stream=st)
     for _ in range(3):
-        y1, _ = c1.fit_query(x, ln, rgb, xq, lq)
+        c1.fit_query(x, ln, rgb, xq, lq)
+        P = rows(c2)
         g.replay()
         torch.cuda.synchronize()
-        # bin order inside a cell and gradient atomics are unordered: fp32 rounding only
-        np.testing.assert_allclose(y1.cpu().numpy(), out.cpu().numpy(), rtol=2e-5, atol=1e-7)
+        yo, lv, _ = oracle.query(c2.goff, P, xqh.astype(np.float64), lqh, grids=c2.grids())
+        check_forward(out.cpu().numpy(), yo, P, c2.goff, xqh, lv, what="replay")
+    # gradient atomics are unordered: the two trajectories agree to fp32 rounding
     np.testing.assert_allclose(rows(c1), rows(c2), rtol=1e-5, atol=1e-6)
