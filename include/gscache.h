@@ -103,8 +103,7 @@ gc_status gc_destroy(gc_cache c);
 
 /* Pre-size scratch for batches of up to S_fit fit samples and S_query query points, so that
  * later gc_fit / gc_query / gc_fit_query(S_fit, S_query) calls never allocate (required
- * before CUDA-graph capture).  The fit scratch is sized for S_fit + S_query so that the
- * fused call fits. */
+ * before CUDA-graph capture). */
 gc_status gc_reserve(gc_cache c, int64_t S_fit, int64_t S_query);
 
 /* One optimisation step on a batch of S renderer samples (sec.3.5, sec.3.6):
@@ -122,8 +121,10 @@ gc_status gc_fit(gc_cache c, const float* pos, const int32_t* path_len, const fl
  * lookups of the frame are answered from the parameters as they are BEFORE this call's
  * optimisation step (the frame's renderer reads the cache fitted through the previous
  * frame), then the S fit samples take the step exactly as gc_fit.  Results equal gc_query
- * followed by gc_fit up to fp32 summation rounding; the two sample sets share one binning
- * pass and one staging of every cell's culling list.
+ * followed by gc_fit (up to fp32 summation order).  The lookups run on the handle's own
+ * stream, forked from `stream` at the call and joined back before the optimizer step, so
+ * their binning and evaluation overlap the fit samples' binning and fwd/bwd; to the caller
+ * the call is ordered on `stream` like any other (and CUDA-graph capturable).
  *  pos/path_len/rgb/S: as gc_fit.  qpos [S_q][3] f32, qlen [S_q] i32 or NULL (then `qlevel`
  *  for every lookup), attenuation/beta/unbiased_rgb: the gc_query_radiance epilogue (each
  *  NULL = none), out_rgb [S_q][3]: caller order; all host or device.  Lookups with

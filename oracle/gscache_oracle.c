@@ -309,7 +309,7 @@ void orc_cull_ranges(int64_t G, const double* P, double tau, const double* origi
                      double* r2 /*[G] or NULL*/) {
   for (int64_t j = 0; j < G; ++j) {
     const double* p = P + j * NP;
-    double qh[4], qn, R[3][3], U2[3];
+    double qh[4], qn, R[3][3], U1[3], U2[3];
     int deg;
     orc_qnorm(p + 3, qh, &qn, &deg);
     orc_rot(qh, R);
@@ -321,13 +321,17 @@ void orc_cull_ranges(int64_t G, const double* P, double tau, const double* origi
       int32_t Qe = (k >= 0) ? k / 32 : -((-k + 31) / 32);   /* floor(k/32) */
       int32_t r = k - 32 * Qe;
       double U = ldexp(orc_T32[r], Qe);
+      U1[b] = U;
       U2[b] = U * U;
     }
+    /* isotropic (s_0 = s_1 = s_2): the ellipsoid is a ball of radius tau e^s <= tau U, so
+     * h_a = tau U exactly (R R^T = I; C8) */
+    const int iso = p[10] == p[11] && p[11] == p[12];
     for (int a = 0; a < 3; ++a) {
       double s0 = R[a][0] * R[a][0] * U2[0];
       double s1 = R[a][1] * R[a][1] * U2[1];
       double s2 = R[a][2] * R[a][2] * U2[2];
-      double h = tau * sqrt((s0 + s1) + s2);
+      double h = iso ? tau * U1[0] : tau * sqrt((s0 + s1) + s2);
       double flo = floor(((p[a] - h) - origin[a]) * inv_cell[a]);
       double fhi = floor(((p[a] + h) - origin[a]) * inv_cell[a]);
       rng[6 * j + a] = orc_clampcell(flo, dims[a]);

@@ -30,6 +30,8 @@ __global__ void k_step_scalars(const LvlStats* __restrict__ lvl, DevState* st, S
   step_scalars_warp(lvl, st, hp, out, threadIdx.x);
 }
 
+constexpr int kAdamThreads = 128, kAdamBlocksPerSM = 4;
+
 struct AdamHP {
   float wd[GC_NGROUPS]; float beta1, beta2, eps; double tau;
 };
@@ -93,26 +95,26 @@ __device__ void chain_rule(const float p[kNP], const float cg[12], float out[kNP
 // Fused normalise + chain rule + AdamW of one Gaussian per thread (A6); zeroes the gradient
 // slots it consumes.  The next step's evaluation record and culling counts are emitted by
 // k_record_cull right after (split so both kernels stay spill-free and latency-hidden).
-__global__ void __launch_bounds__(256, 3) k_adamw(int64_t G, float* __restrict__ P, float* __restrict__ M,
-                                                  float* __restrict__ V, float* __restrict__ grad,
-                                                  float* dbg, const DevState* __restrict__ st, AdamHP hp,
-                                                  LevelGeom g, gc_fit_stats* out) {
+__global__ void __launch_bounds__(kAdamThreads, kAdamBlocksPerSM) k_adamw(
+    int64_t G, float* __restrict__ P, float* __restrict__ M, float* __restrict__ V, float* __restrict__ grad,
+    float* __restrict__ dbg, const DevState* __restrict__ st, AdamHP hp, LevelGeom g, gc_fit_stats* out) {
   pdl_enter();
   unsigned long long bad = 0;
   float eta[GC_NGROUPS], dec[GC_NGROUPS];
 #pragma unroll
   for (int k = 0; k < GC_NGROUPS; ++k) { eta[k] = st->eta[k]; dec[k] = 1.f - eta[k] * hp.wd[k]; }
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < G; j += (int64_t)gridDim.x * blockDim.x) {
-    const int l = level_of_gaussian(g, j);
-    const bool act = st->active[l] != 0;
+    // every load of the Gaussian is issued before any is consumed (one memory latency, not three)
     float4* gp = reinterpret_cast<float4*>(grad + 12 * j);
     const float4 c0 = gp[0], c1 = gp[1], c2 = gp[2];
+    float p[kNP], m[kNP], v[kNP];
+#pragma unroll
+    for (int k = 0; k < kNP; ++k) { p[k] = P[k * G + j]; m[k] = M[k * G + j]; v[k] = V[k * G + j]; }
+    const int l = level_of_gaussian(g, j);
+    const bool act = st->active[l] != 0;
     const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
     gp[0] = zero; gp[1] = zero; gp[2] = zero;
     if (!act && !dbg) continue;
-    float p[kNP];
-#pragma unroll
-    for (int k = 0; k < kNP; ++k) p[k] = P[k * G + j];
     const float s = st->inv3k[l];
     const float cg[12] = {c0.x * s, c0.y * s, c0.z * s, c0.w * s, c1.x * s, c1.y * s,
                           c1.z * s, c1.w * s, c2.x * s, c2.y * s, c2.z * s, c2.w * s};
@@ -124,9 +126,6 @@ __global__ void __launch_bounds__(256, 3) k_adamw(int64_t G, float* __restrict__
     }
     if (!act) continue;
     const float ibc1 = 1.f / st->bc1[l], ibc2 = 1.f / st->bc2[l];
-    float m[kNP], v[kNP];
-#pragma unroll
-    for (int k = 0; k < kNP; ++k) { m[k] = M[k * G + j]; v[k] = V[k * G + j]; }   // all loads in flight
 #pragma unroll
     for (int k = 0; k < kNP; ++k) {
       const int grp = k < 3 ? 0 : (k < 7 ? 1 : (k < 10 ? 2 : (k < 13 ? 3 : 4)));   // constant after unroll
@@ -171,8 +170,8 @@ void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, float4* 
   h.beta1 = hp.beta1; h.beta2 = hp.beta2; h.eps = hp.adam_eps; h.tau = (double)hp.cutoff_sigma;
   {
     ProfScope ps(prof, "adamw", s);
-    int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((G + 255) / 256, 148 * 8));
-    launch_pdl(k_adamw, dim3(blocks), dim3(256), 0, s, G, P, M, V, grad, dbg_grad, (const DevState*)st, h, g, dev_stats);
+    int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((G + kAdamThreads - 1) / kAdamThreads, 148 * kAdamBlocksPerSM));
+    launch_pdl(k_adamw, dim3(blocks), dim3(kAdamThreads), 0, s, G, P, M, V, grad, dbg_grad, (const DevState*)st, h, g, dev_stats);
   }
   {
     ProfScope ps(prof, "record_cull", s);

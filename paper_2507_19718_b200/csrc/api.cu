@@ -58,11 +58,11 @@ struct Scratch {
   uint32_t *cell_count = nullptr, *cell_start = nullptr, *totals = nullptr;
   uint2* tiles = nullptr;
   WorkItem* work = nullptr;
-  float *in_pos = nullptr, *in_rgb = nullptr, *out = nullptr, *in_qpos = nullptr;
-  int32_t *in_len = nullptr, *in_qlen = nullptr;
+  float *in_pos = nullptr, *in_rgb = nullptr, *out = nullptr;
+  int32_t* in_len = nullptr;
   void release() {
     void* ps[] = {key, rank, bin, cell_count, cell_start, totals, tiles, work,
-                  in_pos, in_rgb, out, in_len, in_qpos, in_qlen};
+                  in_pos, in_rgb, out, in_len};
     for (void* p : ps) if (p) cudaFree(p);
     *this = Scratch();
   }
@@ -101,6 +101,8 @@ struct gc_cache_s {
   int rank = 0, world = 1;
   float* pack_tmp = nullptr;
   int64_t pack_cap = 0;
+  cudaStream_t side = nullptr;            // gc_fit_query: lookups run beside the fit samples' ingest
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 // ------------------------------------------------------------------------- helpers
@@ -373,6 +375,9 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
 
   c->fb_grid = fwdbwd_grid();
   c->q_grid = query_grid();
+  CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   CK(dalloc(&c->partial, (size_t)kSlots * kPart));
   CK(cudaMemset(c->partial, 0, sizeof(double) * kSlots * kPart));
   CK(cudaDeviceSynchronize());
@@ -391,6 +396,9 @@ static void destroy_impl(gc_cache c) {
   c->qry.release();
   for (auto* p : c->payloads) delete p;
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
 }
 
@@ -433,13 +441,9 @@ gc_status gc_destroy(gc_cache c) {
 gc_status gc_reserve(gc_cache c, int64_t S_fit, int64_t S_query) {
   if (!c || S_fit < 0 || S_query < 0) return fail(GC_ERR_ARG, "bad arguments");
   CK(cudaSetDevice(c->device));
-  if (S_fit > 0) { gc_status s = ensure_scratch(c, c->fit, S_fit + S_query, true, 0); if (s) return s; }
+  if (S_fit > 0) { gc_status s = ensure_scratch(c, c->fit, S_fit, true, 0); if (s) return s; }
   if (S_query > 0) { gc_status s = ensure_scratch(c, c->qry, S_query, false, 0); if (s) return s; }
-  if (S_fit > 0) { gc_status s = ensure_staging(c->fit, true, true, true, S_query > 0); if (s) return s; }
-  if (S_fit > 0 && S_query > 0) {
-    if (!c->fit.in_qpos) CK(dalloc(&c->fit.in_qpos, 3 * c->fit.cap));
-    if (!c->fit.in_qlen) CK(dalloc(&c->fit.in_qlen, c->fit.cap));
-  }
+  if (S_fit > 0) { gc_status s = ensure_staging(c->fit, true, true, true, false); if (s) return s; }
   if (S_query > 0) { gc_status s = ensure_staging(c->qry, true, true, false, true); if (s) return s; }
   return GC_OK;
 }
@@ -469,23 +473,18 @@ struct Epilogue {
   }
 };
 
-// gc_fit (S_q = 0) and gc_fit_query: one binning pass over fit samples [0, S) followed by
-// the lookups [S, S + S_q) in the same counters and bins; k_fwdbwd evaluates both, takes
-// the loss and gradients of the fitted ones and writes the lookups' outputs (pre-step
-// parameters), then the step.
+// One optimisation step (gc_fit, and the fit half of gc_fit_query: `join`, if set, is waited
+// on before the optimizer step so that the lookups forked off beside it read pre-step
+// parameters).
 static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len, const float* rgb, int64_t S,
-                          const float* qpos, const int32_t* qlen, int qlevel, int64_t S_q, const float* att,
-                          const float* beta, const float* unb, float* out_rgb, gc_stream stream,
-                          gc_fit_stats* stats) {
+                          gc_stream stream, gc_fit_stats* stats, cudaEvent_t join = nullptr) {
   if (!c) return fail(GC_ERR_ARG, "NULL handle");
-  if (S < 0 || S_q < 0 || S + S_q >= ((int64_t)1 << 31)) return fail(GC_ERR_ARG, "S out of range");
+  if (S < 0 || S >= ((int64_t)1 << 31)) return fail(GC_ERR_ARG, "S out of range");
   if (S > 0 && (!pos || !path_len || !rgb)) return fail(GC_ERR_ARG, "NULL sample pointer");
-  if (S_q > 0 && (!qpos || !out_rgb)) return fail(GC_ERR_ARG, "NULL query pointer");
-  if (S_q > 0 && !qlen && (qlevel < 0 || qlevel >= c->L)) return fail(GC_ERR_ARG, "qlevel %d not in [0, %d)", qlevel, c->L);
   cudaStream_t s = (cudaStream_t)stream;
   CK(cudaSetDevice(c->device));
   if (gc_status e = check_sticky(c)) return e;
-  if (gc_status e = ensure_scratch(c, c->fit, std::max<int64_t>(S + S_q, 1), true, s)) return e;
+  if (gc_status e = ensure_scratch(c, c->fit, std::max<int64_t>(S, 1), true, s)) return e;
   Scratch& F = c->fit;
   if (S > 0) {
     const bool hpos = !is_device_ptr(pos), hlen = !is_device_ptr(path_len), hrgb = !is_device_ptr(rgb);
@@ -497,45 +496,19 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
       if (hrgb) { CK(cudaMemcpyAsync(F.in_rgb, rgb, sizeof(float) * 3 * S, cudaMemcpyHostToDevice, s)); rgb = F.in_rgb; }
     }
   }
-  float* dout = out_rgb;
-  bool hout = false;
-  Epilogue ep;
-  if (S_q > 0) {
-    const bool hpos = !is_device_ptr(qpos), hlen = qlen && !is_device_ptr(qlen);
-    hout = !is_device_ptr(out_rgb);
-    if (hpos || hlen || hout) {
-      if (capturing(s) && ((hpos && !F.in_qpos) || (hlen && !F.in_qlen) || (hout && !F.out)))
-        return fail(GC_ERR_STATE, "staging not reserved before capture");
-      if (hpos && !F.in_qpos) CK(dalloc(&F.in_qpos, 3 * F.cap));
-      if (hlen && !F.in_qlen) CK(dalloc(&F.in_qlen, F.cap));
-      if (gc_status e = ensure_staging(F, false, false, false, hout)) return e;
-      if (hpos) { CK(cudaMemcpyAsync(F.in_qpos, qpos, sizeof(float) * 3 * S_q, cudaMemcpyHostToDevice, s)); qpos = F.in_qpos; }
-      if (hlen) { CK(cudaMemcpyAsync(F.in_qlen, qlen, sizeof(int32_t) * S_q, cudaMemcpyHostToDevice, s)); qlen = F.in_qlen; }
-      if (hout) dout = F.out;
-    }
-    if (gc_status e = ep.stage(att, beta, unb, S_q, s)) return e;
-  }
-  // with lookups riding along, fit samples count on replicas 0-3 and lookups on 4-7: every
-  // cell's bin range is [fitted | lookups], so work items are pure except one per cell
-  const uint32_t rm = S_q > 0 ? kRep / 2 - 1 : kRep - 1;
-  IngestBufs b{F.key, F.rank, F.cell_count, F.bin, c->NC, 0u, rm};
-  IngestBufs bq{F.key + S, F.rank + S, F.cell_count, F.bin, c->NC, kRep / 2, kRep / 2 - 1};
+  IngestBufs b{F.key, F.rank, F.cell_count, F.bin, c->NC};
   if (S > 0) launch_keys(pos, path_len, rgb, -1, S, c->geom, b, s, &c->prof);
-  if (S_q > 0) launch_keys_query(qpos, qlen, qlen ? -1 : qlevel, S_q, c->geom, bq, dout, s, &c->prof);
   launch_scan(F.cell_count, c->NC * kRep, kCH, F.tiles, F.totals, F.cell_start, nullptr, F.work, c->geom, s, &c->prof);
-  if (S > 0) launch_scatter(pos, rgb, S, F.cell_start, b, 0, s, &c->prof);
-  if (S_q > 0) launch_scatter(qpos, nullptr, S_q, F.cell_start, bq, 2, s, &c->prof);
+  if (S > 0) launch_scatter(pos, rgb, S, F.cell_start, b, s, &c->prof);
   FitArgs fa;
   fa.work = F.work; fa.n_work = F.totals + 1; fa.csr_off = c->csr_off; fa.csr_idx = c->csr_idx; fa.rec = c->rec;
   fa.bin = F.bin;
-  fa.out = dout; fa.att = ep.dev[0]; fa.beta = ep.dev[1]; fa.unb = ep.dev[2];
   fa.grad = c->grad; fa.partial = c->partial;
   const float tau = c->hp.cutoff_sigma;
   fa.tau2 = tau * tau; fa.hdr_eps = c->hp.hdr_eps; fa.mode = c->hp.loss_grad_mode; fa.L = c->L;
   fa.lite = (c->hp.lr[GC_SCALE] == 0.f && !c->dbg_on) ? 1 : 0;
   const bool dp = c->comm != nullptr;
   launch_fwdbwd(fa, c->fb_grid, s, &c->prof);
-  if (hout) CK(cudaMemcpyAsync(out_rgb, dout, sizeof(float) * 3 * S_q, cudaMemcpyDeviceToHost, s));
   // single GPU: the step scalars ride in the statistics launch
   launch_stats(c->partial, c->geom, S, c->lvl, !dp, c->st, c->hp, c->L, c->dstats, s, &c->prof);
   if (dp) {                         // data parallel: one sum over ranks of grads + level stats
@@ -543,13 +516,13 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
     NK(ncclAllReduce(c->grad, c->grad, (size_t)12 * c->G, ncclFloat32, ncclSum, c->comm, s));
     NK(ncclAllReduce(c->lvl, c->lvl, sizeof(LvlStats) / sizeof(double), ncclFloat64, ncclSum, c->comm, s));
     NK(ncclGroupEnd());
+    launch_step_scalars(c->lvl, c->st, c->hp, c->L, c->dstats, s);
   }
-  if (dp) launch_step_scalars(c->lvl, c->st, c->hp, c->L, c->dstats, s);
+  if (join) CK(cudaStreamWaitEvent(s, join, 0));
   launch_adamw(c->G, c->P, c->M, c->V, c->grad, c->rec, c->range, c->rad2, c->csr_count, c->dbg_on ? c->dbg : nullptr,
                c->st, c->hp, c->geom, c->dstats, s, &c->prof);
   if (gc_status e = rebuild_csr(c, s, false)) return e;
   if (gc_status e = emit_stats(c, stats, s)) return e;
-  if (gc_status e = ep.release(s)) return e;
   CK(cudaGetLastError());
   c->last_fit_S = S;
   return GC_OK;
@@ -557,20 +530,36 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
 
 gc_status gc_fit(gc_cache c, const float* pos, const int32_t* path_len, const float* rgb, int64_t S,
                  gc_stream stream, gc_fit_stats* stats) {
-  return fit_impl(c, pos, path_len, rgb, S, nullptr, nullptr, 0, 0, nullptr, nullptr, nullptr, nullptr, stream, stats);
-}
-
-gc_status gc_fit_query(gc_cache c, const float* pos, const int32_t* path_len, const float* rgb, int64_t S,
-                       const float* qpos, const int32_t* qlen, int qlevel, int64_t S_q, const float* attenuation,
-                       const float* beta, const float* unbiased_rgb, float* out_rgb, gc_stream stream,
-                       gc_fit_stats* stats) {
-  return fit_impl(c, pos, path_len, rgb, S, qpos, qlen, qlevel, S_q, attenuation, beta, unbiased_rgb, out_rgb,
-                  stream, stats);
+  return fit_impl(c, pos, path_len, rgb, S, stream, stats);
 }
 
 static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_len, int level, int64_t S,
                             const float* att, const float* beta, const float* unb, float* out_rgb,
                             gc_stream stream);
+
+// The frame's lookups run on the handle's side stream, forked from `stream` and joined back
+// before the optimizer step, so their ingest and evaluation overlap the fit samples' ingest
+// and fwd/bwd (independent work; both read the pre-step parameters and culling lists).
+gc_status gc_fit_query(gc_cache c, const float* pos, const int32_t* path_len, const float* rgb, int64_t S,
+                       const float* qpos, const int32_t* qlen, int qlevel, int64_t S_q, const float* attenuation,
+                       const float* beta, const float* unbiased_rgb, float* out_rgb, gc_stream stream,
+                       gc_fit_stats* stats) {
+  if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  if (S_q < 0 || S_q >= ((int64_t)1 << 31)) return fail(GC_ERR_ARG, "S_q out of range");
+  if (S_q > 0 && (!qpos || !out_rgb)) return fail(GC_ERR_ARG, "NULL query pointer");
+  if (S_q > 0 && !qlen && (qlevel < 0 || qlevel >= c->L)) return fail(GC_ERR_ARG, "qlevel %d not in [0, %d)", qlevel, c->L);
+  if (S_q == 0) return fit_impl(c, pos, path_len, rgb, S, stream, stats);
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->device));
+  CK(cudaEventRecord(c->ev_fork, s));
+  CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+  const gc_status qs = query_impl(c, qpos, qlen, qlevel, S_q, attenuation, beta, unbiased_rgb, out_rgb,
+                                  (gc_stream)c->side);
+  CK(cudaEventRecord(c->ev_join, c->side));     // always joined (keeps a capture well-formed)
+  if (qs != GC_OK) { CK(cudaStreamWaitEvent(s, c->ev_join, 0)); return qs; }
+  return fit_impl(c, pos, path_len, rgb, S, stream, stats, c->ev_join);
+}
+
 
 gc_status gc_query(gc_cache c, const float* pos, const int32_t* path_len, int level, int64_t S,
                    float* out_rgb, gc_stream stream) {
@@ -604,10 +593,10 @@ static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_le
     if (hlen) { CK(cudaMemcpyAsync(Q.in_len, path_len, sizeof(int32_t) * S, cudaMemcpyHostToDevice, s)); path_len = Q.in_len; }
   }
   float* dout = hout ? Q.out : out_rgb;
-  IngestBufs b{Q.key, Q.rank, Q.cell_count, Q.bin, c->NC, 0u, kRep - 1};
+  IngestBufs b{Q.key, Q.rank, Q.cell_count, Q.bin, c->NC};
   launch_keys_query(pos, path_len, path_len ? -1 : level, S, c->geom, b, dout, s, &c->prof);
   launch_scan(Q.cell_count, c->NC * kRep, kCH, Q.tiles, Q.totals, Q.cell_start, nullptr, Q.work, c->geom, s, &c->prof);
-  launch_scatter(pos, nullptr, S, Q.cell_start, b, 1, s, &c->prof);
+  launch_scatter(pos, nullptr, S, Q.cell_start, b, s, &c->prof);
   QueryArgs qa;
   qa.work = Q.work; qa.n_work = Q.totals + 1; qa.csr_off = c->csr_off; qa.csr_idx = c->csr_idx; qa.rec = c->rec;
   qa.bin = Q.bin; qa.out = dout;

@@ -111,7 +111,7 @@ __device__ __forceinline__ float iso_s(const float (&x)[3], const float4& c) {
 template <bool kRecord>
 __device__ __forceinline__ void eval_chunk_iso(const ChunkSmem& w, int kc, const float (&xa)[3], const float (&xb)[3],
                                                float (&ya)[3], float (&yb)[3], uint16_t* pkey, float* pe,
-                                               int& pbase, int cap, int lane, uint32_t fa = ~0u, uint32_t fb = ~0u) {
+                                               int& pbase, int cap, int lane) {
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll 2
   for (int k = 0; k < kc; ++k) {
@@ -125,17 +125,16 @@ __device__ __forceinline__ void eval_chunk_iso(const ChunkSmem& w, int kc, const
       yb[0] = fmaf(f.y, eb, yb[0]); yb[1] = fmaf(f.z, eb, yb[1]); yb[2] = fmaf(f.w, eb, yb[2]);
       continue;
     }
-    const uint32_t ia = __ballot_sync(0xffffffffu, ina), ib = __ballot_sync(0xffffffffu, inb);
-    if (ia | ib) {
-      const uint32_t ma = ia & fa, mb = ib & fb;      // pairs of fitted samples only
+    const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = __ballot_sync(0xffffffffu, inb);
+    if (ma | mb) {
       const float xa_ = ex2_approx(f.x * sa), xb_ = ex2_approx(f.x * sb);
       const float ea = ina ? xa_ : 0.f, eb = inb ? xb_ : 0.f;
       ya[0] = fmaf(f.y, ea, ya[0]); ya[1] = fmaf(f.z, ea, ya[1]); ya[2] = fmaf(f.w, ea, ya[2]);
       yb[0] = fmaf(f.y, eb, yb[0]); yb[1] = fmaf(f.z, eb, yb[1]); yb[2] = fmaf(f.w, eb, yb[2]);
       const int na = __popc(ma);
       const int pa = min(pbase + __popc(ma & lt), cap - 1), pb = min(pbase + na + __popc(mb & lt), cap - 1);
-      if ((ma >> lane) & 1u) { pkey[pa] = (uint16_t)((k << 6) | lane); pe[pa] = ea; }
-      if ((mb >> lane) & 1u) { pkey[pb] = (uint16_t)((k << 6) | (lane + 32)); pe[pb] = eb; }
+      if (ina) { pkey[pa] = (uint16_t)((k << 6) | lane); pe[pa] = ea; }
+      if (inb) { pkey[pb] = (uint16_t)((k << 6) | (lane + 32)); pe[pb] = eb; }
       pbase += na + __popc(mb);
     }
   }
@@ -148,8 +147,7 @@ __device__ __forceinline__ void eval_chunk_iso(const ChunkSmem& w, int kc, const
 template <bool kRecord>
 __device__ __forceinline__ void eval_chunk(const ChunkSmem& w, int kc, const float (&xa)[3], const float (&xb)[3],
                                            float tau2, float (&ya)[3], float (&yb)[3],
-                                           uint16_t* pkey, float* pe, int& pbase, int cap, int lane,
-                                           uint32_t fa = ~0u, uint32_t fb = ~0u) {
+                                           uint16_t* pkey, float* pe, int& pbase, int cap, int lane) {
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll 2
   for (int k = 0; k < kc; ++k) {
@@ -165,17 +163,16 @@ __device__ __forceinline__ void eval_chunk(const ChunkSmem& w, int kc, const flo
       yb[0] = fmaf(g.v0, eb, yb[0]); yb[1] = fmaf(g.v1, eb, yb[1]); yb[2] = fmaf(g.v2, eb, yb[2]);
       continue;
     }
-    const uint32_t ia = __ballot_sync(0xffffffffu, ina), ib = __ballot_sync(0xffffffffu, inb);
-    if (ia | ib) {
-      const uint32_t ma = ia & fa, mb = ib & fb;      // pairs of fitted samples only
+    const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = __ballot_sync(0xffffffffu, inb);
+    if (ma | mb) {
       const float xa_ = ex2_approx(Qa * kNegHalfLog2e), xb_ = ex2_approx(Qb * kNegHalfLog2e);
       const float ea = ina ? xa_ : 0.f, eb = inb ? xb_ : 0.f;
       ya[0] = fmaf(g.v0, ea, ya[0]); ya[1] = fmaf(g.v1, ea, ya[1]); ya[2] = fmaf(g.v2, ea, ya[2]);
       yb[0] = fmaf(g.v0, eb, yb[0]); yb[1] = fmaf(g.v1, eb, yb[1]); yb[2] = fmaf(g.v2, eb, yb[2]);
       const int na = __popc(ma);
       const int pa = min(pbase + __popc(ma & lt), cap - 1), pb = min(pbase + na + __popc(mb & lt), cap - 1);
-      if ((ma >> lane) & 1u) { pkey[pa] = (uint16_t)((k << 6) | lane); pe[pa] = ea; }
-      if ((mb >> lane) & 1u) { pkey[pb] = (uint16_t)((k << 6) | (lane + 32)); pe[pb] = eb; }
+      if (ina) { pkey[pa] = (uint16_t)((k << 6) | lane); pe[pa] = ea; }
+      if (inb) { pkey[pb] = (uint16_t)((k << 6) | (lane + 32)); pe[pb] = eb; }
       pbase += na + __popc(mb);
     }
   }
@@ -306,9 +303,6 @@ __device__ __forceinline__ void query_out(float* out, const float* att, const fl
   __stcs(out + 3 * i, o0); __stcs(out + 3 * i + 1, o1); __stcs(out + 3 * i + 2, o2);
 }
 
-// kQ: lookups ride along in the bins (gc_fit_query); instantiated apart so that gc_fit's
-// kernel carries no query bookkeeping.
-template <bool kQ>
 __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
   pdl_enter();
   extern __shared__ __align__(16) unsigned char dsm[];
@@ -336,38 +330,18 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
     float4 pa, pb4;
     load_pos(a.bin, 2, wi.start, wi.count, lane, xa, pa);
     load_pos(a.bin, 2, wi.start, wi.count, lane + 32, xb, pb4);
-    bool fita = false, fitb = false;              // fitted sample (else a query riding along, q.z = 1)
     if (lane < wi.count) {
       const float4 q = __ldcs(a.bin + 2 * (int64_t)(wi.start + lane) + 1);
       ta[0] = pa.w; ta[1] = q.x; ta[2] = q.y;
-      fita = !kQ || q.z == 0.f;
     }
     if (lane + 32 < wi.count) {
       const float4 q = __ldcs(a.bin + 2 * (int64_t)(wi.start + lane + 32) + 1);
       tb[0] = pb4.w; tb[1] = q.x; tb[2] = q.y;
-      fitb = !kQ || q.z == 0.f;
     }
-    const uint32_t fa = kQ ? __ballot_sync(0xffffffffu, fita) : ~0u;
-    const uint32_t fb = kQ ? __ballot_sync(0xffffffffu, fitb) : ~0u;
-    const int nfit = kQ ? __popc(fa) + __popc(fb) : wi.count;
     const float xref = __shfl_sync(0xffffffffu, xa[0], 0), yref = __shfl_sync(0xffffffffu, xa[1], 0),
                 zref = __shfl_sync(0xffffffffu, xa[2], 0);
     xa[0] -= xref; xa[1] -= yref; xa[2] -= zref;            // NaN stays NaN
     xb[0] -= xref; xb[1] -= yref; xb[2] -= zref;
-    if (kQ && nfit == 0) {                      // lookups only: gc_query's forward pass
-      float ya[3] = {0.f, 0.f, 0.f}, yb[3] = {0.f, 0.f, 0.f};
-      int pbase = 0;
-      for (int cb = 0; cb < C; cb += 32) {
-        const int kc = min(32, C - cb);
-        if (stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref, tau2))
-          eval_chunk_iso<false>(w, kc, xa, xb, ya, yb, nullptr, nullptr, pbase, 0, lane);
-        else
-          eval_chunk<false>(w, kc, xa, xb, tau2, ya, yb, nullptr, nullptr, pbase, 0, lane);
-      }
-      if (lane < wi.count) query_out(a.out, a.att, a.beta, a.unb, __float_as_uint(pa.w), ya);
-      if (lane + 32 < wi.count) query_out(a.out, a.att, a.beta, a.unb, __float_as_uint(pb4.w), yb);
-      continue;
-    }
     // ---------------- pass 1 (records the inside pairs while they fit)
     float ya[3] = {0.f, 0.f, 0.f}, yb[3] = {0.f, 0.f, 0.f};
     int pbase = 0;
@@ -376,27 +350,25 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
     for (int cb = 0, c = 0; cb < C; cb += 32, ++c) {
       const int kc = min(32, C - cb);
       iso = stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref, tau2);
-      if (iso) eval_chunk_iso<true>(w, kc, xa, xb, ya, yb, w.pkey, w.pe, pbase, kPairCap, lane, fa, fb);
-      else eval_chunk<true>(w, kc, xa, xb, tau2, ya, yb, w.pkey, w.pe, pbase, kPairCap, lane, fa, fb);
+      if (iso) eval_chunk_iso<true>(w, kc, xa, xb, ya, yb, w.pkey, w.pe, pbase, kPairCap, lane);
+      else eval_chunk<true>(w, kc, xa, xb, tau2, ya, yb, w.pkey, w.pe, pbase, kPairCap, lane);
       if (lane == 0 && c < kMaxChunks) w.cend[c] = (uint16_t)min(pbase, 0xFFFF);
     }
     const int np = pbase;                        // inside pairs of the item (warp-uniform)
     const bool recorded = chunks_fit && pbase <= kPairCap;
     // ---------------- Eq. 4 loss and dL/dyhat (unnormalised)
     float ga[3] = {0.f, 0.f, 0.f}, gb[3] = {0.f, 0.f, 0.f}, ls = 0.f;
-    if (fita) hdr_grad(a.mode, eps, ya, ta, ga, ls);
-    else if (kQ && lane < wi.count) query_out(a.out, a.att, a.beta, a.unb, __float_as_uint(pa.w), ya);
-    if (fitb) hdr_grad(a.mode, eps, yb, tb, gb, ls);
-    else if (kQ && lane + 32 < wi.count) query_out(a.out, a.att, a.beta, a.unb, __float_as_uint(pb4.w), yb);
+    if (lane < wi.count) hdr_grad(a.mode, eps, ya, ta, ga, ls);
+    if (lane + 32 < wi.count) hdr_grad(a.mode, eps, yb, tb, gb, ls);
     w.sxg[lane] = make_float4(xa[0], xa[1], xa[2], ga[0]);
     w.sg[lane] = make_float2(ga[1], ga[2]);
     w.sxg[lane + 32] = make_float4(xb[0], xb[1], xb[2], gb[0]);
     w.sg[lane + 32] = make_float2(gb[1], gb[2]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
-    if (lane == 0) { s_loss[wid][wi.level] += (double)ls; s_nfit[wid][wi.level] += (uint32_t)nfit; }
+    if (lane == 0) { s_loss[wid][wi.level] += (double)ls; s_nfit[wid][wi.level] += (uint32_t)wi.count; }
     pairs_acc += (unsigned)np;
-    cand_acc += (unsigned long long)nfit * (unsigned long long)C;
+    cand_acc += (unsigned long long)wi.count * (unsigned long long)C;
     __syncwarp();
     if (np == 0) continue;
     // ---------------- pass 2
@@ -432,15 +404,15 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
             ina = Qa <= tau2; inb = Qb <= tau2;
             ea = ex2_approx(Qa * kNegHalfLog2e); eb = ex2_approx(Qb * kNegHalfLog2e);
           }
-          const uint32_t ma = __ballot_sync(0xffffffffu, ina) & fa, mb = __ballot_sync(0xffffffffu, inb) & fb;
+          const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = __ballot_sync(0xffffffffu, inb);
           if (!(ma | mb)) continue;
           if (pb + 64 > kPairCap) { chunk_pairs_bwd(w, 0, pb, a.grad, lane, ci, a.lite); pb = 0; }
-          if ((ma >> lane) & 1u) {
+          if (ina) {
             const int pos = pb + __popc(ma & lt);
             w.pkey[pos] = (uint16_t)((k << 6) | lane);
             w.pe[pos] = ea;
           }
-          if ((mb >> lane) & 1u) {
+          if (inb) {
             const int pos = pb + __popc(ma) + __popc(mb & lt);
             w.pkey[pos] = (uint16_t)((k << 6) | (lane + 32));
             w.pe[pos] = eb;
@@ -522,10 +494,8 @@ static int persistent_grid(const void* fn, size_t smem) {
 
 int fwdbwd_grid() {
   static int g = [] {
-    cudaFuncSetAttribute(k_fwdbwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdBwdSmem);
-    cudaFuncSetAttribute(k_fwdbwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdBwdSmem);
-    return std::min(persistent_grid((const void*)k_fwdbwd<false>, kFwdBwdSmem),
-                    persistent_grid((const void*)k_fwdbwd<true>, kFwdBwdSmem));
+    cudaFuncSetAttribute(k_fwdbwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdBwdSmem);
+    return persistent_grid((const void*)k_fwdbwd, kFwdBwdSmem);
   }();
   return g;
 }
@@ -533,8 +503,7 @@ int query_grid() { static int g = persistent_grid((const void*)k_query, 0); retu
 
 void launch_fwdbwd(const FitArgs& a, int grid, cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "fwdbwd", s);
-  if (a.out) launch_pdl(k_fwdbwd<true>, dim3(grid), dim3(256), kFwdBwdSmem, s, a);
-  else launch_pdl(k_fwdbwd<false>, dim3(grid), dim3(256), kFwdBwdSmem, s, a);
+  launch_pdl(k_fwdbwd, dim3(grid), dim3(256), kFwdBwdSmem, s, a);
 }
 
 void launch_query(const QueryArgs& a, int grid, cudaStream_t s, Profiler* prof) {

@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(256, 4) k_keys(const float* __restrict__ pos, 
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       base[u] = 0;
-      const uint32_t r = b.rep_base + (uint32_t)(((i0 + u * 32) >> 5) & b.rep_mask);
+      const uint32_t r = (uint32_t)(((i0 + u * 32) >> 5) & (kRep - 1));
       if (key[u] != kInvalidKey && lane == __ffs(peers[u]) - 1)
         base[u] = atomicAdd(b.cell_count + (size_t)r * b.nc + key[u], (uint32_t)__popc(peers[u]));
     }
@@ -89,8 +89,7 @@ __global__ void __launch_bounds__(256, 4) k_keys(const float* __restrict__ pos, 
 }
 
 __global__ void __launch_bounds__(256, 4) k_scatter(const float* __restrict__ pos, const float* __restrict__ rgb,
-                                                 int64_t S, const uint32_t* __restrict__ cell_start, IngestBufs b,
-                                                 int mode) {
+                                                 int64_t S, const uint32_t* __restrict__ cell_start, IngestBufs b) {
   pdl_enter();
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t T = (int64_t)gridDim.x * blockDim.x;
@@ -105,8 +104,7 @@ __global__ void __launch_bounds__(256, 4) k_scatter(const float* __restrict__ po
 #pragma unroll
     for (int u = 0; u < kU; ++u)
       d[u] = key[u] != kInvalidKey
-                 ? __ldg(cell_start + (size_t)(b.rep_base + (((i0 + u * 32) >> 5) & b.rep_mask)) * b.nc + key[u]) +
-                       rank[u]
+                 ? __ldg(cell_start + (size_t)(((i0 + u * 32) >> 5) & (kRep - 1)) * b.nc + key[u]) + rank[u]
                  : 0u;
     float v[kU][6];
 #pragma unroll
@@ -121,12 +119,9 @@ __global__ void __launch_bounds__(256, 4) k_scatter(const float* __restrict__ po
     for (int u = 0; u < kU; ++u) {
       if (key[u] == kInvalidKey) continue;
       const int64_t i = i0 + u * 32;
-      if (mode == 0) {
+      if (rgb) {
         b.bin[2 * (int64_t)d[u]] = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
         b.bin[2 * (int64_t)d[u] + 1] = make_float4(v[u][4], v[u][5], 0.f, 0.f);
-      } else if (mode == 2) {
-        b.bin[2 * (int64_t)d[u]] = make_float4(v[u][0], v[u][1], v[u][2], __uint_as_float((uint32_t)i));
-        b.bin[2 * (int64_t)d[u] + 1] = make_float4(0.f, 0.f, 1.f, 0.f);
       } else {
         b.bin[d[u]] = make_float4(v[u][0], v[u][1], v[u][2], __uint_as_float((uint32_t)i));
       }
@@ -159,9 +154,9 @@ void launch_keys_query(const float* pos, const int32_t* len, int level_fixed, in
 }
 
 void launch_scatter(const float* pos, const float* rgb, int64_t S, const uint32_t* cell_start,
-                    IngestBufs b, int mode, cudaStream_t s, Profiler* prof) {
-  ProfScope ps(prof, mode == 0 ? "ingest_scatter" : "query_scatter", s);
-  launch_pdl(k_scatter, dim3(grid_for(S)), dim3(256), 0, s, pos, rgb, S, cell_start, b, mode);
+                    IngestBufs b, cudaStream_t s, Profiler* prof) {
+  ProfScope ps(prof, rgb ? "ingest_scatter" : "query_scatter", s);
+  launch_pdl(k_scatter, dim3(grid_for(S)), dim3(256), 0, s, pos, rgb, S, cell_start, b);
 }
 
 void launch_levels_of(const uint32_t* key, int64_t S, const LevelGeom& g, int32_t* out, cudaStream_t s) {

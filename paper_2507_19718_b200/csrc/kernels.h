@@ -90,16 +90,14 @@ struct IngestBufs {
   float4* bin;          // binned samples, cell-major: fit 2 x float4 (x,y,z,r | g,b,-,-),
                         // query 1 x float4 (x,y,z, original index as bits)
   int64_t nc;           // cells (counters are replica-major [kRep][nc])
-  uint32_t rep_base, rep_mask;   // counter replica of sample i: rep_base + ((i >> 5) & rep_mask)
 };
 void launch_keys(const float* pos, const int32_t* len, const float* rgb, int level_fixed,
                  int64_t S, const LevelGeom& g, IngestBufs b, cudaStream_t s, Profiler* prof);
 void launch_keys_query(const float* pos, const int32_t* len, int level_fixed, int64_t S,
                        const LevelGeom& g, IngestBufs b, float* out, cudaStream_t s, Profiler* prof);
-// mode 0: fit samples, 32-B bins (x y z r | g b 0 -); mode 1: query-only, 16-B bins
-// (x y z idx); mode 2: queries riding in fit bins (x y z idx | 0 0 1 -).
+// rgb != NULL: fit samples, 32-B bins (x y z r | g b - -); else lookups, 16-B bins (x y z idx).
 void launch_scatter(const float* pos, const float* rgb, int64_t S, const uint32_t* cell_start,
-                    IngestBufs b, int mode, cudaStream_t s, Profiler* prof);
+                    IngestBufs b, cudaStream_t s, Profiler* prof);
 void launch_levels_of(const uint32_t* key, int64_t S, const LevelGeom& g, int32_t* out,
                       cudaStream_t s);
 
@@ -108,7 +106,6 @@ struct FitArgs {
   const WorkItem* work; const uint32_t* n_work;
   const uint32_t* csr_off; const int32_t* csr_idx; const float4* rec;
   const float4* bin;
-  float* out; const float* att; const float* beta; const float* unb;   // queries riding along
   float* grad;          // [G][12]
   double* partial;      // [grid][kMaxL + 2]: per-block loss sums, pairs, candidates
   float tau2, hdr_eps; int mode; int L;

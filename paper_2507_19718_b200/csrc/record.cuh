@@ -58,24 +58,7 @@ __device__ __forceinline__ void make_record(const float p[kNP], float4 out[3]) {
 // the order the oracle writes them, so both produce the same integers.
 __device__ __forceinline__ void cull_range(const float p[kNP], double tau, const LevelGeom& g, int l,
                                            int32_t lo[3], int32_t hi[3], double& r2) {
-  double w = p[P_Q], x = p[P_Q + 1], y = p[P_Q + 2], z = p[P_Q + 3];
-  double n2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(w, w), __dmul_rn(x, x)), __dmul_rn(y, y)), __dmul_rn(z, z));
-  if (n2 < 1e-24) { w = 1.0; x = 0.0; y = 0.0; z = 0.0; }
-  else {
-    double n = __dsqrt_rn(n2);
-    w = __ddiv_rn(w, n); x = __ddiv_rn(x, n); y = __ddiv_rn(y, n); z = __ddiv_rn(z, n);
-  }
-  double R[3][3];
-  R[0][0] = __dsub_rn(1.0, __dmul_rn(2.0, __dadd_rn(__dmul_rn(y, y), __dmul_rn(z, z))));
-  R[0][1] = __dmul_rn(2.0, __dsub_rn(__dmul_rn(x, y), __dmul_rn(w, z)));
-  R[0][2] = __dmul_rn(2.0, __dadd_rn(__dmul_rn(x, z), __dmul_rn(w, y)));
-  R[1][0] = __dmul_rn(2.0, __dadd_rn(__dmul_rn(x, y), __dmul_rn(w, z)));
-  R[1][1] = __dsub_rn(1.0, __dmul_rn(2.0, __dadd_rn(__dmul_rn(x, x), __dmul_rn(z, z))));
-  R[1][2] = __dmul_rn(2.0, __dsub_rn(__dmul_rn(y, z), __dmul_rn(w, x)));
-  R[2][0] = __dmul_rn(2.0, __dsub_rn(__dmul_rn(x, z), __dmul_rn(w, y)));
-  R[2][1] = __dmul_rn(2.0, __dadd_rn(__dmul_rn(y, z), __dmul_rn(w, x)));
-  R[2][2] = __dsub_rn(1.0, __dmul_rn(2.0, __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y))));
-  double U2[3];
+  double U1[3], U2[3];
 #pragma unroll
   for (int b = 0; b < 3; ++b) {
     double sk = __dmul_rn((double)p[P_S + b], kK32);
@@ -83,18 +66,44 @@ __device__ __forceinline__ void cull_range(const float p[kNP], double tau, const
     if (sk > 32000.0) sk = 32000.0;
     int32_t k = (int32_t)ceil(sk) + 1;
     int32_t Qe = (k >= 0) ? k / 32 : -((-k + 31) / 32);
-    double U = ldexp(kT32[k - 32 * Qe], Qe);
-    U2[b] = __dmul_rn(U, U);
+    U1[b] = ldexp(kT32[k - 32 * Qe], Qe);
+    U2[b] = __dmul_rn(U1[b], U1[b]);
+  }
+  double h[3];
+  if (p[P_S] == p[P_S + 1] && p[P_S + 1] == p[P_S + 2]) {
+    // isotropic: a ball of radius tau e^s <= tau U (R R^T = I), no rotation needed
+    h[0] = h[1] = h[2] = __dmul_rn(tau, U1[0]);
+  } else {
+    double w = p[P_Q], x = p[P_Q + 1], y = p[P_Q + 2], z = p[P_Q + 3];
+    double n2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(w, w), __dmul_rn(x, x)), __dmul_rn(y, y)), __dmul_rn(z, z));
+    if (n2 < 1e-24) { w = 1.0; x = 0.0; y = 0.0; z = 0.0; }
+    else {
+      double n = __dsqrt_rn(n2);
+      w = __ddiv_rn(w, n); x = __ddiv_rn(x, n); y = __ddiv_rn(y, n); z = __ddiv_rn(z, n);
+    }
+    double R[3][3];
+    R[0][0] = __dsub_rn(1.0, __dmul_rn(2.0, __dadd_rn(__dmul_rn(y, y), __dmul_rn(z, z))));
+    R[0][1] = __dmul_rn(2.0, __dsub_rn(__dmul_rn(x, y), __dmul_rn(w, z)));
+    R[0][2] = __dmul_rn(2.0, __dadd_rn(__dmul_rn(x, z), __dmul_rn(w, y)));
+    R[1][0] = __dmul_rn(2.0, __dadd_rn(__dmul_rn(x, y), __dmul_rn(w, z)));
+    R[1][1] = __dsub_rn(1.0, __dmul_rn(2.0, __dadd_rn(__dmul_rn(x, x), __dmul_rn(z, z))));
+    R[1][2] = __dmul_rn(2.0, __dsub_rn(__dmul_rn(y, z), __dmul_rn(w, x)));
+    R[2][0] = __dmul_rn(2.0, __dsub_rn(__dmul_rn(x, z), __dmul_rn(w, y)));
+    R[2][1] = __dmul_rn(2.0, __dadd_rn(__dmul_rn(y, z), __dmul_rn(w, x)));
+    R[2][2] = __dsub_rn(1.0, __dmul_rn(2.0, __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y))));
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double s0 = __dmul_rn(__dmul_rn(R[a][0], R[a][0]), U2[0]);
+      double s1 = __dmul_rn(__dmul_rn(R[a][1], R[a][1]), U2[1]);
+      double s2 = __dmul_rn(__dmul_rn(R[a][2], R[a][2]), U2[2]);
+      h[a] = __dmul_rn(tau, __dsqrt_rn(__dadd_rn(__dadd_rn(s0, s1), s2)));
+    }
   }
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    double s0 = __dmul_rn(__dmul_rn(R[a][0], R[a][0]), U2[0]);
-    double s1 = __dmul_rn(__dmul_rn(R[a][1], R[a][1]), U2[1]);
-    double s2 = __dmul_rn(__dmul_rn(R[a][2], R[a][2]), U2[2]);
-    double h = __dmul_rn(tau, __dsqrt_rn(__dadd_rn(__dadd_rn(s0, s1), s2)));
     double mu = (double)p[P_MU + a];
-    lo[a] = clampcell(floor(__dmul_rn(__dsub_rn(__dsub_rn(mu, h), g.origin[l][a]), g.inv_cell[l][a])), g.dims[l][a]);
-    hi[a] = clampcell(floor(__dmul_rn(__dsub_rn(__dadd_rn(mu, h), g.origin[l][a]), g.inv_cell[l][a])), g.dims[l][a]);
+    lo[a] = clampcell(floor(__dmul_rn(__dsub_rn(__dsub_rn(mu, h[a]), g.origin[l][a]), g.inv_cell[l][a])), g.dims[l][a]);
+    hi[a] = clampcell(floor(__dmul_rn(__dsub_rn(__dadd_rn(mu, h[a]), g.origin[l][a]), g.inv_cell[l][a])), g.dims[l][a]);
   }
   double um = U2[0];
   if (U2[1] > um) um = U2[1];

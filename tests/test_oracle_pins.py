@@ -444,6 +444,26 @@ def test_cull_bound_is_transcendental_free_and_tight():
         assert 2 ** (1 / 32) < np.sqrt(r2[0]) / np.exp(s) <= 2 ** (2 / 32)
 
 
+def test_cull_range_isotropic_ignores_rotation_and_contains_ball():
+    """C8 isotropic case: a ball's extent does not depend on the quaternion (h = tau U), and
+    every point of the tau e^s ball lies inside the cell range."""
+    r = np.random.default_rng(21)
+    grid = (np.zeros(3) - 1.0, np.full(3, 37.3), np.full(3, 75, np.int32))
+    for _ in range(200):
+        P = np.zeros((2, 14))
+        P[:, 0:3] = r.uniform(-0.8, 0.8, 3)
+        P[:, 10:13] = r.uniform(-4.5, -2.0)
+        P[0, 3] = 1.0
+        P[1, 3:7] = r.normal(size=4)                          # arbitrary rotation
+        rng, r2 = oracle.cull_ranges(P, 3.0, *grid)
+        np.testing.assert_array_equal(rng[0], rng[1])
+        assert r2[0] == r2[1]
+        u = r.normal(size=(500, 3)); u /= np.linalg.norm(u, axis=1, keepdims=True)
+        pts = P[0, 0:3] + u * 3.0 * np.exp(P[0, 10])        # the ball's surface
+        c = oracle.sample_cell(pts, *grid)
+        assert np.all(c >= rng[0, :3]) and np.all(c <= rng[0, 3:])
+
+
 def test_cell_sphere_test_prunes_aabb_corners():
     """C8 list membership = AABB range AND sphere-box test: strictly fewer entries than the
     AABB alone for an isotropic Gaussian straddling cells, and never losing a covered cell."""
