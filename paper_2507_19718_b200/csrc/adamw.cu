@@ -162,8 +162,8 @@ void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp
   launch_pdl(k_step_scalars, dim3(1), dim3(32), 0, s, lvl, st, step_hp(hp, L), dev_stats);
 }
 
-void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, float4* rec, uint4* range,
-                  double* rad2, uint32_t* csr_count, float* dbg_grad, DevState* st, const gc_hparams& hp,
+void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, CullBufs cb, float* dbg_grad,
+                  DevState* st, const gc_hparams& hp,
                   const LevelGeom& g, gc_fit_stats* dev_stats, cudaStream_t s, Profiler* prof) {
   AdamHP h;
   for (int k = 0; k < GC_NGROUPS; ++k) h.wd[k] = hp.weight_decay[k];
@@ -175,7 +175,7 @@ void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, float4* 
   }
   {
     ProfScope ps(prof, "record_cull", s);
-    launch_record_cull(G, P, h.tau, g, rec, range, rad2, csr_count, s);
+    launch_record_cull(G, P, h.tau, g, cb, st, s);
   }
 }
 

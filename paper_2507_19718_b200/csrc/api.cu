@@ -81,7 +81,8 @@ struct gc_cache_s {
   float4* rec = nullptr;
   uint4* range = nullptr;
   double* rad2 = nullptr;
-  uint32_t *csr_count = nullptr, *csr_off = nullptr, *csr_cursor = nullptr, *csr_totals = nullptr;
+  uint32_t *csr_count = nullptr, *csr_off = nullptr, *csr_totals = nullptr;
+  uint32_t *csr_rank = nullptr, *csr_ovf = nullptr;   // entry ranks from the counting pass (CullBufs)
   int32_t* csr_idx = nullptr;
   uint2* csr_tiles = nullptr;
   uint32_t csr_cap = 0;
@@ -158,13 +159,16 @@ static gc_status ensure_staging(Scratch& sc, bool need_pos, bool need_len, bool 
   return GC_OK;
 }
 
+static CullBufs cull_bufs(gc_cache c) {
+  return CullBufs{c->rec, c->range, c->rad2, c->csr_count, c->csr_rank, c->csr_ovf, c->csr_cap};
+}
+
 static gc_status rebuild_csr(gc_cache c, cudaStream_t s, bool recompute_records) {
-  if (recompute_records) {
-    launch_record_cull(c->G, c->P, (double)c->hp.cutoff_sigma, c->geom, c->rec, c->range, c->rad2, c->csr_count, s);
-  }
-  launch_scan(c->csr_count, c->NC, 0, c->csr_tiles, c->csr_totals, c->csr_off, c->csr_cursor, nullptr,
-              c->geom, s, &c->prof);
-  launch_cull_emit(c->G, c->range, c->rad2, c->P, c->geom, c->csr_cursor, c->csr_idx, c->csr_cap, c->st, s, &c->prof);
+  if (recompute_records)
+    launch_record_cull(c->G, c->P, (double)c->hp.cutoff_sigma, c->geom, cull_bufs(c), c->st, s);
+  launch_scan(c->csr_count, c->NC, 0, c->csr_tiles, c->csr_totals, c->csr_off, nullptr, nullptr, c->geom, s,
+              &c->prof);
+  launch_cull_emit(c->G, cull_bufs(c), c->P, c->geom, c->csr_off, c->csr_idx, c->csr_cap, c->st, s, &c->prof);
   CK(cudaGetLastError());
   return GC_OK;
 }
@@ -356,13 +360,17 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
   if (c->NC >= (int64_t)1 << 31) return fail(GC_ERR_ARG, "culling grid too large (%lld cells)", (long long)c->NC);
 
   // records + culling lists; exact size of the first CSR sets the list capacity
-  CK(dalloc(&c->csr_count, c->NC)); CK(dalloc(&c->csr_off, c->NC + 1)); CK(dalloc(&c->csr_cursor, c->NC));
+  CK(dalloc(&c->csr_count, c->NC)); CK(dalloc(&c->csr_off, c->NC + 1));
   CK(dalloc(&c->csr_tiles, scan_state_words(c->NC)));
   CK(cudaMemset(c->csr_tiles, 0, sizeof(uint2) * scan_state_words(c->NC)));
   CK(dalloc(&c->csr_totals, 4));
   CK(cudaMemset(c->csr_count, 0, sizeof(uint32_t) * c->NC));
-  launch_record_cull(G, c->P, tau, c->geom, c->rec, c->range, c->rad2, c->csr_count, s);
-  launch_scan(c->csr_count, c->NC, 0, c->csr_tiles, c->csr_totals, c->csr_off, c->csr_cursor, nullptr, c->geom, s, nullptr);
+  CK(dalloc(&c->csr_rank, 27 * G));
+  // sizing pass (counts only; no wide-range rank slots yet): the first CSR's exact size sets
+  // the list capacity, then the real counting pass runs with full slot capacity
+  launch_record_cull(G, c->P, tau, c->geom, CullBufs{c->rec, c->range, c->rad2, c->csr_count, c->csr_rank, nullptr, 0u},
+                     c->st, s);
+  launch_scan(c->csr_count, c->NC, 0, c->csr_tiles, c->csr_totals, c->csr_off, nullptr, nullptr, c->geom, s, nullptr);
   CK(cudaGetLastError());
   uint32_t total = 0;
   CK(cudaMemcpy(&total, c->csr_totals, sizeof(uint32_t), cudaMemcpyDeviceToHost));
@@ -370,7 +378,12 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
   cap = std::min<uint64_t>(cap, 0x7FFFFFFFull);
   c->csr_cap = (uint32_t)cap;
   CK(dalloc(&c->csr_idx, c->csr_cap));
-  launch_cull_emit(G, c->range, c->rad2, c->P, c->geom, c->csr_cursor, c->csr_idx, c->csr_cap, c->st, s, nullptr);
+  CK(dalloc(&c->csr_ovf, c->csr_cap));
+  CK(cudaMemset(&c->st->csr_overflow, 0, sizeof(unsigned int)));
+  CK(cudaMemset(&c->st->ovf_next, 0, sizeof(unsigned int)));
+  launch_record_cull(G, c->P, tau, c->geom, cull_bufs(c), c->st, s);
+  launch_scan(c->csr_count, c->NC, 0, c->csr_tiles, c->csr_totals, c->csr_off, nullptr, nullptr, c->geom, s, nullptr);
+  launch_cull_emit(G, cull_bufs(c), c->P, c->geom, c->csr_off, c->csr_idx, c->csr_cap, c->st, s, nullptr);
   CK(cudaGetLastError());
 
   c->fb_grid = fwdbwd_grid();
@@ -388,7 +401,8 @@ static void destroy_impl(gc_cache c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  void* ps[] = {c->P, c->M, c->V, c->grad, c->dbg, c->rec, c->range, c->rad2, c->csr_count, c->csr_off, c->csr_cursor,
+  void* ps[] = {c->P, c->M, c->V, c->grad, c->dbg, c->rec, c->range, c->rad2, c->csr_count, c->csr_off, c->csr_rank,
+                c->csr_ovf,
                 c->csr_totals, c->csr_idx, c->csr_tiles, c->st, c->lvl, c->dstats, c->partial, c->pack_tmp};
   for (void* p : ps) if (p) cudaFree(p);
   if (c->hstats) cudaFreeHost(c->hstats);
@@ -519,8 +533,8 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
     launch_step_scalars(c->lvl, c->st, c->hp, c->L, c->dstats, s);
   }
   if (join) CK(cudaStreamWaitEvent(s, join, 0));
-  launch_adamw(c->G, c->P, c->M, c->V, c->grad, c->rec, c->range, c->rad2, c->csr_count, c->dbg_on ? c->dbg : nullptr,
-               c->st, c->hp, c->geom, c->dstats, s, &c->prof);
+  launch_adamw(c->G, c->P, c->M, c->V, c->grad, cull_bufs(c), c->dbg_on ? c->dbg : nullptr, c->st, c->hp, c->geom,
+               c->dstats, s, &c->prof);
   if (gc_status e = rebuild_csr(c, s, false)) return e;
   if (gc_status e = emit_stats(c, stats, s)) return e;
   CK(cudaGetLastError());

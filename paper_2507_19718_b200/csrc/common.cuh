@@ -43,7 +43,7 @@ struct DevState {
   unsigned long long nonfinite;      // non-finite gradient elements skipped (this call)
   unsigned int csr_total;            // culling-list entries of the current CSR
   unsigned int csr_overflow;         // sticky: a rebuild exceeded the list capacity
-  unsigned int done;                 // (unused, kept for layout)
+  unsigned int ovf_next;             // bump allocator of the wide-range rank slots (per rebuild)
 };
 
 // Per-call level statistics; summed over ranks under data parallelism (all doubles so a

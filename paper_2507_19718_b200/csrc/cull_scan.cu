@@ -6,49 +6,40 @@
 
 namespace gsc {
 
-__global__ void k_record_cull(int64_t G, const float* __restrict__ P, double tau, LevelGeom g,
-                              float4* rec, uint4* range, double* rad2, uint32_t* csr_count) {
+__global__ void k_record_cull(int64_t G, const float* __restrict__ P, double tau, LevelGeom g, CullBufs cb,
+                              DevState* st) {
   pdl_enter();
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < G; j += (int64_t)gridDim.x * blockDim.x) {
     float p[kNP];
 #pragma unroll
     for (int k = 0; k < kNP; ++k) p[k] = P[k * G + j];
-    record_and_count(j, p, tau, g, rec, range, rad2, csr_count);
+    record_and_count(j, p, tau, g, cb, st);
   }
 }
 
-// Fill the culling lists: each Gaussian appends its global index to every cell of its range.
-// The order inside a cell is atomic order (unspecified); gc_debug_cull sorts on export.
-__global__ void k_cull_emit(int64_t G, const uint4* __restrict__ range, const double* __restrict__ rad2,
-                            const float* __restrict__ P, LevelGeom g, uint32_t* cursor, int32_t* idx,
-                            uint32_t cap, DevState* st) {
+// Fill the culling lists: entry of Gaussian j in cell c = off[c] + its rank from the counting
+// pass.  The order inside a cell is atomic order (unspecified); gc_debug_cull sorts on export.
+__global__ void k_cull_emit(int64_t G, CullBufs cb, const float* __restrict__ P, LevelGeom g,
+                            const uint32_t* __restrict__ off, int32_t* idx, uint32_t cap, DevState* st) {
   pdl_enter();
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->ovf_next = 0u;   // the counting pass is done
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < G; j += (int64_t)gridDim.x * blockDim.x) {
-    uint4 r = range[j];
-    const double r2 = rad2[j];
-    const double m0 = P[P_MU * G + j], m1 = P[(P_MU + 1) * G + j], m2 = P[(P_MU + 2) * G + j];
-    int l = level_of_gaussian(g, j);
+    const uint4 r = cb.range[j];
+    const int l = level_of_gaussian(g, j);
     const int32_t lo[3] = {(int32_t)(r.x & 0xFFFF), (int32_t)(r.y & 0xFFFF), (int32_t)(r.z & 0xFFFF)};
     const int32_t hi[3] = {(int32_t)(r.x >> 16), (int32_t)(r.y >> 16), (int32_t)(r.z >> 16)};
-    const int32_t nx = hi[0] - lo[0] + 1, ny = hi[1] - lo[1] + 1, nz = hi[2] - lo[2] + 1;
-    if (nx <= 3 && ny <= 3 && nz <= 3) {
-      // common case (a range spans <= 3 cells per axis at the auto cell size): all cursor
-      // atomics of the Gaussian are issued before any result is used
+    if (!(r.w >> 31)) {
       const int64_t dx = g.dims[l][0], dy = g.dims[l][1];
-      double tx[3], ty[3], tz[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        tx[c] = c < nx ? axis_d2(m0, lo[0] + c, g, l, 0) : 0.0;
-        ty[c] = c < ny ? axis_d2(m1, lo[1] + c, g, l, 1) : 0.0;
-        tz[c] = c < nz ? axis_d2(m2, lo[2] + c, g, l, 2) : 0.0;
-      }
+      const uint32_t mask = r.w;
       uint32_t pos[27];
 #pragma unroll
-      for (int q = 0; q < 27; ++q) {
-        const int qx = q % 3, qy = (q / 3) % 3, qz = q / 9;
+      for (int q = 0; q < 27; ++q) {               // all gathers in flight before the stores
         pos[q] = 0xFFFFFFFFu;
-        if (qx < nx && qy < ny && qz < nz && __dadd_rn(__dadd_rn(tx[qx], ty[qy]), tz[qz]) <= r2)
-          pos[q] = atomicAdd(cursor + g.coff[l] + ((int64_t)(lo[2] + qz) * dy + (lo[1] + qy)) * dx + (lo[0] + qx), 1u);
+        if ((mask >> q) & 1u) {
+          const int qx = q % 3, qy = (q / 3) % 3, qz = q / 9;
+          pos[q] = __ldg(off + g.coff[l] + ((int64_t)(lo[2] + qz) * dy + (lo[1] + qy)) * dx + (lo[0] + qx)) +
+                   __ldg(cb.rank + 27 * j + q);
+        }
       }
 #pragma unroll
       for (int q = 0; q < 27; ++q) {
@@ -58,10 +49,16 @@ __global__ void k_cull_emit(int64_t G, const uint4* __restrict__ range, const do
       }
       continue;
     }
-    for_each_cell(lo, hi, m0, m1, m2, r2, g, l, [&](int64_t cell) {
-      const uint32_t pos = atomicAdd(cursor + cell, 1u);
-      if (pos < cap) idx[pos] = (int32_t)j;
-      else atomicOr(&st->csr_overflow, 1u);
+    const uint32_t base = r.w & 0x7FFFFFFFu;
+    const double m0 = P[P_MU * G + j], m1 = P[(P_MU + 1) * G + j], m2 = P[(P_MU + 2) * G + j];
+    uint32_t i = 0;
+    for_each_cell(lo, hi, m0, m1, m2, cb.rad2[j], g, l, [&](int64_t cell) {
+      if (base + i < cb.ovf_cap) {
+        const uint32_t pos = off[cell] + cb.ovf[base + i];
+        if (pos < cap) idx[pos] = (int32_t)j;
+        else atomicOr(&st->csr_overflow, 1u);
+      }
+      ++i;
     });
   }
 }
@@ -272,19 +269,19 @@ void launch_scan(uint32_t* cnt, int64_t n, int ch, uint2* state, uint32_t* total
   launch_pdl(k_scan, dim3(ntiles), dim3(kScanThreads), 0, s, cnt, n, ch, st, ctl, ntiles, totals, excl, excl_copy, work, g);
 }
 
-void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& g, float4* rec,
-                        uint4* range, double* rad2, uint32_t* csr_count, cudaStream_t s) {
-  int blocks = (int)std::min<int64_t>((G + 255) / 256, 148 * 16);
+void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& g, CullBufs cb, DevState* st,
+                        cudaStream_t s) {
+  int blocks = (int)std::min<int64_t>((G + 127) / 128, 148 * 32);
   if (blocks < 1) blocks = 1;
-  launch_pdl(k_record_cull, dim3(blocks), dim3(256), 0, s, G, P, tau, g, rec, range, rad2, csr_count);
+  launch_pdl(k_record_cull, dim3(blocks), dim3(128), 0, s, G, P, tau, g, cb, st);
 }
 
-void launch_cull_emit(int64_t G, const uint4* range, const double* rad2, const float* P, const LevelGeom& g,
-                      uint32_t* cursor, int32_t* idx, uint32_t cap, DevState* st, cudaStream_t s, Profiler* prof) {
+void launch_cull_emit(int64_t G, CullBufs cb, const float* P, const LevelGeom& g, const uint32_t* off,
+                      int32_t* idx, uint32_t cap, DevState* st, cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "cull_emit", s);
-  int blocks = (int)std::min<int64_t>((G + 255) / 256, 148 * 16);
+  int blocks = (int)std::min<int64_t>((G + 127) / 128, 148 * 32);
   if (blocks < 1) blocks = 1;
-  launch_pdl(k_cull_emit, dim3(blocks), dim3(256), 0, s, G, range, rad2, P, g, cursor, idx, cap, st);
+  launch_pdl(k_cull_emit, dim3(blocks), dim3(128), 0, s, G, cb, P, g, off, idx, cap, st);
 }
 
 }  // namespace gsc

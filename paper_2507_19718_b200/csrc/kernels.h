@@ -77,10 +77,18 @@ int scan_state_words(int64_t n);   // uint2 words of look-back state for an n-en
 void launch_scan(uint32_t* cnt, int64_t n, int ch, uint2* state, uint32_t* totals,
                  uint32_t* excl, uint32_t* excl_copy, WorkItem* work, const LevelGeom& g,
                  cudaStream_t s, Profiler* prof);
-void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& g, float4* rec,
-                        uint4* range, double* rad2, uint32_t* csr_count, cudaStream_t s);
-void launch_cull_emit(int64_t G, const uint4* range, const double* rad2, const float* P, const LevelGeom& g,
-                      uint32_t* cursor, int32_t* idx, uint32_t cap, DevState* st, cudaStream_t s, Profiler* prof);
+// Per-Gaussian culling state.  range[j] = (lo|hi<<16 per axis, w): w < 2^31 is the 27-bit
+// membership mask of the <= 3x3x3 range box, the rank of Gaussian j in cell q of that box in
+// rank[27 j + q]; w >= 2^31 marks a wider range whose ranks sit in ovf[w & 0x7fffffff ...] in
+// visiting order.  Ranks come from the counting atomics, so the emit pass needs neither
+// atomics nor the fp64 membership tests of the common case.
+struct CullBufs {
+  float4* rec; uint4* range; double* rad2; uint32_t* count; uint32_t* rank; uint32_t* ovf; uint32_t ovf_cap;
+};
+void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& g, CullBufs cb, DevState* st,
+                        cudaStream_t s);
+void launch_cull_emit(int64_t G, CullBufs cb, const float* P, const LevelGeom& g, const uint32_t* off,
+                      int32_t* idx, uint32_t cap, DevState* st, cudaStream_t s, Profiler* prof);
 
 // ingest.cu
 struct IngestBufs {
@@ -129,8 +137,8 @@ void launch_stats(double* partial, const LevelGeom& g, int64_t S, LvlStats* lvl,
                   const gc_hparams& hp, int L, gc_fit_stats* dev_stats, cudaStream_t s, Profiler* prof);
 void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp, int L,
                          gc_fit_stats* dev_stats, cudaStream_t s);
-void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, float4* rec, uint4* range,
-                  double* rad2, uint32_t* csr_count, float* dbg_grad, DevState* st, const gc_hparams& hp,
+void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, CullBufs cb, float* dbg_grad,
+                  DevState* st, const gc_hparams& hp,
                   const LevelGeom& g, gc_fit_stats* dev_stats, cudaStream_t s, Profiler* prof);
 
 // create.cu

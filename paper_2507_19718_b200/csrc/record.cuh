@@ -148,20 +148,59 @@ __device__ __forceinline__ void for_each_cell(const int32_t lo[3], const int32_t
   }
 }
 
+// Record, C8 range and membership counts of Gaussian j; the counting atomics return each
+// entry's rank inside its cell (see CullBufs).
 __device__ __forceinline__ void record_and_count(int64_t j, const float p[kNP], double tau, const LevelGeom& g,
-                                                 float4* rec, uint4* range, double* rad2, uint32_t* csr_count) {
+                                                 const CullBufs& cb, DevState* st) {
   float4 r[3];
   make_record(p, r);
-  rec[3 * j] = r[0]; rec[3 * j + 1] = r[1]; rec[3 * j + 2] = r[2];
+  cb.rec[3 * j] = r[0]; cb.rec[3 * j + 1] = r[1]; cb.rec[3 * j + 2] = r[2];
   const int l = level_of_gaussian(g, j);
   int32_t lo[3], hi[3];
   double r2;
   cull_range(p, tau, g, l, lo, hi, r2);
-  range[j] = make_uint4((uint32_t)lo[0] | ((uint32_t)hi[0] << 16), (uint32_t)lo[1] | ((uint32_t)hi[1] << 16),
-                        (uint32_t)lo[2] | ((uint32_t)hi[2] << 16), 0u);
-  rad2[j] = r2;
-  for_each_cell(lo, hi, (double)p[P_MU], (double)p[P_MU + 1], (double)p[P_MU + 2], r2, g, l,
-                [&](int64_t cell) { atomicAdd(csr_count + cell, 1u); });
+  cb.rad2[j] = r2;
+  const double m0 = p[P_MU], m1 = p[P_MU + 1], m2 = p[P_MU + 2];
+  const int32_t nx = hi[0] - lo[0] + 1, ny = hi[1] - lo[1] + 1, nz = hi[2] - lo[2] + 1;
+  uint32_t w;
+  if (nx <= 3 && ny <= 3 && nz <= 3) {
+    // common case: all counting atomics of the Gaussian in flight before any rank is stored
+    const int64_t dx = g.dims[l][0], dy = g.dims[l][1];
+    double tx[3], ty[3], tz[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      tx[c] = c < nx ? axis_d2(m0, lo[0] + c, g, l, 0) : 0.0;
+      ty[c] = c < ny ? axis_d2(m1, lo[1] + c, g, l, 1) : 0.0;
+      tz[c] = c < nz ? axis_d2(m2, lo[2] + c, g, l, 2) : 0.0;
+    }
+    uint32_t mask = 0, rk[27];
+#pragma unroll
+    for (int q = 0; q < 27; ++q) {
+      const int qx = q % 3, qy = (q / 3) % 3, qz = q / 9;
+      if (qx < nx && qy < ny && qz < nz && __dadd_rn(__dadd_rn(tx[qx], ty[qy]), tz[qz]) <= r2) {
+        mask |= 1u << q;
+        rk[q] = atomicAdd(cb.count + g.coff[l] + ((int64_t)(lo[2] + qz) * dy + (lo[1] + qy)) * dx + (lo[0] + qx), 1u);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 27; ++q)
+      if ((mask >> q) & 1u) cb.rank[27 * j + q] = rk[q];
+    w = mask;
+  } else {
+    int n = 0;
+    for_each_cell(lo, hi, m0, m1, m2, r2, g, l, [&](int64_t) { ++n; });
+    const uint32_t base = atomicAdd(&st->ovf_next, (uint32_t)n);
+    int i = 0;
+    for_each_cell(lo, hi, m0, m1, m2, r2, g, l, [&](int64_t cell) {
+      const uint32_t rk = atomicAdd(cb.count + cell, 1u);
+      if (base + i < cb.ovf_cap) cb.ovf[base + i] = rk;
+      else atomicOr(&st->csr_overflow, 1u);
+      ++i;
+    });
+    w = 0x80000000u | (base & 0x7FFFFFFFu);
+  }
+  cb.range[j] = make_uint4((uint32_t)lo[0] | ((uint32_t)hi[0] << 16), (uint32_t)lo[1] | ((uint32_t)hi[1] << 16),
+                           (uint32_t)lo[2] | ((uint32_t)hi[2] << 16), w);
 }
 
 }  // namespace gsc
