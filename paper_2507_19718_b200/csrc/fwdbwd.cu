@@ -107,8 +107,8 @@ __device__ __forceinline__ float iso_s(const float (&x)[3], const float4& c) {
 // Branch-free: e is computed for every lane and zeroed outside (MUFU has the slack; a
 // divergent inside block costs more issue slots than it saves).  Record positions are
 // clamped to cap - 1: an overflowing item is re-derived by the caller, so the clobbered
-// last slot is never read.
-template <bool kRecord>
+// last slot is never read.  kTwo = false: the item has <= 32 samples, sample b is skipped.
+template <bool kRecord, bool kTwo>
 __device__ __forceinline__ void eval_chunk_iso(const ChunkSmem& w, int kc, const float (&xa)[3], const float (&xb)[3],
                                                float (&ya)[3], float (&yb)[3], uint16_t* pkey, float* pe,
                                                int& pbase, int cap, int lane) {
@@ -116,25 +116,34 @@ __device__ __forceinline__ void eval_chunk_iso(const ChunkSmem& w, int kc, const
 #pragma unroll 2
   for (int k = 0; k < kc; ++k) {
     const float4 c = w.r0[k], f = w.r1[k];
-    const float sa = iso_s(xa, c), sb = iso_s(xb, c);
-    const bool ina = sa <= c.w, inb = sb <= c.w;
+    const float sa = iso_s(xa, c), sb = kTwo ? iso_s(xb, c) : 0.f;
+    const bool ina = sa <= c.w, inb = kTwo && sb <= c.w;
     if (!kRecord) {
-      const float xa_ = ex2_approx(f.x * sa), xb_ = ex2_approx(f.x * sb);
-      const float ea = ina ? xa_ : 0.f, eb = inb ? xb_ : 0.f;
+      const float xa_ = ex2_approx(f.x * sa);
+      const float ea = ina ? xa_ : 0.f;
       ya[0] = fmaf(f.y, ea, ya[0]); ya[1] = fmaf(f.z, ea, ya[1]); ya[2] = fmaf(f.w, ea, ya[2]);
-      yb[0] = fmaf(f.y, eb, yb[0]); yb[1] = fmaf(f.z, eb, yb[1]); yb[2] = fmaf(f.w, eb, yb[2]);
+      if constexpr (kTwo) {
+        const float xb_ = ex2_approx(f.x * sb);
+        const float eb = inb ? xb_ : 0.f;
+        yb[0] = fmaf(f.y, eb, yb[0]); yb[1] = fmaf(f.z, eb, yb[1]); yb[2] = fmaf(f.w, eb, yb[2]);
+      }
       continue;
     }
-    const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = __ballot_sync(0xffffffffu, inb);
+    const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = kTwo ? __ballot_sync(0xffffffffu, inb) : 0u;
     if (ma | mb) {
-      const float xa_ = ex2_approx(f.x * sa), xb_ = ex2_approx(f.x * sb);
-      const float ea = ina ? xa_ : 0.f, eb = inb ? xb_ : 0.f;
+      const float xa_ = ex2_approx(f.x * sa);
+      const float ea = ina ? xa_ : 0.f;
       ya[0] = fmaf(f.y, ea, ya[0]); ya[1] = fmaf(f.z, ea, ya[1]); ya[2] = fmaf(f.w, ea, ya[2]);
-      yb[0] = fmaf(f.y, eb, yb[0]); yb[1] = fmaf(f.z, eb, yb[1]); yb[2] = fmaf(f.w, eb, yb[2]);
       const int na = __popc(ma);
-      const int pa = min(pbase + __popc(ma & lt), cap - 1), pb = min(pbase + na + __popc(mb & lt), cap - 1);
+      const int pa = min(pbase + __popc(ma & lt), cap - 1);
       if (ina) { pkey[pa] = (uint16_t)((k << 6) | lane); pe[pa] = ea; }
-      if (inb) { pkey[pb] = (uint16_t)((k << 6) | (lane + 32)); pe[pb] = eb; }
+      if constexpr (kTwo) {
+        const float xb_ = ex2_approx(f.x * sb);
+        const float eb = inb ? xb_ : 0.f;
+        yb[0] = fmaf(f.y, eb, yb[0]); yb[1] = fmaf(f.z, eb, yb[1]); yb[2] = fmaf(f.w, eb, yb[2]);
+        const int pb = min(pbase + na + __popc(mb & lt), cap - 1);
+        if (inb) { pkey[pb] = (uint16_t)((k << 6) | (lane + 32)); pe[pb] = eb; }
+      }
       pbase += na + __popc(mb);
     }
   }
@@ -144,7 +153,7 @@ __device__ __forceinline__ void eval_chunk_iso(const ChunkSmem& w, int kc, const
 // Two samples per lane (a = lane, b = lane + 32; inactive samples carry x' = NaN, never
 // inside).  Accumulates yhat and, if kRecord, appends every inside pair at pbase + its rank
 // (candidate-major; sample a's before sample b's), up to `cap`; pbase advances regardless.
-template <bool kRecord>
+template <bool kRecord, bool kTwo>
 __device__ __forceinline__ void eval_chunk(const ChunkSmem& w, int kc, const float (&xa)[3], const float (&xb)[3],
                                            float tau2, float (&ya)[3], float (&yb)[3],
                                            uint16_t* pkey, float* pe, int& pbase, int cap, int lane) {
@@ -154,29 +163,53 @@ __device__ __forceinline__ void eval_chunk(const ChunkSmem& w, int kc, const flo
     const Cand g = cand_from(w, k);
     float w0, w1, w2;
     const float Qa = cand_q(g, xa[0], xa[1], xa[2], w0, w1, w2);
-    const float Qb = cand_q(g, xb[0], xb[1], xb[2], w0, w1, w2);
-    const bool ina = Qa <= tau2, inb = Qb <= tau2;
+    const float Qb = kTwo ? cand_q(g, xb[0], xb[1], xb[2], w0, w1, w2) : 0.f;
+    const bool ina = Qa <= tau2, inb = kTwo && Qb <= tau2;
     if (!kRecord) {
-      const float xa_ = ex2_approx(Qa * kNegHalfLog2e), xb_ = ex2_approx(Qb * kNegHalfLog2e);
-      const float ea = ina ? xa_ : 0.f, eb = inb ? xb_ : 0.f;
+      const float xa_ = ex2_approx(Qa * kNegHalfLog2e);
+      const float ea = ina ? xa_ : 0.f;
       ya[0] = fmaf(g.v0, ea, ya[0]); ya[1] = fmaf(g.v1, ea, ya[1]); ya[2] = fmaf(g.v2, ea, ya[2]);
-      yb[0] = fmaf(g.v0, eb, yb[0]); yb[1] = fmaf(g.v1, eb, yb[1]); yb[2] = fmaf(g.v2, eb, yb[2]);
+      if constexpr (kTwo) {
+        const float xb_ = ex2_approx(Qb * kNegHalfLog2e);
+        const float eb = inb ? xb_ : 0.f;
+        yb[0] = fmaf(g.v0, eb, yb[0]); yb[1] = fmaf(g.v1, eb, yb[1]); yb[2] = fmaf(g.v2, eb, yb[2]);
+      }
       continue;
     }
-    const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = __ballot_sync(0xffffffffu, inb);
+    const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = kTwo ? __ballot_sync(0xffffffffu, inb) : 0u;
     if (ma | mb) {
-      const float xa_ = ex2_approx(Qa * kNegHalfLog2e), xb_ = ex2_approx(Qb * kNegHalfLog2e);
-      const float ea = ina ? xa_ : 0.f, eb = inb ? xb_ : 0.f;
+      const float xa_ = ex2_approx(Qa * kNegHalfLog2e);
+      const float ea = ina ? xa_ : 0.f;
       ya[0] = fmaf(g.v0, ea, ya[0]); ya[1] = fmaf(g.v1, ea, ya[1]); ya[2] = fmaf(g.v2, ea, ya[2]);
-      yb[0] = fmaf(g.v0, eb, yb[0]); yb[1] = fmaf(g.v1, eb, yb[1]); yb[2] = fmaf(g.v2, eb, yb[2]);
       const int na = __popc(ma);
-      const int pa = min(pbase + __popc(ma & lt), cap - 1), pb = min(pbase + na + __popc(mb & lt), cap - 1);
+      const int pa = min(pbase + __popc(ma & lt), cap - 1);
       if (ina) { pkey[pa] = (uint16_t)((k << 6) | lane); pe[pa] = ea; }
-      if (inb) { pkey[pb] = (uint16_t)((k << 6) | (lane + 32)); pe[pb] = eb; }
+      if constexpr (kTwo) {
+        const float xb_ = ex2_approx(Qb * kNegHalfLog2e);
+        const float eb = inb ? xb_ : 0.f;
+        yb[0] = fmaf(g.v0, eb, yb[0]); yb[1] = fmaf(g.v1, eb, yb[1]); yb[2] = fmaf(g.v2, eb, yb[2]);
+        const int pb = min(pbase + na + __popc(mb & lt), cap - 1);
+        if (inb) { pkey[pb] = (uint16_t)((k << 6) | (lane + 32)); pe[pb] = eb; }
+      }
       pbase += na + __popc(mb);
     }
   }
   __syncwarp();
+}
+
+// One chunk of pass 1 (kRecord) or of a lookup: the isotropic or general evaluator, with
+// both samples per lane only when the item has more than 32.
+template <bool kRecord>
+__device__ __forceinline__ void eval_any(const ChunkSmem& w, bool iso, bool two, int kc, const float (&xa)[3],
+                                         const float (&xb)[3], float tau2, float (&ya)[3], float (&yb)[3],
+                                         uint16_t* pkey, float* pe, int& pbase, int cap, int lane) {
+  if (iso) {
+    if (two) eval_chunk_iso<kRecord, true>(w, kc, xa, xb, ya, yb, pkey, pe, pbase, cap, lane);
+    else eval_chunk_iso<kRecord, false>(w, kc, xa, xb, ya, yb, pkey, pe, pbase, cap, lane);
+  } else {
+    if (two) eval_chunk<kRecord, true>(w, kc, xa, xb, tau2, ya, yb, pkey, pe, pbase, cap, lane);
+    else eval_chunk<kRecord, false>(w, kc, xa, xb, tau2, ya, yb, pkey, pe, pbase, cap, lane);
+  }
 }
 
 // Gradient terms of pairs [p0, p1) of the staged chunk (lane = pair): 12 coefficient
@@ -350,8 +383,7 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
     for (int cb = 0, c = 0; cb < C; cb += 32, ++c) {
       const int kc = min(32, C - cb);
       iso = stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref, tau2);
-      if (iso) eval_chunk_iso<true>(w, kc, xa, xb, ya, yb, w.pkey, w.pe, pbase, kPairCap, lane);
-      else eval_chunk<true>(w, kc, xa, xb, tau2, ya, yb, w.pkey, w.pe, pbase, kPairCap, lane);
+      eval_any<true>(w, iso, wi.count > 32, kc, xa, xb, tau2, ya, yb, w.pkey, w.pe, pbase, kPairCap, lane);
       if (lane == 0 && c < kMaxChunks) w.cend[c] = (uint16_t)min(pbase, 0xFFFF);
     }
     const int np = pbase;                        // inside pairs of the item (warp-uniform)
@@ -472,10 +504,8 @@ __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
     int pbase = 0;
     for (int cb = 0; cb < C; cb += 32) {
       const int kc = min(32, C - cb);
-      if (stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref, tau2))
-        eval_chunk_iso<false>(w, kc, xa, xb, ya, yb, nullptr, nullptr, pbase, 0, lane);
-      else
-        eval_chunk<false>(w, kc, xa, xb, tau2, ya, yb, nullptr, nullptr, pbase, 0, lane);
+      const bool iso = stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref, tau2);
+      eval_any<false>(w, iso, wi.count > 32, kc, xa, xb, tau2, ya, yb, nullptr, nullptr, pbase, 0, lane);
     }
     if (lane < wi.count) query_out(a.out, a.att, a.beta, a.unb, __float_as_uint(pa.w), ya);
     if (lane + 32 < wi.count) query_out(a.out, a.att, a.beta, a.unb, __float_as_uint(pb4.w), yb);
