@@ -285,10 +285,13 @@ def run_ours(args):
     top = max(prof, key=lambda k: prof[k][0])
     n_pairs, n_cand = int(st.n_pairs), int(st.n_candidates)
     pk, pk_kind = peaks()
-    traffic = None
-    try:   # per-launch DRAM bytes of the dominant kernel from the committed ncu capture
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
-            traffic = json.load(f).get("gsc::k_" + top)
+    traffic, traffic_src = None, None
+    try:   # per-launch DRAM bytes of the dominant kernel from the committed ncu launch list
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        traffic = next((v for k, v in tj["bytes_per_launch"].items() if k.endswith("k_" + top) or
+                        k.endswith("k_" + top + "<0>")), None)
+        traffic_src = "profiles/traffic.json: " + tj["source"]
     except Exception:
         pass
     if top == "fwdbwd":
@@ -296,7 +299,7 @@ def run_ours(args):
         achieved = flops / (kernel_ms[top] * 1e-3) / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic, "kernel": top,
-                "traffic_source": "profiles/r01_traffic.json (ncu dram__bytes_read+write per launch)",
+                "traffic_source": traffic_src,
                 "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (B200_PROFILING.md counts/clock)",
                 "algorithmic": f"{FLOPS_PER_PAIR:.0f} flop/contributing pair + {FLOPS_PER_SAMPLE:.0f}/sample"}
     else:

@@ -33,9 +33,10 @@ def launches(path):
 def main(csv_path, rep_path, tag):
     L = launches(csv_path)
     per = collections.defaultdict(lambda: [0, 0.0, 0.0])
-    create = ("k_eq2", "k_knn3", "k_gather_init", "k_record_cull", "at::")   # gc_create / torch, not the step
+    # everything launched before the first step's k_keys belongs to gc_create; torch fills too
+    first = min((i for (i, name) in L if "k_keys" in name), default=0)
     for (i, name), m in L.items():
-        if any(c in name for c in create):
+        if i < first or name.startswith("at::") or "at::" in name:
             continue
         p = per[name]
         p[0] += 1
@@ -45,8 +46,8 @@ def main(csv_path, rep_path, tag):
     lines = [f"# ncu launch list summary ({tag})", "",
              "Cold-cache, serialised per-launch times from `ncu --metrics gpu__time_duration.sum,"
              "dram__bytes_read.sum,dram__bytes_write.sum --clock-control none` over the bench command "
-             "(compare SHARES, not absolutes).  gc_create's one-off kernels (Eq. 2 kNN etc.) and torch fills "
-             "are excluded: shares are of the timed fit+query step.", "",
+             "(compare SHARES, not absolutes).  Launches before the first step (gc_create: Eq. 2 kNN, first "
+             "culling build) and torch fills are excluded: shares are of the fit+query steps.", "",
              "| kernel | launches | mean us | share | DRAM MB/launch |", "|---|---|---|---|---|"]
     traffic = {}
     for name, (n, t, b) in sorted(per.items(), key=lambda x: -x[1][1]):
@@ -71,7 +72,8 @@ def main(csv_path, rep_path, tag):
             d = dict(zip(h, r))
             lines.append(f"| {d['Kernel Name'].split('(')[0]} | " + " | ".join(d[c] for c in h if '__' in c) + " |")
     print("\n".join(lines))
-    json.dump({k: v for k, v in traffic.items()}, open(f"profiles/{tag}_traffic.json", "w"), indent=1)
+    json.dump({"source": f"{tag} ncu launch list (dram__bytes_read.sum + dram__bytes_write.sum, mean per launch)",
+               "bytes_per_launch": traffic}, open("profiles/traffic.json", "w"), indent=1)
 
 
 if __name__ == "__main__":
