@@ -154,6 +154,17 @@ gc_status gc_query_radiance(gc_cache c, const float* pos, const int32_t* path_le
                             int64_t S, const float* attenuation, const float* beta,
                             const float* unbiased_rgb, float* out_rgb, gc_stream stream);
 
+/* Deferred optimizer step (enable != 0; off by default).  gc_fit / gc_fit_query then leave
+ * their optimizer half -- the AdamW step with the next step's evaluation records, and the
+ * culling-list rebuild -- pending, and the next call on the handle launches it on an internal
+ * stream forked from its own, overlapping that call's sample ingest; the pending step always
+ * completes before anything reads the cache (lookups, fwd/bwd, gc_params, gc_set_params,
+ * gc_debug_*, gc_reset_schedule), so every result is the same as without deferral.
+ * gc_fit_stats of a deferred call report nonfinite_grads of the PREVIOUS step (its own is not
+ * known yet).  gc_flush completes a pending step on `stream`. */
+gc_status gc_set_deferred_step(gc_cache c, int enable);
+gc_status gc_flush(gc_cache c, gc_stream stream);
+
 /* Copy out (gc_params) / in (gc_set_params) the raw parameters of one level in the paper's
  * layout.  dst/src arrays: host or device, `count` must equal the level's size.
  * gc_set_params rebuilds the level's evaluation records and culling lists; reset_adam != 0

@@ -24,7 +24,7 @@ STATUS = {0: "GC_OK", 1: "GC_ERR_ARG", 2: "GC_ERR_STATE", 3: "GC_ERR_CUDA", 4: "
 
 # Symbols include/gscache.h declares (checked by tests/test_abi.py).
 EXPORTS = ["gc_default_hparams", "gc_create", "gc_destroy", "gc_reserve", "gc_fit", "gc_query",
-           "gc_query_radiance", "gc_fit_query",
+           "gc_query_radiance", "gc_fit_query", "gc_set_deferred_step", "gc_flush",
            "gc_params", "gc_set_params", "gc_reset_schedule", "gc_grid", "gc_info",
            "gc_nccl_unique_id", "gc_set_comm", "gc_debug_enable_grads", "gc_debug_grads",
            "gc_debug_cull", "gc_debug_levels", "gc_profile_enable", "gc_profile_read",
@@ -97,6 +97,8 @@ def lib():
             "gc_query": (i32, [vp, vp, vp, i32, i64, vp, vp]),
             "gc_query_radiance": (i32, [vp, vp, vp, i32, i64, vp, vp, vp, vp, vp]),
             "gc_fit_query": (i32, [vp, vp, vp, vp, i64, vp, vp, i32, i64, vp, vp, vp, vp, vp, vp]),
+            "gc_set_deferred_step": (i32, [vp, i32]),
+            "gc_flush": (i32, [vp, vp]),
             "gc_params": (i32, [vp, i32, vp, vp]),
             "gc_set_params": (i32, [vp, i32, vp, i32, vp]),
             "gc_reset_schedule": (i32, [vp]),
@@ -339,6 +341,14 @@ class GSCache:
         self.set_params(level, dict(position=rows[:, 0:3], rotation=rows[:, 3:7],
                                     color=rows[:, 7:10], log_scale=rows[:, 10:13],
                                     opacity_logit=rows[:, 13:14]), reset_adam)
+
+    def set_deferred_step(self, on=True):
+        """gc_set_deferred_step: leave each fit's optimizer half pending for the next call."""
+        _check(lib().gc_set_deferred_step(self.h, 1 if on else 0))
+
+    def flush(self, stream=None):
+        """gc_flush: complete a pending (deferred) optimizer step on `stream`."""
+        _check(lib().gc_flush(self.h, _stream_ptr(stream)))
 
     def reset_schedule(self):
         _check(lib().gc_reset_schedule(self.h))

@@ -97,7 +97,7 @@ __device__ void chain_rule(const float p[kNP], const float cg[12], float out[kNP
 // k_record_cull right after (split so both kernels stay spill-free and latency-hidden).
 __global__ void __launch_bounds__(kAdamThreads, kAdamBlocksPerSM) k_adamw(
     int64_t G, float* __restrict__ P, float* __restrict__ M, float* __restrict__ V, float* __restrict__ grad,
-    float* __restrict__ dbg, const DevState* __restrict__ st, AdamHP hp, LevelGeom g, gc_fit_stats* out) {
+    float* __restrict__ dbg, const DevState* __restrict__ st, AdamHP hp, LevelGeom g, unsigned long long* nonfinite) {
   pdl_enter();
   unsigned long long bad = 0;
   float eta[GC_NGROUPS], dec[GC_NGROUPS];
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kAdamThreads, kAdamBlocksPerSM) k_adamw(
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
-  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(reinterpret_cast<unsigned long long*>(&out->nonfinite_grads), bad);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(nonfinite, bad);
 }
 
 static StepHP step_hp(const gc_hparams& hp, int L) {
@@ -164,14 +164,14 @@ void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp
 
 void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, CullBufs cb, float* dbg_grad,
                   DevState* st, const gc_hparams& hp,
-                  const LevelGeom& g, gc_fit_stats* dev_stats, cudaStream_t s, Profiler* prof) {
+                  const LevelGeom& g, unsigned long long* nonfinite, cudaStream_t s, Profiler* prof) {
   AdamHP h;
   for (int k = 0; k < GC_NGROUPS; ++k) h.wd[k] = hp.weight_decay[k];
   h.beta1 = hp.beta1; h.beta2 = hp.beta2; h.eps = hp.adam_eps; h.tau = (double)hp.cutoff_sigma;
   {
     ProfScope ps(prof, "adamw", s);
     int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((G + kAdamThreads - 1) / kAdamThreads, 148 * kAdamBlocksPerSM));
-    launch_pdl(k_adamw, dim3(blocks), dim3(kAdamThreads), 0, s, G, P, M, V, grad, dbg_grad, (const DevState*)st, h, g, dev_stats);
+    launch_pdl(k_adamw, dim3(blocks), dim3(kAdamThreads), 0, s, G, P, M, V, grad, dbg_grad, (const DevState*)st, h, g, nonfinite);
   }
   {
     ProfScope ps(prof, "record_cull", s);

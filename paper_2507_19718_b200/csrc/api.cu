@@ -104,6 +104,11 @@ struct gc_cache_s {
   int64_t pack_cap = 0;
   cudaStream_t side = nullptr;            // gc_fit_query: lookups run beside the fit samples' ingest
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // deferred optimizer step (gc_set_deferred_step): the AdamW step + culling rebuild of the
+  // last fit, launched by the next call on `side2`, overlapping that call's ingest
+  bool defer = false, pending = false;
+  cudaStream_t side2 = nullptr;
+  cudaEvent_t ev_fork2 = nullptr, ev_tail = nullptr;
 };
 
 // ------------------------------------------------------------------------- helpers
@@ -182,6 +187,37 @@ static bool is_pinned_host(const void* p) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
   return a.type == cudaMemoryTypeHost;
+}
+
+// The optimizer half of a fit: AdamW (+ next-step records and culling counts) and the
+// culling-list rebuild.  `nonfinite` receives the skipped-gradient count.
+static gc_status launch_tail(gc_cache c, cudaStream_t s, unsigned long long* nonfinite) {
+  launch_adamw(c->G, c->P, c->M, c->V, c->grad, cull_bufs(c), c->dbg_on ? c->dbg : nullptr, c->st, c->hp, c->geom,
+               nonfinite, s, &c->prof);
+  return rebuild_csr(c, s, false);
+}
+
+// A deferred step still pending is launched on side2, forked from `s`; the returned event
+// (nullptr if nothing was pending) must be waited on before anything reads the parameters,
+// records or culling lists.  Work on `s` that does not (sample ingest) overlaps it.
+static gc_status fork_pending(gc_cache c, cudaStream_t s, cudaEvent_t* done) {
+  *done = nullptr;
+  if (!c->pending) return GC_OK;
+  c->pending = false;
+  CK(cudaEventRecord(c->ev_fork2, s));
+  CK(cudaStreamWaitEvent(c->side2, c->ev_fork2, 0));
+  if (gc_status e = launch_tail(c, c->side2, &c->st->nonfinite)) return e;
+  CK(cudaEventRecord(c->ev_tail, c->side2));
+  *done = c->ev_tail;
+  return GC_OK;
+}
+
+// Completes a pending step on `s` (every call that reads or writes the cache state first).
+static gc_status flush_pending(gc_cache c, cudaStream_t s) {
+  cudaEvent_t ev = nullptr;
+  if (gc_status e = fork_pending(c, s, &ev)) return e;
+  if (ev) CK(cudaStreamWaitEvent(s, ev, 0));
+  return GC_OK;
 }
 
 static gc_status emit_stats(gc_cache c, gc_fit_stats* user, cudaStream_t s) {
@@ -389,8 +425,11 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
   c->fb_grid = fwdbwd_grid();
   c->q_grid = query_grid();
   CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->side2, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_fork2, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_tail, cudaEventDisableTiming));
   CK(dalloc(&c->partial, (size_t)kSlots * kPart));
   CK(cudaMemset(c->partial, 0, sizeof(double) * kSlots * kPart));
   CK(cudaDeviceSynchronize());
@@ -411,8 +450,8 @@ static void destroy_impl(gc_cache c) {
   for (auto* p : c->payloads) delete p;
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->side) cudaStreamDestroy(c->side);
-  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
-  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->side2) cudaStreamDestroy(c->side2);
+  for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_fork2, c->ev_tail}) if (e) cudaEventDestroy(e);
   delete c;
 }
 
@@ -489,9 +528,12 @@ struct Epilogue {
 
 // One optimisation step (gc_fit, and the fit half of gc_fit_query: `join`, if set, is waited
 // on before the optimizer step so that the lookups forked off beside it read pre-step
-// parameters).
+// parameters).  `tail_ev`: a pending deferred step already forked by the caller (else this
+// call forks it itself); its ingest overlaps that step.  With deferral on, this call's own
+// optimizer step is left pending.
 static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len, const float* rgb, int64_t S,
-                          gc_stream stream, gc_fit_stats* stats, cudaEvent_t join = nullptr) {
+                          gc_stream stream, gc_fit_stats* stats, cudaEvent_t join = nullptr,
+                          bool forked = false, cudaEvent_t tail_ev = nullptr) {
   if (!c) return fail(GC_ERR_ARG, "NULL handle");
   if (S < 0 || S >= ((int64_t)1 << 31)) return fail(GC_ERR_ARG, "S out of range");
   if (S > 0 && (!pos || !path_len || !rgb)) return fail(GC_ERR_ARG, "NULL sample pointer");
@@ -499,6 +541,7 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
   CK(cudaSetDevice(c->device));
   if (gc_status e = check_sticky(c)) return e;
   if (gc_status e = ensure_scratch(c, c->fit, std::max<int64_t>(S, 1), true, s)) return e;
+  if (!forked) { if (gc_status e = fork_pending(c, s, &tail_ev)) return e; }
   Scratch& F = c->fit;
   if (S > 0) {
     const bool hpos = !is_device_ptr(pos), hlen = !is_device_ptr(path_len), hrgb = !is_device_ptr(rgb);
@@ -514,6 +557,7 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
   if (S > 0) launch_keys(pos, path_len, rgb, -1, S, c->geom, b, s, &c->prof);
   launch_scan(F.cell_count, c->NC * kRep, kCH, F.tiles, F.totals, F.cell_start, nullptr, F.work, c->geom, s, &c->prof);
   if (S > 0) launch_scatter(pos, rgb, S, F.cell_start, b, s, &c->prof);
+  if (tail_ev) CK(cudaStreamWaitEvent(s, tail_ev, 0));     // the previous step is complete
   FitArgs fa;
   fa.work = F.work; fa.n_work = F.totals + 1; fa.csr_off = c->csr_off; fa.csr_idx = c->csr_idx; fa.rec = c->rec;
   fa.bin = F.bin;
@@ -533,9 +577,11 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
     launch_step_scalars(c->lvl, c->st, c->hp, c->L, c->dstats, s);
   }
   if (join) CK(cudaStreamWaitEvent(s, join, 0));
-  launch_adamw(c->G, c->P, c->M, c->V, c->grad, cull_bufs(c), c->dbg_on ? c->dbg : nullptr, c->st, c->hp, c->geom,
-               c->dstats, s, &c->prof);
-  if (gc_status e = rebuild_csr(c, s, false)) return e;
+  if (c->defer) {
+    c->pending = true;                // AdamW + culling rebuild run at the start of the next call
+  } else {
+    if (gc_status e = launch_tail(c, s, reinterpret_cast<unsigned long long*>(&c->dstats->nonfinite_grads))) return e;
+  }
   if (gc_status e = emit_stats(c, stats, s)) return e;
   CK(cudaGetLastError());
   c->last_fit_S = S;
@@ -549,7 +595,7 @@ gc_status gc_fit(gc_cache c, const float* pos, const int32_t* path_len, const fl
 
 static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_len, int level, int64_t S,
                             const float* att, const float* beta, const float* unb, float* out_rgb,
-                            gc_stream stream);
+                            gc_stream stream, bool forked = false, cudaEvent_t tail_ev = nullptr);
 
 // The frame's lookups run on the handle's side stream, forked from `stream` and joined back
 // before the optimizer step, so their ingest and evaluation overlap the fit samples' ingest
@@ -565,15 +611,20 @@ gc_status gc_fit_query(gc_cache c, const float* pos, const int32_t* path_len, co
   if (S_q == 0) return fit_impl(c, pos, path_len, rgb, S, stream, stats);
   cudaStream_t s = (cudaStream_t)stream;
   CK(cudaSetDevice(c->device));
+  cudaEvent_t tail_ev = nullptr;      // a deferred previous step overlaps both halves' ingest
+  if (gc_status e = fork_pending(c, s, &tail_ev)) return e;
   CK(cudaEventRecord(c->ev_fork, s));
   CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
   const gc_status qs = query_impl(c, qpos, qlen, qlevel, S_q, attenuation, beta, unbiased_rgb, out_rgb,
-                                  (gc_stream)c->side);
+                                  (gc_stream)c->side, true, tail_ev);
   CK(cudaEventRecord(c->ev_join, c->side));     // always joined (keeps a capture well-formed)
-  if (qs != GC_OK) { CK(cudaStreamWaitEvent(s, c->ev_join, 0)); return qs; }
-  return fit_impl(c, pos, path_len, rgb, S, stream, stats, c->ev_join);
+  if (qs != GC_OK) {
+    CK(cudaStreamWaitEvent(s, c->ev_join, 0));
+    if (tail_ev) CK(cudaStreamWaitEvent(s, tail_ev, 0));
+    return qs;
+  }
+  return fit_impl(c, pos, path_len, rgb, S, stream, stats, c->ev_join, true, tail_ev);
 }
-
 
 gc_status gc_query(gc_cache c, const float* pos, const int32_t* path_len, int level, int64_t S,
                    float* out_rgb, gc_stream stream) {
@@ -588,7 +639,7 @@ gc_status gc_query_radiance(gc_cache c, const float* pos, const int32_t* path_le
 
 static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_len, int level, int64_t S,
                             const float* att, const float* beta, const float* unb, float* out_rgb,
-                            gc_stream stream) {
+                            gc_stream stream, bool forked, cudaEvent_t tail_ev) {
   if (!c) return fail(GC_ERR_ARG, "NULL handle");
   if (S < 0 || S >= ((int64_t)1 << 31)) return fail(GC_ERR_ARG, "S out of range");
   if (S > 0 && (!pos || !out_rgb)) return fail(GC_ERR_ARG, "NULL pointer");
@@ -598,6 +649,7 @@ static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_le
   CK(cudaSetDevice(c->device));
   if (gc_status e = check_sticky(c)) return e;
   if (gc_status e = ensure_scratch(c, c->qry, S, false, s)) return e;
+  if (!forked) { if (gc_status e = fork_pending(c, s, &tail_ev)) return e; }
   Scratch& Q = c->qry;
   const bool hpos = !is_device_ptr(pos), hlen = path_len && !is_device_ptr(path_len), hout = !is_device_ptr(out_rgb);
   if (hpos || hlen || hout) {
@@ -619,6 +671,7 @@ static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_le
   qa.att = ep.dev[0]; qa.beta = ep.dev[1]; qa.unb = ep.dev[2];
   const float tau = c->hp.cutoff_sigma;
   qa.tau2 = tau * tau;
+  if (tail_ev) CK(cudaStreamWaitEvent(s, tail_ev, 0));     // a deferred step is complete
   launch_query(qa, c->q_grid, s, &c->prof);
   if (hout) CK(cudaMemcpyAsync(out_rgb, dout, sizeof(float) * 3 * S, cudaMemcpyDeviceToHost, s));
   if (gc_status e = ep.release(s)) return e;
@@ -655,12 +708,28 @@ static gc_status level_io(gc_cache c, int level, gc_level_params* p, bool out, c
 
 gc_status gc_params(gc_cache c, int level, gc_level_params* dst, gc_stream stream) {
   if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  CK(cudaSetDevice(c->device));
+  if (gc_status e = flush_pending(c, (cudaStream_t)stream)) return e;
   return level_io(c, level, dst, true, c->P, (cudaStream_t)stream);
+}
+
+gc_status gc_set_deferred_step(gc_cache c, int enable) {
+  if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  c->defer = enable != 0;
+  return GC_OK;
+}
+
+gc_status gc_flush(gc_cache c, gc_stream stream) {
+  if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  CK(cudaSetDevice(c->device));
+  return flush_pending(c, (cudaStream_t)stream);
 }
 
 gc_status gc_set_params(gc_cache c, int level, const gc_level_params* src, int reset_adam, gc_stream stream) {
   if (!c) return fail(GC_ERR_ARG, "NULL handle");
   cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->device));
+  if (gc_status e = flush_pending(c, s)) return e;
   gc_level_params tmp = *src;
   if (gc_status e = level_io(c, level, &tmp, false, nullptr, s)) return e;
   if (reset_adam) {
@@ -680,6 +749,7 @@ gc_status gc_set_params(gc_cache c, int level, const gc_level_params* src, int r
 gc_status gc_reset_schedule(gc_cache c) {
   if (!c) return fail(GC_ERR_ARG, "NULL handle");
   CK(cudaSetDevice(c->device));
+  if (gc_status e = flush_pending(c, 0)) return e;
   CK(cudaMemsetAsync(&c->st->t, 0, sizeof(long long), 0));
   CK(cudaDeviceSynchronize());
   return GC_OK;
@@ -735,6 +805,8 @@ gc_status gc_debug_enable_grads(gc_cache c, int enable) {
 gc_status gc_debug_grads(gc_cache c, int level, gc_level_params* dst, gc_stream stream) {
   if (!c) return fail(GC_ERR_ARG, "NULL handle");
   if (!c->dbg) return fail(GC_ERR_STATE, "gradient recording not enabled (gc_debug_enable_grads)");
+  CK(cudaSetDevice(c->device));
+  if (gc_status e = flush_pending(c, (cudaStream_t)stream)) return e;
   return level_io(c, level, dst, true, c->dbg, (cudaStream_t)stream);
 }
 
@@ -743,6 +815,7 @@ gc_status gc_debug_cull(gc_cache c, int level, int32_t* offsets, int32_t* idx, i
   if (!c || level < 0 || level >= c->L || !offsets || !n) return fail(GC_ERR_ARG, "bad arguments");
   cudaStream_t s = (cudaStream_t)stream;
   CK(cudaSetDevice(c->device));
+  if (gc_status e = flush_pending(c, s)) return e;
   const int64_t c0 = c->geom.coff[level], nc = c->geom.coff[level + 1] - c0;
   std::vector<uint32_t> off((size_t)nc + 1);
   CK(cudaMemcpyAsync(off.data(), c->csr_off + c0, sizeof(uint32_t) * (nc + 1), cudaMemcpyDeviceToHost, s));

@@ -40,7 +40,7 @@ struct DevState {
   float inv3k[kMaxL];                // 1 / (3 k_l) (0 when the level is skipped)
   int active[kMaxL];                 // level takes a step this call
   int stepped;                       // this call stepped (>= 1 valid sample)
-  unsigned long long nonfinite;      // non-finite gradient elements skipped (this call)
+  unsigned long long nonfinite;      // non-finite gradient elements skipped by a deferred step
   unsigned int csr_total;            // culling-list entries of the current CSR
   unsigned int csr_overflow;         // sticky: a rebuild exceeded the list capacity
   unsigned int ovf_next;             // bump allocator of the wide-range rank slots (per rebuild)

@@ -137,9 +137,11 @@ void launch_stats(double* partial, const LevelGeom& g, int64_t S, LvlStats* lvl,
                   const gc_hparams& hp, int L, gc_fit_stats* dev_stats, cudaStream_t s, Profiler* prof);
 void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp, int L,
                          gc_fit_stats* dev_stats, cudaStream_t s);
+// nonfinite: where the count of skipped non-finite gradient elements is added (the call's
+// gc_fit_stats, or DevState::nonfinite when the step is deferred into the next call)
 void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, CullBufs cb, float* dbg_grad,
-                  DevState* st, const gc_hparams& hp,
-                  const LevelGeom& g, gc_fit_stats* dev_stats, cudaStream_t s, Profiler* prof);
+                  DevState* st, const gc_hparams& hp, const LevelGeom& g, unsigned long long* nonfinite,
+                  cudaStream_t s, Profiler* prof);
 
 // create.cu
 void launch_gather_init(int64_t N0, const float* pos, const float* rgb, const float* log_scale,

@@ -74,13 +74,13 @@ __device__ __forceinline__ void step_scalars_warp(const LvlStats* lvl, DevState*
   }
   if (lane == 0) {
     st->stepped = stepped;
-    st->nonfinite = 0ull;
     st->t = t;
     out->n_in = (int64_t)lvl->n_in;
     out->n_valid = (int64_t)lvl->n_valid;
     out->n_dropped = (int64_t)(lvl->n_in - lvl->n_valid);
     out->step = stepped ? t : 0;
-    out->nonfinite_grads = 0;
+    out->nonfinite_grads = (int64_t)st->nonfinite;   // a deferred previous step's count, else 0
+    st->nonfinite = 0ull;
     out->n_pairs = (int64_t)lvl->n_pairs;
     out->n_candidates = (int64_t)lvl->n_cand;
   }

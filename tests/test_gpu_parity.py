@@ -580,3 +580,57 @@ def test_fit_query_graph_replay_matches_eager(gsc):
         check_forward(out.cpu().numpy(), yo, P, c2.goff, xqh, lv, what="replay")
     # gradient atomics are unordered: the two trajectories agree to fp32 rounding
     np.testing.assert_allclose(rows(c1), rows(c2), rtol=1e-5, atol=1e-6)
+
+
+# ------------------------------------------------------- deferred optimizer step
+def test_deferred_step_same_results(gsc):
+    """gc_set_deferred_step: every lookup, statistic and the final parameters equal the
+    undeferred run (the pending step completes before anything reads the cache)."""
+    c1, _, _ = make_cfg1(gsc)
+    c2, _, _ = make_cfg1(gsc)
+    c2.set_deferred_step(True)
+    for frame in range(4):
+        x, ln, rgb = workload.fit_batch(1, frame=frame, S=120_000)
+        xq, lq = workload.query_batch(1, frame=frame, S=40_000)
+        y1, s1 = c1.fit_query(cuda(x), cuda(ln), cuda(rgb), cuda(xq), cuda(lq))
+        y2, s2 = c2.fit_query(cuda(x), cuda(ln), cuda(rgb), cuda(xq), cuda(lq))
+        torch.cuda.synchronize()
+        np.testing.assert_allclose(y2.cpu().numpy(), y1.cpu().numpy(), rtol=2e-5, atol=1e-7)
+        assert list(s2.count[:3]) == list(s1.count[:3]) and s2.step == s1.step == frame + 1
+        np.testing.assert_allclose(list(s2.loss[:3]), list(s1.loss[:3]), rtol=2e-5)
+        if frame == 1:                          # a plain gc_fit / gc_query in between
+            q1 = c1.query(cuda(xq), cuda(lq))
+            q2 = c2.query(cuda(xq), cuda(lq))    # flushes the pending step first
+            torch.cuda.synchronize()
+            np.testing.assert_allclose(q2.cpu().numpy(), q1.cpu().numpy(), rtol=2e-5, atol=1e-7)
+    np.testing.assert_allclose(rows(c2), rows(c1), rtol=1e-5, atol=1e-6)   # gc_params flushes
+    # the culling lists after the flushed step are the oracle's for those parameters
+    _check_csr(c2, rows(c2))
+
+
+def test_deferred_step_graph_replay(gsc):
+    """A captured deferred gc_fit_query (it contains the previous frame's step) replays in a
+    steady state; gc_flush completes the last one."""
+    c1, _, _ = make_cfg1(gsc)
+    c2, _, _ = make_cfg1(gsc)
+    xh, lh, rh = workload.fit_batch(1, S=50_000)
+    xqh, lqh = workload.query_batch(1, S=20_000)
+    x, ln, rgb, xq, lq = map(cuda, (xh, lh, rh, xqh, lqh))
+    c2.set_deferred_step(True)
+    c2.reserve(50_000, 20_000)
+    out = torch.empty((20_000, 3), device="cuda")
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        c2.fit_query(x, ln, rgb, xq, lq, out=out, stream=st)       # step 1 (left pending)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        c2.fit_query(x, ln, rgb, xq, lq, out=out, stream=st)
+    c1.fit_query(x, ln, rgb, xq, lq)
+    for _ in range(3):
+        c1.fit_query(x, ln, rgb, xq, lq)
+        with torch.cuda.stream(st):             # replays and the flush on one stream
+            g.replay()
+    c2.flush(st)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(rows(c2), rows(c1), rtol=1e-5, atol=1e-6)
