@@ -424,6 +424,7 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
 
   c->fb_grid = fwdbwd_grid();
   c->q_grid = query_grid();
+  // (stream priorities measured: favouring either half was slower than equal priority)
   CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->side2, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
