@@ -109,6 +109,7 @@ struct gc_cache_s {
   bool defer = false, pending = false;
   cudaStream_t side2 = nullptr;
   cudaEvent_t ev_fork2 = nullptr, ev_tail = nullptr;
+  cudaEvent_t ev_staged = nullptr;   // gc_fit_query: lookups' host inputs uploaded (fit uploads after)
 };
 
 // ------------------------------------------------------------------------- helpers
@@ -431,6 +432,7 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
   CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_fork2, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_tail, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_staged, cudaEventDisableTiming));
   CK(dalloc(&c->partial, (size_t)kSlots * kPart));
   CK(cudaMemset(c->partial, 0, sizeof(double) * kSlots * kPart));
   CK(cudaDeviceSynchronize());
@@ -452,7 +454,7 @@ static void destroy_impl(gc_cache c) {
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->side2) cudaStreamDestroy(c->side2);
-  for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_fork2, c->ev_tail}) if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_fork2, c->ev_tail, c->ev_staged}) if (e) cudaEventDestroy(e);
   delete c;
 }
 
@@ -549,6 +551,9 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
     if (hpos || hlen || hrgb) {
       if (capturing(s) && (!F.in_pos || !F.in_len || !F.in_rgb)) return fail(GC_ERR_STATE, "staging not reserved before capture");
       if (gc_status e = ensure_staging(F, hpos, hlen, hrgb, false)) return e;
+      // gc_fit_query: the lookups' inputs go over PCIe first, so their half computes (and its
+      // outputs stream back) while the fit samples upload
+      if (forked) CK(cudaStreamWaitEvent(s, c->ev_staged, 0));
       if (hpos) { CK(cudaMemcpyAsync(F.in_pos, pos, sizeof(float) * 3 * S, cudaMemcpyHostToDevice, s)); pos = F.in_pos; }
       if (hlen) { CK(cudaMemcpyAsync(F.in_len, path_len, sizeof(int32_t) * S, cudaMemcpyHostToDevice, s)); path_len = F.in_len; }
       if (hrgb) { CK(cudaMemcpyAsync(F.in_rgb, rgb, sizeof(float) * 3 * S, cudaMemcpyHostToDevice, s)); rgb = F.in_rgb; }
@@ -659,6 +664,7 @@ static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_le
     if (hpos) { CK(cudaMemcpyAsync(Q.in_pos, pos, sizeof(float) * 3 * S, cudaMemcpyHostToDevice, s)); pos = Q.in_pos; }
     if (hlen) { CK(cudaMemcpyAsync(Q.in_len, path_len, sizeof(int32_t) * S, cudaMemcpyHostToDevice, s)); path_len = Q.in_len; }
   }
+  if (forked) CK(cudaEventRecord(c->ev_staged, s));
   float* dout = hout ? Q.out : out_rgb;
   IngestBufs b{Q.key, Q.rank, Q.cell_count, Q.bin, c->NC};
   launch_keys_query(pos, path_len, path_len ? -1 : level, S, c->geom, b, dout, s, &c->prof);
