@@ -212,85 +212,87 @@ __device__ __forceinline__ void eval_any(const ChunkSmem& w, bool iso, bool two,
   }
 }
 
-// Gradient terms of pairs [p0, p1) of the staged chunk (lane = pair): 12 coefficient
-// gradients (C5), a <= 2-level segmented shuffle scan over each Gaussian's run of pairs,
-// then red.global.add.v4.f32 from every 4th lane of a run counted from its end.
+// Gradient terms of pairs [p0, p1) of the staged chunk: 12 coefficient gradients (C5).  The
+// candidate-major pair list is cut into 32 contiguous slices, one per lane; a lane walks its
+// slice accumulating the current Gaussian's terms in registers and issues
+// red.global.add.v4.f32 whenever the Gaussian changes and at the end -- so every run of a
+// Gaussian's pairs costs one reduction per lane piece, with no shuffles at all.
 // kLite (isotropic chunk, scale group frozen with lr 0, no gradient export): the 6 dA terms
 // only feed dL/ds, whose update is frozen, and dL/dq, which is exactly 0 for isotropic
 // Gaussians -- so only d mu and d v are accumulated (dead work skipped, not approximated).
 template <bool kLite>
+__device__ __forceinline__ void flush_grad(float* __restrict__ grad, int gid, const float (&acc)[kLite ? 6 : 12]) {
+  float* gp = grad + 12 * (int64_t)gid;
+  if constexpr (kLite) {
+    red_add_v4(gp, acc[0], acc[1], acc[2], 0.f);
+    red_add_v4(gp + 8, 0.f, acc[3], acc[4], acc[5]);
+  } else {
+    red_add_v4(gp, acc[0], acc[1], acc[2], acc[3]);
+    red_add_v4(gp + 4, acc[4], acc[5], acc[6], acc[7]);
+    red_add_v4(gp + 8, acc[8], acc[9], acc[10], acc[11]);
+  }
+}
+
+template <bool kLite>
 __device__ __forceinline__ void chunk_pairs_bwd_impl(const WarpSmem& w, int p0, int p1, float* __restrict__ grad,
                                                      int lane, bool iso) {
   constexpr int NV = kLite ? 6 : 12;
-  for (int pb = p0; pb < p1; pb += 32) {
-    const int p = pb + lane;
-    const bool valid = p < p1;
-    int k = 32 + lane;                 // idle lanes form their own segments
-    float v[NV];
+  const int n = p1 - p0;
+  const int pa = p0 + ((n * lane) >> 5), pe_ = p0 + ((n * (lane + 1)) >> 5);
+  float acc[NV];
 #pragma unroll
-    for (int q = 0; q < NV; ++q) v[q] = 0.f;
-    int gid = 0;
-    if (valid) {
-      const uint32_t key = w.pkey[p];
-      const float e = w.pe[p];
-      k = key >> 6;
-      const int s = key & 63;
-      const float4 mu = w.r3[k];
+  for (int q = 0; q < NV; ++q) acc[q] = 0.f;
+  int kcur = -1, gid = 0;
+  float4 mu = make_float4(0.f, 0.f, 0.f, 0.f);
+  float u2 = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f;
+  Cand g{};
+  for (int p = pa; p < pe_; ++p) {
+    const uint32_t key = w.pkey[p];
+    const float e = w.pe[p];
+    const int k = key >> 6, s = key & 63;
+    if (k != kcur) {
+      if (kcur >= 0) {
+        flush_grad<kLite>(grad, gid, acc);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) acc[q] = 0.f;
+      }
+      kcur = k;
+      mu = w.r3[k];
       gid = __float_as_int(mu.w);
-      const float4 sx = w.sxg[s];
-      const float2 sg = w.sg[s];
-      const float dx = sx.x - mu.x, dy = sx.y - mu.y, dz = sx.z - mu.z;
-      float tx, ty, tz, v0, v1, v2;
-      if (iso) {                                                     // t = A d = u^2 d
-        const float u2 = w.r2[k].x;
+      if (iso) {
         const float4 f = w.r1[k];
-        tx = u2 * dx; ty = u2 * dy; tz = u2 * dz;
-        v0 = f.y; v1 = f.z; v2 = f.w;
-      } else {                                                       // t = A d = U^T w
-        const Cand g = cand_from(w, k);
-        float w0, w1, w2;
-        cand_q(g, sx.x, sx.y, sx.z, w0, w1, w2);
-        tx = g.u00 * w0;
-        ty = fmaf(g.u11, w1, g.u01 * w0);
-        tz = fmaf(g.u22, w2, fmaf(g.u12, w1, g.u02 * w0));
+        u2 = w.r2[k].x; v0 = f.y; v1 = f.z; v2 = f.w;
+      } else {
+        g = cand_from(w, k);
         v0 = g.v0; v1 = g.v1; v2 = g.v2;
       }
-      const float he = (sx.w * v0 + sg.x * v1 + sg.y * v2) * e;
-      v[0] = he * tx; v[1] = he * ty; v[2] = he * tz;                 // d mu
-      if constexpr (kLite) {
-        v[3] = sx.w * e; v[4] = sg.x * e; v[5] = sg.y * e;            // d v
-      } else {
-        const float kk = -0.5f * he;
-        const float kx = kk * dx, ky = kk * dy, kz = kk * dz;
-        v[3] = kx * dx; v[4] = ky * dy; v[5] = kz * dz;               // dA00 dA11 dA22
-        v[6] = kx * dy; v[7] = kx * dz; v[8] = ky * dz;               // dA01 dA02 dA12
-        v[9] = sx.w * e; v[10] = sg.x * e; v[11] = sg.y * e;          // d v
-      }
     }
-    const unsigned peers = __match_any_sync(0xffffffffu, k);
-    const int head = __ffs(peers) - 1, tail = 31 - __clz(peers);
-#pragma unroll
-    for (int o = 1; o <= 2; o <<= 1) {
-      const bool need = lane - o >= head;
-      if (!__any_sync(0xffffffffu, need)) break;
-#pragma unroll
-      for (int q = 0; q < NV; ++q) {
-        const float t = __shfl_up_sync(0xffffffffu, v[q], o);
-        if (need) v[q] += t;
-      }
+    const float4 sx = w.sxg[s];
+    const float2 sg = w.sg[s];
+    const float dx = sx.x - mu.x, dy = sx.y - mu.y, dz = sx.z - mu.z;
+    float tx, ty, tz;
+    if (iso) {                                                     // t = A d = u^2 d
+      tx = u2 * dx; ty = u2 * dy; tz = u2 * dz;
+    } else {                                                       // t = A d = U^T w
+      float w0, w1, w2;
+      cand_q(g, sx.x, sx.y, sx.z, w0, w1, w2);
+      tx = g.u00 * w0;
+      ty = fmaf(g.u11, w1, g.u01 * w0);
+      tz = fmaf(g.u22, w2, fmaf(g.u12, w1, g.u02 * w0));
     }
-    if (valid && ((tail - lane) & 3) == 0) {
-      float* gp = grad + 12 * (int64_t)gid;
-      if constexpr (kLite) {
-        red_add_v4(gp, v[0], v[1], v[2], 0.f);
-        red_add_v4(gp + 8, 0.f, v[3], v[4], v[5]);
-      } else {
-        red_add_v4(gp, v[0], v[1], v[2], v[3]);
-        red_add_v4(gp + 4, v[4], v[5], v[6], v[7]);
-        red_add_v4(gp + 8, v[8], v[9], v[10], v[11]);
-      }
+    const float he = (sx.w * v0 + sg.x * v1 + sg.y * v2) * e;
+    acc[0] = fmaf(he, tx, acc[0]); acc[1] = fmaf(he, ty, acc[1]); acc[2] = fmaf(he, tz, acc[2]);   // d mu
+    if constexpr (kLite) {
+      acc[3] = fmaf(sx.w, e, acc[3]); acc[4] = fmaf(sg.x, e, acc[4]); acc[5] = fmaf(sg.y, e, acc[5]);   // d v
+    } else {
+      const float kk = -0.5f * he;
+      const float kx = kk * dx, ky = kk * dy, kz = kk * dz;
+      acc[3] = fmaf(kx, dx, acc[3]); acc[4] = fmaf(ky, dy, acc[4]); acc[5] = fmaf(kz, dz, acc[5]);   // dA00 dA11 dA22
+      acc[6] = fmaf(kx, dy, acc[6]); acc[7] = fmaf(kx, dz, acc[7]); acc[8] = fmaf(ky, dz, acc[8]);   // dA01 dA02 dA12
+      acc[9] = fmaf(sx.w, e, acc[9]); acc[10] = fmaf(sg.x, e, acc[10]); acc[11] = fmaf(sg.y, e, acc[11]);   // d v
     }
   }
+  if (kcur >= 0) flush_grad<kLite>(grad, gid, acc);
   __syncwarp();
 }
 
