@@ -21,8 +21,8 @@
 namespace gsc {
 
 constexpr int kWarps = 8;                                 // warps per CTA
-constexpr int kPairCap = 512;                             // recorded (sample, Gaussian) pairs per warp
-constexpr int kMaxChunks = 64;                            // recorded chunks per work item (C <= 2048)
+constexpr int kPairCap = 512;                             // pair batch of the dense fallback path
+constexpr int kMaskChunks = 12;                           // chunks whose inside masks are kept (C <= 384)
 constexpr float kNegHalfLog2e = -0.72134752044448170f;    // -0.5 * log2(e)
 static_assert(kCH == 64, "two samples per lane");
 
@@ -39,9 +39,14 @@ struct ChunkSmem {
 struct WarpSmem : ChunkSmem {
   float4 sxg[64];                  // sample x', y', z', g0
   float2 sg[64];                   // sample g1, g2
-  uint16_t pkey[kPairCap];         // (candidate-in-chunk << 6) | sample, chunk- then candidate-major
-  float pe[kPairCap];              // e = exp(-Q/2) of the pair, as pass 1 computed it
-  uint16_t cend[kMaxChunks];       // end offset of every chunk's pairs
+  union {
+    uint2 mask[kMaskChunks][32];   // pass 1 -> 2: which samples (a | b<<32) lie inside candidate k of chunk c
+    struct {                       // dense fallback: a batch of pairs, candidate-major
+      uint16_t pkey[kPairCap];     // (candidate-in-chunk << 6) | sample
+      float pe[kPairCap];          // e = exp(-Q/2) of the pair
+    } list;
+  } u;
+  int offs[32];                    // pass 2: first pair of candidate k in the chunk's pair order
 };
 
 struct Cand { float u00, u01, u02, u11, u12, u22, nc0, nc1, nc2, v0, v1, v2; };
@@ -105,59 +110,39 @@ __device__ __forceinline__ float iso_s(const float (&x)[3], const float4& c) {
 
 // Isotropic chunk: s = |x' - m|^2 <= tau^2/u^2, e = 2^{-0.5 log2e u^2 s} (7 ops per test).
 // Branch-free: e is computed for every lane and zeroed outside (MUFU has the slack; a
-// divergent inside block costs more issue slots than it saves).  Record positions are
-// clamped to cap - 1: an overflowing item is re-derived by the caller, so the clobbered
-// last slot is never read.  kTwo = false: the item has <= 32 samples, sample b is skipped.
-template <bool kRecord, bool kTwo>
+// divergent inside block costs more issue slots than it saves).  kMask (pass 1 of a fit):
+// lane k also keeps candidate k's ballots (which samples it covers) in cm -- three
+// instructions per candidate instead of appending a pair list.  kTwo = false: the item has
+// <= 32 samples, sample b is skipped.
+template <bool kMask, bool kTwo>
 __device__ __forceinline__ void eval_chunk_iso(const ChunkSmem& w, int kc, const float (&xa)[3], const float (&xb)[3],
-                                               float (&ya)[3], float (&yb)[3], uint16_t* pkey, float* pe,
-                                               int& pbase, int cap, int lane) {
-  const uint32_t lt = (1u << lane) - 1u;
+                                               float (&ya)[3], float (&yb)[3], uint2& cm, int lane) {
 #pragma unroll 2
   for (int k = 0; k < kc; ++k) {
     const float4 c = w.r0[k], f = w.r1[k];
     const float sa = iso_s(xa, c), sb = kTwo ? iso_s(xb, c) : 0.f;
     const bool ina = sa <= c.w, inb = kTwo && sb <= c.w;
-    if (!kRecord) {
-      const float xa_ = ex2_approx(f.x * sa);
-      const float ea = ina ? xa_ : 0.f;
-      ya[0] = fmaf(f.y, ea, ya[0]); ya[1] = fmaf(f.z, ea, ya[1]); ya[2] = fmaf(f.w, ea, ya[2]);
-      if constexpr (kTwo) {
-        const float xb_ = ex2_approx(f.x * sb);
-        const float eb = inb ? xb_ : 0.f;
-        yb[0] = fmaf(f.y, eb, yb[0]); yb[1] = fmaf(f.z, eb, yb[1]); yb[2] = fmaf(f.w, eb, yb[2]);
-      }
-      continue;
+    const float xa_ = ex2_approx(f.x * sa);
+    const float ea = ina ? xa_ : 0.f;
+    ya[0] = fmaf(f.y, ea, ya[0]); ya[1] = fmaf(f.z, ea, ya[1]); ya[2] = fmaf(f.w, ea, ya[2]);
+    if constexpr (kTwo) {
+      const float xb_ = ex2_approx(f.x * sb);
+      const float eb = inb ? xb_ : 0.f;
+      yb[0] = fmaf(f.y, eb, yb[0]); yb[1] = fmaf(f.z, eb, yb[1]); yb[2] = fmaf(f.w, eb, yb[2]);
     }
-    const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = kTwo ? __ballot_sync(0xffffffffu, inb) : 0u;
-    if (ma | mb) {
-      const float xa_ = ex2_approx(f.x * sa);
-      const float ea = ina ? xa_ : 0.f;
-      ya[0] = fmaf(f.y, ea, ya[0]); ya[1] = fmaf(f.z, ea, ya[1]); ya[2] = fmaf(f.w, ea, ya[2]);
-      const int na = __popc(ma);
-      const int pa = min(pbase + __popc(ma & lt), cap - 1);
-      if (ina) { pkey[pa] = (uint16_t)((k << 6) | lane); pe[pa] = ea; }
-      if constexpr (kTwo) {
-        const float xb_ = ex2_approx(f.x * sb);
-        const float eb = inb ? xb_ : 0.f;
-        yb[0] = fmaf(f.y, eb, yb[0]); yb[1] = fmaf(f.z, eb, yb[1]); yb[2] = fmaf(f.w, eb, yb[2]);
-        const int pb = min(pbase + na + __popc(mb & lt), cap - 1);
-        if (inb) { pkey[pb] = (uint16_t)((k << 6) | (lane + 32)); pe[pb] = eb; }
-      }
-      pbase += na + __popc(mb);
+    if constexpr (kMask) {
+      const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = kTwo ? __ballot_sync(0xffffffffu, inb) : 0u;
+      if (lane == k) cm = make_uint2(ma, mb);
     }
   }
   __syncwarp();
 }
 
 // Two samples per lane (a = lane, b = lane + 32; inactive samples carry x' = NaN, never
-// inside).  Accumulates yhat and, if kRecord, appends every inside pair at pbase + its rank
-// (candidate-major; sample a's before sample b's), up to `cap`; pbase advances regardless.
-template <bool kRecord, bool kTwo>
+// inside).  Accumulates yhat and, if kMask, candidate k's ballots into lane k's cm.
+template <bool kMask, bool kTwo>
 __device__ __forceinline__ void eval_chunk(const ChunkSmem& w, int kc, const float (&xa)[3], const float (&xb)[3],
-                                           float tau2, float (&ya)[3], float (&yb)[3],
-                                           uint16_t* pkey, float* pe, int& pbase, int cap, int lane) {
-  const uint32_t lt = (1u << lane) - 1u;
+                                           float tau2, float (&ya)[3], float (&yb)[3], uint2& cm, int lane) {
 #pragma unroll 2
   for (int k = 0; k < kc; ++k) {
     const Cand g = cand_from(w, k);
@@ -165,50 +150,34 @@ __device__ __forceinline__ void eval_chunk(const ChunkSmem& w, int kc, const flo
     const float Qa = cand_q(g, xa[0], xa[1], xa[2], w0, w1, w2);
     const float Qb = kTwo ? cand_q(g, xb[0], xb[1], xb[2], w0, w1, w2) : 0.f;
     const bool ina = Qa <= tau2, inb = kTwo && Qb <= tau2;
-    if (!kRecord) {
-      const float xa_ = ex2_approx(Qa * kNegHalfLog2e);
-      const float ea = ina ? xa_ : 0.f;
-      ya[0] = fmaf(g.v0, ea, ya[0]); ya[1] = fmaf(g.v1, ea, ya[1]); ya[2] = fmaf(g.v2, ea, ya[2]);
-      if constexpr (kTwo) {
-        const float xb_ = ex2_approx(Qb * kNegHalfLog2e);
-        const float eb = inb ? xb_ : 0.f;
-        yb[0] = fmaf(g.v0, eb, yb[0]); yb[1] = fmaf(g.v1, eb, yb[1]); yb[2] = fmaf(g.v2, eb, yb[2]);
-      }
-      continue;
+    const float xa_ = ex2_approx(Qa * kNegHalfLog2e);
+    const float ea = ina ? xa_ : 0.f;
+    ya[0] = fmaf(g.v0, ea, ya[0]); ya[1] = fmaf(g.v1, ea, ya[1]); ya[2] = fmaf(g.v2, ea, ya[2]);
+    if constexpr (kTwo) {
+      const float xb_ = ex2_approx(Qb * kNegHalfLog2e);
+      const float eb = inb ? xb_ : 0.f;
+      yb[0] = fmaf(g.v0, eb, yb[0]); yb[1] = fmaf(g.v1, eb, yb[1]); yb[2] = fmaf(g.v2, eb, yb[2]);
     }
-    const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = kTwo ? __ballot_sync(0xffffffffu, inb) : 0u;
-    if (ma | mb) {
-      const float xa_ = ex2_approx(Qa * kNegHalfLog2e);
-      const float ea = ina ? xa_ : 0.f;
-      ya[0] = fmaf(g.v0, ea, ya[0]); ya[1] = fmaf(g.v1, ea, ya[1]); ya[2] = fmaf(g.v2, ea, ya[2]);
-      const int na = __popc(ma);
-      const int pa = min(pbase + __popc(ma & lt), cap - 1);
-      if (ina) { pkey[pa] = (uint16_t)((k << 6) | lane); pe[pa] = ea; }
-      if constexpr (kTwo) {
-        const float xb_ = ex2_approx(Qb * kNegHalfLog2e);
-        const float eb = inb ? xb_ : 0.f;
-        yb[0] = fmaf(g.v0, eb, yb[0]); yb[1] = fmaf(g.v1, eb, yb[1]); yb[2] = fmaf(g.v2, eb, yb[2]);
-        const int pb = min(pbase + na + __popc(mb & lt), cap - 1);
-        if (inb) { pkey[pb] = (uint16_t)((k << 6) | (lane + 32)); pe[pb] = eb; }
-      }
-      pbase += na + __popc(mb);
+    if constexpr (kMask) {
+      const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = kTwo ? __ballot_sync(0xffffffffu, inb) : 0u;
+      if (lane == k) cm = make_uint2(ma, mb);
     }
   }
   __syncwarp();
 }
 
-// One chunk of pass 1 (kRecord) or of a lookup: the isotropic or general evaluator, with
+// One chunk of pass 1 (kMask) or of a lookup: the isotropic or general evaluator, with
 // both samples per lane only when the item has more than 32.
-template <bool kRecord>
+template <bool kMask>
 __device__ __forceinline__ void eval_any(const ChunkSmem& w, bool iso, bool two, int kc, const float (&xa)[3],
                                          const float (&xb)[3], float tau2, float (&ya)[3], float (&yb)[3],
-                                         uint16_t* pkey, float* pe, int& pbase, int cap, int lane) {
+                                         uint2& cm, int lane) {
   if (iso) {
-    if (two) eval_chunk_iso<kRecord, true>(w, kc, xa, xb, ya, yb, pkey, pe, pbase, cap, lane);
-    else eval_chunk_iso<kRecord, false>(w, kc, xa, xb, ya, yb, pkey, pe, pbase, cap, lane);
+    if (two) eval_chunk_iso<kMask, true>(w, kc, xa, xb, ya, yb, cm, lane);
+    else eval_chunk_iso<kMask, false>(w, kc, xa, xb, ya, yb, cm, lane);
   } else {
-    if (two) eval_chunk<kRecord, true>(w, kc, xa, xb, tau2, ya, yb, pkey, pe, pbase, cap, lane);
-    else eval_chunk<kRecord, false>(w, kc, xa, xb, tau2, ya, yb, pkey, pe, pbase, cap, lane);
+    if (two) eval_chunk<kMask, true>(w, kc, xa, xb, tau2, ya, yb, cm, lane);
+    else eval_chunk<kMask, false>(w, kc, xa, xb, tau2, ya, yb, cm, lane);
   }
 }
 
@@ -247,8 +216,8 @@ __device__ __forceinline__ void chunk_pairs_bwd_impl(const WarpSmem& w, int p0, 
   float u2 = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f;
   Cand g{};
   for (int p = pa; p < pe_; ++p) {
-    const uint32_t key = w.pkey[p];
-    const float e = w.pe[p];
+    const uint32_t key = w.u.list.pkey[p];
+    const float e = w.u.list.pe[p];
     const int k = key >> 6, s = key & 63;
     if (k != kcur) {
       if (kcur >= 0) {
@@ -300,6 +269,98 @@ __device__ __forceinline__ void chunk_pairs_bwd(const WarpSmem& w, int p0, int p
                                                 int lane, bool iso, bool lite_ok) {
   if (iso && lite_ok) chunk_pairs_bwd_impl<true>(w, p0, p1, grad, lane, true);
   else chunk_pairs_bwd_impl<false>(w, p0, p1, grad, lane, iso);
+}
+
+// Position of the set bit of rank r (0-based) in x (binary search on popcounts).
+__device__ __forceinline__ int select_bit(uint32_t x, int r) {
+  int pos = 0;
+#pragma unroll
+  for (int wd = 16; wd; wd >>= 1) {
+    const int c = __popc(x & ((1u << wd) - 1u));
+    if (c <= r) { r -= c; x >>= wd; pos += wd; }
+  }
+  return pos;
+}
+
+// Backward of one staged chunk from pass 1's inside masks: the chunk's pairs in candidate-major
+// order (candidate k's samples a then b, ascending) are cut into 32 contiguous slices, one per
+// lane; a lane finds its first pair by a binary search over the candidates' pair offsets and a
+// select on the mask, then walks on bit by bit, recomputing e = exp(-Q/2) exactly as pass 1
+// did, accumulating the current Gaussian's coefficient gradients in registers and issuing
+// red.global.add.v4.f32 whenever the Gaussian changes and at the end.
+template <bool kLite>
+__device__ __forceinline__ void chunk_bwd_masks_impl(const WarpSmem& w, const uint2* __restrict__ mask, int P,
+                                                     float tau2, float* __restrict__ grad, int lane, bool iso) {
+  constexpr int NV = kLite ? 6 : 12;
+  const int pa = (P * lane) >> 5, pend = (P * (lane + 1)) >> 5;
+  if (pa >= pend) return;
+  int k = 0;
+#pragma unroll
+  for (int st = 16; st; st >>= 1)
+    if (w.offs[k + st] <= pa) k += st;
+  uint2 mk = mask[k];
+  uint64_t m = ((uint64_t)mk.y << 32) | mk.x;
+  {                                            // drop the candidate's first (pa - offs[k]) pairs
+    const int r = pa - w.offs[k], pl = __popc(mk.x);
+    if (r < pl) m &= ~(uint64_t)((1u << select_bit(mk.x, r)) - 1u);
+    else m = (uint64_t)(mk.y & ~((1u << select_bit(mk.y, r - pl)) - 1u)) << 32;
+  }
+  float acc[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) acc[q] = 0.f;
+  int kcur = -1, gid = 0;
+  float4 mu = make_float4(0.f, 0.f, 0.f, 0.f), c0 = mu;
+  float u2 = 0.f, gx = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f;
+  Cand g{};
+  for (int p = pa; p < pend; ++p) {
+    while (m == 0) { ++k; mk = mask[k]; m = ((uint64_t)mk.y << 32) | mk.x; }
+    const int s = __ffsll((long long)m) - 1;
+    m &= m - 1;
+    if (k != kcur) {
+      if (kcur >= 0) {
+        flush_grad<kLite>(grad, gid, acc);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) acc[q] = 0.f;
+      }
+      kcur = k;
+      mu = w.r3[k];
+      gid = __float_as_int(mu.w);
+      if (iso) {
+        const float4 f = w.r1[k];
+        c0 = w.r0[k]; u2 = w.r2[k].x; gx = f.x; v0 = f.y; v1 = f.z; v2 = f.w;
+      } else {
+        g = cand_from(w, k);
+        v0 = g.v0; v1 = g.v1; v2 = g.v2;
+      }
+    }
+    const float4 sx = w.sxg[s];
+    const float2 sg = w.sg[s];
+    const float x3[3] = {sx.x, sx.y, sx.z};
+    const float dx = sx.x - mu.x, dy = sx.y - mu.y, dz = sx.z - mu.z;
+    float tx, ty, tz, e;
+    if (iso) {                                                     // same arithmetic as pass 1
+      e = ex2_approx(gx * iso_s(x3, c0));
+      tx = u2 * dx; ty = u2 * dy; tz = u2 * dz;                    // t = A d = u^2 d
+    } else {
+      float w0, w1, w2;
+      e = ex2_approx(cand_q(g, sx.x, sx.y, sx.z, w0, w1, w2) * kNegHalfLog2e);
+      tx = g.u00 * w0;                                             // t = A d = U^T w
+      ty = fmaf(g.u11, w1, g.u01 * w0);
+      tz = fmaf(g.u22, w2, fmaf(g.u12, w1, g.u02 * w0));
+    }
+    const float he = (sx.w * v0 + sg.x * v1 + sg.y * v2) * e;
+    acc[0] = fmaf(he, tx, acc[0]); acc[1] = fmaf(he, ty, acc[1]); acc[2] = fmaf(he, tz, acc[2]);   // d mu
+    if constexpr (kLite) {
+      acc[3] = fmaf(sx.w, e, acc[3]); acc[4] = fmaf(sg.x, e, acc[4]); acc[5] = fmaf(sg.y, e, acc[5]);   // d v
+    } else {
+      const float kk = -0.5f * he;
+      const float kx = kk * dx, ky = kk * dy, kz = kk * dz;
+      acc[3] = fmaf(kx, dx, acc[3]); acc[4] = fmaf(ky, dy, acc[4]); acc[5] = fmaf(kz, dz, acc[5]);   // dA00 dA11 dA22
+      acc[6] = fmaf(kx, dy, acc[6]); acc[7] = fmaf(kx, dz, acc[7]); acc[8] = fmaf(ky, dz, acc[8]);   // dA01 dA02 dA12
+      acc[9] = fmaf(sx.w, e, acc[9]); acc[10] = fmaf(sg.x, e, acc[10]); acc[11] = fmaf(sg.y, e, acc[11]);   // d v
+    }
+  }
+  flush_grad<kLite>(grad, gid, acc);
 }
 
 __device__ __forceinline__ void load_pos(const float4* __restrict__ bin, int stride, int start, int count, int s,
@@ -377,19 +438,19 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
                 zref = __shfl_sync(0xffffffffu, xa[2], 0);
     xa[0] -= xref; xa[1] -= yref; xa[2] -= zref;            // NaN stays NaN
     xb[0] -= xref; xb[1] -= yref; xb[2] -= zref;
-    // ---------------- pass 1 (records the inside pairs while they fit)
+    // ---------------- pass 1 (keeps each candidate's inside masks while they fit)
     float ya[3] = {0.f, 0.f, 0.f}, yb[3] = {0.f, 0.f, 0.f};
-    int pbase = 0;
+    int np = 0;
     bool iso = false;
-    const bool chunks_fit = C <= 32 * kMaxChunks;
+    const bool masked = C <= 32 * kMaskChunks;
     for (int cb = 0, c = 0; cb < C; cb += 32, ++c) {
       const int kc = min(32, C - cb);
       iso = stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref, tau2);
-      eval_any<true>(w, iso, wi.count > 32, kc, xa, xb, tau2, ya, yb, w.pkey, w.pe, pbase, kPairCap, lane);
-      if (lane == 0 && c < kMaxChunks) w.cend[c] = (uint16_t)min(pbase, 0xFFFF);
+      uint2 cm = make_uint2(0u, 0u);
+      eval_any<true>(w, iso, wi.count > 32, kc, xa, xb, tau2, ya, yb, cm, lane);
+      if (masked) w.u.mask[c][lane] = cm;
+      np += (int)__reduce_add_sync(0xffffffffu, (unsigned)(__popc(cm.x) + __popc(cm.y)));
     }
-    const int np = pbase;                        // inside pairs of the item (warp-uniform)
-    const bool recorded = chunks_fit && pbase <= kPairCap;
     // ---------------- Eq. 4 loss and dL/dyhat (unnormalised)
     float ga[3] = {0.f, 0.f, 0.f}, gb[3] = {0.f, 0.f, 0.f}, ls = 0.f;
     if (lane < wi.count) hdr_grad(a.mode, eps, ya, ta, ga, ls);
@@ -406,14 +467,24 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
     __syncwarp();
     if (np == 0) continue;
     // ---------------- pass 2
-    if (recorded) {
-      int pstart = 0;
+    if (masked) {
       for (int cb = 0, c = 0; cb < C; cb += 32, ++c) {
-        const int pend = w.cend[c];
-        if (pend == pstart) continue;
+        const uint2 mk = w.u.mask[c][lane];
+        const int nk = __popc(mk.x) + __popc(mk.y);
+        int incl = nk;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const int P = __shfl_sync(0xffffffffu, incl, 31);
+        if (P == 0) continue;
         if (C > 32) iso = stage_chunk(w, a.csr_idx, a.rec, lo + cb, min(32, C - cb), lane, xref, yref, zref, tau2);
-        chunk_pairs_bwd(w, pstart, pend, a.grad, lane, iso, a.lite);
-        pstart = pend;
+        w.offs[lane] = incl - nk;
+        __syncwarp();
+        if (iso && a.lite) chunk_bwd_masks_impl<true>(w, w.u.mask[c], P, tau2, a.grad, lane, true);
+        else chunk_bwd_masks_impl<false>(w, w.u.mask[c], P, tau2, a.grad, lane, iso);
+        __syncwarp();
       }
     } else {
       // rare dense case: re-derive each chunk's pairs exactly as pass 1 did, in batches
@@ -443,13 +514,13 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
           if (pb + 64 > kPairCap) { chunk_pairs_bwd(w, 0, pb, a.grad, lane, ci, a.lite); pb = 0; }
           if (ina) {
             const int pos = pb + __popc(ma & lt);
-            w.pkey[pos] = (uint16_t)((k << 6) | lane);
-            w.pe[pos] = ea;
+            w.u.list.pkey[pos] = (uint16_t)((k << 6) | lane);
+            w.u.list.pe[pos] = ea;
           }
           if (inb) {
             const int pos = pb + __popc(ma) + __popc(mb & lt);
-            w.pkey[pos] = (uint16_t)((k << 6) | (lane + 32));
-            w.pe[pos] = eb;
+            w.u.list.pkey[pos] = (uint16_t)((k << 6) | (lane + 32));
+            w.u.list.pe[pos] = eb;
           }
           pb += __popc(ma) + __popc(mb);
           __syncwarp();
@@ -503,11 +574,11 @@ __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
     xa[0] -= xref; xa[1] -= yref; xa[2] -= zref;
     xb[0] -= xref; xb[1] -= yref; xb[2] -= zref;
     float ya[3] = {0.f, 0.f, 0.f}, yb[3] = {0.f, 0.f, 0.f};
-    int pbase = 0;
     for (int cb = 0; cb < C; cb += 32) {
       const int kc = min(32, C - cb);
       const bool iso = stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref, tau2);
-      eval_any<false>(w, iso, wi.count > 32, kc, xa, xb, tau2, ya, yb, nullptr, nullptr, pbase, 0, lane);
+      uint2 cm;
+      eval_any<false>(w, iso, wi.count > 32, kc, xa, xb, tau2, ya, yb, cm, lane);
     }
     if (lane < wi.count) query_out(a.out, a.att, a.beta, a.unb, __float_as_uint(pa.w), ya);
     if (lane + 32 < wi.count) query_out(a.out, a.att, a.beta, a.unb, __float_as_uint(pb4.w), yb);

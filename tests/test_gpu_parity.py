@@ -366,16 +366,23 @@ def test_cuda_graph_replay_matches_eager(gsc):
     np.testing.assert_allclose(rows(c2), rows(c1), rtol=1e-5, atol=1e-6)
 
 
-def test_gradient_parity_dense_no_cutoff(gsc):
-    """tau = INFINITY: every (sample, Gaussian) pair contributes, so the per-warp pair list
-    overflows and the kernel's re-derivation path runs; gradients must still match."""
-    pos, alb, ls = workload.cfg0_lattice()
-    hp = gsc.default_hparams(cutoff_sigma=float("inf"))
-    c = gsc.GSCache([64, 16], pos, alb, init_log_scale=ls, seed=1, hparams=hp)
+@pytest.mark.parametrize("n0", [64, 448])
+def test_gradient_parity_dense_no_cutoff(gsc, n0):
+    """tau = INFINITY: every (sample, Gaussian) pair contributes.  64 Gaussians: the inside
+    masks of pass 1 drive the backward; 448 (> 384 candidates per cell): the masks do not fit
+    and the kernel's re-derivation path runs.  Gradients must match either way."""
     r = np.random.default_rng(8)
+    if n0 == 64:
+        pos, alb, ls = workload.cfg0_lattice()
+    else:
+        pos = r.uniform(-0.8, 0.8, (n0, 3)).astype(np.float32)
+        alb = r.uniform(0.2, 0.9, (n0, 3)).astype(np.float32)
+        ls = np.full((n0, 3), np.log(0.3), np.float32)
+    hp = gsc.default_hparams(cutoff_sigma=float("inf"))
+    c = gsc.GSCache([n0, 16], pos, alb, init_log_scale=ls, seed=1, hparams=hp)
     P0 = c.params_rows(0)
-    P0[:, 3:7] = r.normal(size=(64, 4)).astype(np.float32)
-    P0[:, 10:13] += r.uniform(-0.3, 0.3, (64, 3)).astype(np.float32)
+    P0[:, 3:7] = r.normal(size=(n0, 4)).astype(np.float32)
+    P0[:, 10:13] += r.uniform(-0.3, 0.3, (n0, 3)).astype(np.float32)
     c.set_params_rows(0, P0)
     P = rows(c)
     c.debug_enable_grads(True)
