@@ -336,7 +336,7 @@ def run_ours(args):
     # ---- CPU oracle baseline (rank 0, N = 1 only), bounded sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cache, cfg, args.cpu_samples)
+        cpu = cpu_baseline(cache, cfg, args.cpu_samples or S)
 
     if rank == 0:
         line = {
@@ -399,7 +399,8 @@ def main():
     ap.add_argument("--separate", action="store_true",
                     help="time gc_query + gc_fit instead of the gc_fit_query frame call")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-samples", type=int, default=200_000)
+    ap.add_argument("--cpu-samples", type=int, default=0,
+                    help="samples (and lookups) of the oracle baseline; 0 = the whole frame")
     ap.add_argument("--ref-samples", type=int, default=100_000)
     ap.add_argument("--clock-window", type=float, default=2.0)
     ap.add_argument("--cell-scale", type=float, default=1.0, help="culling-grid cell edge multiplier")
