@@ -423,16 +423,18 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
     const int lo = (int)__ldg(a.csr_off + wi.cell);
     const int C = (int)__ldg(a.csr_off + wi.cell + 1) - lo;
     float xa[3], xb[3], ta[3] = {0.f, 0.f, 0.f}, tb[3] = {0.f, 0.f, 0.f};
-    float4 pa, pb4;
-    load_pos(a.bin, 2, wi.start, wi.count, lane, xa, pa);
-    load_pos(a.bin, 2, wi.start, wi.count, lane + 32, xb, pb4);
-    if (lane < wi.count) {
-      const float4 q = __ldcs(a.bin + 2 * (int64_t)(wi.start + lane) + 1);
-      ta[0] = pa.w; ta[1] = q.x; ta[2] = q.y;
-    }
-    if (lane + 32 < wi.count) {
-      const float4 q = __ldcs(a.bin + 2 * (int64_t)(wi.start + lane + 32) + 1);
-      tb[0] = pb4.w; tb[1] = q.x; tb[2] = q.y;
+    {                                            // one 32-byte load per sample: x y z r | g b - -
+      const float kNaN = __int_as_float(0x7fffffff);   // inactive samples: never inside
+      xa[0] = xa[1] = xa[2] = xb[0] = xb[1] = xb[2] = kNaN;
+      float4 p, q;
+      if (lane < wi.count) {
+        ld_v8_nc(a.bin + 2 * (int64_t)(wi.start + lane), p, q);
+        xa[0] = p.x; xa[1] = p.y; xa[2] = p.z; ta[0] = p.w; ta[1] = q.x; ta[2] = q.y;
+      }
+      if (lane + 32 < wi.count) {
+        ld_v8_nc(a.bin + 2 * (int64_t)(wi.start + lane + 32), p, q);
+        xb[0] = p.x; xb[1] = p.y; xb[2] = p.z; tb[0] = p.w; tb[1] = q.x; tb[2] = q.y;
+      }
     }
     const float xref = __shfl_sync(0xffffffffu, xa[0], 0), yref = __shfl_sync(0xffffffffu, xa[1], 0),
                 zref = __shfl_sync(0xffffffffu, xa[2], 0);
