@@ -250,17 +250,18 @@ def run_ours(args):
         e1.record(stream)
         barrier()
         ms_total = e0.elapsed_time(e1)
-        if args.clock_window > 0:     # keep the GPU busy long enough for nvidia-smi samples
-            t_end = time.time() + args.clock_window
+        ms = torch.tensor([ms_total / args.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        ms_step = float(ms.item())
+        if args.clock_window > 0:     # keep the GPU busy long enough for nvidia-smi samples;
+            # the same number of frames on every rank (each frame holds an NCCL all-reduce)
+            rounds = max(1, int(args.clock_window * 1e3 / (ms_step * 20)))
             with torch.cuda.stream(stream):
-                while time.time() < t_end:
+                for _ in range(rounds):
                     for k in range(20):
                         (graphs[k % R].replay() if graphs else step(k % R, stream))
                     stream.synchronize()
-    ms = torch.tensor([ms_total / args.steps], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms_step = float(ms.item())
     st = cache._stats
     torch.cuda.synchronize(dev)
     n_valid = int(st.n_valid)           # last step's valid samples (global under DP)
