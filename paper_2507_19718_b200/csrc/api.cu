@@ -145,7 +145,7 @@ static gc_status ensure_scratch(gc_cache c, Scratch& sc, int64_t S, bool fit, cu
   int64_t ntiles = (nbins + kScanTile - 1) / kScanTile;
   int64_t work_cap = cap / kCH + std::min<int64_t>(cap, c->NC) + 2;
   CK(dalloc(&sc.key, cap)); CK(dalloc(&sc.rank, cap));
-  CK(dalloc(&sc.bin, (fit ? 2 : 1) * cap));
+  CK(dalloc(&sc.bin, 2 * cap));                       // 32-B bins (full sectors) for both
   CK(dalloc(&sc.cell_count, nbins)); CK(dalloc(&sc.cell_start, nbins + 1));
   CK(cudaMemset(sc.cell_count, 0, sizeof(uint32_t) * nbins));   // kept zero by the scan
   (void)ntiles;

@@ -569,8 +569,8 @@ __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
     const int C = (int)__ldg(a.csr_off + wi.cell + 1) - lo;
     float xa[3], xb[3];
     float4 pa, pb4;
-    load_pos(a.bin, 1, wi.start, wi.count, lane, xa, pa);
-    load_pos(a.bin, 1, wi.start, wi.count, lane + 32, xb, pb4);
+    load_pos(a.bin, 2, wi.start, wi.count, lane, xa, pa);
+    load_pos(a.bin, 2, wi.start, wi.count, lane + 32, xb, pb4);
     const float xref = __shfl_sync(0xffffffffu, xa[0], 0), yref = __shfl_sync(0xffffffffu, xa[1], 0),
                 zref = __shfl_sync(0xffffffffu, xa[2], 0);
     xa[0] -= xref; xa[1] -= yref; xa[2] -= zref;

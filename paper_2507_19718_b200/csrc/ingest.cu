@@ -113,8 +113,9 @@ __global__ void __launch_bounds__(256, 4) k_scatter(const float* __restrict__ po
       if (rgb) {
         st_v8(b.bin + 2 * (int64_t)d[u], make_float4(v[u][0], v[u][1], v[u][2], v[u][3]),
               make_float4(v[u][4], v[u][5], 0.f, 0.f));
-      } else {
-        b.bin[d[u]] = make_float4(v[u][0], v[u][1], v[u][2], __uint_as_float((uint32_t)i));
+      } else {   // full 32-B sectors here too: a half-sector write costs a read-modify-write in DRAM
+        st_v8(b.bin + 2 * (int64_t)d[u], make_float4(v[u][0], v[u][1], v[u][2], __uint_as_float((uint32_t)i)),
+              make_float4(0.f, 0.f, 0.f, 0.f));
       }
     }
   }

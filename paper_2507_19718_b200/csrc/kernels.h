@@ -103,7 +103,7 @@ void launch_keys(const float* pos, const int32_t* len, const float* rgb, int lev
                  int64_t S, const LevelGeom& g, IngestBufs b, cudaStream_t s, Profiler* prof);
 void launch_keys_query(const float* pos, const int32_t* len, int level_fixed, int64_t S,
                        const LevelGeom& g, IngestBufs b, float* out, cudaStream_t s, Profiler* prof);
-// rgb != NULL: fit samples, 32-B bins (x y z r | g b - -); else lookups, 16-B bins (x y z idx).
+// 32-B bins: fit samples (x y z r | g b - -) if rgb != NULL, else lookups (x y z idx | - - - -).
 void launch_scatter(const float* pos, const float* rgb, int64_t S, const uint32_t* cell_start,
                     IngestBufs b, cudaStream_t s, Profiler* prof);
 void launch_levels_of(const uint32_t* key, int64_t S, const LevelGeom& g, int32_t* out,
