@@ -90,6 +90,7 @@ struct gc_cache_s {
   LvlStats* lvl = nullptr;
   gc_fit_stats* dstats = nullptr;
   gc_fit_stats* hstats = nullptr;   // pinned staging
+  uint32_t* hcsr = nullptr;         // pinned: entries of the latest culling-list rebuild (capacity guard)
   double* partial = nullptr;
   int fb_grid = 0, q_grid = 0;
   bool dbg_on = false;
@@ -175,8 +176,37 @@ static gc_status rebuild_csr(gc_cache c, cudaStream_t s, bool recompute_records)
   launch_scan(c->csr_count, c->NC, 0, c->csr_tiles, c->csr_totals, c->csr_off, nullptr, nullptr, c->geom, s,
               &c->prof);
   launch_cull_emit(c->G, cull_bufs(c), c->P, c->geom, c->csr_off, c->csr_idx, c->csr_cap, c->st, s, &c->prof);
+  // the rebuild's entry count goes to pinned memory for the capacity guard of later calls
+  CK(cudaMemcpyAsync(c->hcsr, c->csr_totals, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   CK(cudaGetLastError());
   return GC_OK;
+}
+
+// Capacity guard of the culling lists, checked on the host at the start of each call from the
+// entry count of the latest completed rebuild (pinned, no synchronisation).  Lists past half
+// of their capacity (Gaussians growing, scale LR > 0) are reallocated to 4x their size; lists
+// that overflowed (entries past the capacity were dropped, so the lookups / fit that used them
+// were incomplete) are reallocated AND rebuilt, and the call reports GC_ERR_STATE once.
+static gc_status csr_guard(gc_cache c, cudaStream_t s) {
+  const uint32_t total = *(volatile uint32_t*)c->hcsr;
+  if (total <= c->csr_cap / 2 || capturing(s)) return GC_OK;
+  const bool overflowed = total > c->csr_cap;
+  CK(cudaDeviceSynchronize());
+  const uint64_t cap = std::min<uint64_t>(4ull * total, 0x7FFFFFFFull);
+  int32_t* idx = nullptr;
+  uint32_t* ovf = nullptr;
+  CK(dalloc(&idx, cap)); CK(dalloc(&ovf, cap));
+  CK(cudaMemcpy(idx, c->csr_idx, sizeof(int32_t) * std::min<uint64_t>(total, c->csr_cap), cudaMemcpyDeviceToDevice));
+  cudaFree(c->csr_idx); cudaFree(c->csr_ovf);
+  c->csr_idx = idx; c->csr_ovf = ovf; c->csr_cap = (uint32_t)cap;
+  if (!overflowed) return GC_OK;
+  CK(cudaMemset(&c->st->csr_overflow, 0, sizeof(unsigned int)));
+  if (!c->pending) {                 // a pending deferred step rebuilds with the new capacity anyway
+    CK(cudaMemset(c->csr_count, 0, sizeof(uint32_t) * c->NC));
+    if (gc_status e = rebuild_csr(c, s, true)) return e;
+  }
+  return fail(GC_ERR_STATE, "culling lists overflowed (%u entries > capacity); capacity grown to %u and lists "
+              "rebuilt -- the previous call's lookups / fit used incomplete lists", total, c->csr_cap);
 }
 
 static void CUDART_CB stats_cb(void* arg) {
@@ -315,6 +345,8 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
   }
   CK(dalloc(&c->lvl, 1)); CK(dalloc(&c->dstats, 1)); CK(cudaMemset(c->dstats, 0, sizeof(gc_fit_stats)));
   CK(cudaHostAlloc((void**)&c->hstats, sizeof(gc_fit_stats), cudaHostAllocDefault));
+  CK(cudaHostAlloc((void**)&c->hcsr, sizeof(uint32_t), cudaHostAllocDefault));
+  *c->hcsr = 0u;
 
   // inputs (host or device)
   float *dpos = nullptr, *drgb = nullptr, *dls = nullptr;
@@ -448,6 +480,7 @@ static void destroy_impl(gc_cache c) {
                 c->csr_totals, c->csr_idx, c->csr_tiles, c->st, c->lvl, c->dstats, c->partial, c->pack_tmp};
   for (void* p : ps) if (p) cudaFree(p);
   if (c->hstats) cudaFreeHost(c->hstats);
+  if (c->hcsr) cudaFreeHost(c->hcsr);
   c->fit.release();
   c->qry.release();
   for (auto* p : c->payloads) delete p;
@@ -544,7 +577,10 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
   CK(cudaSetDevice(c->device));
   if (gc_status e = check_sticky(c)) return e;
   if (gc_status e = ensure_scratch(c, c->fit, std::max<int64_t>(S, 1), true, s)) return e;
-  if (!forked) { if (gc_status e = fork_pending(c, s, &tail_ev)) return e; }
+  if (!forked) {
+    if (gc_status e = csr_guard(c, s)) return e;
+    if (gc_status e = fork_pending(c, s, &tail_ev)) return e;
+  }
   Scratch& F = c->fit;
   if (S > 0) {
     const bool hpos = !is_device_ptr(pos), hlen = !is_device_ptr(path_len), hrgb = !is_device_ptr(rgb);
@@ -618,6 +654,7 @@ gc_status gc_fit_query(gc_cache c, const float* pos, const int32_t* path_len, co
   cudaStream_t s = (cudaStream_t)stream;
   CK(cudaSetDevice(c->device));
   cudaEvent_t tail_ev = nullptr;      // a deferred previous step overlaps both halves' ingest
+  if (gc_status e = csr_guard(c, s)) return e;
   if (gc_status e = fork_pending(c, s, &tail_ev)) return e;
   CK(cudaEventRecord(c->ev_fork, s));
   CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
@@ -655,7 +692,10 @@ static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_le
   CK(cudaSetDevice(c->device));
   if (gc_status e = check_sticky(c)) return e;
   if (gc_status e = ensure_scratch(c, c->qry, S, false, s)) return e;
-  if (!forked) { if (gc_status e = fork_pending(c, s, &tail_ev)) return e; }
+  if (!forked) {
+    if (gc_status e = csr_guard(c, s)) return e;
+    if (gc_status e = fork_pending(c, s, &tail_ev)) return e;
+  }
   Scratch& Q = c->qry;
   const bool hpos = !is_device_ptr(pos), hlen = path_len && !is_device_ptr(path_len), hout = !is_device_ptr(out_rgb);
   if (hpos || hlen || hout) {
