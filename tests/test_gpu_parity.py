@@ -419,6 +419,19 @@ def test_data_parallel_one_rank_nccl_path_is_identity(gsc):
         torch.cuda.synchronize()
         np.testing.assert_allclose(list(s2.loss[:3]), l1, rtol=1e-6)
     np.testing.assert_allclose(rows(c1), rows(c2), rtol=1e-5, atol=1e-6)
+    # the frame call with a deferred step over the communicator (bench.py's N > 1 sequence)
+    c2.set_deferred_step(True)
+    for f in range(3, 5):
+        x, ln, rgb = workload.fit_batch(1, frame=f, S=50_000)
+        xq, lq = workload.query_batch(1, frame=f, S=20_000)
+        y1, s1 = c1.fit_query(cuda(x), cuda(ln), cuda(rgb), cuda(xq), cuda(lq))
+        torch.cuda.synchronize()
+        l1 = list(s1.loss[:3])
+        y2, s2 = c2.fit_query(cuda(x), cuda(ln), cuda(rgb), cuda(xq), cuda(lq))
+        torch.cuda.synchronize()
+        np.testing.assert_allclose(list(s2.loss[:3]), l1, rtol=2e-5)
+        np.testing.assert_allclose(y2.cpu().numpy(), y1.cpu().numpy(), rtol=2e-5, atol=1e-7)
+    np.testing.assert_allclose(rows(c1), rows(c2), rtol=1e-5, atol=1e-6)
 
 
 def test_query_radiance_epilogue(gsc):
