@@ -58,12 +58,18 @@ struct Scratch {
   uint32_t *cell_count = nullptr, *cell_start = nullptr, *totals = nullptr;
   uint2* tiles = nullptr;
   WorkItem* work = nullptr;
-  float *in_pos = nullptr, *in_rgb = nullptr, *out = nullptr;
-  int32_t* in_len = nullptr;
+  // host-input staging, two sets: a call's upload may start while the previous call still
+  // reads the other set (see stage_inputs)
+  float *in_pos[2] = {nullptr, nullptr}, *in_rgb[2] = {nullptr, nullptr}, *out = nullptr;
+  int32_t* in_len[2] = {nullptr, nullptr};
+  int set = 0;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+  bool free_rec[2] = {false, false};
   void release() {
-    void* ps[] = {key, rank, bin, cell_count, cell_start, totals, tiles, work,
-                  in_pos, in_rgb, out, in_len};
+    void* ps[] = {key, rank, bin, cell_count, cell_start, totals, tiles, work, out,
+                  in_pos[0], in_pos[1], in_rgb[0], in_rgb[1], in_len[0], in_len[1]};
     for (void* p : ps) if (p) cudaFree(p);
+    for (cudaEvent_t e : {ev_copied[0], ev_copied[1], ev_free[0], ev_free[1]}) if (e) cudaEventDestroy(e);
     *this = Scratch();
   }
 };
@@ -110,7 +116,8 @@ struct gc_cache_s {
   bool defer = false, pending = false;
   cudaStream_t side2 = nullptr;
   cudaEvent_t ev_fork2 = nullptr, ev_tail = nullptr;
-  cudaEvent_t ev_staged = nullptr;   // gc_fit_query: lookups' host inputs uploaded (fit uploads after)
+  cudaStream_t cp = nullptr;          // uploads of host inputs (stage_inputs)
+  cudaEvent_t ev_cpfork = nullptr;
 };
 
 // ------------------------------------------------------------------------- helpers
@@ -159,10 +166,52 @@ static gc_status ensure_scratch(gc_cache c, Scratch& sc, int64_t S, bool fit, cu
 }
 
 static gc_status ensure_staging(Scratch& sc, bool need_pos, bool need_len, bool need_rgb, bool need_out) {
-  if (need_pos && !sc.in_pos) CK(dalloc(&sc.in_pos, 3 * sc.cap));
-  if (need_len && !sc.in_len) CK(dalloc(&sc.in_len, sc.cap));
-  if (need_rgb && !sc.in_rgb) CK(dalloc(&sc.in_rgb, 3 * sc.cap));
+  for (int k = 0; k < 2; ++k) {
+    if (need_pos && !sc.in_pos[k]) CK(dalloc(&sc.in_pos[k], 3 * sc.cap));
+    if (need_len && !sc.in_len[k]) CK(dalloc(&sc.in_len[k], sc.cap));
+    if (need_rgb && !sc.in_rgb[k]) CK(dalloc(&sc.in_rgb[k], 3 * sc.cap));
+    if ((need_pos || need_len || need_rgb) && !sc.ev_copied[k]) {
+      CK(cudaEventCreateWithFlags(&sc.ev_copied[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&sc.ev_free[k], cudaEventDisableTiming));
+    }
+  }
   if (need_out && !sc.out) CK(dalloc(&sc.out, 3 * sc.cap));
+  return GC_OK;
+}
+
+// Host inputs of a call are uploaded on the handle's copy stream as soon as the call is made
+// -- the host data is final at call time -- into one of two staging sets, so a frame's upload
+// overlaps the previous frame's work (and the previous frame's downloads, the other PCIe
+// direction); the call's stream waits for the copies before its first kernel, and releases the
+// set after its last reader (mark_staging_free).  Under graph capture the copy stream is
+// forked from the call's stream instead (no early start).
+static gc_status stage_inputs(gc_cache c, Scratch& sc, cudaStream_t s, int64_t S, const float*& pos,
+                              const int32_t*& len, const float*& rgb, int& set) {
+  set = -1;
+  const bool hpos = pos && !is_device_ptr(pos), hlen = len && !is_device_ptr(len), hrgb = rgb && !is_device_ptr(rgb);
+  if (!(hpos || hlen || hrgb) || S == 0) return GC_OK;
+  const bool cap_ = capturing(s);
+  if (cap_ && ((hpos && !sc.in_pos[0]) || (hlen && !sc.in_len[0]) || (hrgb && !sc.in_rgb[0])))
+    return fail(GC_ERR_STATE, "staging not reserved before capture");
+  if (gc_status e = ensure_staging(sc, hpos, hlen, hrgb, false)) return e;
+  set = sc.set ^= 1;
+  if (cap_) {
+    CK(cudaEventRecord(c->ev_cpfork, s));
+    CK(cudaStreamWaitEvent(c->cp, c->ev_cpfork, 0));
+  }
+  if (sc.free_rec[set]) CK(cudaStreamWaitEvent(c->cp, sc.ev_free[set], 0));
+  if (hpos) { CK(cudaMemcpyAsync(sc.in_pos[set], pos, sizeof(float) * 3 * S, cudaMemcpyHostToDevice, c->cp)); pos = sc.in_pos[set]; }
+  if (hlen) { CK(cudaMemcpyAsync(sc.in_len[set], len, sizeof(int32_t) * S, cudaMemcpyHostToDevice, c->cp)); len = sc.in_len[set]; }
+  if (hrgb) { CK(cudaMemcpyAsync(sc.in_rgb[set], rgb, sizeof(float) * 3 * S, cudaMemcpyHostToDevice, c->cp)); rgb = sc.in_rgb[set]; }
+  CK(cudaEventRecord(sc.ev_copied[set], c->cp));
+  CK(cudaStreamWaitEvent(s, sc.ev_copied[set], 0));
+  return GC_OK;
+}
+
+static gc_status mark_staging_free(Scratch& sc, cudaStream_t s, int set) {
+  if (set < 0) return GC_OK;
+  CK(cudaEventRecord(sc.ev_free[set], s));
+  sc.free_rec[set] = true;
   return GC_OK;
 }
 
@@ -464,7 +513,8 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
   CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_fork2, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_tail, cudaEventDisableTiming));
-  CK(cudaEventCreateWithFlags(&c->ev_staged, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_cpfork, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&c->cp, cudaStreamNonBlocking));
   CK(dalloc(&c->partial, (size_t)kSlots * kPart));
   CK(cudaMemset(c->partial, 0, sizeof(double) * kSlots * kPart));
   CK(cudaDeviceSynchronize());
@@ -487,7 +537,8 @@ static void destroy_impl(gc_cache c) {
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->side2) cudaStreamDestroy(c->side2);
-  for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_fork2, c->ev_tail, c->ev_staged}) if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_fork2, c->ev_tail, c->ev_cpfork}) if (e) cudaEventDestroy(e);
+  if (c->cp) cudaStreamDestroy(c->cp);
   delete c;
 }
 
@@ -582,23 +633,13 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
     if (gc_status e = fork_pending(c, s, &tail_ev)) return e;
   }
   Scratch& F = c->fit;
-  if (S > 0) {
-    const bool hpos = !is_device_ptr(pos), hlen = !is_device_ptr(path_len), hrgb = !is_device_ptr(rgb);
-    if (hpos || hlen || hrgb) {
-      if (capturing(s) && (!F.in_pos || !F.in_len || !F.in_rgb)) return fail(GC_ERR_STATE, "staging not reserved before capture");
-      if (gc_status e = ensure_staging(F, hpos, hlen, hrgb, false)) return e;
-      // gc_fit_query: the lookups' inputs go over PCIe first, so their half computes (and its
-      // outputs stream back) while the fit samples upload
-      if (forked) CK(cudaStreamWaitEvent(s, c->ev_staged, 0));
-      if (hpos) { CK(cudaMemcpyAsync(F.in_pos, pos, sizeof(float) * 3 * S, cudaMemcpyHostToDevice, s)); pos = F.in_pos; }
-      if (hlen) { CK(cudaMemcpyAsync(F.in_len, path_len, sizeof(int32_t) * S, cudaMemcpyHostToDevice, s)); path_len = F.in_len; }
-      if (hrgb) { CK(cudaMemcpyAsync(F.in_rgb, rgb, sizeof(float) * 3 * S, cudaMemcpyHostToDevice, s)); rgb = F.in_rgb; }
-    }
-  }
+  int set = -1;
+  if (gc_status e = stage_inputs(c, F, s, S, pos, path_len, rgb, set)) return e;
   IngestBufs b{F.key, F.rank, F.cell_count, F.bin, c->NC};
   if (S > 0) launch_keys(pos, path_len, rgb, -1, S, c->geom, b, s, &c->prof);
   launch_scan(F.cell_count, c->NC * kRep, kCH, F.tiles, F.totals, F.cell_start, nullptr, F.work, c->geom, s, &c->prof);
   if (S > 0) launch_scatter(pos, rgb, S, F.cell_start, b, s, &c->prof);
+  if (gc_status e = mark_staging_free(F, s, set)) return e;
   if (tail_ev) CK(cudaStreamWaitEvent(s, tail_ev, 0));     // the previous step is complete
   FitArgs fa;
   fa.work = F.work; fa.n_work = F.totals + 1; fa.csr_off = c->csr_off; fa.csr_idx = c->csr_idx; fa.rec = c->rec;
@@ -697,19 +738,20 @@ static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_le
     if (gc_status e = fork_pending(c, s, &tail_ev)) return e;
   }
   Scratch& Q = c->qry;
-  const bool hpos = !is_device_ptr(pos), hlen = path_len && !is_device_ptr(path_len), hout = !is_device_ptr(out_rgb);
-  if (hpos || hlen || hout) {
-    if (capturing(s) && (!Q.in_pos || !Q.in_len || !Q.out)) return fail(GC_ERR_STATE, "staging not reserved before capture");
-    if (gc_status e = ensure_staging(Q, hpos, hlen, false, hout)) return e;
-    if (hpos) { CK(cudaMemcpyAsync(Q.in_pos, pos, sizeof(float) * 3 * S, cudaMemcpyHostToDevice, s)); pos = Q.in_pos; }
-    if (hlen) { CK(cudaMemcpyAsync(Q.in_len, path_len, sizeof(int32_t) * S, cudaMemcpyHostToDevice, s)); path_len = Q.in_len; }
+  const bool hout = !is_device_ptr(out_rgb);
+  if (hout) {
+    if (capturing(s) && !Q.out) return fail(GC_ERR_STATE, "staging not reserved before capture");
+    if (gc_status e = ensure_staging(Q, false, false, false, true)) return e;
   }
-  if (forked) CK(cudaEventRecord(c->ev_staged, s));
+  int set = -1;
+  const float* no_rgb = nullptr;
+  if (gc_status e = stage_inputs(c, Q, s, S, pos, path_len, no_rgb, set)) return e;
   float* dout = hout ? Q.out : out_rgb;
   IngestBufs b{Q.key, Q.rank, Q.cell_count, Q.bin, c->NC};
   launch_keys_query(pos, path_len, path_len ? -1 : level, S, c->geom, b, dout, s, &c->prof);
   launch_scan(Q.cell_count, c->NC * kRep, kCH, Q.tiles, Q.totals, Q.cell_start, nullptr, Q.work, c->geom, s, &c->prof);
   launch_scatter(pos, nullptr, S, Q.cell_start, b, s, &c->prof);
+  if (gc_status e = mark_staging_free(Q, s, set)) return e;
   QueryArgs qa;
   qa.work = Q.work; qa.n_work = Q.totals + 1; qa.csr_off = c->csr_off; qa.csr_idx = c->csr_idx; qa.rec = c->rec;
   qa.bin = Q.bin; qa.out = dout;
