@@ -301,6 +301,17 @@ def run_ours(args):
         traffic_src = "profiles/traffic.json: " + tj["source"]
     except Exception:
         pass
+    issue = None
+    try:   # the kernel's issue rate from the committed ncu capture (its real limiter)
+        with open(os.path.join(ROOT, "profiles", "issue.json")) as f:
+            ij = json.load(f)
+        m = ij["kernels"].get("k_" + top)
+        if m:
+            issue = {"ipc": m["ipc"], "peak_ipc": 4.0, "frac": m["ipc"] / 4.0,
+                     "fma_pipe_pct": m["fma_pipe_pct"], "xu_pipe_pct": m["xu_pipe_pct"],
+                     "source": "profiles/issue.json: " + ij["source"]}
+    except Exception:
+        pass
     if top == "fwdbwd":
         flops = (n_pairs / world) * FLOPS_PER_PAIR + n_valid_local * FLOPS_PER_SAMPLE
         achieved = flops / (kernel_ms[top] * 1e-3) / 1e12
@@ -308,7 +319,8 @@ def run_ours(args):
                 "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic, "kernel": top,
                 "traffic_source": traffic_src,
                 "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (B200_PROFILING.md counts/clock)",
-                "algorithmic": f"{FLOPS_PER_PAIR:.0f} flop/contributing pair + {FLOPS_PER_SAMPLE:.0f}/sample"}
+                "algorithmic": f"{FLOPS_PER_PAIR:.0f} flop/contributing pair + {FLOPS_PER_SAMPLE:.0f}/sample",
+                "issue_bound": issue}
     else:
         roof = {"bound": "hbm", "achieved": None, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": None, "traffic": None, "kernel": top}

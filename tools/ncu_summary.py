@@ -68,9 +68,20 @@ def main(csv_path, rep_path, tag):
         lines += ["", f"## `ncu --set full` ({rep_path.split('/')[-1]})", "",
                   "| kernel | " + " | ".join(c.split('__')[1] for c in h if '__' in c) + " |",
                   "|---|" + "---|" * len([c for c in h if '__' in c])]
+        issue = {}
         for r in rows[2:]:
             d = dict(zip(h, r))
             lines.append(f"| {d['Kernel Name'].split('(')[0]} | " + " | ".join(d[c] for c in h if '__' in c) + " |")
+            name = d['Kernel Name'].split('(')[0].replace('void ', '').split('<')[0]
+            try:
+                issue.setdefault(name, {"ipc": float(d['sm__inst_executed.avg.per_cycle_active']),
+                                        "fma_pipe_pct": float(d['sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active']),
+                                        "xu_pipe_pct": float(d['sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active'])})
+            except (KeyError, ValueError):
+                pass
+        json.dump({"source": f"{tag} ncu --set full ({rep_path.split('/')[-1]}): sm__inst_executed.avg.per_cycle_active "
+                             "(issue peak 4 per SM per cycle), FMA / XU pipe utilisation",
+                   "kernels": issue}, open("profiles/issue.json", "w"), indent=1)
     print("\n".join(lines))
     json.dump({"source": f"{tag} ncu launch list (dram__bytes_read.sum + dram__bytes_write.sum, mean per launch)",
                "bytes_per_launch": traffic}, open("profiles/traffic.json", "w"), indent=1)
