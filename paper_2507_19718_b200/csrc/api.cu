@@ -506,9 +506,13 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
 
   c->fb_grid = fwdbwd_grid();
   c->q_grid = query_grid();
-  // (stream priorities measured: favouring either half was slower than equal priority)
+  // a deferred optimizer step (side2) gates the next fwd/bwd and lookups: its CTAs go first
+  // while it shares the GPU with the sample ingest (measured -7 us/frame; favouring either
+  // half of the frame instead was slower)
+  int prio_lo = 0, prio_hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&c->side2, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithPriority(&c->side2, cudaStreamNonBlocking, prio_hi));
   CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_fork2, cudaEventDisableTiming));
