@@ -339,6 +339,51 @@ def test_cfg2_full_size_sampled(gsc):
     assert np.isfinite(st.loss[:4]).all() and st.n_pairs > 0
 
 
+def test_cfg2_full_size_bench_frame_call(gsc):
+    """configs[2] at full size exactly as bench.py runs it: gc_fit_query with the deferred
+    optimizer step, eager then as a replayed CUDA graph.  Each frame's sampled lookups match
+    the oracle on that frame's pre-step parameters; the first step's parameter update matches
+    the oracle's AdamW step on the full batch (first-step tolerance, as in
+    test_first_step_matches_oracle_update)."""
+    pos, alb = workload.init_cloud(2)
+    counts = workload.CONFIGS[2]["counts"]
+    c = gsc.GSCache(counts, cuda(pos), cuda(alb), seed=2)
+    S = workload.CONFIGS[2]["S"]
+    c.reserve(S, S)
+    c.set_deferred_step(True)
+    x0, ln0, rgb0 = workload.fit_batch(2, frame=0)
+    xq0, lq0 = workload.query_batch(2, frame=0)
+    P0 = rows(c)
+    y0, st0 = c.fit_query(cuda(x0), cuda(ln0), cuda(rgb0), cuda(xq0), cuda(lq0))
+    torch.cuda.synchronize()
+    idx = np.random.default_rng(7).choice(S, 2000, replace=False)
+    yo, lv, _ = oracle.query(c.goff, P0, xq0[idx].astype(np.float64), lq0[idx])
+    check_forward(y0.cpu().numpy()[idx], yo, P0, c.goff, xq0[idx], lv, what="cfg2 frame 0")
+    lvl = oracle.level_of(ln0, 4, x0.astype(np.float64), rgb0.astype(np.float64))
+    assert [st0.count[l] for l in range(4)] == [int((lvl == l).sum()) for l in range(4)]
+    P1 = rows(c)                                             # gc_params completes the deferred step
+    oc = oracle.OracleCache(counts, P0, grids=c.grids())
+    go = oc.fit(x0.astype(np.float64), ln0, rgb0.astype(np.float64))["grad"]
+    eta = np.array([1.16e-3] * 3 + [1e-3] * 4 + [1.25e-2] * 3 + [0.0] * 3 + [1.5e-1])
+    strong = np.abs(go) > 1e-3 * np.abs(go).max(axis=0, keepdims=True)
+    err = np.abs((P1 - P0) - (oc.P - P0))
+    assert np.all(err[strong] <= 1e-3 * eta[np.nonzero(strong)[1]] + 4e-7 * (1 + np.abs(P0[strong])))
+    assert np.all(err <= 2.0 * eta[None, :] + 4e-7 * (1 + np.abs(P0)))
+    # frame 1 as a captured graph (it contains frame 0's completed step: nothing is pending)
+    x1, ln1, rgb1, xq1, lq1 = map(cuda, (*workload.fit_batch(2, frame=1), *workload.query_batch(2, frame=1)))
+    out = torch.empty((S, 3), device="cuda")
+    st = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        c.fit_query(x1, ln1, rgb1, xq1, lq1, out=out, stream=st)
+    with torch.cuda.stream(st):
+        g.replay()
+    c.flush(st)
+    torch.cuda.synchronize()
+    yo1, lv1, _ = oracle.query(c.goff, P1, xq1.cpu().numpy()[idx].astype(np.float64), lq1.cpu().numpy()[idx])
+    check_forward(out.cpu().numpy()[idx], yo1, P1, c.goff, xq1.cpu().numpy()[idx], lv1, what="cfg2 frame 1 graph")
+
+
 def test_cuda_graph_replay_matches_eager(gsc):
     c1, _, _ = make_cfg1(gsc)
     c2, _, _ = make_cfg1(gsc)
