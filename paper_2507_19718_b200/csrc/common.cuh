@@ -41,8 +41,8 @@ struct DevState {
   int active[kMaxL];                 // level takes a step this call
   int stepped;                       // this call stepped (>= 1 valid sample)
   unsigned long long nonfinite;      // non-finite gradient elements skipped by a deferred step
-  unsigned int csr_total;            // culling-list entries of the current CSR
-  unsigned int csr_overflow;         // sticky: a rebuild exceeded the list capacity
+  unsigned int csr_overflow;         // a rebuild dropped entries past the list capacity (the
+                                     // host guard detects it from the entry count, csr_guard)
   unsigned int ovf_next;             // bump allocator of the wide-range rank slots (per rebuild)
 };
 
