@@ -53,7 +53,7 @@ static cudaError_t dalloc(T** p, size_t n) {
 
 struct Scratch {
   int64_t cap = 0;
-  uint32_t *key = nullptr, *rank = nullptr;
+  uint2* kr = nullptr;
   float4* bin = nullptr;
   uint32_t *cell_count = nullptr, *cell_start = nullptr, *totals = nullptr;
   uint2* tiles = nullptr;
@@ -66,7 +66,7 @@ struct Scratch {
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   bool free_rec[2] = {false, false};
   void release() {
-    void* ps[] = {key, rank, bin, cell_count, cell_start, totals, tiles, work, out,
+    void* ps[] = {kr, bin, cell_count, cell_start, totals, tiles, work, out,
                   in_pos[0], in_pos[1], in_rgb[0], in_rgb[1], in_len[0], in_len[1]};
     for (void* p : ps) if (p) cudaFree(p);
     for (cudaEvent_t e : {ev_copied[0], ev_copied[1], ev_free[0], ev_free[1]}) if (e) cudaEventDestroy(e);
@@ -152,7 +152,7 @@ static gc_status ensure_scratch(gc_cache c, Scratch& sc, int64_t S, bool fit, cu
   const int64_t nbins = c->NC * kRep;                 // replicated per-cell counters
   int64_t ntiles = (nbins + kScanTile - 1) / kScanTile;
   int64_t work_cap = cap / kCH + std::min<int64_t>(cap, c->NC) + 2;
-  CK(dalloc(&sc.key, cap)); CK(dalloc(&sc.rank, cap));
+  CK(dalloc(&sc.kr, cap));
   CK(dalloc(&sc.bin, 2 * cap));                       // 32-B bins (full sectors) for both
   CK(dalloc(&sc.cell_count, nbins)); CK(dalloc(&sc.cell_start, nbins + 1));
   CK(cudaMemset(sc.cell_count, 0, sizeof(uint32_t) * nbins));   // kept zero by the scan
@@ -639,7 +639,7 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
   Scratch& F = c->fit;
   int set = -1;
   if (gc_status e = stage_inputs(c, F, s, S, pos, path_len, rgb, set)) return e;
-  IngestBufs b{F.key, F.rank, F.cell_count, F.bin, c->NC};
+  IngestBufs b{F.kr, F.cell_count, F.bin, c->NC};
   if (S > 0) launch_keys(pos, path_len, rgb, -1, S, c->geom, b, s, &c->prof);
   launch_scan(F.cell_count, c->NC * kRep, kCH, F.tiles, F.totals, F.cell_start, nullptr, F.work, c->geom, s, &c->prof);
   if (S > 0) launch_scatter(pos, rgb, S, F.cell_start, b, s, &c->prof);
@@ -751,7 +751,7 @@ static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_le
   const float* no_rgb = nullptr;
   if (gc_status e = stage_inputs(c, Q, s, S, pos, path_len, no_rgb, set)) return e;
   float* dout = hout ? Q.out : out_rgb;
-  IngestBufs b{Q.key, Q.rank, Q.cell_count, Q.bin, c->NC};
+  IngestBufs b{Q.kr, Q.cell_count, Q.bin, c->NC};
   launch_keys_query(pos, path_len, path_len ? -1 : level, S, c->geom, b, dout, s, &c->prof);
   launch_scan(Q.cell_count, c->NC * kRep, kCH, Q.tiles, Q.totals, Q.cell_start, nullptr, Q.work, c->geom, s, &c->prof);
   launch_scatter(pos, nullptr, S, Q.cell_start, b, s, &c->prof);
@@ -935,11 +935,11 @@ gc_status gc_debug_levels(gc_cache c, int32_t* level_of, gc_stream stream) {
   CK(cudaSetDevice(c->device));
   const int64_t S = c->last_fit_S;
   if (S == 0) return GC_OK;
-  if (is_device_ptr(level_of)) { launch_levels_of(c->fit.key, S, c->geom, level_of, s); }
+  if (is_device_ptr(level_of)) { launch_levels_of(c->fit.kr, S, c->geom, level_of, s); }
   else {
     int32_t* d = nullptr;
     CK(dalloc(&d, S));
-    launch_levels_of(c->fit.key, S, c->geom, d, s);
+    launch_levels_of(c->fit.kr, S, c->geom, d, s);
     CK(cudaMemcpyAsync(level_of, d, sizeof(int32_t) * S, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     cudaFree(d);

@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256, 4) k_keys(const float* __restrict__ pos, 
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int64_t i = i0 + u * 32 + lane;
-      if (i < S) { b.key[i] = key[u]; b.rank[i] = rank[u]; }
+      if (i < S) b.kr[i] = make_uint2(key[u], rank[u]);
     }
   }
 }
@@ -89,8 +89,8 @@ __global__ void __launch_bounds__(256, 4) k_scatter(const float* __restrict__ po
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int64_t i = i0 + u * 32;
-      key[u] = i < S ? __ldcs(b.key + i) : kInvalidKey;
-      rank[u] = i < S ? __ldcs(b.rank + i) : 0u;
+      const uint2 kr = i < S ? __ldcs(b.kr + i) : make_uint2(kInvalidKey, 0u);
+      key[u] = kr.x; rank[u] = kr.y;
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u)
@@ -121,9 +121,9 @@ __global__ void __launch_bounds__(256, 4) k_scatter(const float* __restrict__ po
   }
 }
 
-__global__ void k_levels_of(const uint32_t* key, int64_t S, LevelGeom g, int32_t* out) {
+__global__ void k_levels_of(const uint2* kr, int64_t S, LevelGeom g, int32_t* out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t k = key[i];
+    uint32_t k = kr[i].x;
     out[i] = (k == kInvalidKey) ? -1 : level_of_cell(g, k);
   }
 }
@@ -151,8 +151,8 @@ void launch_scatter(const float* pos, const float* rgb, int64_t S, const uint32_
   launch_pdl(k_scatter, dim3(grid_for(S)), dim3(256), 0, s, pos, rgb, S, cell_start, b);
 }
 
-void launch_levels_of(const uint32_t* key, int64_t S, const LevelGeom& g, int32_t* out, cudaStream_t s) {
-  k_levels_of<<<grid_for(S), 256, 0, s>>>(key, S, g, out);
+void launch_levels_of(const uint2* kr, int64_t S, const LevelGeom& g, int32_t* out, cudaStream_t s) {
+  k_levels_of<<<grid_for(S), 256, 0, s>>>(kr, S, g, out);
 }
 
 }  // namespace gsc

@@ -92,11 +92,10 @@ void launch_cull_emit(int64_t G, CullBufs cb, const float* P, const LevelGeom& g
 
 // ingest.cu
 struct IngestBufs {
-  uint32_t* key;        // [S] global cell id or kInvalidKey
-  uint32_t* rank;       // [S] arrival rank inside the cell
+  uint2* kr;            // [S] (global cell id or kInvalidKey, arrival rank inside the cell)
   uint32_t* cell_count; // [NC]
-  float4* bin;          // binned samples, cell-major: fit 2 x float4 (x,y,z,r | g,b,-,-),
-                        // query 1 x float4 (x,y,z, original index as bits)
+  float4* bin;          // binned samples, cell-major, one 32-B sector each: fit (x,y,z,r | g,b,-,-),
+                        // query (x,y,z, original index as bits | -)
   int64_t nc;           // cells (counters are replica-major [kRep][nc])
 };
 void launch_keys(const float* pos, const int32_t* len, const float* rgb, int level_fixed,
@@ -106,7 +105,7 @@ void launch_keys_query(const float* pos, const int32_t* len, int level_fixed, in
 // 32-B bins: fit samples (x y z r | g b - -) if rgb != NULL, else lookups (x y z idx | - - - -).
 void launch_scatter(const float* pos, const float* rgb, int64_t S, const uint32_t* cell_start,
                     IngestBufs b, cudaStream_t s, Profiler* prof);
-void launch_levels_of(const uint32_t* key, int64_t S, const LevelGeom& g, int32_t* out,
+void launch_levels_of(const uint2* kr, int64_t S, const LevelGeom& g, int32_t* out,
                       cudaStream_t s);
 
 // fwdbwd.cu
