@@ -193,8 +193,8 @@ def run_ours(args):
     R = 4                                   # rotating frames: inputs of step k last used 4 steps ago
     frames = []
     for f in range(R):
-        x, ln, rgb = workload.fit_batch(cfg, frame=rank * R + f)
-        xq, lq = workload.query_batch(cfg, frame=rank * R + f)
+        x, ln, rgb = workload.fit_batch(cfg, frame=rank * R + f, morton=args.morton)
+        xq, lq = workload.query_batch(cfg, frame=rank * R + f, morton=args.morton)
         frames.append(tuple(torch.from_numpy(a).to(dev) for a in (x, ln, rgb, xq, lq)))
     in_bytes = sum(t.numel() * t.element_size() for t in frames[0])
     outq = torch.empty((S, 3), dtype=torch.float32, device=dev)
@@ -362,7 +362,8 @@ def run_ours(args):
                        "l2": f"{R} rotating device-resident frames ({R * in_bytes / 1e6:.0f} MB) > 126 MB L2",
                        "cuda_graph": not args.no_graph,
                        "frame_call": "gc_query + gc_fit" if args.separate else "gc_fit_query",
-                       "deferred_step": not args.no_defer},
+                       "deferred_step": not args.no_defer,
+                       "sample_order": "morton" if args.morton else "random"},
             "queries_per_s": S * world / (ms_step * 1e-3),
             "pairs_per_sample": n_pairs / max(n_valid, 1),
             "candidates_per_sample": n_cand / max(n_valid, 1),
@@ -407,6 +408,8 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--morton", action="store_true",
+                    help="samples in Morton order (a screen-coherent renderer) instead of random order")
     ap.add_argument("--no-defer", action="store_true",
                     help="complete each frame's optimizer step inside its own call (no deferral)")
     ap.add_argument("--separate", action="store_true",

@@ -60,16 +60,34 @@ __global__ void __launch_bounds__(256, 4) k_keys(const float* __restrict__ pos, 
       }
       if (!ok && out_zero && i < S) { out_zero[3 * i] = 0.f; out_zero[3 * i + 1] = 0.f; out_zero[3 * i + 2] = 0.f; }
     }
-    // one returning atomic per sample, all kU in flight before any result is consumed (random
-    // renderer order leaves nothing to aggregate within a warp); counter replica
-    // r = (i >> 5) % kRep spreads a hot cell's arrivals over kRep addresses (the same-address
-    // L2 atomic rate, ~55 M/s, otherwise serialises a 4k-sample cell for 70 us)
+    // Returning atomics, all kU in flight before any result is consumed.  Random renderer
+    // order leaves nothing to aggregate within a warp: one atomic per sample.  A screen-coherent
+    // order (neighbouring lanes in one cell, detected warp-uniformly) aggregates per distinct
+    // key instead, so a warp's samples of one cell do not serialise on one address.  Counter
+    // replica r = (i >> 5) % kRep spreads a hot cell's arrivals over kRep addresses (the
+    // same-address L2 atomic rate, ~55 M/s, otherwise serialises a 4k-sample cell for 70 us).
     uint32_t rank[kU];
+    unsigned peers[kU];
+    bool agg[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t prev = __shfl_up_sync(0xffffffffu, key[u], 1);
+      agg[u] = __any_sync(0xffffffffu, lane > 0 && key[u] != kInvalidKey && prev == key[u]);
+      peers[u] = agg[u] ? __match_any_sync(0xffffffffu, key[u]) : (1u << lane);
+    }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       rank[u] = 0u;
       const uint32_t r = (uint32_t)(((i0 + u * 32) >> 5) & (kRep - 1));
-      if (key[u] != kInvalidKey) rank[u] = atomicAdd(b.cell_count + (size_t)r * b.nc + key[u], 1u);
+      if (key[u] != kInvalidKey && lane == __ffs(peers[u]) - 1)
+        rank[u] = atomicAdd(b.cell_count + (size_t)r * b.nc + key[u], (uint32_t)__popc(peers[u]));
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (agg[u]) {                              // warp-uniform
+        const uint32_t bb = __shfl_sync(0xffffffffu, rank[u], __ffs(peers[u]) - 1);
+        rank[u] = key[u] != kInvalidKey ? bb + __popc(peers[u] & ((1u << lane) - 1u)) : 0u;
+      }
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {

@@ -123,7 +123,7 @@ def fit_batch(cfg: int, frame: int = 0, S: int | None = None, morton: bool = Fal
     return pos.astype(np.float32), ln.astype(np.int32), rgb.astype(np.float32)
 
 
-def query_batch(cfg: int, frame: int = 0, S: int | None = None):
+def query_batch(cfg: int, frame: int = 0, S: int | None = None, morton: bool = False):
     """Cache lookups of one frame: pos f32[S][3], len i32[S] (all >= 1)."""
     c = CONFIGS[cfg]
     S = c["S"] if S is None else S
@@ -132,6 +132,9 @@ def query_batch(cfg: int, frame: int = 0, S: int | None = None):
     r = rng_for(cfg, 50_000 + frame)
     pos, _ = sc.points(S, r)
     ln = path_lengths(S, L, r, p_zero=0.0)
+    if morton:
+        order = np.argsort(_morton(pos), kind="stable")
+        pos, ln = pos[order], ln[order]
     return pos.astype(np.float32), ln.astype(np.int32)
 
 
