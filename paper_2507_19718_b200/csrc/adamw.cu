@@ -40,6 +40,21 @@ __device__ __forceinline__ int group_of(int k) { return k < 3 ? 0 : (k < 7 ? 1 :
 
 // Chain rule (C5) from the 12 coefficient gradients (dmu, packed dA, dv) to 14 raw grads.
 __device__ void chain_rule(const float p[kNP], const float cg[12], float out[kNP]) {
+  out[0] = cg[0]; out[1] = cg[1]; out[2] = cg[2];
+  const float wo = 1.f / (1.f + expf(-p[P_O]));
+  const float c0 = fmaxf(p[P_C], 0.f), c1 = fmaxf(p[P_C + 1], 0.f), c2 = fmaxf(p[P_C + 2], 0.f);
+  const float dwo = cg[9] * c0 + cg[10] * c1 + cg[11] * c2;
+  out[P_O] = dwo * wo * (1.f - wo);
+  out[P_C] = p[P_C] > 0.f ? wo * cg[9] : 0.f;
+  out[P_C + 1] = p[P_C + 1] > 0.f ? wo * cg[10] : 0.f;
+  out[P_C + 2] = p[P_C + 2] > 0.f ? wo * cg[11] : 0.f;
+  if (cg[3] == 0.f && cg[4] == 0.f && cg[5] == 0.f && cg[6] == 0.f && cg[7] == 0.f && cg[8] == 0.f) {
+    // dL/dA = 0 (the lite backward of an isotropic chunk with the scale group frozen):
+    // ds = -2 D (R^T 0 R) = 0 and dR = 2 * 0 * R D = 0 exactly -- skip the rotation algebra
+    out[3] = out[4] = out[5] = out[6] = 0.f;
+    out[P_S] = out[P_S + 1] = out[P_S + 2] = 0.f;
+    return;
+  }
   const float qw0 = p[P_Q], qx0 = p[P_Q + 1], qy0 = p[P_Q + 2], qz0 = p[P_Q + 3];
   const float n2 = qw0 * qw0 + qx0 * qx0 + qy0 * qy0 + qz0 * qz0;
   const bool deg = n2 < 1e-24f;
@@ -51,7 +66,6 @@ __device__ void chain_rule(const float p[kNP], const float cg[12], float out[kNP
   R[2][0] = 2.f * (x * z - w * y); R[2][1] = 2.f * (y * z + w * x); R[2][2] = 1.f - 2.f * (x * x + y * y);
   const float D[3] = {expf(-2.f * p[P_S]), expf(-2.f * p[P_S + 1]), expf(-2.f * p[P_S + 2])};
   const float G[3][3] = {{cg[3], cg[6], cg[7]}, {cg[6], cg[4], cg[8]}, {cg[7], cg[8], cg[5]}};
-  out[0] = cg[0]; out[1] = cg[1]; out[2] = cg[2];
   // GR = G R ; M_kk = (R^T G R)_kk ; dR = 2 G R D
   float GR[3][3];
 #pragma unroll
@@ -83,13 +97,6 @@ __device__ void chain_rule(const float p[kNP], const float cg[12], float out[kNP
     out[3] = (dw - w * dot) / qn; out[4] = (dx - x * dot) / qn;
     out[5] = (dy - y * dot) / qn; out[6] = (dz - z * dot) / qn;
   }
-  const float wo = 1.f / (1.f + expf(-p[P_O]));
-  const float c0 = fmaxf(p[P_C], 0.f), c1 = fmaxf(p[P_C + 1], 0.f), c2 = fmaxf(p[P_C + 2], 0.f);
-  const float dwo = cg[9] * c0 + cg[10] * c1 + cg[11] * c2;
-  out[P_O] = dwo * wo * (1.f - wo);
-  out[P_C] = p[P_C] > 0.f ? wo * cg[9] : 0.f;
-  out[P_C + 1] = p[P_C + 1] > 0.f ? wo * cg[10] : 0.f;
-  out[P_C + 2] = p[P_C + 2] > 0.f ? wo * cg[11] : 0.f;
 }
 
 // Fused normalise + chain rule + AdamW of one Gaussian per thread (A6); zeroes the gradient
