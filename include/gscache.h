@@ -9,7 +9,11 @@
  *
  * Conventions
  *  - Pointers marked "host or device" may point to either; the library detects the kind with
- *    cudaPointerGetAttributes and stages host data through its own pinned buffers.
+ *    cudaPointerGetAttributes and stages host data through its own device buffers.  Host
+ *    inputs of gc_fit / gc_query / gc_fit_query are read when the call is made (uploaded on
+ *    an internal copy stream, two staging sets, so a frame's upload overlaps the previous
+ *    frame's work; the call's stream waits for it); host outputs are written when `stream`
+ *    reaches the end of the call.
  *  - Ownership: all buffers passed in stay owned by the caller and must stay valid until
  *    the work enqueued on `stream` completes.  The library owns parameters, AdamW state,
  *    evaluation records, grids, culling lists and scratch (cudaMalloc at create/reserve).
@@ -19,8 +23,8 @@
  *    returned by the next call.  No C++ exception crosses the ABI.  gc_last_error()
  *    returns a thread-local message for the last non-OK status.
  *  - Streams: every call enqueues work on `stream` (NULL = legacy default stream) and
- *    returns; calls on one handle are stream-ordered and not thread-safe.  gc_fit and
- *    gc_query are CUDA-graph capturable once gc_reserve has sized the scratch.
+ *    returns; calls on one handle are stream-ordered and not thread-safe.  gc_fit, gc_query
+ *    and gc_fit_query are CUDA-graph capturable once gc_reserve has sized the scratch.
  *  - There is no CPU fallback: without a usable sm_100 device gc_create fails.
  */
 #ifndef GSCACHE_H_
