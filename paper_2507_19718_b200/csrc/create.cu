@@ -44,7 +44,9 @@ __global__ void __launch_bounds__(256) k_knn3(const float* __restrict__ P, int64
       for (int k = 0; k < m; ++k) {
         if (t0 + k == i) continue;
         const double dx = __dsub_rn(sx[k], xi), dy = __dsub_rn(sy[k], yi), dz = __dsub_rn(sz[k], zi);
-        const double d = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+        // squared distances are ranked (the correctly rounded sqrt is monotone, so the three
+        // smallest distances are the square roots of the three smallest squares: exact)
+        const double d = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
         if (d < b2) {
           if (d < b1) { b2 = b1; if (d < b0) { b1 = b0; b0 = d; } else { b1 = d; } }
           else b2 = d;
@@ -55,9 +57,9 @@ __global__ void __launch_bounds__(256) k_knn3(const float* __restrict__ P, int64
   if (i < n) {
     const int k = (int)((n - 1) < 3 ? (n - 1) : 3);
     double s = 0.0;
-    if (k >= 1) s = __dadd_rn(s, b0);
-    if (k >= 2) s = __dadd_rn(s, b1);
-    if (k >= 3) s = __dadd_rn(s, b2);
+    if (k >= 1) s = __dadd_rn(s, __dsqrt_rn(b0));
+    if (k >= 2) s = __dadd_rn(s, __dsqrt_rn(b1));
+    if (k >= 3) s = __dadd_rn(s, __dsqrt_rn(b2));
     dbar[i] = k > 0 ? __ddiv_rn(s, (double)k) : 0.0;
   }
 }
