@@ -150,13 +150,11 @@ static gc_status ensure_scratch(gc_cache c, Scratch& sc, int64_t S, bool fit, cu
   sc.release();
   int64_t cap = std::max<int64_t>(S, 1024);
   const int64_t nbins = c->NC * kRep;                 // replicated per-cell counters
-  int64_t ntiles = (nbins + kScanTile - 1) / kScanTile;
   int64_t work_cap = cap / kCH + std::min<int64_t>(cap, c->NC) + 2;
   CK(dalloc(&sc.kr, cap));
   CK(dalloc(&sc.bin, 2 * cap));                       // 32-B bins (full sectors) for both
   CK(dalloc(&sc.cell_count, nbins)); CK(dalloc(&sc.cell_start, nbins + 1));
   CK(cudaMemset(sc.cell_count, 0, sizeof(uint32_t) * nbins));   // kept zero by the scan
-  (void)ntiles;
   CK(dalloc(&sc.tiles, scan_state_words(nbins)));
   CK(cudaMemset(sc.tiles, 0, sizeof(uint2) * scan_state_words(nbins)));
   CK(dalloc(&sc.totals, 4));
