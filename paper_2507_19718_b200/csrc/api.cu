@@ -651,15 +651,19 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
   fa.tau2 = tau * tau; fa.hdr_eps = c->hp.hdr_eps; fa.mode = c->hp.loss_grad_mode; fa.L = c->L;
   fa.lite = (c->hp.lr[GC_SCALE] == 0.f && !c->dbg_on) ? 1 : 0;
   const bool dp = c->comm != nullptr;
+  // with the step deferred nothing after the statistics launch touches the call's stats, so a
+  // page-locked caller struct is written by the kernel itself (mapped through UVA): no copy
+  const bool stats_in_place = c->defer && stats && is_pinned_host(stats);
+  gc_fit_stats* out_stats = stats_in_place ? stats : c->dstats;
   launch_fwdbwd(fa, c->fb_grid, s, &c->prof);
   // single GPU: the step scalars ride in the statistics launch
-  launch_stats(c->partial, c->geom, S, c->lvl, !dp, c->st, c->hp, c->L, c->dstats, s, &c->prof);
+  launch_stats(c->partial, c->geom, S, c->lvl, !dp, c->st, c->hp, c->L, out_stats, s, &c->prof);
   if (dp) {                         // data parallel: one sum over ranks of grads + level stats
     NK(ncclGroupStart());
     NK(ncclAllReduce(c->grad, c->grad, (size_t)12 * c->G, ncclFloat32, ncclSum, c->comm, s));
     NK(ncclAllReduce(c->lvl, c->lvl, sizeof(LvlStats) / sizeof(double), ncclFloat64, ncclSum, c->comm, s));
     NK(ncclGroupEnd());
-    launch_step_scalars(c->lvl, c->st, c->hp, c->L, c->dstats, s);
+    launch_step_scalars(c->lvl, c->st, c->hp, c->L, out_stats, s);
   }
   if (join) CK(cudaStreamWaitEvent(s, join, 0));
   if (c->defer) {
@@ -667,7 +671,7 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
   } else {
     if (gc_status e = launch_tail(c, s, reinterpret_cast<unsigned long long*>(&c->dstats->nonfinite_grads))) return e;
   }
-  if (gc_status e = emit_stats(c, stats, s)) return e;
+  if (!stats_in_place) { if (gc_status e = emit_stats(c, stats, s)) return e; }
   CK(cudaGetLastError());
   c->last_fit_S = S;
   return GC_OK;
