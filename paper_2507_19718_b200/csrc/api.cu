@@ -222,9 +222,9 @@ static gc_status rebuild_csr(gc_cache c, cudaStream_t s, bool recompute_records)
     launch_record_cull(c->G, c->P, (double)c->hp.cutoff_sigma, c->geom, cull_bufs(c), c->st, s);
   launch_scan(c->csr_count, c->NC, 0, c->csr_tiles, c->csr_totals, c->csr_off, nullptr, nullptr, c->geom, s,
               &c->prof);
-  launch_cull_emit(c->G, cull_bufs(c), c->P, c->geom, c->csr_off, c->csr_idx, c->csr_cap, c->st, s, &c->prof);
-  // the rebuild's entry count goes to pinned memory for the capacity guard of later calls
-  CK(cudaMemcpyAsync(c->hcsr, c->csr_totals, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  // (the rebuild's entry count goes to pinned memory for the capacity guard of later calls)
+  launch_cull_emit(c->G, cull_bufs(c), c->P, c->geom, c->csr_off, c->csr_idx, c->csr_cap, c->st, c->csr_totals, c->hcsr,
+                   s, &c->prof);
   CK(cudaGetLastError());
   return GC_OK;
 }
@@ -499,7 +499,8 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
   CK(cudaMemset(&c->st->ovf_next, 0, sizeof(unsigned int)));
   launch_record_cull(G, c->P, tau, c->geom, cull_bufs(c), c->st, s);
   launch_scan(c->csr_count, c->NC, 0, c->csr_tiles, c->csr_totals, c->csr_off, nullptr, nullptr, c->geom, s, nullptr);
-  launch_cull_emit(G, cull_bufs(c), c->P, c->geom, c->csr_off, c->csr_idx, c->csr_cap, c->st, s, nullptr);
+  launch_cull_emit(G, cull_bufs(c), c->P, c->geom, c->csr_off, c->csr_idx, c->csr_cap, c->st, c->csr_totals, c->hcsr, s,
+                   nullptr);
   CK(cudaGetLastError());
 
   c->fb_grid = fwdbwd_grid();

@@ -20,9 +20,13 @@ __global__ void k_record_cull(int64_t G, const float* __restrict__ P, double tau
 // Fill the culling lists: entry of Gaussian j in cell c = off[c] + its rank from the counting
 // pass.  The order inside a cell is atomic order (unspecified); gc_debug_cull sorts on export.
 __global__ void k_cull_emit(int64_t G, CullBufs cb, const float* __restrict__ P, LevelGeom g,
-                            const uint32_t* __restrict__ off, int32_t* idx, uint32_t cap, DevState* st) {
+                            const uint32_t* __restrict__ off, int32_t* idx, uint32_t cap, DevState* st,
+                            const uint32_t* total, uint32_t* host_total) {
   pdl_enter();
-  if (blockIdx.x == 0 && threadIdx.x == 0) st->ovf_next = 0u;   // the counting pass is done
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->ovf_next = 0u;                           // the counting pass is done
+    if (host_total) *host_total = *total;        // entry count for the host's capacity guard
+  }
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < G; j += (int64_t)gridDim.x * blockDim.x) {
     const uint4 r = cb.range[j];
     const int l = level_of_gaussian(g, j);
@@ -277,11 +281,12 @@ void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& 
 }
 
 void launch_cull_emit(int64_t G, CullBufs cb, const float* P, const LevelGeom& g, const uint32_t* off,
-                      int32_t* idx, uint32_t cap, DevState* st, cudaStream_t s, Profiler* prof) {
+                      int32_t* idx, uint32_t cap, DevState* st, const uint32_t* total, uint32_t* host_total,
+                      cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "cull_emit", s);
   int blocks = (int)std::min<int64_t>((G + 127) / 128, 148 * 32);
   if (blocks < 1) blocks = 1;
-  launch_pdl(k_cull_emit, dim3(blocks), dim3(128), 0, s, G, cb, P, g, off, idx, cap, st);
+  launch_pdl(k_cull_emit, dim3(blocks), dim3(128), 0, s, G, cb, P, g, off, idx, cap, st, total, host_total);
 }
 
 }  // namespace gsc

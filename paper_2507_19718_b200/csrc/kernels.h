@@ -87,8 +87,10 @@ struct CullBufs {
 };
 void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& g, CullBufs cb, DevState* st,
                         cudaStream_t s);
+// host_total (page-locked, nullable): receives the rebuild's entry count (written by the kernel)
 void launch_cull_emit(int64_t G, CullBufs cb, const float* P, const LevelGeom& g, const uint32_t* off,
-                      int32_t* idx, uint32_t cap, DevState* st, cudaStream_t s, Profiler* prof);
+                      int32_t* idx, uint32_t cap, DevState* st, const uint32_t* total, uint32_t* host_total,
+                      cudaStream_t s, Profiler* prof);
 
 // ingest.cu
 struct IngestBufs {
