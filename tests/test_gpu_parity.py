@@ -720,3 +720,30 @@ def test_culling_list_capacity_guard(gsc):
     # ~10x the pairs per sample of the Eq. 2 cache -> ~10x the A3 boundary cases
     check_forward(y, yo, P, c.goff, x, lv, what="after growth", amb_rate=1e-3)
     _check_csr(c, P)
+
+
+def test_coherent_sample_order(gsc):
+    """Screen-coherent (Morton-ordered) samples take k_keys' warp-aggregated atomic path:
+    level assignment bit-exact, lookups and gradients match the oracle as for random order."""
+    c, _, _ = make_cfg1(gsc)
+    P = rows(c)
+    x, ln, rgb = workload.fit_batch(1, morton=True)
+    xq, lq = workload.query_batch(1, morton=True)
+    y = c.query(cuda(xq), cuda(lq)).cpu().numpy()
+    yo, lv, _ = oracle.query(c.goff, P, xq.astype(np.float64), lq, grids=c.grids())
+    check_forward(y, yo, P, c.goff, xq, lv, what="morton lookups")
+    c.debug_enable_grads(True)
+    st = c.fit(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(c.debug_levels(len(x)), oracle.level_of(ln, 3, x.astype(np.float64),
+                                                                         rgb.astype(np.float64)))
+    g = np.concatenate([c.debug_grads_rows(l) for l in range(3)]).astype(np.float64)
+    ro = oracle.loss_grad(c.goff, P, x.astype(np.float64), ln, rgb.astype(np.float64), grids=c.grids())
+    for l in range(3):
+        assert st.count[l] == ro["count"][l]
+        sl = slice(c.goff[l], c.goff[l + 1])
+        for name, cs in oracle.GROUP_SLICES.items():
+            if name == "rotation":
+                continue                              # isotropic cache: dq = 0
+            a, b = g[sl, cs], ro["grad"][sl, cs]
+            assert np.linalg.norm(a - b) <= 1e-4 * np.linalg.norm(b), (l, name)
