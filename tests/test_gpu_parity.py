@@ -747,3 +747,35 @@ def test_coherent_sample_order(gsc):
                 continue                              # isotropic cache: dq = 0
             a, b = g[sl, cs], ro["grad"][sl, cs]
             assert np.linalg.norm(a - b) <= 1e-4 * np.linalg.norm(b), (l, name)
+
+
+def test_fit_query_fixed_level_and_tiny_caches(gsc):
+    """gc_fit_query with a fixed lookup level (qlen NULL); a cache of one Gaussian per level;
+    eight levels: lookups vs the oracle on the pre-step parameters, level counts exact."""
+    r = np.random.default_rng(11)
+    # eight levels, 512 -> 4 Gaussians
+    counts = [512, 256, 128, 64, 32, 16, 8, 4]
+    pos, alb = workload.init_cloud(1)
+    c = gsc.GSCache(counts, cuda(pos[:512]), cuda(alb[:512]), seed=5)
+    P = rows(c)
+    x, ln, rgb = workload.fit_batch(1, S=30_000)
+    ln = r.integers(0, 10, len(ln)).astype(np.int32)          # levels beyond 8 clamp to the last
+    xq, _ = workload.query_batch(1, frame=2, S=10_000)
+    y, st = c.fit_query(cuda(x), cuda(ln), cuda(rgb), cuda(xq), None, qlevel=5)
+    torch.cuda.synchronize()
+    yo, lv, _ = oracle.query(c.goff, P, xq.astype(np.float64), None, level=5, grids=c.grids())
+    check_forward(y.cpu().numpy(), yo, P, c.goff, xq, lv, what="fixed level 5")
+    lvl = oracle.level_of(ln, 8, x.astype(np.float64), rgb.astype(np.float64))
+    assert [st.count[l] for l in range(8)] == [int((lvl == l).sum()) for l in range(8)]
+    # one Gaussian per level
+    c1 = gsc.GSCache([1, 1], cuda(pos[:1]), cuda(alb[:1]), seed=5,
+                     init_log_scale=cuda(np.full((1, 3), np.log(0.3), np.float32)))
+    P1 = rows(c1)
+    xq1 = (pos[:1] + r.normal(scale=0.2, size=(500, 3))).astype(np.float32)
+    lq1 = r.integers(1, 3, 500).astype(np.int32)
+    y1 = c1.query(cuda(xq1), cuda(lq1)).cpu().numpy()
+    yo1, lv1, _ = oracle.query(c1.goff, P1, xq1.astype(np.float64), lq1, grids=c1.grids())
+    check_forward(y1, yo1, P1, c1.goff, xq1, lv1, what="one Gaussian")
+    s1 = c1.fit(cuda(xq1), cuda(lq1), cuda(np.abs(r.normal(size=(500, 3))).astype(np.float32)))
+    torch.cuda.synchronize()
+    assert s1.step == 1 and np.isfinite(rows(c1)).all()
