@@ -309,7 +309,7 @@ __device__ __forceinline__ void chunk_bwd_masks_impl(const WarpSmem& w, const ui
 #pragma unroll
   for (int q = 0; q < NV; ++q) acc[q] = 0.f;
   int kcur = -1, gid = 0;
-  float4 mu = make_float4(0.f, 0.f, 0.f, 0.f), c0 = mu;
+  float4 mu = make_float4(0.f, 0.f, 0.f, 0.f);
   float u2 = 0.f, gx = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f;
   Cand g{};
   for (int p = pa; p < pend; ++p) {
@@ -327,7 +327,7 @@ __device__ __forceinline__ void chunk_bwd_masks_impl(const WarpSmem& w, const ui
       gid = __float_as_int(mu.w);
       if (iso) {
         const float4 f = w.r1[k];
-        c0 = w.r0[k]; u2 = w.r2[k].x; gx = f.x; v0 = f.y; v1 = f.z; v2 = f.w;
+        u2 = w.r2[k].x; gx = f.x; v0 = f.y; v1 = f.z; v2 = f.w;
       } else {
         g = cand_from(w, k);
         v0 = g.v0; v1 = g.v1; v2 = g.v2;
@@ -335,11 +335,11 @@ __device__ __forceinline__ void chunk_bwd_masks_impl(const WarpSmem& w, const ui
     }
     const float4 sx = w.sxg[s];
     const float2 sg = w.sg[s];
-    const float x3[3] = {sx.x, sx.y, sx.z};
-    const float dx = sx.x - mu.x, dy = sx.y - mu.y, dz = sx.z - mu.z;
+    // d = x' - mu (r3 and r0 hold the same recentred mu, so this is also iso_s's difference)
+    const float dx = __fsub_rn(sx.x, mu.x), dy = __fsub_rn(sx.y, mu.y), dz = __fsub_rn(sx.z, mu.z);
     float tx, ty, tz, e;
     if (iso) {                                                     // same arithmetic as pass 1
-      e = ex2_approx(gx * iso_s(x3, c0));
+      e = ex2_approx(gx * __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx))));
       tx = u2 * dx; ty = u2 * dy; tz = u2 * dz;                    // t = A d = u^2 d
     } else {
       float w0, w1, w2;
