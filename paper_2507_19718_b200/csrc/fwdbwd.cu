@@ -14,6 +14,7 @@
 //          <= 2-level segmented warp-shuffle scan over each Gaussian's run of pairs, and
 //          red.global.add.v4.f32 from every 4th lane of a run.  Work is proportional to the
 //          contributing pairs; never shared-memory float atomics (a CAS loop on sm_100a).
+#include <type_traits>
 #include "common.cuh"
 #include "kernels.h"
 #include "stats.cuh"
@@ -288,7 +289,7 @@ __device__ __forceinline__ int select_bit(uint32_t x, int r) {
 // select on the mask, then walks on bit by bit, recomputing e = exp(-Q/2) exactly as pass 1
 // did, accumulating the current Gaussian's coefficient gradients in registers and issuing
 // red.global.add.v4.f32 whenever the Gaussian changes and at the end.
-template <bool kLite>
+template <bool kLite, bool kWide>
 __device__ __forceinline__ void chunk_bwd_masks_impl(const WarpSmem& w, const uint2* __restrict__ mask, int P,
                                                      float tau2, float* __restrict__ grad, int lane, bool iso) {
   constexpr int NV = kLite ? 6 : 12;
@@ -298,12 +299,14 @@ __device__ __forceinline__ void chunk_bwd_masks_impl(const WarpSmem& w, const ui
 #pragma unroll
   for (int st = 16; st; st >>= 1)
     if (w.offs[k + st] <= pa) k += st;
+  // items of <= 32 samples (kWide false) have empty high mask words: 32-bit bit walk
+  using M = typename std::conditional<kWide, uint64_t, uint32_t>::type;
   uint2 mk = mask[k];
-  uint64_t m = ((uint64_t)mk.y << 32) | mk.x;
+  M m = kWide ? (M)(((uint64_t)mk.y << 32) | mk.x) : (M)mk.x;
   {                                            // drop the candidate's first (pa - offs[k]) pairs
     const int r = pa - w.offs[k], pl = __popc(mk.x);
-    if (r < pl) m &= ~(uint64_t)((1u << select_bit(mk.x, r)) - 1u);
-    else m = (uint64_t)(mk.y & ~((1u << select_bit(mk.y, r - pl)) - 1u)) << 32;
+    if (!kWide || r < pl) m &= ~(M)((1u << select_bit(mk.x, r)) - 1u);
+    else m = (M)((uint64_t)(mk.y & ~((1u << select_bit(mk.y, r - pl)) - 1u)) << 32);
   }
   float acc[NV];
 #pragma unroll
@@ -313,8 +316,12 @@ __device__ __forceinline__ void chunk_bwd_masks_impl(const WarpSmem& w, const ui
   float u2 = 0.f, gx = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f;
   Cand g{};
   for (int p = pa; p < pend; ++p) {
-    while (m == 0) { ++k; mk = mask[k]; m = ((uint64_t)mk.y << 32) | mk.x; }
-    const int s = __ffsll((long long)m) - 1;
+    while (m == 0) {
+      ++k;
+      if constexpr (kWide) { mk = mask[k]; m = ((uint64_t)mk.y << 32) | mk.x; }
+      else m = mask[k].x;
+    }
+    const int s = kWide ? __ffsll((long long)m) - 1 : __ffs((int)m) - 1;
     m &= m - 1;
     if (k != kcur) {
       if (kcur >= 0) {
@@ -484,8 +491,13 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
         if (C > 32) iso = stage_chunk(w, a.csr_idx, a.rec, lo + cb, min(32, C - cb), lane, xref, yref, zref, tau2);
         w.offs[lane] = incl - nk;
         __syncwarp();
-        if (iso && a.lite) chunk_bwd_masks_impl<true>(w, w.u.mask[c], P, tau2, a.grad, lane, true);
-        else chunk_bwd_masks_impl<false>(w, w.u.mask[c], P, tau2, a.grad, lane, iso);
+        if (wi.count > 32) {
+          if (iso && a.lite) chunk_bwd_masks_impl<true, true>(w, w.u.mask[c], P, tau2, a.grad, lane, true);
+          else chunk_bwd_masks_impl<false, true>(w, w.u.mask[c], P, tau2, a.grad, lane, iso);
+        } else {
+          if (iso && a.lite) chunk_bwd_masks_impl<true, false>(w, w.u.mask[c], P, tau2, a.grad, lane, true);
+          else chunk_bwd_masks_impl<false, false>(w, w.u.mask[c], P, tau2, a.grad, lane, iso);
+        }
         __syncwarp();
       }
     } else {
