@@ -173,6 +173,35 @@ __device__ __forceinline__ void eval_chunk_iso(const ChunkSmem& w, int kc, const
 template <bool kMask, bool kTwo>
 __device__ __forceinline__ void eval_chunk(const ChunkSmem& w, int kc, const float (&xa)[3], const float (&xb)[3],
                                            float tau2, float (&ya)[3], float (&yb)[3], uint2& cm, int lane) {
+  if constexpr (kTwo) {            // packed fp32x2, bit-identical to cand_q per half (see eval_chunk_iso)
+    const float2 X = make_float2(xa[0], xb[0]), Y = make_float2(xa[1], xb[1]), Z = make_float2(xa[2], xb[2]);
+    float2 A0 = make_float2(ya[0], yb[0]), A1 = make_float2(ya[1], yb[1]), A2 = make_float2(ya[2], yb[2]);
+#pragma unroll 2
+    for (int k = 0; k < kc; ++k) {
+      const Cand g = cand_from(w, k);
+      const float2 w0 = __ffma2_rn(Z, make_float2(g.u02, g.u02), __ffma2_rn(Y, make_float2(g.u01, g.u01),
+                                   __ffma2_rn(X, make_float2(g.u00, g.u00), make_float2(g.nc0, g.nc0))));
+      const float2 w1 = __ffma2_rn(Z, make_float2(g.u12, g.u12), __ffma2_rn(Y, make_float2(g.u11, g.u11),
+                                   make_float2(g.nc1, g.nc1)));
+      const float2 w2 = __ffma2_rn(Z, make_float2(g.u22, g.u22), make_float2(g.nc2, g.nc2));
+      const float2 Q = __ffma2_rn(w2, w2, __ffma2_rn(w1, w1, __fmul2_rn(w0, w0)));
+      const bool ina = Q.x <= tau2, inb = Q.y <= tau2;
+      const float2 t = __fmul2_rn(Q, make_float2(kNegHalfLog2e, kNegHalfLog2e));
+      const float ea_ = ex2_approx(t.x), eb_ = ex2_approx(t.y);
+      const float2 e = make_float2(ina ? ea_ : 0.f, inb ? eb_ : 0.f);
+      A0 = __ffma2_rn(e, make_float2(g.v0, g.v0), A0);
+      A1 = __ffma2_rn(e, make_float2(g.v1, g.v1), A1);
+      A2 = __ffma2_rn(e, make_float2(g.v2, g.v2), A2);
+      if constexpr (kMask) {
+        const uint32_t ma = __ballot_sync(0xffffffffu, ina), mb = __ballot_sync(0xffffffffu, inb);
+        if (lane == k) cm = make_uint2(ma, mb);
+      }
+    }
+    ya[0] = A0.x; ya[1] = A1.x; ya[2] = A2.x;
+    yb[0] = A0.y; yb[1] = A1.y; yb[2] = A2.y;
+    __syncwarp();
+    return;
+  }
 #pragma unroll 2
   for (int k = 0; k < kc; ++k) {
     const Cand g = cand_from(w, k);
@@ -312,6 +341,20 @@ __device__ __forceinline__ int select_bit(uint32_t x, int r) {
   return pos;
 }
 
+// End of a Gaussian's run in pass 2: acc[0..2] holds sum h e d (isotropic) or sum h e w
+// (general); d mu = u^2 * that, or U^T * that (t = A d = U^T U d = U^T w).
+template <int NV>
+__device__ __forceinline__ void run_to_dmu(bool iso, float u2, const Cand& g, float (&acc)[NV]) {
+  if (iso) {
+    acc[0] *= u2; acc[1] *= u2; acc[2] *= u2;
+  } else {
+    const float a0 = acc[0], a1 = acc[1], a2 = acc[2];
+    acc[0] = g.u00 * a0;
+    acc[1] = fmaf(g.u11, a1, g.u01 * a0);
+    acc[2] = fmaf(g.u22, a2, fmaf(g.u12, a1, g.u02 * a0));
+  }
+}
+
 // Backward of one staged chunk from pass 1's inside masks: the chunk's pairs in candidate-major
 // order (candidate k's samples a then b, ascending) are cut into 32 contiguous slices, one per
 // lane; a lane finds its first pair by a binary search over the candidates' pair offsets and a
@@ -354,6 +397,7 @@ __device__ __forceinline__ void chunk_bwd_masks_impl(const WarpSmem& w, const ui
     m &= m - 1;
     if (k != kcur) {
       if (kcur >= 0) {
+        run_to_dmu(iso, u2, g, acc);
         flush_grad<kLite>(grad, gid, acc);
 #pragma unroll
         for (int q = 0; q < NV; ++q) acc[q] = 0.f;
@@ -373,16 +417,15 @@ __device__ __forceinline__ void chunk_bwd_masks_impl(const WarpSmem& w, const ui
     const float2 sg = w.sg[s];
     // d = x' - mu (r3 and r0 hold the same recentred mu, so this is also iso_s's difference)
     const float dx = __fsub_rn(sx.x, mu.x), dy = __fsub_rn(sx.y, mu.y), dz = __fsub_rn(sx.z, mu.z);
+    // d mu = sum_p h_p e_p A d_p = A sum_p h_p e_p d_p over the run (A fixed per Gaussian):
+    // the run accumulates h e d (isotropic, A = u^2 I) or h e w (general, A d = U^T w) and
+    // run_to_dmu applies u^2 or U^T once per run instead of per pair
     float tx, ty, tz, e;
     if (iso) {                                                     // same arithmetic as pass 1
       e = ex2_approx(gx * __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx))));
-      tx = u2 * dx; ty = u2 * dy; tz = u2 * dz;                    // t = A d = u^2 d
+      tx = dx; ty = dy; tz = dz;
     } else {
-      float w0, w1, w2;
-      e = ex2_approx(cand_q(g, sx.x, sx.y, sx.z, w0, w1, w2) * kNegHalfLog2e);
-      tx = g.u00 * w0;                                             // t = A d = U^T w
-      ty = fmaf(g.u11, w1, g.u01 * w0);
-      tz = fmaf(g.u22, w2, fmaf(g.u12, w1, g.u02 * w0));
+      e = ex2_approx(cand_q(g, sx.x, sx.y, sx.z, tx, ty, tz) * kNegHalfLog2e);
     }
     const float he = (sx.w * v0 + sg.x * v1 + sg.y * v2) * e;
     acc[0] = fmaf(he, tx, acc[0]); acc[1] = fmaf(he, ty, acc[1]); acc[2] = fmaf(he, tz, acc[2]);   // d mu
@@ -396,6 +439,7 @@ __device__ __forceinline__ void chunk_bwd_masks_impl(const WarpSmem& w, const ui
       acc[9] = fmaf(sx.w, e, acc[9]); acc[10] = fmaf(sg.x, e, acc[10]); acc[11] = fmaf(sg.y, e, acc[11]);   // d v
     }
   }
+  run_to_dmu(iso, u2, g, acc);
   flush_grad<kLite>(grad, gid, acc);
 }
 
