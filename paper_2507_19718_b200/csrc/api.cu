@@ -89,7 +89,7 @@ struct gc_cache_s {
   double* rad2 = nullptr;
   uint32_t *csr_count = nullptr, *csr_off = nullptr, *csr_totals = nullptr;
   uint32_t *csr_rank = nullptr, *csr_ovf = nullptr;   // entry ranks from the counting pass (CullBufs)
-  int32_t* csr_idx = nullptr;
+  float4* csr_rec = nullptr;              // [csr_cap][4] list-ordered record copies (evaluator staging)
   uint2* csr_tiles = nullptr;
   uint32_t csr_cap = 0;
   DevState* st = nullptr;
@@ -214,7 +214,7 @@ static gc_status mark_staging_free(Scratch& sc, cudaStream_t s, int set) {
 }
 
 static CullBufs cull_bufs(gc_cache c) {
-  return CullBufs{c->rec, c->range, c->rad2, c->csr_count, c->csr_rank, c->csr_ovf, c->csr_cap};
+  return CullBufs{c->rec, c->range, c->rad2, c->csr_count, c->csr_rank, c->csr_ovf, c->csr_cap, c->csr_rec};
 }
 
 static gc_status rebuild_csr(gc_cache c, cudaStream_t s, bool recompute_records) {
@@ -223,7 +223,7 @@ static gc_status rebuild_csr(gc_cache c, cudaStream_t s, bool recompute_records)
   launch_scan(c->csr_count, c->NC, 0, c->csr_tiles, c->csr_totals, c->csr_off, nullptr, nullptr, c->geom, s,
               &c->prof);
   // (the rebuild's entry count goes to pinned memory for the capacity guard of later calls)
-  launch_cull_emit(c->G, cull_bufs(c), c->P, c->geom, c->csr_off, c->csr_idx, c->csr_cap, c->st, c->csr_totals, c->hcsr,
+  launch_cull_emit(c->G, cull_bufs(c), c->P, c->geom, c->csr_off, c->csr_cap, c->st, c->csr_totals, c->hcsr,
                    s, &c->prof);
   CK(cudaGetLastError());
   return GC_OK;
@@ -240,12 +240,13 @@ static gc_status csr_guard(gc_cache c, cudaStream_t s) {
   const bool overflowed = total > c->csr_cap;
   CK(cudaDeviceSynchronize());
   const uint64_t cap = std::min<uint64_t>(4ull * total, 0x7FFFFFFFull);
-  int32_t* idx = nullptr;
   uint32_t* ovf = nullptr;
-  CK(dalloc(&idx, cap)); CK(dalloc(&ovf, cap));
-  CK(cudaMemcpy(idx, c->csr_idx, sizeof(int32_t) * std::min<uint64_t>(total, c->csr_cap), cudaMemcpyDeviceToDevice));
-  cudaFree(c->csr_idx); cudaFree(c->csr_ovf);
-  c->csr_idx = idx; c->csr_ovf = ovf; c->csr_cap = (uint32_t)cap;
+  float4* lrec = nullptr;
+  CK(dalloc(&ovf, cap)); CK(dalloc(&lrec, 4 * cap));
+  const uint64_t keep = std::min<uint64_t>(total, c->csr_cap);
+  CK(cudaMemcpy(lrec, c->csr_rec, sizeof(float4) * 4 * keep, cudaMemcpyDeviceToDevice));
+  cudaFree(c->csr_ovf); cudaFree(c->csr_rec);
+  c->csr_ovf = ovf; c->csr_rec = lrec; c->csr_cap = (uint32_t)cap;
   if (!overflowed) return GC_OK;
   CK(cudaMemset(&c->st->csr_overflow, 0, sizeof(unsigned int)));
   if (!c->pending) {                 // a pending deferred step rebuilds with the new capacity anyway
@@ -484,7 +485,7 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
   CK(dalloc(&c->csr_rank, 27 * G));
   // sizing pass (counts only; no wide-range rank slots yet): the first CSR's exact size sets
   // the list capacity, then the real counting pass runs with full slot capacity
-  launch_record_cull(G, c->P, tau, c->geom, CullBufs{c->rec, c->range, c->rad2, c->csr_count, c->csr_rank, nullptr, 0u},
+  launch_record_cull(G, c->P, tau, c->geom, CullBufs{c->rec, c->range, c->rad2, c->csr_count, c->csr_rank, nullptr, 0u, nullptr},
                      c->st, s);
   launch_scan(c->csr_count, c->NC, 0, c->csr_tiles, c->csr_totals, c->csr_off, nullptr, nullptr, c->geom, s, nullptr);
   CK(cudaGetLastError());
@@ -493,13 +494,13 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
   uint64_t cap = std::max<uint64_t>(4ull * total, (uint64_t)total + (1u << 20));
   cap = std::min<uint64_t>(cap, 0x7FFFFFFFull);
   c->csr_cap = (uint32_t)cap;
-  CK(dalloc(&c->csr_idx, c->csr_cap));
   CK(dalloc(&c->csr_ovf, c->csr_cap));
+  CK(dalloc(&c->csr_rec, 4 * (size_t)c->csr_cap));
   CK(cudaMemset(&c->st->csr_overflow, 0, sizeof(unsigned int)));
   CK(cudaMemset(&c->st->ovf_next, 0, sizeof(unsigned int)));
   launch_record_cull(G, c->P, tau, c->geom, cull_bufs(c), c->st, s);
   launch_scan(c->csr_count, c->NC, 0, c->csr_tiles, c->csr_totals, c->csr_off, nullptr, nullptr, c->geom, s, nullptr);
-  launch_cull_emit(G, cull_bufs(c), c->P, c->geom, c->csr_off, c->csr_idx, c->csr_cap, c->st, c->csr_totals, c->hcsr, s,
+  launch_cull_emit(G, cull_bufs(c), c->P, c->geom, c->csr_off, c->csr_cap, c->st, c->csr_totals, c->hcsr, s,
                    nullptr);
   CK(cudaGetLastError());
 
@@ -530,7 +531,7 @@ static void destroy_impl(gc_cache c) {
   cudaDeviceSynchronize();
   void* ps[] = {c->P, c->M, c->V, c->grad, c->dbg, c->rec, c->range, c->rad2, c->csr_count, c->csr_off, c->csr_rank,
                 c->csr_ovf,
-                c->csr_totals, c->csr_idx, c->csr_tiles, c->st, c->lvl, c->dstats, c->partial, c->pack_tmp};
+                c->csr_totals, c->csr_rec, c->csr_tiles, c->st, c->lvl, c->dstats, c->partial, c->pack_tmp};
   for (void* p : ps) if (p) cudaFree(p);
   if (c->hstats) cudaFreeHost(c->hstats);
   if (c->hcsr) cudaFreeHost(c->hcsr);
@@ -645,7 +646,7 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
   if (gc_status e = mark_staging_free(F, s, set)) return e;
   if (tail_ev) CK(cudaStreamWaitEvent(s, tail_ev, 0));     // the previous step is complete
   FitArgs fa;
-  fa.work = F.work; fa.n_work = F.totals + 1; fa.csr_off = c->csr_off; fa.csr_idx = c->csr_idx; fa.rec = c->rec;
+  fa.work = F.work; fa.n_work = F.totals + 1; fa.csr_off = c->csr_off; fa.lrec = c->csr_rec;
   fa.bin = F.bin;
   fa.grad = c->grad; fa.partial = c->partial;
   const float tau = c->hp.cutoff_sigma;
@@ -760,7 +761,7 @@ static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_le
   launch_scatter(pos, nullptr, S, Q.cell_start, b, s, &c->prof);
   if (gc_status e = mark_staging_free(Q, s, set)) return e;
   QueryArgs qa;
-  qa.work = Q.work; qa.n_work = Q.totals + 1; qa.csr_off = c->csr_off; qa.csr_idx = c->csr_idx; qa.rec = c->rec;
+  qa.work = Q.work; qa.n_work = Q.totals + 1; qa.csr_off = c->csr_off; qa.lrec = c->csr_rec;
   qa.bin = Q.bin; qa.out = dout;
   Epilogue ep;
   if (gc_status e = ep.stage(att, beta, unb, S, s)) return e;
@@ -921,7 +922,9 @@ gc_status gc_debug_cull(gc_cache c, int level, int32_t* offsets, int32_t* idx, i
   for (int64_t k = 0; k <= nc; ++k) offsets[k] = (int32_t)(off[k] - off[0]);
   if (!idx || cap < total) return fail(GC_ERR_ARG, "idx capacity %lld < %lld", (long long)cap, (long long)total);
   std::vector<int32_t> h((size_t)std::max<int64_t>(total, 1));
-  CK(cudaMemcpyAsync(h.data(), c->csr_idx + off[0], sizeof(int32_t) * total, cudaMemcpyDeviceToHost, s));
+  if (total > 0)                     // the Gaussian index of each list entry (its 13th word)
+    CK(cudaMemcpy2DAsync(h.data(), sizeof(int32_t), reinterpret_cast<const char*>(c->csr_rec + 4 * (size_t)off[0]) + 48,
+                         4 * sizeof(float4), sizeof(int32_t), (size_t)total, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   const int64_t g0 = c->geom.goff[level];
   for (int64_t k = 0; k < nc; ++k) {

@@ -20,7 +20,7 @@ __global__ void k_record_cull(int64_t G, const float* __restrict__ P, double tau
 // Fill the culling lists: entry of Gaussian j in cell c = off[c] + its rank from the counting
 // pass.  The order inside a cell is atomic order (unspecified); gc_debug_cull sorts on export.
 __global__ void k_cull_emit(int64_t G, CullBufs cb, const float* __restrict__ P, LevelGeom g,
-                            const uint32_t* __restrict__ off, int32_t* idx, uint32_t cap, DevState* st,
+                            const uint32_t* __restrict__ off, uint32_t cap, DevState* st,
                             const uint32_t* total, uint32_t* host_total) {
   pdl_enter();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -32,6 +32,10 @@ __global__ void k_cull_emit(int64_t G, CullBufs cb, const float* __restrict__ P,
     const int l = level_of_gaussian(g, j);
     const int32_t lo[3] = {(int32_t)(r.x & 0xFFFF), (int32_t)(r.y & 0xFFFF), (int32_t)(r.z & 0xFFFF)};
     const int32_t hi[3] = {(int32_t)(r.x >> 16), (int32_t)(r.y >> 16), (int32_t)(r.z >> 16)};
+    // the record travels with the index: an evaluator's staging is then one load level
+    // (list entry) instead of two (index, then record)
+    const float4 ra = __ldg(cb.rec + 3 * j), rb = __ldg(cb.rec + 3 * j + 1), rc = __ldg(cb.rec + 3 * j + 2);
+    const float4 rd = make_float4(__int_as_float((int32_t)j), 0.f, 0.f, 0.f);
     if (!(r.w >> 31)) {
       const int64_t dx = g.dims[l][0], dy = g.dims[l][1];
       const uint32_t mask = r.w;
@@ -48,8 +52,11 @@ __global__ void k_cull_emit(int64_t G, CullBufs cb, const float* __restrict__ P,
 #pragma unroll
       for (int q = 0; q < 27; ++q) {
         if (pos[q] == 0xFFFFFFFFu) continue;
-        if (pos[q] < cap) idx[pos[q]] = (int32_t)j;
-        else atomicOr(&st->csr_overflow, 1u);
+        if (pos[q] < cap) {
+          st_v8(cb.lrec + 4 * (size_t)pos[q], ra, rb); st_v8(cb.lrec + 4 * (size_t)pos[q] + 2, rc, rd);
+        } else {
+          atomicOr(&st->csr_overflow, 1u);
+        }
       }
       continue;
     }
@@ -59,8 +66,11 @@ __global__ void k_cull_emit(int64_t G, CullBufs cb, const float* __restrict__ P,
     for_each_cell(lo, hi, m0, m1, m2, cb.rad2[j], g, l, [&](int64_t cell) {
       if (base + i < cb.ovf_cap) {
         const uint32_t pos = off[cell] + cb.ovf[base + i];
-        if (pos < cap) idx[pos] = (int32_t)j;
-        else atomicOr(&st->csr_overflow, 1u);
+        if (pos < cap) {
+          st_v8(cb.lrec + 4 * (size_t)pos, ra, rb); st_v8(cb.lrec + 4 * (size_t)pos + 2, rc, rd);
+        } else {
+          atomicOr(&st->csr_overflow, 1u);
+        }
       }
       ++i;
     });
@@ -281,12 +291,12 @@ void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& 
 }
 
 void launch_cull_emit(int64_t G, CullBufs cb, const float* P, const LevelGeom& g, const uint32_t* off,
-                      int32_t* idx, uint32_t cap, DevState* st, const uint32_t* total, uint32_t* host_total,
+                      uint32_t cap, DevState* st, const uint32_t* total, uint32_t* host_total,
                       cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "cull_emit", s);
   int blocks = (int)std::min<int64_t>((G + 127) / 128, 148 * 32);
   if (blocks < 1) blocks = 1;
-  launch_pdl(k_cull_emit, dim3(blocks), dim3(128), 0, s, G, cb, P, g, off, idx, cap, st, total, host_total);
+  launch_pdl(k_cull_emit, dim3(blocks), dim3(128), 0, s, G, cb, P, g, off, cap, st, total, host_total);
 }
 
 }  // namespace gsc

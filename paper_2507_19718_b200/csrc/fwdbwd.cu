@@ -70,15 +70,16 @@ __device__ __forceinline__ float cand_q(const Cand& g, float x, float y, float z
 // layout r0 = (mu - x_ref, tau^2/u^2), r1 = (-0.5 log2e u^2, v), r2.x = u^2, r3 as usual;
 // general chunks r0..r2 as documented on ChunkSmem.  (The expanded form g|x'|^2 + g|m|^2 -
 // 2g x'.m saves 2 ops per test but its cancellation costs ~1e-5 relative: measured, rejected.)
-__device__ __forceinline__ bool stage_chunk(ChunkSmem& w, const int32_t* __restrict__ csr_idx,
-                                            const float4* __restrict__ rec, int base, int kc, int lane,
+__device__ __forceinline__ bool stage_chunk(ChunkSmem& w, const float4* __restrict__ lrec, int base, int kc, int lane,
                                             float xr, float yr, float zr, float tau2) {
   __syncwarp();
   float4 p = make_float4(0.f, 0.f, 0.f, 0.f), q = p, r = p;
   int gid = 0;
   if (lane < kc) {
-    gid = __ldg(csr_idx + base + lane);
-    p = __ldg(rec + 3 * gid); q = __ldg(rec + 3 * gid + 1); r = __ldg(rec + 3 * gid + 2);
+    float4 t;                                    // list entry: record (3 x float4) + gid
+    ld_v8_nc(lrec + 4 * (int64_t)(base + lane), p, q);
+    ld_v8_nc(lrec + 4 * (int64_t)(base + lane) + 2, r, t);
+    gid = __float_as_int(t.x);
   }
   const bool iso = __all_sync(0xffffffffu, lane >= kc || (p.y == 0.f && p.z == 0.f && q.x == 0.f &&
                                                            p.x == p.w && p.w == q.y));
@@ -527,7 +528,7 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
     const bool masked = C <= 32 * kMaskChunks;
     for (int cb = 0, c = 0; cb < C; cb += 32, ++c) {
       const int kc = min(32, C - cb);
-      iso = stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref, tau2);
+      iso = stage_chunk(w, a.lrec, lo + cb, kc, lane, xref, yref, zref, tau2);
       uint2 cm = make_uint2(0u, 0u);
       eval_any<true>(w, iso, wi.count > 32, kc, xa, xb, tau2, ya, yb, cm, lane);
       if (masked) w.u.mask[c][lane] = cm;
@@ -561,7 +562,7 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
         }
         const int P = __shfl_sync(0xffffffffu, incl, 31);
         if (P == 0) continue;
-        if (C > 32) iso = stage_chunk(w, a.csr_idx, a.rec, lo + cb, min(32, C - cb), lane, xref, yref, zref, tau2);
+        if (C > 32) iso = stage_chunk(w, a.lrec, lo + cb, min(32, C - cb), lane, xref, yref, zref, tau2);
         w.offs[lane] = incl - nk;
         __syncwarp();
         if (wi.count > 32) {
@@ -578,7 +579,7 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
       const uint32_t lt = (1u << lane) - 1u;
       for (int cb = 0; cb < C; cb += 32) {
         const int kc = min(32, C - cb);
-        const bool ci = stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref, tau2);
+        const bool ci = stage_chunk(w, a.lrec, lo + cb, kc, lane, xref, yref, zref, tau2);
         int pb = 0;
         for (int k = 0; k < kc; ++k) {
           float Qa, Qb, ea, eb;                    // same arithmetic as eval_chunk[_iso]
@@ -663,7 +664,7 @@ __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
     float ya[3] = {0.f, 0.f, 0.f}, yb[3] = {0.f, 0.f, 0.f};
     for (int cb = 0; cb < C; cb += 32) {
       const int kc = min(32, C - cb);
-      const bool iso = stage_chunk(w, a.csr_idx, a.rec, lo + cb, kc, lane, xref, yref, zref, tau2);
+      const bool iso = stage_chunk(w, a.lrec, lo + cb, kc, lane, xref, yref, zref, tau2);
       uint2 cm;
       eval_any<false>(w, iso, wi.count > 32, kc, xa, xb, tau2, ya, yb, cm, lane);
     }

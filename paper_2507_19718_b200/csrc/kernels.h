@@ -84,12 +84,13 @@ void launch_scan(uint32_t* cnt, int64_t n, int ch, uint2* state, uint32_t* total
 // atomics nor the fp64 membership tests of the common case.
 struct CullBufs {
   float4* rec; uint4* range; double* rad2; uint32_t* count; uint32_t* rank; uint32_t* ovf; uint32_t ovf_cap;
+  float4* lrec;         // [cap][4] the culling lists: per entry the record (3 x float4) + (gid, 0, 0, 0)
 };
 void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& g, CullBufs cb, DevState* st,
                         cudaStream_t s);
 // host_total (page-locked, nullable): receives the rebuild's entry count (written by the kernel)
 void launch_cull_emit(int64_t G, CullBufs cb, const float* P, const LevelGeom& g, const uint32_t* off,
-                      int32_t* idx, uint32_t cap, DevState* st, const uint32_t* total, uint32_t* host_total,
+                      uint32_t cap, DevState* st, const uint32_t* total, uint32_t* host_total,
                       cudaStream_t s, Profiler* prof);
 
 // ingest.cu
@@ -113,7 +114,7 @@ void launch_levels_of(const uint2* kr, int64_t S, const LevelGeom& g, int32_t* o
 // fwdbwd.cu
 struct FitArgs {
   const WorkItem* work; const uint32_t* n_work;
-  const uint32_t* csr_off; const int32_t* csr_idx; const float4* rec;
+  const uint32_t* csr_off; const float4* lrec;
   const float4* bin;
   float* grad;          // [G][12]
   double* partial;      // [grid][kMaxL + 2]: per-block loss sums, pairs, candidates
@@ -125,7 +126,7 @@ int fwdbwd_grid();
 void launch_fwdbwd(const FitArgs& a, int grid, cudaStream_t s, Profiler* prof);
 struct QueryArgs {
   const WorkItem* work; const uint32_t* n_work;
-  const uint32_t* csr_off; const int32_t* csr_idx; const float4* rec;
+  const uint32_t* csr_off; const float4* lrec;
   const float4* bin;
   float* out; float tau2;
   const float* att; const float* beta; const float* unb;   // optional f3 epilogue (caller order)
