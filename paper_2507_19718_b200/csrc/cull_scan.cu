@@ -120,6 +120,7 @@ __device__ __forceinline__ void load8(const uint32_t* cnt, int64_t n, int64_t ba
   }
 }
 
+static_assert(kRep == 8, "a scan thread owns one cell's 8 replica counters");
 // ch > 0: sample bins, whose counts come as kRep replicas per cell (one thread's 8 items =
 // one cell, so that work items of <= ch samples are cut per cell); ch == 0: plain counts.
 __device__ __forceinline__ uint2 sum8(const uint32_t c[8], int ch) {

@@ -24,6 +24,8 @@ namespace gsc {
 constexpr int kWarps = 8;                                 // warps per CTA
 constexpr int kPairCap = 512;                             // pair batch of the dense fallback path
 constexpr int kMaskChunks = 12;                           // chunks whose inside masks are kept (C <= 384)
+constexpr uint32_t kClaimFit = 1, kClaimQuery = 2;        // work items per claim (measured: the
+                                                          // lookups' lighter items gain from 2, fwd/bwd's tail loses)
 constexpr float kNegHalfLog2e = -0.72134752044448170f;    // -0.5 * log2(e)
 static_assert(kCH == 64, "two samples per lane");
 
@@ -495,10 +497,16 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
   uint32_t* next = const_cast<uint32_t*>(a.n_work) + 1;   // dynamic work counter (zeroed by the scan)
   const float tau2 = a.tau2, eps = a.hdr_eps;
 
+  uint32_t claim = 0, left = 0;          // items are claimed kClaimFit at a time (fewer contended atomics)
   for (;;) {
-    uint32_t it = 0;
-    if (lane == 0) it = atomicAdd(next, 1u);
-    it = __shfl_sync(0xffffffffu, it, 0);
+    if (left == 0) {
+      uint32_t c0 = 0;
+      if (lane == 0) c0 = atomicAdd(next, kClaimFit);
+      claim = __shfl_sync(0xffffffffu, c0, 0);
+      left = kClaimFit;
+    }
+    const uint32_t it = claim++;
+    --left;
     if (it >= n_work) break;
     const WorkItem wi = a.work[it];
     const int lo = (int)__ldg(a.csr_off + wi.cell);
@@ -551,7 +559,10 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
     if (np == 0) continue;
     // ---------------- pass 2
     if (masked) {
-      for (int cb = 0, c = 0; cb < C; cb += 32, ++c) {
+      // last chunk first: pass 1 left it staged, so only the earlier chunks are re-staged
+      const int nch = (C + 31) >> 5;
+      for (int c = nch - 1; c >= 0; --c) {
+        const int cb = 32 * c;
         const uint2 mk = w.u.mask[c][lane];
         const int nk = __popc(mk.x) + __popc(mk.y);
         int incl = nk;
@@ -562,7 +573,7 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
         }
         const int P = __shfl_sync(0xffffffffu, incl, 31);
         if (P == 0) continue;
-        if (C > 32) iso = stage_chunk(w, a.lrec, lo + cb, min(32, C - cb), lane, xref, yref, zref, tau2);
+        if (c != nch - 1) iso = stage_chunk(w, a.lrec, lo + cb, 32, lane, xref, yref, zref, tau2);
         w.offs[lane] = incl - nk;
         __syncwarp();
         if (wi.count > 32) {
@@ -645,10 +656,16 @@ __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
   const uint32_t n_work = a.n_work[0];
   uint32_t* next = const_cast<uint32_t*>(a.n_work) + 1;   // dynamic work counter (zeroed by the scan)
   const float tau2 = a.tau2;
+  uint32_t claim = 0, left = 0;          // items are claimed kClaimQuery at a time (fewer contended atomics)
   for (;;) {
-    uint32_t it = 0;
-    if (lane == 0) it = atomicAdd(next, 1u);
-    it = __shfl_sync(0xffffffffu, it, 0);
+    if (left == 0) {
+      uint32_t c0 = 0;
+      if (lane == 0) c0 = atomicAdd(next, kClaimQuery);
+      claim = __shfl_sync(0xffffffffu, c0, 0);
+      left = kClaimQuery;
+    }
+    const uint32_t it = claim++;
+    --left;
     if (it >= n_work) break;
     const WorkItem wi = a.work[it];
     const int lo = (int)__ldg(a.csr_off + wi.cell);
