@@ -2,18 +2,21 @@
 // forward-only lookup kernel of gc_query (A7).  Warp-centric: no block barriers.
 //
 // A work item is <= 64 binned samples of one (level, cell) bin; one warp owns it, every lane
-// two samples (s = lane, lane + 32) so that each staged candidate feeds two evaluations.
-// The cell's culling list (C8) is staged into the warp's shared memory 32 candidates at a
-// time, recentred on the item's first sample.
+// two samples (s = lane, lane + 32; one when the item has <= 32) so that each staged
+// candidate feeds two evaluations, run as packed fp32x2 (FADD2/FMUL2/FFMA2) issues.  The
+// cell's culling list (C8: 64-B entries, record + Gaussian index) is staged into the warp's
+// shared memory 32 candidates at a time, recentred on the item's first sample.
 //   pass 1 (lane = sample pair): yhat = sum v_j e^{-Q/2} over the candidates with
-//          Q <= tau^2 (C3); every inside pair (candidate, sample, e) is appended to a
-//          candidate-major pair list (ballot + popc ranks); the Eq. 4 loss and g = dL/dyhat
-//          (C4, unnormalised -- the 1/(3 k_l) factor is applied by the optimizer once k_l is
-//          known globally, C9).
-//   pass 2 (lane = contributing pair): the 12 coefficient-gradient terms of C5 per pair, a
-//          <= 2-level segmented warp-shuffle scan over each Gaussian's run of pairs, and
-//          red.global.add.v4.f32 from every 4th lane of a run.  Work is proportional to the
-//          contributing pairs; never shared-memory float atomics (a CAS loop on sm_100a).
+//          Q <= tau^2 (C3); lane k keeps candidate k's inside ballots (which samples it
+//          covers); the Eq. 4 loss and g = dL/dyhat (C4, unnormalised -- the 1/(3 k_l)
+//          factor is applied by the optimizer once k_l is known globally, C9).
+//   pass 2 (lane = slice of contributing pairs): per chunk, the pairs in candidate-major
+//          order are cut into 32 contiguous slices; a lane walks its slice through the
+//          ballots, recomputes e with pass 1's arithmetic, accumulates the C5 coefficient
+//          gradients of the current Gaussian in registers and issues red.global.add.v4.f32
+//          at each change of Gaussian.  Work is proportional to the contributing pairs;
+//          never shared-memory float atomics (a CAS loop on sm_100a).  Cells with more than
+//          384 candidates re-derive their pairs in batches (dense fallback).
 #include <type_traits>
 #include "common.cuh"
 #include "kernels.h"
