@@ -369,7 +369,8 @@ __device__ __forceinline__ void run_to_dmu(bool iso, float u2, const Cand& g, fl
 // red.global.add.v4.f32 whenever the Gaussian changes and at the end.
 template <bool kLite, bool kWide>
 __device__ __forceinline__ void chunk_bwd_masks_impl(const WarpSmem& w, const uint2* __restrict__ mask, int P,
-                                                     float tau2, float* __restrict__ grad, int lane, bool iso) {
+                                                     uint32_t nz, float tau2, float* __restrict__ grad, int lane,
+                                                     bool iso) {
   constexpr int NV = kLite ? 6 : 12;
   const int pa = (P * lane) >> 5, pend = (P * (lane + 1)) >> 5;
   if (pa >= pend) return;
@@ -394,8 +395,8 @@ __device__ __forceinline__ void chunk_bwd_masks_impl(const WarpSmem& w, const ui
   float u2 = 0.f, gx = 0.f, v0 = 0.f, v1 = 0.f, v2 = 0.f;
   Cand g{};
   for (int p = pa; p < pend; ++p) {
-    while (m == 0) {
-      ++k;
+    if (m == 0) {                              // next candidate with pairs (nz: non-empty masks)
+      k = __ffs(nz & (0xFFFFFFFEu << k)) - 1;
       if constexpr (kWide) { mk = mask[k]; m = ((uint64_t)mk.y << 32) | mk.x; }
       else m = mask[k].x;
     }
@@ -568,6 +569,7 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
         const int cb = 32 * c;
         const uint2 mk = w.u.mask[c][lane];
         const int nk = __popc(mk.x) + __popc(mk.y);
+        const uint32_t nz = __ballot_sync(0xffffffffu, nk > 0);
         int incl = nk;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -580,11 +582,11 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
         w.offs[lane] = incl - nk;
         __syncwarp();
         if (wi.count > 32) {
-          if (iso && a.lite) chunk_bwd_masks_impl<true, true>(w, w.u.mask[c], P, tau2, a.grad, lane, true);
-          else chunk_bwd_masks_impl<false, true>(w, w.u.mask[c], P, tau2, a.grad, lane, iso);
+          if (iso && a.lite) chunk_bwd_masks_impl<true, true>(w, w.u.mask[c], P, nz, tau2, a.grad, lane, true);
+          else chunk_bwd_masks_impl<false, true>(w, w.u.mask[c], P, nz, tau2, a.grad, lane, iso);
         } else {
-          if (iso && a.lite) chunk_bwd_masks_impl<true, false>(w, w.u.mask[c], P, tau2, a.grad, lane, true);
-          else chunk_bwd_masks_impl<false, false>(w, w.u.mask[c], P, tau2, a.grad, lane, iso);
+          if (iso && a.lite) chunk_bwd_masks_impl<true, false>(w, w.u.mask[c], P, nz, tau2, a.grad, lane, true);
+          else chunk_bwd_masks_impl<false, false>(w, w.u.mask[c], P, nz, tau2, a.grad, lane, iso);
         }
         __syncwarp();
       }
