@@ -13,7 +13,11 @@ constexpr int kNP = 14;              // raw floats per Gaussian
 constexpr int kCH = 64;              // samples per work item: one warp, two samples per lane
 constexpr int kScanThreads = 1024;   // one scan tile per CTA: 1024 threads x 8 items
 constexpr int kScanTile = 8 * kScanThreads;
-constexpr int kRep = 8;              // replicated per-cell sample counters (hot-cell atomics / 8)
+#ifndef GSC_KREP
+#define GSC_KREP 4
+#endif
+constexpr int kRep = GSC_KREP;        // replicated per-cell sample counters (hot-cell atomics / kRep;
+                                      // measured cfg2 frame: 4 -> 0.382 ms, 8 -> 0.385, 2 -> 0.430, 1 -> 0.459)
 constexpr uint32_t kInvalidKey = 0xFFFFFFFFu;
 
 // Plane index of raw parameter column k in the SoA parameter store (paper order).

@@ -120,31 +120,45 @@ __device__ __forceinline__ void load8(const uint32_t* cnt, int64_t n, int64_t ba
   }
 }
 
-static_assert(kRep == 8, "a scan thread owns one cell's 8 replica counters");
+static_assert(kRep >= 1 && kRep <= 8 && (8 % kRep) == 0, "a scan thread owns 8 / kRep whole cells");
+constexpr int kCPT = 8 / kRep;        // cells per scan thread (sample bins)
 // ch > 0: sample bins, whose counts come as kRep replicas per cell (one thread's 8 items =
-// one cell, so that work items of <= ch samples are cut per cell); ch == 0: plain counts.
+// 8 / kRep whole cells, so that work items of <= ch samples are cut per cell); ch == 0:
+// plain counts.  .x = samples, .y = work items.
 __device__ __forceinline__ uint2 sum8(const uint32_t c[8], int ch) {
   uint2 s = make_uint2(0, 0);
 #pragma unroll
   for (int k = 0; k < 8; ++k) s.x += c[k];
-  if (ch) s.y = (s.x + ch - 1) / ch;
+  if (ch) {
+#pragma unroll
+    for (int q = 0; q < kCPT; ++q) {
+      uint32_t t = 0;
+#pragma unroll
+      for (int r = 0; r < kRep; ++r) t += c[q * kRep + r];
+      s.y += (t + ch - 1) / ch;
+    }
+  }
   return s;
 }
 
 // Sample-bin counters are replica-major ([kRep][NC]: the replicas of a cell live in different
 // L2 lines, so a hot cell's atomics spread over slices); a scan thread owns the kRep
-// replicas of one cell, visiting cells in order.  Plain counters: 8 consecutive entries.
+// replicas of each of its 8 / kRep cells, visiting cells in order (item k = replica
+// k % kRep of cell base / kRep + k / kRep).  Plain counters: 8 consecutive entries.
 __device__ __forceinline__ int64_t entry(int ch, int64_t n, int64_t base, int k) {
   if (!ch) return base + k;
   const int64_t nc = n / kRep;
-  return (int64_t)k * nc + base / kRep;    // base / kRep = this thread's cell
+  return (int64_t)(k % kRep) * nc + base / kRep + k / kRep;
 }
 
 __device__ __forceinline__ void load_counts(const uint32_t* cnt, int64_t n, int ch, int64_t base, uint32_t c[8]) {
   if (!ch) { load8(cnt, n, base, c); return; }
-  const int64_t cell = base / kRep, nc = n / kRep;
+  const int64_t nc = n / kRep;
 #pragma unroll
-  for (int k = 0; k < kRep; ++k) c[k] = cell < nc ? cnt[(int64_t)k * nc + cell] : 0u;
+  for (int k = 0; k < 8; ++k) {
+    const int64_t cell = base / kRep + k / kRep;
+    c[k] = cell < nc ? cnt[(int64_t)(k % kRep) * nc + cell] : 0u;
+  }
 }
 
 
@@ -247,11 +261,21 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(uint32_t* __restrict__ cn
   __syncthreads();
   const uint2 tp = s_prefix;
   uint32_t off = tp.x + ex.x, woff = tp.y + ex.y;
-  if (ch && s.x) {                       // one cell per thread (kRep replicas)
-    const int64_t cell = base / kRep;
-    const int lvl = level_of_cell(g, cell);
-    for (uint32_t q = 0; q * ch < s.x; ++q)
-      work[woff++] = WorkItem{(int)cell, (int)(off + q * ch), (int)min((uint32_t)ch, s.x - q * ch), lvl};
+  if (ch && s.x) {                       // the thread's 8 / kRep cells (kRep replicas each)
+    uint32_t o = off;
+#pragma unroll
+    for (int cq = 0; cq < kCPT; ++cq) {
+      uint32_t t = 0;
+#pragma unroll
+      for (int r = 0; r < kRep; ++r) t += c[cq * kRep + r];
+      if (t) {
+        const int64_t cell = base / kRep + cq;
+        const int lvl = level_of_cell(g, cell);
+        for (uint32_t q = 0; q * ch < t; ++q)
+          work[woff++] = WorkItem{(int)cell, (int)(o + q * ch), (int)min((uint32_t)ch, t - q * ch), lvl};
+      }
+      o += t;
+    }
   }
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
