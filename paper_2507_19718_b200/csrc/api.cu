@@ -412,8 +412,8 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
     double *dbar = nullptr, *capfl = nullptr;
     CK(dalloc(&dbar, N0)); CK(dalloc(&capfl, 2));
     for (int l = 0; l < L; ++l)
-      launch_eq2_level(c->P, G, c->geom.goff[l], counts[l], dbar, capfl, (double)c->hp.init_zcap,
-                       (double)c->hp.init_scale_factor, c->P, s);
+      CK(launch_eq2_level(c->P, G, c->geom.goff[l], counts[l], dbar, capfl, (double)c->hp.init_zcap,
+                          (double)c->hp.init_scale_factor, c->P, s));
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     cudaFree(dbar); cudaFree(capfl);

@@ -1,6 +1,10 @@
 // create.cu -- gc_create's device work (C7): gather of the nested level subsets, Eq. 2
-// initial scales from a brute-force fp64 3-NN search, and the pack/unpack of the
-// paper-order parameter layout used by gc_params / gc_set_params.
+// initial scales from an exact fp64 3-NN search over a uniform grid, and the
+// pack/unpack of the paper-order parameter layout used by gc_params / gc_set_params.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -22,46 +26,206 @@ __global__ void k_gather_init(int64_t N0, const float* __restrict__ pos, const f
   }
 }
 
-// dbar_i = mean distance to the 3 nearest other points of the level (fp64, no contraction,
-// comparisons in the oracle's order so the distances and their mean are bit-identical).
-__global__ void __launch_bounds__(256) k_knn3(const float* __restrict__ P, int64_t G, int64_t base,
-                                              int64_t n, double* dbar) {
-  __shared__ double sx[256], sy[256], sz[256];
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  double xi = 0, yi = 0, zi = 0;
-  if (i < n) { xi = P[P_MU * G + base + i]; yi = P[(P_MU + 1) * G + base + i]; zi = P[(P_MU + 2) * G + base + i]; }
-  double b0 = INFINITY, b1 = INFINITY, b2 = INFINITY;
-  for (int64_t t0 = 0; t0 < n; t0 += 256) {
-    __syncthreads();
-    const int64_t jl = t0 + threadIdx.x;
-    if (jl < n) {
-      sx[threadIdx.x] = P[P_MU * G + base + jl]; sy[threadIdx.x] = P[(P_MU + 1) * G + base + jl];
-      sz[threadIdx.x] = P[(P_MU + 2) * G + base + jl];
+// dbar_i = mean distance to the 3 nearest other points of the level (Eq. 2).
+// Exact k-NN over a uniform grid (sub-quadratic, next row f2): the level's points are binned
+// into ~n/2 cells, then each point visits cells in Chebyshev shells r = 0, 1, 2, ... around
+// its own and stops once its third-smallest squared distance lies strictly below the squared
+// distance to the unvisited region (minus a slack far above the rounding of the cell bounds),
+// so the three smallest squared distances are those of the brute-force search.  They are
+// computed in fp64 with the oracle's operation sequence (no contraction) and ranked by value:
+// the multiset of the three smallest values, hence their square roots and mean summed in
+// ascending order, are bit-identical to the oracle whatever the visiting order.
+
+__global__ void __launch_bounds__(1024) k_knn_bbox(const float* __restrict__ P, int64_t G, int64_t base,
+                                                   int64_t n, float* box /*lo[3], hi[3]*/) {
+  __shared__ float slo[3][32], shi[3][32];
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float v = P[(P_MU + a) * G + base + i];
+      lo[a] = fminf(lo[a], v); hi[a] = fmaxf(hi[a], v);
     }
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+      hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+    }
+  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (ln == 0)
+    for (int a = 0; a < 3; ++a) { slo[a][w] = lo[a]; shi[a][w] = hi[a]; }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    float l = INFINITY, h = -INFINITY;
+    for (int k = 0; k < nw; ++k) { l = fminf(l, slo[threadIdx.x][k]); h = fmaxf(h, shi[threadIdx.x][k]); }
+    box[threadIdx.x] = l; box[3 + threadIdx.x] = h;
+  }
+}
+
+struct KnnGrid {
+  double lo[3], inv[3], edge[3];
+  int dims[3];
+};
+
+__device__ __forceinline__ int knn_cell_axis(double x, const KnnGrid& g, int a) {
+  const int c = (int)__dmul_rn(__dsub_rn(x, g.lo[a]), g.inv[a]);
+  return c < 0 ? 0 : (c >= g.dims[a] ? g.dims[a] - 1 : c);
+}
+
+__global__ void k_knn_count(const float* __restrict__ P, int64_t G, int64_t base, int64_t n, KnnGrid g,
+                            int32_t* __restrict__ cell_of, uint32_t* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int cx = knn_cell_axis(P[P_MU * G + base + i], g, 0);
+    const int cy = knn_cell_axis(P[(P_MU + 1) * G + base + i], g, 1);
+    const int cz = knn_cell_axis(P[(P_MU + 2) * G + base + i], g, 2);
+    const int q = (cz * g.dims[1] + cy) * g.dims[0] + cx;
+    cell_of[i] = q;
+    atomicAdd(&cnt[q], 1u);
+  }
+}
+
+// exclusive scan of the cell counts into start[0..cells] (one block: create-time only)
+__global__ void __launch_bounds__(1024) k_knn_scan(const uint32_t* __restrict__ cnt, int64_t cells,
+                                                   uint32_t* __restrict__ start) {
+  __shared__ uint32_t part[1024];
+  const int64_t per = (cells + blockDim.x - 1) / blockDim.x;
+  const int64_t b = threadIdx.x * per, e = b + per < cells ? b + per : cells;
+  uint32_t t = 0;
+  for (int64_t k = b; k < e; ++k) t += cnt[k];
+  part[threadIdx.x] = t;
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+    const uint32_t v = threadIdx.x >= (unsigned)o ? part[threadIdx.x - o] : 0u;
     __syncthreads();
-    const int m = (int)((n - t0) < 256 ? (n - t0) : 256);
-    if (i < n) {
-      for (int k = 0; k < m; ++k) {
-        if (t0 + k == i) continue;
-        const double dx = __dsub_rn(sx[k], xi), dy = __dsub_rn(sy[k], yi), dz = __dsub_rn(sz[k], zi);
-        // squared distances are ranked (the correctly rounded sqrt is monotone, so the three
-        // smallest distances are the square roots of the three smallest squares: exact)
-        const double d = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-        if (d < b2) {
-          if (d < b1) { b2 = b1; if (d < b0) { b1 = b0; b0 = d; } else { b1 = d; } }
-          else b2 = d;
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  uint32_t run = part[threadIdx.x] - t;
+  for (int64_t k = b; k < e; ++k) { start[k] = run; run += cnt[k]; }
+  if (threadIdx.x == blockDim.x - 1) start[cells] = part[threadIdx.x];
+}
+
+__global__ void k_knn_scatter(const float* __restrict__ P, int64_t G, int64_t base, int64_t n,
+                              const int32_t* __restrict__ cell_of, const uint32_t* __restrict__ start,
+                              uint32_t* __restrict__ fill, float4* __restrict__ sorted) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int q = cell_of[i];
+    const uint32_t k = start[q] + atomicAdd(&fill[q], 1u);
+    sorted[k] = make_float4(P[P_MU * G + base + i], P[(P_MU + 1) * G + base + i], P[(P_MU + 2) * G + base + i],
+                            __int_as_float((int)i));
+  }
+}
+
+// one thread per sorted slot (neighbouring threads share cells), dbar written at the point's index
+__global__ void __launch_bounds__(256) k_knn3_grid(const float4* __restrict__ sorted, int64_t n,
+                                                   const uint32_t* __restrict__ start, KnnGrid g,
+                                                   double slack, double* __restrict__ dbar) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const float4 me = sorted[t];
+  const int i = __float_as_int(me.w);
+  const double xi = me.x, yi = me.y, zi = me.z;
+  const int c[3] = {knn_cell_axis(xi, g, 0), knn_cell_axis(yi, g, 1), knn_cell_axis(zi, g, 2)};
+  const double pt[3] = {xi, yi, zi};
+  double b0 = INFINITY, b1 = INFINITY, b2 = INFINITY;
+  const int rmax = max(g.dims[0], max(g.dims[1], g.dims[2]));
+  for (int r = 0; r <= rmax; ++r) {
+    const int z0 = max(0, c[2] - r), z1 = min(g.dims[2] - 1, c[2] + r);
+    const int y0 = max(0, c[1] - r), y1 = min(g.dims[1] - 1, c[1] + r);
+    for (int z = z0; z <= z1; ++z)
+      for (int y = y0; y <= y1; ++y) {
+        // a face row of the shell visits every x of the cube; an inner row only its two ends
+        const bool face = abs(z - c[2]) == r || abs(y - c[1]) == r;
+        const int xa = c[0] - r, xb = c[0] + r;
+        const int x0 = face ? max(0, xa) : xa, x1 = face ? min(g.dims[0] - 1, xb) : xb;
+        const int step = face ? 1 : 2 * r;
+        for (int x = x0; x <= x1; x += step) {
+          if (x < 0 || x >= g.dims[0]) continue;
+          const int q = (z * g.dims[1] + y) * g.dims[0] + x;
+          for (uint32_t k = start[q], ke = start[q + 1]; k < ke; ++k) {
+            const float4 o = sorted[k];
+            if (__float_as_int(o.w) == i) continue;
+            const double dx = __dsub_rn((double)o.x, xi), dy = __dsub_rn((double)o.y, yi), dz = __dsub_rn((double)o.z, zi);
+            const double d = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+            if (d < b2) {
+              if (d < b1) { b2 = b1; if (d < b0) { b1 = b0; b0 = d; } else { b1 = d; } }
+              else b2 = d;
+            }
+          }
         }
       }
+    // distance from the point to the region outside the visited (2r+1)^3 cube
+    double bound = INFINITY;
+    for (int a = 0; a < 3; ++a) {
+      if (c[a] - r > 0) bound = fmin(bound, pt[a] - (g.lo[a] + (c[a] - r) * g.edge[a]));
+      if (c[a] + r < g.dims[a] - 1) bound = fmin(bound, (g.lo[a] + (c[a] + r + 1) * g.edge[a]) - pt[a]);
     }
+    if (bound == INFINITY) break;                   // the whole grid has been visited
+    bound -= slack;
+    if (bound > 0.0 && b2 < bound * bound) break;   // nothing unvisited can enter the top 3
   }
-  if (i < n) {
-    const int k = (int)((n - 1) < 3 ? (n - 1) : 3);
-    double s = 0.0;
-    if (k >= 1) s = __dadd_rn(s, __dsqrt_rn(b0));
-    if (k >= 2) s = __dadd_rn(s, __dsqrt_rn(b1));
-    if (k >= 3) s = __dadd_rn(s, __dsqrt_rn(b2));
-    dbar[i] = k > 0 ? __ddiv_rn(s, (double)k) : 0.0;
+  const int k = (int)((n - 1) < 3 ? (n - 1) : 3);
+  double s = 0.0;
+  if (k >= 1) s = __dadd_rn(s, __dsqrt_rn(b0));
+  if (k >= 2) s = __dadd_rn(s, __dsqrt_rn(b1));
+  if (k >= 3) s = __dadd_rn(s, __dsqrt_rn(b2));
+  dbar[i] = k > 0 ? __ddiv_rn(s, (double)k) : 0.0;
+}
+
+static cudaError_t knn3_level(const float* P, int64_t G, int64_t base, int64_t n, double* dbar, cudaStream_t s) {
+  float* box = nullptr;
+  cudaError_t e = cudaMalloc(&box, 6 * sizeof(float));
+  if (e != cudaSuccess) return e;
+  k_knn_bbox<<<1, 1024, 0, s>>>(P, G, base, n, box);
+  float hb[6];
+  e = cudaMemcpyAsync(hb, box, sizeof(hb), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(box);
+  if (e != cudaSuccess) return e;
+  KnnGrid g;
+  double ext[3], diag2 = 0.0;
+  for (int a = 0; a < 3; ++a) { g.lo[a] = hb[a]; ext[a] = (double)hb[3 + a] - (double)hb[a]; diag2 += ext[a] * ext[a]; }
+  const double diag = std::sqrt(diag2);
+  // cell edge: ~2 points per cell of the (floored) bounding volume, total cells <= 2n + 8
+  const int64_t cap = 2 * n + 8;
+  double vol = 1.0;
+  for (int a = 0; a < 3; ++a) vol *= std::max(ext[a], 1e-3 * diag);
+  double edge = diag > 0.0 ? std::cbrt(vol / (0.5 * (double)n)) : 1.0;
+  for (int it = 0; it < 400; ++it) {
+    int64_t prod = 1;
+    for (int a = 0; a < 3; ++a) {
+      g.dims[a] = ext[a] > 0.0 ? (int)std::max(1.0, std::min(1024.0, std::ceil(ext[a] / edge))) : 1;
+      prod *= g.dims[a];
+    }
+    if (prod <= cap) break;
+    edge *= 1.25;
   }
+  for (int a = 0; a < 3; ++a) {
+    g.inv[a] = ext[a] > 0.0 ? (double)g.dims[a] / ext[a] : 0.0;
+    g.edge[a] = ext[a] > 0.0 ? ext[a] / (double)g.dims[a] : 0.0;
+  }
+  const int64_t cells = (int64_t)g.dims[0] * g.dims[1] * g.dims[2];
+  int32_t* cell_of = nullptr;
+  uint32_t *cnt = nullptr, *start = nullptr;
+  float4* sorted = nullptr;
+  if ((e = cudaMalloc(&cell_of, sizeof(int32_t) * n)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&cnt, sizeof(uint32_t) * cells)) == cudaSuccess &&
+      (e = cudaMalloc(&start, sizeof(uint32_t) * (cells + 1))) == cudaSuccess &&
+      (e = cudaMalloc(&sorted, sizeof(float4) * n)) == cudaSuccess &&
+      (e = cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * cells, s)) == cudaSuccess) {
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16));
+    k_knn_count<<<nb, 256, 0, s>>>(P, G, base, n, g, cell_of, cnt);
+    k_knn_scan<<<1, 1024, 0, s>>>(cnt, cells, start);
+    cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * cells, s);
+    k_knn_scatter<<<nb, 256, 0, s>>>(P, G, base, n, cell_of, start, cnt, sorted);
+    // slack: 1e-9 of the diagonal, orders of magnitude above the rounding of lo + c * edge
+    k_knn3_grid<<<(int)((n + 255) / 256), 256, 0, s>>>(sorted, n, start, g, 1e-9 * diag, dbar);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  }
+  cudaFree(cell_of); cudaFree(cnt); cudaFree(start); cudaFree(sorted);
+  return e;
 }
 
 // One thread, sequential in index order (same rounding sequence as the oracle): mean and
@@ -127,11 +291,14 @@ void launch_gather_init(int64_t N0, const float* pos, const float* rgb, const fl
   k_gather_init<<<blocks_for(G), 256, 0, s>>>(N0, pos, rgb, log_scale, src, G, P, opacity_logit);
 }
 
-void launch_eq2_level(const float* P, int64_t G, int64_t base, int64_t n, double* dbar, double* capfl,
-                      double zcap, double factor, float* Pw, cudaStream_t s) {
-  k_knn3<<<(int)((n + 255) / 256), 256, 0, s>>>(P, G, base, n, dbar);
+cudaError_t launch_eq2_level(const float* P, int64_t G, int64_t base, int64_t n, double* dbar, double* capfl,
+                             double zcap, double factor, float* Pw, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const cudaError_t e = knn3_level(P, G, base, n, dbar, s);
+  if (e != cudaSuccess) return e;
   k_eq2_stats<<<1, 32, 0, s>>>(P, G, base, n, dbar, zcap, capfl);
   k_eq2_apply<<<blocks_for(n), 256, 0, s>>>(n, dbar, capfl, factor, Pw, G, base);
+  return cudaGetLastError();
 }
 
 void launch_pack(const float* P, int64_t G, int64_t base, int64_t n, float* out, cudaStream_t s) {

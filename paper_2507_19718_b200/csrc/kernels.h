@@ -148,8 +148,8 @@ void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, CullBufs
 // create.cu
 void launch_gather_init(int64_t N0, const float* pos, const float* rgb, const float* log_scale,
                         const int64_t* src, int64_t G, float* P, float opacity_logit, cudaStream_t s);
-void launch_eq2_level(const float* P, int64_t G, int64_t base, int64_t n, double* dbar, double* capfl,
-                      double zcap, double factor, float* Pw, cudaStream_t s);
+cudaError_t launch_eq2_level(const float* P, int64_t G, int64_t base, int64_t n, double* dbar, double* capfl,
+                             double zcap, double factor, float* Pw, cudaStream_t s);
 void launch_pack(const float* P, int64_t G, int64_t base, int64_t n, float* out14, cudaStream_t s);
 void launch_unpack(const float* in14, int64_t G, int64_t base, int64_t n, float* P, cudaStream_t s);
 

@@ -77,6 +77,31 @@ def test_create_layout_bit_exact(gsc):
     assert ulp.max() <= 2, ulp.max()                                 # Eq. 2 log-scales
 
 
+@pytest.mark.parametrize("shape", ["mixed", "planar"])
+def test_create_grid_knn_matches_brute_force(gsc, shape):
+    """Eq. 2 through the grid 3-NN on clustered / planar / duplicated / outlying
+    points: every level's initial log-scale within 2 ulp of the oracle's O(N^2) fp64 search
+    (no z-score cap, so each point's own 3-NN mean decides its scale)."""
+    r = np.random.default_rng(5)
+    if shape == "mixed":
+        blobs = r.normal(scale=0.02, size=(12000, 3)) + r.uniform(-1, 1, (40, 3)).repeat(300, 0)
+        sheet = np.c_[r.uniform(-1, 1, (8000, 2)), np.full(8000, 0.3)]
+        dup = np.repeat(r.uniform(-1, 1, (500, 3)), 2, 0)              # exact duplicates
+        far = r.uniform(-40, 40, (20, 3))                               # outliers: sparse grid cells
+        pos = np.concatenate([blobs, sheet, dup, far])
+    else:                                                               # zero-extent z axis
+        pos = np.c_[r.uniform(-2, 3, (15000, 2)), np.zeros(15000)]
+    pos = pos[r.permutation(len(pos))].astype(np.float32)
+    alb = r.uniform(0, 1, pos.shape).astype(np.float32)
+    counts = [len(pos), len(pos) // 7]
+    c = gsc.GSCache(counts, cuda(pos), cuda(alb), seed=4, hparams=dict(init_zcap=1e6))
+    Po = oracle.create(counts, pos.astype(np.float64), alb.astype(np.float64), seed=4,
+                       init_opacity=F32(0.1), zcap=1e6, factor=0.5)
+    g = rows(c)[:, 10:13].astype(np.float32).view(np.int32).astype(np.int64)
+    o = Po[:, 10:13].astype(np.float32).view(np.int32).astype(np.int64)
+    assert np.abs(g - o).max() <= 2, np.abs(g - o).max()
+
+
 def test_create_with_given_scales_exact(gsc):
     pos, alb = workload.init_cloud(1)
     ls = np.log(np.random.default_rng(1).uniform(0.01, 0.03, (4096, 3))).astype(np.float32)
