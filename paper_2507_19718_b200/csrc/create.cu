@@ -228,25 +228,52 @@ static cudaError_t knn3_level(const float* P, int64_t G, int64_t base, int64_t n
   return e;
 }
 
-// One thread, sequential in index order (same rounding sequence as the oracle): mean and
-// population std of dbar, the level's AABB diagonal, then cap = mu + zcap * sigma.
-__global__ void k_eq2_stats(const float* __restrict__ P, int64_t G, int64_t base, int64_t n,
-                            const double* __restrict__ dbar, double zcap, double* out /*cap, floor*/) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double mu = 0.0;
-  for (int64_t i = 0; i < n; ++i) mu = __dadd_rn(mu, dbar[i]);
-  mu = __ddiv_rn(mu, (double)n);
-  double var = 0.0;
-  for (int64_t i = 0; i < n; ++i) { const double d = __dsub_rn(dbar[i], mu); var = __dadd_rn(var, __dmul_rn(d, d)); }
-  var = __ddiv_rn(var, (double)n);
-  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-  for (int64_t i = 0; i < n; ++i)
+// One CTA: mean and population std of dbar, the level's AABB diagonal, then
+// cap = mu + zcap * sigma.  Each thread sums the indices congruent to it mod the block size in
+// index order, then a fixed-shape tree combines the partials: deterministic, and within a
+// few fp64 ulp of the oracle's sequential sums (DESIGN A19); min / max are order-free.
+__device__ __forceinline__ double eq2_block_sum(double v, double* sh) {
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = blockDim.x >> 1; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + o]);
+    __syncthreads();
+  }
+  const double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(1024) k_eq2_stats(const float* __restrict__ P, int64_t G, int64_t base,
+                                                    int64_t n, const double* __restrict__ dbar, double zcap,
+                                                    double* out /*cap, floor*/) {
+  __shared__ double sh[1024];
+  __shared__ float sb[6][1024];
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc = __dadd_rn(acc, dbar[i]);
+  const double mu = __ddiv_rn(eq2_block_sum(acc, sh), (double)n);
+  acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double d = __dsub_rn(dbar[i], mu);
+    acc = __dadd_rn(acc, __dmul_rn(d, d));
+  }
+  const double var = __ddiv_rn(eq2_block_sum(acc, sh), (double)n);
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
     for (int a = 0; a < 3; ++a) {
-      const double v = P[(P_MU + a) * G + base + i];
-      if (v < lo[a]) lo[a] = v;
-      if (v > hi[a]) hi[a] = v;
+      const float v = P[(P_MU + a) * G + base + i];
+      lo[a] = fminf(lo[a], v); hi[a] = fmaxf(hi[a], v);
     }
-  const double dx = __dsub_rn(hi[0], lo[0]), dy = __dsub_rn(hi[1], lo[1]), dz = __dsub_rn(hi[2], lo[2]);
+  for (int a = 0; a < 3; ++a) { sb[a][threadIdx.x] = lo[a]; sb[3 + a][threadIdx.x] = hi[a]; }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double l[3], h[3];
+  for (int a = 0; a < 3; ++a) {
+    float fl = INFINITY, fh = -INFINITY;
+    for (int k = 0; k < (int)blockDim.x; ++k) { fl = fminf(fl, sb[a][k]); fh = fmaxf(fh, sb[3 + a][k]); }
+    l[a] = fl; h[a] = fh;
+  }
+  const double dx = __dsub_rn(h[0], l[0]), dy = __dsub_rn(h[1], l[1]), dz = __dsub_rn(h[2], l[2]);
   const double diag = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
   out[0] = __dadd_rn(mu, __dmul_rn(zcap, __dsqrt_rn(var)));
   out[1] = __dmul_rn(1e-6, diag);
@@ -296,7 +323,7 @@ cudaError_t launch_eq2_level(const float* P, int64_t G, int64_t base, int64_t n,
   if (n <= 0) return cudaSuccess;
   const cudaError_t e = knn3_level(P, G, base, n, dbar, s);
   if (e != cudaSuccess) return e;
-  k_eq2_stats<<<1, 32, 0, s>>>(P, G, base, n, dbar, zcap, capfl);
+  k_eq2_stats<<<1, 1024, 0, s>>>(P, G, base, n, dbar, zcap, capfl);
   k_eq2_apply<<<blocks_for(n), 256, 0, s>>>(n, dbar, capfl, factor, Pw, G, base);
   return cudaGetLastError();
 }
