@@ -102,6 +102,33 @@ def test_create_grid_knn_matches_brute_force(gsc, shape):
     assert np.abs(g - o).max() <= 2, np.abs(g - o).max()
 
 
+def test_create_cfg4_full_size_sampled(gsc):
+    """cfg4's create (6 levels, 1,048,576 level-0 points) in the bench's configuration: the
+    Eq. 2 log-scale of 192 sampled Gaussians per checked level equals, within 2 ulp,
+    the plain definition evaluated one point at a time (3 smallest fp64 squared distances to
+    every other point of the level, square roots summed in ascending order, / 3), then the
+    oracle's Eq. 2 with the level's diagonal floor (no z-score cap)."""
+    counts = workload.CONFIGS[4]["counts"]
+    pos, alb = workload.init_cloud(4)
+    c = gsc.GSCache(counts, cuda(pos), cuda(alb), seed=4, hparams=dict(init_zcap=1e6))
+    r = np.random.default_rng(9)
+    for l in (0, 2):
+        Pl = c.params_rows(l)
+        pts = Pl[:, 0:3].astype(np.float32).astype(np.float64)
+        idx = r.choice(len(pts), 192, replace=False)
+        dbar = np.empty(len(idx))
+        for k, i in enumerate(idx):
+            dx, dy, dz = pts[:, 0] - pts[i, 0], pts[:, 1] - pts[i, 1], pts[:, 2] - pts[i, 2]
+            d = dx * dx + dy * dy + dz * dz
+            d[i] = np.inf
+            b = np.sort(np.partition(d, 3)[:3])
+            dbar[k] = ((0.0 + np.sqrt(b[0])) + np.sqrt(b[1]) + np.sqrt(b[2])) / 3.0
+        s = oracle.eq2_from_dbar(dbar, oracle.diag(pts), zcap=1e6, factor=0.5)
+        want = np.log(s).astype(np.float32).view(np.int32).astype(np.int64)
+        got = Pl[idx, 10:13].astype(np.float32).view(np.int32).astype(np.int64)
+        assert np.abs(got - want[:, None]).max() <= 2, (l, np.abs(got - want[:, None]).max())
+
+
 def test_create_with_given_scales_exact(gsc):
     pos, alb = workload.init_cloud(1)
     ls = np.log(np.random.default_rng(1).uniform(0.01, 0.03, (4096, 3))).astype(np.float32)
