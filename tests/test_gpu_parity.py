@@ -391,6 +391,30 @@ def test_cfg2_full_size_sampled(gsc):
     assert np.isfinite(st.loss[:4]).all() and st.n_pairs > 0
 
 
+def test_cfg4_full_size_sampled(gsc):
+    """configs[4] at full size (6 levels, 1.4 M Gaussians, 16.8 M fit samples + 16.8 M
+    lookups): sampled query outputs against per-point brute force (120 points, the fp64 oracle
+    at ~50 ms each), level counts of the fit exact."""
+    pos, alb = workload.init_cloud(4)
+    counts = workload.CONFIGS[4]["counts"]
+    c = gsc.GSCache(counts, cuda(pos), cuda(alb), seed=4)
+    x, ln, rgb = workload.fit_batch(4)
+    xq, lq = workload.query_batch(4)
+    c.reserve(len(x), len(xq))
+    P = rows(c)
+    y = c.query(cuda(xq), cuda(lq)).cpu().numpy()
+    st = c.fit(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    idx = np.random.default_rng(8).choice(len(xq), 120, replace=False)
+    yo, lv, _ = oracle.query(c.goff, P, xq[idx].astype(np.float64), lq[idx])
+    check_forward(y[idx], yo, P, c.goff, xq[idx], lv, what="cfg4 sampled")
+    lvl = oracle.level_of(ln, len(counts), x.astype(np.float64), rgb.astype(np.float64))
+    for l in range(len(counts)):
+        assert st.count[l] == int((lvl == l).sum())
+    assert st.n_valid + st.n_dropped == len(x)
+    assert np.isfinite(st.loss[:len(counts)]).all() and st.n_pairs > 0
+
+
 def test_cfg2_full_size_bench_frame_call(gsc):
     """configs[2] at full size exactly as bench.py runs it: gc_fit_query with the deferred
     optimizer step, eager then as a replayed CUDA graph.  Each frame's sampled lookups match
