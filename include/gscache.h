@@ -96,7 +96,9 @@ void gc_default_hparams(gc_hparams* hp);
  *    P:72).  Level 0 takes the points in caller order; level l >= 1 takes the first counts[l]
  *    points of the permutation pi = stable argsort(splitmix64(seed + i)) (nested subsets, C7).
  *  init_log_scale [N0][3] (host or device) or NULL: NULL computes Eq. 2 per level:
- *    s_i = min(mu_N + zcap sigma_N, max(mean 3-NN distance, 1e-6 diag)) * factor, isotropic.
+ *    s_i = max(min(mu_N + zcap sigma_N, mean 3-NN distance), fl) * factor, isotropic, with
+ *    fl = 1e-6 diag (the level's AABB diagonal), or 1e-6 when diag = 0 (one point or all
+ *    points coincident: reading A20), so every log-scale is finite.
  *  Rotation (1,0,0,0), opacity logit ln(p/(1-p)), colour = albedo, AdamW moments 0, t = 0.
  *  hp: NULL = defaults.  On success *out receives the handle.  Synchronises the device. */
 gc_status gc_create(int levels, const int64_t* counts, const float* init_pos,

@@ -89,8 +89,11 @@ void orc_knn3_mean(int64_t n, const double* pts, double* dbar) {
   }
 }
 
-/* Eq. 2: s_i = min(mu_N + zcap*sigma_N, max(dbar_i, 1e-6*diag)) * factor
- * ("\land" read as min; sigma population, ddof 0; floor for duplicate points). */
+/* Eq. 2: s_i = max(min(mu_N + zcap*sigma_N, dbar_i), fl) * factor
+ * ("\land" read as min; sigma population, ddof 0; floor for duplicate points).
+ * fl = 1e-6*diag, or 1e-6 (world units) when diag = 0 -- a level of one point or of
+ * coincident points (reading A20): the floor is applied after the cap so that no level can
+ * produce s = 0 (ln s = -inf). */
 void orc_eq2_from_dbar(int64_t n, const double* dbar, double diag, double zcap, double factor,
                        double* s) {
   double mu = 0.0;
@@ -100,10 +103,10 @@ void orc_eq2_from_dbar(int64_t n, const double* dbar, double diag, double zcap, 
   for (int64_t i = 0; i < n; ++i) { double d = dbar[i] - mu; var = var + d * d; }
   var = var / (double)n;
   double cap = mu + zcap * sqrt(var);
-  double fl = 1e-6 * diag;
+  double fl = diag > 0.0 ? 1e-6 * diag : 1e-6;
   for (int64_t i = 0; i < n; ++i) {
-    double r = dbar[i] > fl ? dbar[i] : fl;
-    s[i] = (cap < r ? cap : r) * factor;
+    double r = cap < dbar[i] ? cap : dbar[i];
+    s[i] = (r > fl ? r : fl) * factor;
   }
 }
 

@@ -276,15 +276,16 @@ __global__ void __launch_bounds__(1024) k_eq2_stats(const float* __restrict__ P,
   const double dx = __dsub_rn(h[0], l[0]), dy = __dsub_rn(h[1], l[1]), dz = __dsub_rn(h[2], l[2]);
   const double diag = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
   out[0] = __dadd_rn(mu, __dmul_rn(zcap, __dsqrt_rn(var)));
-  out[1] = __dmul_rn(1e-6, diag);
-}
+  out[1] = diag > 0.0 ? __dmul_rn(1e-6, diag) : 1e-6;   // reading A20: degenerate level (one point /
+}                                                         // coincident points) -> absolute floor
 
 __global__ void k_eq2_apply(int64_t n, const double* __restrict__ dbar, const double* __restrict__ capfl,
                             double factor, float* P, int64_t G, int64_t base) {
   const double cap = capfl[0], fl = capfl[1];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double r = dbar[i] > fl ? dbar[i] : fl;
-    const double s = __dmul_rn(cap < r ? cap : r, factor);
+    // Eq. 2 with the floor applied after the cap (reading A20): s = max(min(cap, dbar), fl)
+    const double r = cap < dbar[i] ? cap : dbar[i];
+    const double s = __dmul_rn(r > fl ? r : fl, factor);
     const float ls = (float)log(s);
     P[P_S * G + base + i] = ls; P[(P_S + 1) * G + base + i] = ls; P[(P_S + 2) * G + base + i] = ls;
   }

@@ -120,6 +120,86 @@ def test_knn_brute_matches_scipy():
     np.testing.assert_allclose(oracle.knn3_mean(pts), d[:, 1:].mean(1), rtol=1e-13)
 
 
+def test_diag_matches_numpy():
+    """The Eq. 2 floor reference (reading A7: AABB diagonal of the level's points), checked
+    against numpy's own min/max/norm rather than against orc_diag."""
+    r = np.random.default_rng(11)
+    for n in (1, 2, 7, 300):
+        pts = r.normal(size=(n, 3)) * r.uniform(0.1, 3.0, 3) + r.uniform(-5, 5, 3)
+        want = float(np.linalg.norm(pts.max(0) - pts.min(0)))
+        assert abs(oracle.diag(pts) - want) <= 1e-14 * max(want, 1.0)
+    assert oracle.diag(np.zeros((5, 3))) == 0.0
+
+
+def _splitmix64_py(x):
+    """SplitMix64 in Python integers; its constants are pinned by the published test vectors
+    (test_splitmix64_vectors), independently of the C oracle."""
+    m = (1 << 64) - 1
+    z = (x + 0x9E3779B97F4A7C15) & m
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+    return z ^ (z >> 31)
+
+
+@pytest.mark.parametrize("seed", [5, 6])
+def test_create_eq2_per_level_matches_kdtree(seed):
+    """Pins orc_create's Eq. 2 composition (sec.3.2; reading A7/A9): level l >= 1 is
+    the first counts[l] points of the stable argsort of splitmix64(seed + i) (computed here in
+    Python), its scale comes from the 3-NN of exactly that level's own points (scipy cKDTree,
+    self excluded), mu_N / sigma_N (ddof 0) over that level only, the floor from that level's
+    own AABB diagonal, then ln s on all three axes.  Using level 0's points for every level,
+    storing s instead of ln s, or a single axis would each fail here."""
+    from scipy.spatial import cKDTree
+    r = np.random.default_rng(seed)
+    N0 = 900
+    # clustered cloud: levels differ strongly in density, so level-0 kNN distances differ
+    # from each subset's own by a large factor
+    centres = r.uniform(-1, 1, (6, 3))
+    pos = centres[r.integers(0, 6, N0)] + r.normal(scale=0.05, size=(N0, 3))
+    pos[:5] += r.uniform(2, 4, (5, 3))                       # a few outliers for the z-cap
+    rgb = r.uniform(0, 1, (N0, 3))
+    counts = [900, 225, 56, 14]
+    P = oracle.create(counts, pos, rgb, seed=seed)
+    keys = [_splitmix64_py(seed + i) for i in range(N0)]
+    perm = sorted(range(N0), key=lambda i: (keys[i], i))
+    off = 0
+    for l, n in enumerate(counts):
+        idx = np.arange(n) if l == 0 else np.array(perm[:n])
+        pts = pos[idx]
+        d, _ = cKDTree(pts).query(pts, k=4)
+        dbar = d[:, 1:].mean(1)
+        mu, sd = dbar.mean(), dbar.std()
+        dg = float(np.linalg.norm(pts.max(0) - pts.min(0)))
+        s = np.maximum(np.minimum(mu + 2.0 * sd, dbar), 1e-6 * dg) * 0.5
+        got = P[off:off + n, 10:13]
+        np.testing.assert_allclose(got, np.repeat(np.log(s)[:, None], 3, 1), rtol=0, atol=1e-12)
+        off += n
+    # the per-level subsets really differ in scale: a level-0 kNN would be ~2x smaller
+    assert np.mean(P[900:1125, 10]) > np.mean(P[:900, 10]) + 0.3
+
+
+def test_create_unit_grid_log_scale_closed_form():
+    """S:345 composed through create: a unit grid level gets s = 0.5 -> log-scale ln 0.5 on
+    all three axes (closed form)."""
+    g = np.arange(6.0)
+    pts = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3)
+    P = oracle.create([len(pts)], pts, np.ones_like(pts), seed=1)
+    np.testing.assert_array_equal(P[:, 10:13], math.log(0.5))
+
+
+@pytest.mark.parametrize("kind", ["single", "coincident"])
+def test_create_degenerate_level_is_finite(kind):
+    """Reading A20: a level of one point, or of coincident points, has diag = 0 and
+    no neighbour distance; the Eq. 2 floor then falls back to 1e-6 world units (applied after
+    the cap) so that the log-scale stays finite: ln(0.5e-6)."""
+    if kind == "single":
+        pts = np.array([[0.3, -0.2, 0.1]])
+    else:
+        pts = np.tile([[0.3, -0.2, 0.1]], (9, 1))
+    P = oracle.create([len(pts)], pts, np.ones_like(pts), seed=2)
+    np.testing.assert_allclose(P[:, 10:13], math.log(0.5e-6), rtol=1e-14)
+
+
 # ------------------------------------------------------- C1/C3 evaluator pins
 def test_peak_is_v_at_mean():
     """Unnormalised Gaussian (A2): yhat(mu) = v = sigmoid(o) * max(0, c)."""
