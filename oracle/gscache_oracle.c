@@ -688,6 +688,10 @@ int orc_fit_step(int L, const int64_t* goff, double* P, double* M, double* V, in
     for (int64_t j = goff[l]; j < goff[l + 1]; ++j)
       for (int k = 0; k < NP; ++k) {
         int gI = orc_group(k);
+        /* reading A16: a group whose learning rate is 0 is excluded from the optimizer
+         * (App. A.2: covariance optimization "by default we disabled"): its parameters
+         * and AdamW moments stay unchanged and its gradients are not counted */
+        if (hp[gI] == 0.0) continue;
         *nonfinite += orc_adamw(1, P + j * NP + k, M + j * NP + k, V + j * NP + k,
                                 grad + j * NP + k, eta[gI], hp[5 + gI], hp[10], hp[11], hp[12],
                                 adam_step[l]);

@@ -34,6 +34,7 @@ constexpr int kAdamThreads = 128, kAdamBlocksPerSM = 4;
 
 struct AdamHP {
   float wd[GC_NGROUPS]; float beta1, beta2, eps; double tau;
+  int frozen[GC_NGROUPS];   // reading A16: lr 0 -> group excluded from the optimizer
 };
 
 __device__ __forceinline__ int group_of(int k) { return k < 3 ? 0 : (k < 7 ? 1 : (k < 10 ? 2 : (k < 13 ? 3 : 4))); }
@@ -136,6 +137,7 @@ __global__ void __launch_bounds__(kAdamThreads, kAdamBlocksPerSM) k_adamw(
 #pragma unroll
     for (int k = 0; k < kNP; ++k) {
       const int grp = k < 3 ? 0 : (k < 7 ? 1 : (k < 10 ? 2 : (k < 13 ? 3 : 4)));   // constant after unroll
+      if (hp.frozen[grp]) continue;            // parameters and moments unchanged (A16)
       const float gk = raw[k];
       const bool ok = isfinite(gk);
       bad += !ok;
@@ -175,6 +177,7 @@ void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, CullBufs
   AdamHP h;
   for (int k = 0; k < GC_NGROUPS; ++k) h.wd[k] = hp.weight_decay[k];
   h.beta1 = hp.beta1; h.beta2 = hp.beta2; h.eps = hp.adam_eps; h.tau = (double)hp.cutoff_sigma;
+  for (int k = 0; k < GC_NGROUPS; ++k) h.frozen[k] = hp.lr[k] == 0.f ? 1 : 0;
   {
     ProfScope ps(prof, "adamw", s);
     int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((G + kAdamThreads - 1) / kAdamThreads, 148 * kAdamBlocksPerSM));

@@ -419,6 +419,27 @@ def test_adamw_matches_torch_adamw():
         np.testing.assert_allclose(p, tp.detach().numpy(), rtol=1e-12, atol=1e-14)
 
 
+def test_zero_lr_group_is_frozen():
+    """Reading A16 (P:267 scale LR 0; P:430 covariance optimization "by default ... disabled"):
+    with the default hyper-parameters the scale group's parameters AND moments never move,
+    while the other groups step; with scale LR > 0 (the -CO variant) they do move."""
+    r = np.random.default_rng(21)
+    G = 6
+    P = rand_params(G, r)
+    x = r.uniform(-0.6, 0.6, (200, 3))
+    ln = np.ones(200, np.int32)
+    rgb = r.uniform(0, 2, (200, 3))
+    oc = oracle.OracleCache([G], P, hp=dict(tau=np.inf))
+    for _ in range(3):
+        oc.fit(x, ln, rgb)
+    np.testing.assert_array_equal(oc.P[:, 10:13], P[:, 10:13])
+    assert np.all(oc.M[:, 10:13] == 0) and np.all(oc.V[:, 10:13] == 0)
+    assert np.all(oc.M[:, 0:3] != 0) and np.any(oc.P[:, 0:3] != P[:, 0:3])
+    oc2 = oracle.OracleCache([G], P, hp=dict(tau=np.inf, lr=[1.16e-3, 1e-3, 1.25e-2, 1.25e-2, 0.15]))
+    oc2.fit(x, ln, rgb)
+    assert np.all(oc2.P[:, 10:13] != P[:, 10:13]) and np.all(oc2.V[:, 10:13] > 0)
+
+
 def test_lr_schedule_eq5(golden):
     for ex in golden["lr_schedule_examples"]["value"]:
         t = math.e if ex["t"] == "e" else ex["t"]
