@@ -72,9 +72,18 @@ typedef struct {
   int64_t nonfinite_grads;         /* raw gradient elements skipped by AdamW (C6)                */
   int64_t n_pairs;                 /* contributing (sample, Gaussian) pairs, Q <= tau^2          */
   int64_t n_candidates;            /* (sample, Gaussian) pairs tested via the culling lists      */
+  int64_t flags;                   /* GC_FLAG_* bits, below                                      */
   int64_t count[GC_MAX_LEVELS];    /* k_l: valid samples per level (global under DP)             */
   double loss[GC_MAX_LEVELS];      /* L_l of Eq. 4 / C4, before this call's update               */
 } gc_fit_stats;
+
+/* gc_fit_stats.flags.  GC_FLAG_LISTS_OVERFLOWED: the culling lists read by this call were
+ * incomplete (their last rebuild had more entries than their capacity), so this call's
+ * optimizer step was skipped (step = 0, no level stepped) and its lookups may miss
+ * contributions.  Detected on the device, so it is reported under CUDA-graph replay too; the
+ * next call made outside a capture grows the lists and rebuilds them (and returns
+ * GC_ERR_STATE once). */
+enum { GC_FLAG_LISTS_OVERFLOWED = 1 };
 
 /* Raw parameters of one level in the paper's layout, row-major per Gaussian. */
 typedef struct {
@@ -201,8 +210,23 @@ gc_status gc_set_comm(gc_cache c, const void* nccl_uid, int rank, int world, int
 
 /* ---- debug / parity exports (not on the hot path) ---------------------------------- */
 
-/* Enable (1) / disable (0) recording of the raw 14-parameter gradients of each gc_fit. */
+/* Gradient recording of each gc_fit: enable bit 0 = the raw 14-parameter gradients (this
+ * also switches the hot path's reduced "lite" backward off, because the frozen-scale ∂A terms
+ * it skips are needed for them); bit 1 = a snapshot of the 12 coefficient gradients exactly as
+ * the optimizer reads them (taken after the fused fwd/bwd and any all-reduce, the backward
+ * itself unchanged: this is what exposes the timed lite path).  0 disables both. */
 gc_status gc_debug_enable_grads(gc_cache c, int enable);
+/* Coefficient gradients of the last gc_fit (bit 1 of gc_debug_enable_grads), level `level`:
+ * dst [n][12] f32 (host or device), per Gaussian (dmu_x, dmu_y, dmu_z, dA00, dA11, dA22, dA01,
+ * dA02, dA12, dv_r, dv_g, dv_b) with A = Sigma^-1 (full symmetric element, not doubled) and
+ * v = w max(0,c) (C5), summed over the call's samples and NOT yet divided by 3 k_l (the
+ * optimizer's normalisation, C4).  Synchronises the stream. */
+gc_status gc_debug_coef_grads(gc_cache c, int level, float* dst, gc_stream stream);
+/* Generation of the culling-list buffers: incremented whenever a capacity growth reallocated
+ * them.  A CUDA graph captured at an earlier generation keeps using (and rebuilding) the old
+ * buffers, which stay allocated until gc_destroy (memory-safe, but no longer shared with
+ * eager calls): re-capture after the generation changes. */
+gc_status gc_list_generation(gc_cache c, uint64_t* gen);
 /* Raw gradients d(sum_l L_l)/d(theta) of the last gc_fit (C5), in gc_level_params layout. */
 gc_status gc_debug_grads(gc_cache c, int level, gc_level_params* dst, gc_stream stream);
 /* Culling lists of one level (C8): offsets [cells+1] (level-local, host), idx (host, cap

@@ -268,6 +268,7 @@ def loss_grad(goff, P, x, length, rgb, tau=3.0, hdr_eps=0.01, mode=0, grids=None
     cnt = np.empty(L, np.int64)
     loss = np.empty(L, np.float64)
     grad = np.empty_like(P)
+    cg = np.empty((len(P), 15), np.float64)
     npairs = C.c_int64()
     o, ic, dm = _grids(grids, L)
     lib().orc_loss_grad(C.c_int(L), _p(goff, np.int64), _p(P, np.float64), C.c_double(tau),
@@ -275,8 +276,13 @@ def loss_grad(goff, P, x, length, rgb, tau=3.0, hdr_eps=0.01, mode=0, grids=None
                         _p(ln, np.int32), _p(rgb, np.float64), _p(o, np.float64),
                         _p(ic, np.float64), _p(dm, np.int32), _p(lv, np.int32), _p(y, np.float64),
                         _p(cnt, np.int64), _p(loss, np.float64), _p(grad, np.float64),
-                        C.byref(npairs))
-    return dict(level=lv, yhat=y, count=cnt, loss=loss, grad=grad, npairs=npairs.value)
+                        C.byref(npairs), _p(cg, np.float64))
+    # coefficient gradients in the library's debug layout (gc_debug_coef_grads): dmu (3),
+    # dA00 dA11 dA22 dA01 dA02 dA12 (full symmetric elements), dv (3); normalised by 1/(3 k_l)
+    coef = np.stack([cg[:, 0], cg[:, 1], cg[:, 2], cg[:, 3], cg[:, 7], cg[:, 11], cg[:, 4],
+                     cg[:, 5], cg[:, 8], cg[:, 12], cg[:, 13], cg[:, 14]], axis=1)
+    return dict(level=lv, yhat=y, count=cnt, loss=loss, grad=grad, npairs=npairs.value,
+                coef=coef)
 
 
 def adamw(p, m, v, g, lr, wd, beta1, beta2, eps, step):

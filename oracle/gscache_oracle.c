@@ -550,7 +550,7 @@ int orc_loss_grad(int L, const int64_t* goff, const double* P, double tau, doubl
                   int mode, int64_t S, const double* x, const int32_t* len, const double* rgb,
                   const double* g_origin, const double* g_inv, const int32_t* g_dims,
                   int32_t* level_of, double* yhat, int64_t* count, double* loss, double* grad,
-                  int64_t* npairs) {
+                  int64_t* npairs, double* cgrad) {
   int64_t G = goff[L];
   orc_gauss* gs = orc_activate_all(G, P);
   double* cg = (double*)calloc((size_t)(G > 0 ? G : 1) * 15, sizeof(double)); /* dmu3 dA9 dv3 */
@@ -635,6 +635,9 @@ int orc_loss_grad(int L, const int64_t* goff, const double* P, double tau, doubl
     orc_chain(&gs[j], P + j * NP, cj, dA, cj + 12, grad + j * NP);
   }
   if (yhat) memcpy(yhat, yy, sizeof(double) * 3 * (size_t)S);
+  /* cgrad (nullable, [G][15]): the coefficient gradients of C5 before the chain rule --
+   * dL/dmu (3), dL/dA as the full symmetric 3x3 (9, row-major), dL/dv (3) */
+  if (cgrad) memcpy(cgrad, cg, sizeof(double) * 15 * (size_t)G);
   if (npairs) *npairs = np;
   if (csr) { for (int l = 0; l < L; ++l) orc_csr_free(&csr[l]); free(csr); }
   free(yy); free(cg); free(gs);
@@ -673,7 +676,7 @@ int orc_fit_step(int L, const int64_t* goff, double* P, double* M, double* V, in
   int64_t G = goff[L];
   int32_t* lv = (int32_t*)malloc(sizeof(int32_t) * (size_t)(S > 0 ? S : 1));
   orc_loss_grad(L, goff, P, hp[14], hp[13], (int)hp[15], S, x, len, rgb, g_origin, g_inv, g_dims,
-                lv, NULL, count, loss, grad, npairs);
+                lv, NULL, count, loss, grad, npairs, NULL);
   free(lv);
   int64_t tot = 0;
   for (int l = 0; l < L; ++l) tot += count[l];

@@ -27,6 +27,7 @@ EXPORTS = ["gc_default_hparams", "gc_create", "gc_destroy", "gc_reserve", "gc_fi
            "gc_query_radiance", "gc_fit_query", "gc_set_deferred_step", "gc_flush",
            "gc_params", "gc_set_params", "gc_reset_schedule", "gc_grid", "gc_info",
            "gc_nccl_unique_id", "gc_set_comm", "gc_debug_enable_grads", "gc_debug_grads",
+           "gc_debug_coef_grads", "gc_list_generation",
            "gc_debug_cull", "gc_debug_levels", "gc_profile_enable", "gc_profile_read",
            "gc_last_error", "gc_status_string"]
 
@@ -49,13 +50,13 @@ class gc_hparams(C.Structure):
 class gc_fit_stats(C.Structure):
     _fields_ = [("n_in", C.c_int64), ("n_valid", C.c_int64), ("n_dropped", C.c_int64),
                 ("step", C.c_int64), ("nonfinite_grads", C.c_int64), ("n_pairs", C.c_int64),
-                ("n_candidates", C.c_int64), ("count", C.c_int64 * MAX_LEVELS),
+                ("n_candidates", C.c_int64), ("flags", C.c_int64), ("count", C.c_int64 * MAX_LEVELS),
                 ("loss", C.c_double * MAX_LEVELS)]
 
     def as_dict(self, L=MAX_LEVELS):
         return dict(n_in=self.n_in, n_valid=self.n_valid, n_dropped=self.n_dropped,
                     step=self.step, nonfinite_grads=self.nonfinite_grads, n_pairs=self.n_pairs,
-                    n_candidates=self.n_candidates, count=list(self.count)[:L],
+                    n_candidates=self.n_candidates, flags=self.flags, count=list(self.count)[:L],
                     loss=list(self.loss)[:L])
 
 
@@ -108,6 +109,8 @@ def lib():
             "gc_set_comm": (i32, [vp, vp, i32, i32, i32]),
             "gc_debug_enable_grads": (i32, [vp, i32]),
             "gc_debug_grads": (i32, [vp, i32, vp, vp]),
+            "gc_debug_coef_grads": (i32, [vp, i32, vp, vp]),
+            "gc_list_generation": (i32, [vp, vp]),
             "gc_debug_cull": (i32, [vp, i32, vp, vp, i64, vp, vp]),
             "gc_debug_levels": (i32, [vp, vp, vp]),
             "gc_profile_enable": (i32, [vp, i32]),
@@ -368,8 +371,22 @@ class GSCache:
         _check(lib().gc_set_comm(self.h, buf, rank, world, mode))
 
     # ----------------------------------------------------------------- debug
-    def debug_enable_grads(self, on=True):
-        _check(lib().gc_debug_enable_grads(self.h, int(bool(on))))
+    def debug_enable_grads(self, on=True, coef=False):
+        """Bit 0 (on): raw 14-parameter gradients; bit 1 (coef): the coefficient-gradient
+        snapshot of the unchanged (lite) hot path."""
+        _check(lib().gc_debug_enable_grads(self.h, int(bool(on)) | (2 if coef else 0)))
+
+    def debug_coef_grads(self, level, stream=None):
+        """[n][12] coefficient gradients of the last fit (dmu, dA00 dA11 dA22 dA01 dA02 dA12,
+        dv), not divided by 3 k_l."""
+        out = np.empty((int(self.counts[level]), 12), np.float32)
+        _check(lib().gc_debug_coef_grads(self.h, level, out.ctypes.data, _stream_ptr(stream)))
+        return out
+
+    def list_generation(self):
+        g = C.c_uint64()
+        _check(lib().gc_list_generation(self.h, C.byref(g)))
+        return g.value
 
     def debug_grads_rows(self, level, stream=None):
         a = self._empty_level(level)

@@ -34,7 +34,7 @@ constexpr int kAdamThreads = 128, kAdamBlocksPerSM = 4;
 
 struct AdamHP {
   float wd[GC_NGROUPS]; float beta1, beta2, eps; double tau;
-  int frozen[GC_NGROUPS];   // reading A16: lr 0 -> group excluded from the optimizer
+  int frozen;               // bit g: reading A16, lr 0 -> group g excluded from the optimizer
 };
 
 __device__ __forceinline__ int group_of(int k) { return k < 3 ? 0 : (k < 7 ? 1 : (k < 10 ? 2 : (k < 13 ? 3 : 4))); }
@@ -105,8 +105,11 @@ __device__ void chain_rule(const float p[kNP], const float cg[12], float out[kNP
 // k_record_cull right after (split so both kernels stay spill-free and latency-hidden).
 __global__ void __launch_bounds__(kAdamThreads, kAdamBlocksPerSM) k_adamw(
     int64_t G, float* __restrict__ P, float* __restrict__ M, float* __restrict__ V, float* __restrict__ grad,
-    float* __restrict__ dbg, const DevState* __restrict__ st, AdamHP hp, LevelGeom g, unsigned long long* nonfinite) {
+    float* __restrict__ dbg, DevState* st, AdamHP hp, LevelGeom g, unsigned long long* nonfinite) {
   pdl_enter();
+  // the culling rebuild that follows this kernel (k_record_cull -> scan -> k_cull_emit) sets the
+  // overflow flag afresh; the previous rebuild's flag has been read by this call's k_stats
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->csr_overflow = 0u;
   unsigned long long bad = 0;
   float eta[GC_NGROUPS], dec[GC_NGROUPS];
 #pragma unroll
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(kAdamThreads, kAdamBlocksPerSM) k_adamw(
 #pragma unroll
     for (int k = 0; k < kNP; ++k) {
       const int grp = k < 3 ? 0 : (k < 7 ? 1 : (k < 10 ? 2 : (k < 13 ? 3 : 4)));   // constant after unroll
-      if (hp.frozen[grp]) continue;            // parameters and moments unchanged (A16)
+      if ((hp.frozen >> grp) & 1) continue;    // parameters and moments unchanged (A16)
       const float gk = raw[k];
       const bool ok = isfinite(gk);
       bad += !ok;
@@ -177,11 +180,12 @@ void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, CullBufs
   AdamHP h;
   for (int k = 0; k < GC_NGROUPS; ++k) h.wd[k] = hp.weight_decay[k];
   h.beta1 = hp.beta1; h.beta2 = hp.beta2; h.eps = hp.adam_eps; h.tau = (double)hp.cutoff_sigma;
-  for (int k = 0; k < GC_NGROUPS; ++k) h.frozen[k] = hp.lr[k] == 0.f ? 1 : 0;
+  h.frozen = 0;
+  for (int k = 0; k < GC_NGROUPS; ++k) h.frozen |= (hp.lr[k] == 0.f ? 1 : 0) << k;
   {
     ProfScope ps(prof, "adamw", s);
     int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((G + kAdamThreads - 1) / kAdamThreads, 148 * kAdamBlocksPerSM));
-    launch_pdl(k_adamw, dim3(blocks), dim3(kAdamThreads), 0, s, G, P, M, V, grad, dbg_grad, (const DevState*)st, h, g, nonfinite);
+    launch_pdl(k_adamw, dim3(blocks), dim3(kAdamThreads), 0, s, G, P, M, V, grad, dbg_grad, st, h, g, nonfinite);
   }
   {
     ProfScope ps(prof, "record_cull", s);

@@ -74,7 +74,16 @@ struct Scratch {
   }
 };
 
-struct StatsPayload { gc_fit_stats* dst; const gc_fit_stats* src; };
+// Pageable caller stats: the device statistics are copied into the payload's own page-locked
+// slot, then a stream host callback copies the slot into the caller's struct.  Every payload
+// has its own slot and a completion event, so payloads in flight never share a buffer; a
+// payload is reused only once its event (recorded after the callback) has completed.
+struct StatsPayload {
+  gc_fit_stats* dst = nullptr;
+  gc_fit_stats* src = nullptr;        // page-locked slot
+  cudaEvent_t done = nullptr;
+  bool used = false;
+};
 
 struct gc_cache_s {
   int device = 0, sms = 148;
@@ -95,15 +104,22 @@ struct gc_cache_s {
   DevState* st = nullptr;
   LvlStats* lvl = nullptr;
   gc_fit_stats* dstats = nullptr;
-  gc_fit_stats* hstats = nullptr;   // pinned staging
   uint32_t* hcsr = nullptr;         // pinned: entries of the latest culling-list rebuild (capacity guard)
   double* partial = nullptr;
   int fb_grid = 0, q_grid = 0;
   bool dbg_on = false;
   Scratch fit, qry;
   int64_t last_fit_S = -1;
-  std::vector<StatsPayload*> payloads;
-  size_t payload_next = 0;
+  std::vector<StatsPayload*> payloads;    // all payloads (freed at destroy)
+  std::vector<StatsPayload*> ring;        // the reusable ones of eager calls
+  size_t payload_next = 0, captured_payloads = 0;
+  std::vector<void*> retired;             // culling lists replaced by a capacity growth: kept
+                                          // (not freed) until gc_destroy, because a CUDA graph
+                                          // captured earlier may still reference them
+  uint64_t list_generation = 0;           // bumped by every reallocation of the culling lists
+  CellRef cref{};                         // fp32 cell geometry of the evaluators (CellRef)
+  int dbg_mode = 0;                       // gc_debug_enable_grads: bit 0 raw grads, bit 1 coef grads
+  float* dbg_coef = nullptr;              // [G][12] coefficient-gradient snapshot (bit 1)
   Profiler prof;
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
@@ -218,6 +234,7 @@ static CullBufs cull_bufs(gc_cache c) {
 }
 
 static gc_status rebuild_csr(gc_cache c, cudaStream_t s, bool recompute_records) {
+  if (recompute_records) CK(cudaMemsetAsync(&c->st->csr_overflow, 0, sizeof(unsigned int), s));
   if (recompute_records)
     launch_record_cull(c->G, c->P, (double)c->hp.cutoff_sigma, c->geom, cull_bufs(c), c->st, s);
   launch_scan(c->csr_count, c->NC, 0, c->csr_tiles, c->csr_totals, c->csr_off, nullptr, nullptr, c->geom, s,
@@ -245,8 +262,9 @@ static gc_status csr_guard(gc_cache c, cudaStream_t s) {
   CK(dalloc(&ovf, cap)); CK(dalloc(&lrec, 4 * cap));
   const uint64_t keep = std::min<uint64_t>(total, c->csr_cap);
   CK(cudaMemcpy(lrec, c->csr_rec, sizeof(float4) * 4 * keep, cudaMemcpyDeviceToDevice));
-  cudaFree(c->csr_ovf); cudaFree(c->csr_rec);
-  c->csr_ovf = ovf; c->csr_rec = lrec; c->csr_cap = (uint32_t)cap;
+  c->retired.push_back(c->csr_ovf); c->retired.push_back(c->csr_rec);   // a captured graph may
+  c->csr_ovf = ovf; c->csr_rec = lrec; c->csr_cap = (uint32_t)cap;       // still point at them
+  c->list_generation += 1;
   if (!overflowed) return GC_OK;
   CK(cudaMemset(&c->st->csr_overflow, 0, sizeof(unsigned int)));
   if (!c->pending) {                 // a pending deferred step rebuilds with the new capacity anyway
@@ -260,6 +278,18 @@ static gc_status csr_guard(gc_cache c, cudaStream_t s) {
 static void CUDART_CB stats_cb(void* arg) {
   StatsPayload* p = (StatsPayload*)arg;
   memcpy(p->dst, p->src, sizeof(gc_fit_stats));
+}
+
+static gc_status new_payload(StatsPayload** out) {
+  StatsPayload* p = new StatsPayload();
+  if (cudaHostAlloc((void**)&p->src, sizeof(gc_fit_stats), cudaHostAllocDefault) != cudaSuccess ||
+      cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming) != cudaSuccess) {
+    if (p->src) cudaFreeHost(p->src);
+    delete p;
+    return fail(GC_ERR_OOM, "stats payload allocation failed");
+  }
+  *out = p;
+  return GC_OK;
 }
 
 static bool is_pinned_host(const void* p) {
@@ -305,18 +335,27 @@ static gc_status emit_stats(gc_cache c, gc_fit_stats* user, cudaStream_t s) {
     CK(cudaMemcpyAsync(user, c->dstats, sizeof(gc_fit_stats), cudaMemcpyDeviceToHost, s));
     return GC_OK;
   }
-  CK(cudaMemcpyAsync(c->hstats, c->dstats, sizeof(gc_fit_stats), cudaMemcpyDeviceToHost, s));
-  StatsPayload* p;
-  if (capturing(s)) {
-    p = new StatsPayload{user, c->hstats};
-    c->payloads.push_back(p);          // owned by the handle for the graph's lifetime
+  StatsPayload* p = nullptr;
+  const size_t ring = 64;
+  if (capturing(s)) {                  // a graph owns its payload for the handle's lifetime
+    if (gc_status e = new_payload(&p)) return e;
+    c->payloads.push_back(p);
+    c->captured_payloads += 1;
   } else {
-    const size_t ring = 64;
-    if (c->payloads.size() < ring) c->payloads.push_back(new StatsPayload{});
-    p = c->payloads[c->payload_next++ % std::min(c->payloads.size(), ring)];
-    p->dst = user; p->src = c->hstats;
+    const size_t live = c->payloads.size() - c->captured_payloads;
+    if (live < ring) {
+      if (gc_status e = new_payload(&p)) return e;
+      c->payloads.push_back(p);
+      c->ring.push_back(p);
+    } else {
+      p = c->ring[c->payload_next++ % ring];
+      if (p->used) CK(cudaEventSynchronize(p->done));   // its previous callback has run
+    }
   }
+  p->dst = user; p->used = true;
+  CK(cudaMemcpyAsync(p->src, c->dstats, sizeof(gc_fit_stats), cudaMemcpyDeviceToHost, s));
   CK(cudaLaunchHostFunc(s, stats_cb, p));
+  CK(cudaEventRecord(p->done, s));
   return GC_OK;
 }
 
@@ -392,7 +431,6 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
     CK(cudaMemcpy(c->st, &h0, sizeof h0, cudaMemcpyHostToDevice));
   }
   CK(dalloc(&c->lvl, 1)); CK(dalloc(&c->dstats, 1)); CK(cudaMemset(c->dstats, 0, sizeof(gc_fit_stats)));
-  CK(cudaHostAlloc((void**)&c->hstats, sizeof(gc_fit_stats), cudaHostAllocDefault));
   CK(cudaHostAlloc((void**)&c->hcsr, sizeof(uint32_t), cudaHostAllocDefault));
   *c->hcsr = 0u;
 
@@ -504,8 +542,12 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
                    nullptr);
   CK(cudaGetLastError());
 
+  // per device (the dynamic shared-memory attribute and the occupancy-based persistent grid
+  // sizes are properties of this device, set after cudaSetDevice above)
   c->fb_grid = fwdbwd_grid();
   c->q_grid = query_grid();
+  if (c->fb_grid <= 0 || c->q_grid <= 0) return fail(GC_ERR_CUDA, "evaluator configuration failed");
+  c->cref = cell_ref(c->geom);
   // a deferred optimizer step (side2) gates the next fwd/bwd and lookups: its CTAs go first
   // while it shares the GPU with the sample ingest (measured -7 us/frame; favouring either
   // half of the frame instead was slower)
@@ -533,11 +575,16 @@ static void destroy_impl(gc_cache c) {
                 c->csr_ovf,
                 c->csr_totals, c->csr_rec, c->csr_tiles, c->st, c->lvl, c->dstats, c->partial, c->pack_tmp};
   for (void* p : ps) if (p) cudaFree(p);
-  if (c->hstats) cudaFreeHost(c->hstats);
   if (c->hcsr) cudaFreeHost(c->hcsr);
   c->fit.release();
   c->qry.release();
-  for (auto* p : c->payloads) delete p;
+  for (auto* p : c->payloads) {
+    if (p->src) cudaFreeHost(p->src);
+    if (p->done) cudaEventDestroy(p->done);
+    delete p;
+  }
+  for (void* p : c->retired) cudaFree(p);
+  if (c->dbg_coef) cudaFree(c->dbg_coef);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->side2) cudaStreamDestroy(c->side2);
@@ -652,6 +699,7 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
   const float tau = c->hp.cutoff_sigma;
   fa.tau2 = tau * tau; fa.hdr_eps = c->hp.hdr_eps; fa.mode = c->hp.loss_grad_mode; fa.L = c->L;
   fa.lite = (c->hp.lr[GC_SCALE] == 0.f && !c->dbg_on) ? 1 : 0;
+  fa.ref = c->cref;
   const bool dp = c->comm != nullptr;
   // with the step deferred nothing after the statistics launch touches the call's stats, so a
   // page-locked caller struct is written by the kernel itself (mapped through UVA): no copy
@@ -667,6 +715,8 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
     NK(ncclGroupEnd());
     launch_step_scalars(c->lvl, c->st, c->hp, c->L, out_stats, s);
   }
+  if (c->dbg_mode & 2)   // debug snapshot of the coefficient gradients the optimizer will read
+    CK(cudaMemcpyAsync(c->dbg_coef, c->grad, sizeof(float) * 12 * c->G, cudaMemcpyDeviceToDevice, s));
   if (join) CK(cudaStreamWaitEvent(s, join, 0));
   if (c->defer) {
     c->pending = true;                // AdamW + culling rebuild run at the start of the next call
@@ -768,6 +818,7 @@ static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_le
   qa.att = ep.dev[0]; qa.beta = ep.dev[1]; qa.unb = ep.dev[2];
   const float tau = c->hp.cutoff_sigma;
   qa.tau2 = tau * tau;
+  qa.ref = c->cref;
   if (tail_ev) CK(cudaStreamWaitEvent(s, tail_ev, 0));     // a deferred step is complete
   launch_query(qa, c->q_grid, s, &c->prof);
   if (hout) CK(cudaMemcpyAsync(out_rgb, dout, sizeof(float) * 3 * S, cudaMemcpyDeviceToHost, s));
@@ -823,7 +874,7 @@ gc_status gc_flush(gc_cache c, gc_stream stream) {
 }
 
 gc_status gc_set_params(gc_cache c, int level, const gc_level_params* src, int reset_adam, gc_stream stream) {
-  if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  if (!c || !src) return fail(GC_ERR_ARG, "NULL handle or src");
   cudaStream_t s = (cudaStream_t)stream;
   CK(cudaSetDevice(c->device));
   if (gc_status e = flush_pending(c, s)) return e;
@@ -892,10 +943,32 @@ gc_status gc_set_comm(gc_cache c, const void* nccl_uid, int rank, int world, int
 }
 
 gc_status gc_debug_enable_grads(gc_cache c, int enable) {
-  if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  if (!c || enable < 0 || enable > 3) return fail(GC_ERR_ARG, "NULL handle or enable not in 0..3");
   CK(cudaSetDevice(c->device));
-  if (enable && !c->dbg) { CK(dalloc(&c->dbg, kNP * c->G)); CK(cudaMemset(c->dbg, 0, sizeof(float) * kNP * c->G)); }
-  c->dbg_on = enable != 0;
+  if ((enable & 1) && !c->dbg) { CK(dalloc(&c->dbg, kNP * c->G)); CK(cudaMemset(c->dbg, 0, sizeof(float) * kNP * c->G)); }
+  if ((enable & 2) && !c->dbg_coef) {
+    CK(dalloc(&c->dbg_coef, 12 * c->G));
+    CK(cudaMemset(c->dbg_coef, 0, sizeof(float) * 12 * c->G));
+  }
+  c->dbg_on = (enable & 1) != 0;
+  c->dbg_mode = enable;
+  return GC_OK;
+}
+
+gc_status gc_debug_coef_grads(gc_cache c, int level, float* dst, gc_stream stream) {
+  if (!c || !dst || level < 0 || level >= c->L) return fail(GC_ERR_ARG, "bad arguments");
+  if (!c->dbg_coef) return fail(GC_ERR_STATE, "coefficient-gradient recording not enabled (gc_debug_enable_grads bit 1)");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaMemcpyAsync(dst, c->dbg_coef + 12 * c->geom.goff[level], sizeof(float) * 12 * c->counts[level],
+                     cudaMemcpyDefault, s));
+  CK(cudaStreamSynchronize(s));
+  return GC_OK;
+}
+
+gc_status gc_list_generation(gc_cache c, uint64_t* gen) {
+  if (!c || !gen) return fail(GC_ERR_ARG, "bad arguments");
+  *gen = c->list_generation;
   return GC_OK;
 }
 

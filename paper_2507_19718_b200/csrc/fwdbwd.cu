@@ -5,7 +5,7 @@
 // two samples (s = lane, lane + 32; one when the item has <= 32) so that each staged
 // candidate feeds two evaluations, run as packed fp32x2 (FADD2/FMUL2/FFMA2) issues.  The
 // cell's culling list (C8: 64-B entries, record + Gaussian index) is staged into the warp's
-// shared memory 32 candidates at a time, recentred on the item's first sample.
+// shared memory 32 candidates at a time, recentred on the centre of the item's cell.
 //   pass 1 (lane = sample pair): yhat = sum v_j e^{-Q/2} over the candidates with
 //          Q <= tau^2 (C3); lane k keeps candidate k's inside ballots (which samples it
 //          covers); the Eq. 4 loss and g = dL/dyhat (C4, unnormalised -- the 1/(3 k_l)
@@ -33,7 +33,7 @@ constexpr float kNegHalfLog2e = -0.72134752044448170f;    // -0.5 * log2(e)
 static_assert(kCH == 64, "two samples per lane");
 
 // Staged candidate (64 B in shared memory), relative to the work item's reference point
-// x_ref (its first sample): c = U (mu - x_ref), so that for x' = x - x_ref
+// x_ref (the centre of its cell, CellRef): c = U (mu - x_ref), so that for x' = x - x_ref
 //   w = U x' - c = U (x - mu),  Q = |w|^2   (9 FMA per pair; recentring keeps fp32 exact enough)
 struct ChunkSmem {
   float4 r0[32];                   // U00 U01 U02 U11
@@ -461,6 +461,16 @@ __device__ __forceinline__ void load_pos(const float4* __restrict__ bin, int str
   }
 }
 
+// Centre of a work item's cell (fp32; any point of the cell would do as long as every pass
+// of the item uses the same one).
+__device__ __forceinline__ void cell_centre(const CellRef& r, int cell, int l, float& x, float& y, float& z) {
+  const int loc = cell - r.coff[l], dx = r.dx[l], dy = r.dy[l];
+  const int cx = loc % dx, t = loc / dx, cy = t % dy, cz = t / dy;
+  x = fmaf((float)cx + 0.5f, r.edge[l][0], r.org[l][0]);
+  y = fmaf((float)cy + 0.5f, r.edge[l][1], r.org[l][1]);
+  z = fmaf((float)cz + 0.5f, r.edge[l][2], r.org[l][2]);
+}
+
 __device__ __forceinline__ void hdr_grad(int mode, float eps, const float (&y)[3], const float (&t)[3],
                                          float (&g)[3], float& ls) {
 #pragma unroll
@@ -531,8 +541,8 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
         xb[0] = p.x; xb[1] = p.y; xb[2] = p.z; tb[0] = p.w; tb[1] = q.x; tb[2] = q.y;
       }
     }
-    const float xref = __shfl_sync(0xffffffffu, xa[0], 0), yref = __shfl_sync(0xffffffffu, xa[1], 0),
-                zref = __shfl_sync(0xffffffffu, xa[2], 0);
+    float xref, yref, zref;                                 // the cell's centre (CellRef)
+    cell_centre(a.ref, wi.cell, wi.level, xref, yref, zref);
     xa[0] -= xref; xa[1] -= yref; xa[2] -= zref;            // NaN stays NaN
     xb[0] -= xref; xb[1] -= yref; xb[2] -= zref;
     // ---------------- pass 1 (keeps each candidate's inside masks while they fit)
@@ -681,8 +691,8 @@ __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
     float4 pa, pb4;
     load_pos(a.bin, 2, wi.start, wi.count, lane, xa, pa);
     load_pos(a.bin, 2, wi.start, wi.count, lane + 32, xb, pb4);
-    const float xref = __shfl_sync(0xffffffffu, xa[0], 0), yref = __shfl_sync(0xffffffffu, xa[1], 0),
-                zref = __shfl_sync(0xffffffffu, xa[2], 0);
+    float xref, yref, zref;
+    cell_centre(a.ref, wi.cell, wi.level, xref, yref, zref);
     xa[0] -= xref; xa[1] -= yref; xa[2] -= zref;
     xb[0] -= xref; xb[1] -= yref; xb[2] -= zref;
     float ya[3] = {0.f, 0.f, 0.f}, yb[3] = {0.f, 0.f, 0.f};
@@ -697,6 +707,15 @@ __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
   }
 }
 
+CellRef cell_ref(const LevelGeom& g) {
+  CellRef r{};
+  for (int l = 0; l < g.L; ++l) {
+    for (int a = 0; a < 3; ++a) { r.org[l][a] = (float)g.origin[l][a]; r.edge[l][a] = (float)g.edge[l][a]; }
+    r.dx[l] = g.dims[l][0]; r.dy[l] = g.dims[l][1]; r.coff[l] = (int)g.coff[l];
+  }
+  return r;
+}
+
 constexpr size_t kFwdBwdSmem = sizeof(WarpSmem) * kWarps;
 
 static int persistent_grid(const void* fn, size_t smem) {
@@ -707,14 +726,15 @@ static int persistent_grid(const void* fn, size_t smem) {
   return sms * std::max(per, 1);
 }
 
+// Both are per device: called by gc_create after cudaSetDevice (the dynamic shared-memory
+// attribute is a property of the current device's context; a handle on another device sets
+// its own).  Returns 0 on failure.
 int fwdbwd_grid() {
-  static int g = [] {
-    cudaFuncSetAttribute(k_fwdbwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdBwdSmem);
-    return persistent_grid((const void*)k_fwdbwd, kFwdBwdSmem);
-  }();
-  return g;
+  if (cudaFuncSetAttribute(k_fwdbwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdBwdSmem) != cudaSuccess)
+    return 0;
+  return persistent_grid((const void*)k_fwdbwd, kFwdBwdSmem);
 }
-int query_grid() { static int g = persistent_grid((const void*)k_query, 0); return g; }
+int query_grid() { return persistent_grid((const void*)k_query, 0); }
 
 void launch_fwdbwd(const FitArgs& a, int grid, cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "fwdbwd", s);

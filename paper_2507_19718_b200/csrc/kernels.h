@@ -112,6 +112,14 @@ void launch_levels_of(const uint2* kr, int64_t S, const LevelGeom& g, int32_t* o
                       cudaStream_t s);
 
 // fwdbwd.cu
+// Per-level cell geometry in fp32 for the evaluators' reference point: a work item's samples
+// and staged candidates are recentred on the centre of its cell (inside the grid even when
+// samples lie far outside it, reading A17), so |x - x_ref| stays at the cell scale.
+struct CellRef {
+  float org[kMaxL][3], edge[kMaxL][3];
+  int dx[kMaxL], dy[kMaxL], coff[kMaxL];
+};
+CellRef cell_ref(const LevelGeom& g);
 struct FitArgs {
   const WorkItem* work; const uint32_t* n_work;
   const uint32_t* csr_off; const float4* lrec;
@@ -120,6 +128,7 @@ struct FitArgs {
   double* partial;      // [grid][kMaxL + 2]: per-block loss sums, pairs, candidates
   float tau2, hdr_eps; int mode; int L;
   int lite;             // scale group frozen (lr 0) and no gradient export: skip dA on isotropic chunks
+  CellRef ref;
 
 };
 int fwdbwd_grid();
@@ -130,6 +139,7 @@ struct QueryArgs {
   const float4* bin;
   float* out; float tau2;
   const float* att; const float* beta; const float* unb;   // optional f3 epilogue (caller order)
+  CellRef ref;
 };
 int query_grid();
 void launch_query(const QueryArgs& a, int grid, cudaStream_t s, Profiler* prof);

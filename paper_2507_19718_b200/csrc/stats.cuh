@@ -50,7 +50,10 @@ __device__ __forceinline__ void step_scalars_warp(const LvlStats* lvl, DevState*
                                                   gc_fit_stats* out, int lane) {
   double tot = 0.0;
   for (int l = 0; l < hp.L; ++l) tot += lvl->count[l];
-  const int stepped = tot > 0.0;
+  // lists that overflowed at their last rebuild were incomplete for this call's fwd/bwd:
+  // skip the step (reported in gc_fit_stats.flags; the host grows the lists on its next call)
+  const unsigned int ovf = *(volatile unsigned int*)&st->csr_overflow;
+  const int stepped = tot > 0.0 && ovf == 0u;
   const long long t = st->t + stepped;
   __syncwarp();
   if (lane < GC_NGROUPS)
@@ -83,6 +86,7 @@ __device__ __forceinline__ void step_scalars_warp(const LvlStats* lvl, DevState*
     st->nonfinite = 0ull;
     out->n_pairs = (int64_t)lvl->n_pairs;
     out->n_candidates = (int64_t)lvl->n_cand;
+    out->flags = ovf ? (int64_t)GC_FLAG_LISTS_OVERFLOWED : 0;
   }
 }
 

@@ -1,0 +1,236 @@
+"""Round-2 parity cases (-m gpu), through the C ABI, against the fp64 oracle:
+
+* the timed "lite" backward's coefficient gradients (gc_debug_coef_grads snapshot, the
+  backward itself unchanged) and the raw gradients, at configs[2]'s full frame size, on the
+  whole frame, against the culled oracle (SURVEY 8(c) gradient bar, both forms);
+* the general path (rotated, anisotropic, scale LR > 0: north_star's "covariance factors") at
+  full cfg2 size;
+* finite samples far outside the culling grid (A17) mixed into border cells;
+* culling-list overflow detected on the device under CUDA-graph replay, and list growth;
+* Eq. 2 on degenerate levels (reading A20);
+* the pageable-statistics ring with more than 64 calls in flight.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle
+import workload
+from test_gpu_parity import check_forward, check_grad_group, check_grads, cuda, make_cfg1, rows
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gsc():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2507_19718_b200 as m
+    assert torch.cuda.is_available()
+    return m
+
+
+COEF_GROUPS = {"dmu": slice(0, 3), "dA": slice(3, 9), "dv": slice(9, 12)}
+
+
+def check_coef(dev, st, ro, goff, what, lite_levels=()):
+    """Device coefficient gradients (unnormalised sums) vs the oracle's (normalised by
+    1/(3 k_l)): every (level, coefficient group) under both gradient bars; on levels run by
+    the lite backward (isotropic, scale group frozen) dA is exactly 0 on the device."""
+    for l in range(len(goff) - 1):
+        sl = slice(goff[l], goff[l + 1])
+        k = int(st.count[l])
+        assert k == ro["count"][l]
+        if k == 0:
+            continue
+        d = dev[sl].astype(np.float64) / (3.0 * k)
+        for name, cs in COEF_GROUPS.items():
+            if name == "dA" and l in lite_levels:
+                assert np.all(dev[sl, cs] == 0.0), (what, l, "lite dA")
+                continue
+            check_grad_group(d[:, cs], ro["coef"][sl, cs], f"{what} level {l} {name}")
+
+
+def test_cfg2_full_frame_gradients_lite_and_raw(gsc):
+    """configs[2], one full 1920x1080 frame (2,073,600 samples), default hyper-parameters:
+    (1) the coefficient gradients of the timed lite backward, (2) the raw 14-parameter
+    gradients (recording on), both against the culled oracle on the whole frame."""
+    pos, alb = workload.init_cloud(2)
+    counts = workload.CONFIGS[2]["counts"]
+    x, ln, rgb = workload.fit_batch(2, frame=1)
+    c = gsc.GSCache(counts, cuda(pos), cuda(alb), seed=2)
+    c.reserve(len(x), 0)
+    P = rows(c)
+    ro = oracle.loss_grad(c.goff, P, x.astype(np.float64), ln, rgb.astype(np.float64), grids=c.grids())
+    c.debug_enable_grads(False, coef=True)
+    st = c.fit(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    for l in range(4):
+        assert abs(st.loss[l] - ro["loss"][l]) <= 1e-4 * ro["loss"][l]
+    dev = np.concatenate([c.debug_coef_grads(l) for l in range(4)])
+    check_coef(dev, st, ro, c.goff, "cfg2 lite", lite_levels=(0, 1, 2, 3))
+    c2 = gsc.GSCache(counts, cuda(pos), cuda(alb), seed=2)
+    c2.reserve(len(x), 0)
+    c2.debug_enable_grads(True)
+    st2 = c2.fit(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    g = np.concatenate([c2.debug_grads_rows(l) for l in range(4)]).astype(np.float64)
+    check_grads(g, ro["grad"], c2.goff, "cfg2 raw", iso_levels=(0, 1, 2, 3))
+    assert st2.n_pairs == st.n_pairs
+
+
+def test_cfg2_full_frame_anisotropic_scale_lr(gsc):
+    """The general (non-lite) path at full cfg2 size: every level rotated and anisotropic,
+    scale LR 0.0125 (the paper's -CO variant): raw and coefficient gradients on the
+    whole frame, then the first AdamW step of the scale group vs the oracle's."""
+    pos, alb = workload.init_cloud(2)
+    counts = workload.CONFIGS[2]["counts"]
+    lr = [1.16e-3, 1e-3, 1.25e-2, 1.25e-2, 1.5e-1]
+    hp = gsc.default_hparams(lr=lr)
+    c = gsc.GSCache(counts, cuda(pos), cuda(alb), seed=2, hparams=hp)
+    r = np.random.default_rng(31)
+    for l in range(4):
+        Pl = c.params_rows(l)
+        Pl[:, 3:7] = r.normal(size=(len(Pl), 4)).astype(np.float32)
+        Pl[:, 10:13] += r.uniform(-0.4, 0.2, (len(Pl), 3)).astype(np.float32)
+        c.set_params_rows(l, Pl)
+    x, ln, rgb = workload.fit_batch(2, frame=2)
+    c.reserve(len(x), 0)
+    P = rows(c)
+    c.debug_enable_grads(True, coef=True)
+    st = c.fit(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    oc = oracle.OracleCache(counts, P, hp=dict(lr=lr), grids=c.grids())
+    ro = oracle.loss_grad(c.goff, P, x.astype(np.float64), ln, rgb.astype(np.float64), grids=c.grids())
+    oc.fit(x.astype(np.float64), ln, rgb.astype(np.float64))
+    g = np.concatenate([c.debug_grads_rows(l) for l in range(4)]).astype(np.float64)
+    check_grads(g, ro["grad"], c.goff, "cfg2 aniso")
+    dev = np.concatenate([c.debug_coef_grads(l) for l in range(4)])
+    check_coef(dev, st, ro, c.goff, "cfg2 aniso coef")
+    P1 = rows(c)
+    # the scale group now steps: first AdamW step = -eta sign(g) wherever g is well above the
+    # fp32 rounding level (test_first_step_matches_oracle_update's criterion)
+    go = ro["grad"][:, 10:13]
+    strong = np.abs(go) > 1e-3 * np.abs(go).max()
+    d_dev, d_or = (P1 - P)[:, 10:13], (oc.P - P)[:, 10:13]
+    assert strong.mean() > 0.5
+    assert np.all(np.abs(d_dev - d_or)[strong] <= 1e-3 * 1.25e-2 + 4e-7 * (1 + np.abs(P[:, 10:13][strong])))
+
+
+def test_far_outside_grid_samples(gsc):
+    """Finite samples far outside a level's culling grid (x = +-5, +-1e3, +-1e30 on one or
+    all axes) clamp into border cells (A17) and share work items with in-grid samples of those
+    cells.  Lookups and gradients of every sample must match the oracle: the evaluators
+    recentre on the cell's centre, not on an item's first sample."""
+    c, _, _ = make_cfg1(gsc)
+    P = rows(c)
+    x, ln, rgb = workload.fit_batch(1, S=120_000, frame=5)
+    r = np.random.default_rng(17)
+    n_out = 6000
+    far = r.choice([5.0, -5.0, 1e3, -1e3, 1e30, -1e30], size=(n_out, 3))
+    keep = r.random((n_out, 3)) < 0.5                       # some axes stay in the grid
+    far = np.where(keep, x[:n_out], far).astype(np.float32)
+    far[keep.all(axis=1), 0] = 1e30
+    idx = r.choice(len(x), n_out, replace=False)
+    x[idx] = far
+    # samples on the grid boundary region (border cells hold both kinds)
+    y = c.query(cuda(x), cuda(ln)).cpu().numpy()
+    yo, lv, _ = oracle.query(c.goff, P, x.astype(np.float64), ln, grids=c.grids())
+    assert np.all(np.isfinite(y))
+    check_forward(y, yo, P, c.goff, x, lv, what="outside-grid lookups")
+    c.debug_enable_grads(True, coef=True)
+    st = c.fit(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    ro = oracle.loss_grad(c.goff, P, x.astype(np.float64), ln, rgb.astype(np.float64), grids=c.grids())
+    for l in range(3):
+        assert st.count[l] == ro["count"][l]
+        assert abs(st.loss[l] - ro["loss"][l]) <= 1e-4 * ro["loss"][l]
+    g = np.concatenate([c.debug_grads_rows(l) for l in range(3)]).astype(np.float64)
+    check_grads(g, ro["grad"], c.goff, "outside-grid", iso_levels=(0, 1, 2))
+    assert np.isfinite(rows(c)).all()
+
+
+def test_overflow_detected_under_graph_replay(gsc):
+    """Culling-list overflow is detected on the device: a CUDA-graph replay whose lists
+    overflowed reports GC_FLAG_LISTS_OVERFLOWED and skips its optimizer step (no host code
+    runs during replay).  The next eager call grows the lists (GC_ERR_STATE once, list
+    generation + 1); a graph captured before the growth keeps its own (retired, still
+    allocated) lists and keeps reporting the overflow instead of touching freed memory."""
+    c, _, _ = make_cfg1(gsc)
+    x, ln, rgb = workload.fit_batch(1, S=50_000, frame=7)
+    xd, lnd, rgbd = cuda(x), cuda(ln), cuda(rgb)
+    c.reserve(len(x), 0)
+    s = torch.cuda.Stream()
+    st = gsc.pinned_stats()
+    with torch.cuda.stream(s):
+        c.fit(xd, lnd, rgbd, stream=s, stats=st)              # warm-up (eager)
+    s.synchronize()
+    assert st.flags == 0 and st.step == 1
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        c.fit(xd, lnd, rgbd, stream=s, stats=st)
+    gen0 = c.list_generation()
+    P0 = c.params_rows(0)
+    P0[:, 10:13] = np.log(0.25)                                # ~10x the Eq. 2 extent
+    c.set_params_rows(0, P0)                                   # its rebuild overflows
+    before = rows(c)
+    with torch.cuda.stream(s):
+        g.replay()
+    s.synchronize()
+    assert st.flags == 1 and st.step == 0                      # detected without the host
+    np.testing.assert_array_equal(rows(c), before)             # step skipped
+    with pytest.raises(gsc.GCError) as ei:                     # eager: grow + rebuild, once
+        c.fit(xd, lnd, rgbd)
+    assert ei.value.status == 2
+    assert c.list_generation() == gen0 + 1
+    st2 = c.fit(xd, lnd, rgbd)
+    torch.cuda.synchronize()
+    assert st2.flags == 0 and st2.step >= 1
+    with torch.cuda.stream(s):                                 # stale graph: old lists, safe
+        g.replay()
+    s.synchronize()
+    assert st.flags == 1
+
+
+@pytest.mark.parametrize("kind", ["single", "coincident"])
+def test_degenerate_level_eq2(gsc, kind):
+    """Reading A20: a level of one point (counts[l] = 1) or of coincident points gets the
+    absolute floor ln(0.5e-6) from Eq. 2 (NULL init scales), finite, equal to the oracle's;
+    the cache then fits and answers lookups."""
+    pos, alb = workload.init_cloud(1)
+    pos, alb = pos[:256].copy(), alb[:256].copy()
+    if kind == "coincident":
+        pos[:] = pos[0]
+    counts = [256, 1]
+    c = gsc.GSCache(counts, cuda(pos), cuda(alb), seed=9)
+    P = rows(c)
+    Po = oracle.create(counts, pos.astype(np.float64), alb.astype(np.float64), seed=9)
+    assert np.isfinite(P).all()
+    np.testing.assert_allclose(P[:, 10:13], Po[:, 10:13].astype(np.float32), rtol=3e-7)
+    x, ln, rgb = workload.fit_batch(1, S=5000)
+    ln = np.minimum(ln, 2).astype(np.int32)
+    y = c.query(cuda(x), cuda(ln)).cpu().numpy()
+    yo, lv, _ = oracle.query(c.goff, P, x.astype(np.float64), ln, grids=c.grids())
+    check_forward(y, yo, P, c.goff, x, lv, what=f"{kind} level")
+    st = c.fit(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    assert st.step == 1 and np.isfinite(rows(c)).all()
+
+
+def test_pageable_stats_ring_many_in_flight(gsc):
+    """More than the 64-slot ring of pageable statistics in flight without a synchronisation:
+    every caller struct receives its own call's statistics."""
+    c, _, _ = make_cfg1(gsc)
+    x, ln, rgb = workload.fit_batch(1, S=4000, frame=9)
+    xd, lnd, rgbd = cuda(x), cuda(ln), cuda(rgb)
+    sts = []
+    for k in range(150):
+        stk = gsc.gc_fit_stats()                               # pageable
+        n = 1000 + 17 * k
+        c.fit(xd[:n], lnd[:n], rgbd[:n], stats=stk)
+        sts.append((n, stk))
+    torch.cuda.synchronize()
+    for k, (n, stk) in enumerate(sts):
+        assert stk.n_in == n and stk.step == k + 1, (k, stk.n_in, stk.step)

@@ -336,6 +336,30 @@ def _fd(fun, P, h=1e-6):
     return g
 
 
+def test_coefficient_gradients_vs_finite_differences():
+    """The oracle's coefficient gradients (C5: dL/dmu, dL/dA, dL/dv before the chain rule, the
+    quantity gc_debug_coef_grads exposes) against central finite differences of the loss in
+    the raw parameters, composed by hand through scipy's rotation: dL/dmu = FD(position);
+    dL/dc_ch = w dL/dv_ch (c > 0); dL/ds_k = -2 e^{-2 s_k} (R^T dA R)_kk."""
+    goff, P, x, ln, rgb = _tiny_problem(12, L=1, G=(5,), S=40)
+
+    def loss(Pp):
+        return oracle.loss_grad(goff, Pp, x, ln, rgb, tau=np.inf, mode=1)["loss"].sum()
+
+    r = oracle.loss_grad(goff, P, x, ln, rgb, tau=np.inf, mode=1)
+    cg = r["coef"]
+    fd = _fd(loss, P)
+    np.testing.assert_allclose(cg[:, 0:3], fd[:, 0:3], rtol=1e-6, atol=1e-9)
+    w = 1.0 / (1.0 + np.exp(-P[:, 13]))
+    np.testing.assert_allclose(w[:, None] * cg[:, 9:12], fd[:, 7:10], rtol=1e-6, atol=1e-9)
+    for j in range(len(P)):
+        R = scipy_R(P[j, 3:7])
+        a = cg[j]
+        dA = np.array([[a[3], a[6], a[7]], [a[6], a[4], a[8]], [a[7], a[8], a[5]]])
+        ds = -2.0 * np.exp(-2.0 * P[j, 10:13]) * np.diag(R.T @ dA @ R)
+        np.testing.assert_allclose(ds, fd[j, 10:13], rtol=1e-6, atol=1e-9)
+
+
 def _check_groups(g, fd, tol):
     for name, sl in oracle.GROUP_SLICES.items():
         a, b = g[:, sl], fd[:, sl]
