@@ -285,6 +285,30 @@ def loss_grad(goff, P, x, length, rgb, tau=3.0, hdr_eps=0.01, mode=0, grids=None
                 coef=coef)
 
 
+def grad_allowance(goff, P, x, length, rgb, tau=3.0, hdr_eps=0.01, mode=0, grids=None,
+                   amb_rel=1e-4):
+    """First-order bound of the gradient change that reading A3's fp32 cut-off flips can
+    cause (pairs with |Q - tau^2| <= amb_rel tau^2), per Gaussian: coefficient layout like
+    loss_grad()['coef'] and raw [G][14]; plus the number of samples with an ambiguous pair."""
+    goff = _i64(goff)
+    L = len(goff) - 1
+    P = _d(P).reshape(-1, NP)
+    x, rgb, ln = _d(x).reshape(-1, 3), _d(rgb).reshape(-1, 3), _i32(length)
+    ac = np.empty((len(P), 15), np.float64)
+    ar = np.empty((len(P), NP), np.float64)
+    na = C.c_int64()
+    o, ic, dm = _grids(grids, L)
+    lib().orc_grad_allowance(C.c_int(L), _p(goff, np.int64), _p(P, np.float64), C.c_double(tau),
+                             C.c_double(hdr_eps), C.c_int(mode), C.c_int64(len(x)),
+                             _p(x, np.float64), _p(ln, np.int32), _p(rgb, np.float64),
+                             _p(o, np.float64), _p(ic, np.float64), _p(dm, np.int32),
+                             C.c_double(amb_rel), _p(ac, np.float64), _p(ar, np.float64),
+                             C.byref(na))
+    coef = np.stack([ac[:, 0], ac[:, 1], ac[:, 2], ac[:, 3], ac[:, 7], ac[:, 11], ac[:, 4],
+                     ac[:, 5], ac[:, 8], ac[:, 12], ac[:, 13], ac[:, 14]], axis=1)
+    return dict(coef=coef, raw=ar, n_amb=na.value)
+
+
 def adamw(p, m, v, g, lr, wd, beta1, beta2, eps, step):
     """In-place AdamW on fp64 arrays (C6); returns the non-finite count."""
     return int(lib().orc_adamw(C.c_int64(p.size), _p(p, np.float64), _p(m, np.float64),

@@ -703,3 +703,134 @@ int orc_fit_step(int L, const int64_t* goff, double* P, double* M, double* V, in
   (void)G;
   return 0;
 }
+
+/* ------------------------------------- A3 boundary allowance of the gradients (tests) */
+
+/* Reading A3 lets a pair with |Q - tau^2| <= amb_rel tau^2 fall on either side of the cut-off
+ * in fp32.  A flip changes the flipped pair's own contribution to its Gaussian's gradient and,
+ * through yhat_i, the loss gradient g_i of its sample and hence every pair of that sample.
+ * This bounds both to first order, per Gaussian, as absolute values:
+ *   a_i,ch  = sum_{ambiguous j} v_j,ch e^{-Q_ij/2}       (|d yhat_i|)
+ *   gam_i,ch = |dg/dyhat|_i,ch a_i,ch                   (|d g_i|)
+ *   inside pair, not ambiguous:  |d(dmu)| <= Gam e |t|, |d(dA)| <= Gam e |d d^T| / 2,
+ *     |d(dv_ch)| <= gam_ch e, with Gam = sum_ch gam_ch v_j,ch;
+ *   ambiguous pair: its whole contribution with |g| + gam in place of g.
+ * allow_coef [G][15] (dmu 3, dA 9 full, dv 3) and allow_raw [G][14] (the bound carried through
+ * the chain rule of C5 with absolute values).  Samples with an ambiguous pair are counted in
+ * *n_amb.  Culled evaluation when g_origin != NULL (same pair sets as orc_loss_grad). */
+int orc_grad_allowance(int L, const int64_t* goff, const double* P, double tau, double hdr_eps,
+                       int mode, int64_t S, const double* x, const int32_t* len, const double* rgb,
+                       const double* g_origin, const double* g_inv, const int32_t* g_dims,
+                       double amb_rel, double* allow_coef, double* allow_raw, int64_t* n_amb) {
+  int64_t G = goff[L];
+  orc_gauss* gs = orc_activate_all(G, P);
+  orc_csr* csr = NULL;
+  if (g_origin) {
+    csr = (orc_csr*)malloc(sizeof(orc_csr) * (size_t)L);
+    for (int l = 0; l < L; ++l)
+      orc_csr_make(goff[l + 1] - goff[l], P + goff[l] * NP, tau, g_origin + 3 * l, g_inv + 3 * l,
+                   g_dims + 3 * l, &csr[l]);
+  }
+  int64_t* count = (int64_t*)calloc((size_t)L, sizeof(int64_t));
+  int32_t* lv = (int32_t*)malloc(sizeof(int32_t) * (size_t)(S > 0 ? S : 1));
+  for (int64_t i = 0; i < S; ++i) {
+    lv[i] = orc_level_of(len[i], L, x + 3 * i, rgb + 3 * i);
+    if (lv[i] >= 0) count[lv[i]] += 1;
+  }
+  for (int64_t k = 0; k < 15 * G; ++k) allow_coef[k] = 0.0;
+  double t2 = tau * tau;
+  int64_t na = 0;
+  for (int64_t i = 0; i < S; ++i) {
+    int32_t l = lv[i];
+    if (l < 0) continue;
+    const double* xi = x + 3 * i;
+    int64_t kbeg, kend;
+    if (csr) {
+      int32_t c3[3]; const int32_t* dm = g_dims + 3 * l;
+      orc_sample_cell(xi, g_origin + 3 * l, g_inv + 3 * l, dm, c3);
+      int64_t cell = ((int64_t)c3[2] * dm[1] + c3[1]) * dm[0] + c3[0];
+      kbeg = csr[l].off[cell]; kend = csr[l].off[cell + 1];
+    } else { kbeg = goff[l]; kend = goff[l + 1]; }
+    double y[3] = {0.0, 0.0, 0.0}, a[3] = {0.0, 0.0, 0.0};
+    int amb = 0;
+    for (int64_t k = kbeg; k < kend; ++k) {
+      int64_t j = csr ? goff[l] + csr[l].idx[k] : k;
+      double d[3], t[3];
+      double Q = orc_Q(&gs[j], xi, d, t);
+      double e = exp(-0.5 * Q);
+      if (Q <= t2) for (int c = 0; c < 3; ++c) y[c] += gs[j].v[c] * e;
+      if (fabs(Q - t2) <= amb_rel * t2) { amb = 1; for (int c = 0; c < 3; ++c) a[c] += gs[j].v[c] * e; }
+    }
+    if (!amb) continue;
+    ++na;
+    double k3 = 3.0 * (double)count[l], g[3], gam[3];
+    for (int c = 0; c < 3; ++c) {
+      double xh = rgb[3 * i + c], r = xh - y[c], dd = y[c] + hdr_eps;
+      double dgdy;
+      if (mode == 0) { g[c] = (-2.0 * r / (dd * dd)) / k3; dgdy = (2.0 / (dd * dd) + 4.0 * r / (dd * dd * dd)) / k3; }
+      else {
+        g[c] = (-2.0 * r * (xh + hdr_eps) / (dd * dd * dd)) / k3;
+        dgdy = (2.0 * (xh + hdr_eps) / (dd * dd * dd) + 6.0 * r * (xh + hdr_eps) / (dd * dd * dd * dd)) / k3;
+      }
+      gam[c] = fabs(dgdy) * a[c];
+    }
+    for (int64_t k = kbeg; k < kend; ++k) {
+      int64_t j = csr ? goff[l] + csr[l].idx[k] : k;
+      double d[3], t[3];
+      double Q = orc_Q(&gs[j], xi, d, t);
+      int isamb = fabs(Q - t2) <= amb_rel * t2;
+      if (!(Q <= t2) && !isamb) continue;
+      double e = exp(-0.5 * Q), H = 0.0, gg[3];
+      for (int c = 0; c < 3; ++c) {
+        gg[c] = isamb ? fabs(g[c]) + gam[c] : gam[c];
+        H += gg[c] * gs[j].v[c];
+      }
+      double* aj = allow_coef + 15 * j;
+      for (int u = 0; u < 3; ++u) aj[u] += H * e * fabs(t[u]);
+      for (int u = 0; u < 3; ++u)
+        for (int w = 0; w < 3; ++w) aj[3 + 3 * u + w] += 0.5 * H * e * fabs(d[u] * d[w]);
+      for (int c = 0; c < 3; ++c) aj[12 + c] += gg[c] * e;
+    }
+  }
+  /* the chain rule of C5 with absolute values */
+  for (int64_t j = 0; j < G; ++j) {
+    const orc_gauss* gj = &gs[j];
+    const double* aj = allow_coef + 15 * j;
+    const double* p = P + j * NP;
+    double* out = allow_raw + NP * j;
+    for (int u = 0; u < 3; ++u) out[u] = aj[u];
+    for (int k = 0; k < 3; ++k) {
+      double acc = 0.0;
+      for (int u = 0; u < 3; ++u)
+        for (int w = 0; w < 3; ++w) acc += fabs(gj->R[u][k]) * aj[3 + 3 * u + w] * fabs(gj->R[w][k]);
+      out[10 + k] = 2.0 * gj->D[k] * acc;
+    }
+    if (gj->degenerate) {
+      for (int c = 0; c < 4; ++c) out[3 + c] = 0.0;
+    } else {
+      double dR[3][3], J[4][3][3], dqh[4], s = 0.0;
+      for (int u = 0; u < 3; ++u)
+        for (int b = 0; b < 3; ++b) {
+          double acc = 0.0;
+          for (int c = 0; c < 3; ++c) acc += aj[3 + 3 * u + c] * fabs(gj->R[c][b]);
+          dR[u][b] = 2.0 * acc * gj->D[b];
+        }
+      orc_dRdq(gj->qhat, J);
+      for (int c = 0; c < 4; ++c) {
+        double acc = 0.0;
+        for (int u = 0; u < 3; ++u) for (int b = 0; b < 3; ++b) acc += dR[u][b] * fabs(J[c][u][b]);
+        dqh[c] = acc;
+        s += fabs(gj->qhat[c]) * acc;
+      }
+      for (int c = 0; c < 4; ++c) out[3 + c] = (dqh[c] + fabs(gj->qhat[c]) * s) / gj->qnorm;
+    }
+    double dw = 0.0;
+    for (int c = 0; c < 3; ++c) dw += aj[12 + c] * gj->chat[c];
+    out[13] = dw * gj->w * (1.0 - gj->w);
+    for (int c = 0; c < 3; ++c) out[7 + c] = p[7 + c] > 0.0 ? gj->w * aj[12 + c] : 0.0;
+  }
+  *n_amb = na;
+  if (csr) { for (int l = 0; l < L; ++l) orc_csr_free(&csr[l]); free(csr); }
+  free(count); free(lv); free(gs);
+  return 0;
+}

@@ -65,10 +65,14 @@ def check_forward(y, yo, P, goff, x, lv, tau=3.0, what="", amb_rate=1e-4):
     return amb_count
 
 
-def check_grad_group(a, b, what, scale=None):
+def check_grad_group(a, b, what, scale=None, allow=None):
     """SURVEY 8(c) gradient bar for one (level, group): ||a - b|| / ||b|| <= 1e-4 AND, per
     element, |a_i - b_i| <= 1e-4 |b_i| + 1e-6 ||b||_inf (``scale`` replaces ||b||_inf / ||b||
-    for groups that are exactly zero in the oracle, e.g. the rotation of isotropic levels)."""
+    for groups that are exactly zero in the oracle, e.g. the rotation of isotropic levels).
+    ``allow`` (same shape, or None): reading A3's boundary allowance, the first-order bound of
+    what fp32 cut-off flips of pairs with |Q - tau^2| <= 1e-4 tau^2 can change
+    (oracle.grad_allowance, pinned against real flips in test_oracle_pins); it widens the
+    per-element bar only."""
     a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
     nb = np.linalg.norm(b)
     ninf = np.abs(b).max() if b.size else 0.0
@@ -78,6 +82,8 @@ def check_grad_group(a, b, what, scale=None):
     rel = np.linalg.norm(a - b) / nb
     assert rel <= 1e-4, (what, "relative L2", rel)
     tol = 1e-4 * np.abs(b) + 1e-6 * ninf
+    if allow is not None:
+        tol = tol + np.asarray(allow, np.float64) * (1 + 1e-6)
     bad = np.abs(a - b) > tol
     if bad.any():
         i = np.unravel_index(np.argmax(np.abs(a - b) - tol), a.shape)
@@ -86,9 +92,10 @@ def check_grad_group(a, b, what, scale=None):
     return rel
 
 
-def check_grads(g, go, goff, what="", iso_levels=()):
+def check_grads(g, go, goff, what="", iso_levels=(), allow=None):
     """Both gradient bars on every (level, group) of raw 14-parameter gradients; levels in
-    ``iso_levels`` hold isotropic Gaussians, whose rotation gradient is exactly 0 (C5)."""
+    ``iso_levels`` hold isotropic Gaussians, whose rotation gradient is exactly 0 (C5).
+    ``allow``: oracle.grad_allowance()["raw"] (A3 boundary flips), or None."""
     for l in range(len(goff) - 1):
         sl = slice(goff[l], goff[l + 1])
         for name, cs in oracle.GROUP_SLICES.items():
@@ -97,7 +104,8 @@ def check_grads(g, go, goff, what="", iso_levels=()):
                 ref = np.abs(go[sl]).max()
                 assert np.abs(a).max() <= 1e-6 * ref + 1e-12, (what, l, "isotropic dq")
                 continue
-            check_grad_group(a, b, f"{what} level {l} {name}")
+            check_grad_group(a, b, f"{what} level {l} {name}",
+                             allow=None if allow is None else allow[sl, cs])
 
 
 # ----------------------------------------------------------------------- create (C7)
@@ -295,7 +303,9 @@ def test_gradient_parity(gsc, mode):
     for l in range(3):
         assert st.count[l] == ro["count"][l]
         assert abs(st.loss[l] - ro["loss"][l]) <= 1e-4 * ro["loss"][l]
-    check_grads(g, go, c.goff, f"cfg1 mode {mode}", iso_levels=(1, 2))
+    al = oracle.grad_allowance(c.goff, P, x.astype(np.float64), ln, rgb.astype(np.float64),
+                               mode=mode, grids=c.grids())
+    check_grads(g, go, c.goff, f"cfg1 mode {mode}", iso_levels=(1, 2), allow=al["raw"])
     assert st.n_pairs == ro["npairs"] or abs(st.n_pairs - ro["npairs"]) <= 1e-4 * ro["npairs"]
 
 
@@ -690,7 +700,9 @@ def test_fit_query_lookups_and_gradients(gsc):
     for l in range(3):
         assert st.count[l] == ro["count"][l]
         assert abs(st.loss[l] - ro["loss"][l]) <= 1e-4 * ro["loss"][l]
-    check_grads(g, ro["grad"], c.goff, "fit_query", iso_levels=(1, 2))
+    al = oracle.grad_allowance(c.goff, P, x.astype(np.float64), ln, rgb.astype(np.float64),
+                               grids=c.grids())
+    check_grads(g, ro["grad"], c.goff, "fit_query", iso_levels=(1, 2), allow=al["raw"])
     assert st.step == 1 and st.n_in == len(x)
 
 
@@ -854,7 +866,9 @@ def test_coherent_sample_order(gsc):
     ro = oracle.loss_grad(c.goff, P, x.astype(np.float64), ln, rgb.astype(np.float64), grids=c.grids())
     for l in range(3):
         assert st.count[l] == ro["count"][l]
-    check_grads(g, ro["grad"], c.goff, "morton", iso_levels=(0, 1, 2))
+    al = oracle.grad_allowance(c.goff, P, x.astype(np.float64), ln, rgb.astype(np.float64),
+                               grids=c.grids())
+    check_grads(g, ro["grad"], c.goff, "morton", iso_levels=(0, 1, 2), allow=al["raw"])
 
 
 def test_fit_query_fixed_level_and_tiny_caches(gsc):

@@ -35,10 +35,11 @@ def gsc():
 COEF_GROUPS = {"dmu": slice(0, 3), "dA": slice(3, 9), "dv": slice(9, 12)}
 
 
-def check_coef(dev, st, ro, goff, what, lite_levels=()):
+def check_coef(dev, st, ro, goff, what, lite_levels=(), allow=None):
     """Device coefficient gradients (unnormalised sums) vs the oracle's (normalised by
     1/(3 k_l)): every (level, coefficient group) under both gradient bars; on levels run by
-    the lite backward (isotropic, scale group frozen) dA is exactly 0 on the device."""
+    the lite backward (isotropic, scale group frozen) dA is exactly 0 on the device.
+    ``allow``: oracle.grad_allowance()["coef"] (A3 boundary flips), or None."""
     for l in range(len(goff) - 1):
         sl = slice(goff[l], goff[l + 1])
         k = int(st.count[l])
@@ -50,7 +51,17 @@ def check_coef(dev, st, ro, goff, what, lite_levels=()):
             if name == "dA" and l in lite_levels:
                 assert np.all(dev[sl, cs] == 0.0), (what, l, "lite dA")
                 continue
-            check_grad_group(d[:, cs], ro["coef"][sl, cs], f"{what} level {l} {name}")
+            check_grad_group(d[:, cs], ro["coef"][sl, cs], f"{what} level {l} {name}",
+                             allow=None if allow is None else allow[sl, cs])
+
+
+def allowance(c, P, x, ln, rgb, **kw):
+    """Reading A3's per-element gradient allowance for this batch; the share of samples
+    with an ambiguous pair is bounded like the forward's (expected rare)."""
+    al = oracle.grad_allowance(c.goff, P, x.astype(np.float64), ln, rgb.astype(np.float64),
+                               grids=c.grids(), **kw)
+    assert al["n_amb"] <= max(10, 5e-3 * len(x)), al["n_amb"]
+    return al
 
 
 def test_cfg2_full_frame_gradients_lite_and_raw(gsc):
@@ -69,15 +80,16 @@ def test_cfg2_full_frame_gradients_lite_and_raw(gsc):
     torch.cuda.synchronize()
     for l in range(4):
         assert abs(st.loss[l] - ro["loss"][l]) <= 1e-4 * ro["loss"][l]
+    al = allowance(c, P, x, ln, rgb)
     dev = np.concatenate([c.debug_coef_grads(l) for l in range(4)])
-    check_coef(dev, st, ro, c.goff, "cfg2 lite", lite_levels=(0, 1, 2, 3))
+    check_coef(dev, st, ro, c.goff, "cfg2 lite", lite_levels=(0, 1, 2, 3), allow=al["coef"])
     c2 = gsc.GSCache(counts, cuda(pos), cuda(alb), seed=2)
     c2.reserve(len(x), 0)
     c2.debug_enable_grads(True)
     st2 = c2.fit(cuda(x), cuda(ln), cuda(rgb))
     torch.cuda.synchronize()
     g = np.concatenate([c2.debug_grads_rows(l) for l in range(4)]).astype(np.float64)
-    check_grads(g, ro["grad"], c2.goff, "cfg2 raw", iso_levels=(0, 1, 2, 3))
+    check_grads(g, ro["grad"], c2.goff, "cfg2 raw", iso_levels=(0, 1, 2, 3), allow=al["raw"])
     assert st2.n_pairs == st.n_pairs
 
 
@@ -105,10 +117,11 @@ def test_cfg2_full_frame_anisotropic_scale_lr(gsc):
     oc = oracle.OracleCache(counts, P, hp=dict(lr=lr), grids=c.grids())
     ro = oracle.loss_grad(c.goff, P, x.astype(np.float64), ln, rgb.astype(np.float64), grids=c.grids())
     oc.fit(x.astype(np.float64), ln, rgb.astype(np.float64))
+    al = allowance(c, P, x, ln, rgb)
     g = np.concatenate([c.debug_grads_rows(l) for l in range(4)]).astype(np.float64)
-    check_grads(g, ro["grad"], c.goff, "cfg2 aniso")
+    check_grads(g, ro["grad"], c.goff, "cfg2 aniso", allow=al["raw"])
     dev = np.concatenate([c.debug_coef_grads(l) for l in range(4)])
-    check_coef(dev, st, ro, c.goff, "cfg2 aniso coef")
+    check_coef(dev, st, ro, c.goff, "cfg2 aniso coef", allow=al["coef"])
     P1 = rows(c)
     # the scale group now steps: first AdamW step = -eta sign(g) wherever g is well above the
     # fp32 rounding level (test_first_step_matches_oracle_update's criterion)
@@ -147,8 +160,9 @@ def test_far_outside_grid_samples(gsc):
     for l in range(3):
         assert st.count[l] == ro["count"][l]
         assert abs(st.loss[l] - ro["loss"][l]) <= 1e-4 * ro["loss"][l]
+    al = allowance(c, P, x, ln, rgb)
     g = np.concatenate([c.debug_grads_rows(l) for l in range(3)]).astype(np.float64)
-    check_grads(g, ro["grad"], c.goff, "outside-grid", iso_levels=(0, 1, 2))
+    check_grads(g, ro["grad"], c.goff, "outside-grid", iso_levels=(0, 1, 2), allow=al["raw"])
     assert np.isfinite(rows(c)).all()
 
 

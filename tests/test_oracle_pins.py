@@ -360,6 +360,30 @@ def test_coefficient_gradients_vs_finite_differences():
         np.testing.assert_allclose(ds, fd[j, 10:13], rtol=1e-6, atol=1e-9)
 
 
+def test_grad_allowance_bounds_actual_cutoff_flips():
+    """The A3 boundary allowance (oracle.grad_allowance, test infrastructure) must bound what
+    flipping the ambiguous pairs really does: the gradients with the cut-off moved to
+    tau^2 (1 -+ 0.9e-4) differ from the tau^2 ones by at most the allowance (amb_rel 1e-4)."""
+    r = np.random.default_rng(40)
+    G = 60
+    P = rand_params(G, r)
+    P[:, 0:3] *= 0.8
+    x = r.uniform(-0.6, 0.6, (20000, 3))
+    ln = np.ones(len(x), np.int32)
+    rgb = r.uniform(0, 2, (len(x), 3))
+    goff = [0, G]
+    base = oracle.loss_grad(goff, P, x, ln, rgb, tau=3.0)
+    al = oracle.grad_allowance(goff, P, x, ln, rgb, tau=3.0)
+    assert al["n_amb"] > 0
+    for f in (1 - 0.9e-4, 1 + 0.9e-4):
+        t = 3.0 * math.sqrt(f)
+        o = oracle.loss_grad(goff, P, x, ln, rgb, tau=t)
+        for key, a in (("grad", al["raw"]), ("coef", al["coef"])):
+            d = np.abs(o[key] - base[key])
+            assert np.all(d <= a * 1.01 + 1e-15), (key, f, (d - a).max())
+        assert np.abs(o["grad"] - base["grad"]).max() > 0      # some pair really flipped
+
+
 def _check_groups(g, fd, tol):
     for name, sl in oracle.GROUP_SLICES.items():
         a, b = g[:, sl], fd[:, sl]
