@@ -693,7 +693,7 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
   if (gc_status e = mark_staging_free(F, s, set)) return e;
   if (tail_ev) CK(cudaStreamWaitEvent(s, tail_ev, 0));     // the previous step is complete
   FitArgs fa;
-  fa.work = F.work; fa.n_work = F.totals + 1; fa.csr_off = c->csr_off; fa.lrec = c->csr_rec;
+  fa.work = F.work; fa.n_work = F.totals + 1; fa.csr_off = c->csr_off; fa.lrec = c->csr_rec; fa.cap = c->csr_cap;
   fa.bin = F.bin;
   fa.grad = c->grad; fa.partial = c->partial;
   const float tau = c->hp.cutoff_sigma;
@@ -811,7 +811,7 @@ static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_le
   launch_scatter(pos, nullptr, S, Q.cell_start, b, s, &c->prof);
   if (gc_status e = mark_staging_free(Q, s, set)) return e;
   QueryArgs qa;
-  qa.work = Q.work; qa.n_work = Q.totals + 1; qa.csr_off = c->csr_off; qa.lrec = c->csr_rec;
+  qa.work = Q.work; qa.n_work = Q.totals + 1; qa.csr_off = c->csr_off; qa.lrec = c->csr_rec; qa.cap = c->csr_cap;
   qa.bin = Q.bin; qa.out = dout;
   Epilogue ep;
   if (gc_status e = ep.stage(att, beta, unb, S, s)) return e;

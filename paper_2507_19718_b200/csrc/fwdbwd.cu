@@ -525,8 +525,10 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
     --left;
     if (it >= n_work) break;
     const WorkItem wi = a.work[it];
-    const int lo = (int)__ldg(a.csr_off + wi.cell);
-    const int C = (int)__ldg(a.csr_off + wi.cell + 1) - lo;
+    // clamped to the list capacity: after an overflowing rebuild the offsets run past it (the
+    // entries there were dropped; the call reports GC_FLAG_LISTS_OVERFLOWED and skips its step)
+    const int lo = (int)min(__ldg(a.csr_off + wi.cell), a.cap);
+    const int C = (int)min(__ldg(a.csr_off + wi.cell + 1), a.cap) - lo;
     float xa[3], xb[3], ta[3] = {0.f, 0.f, 0.f}, tb[3] = {0.f, 0.f, 0.f};
     {                                            // one 32-byte load per sample: x y z r | g b - -
       const float kNaN = __int_as_float(0x7fffffff);   // inactive samples: never inside
@@ -685,8 +687,10 @@ __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
     --left;
     if (it >= n_work) break;
     const WorkItem wi = a.work[it];
-    const int lo = (int)__ldg(a.csr_off + wi.cell);
-    const int C = (int)__ldg(a.csr_off + wi.cell + 1) - lo;
+    // clamped to the list capacity: after an overflowing rebuild the offsets run past it (the
+    // entries there were dropped; the call reports GC_FLAG_LISTS_OVERFLOWED and skips its step)
+    const int lo = (int)min(__ldg(a.csr_off + wi.cell), a.cap);
+    const int C = (int)min(__ldg(a.csr_off + wi.cell + 1), a.cap) - lo;
     float xa[3], xb[3];
     float4 pa, pb4;
     load_pos(a.bin, 2, wi.start, wi.count, lane, xa, pa);

@@ -122,7 +122,7 @@ struct CellRef {
 CellRef cell_ref(const LevelGeom& g);
 struct FitArgs {
   const WorkItem* work; const uint32_t* n_work;
-  const uint32_t* csr_off; const float4* lrec;
+  const uint32_t* csr_off; const float4* lrec; uint32_t cap;   // cap: list capacity (entries)
   const float4* bin;
   float* grad;          // [G][12]
   double* partial;      // [grid][kMaxL + 2]: per-block loss sums, pairs, candidates
@@ -135,7 +135,7 @@ int fwdbwd_grid();
 void launch_fwdbwd(const FitArgs& a, int grid, cudaStream_t s, Profiler* prof);
 struct QueryArgs {
   const WorkItem* work; const uint32_t* n_work;
-  const uint32_t* csr_off; const float4* lrec;
+  const uint32_t* csr_off; const float4* lrec; uint32_t cap;
   const float4* bin;
   float* out; float tau2;
   const float* att; const float* beta; const float* unb;   // optional f3 epilogue (caller order)
