@@ -198,15 +198,52 @@ gc_status gc_grid(gc_cache c, int level, double origin[3], double inv_cell[3], i
 /* Number of levels and per-level Gaussian counts (host array of GC_MAX_LEVELS). */
 gc_status gc_info(gc_cache c, int* levels, int64_t* counts);
 
-/* Multi-GPU data parallelism (north star; none in the paper): every rank calls gc_fit
- * with its own shard; one NCCL all-reduce (sum) of the per-level coefficient gradients and
- * level statistics per step makes every replica take the identical AdamW step.
+/* Multi-GPU (north star; none in the paper, which runs on one GPU).
  * nccl_uid: 128-byte ncclUniqueId produced by rank 0 (gc_nccl_unique_id) and broadcast by
- * the caller.  mode: 0 = data parallel (1 = level-sharded: GC_ERR_UNSUPPORTED for now).
+ * the caller; rank in [0, world).  Every rank holds the same cache (same gc_create arguments).
+ *  mode 0 = data parallel: every rank calls gc_fit / gc_fit_query with its own shard of the
+ *    samples; one NCCL all-reduce (sum) of the per-level coefficient gradients and level
+ *    statistics per step makes every replica take the identical AdamW step (C9: the result
+ *    equals the one-rank result on the concatenated batch up to summation order).  Lookups
+ *    are local (replicas).  Graph-capturable.
+ *  mode 1 = level-sharded: levels are partitioned into contiguous groups owned by contiguous
+ *    rank groups (gc_level_plan over the level weights, gc_set_level_weights, default the
+ *    per-level Gaussian counts); every call is COLLECTIVE: each rank passes its own samples /
+ *    lookups, which are routed (ncclSend/ncclRecv) to the owning group of their level and
+ *    split round-robin inside it; a group sums its levels' gradients over its own
+ *    communicator (ncclCommSplit), level statistics are summed over all ranks (global k_l,
+ *    identical t), and each rank steps only the levels it owns.  Lookup results return to the
+ *    caller's rank in caller order.  gc_params is collective too (the owner broadcasts the
+ *    level).  Each call synchronises the host once (the routed sizes are NCCL host
+ *    arguments), so mode 1 is not graph-capturable (GC_ERR_STATE under capture), and the
+ *    gc_query_radiance epilogue is not available (GC_ERR_UNSUPPORTED).
  * nccl_uid == NULL with world == 1 detaches; a uid with world == 1 builds a one-rank
- * communicator (the all-reduce then runs as an identity, used to test the path). */
+ * communicator (mode 0: the all-reduce runs as an identity; mode 1: every sample is routed to
+ * this rank through ncclSend/ncclRecv to itself -- both used to test the paths on one GPU). */
 gc_status gc_nccl_unique_id(void* uid128);
 gc_status gc_set_comm(gc_cache c, const void* nccl_uid, int rank, int world, int mode);
+
+/* Level weights of the mode-1 plan (weights [levels], finite, >= 0; NULL = the default, each
+ * level's share of the Gaussians).  Takes effect at the next gc_set_comm. */
+gc_status gc_set_level_weights(gc_cache c, const double* weights);
+
+/* The mode-1 plan as a pure host function (no device, no handle).  Levels 0..levels-1 with
+ * weights [levels] (>= 0) go to n_groups = min(levels, world) groups of contiguous levels
+ * owned by contiguous rank ranges (group g: ranks group_first_rank[g] .. + group_size[g]):
+ *  world >= levels: one level per group; the surplus ranks join, one at a time, the level
+ *    with the largest weight per rank (data parallel inside that level's group -- level 0,
+ *    with most samples and Gaussians, is the hybrid case of SURVEY 8(e));
+ *  world < levels: one rank per group; the levels are cut into world contiguous ranges
+ *    minimising the largest range weight (exact dynamic programme).
+ * Ties resolve by a fixed order, so every rank computes the same plan.  group_of_level
+ * [levels], group_first_rank / group_size [>= levels] (host).  world <= 1024. */
+gc_status gc_level_plan(int levels, const double* weights, int world, int32_t* group_of_level,
+                        int32_t* group_first_rank, int32_t* group_size, int* n_groups);
+
+/* Communicator state: mode (-1 none, 0, 1), rank, world, the bit mask of levels this rank
+ * steps, and the size of its level group (mode 0: world).  Each pointer nullable. */
+gc_status gc_comm_info(gc_cache c, int* mode, int* rank, int* world, int* owned_levels_mask,
+                       int* group_size);
 
 /* ---- debug / parity exports (not on the hot path) ---------------------------------- */
 
@@ -223,9 +260,9 @@ gc_status gc_debug_enable_grads(gc_cache c, int enable);
  * optimizer's normalisation, C4).  Synchronises the stream. */
 gc_status gc_debug_coef_grads(gc_cache c, int level, float* dst, gc_stream stream);
 /* Generation of the culling-list buffers: incremented whenever a capacity growth reallocated
- * them.  A CUDA graph captured at an earlier generation keeps using (and rebuilding) the old
- * buffers, which stay allocated until gc_destroy (memory-safe, but no longer shared with
- * eager calls): re-capture after the generation changes. */
+ * them.  The kernels reach the lists through the handle's device state, not through launch
+ * arguments, so CUDA graphs captured at an earlier generation stay valid and use the grown
+ * lists (no re-capture needed); the counter is informational. */
 gc_status gc_list_generation(gc_cache c, uint64_t* gen);
 /* Raw gradients d(sum_l L_l)/d(theta) of the last gc_fit (C5), in gc_level_params layout. */
 gc_status gc_debug_grads(gc_cache c, int level, gc_level_params* dst, gc_stream stream);

@@ -286,10 +286,13 @@ def loss_grad(goff, P, x, length, rgb, tau=3.0, hdr_eps=0.01, mode=0, grids=None
 
 
 def grad_allowance(goff, P, x, length, rgb, tau=3.0, hdr_eps=0.01, mode=0, grids=None,
-                   amb_rel=1e-4):
+                   amb_rel=1e-4, cond=False):
     """First-order bound of the gradient change that reading A3's fp32 cut-off flips can
     cause (pairs with |Q - tau^2| <= amb_rel tau^2), per Gaussian: coefficient layout like
-    loss_grad()['coef'] and raw [G][14]; plus the number of samples with an ambiguous pair."""
+    loss_grad()['coef'] and raw [G][14]; plus the number of samples with an ambiguous pair.
+    cond=True returns instead the condition magnitudes kappa (reading A21): the same gradients
+    summed and chained with absolute values, so that a relative perturbation delta of every
+    summed term moves a gradient element by at most delta * kappa."""
     goff = _i64(goff)
     L = len(goff) - 1
     P = _d(P).reshape(-1, NP)
@@ -302,8 +305,8 @@ def grad_allowance(goff, P, x, length, rgb, tau=3.0, hdr_eps=0.01, mode=0, grids
                              C.c_double(hdr_eps), C.c_int(mode), C.c_int64(len(x)),
                              _p(x, np.float64), _p(ln, np.int32), _p(rgb, np.float64),
                              _p(o, np.float64), _p(ic, np.float64), _p(dm, np.int32),
-                             C.c_double(amb_rel), _p(ac, np.float64), _p(ar, np.float64),
-                             C.byref(na))
+                             C.c_double(amb_rel), C.c_int(1 if cond else 0), _p(ac, np.float64),
+                             _p(ar, np.float64), C.byref(na))
     coef = np.stack([ac[:, 0], ac[:, 1], ac[:, 2], ac[:, 3], ac[:, 7], ac[:, 11], ac[:, 4],
                      ac[:, 5], ac[:, 8], ac[:, 12], ac[:, 13], ac[:, 14]], axis=1)
     return dict(coef=coef, raw=ar, n_amb=na.value)

@@ -718,10 +718,15 @@ int orc_fit_step(int L, const int64_t* goff, double* P, double* M, double* V, in
  * allow_coef [G][15] (dmu 3, dA 9 full, dv 3) and allow_raw [G][14] (the bound carried through
  * the chain rule of C5 with absolute values).  Samples with an ambiguous pair are counted in
  * *n_amb.  Culled evaluation when g_origin != NULL (same pair sets as orc_loss_grad). */
+/* cond != 0 computes instead the CONDITION magnitudes of the same gradients: every pair inside
+ * the cut-off contributes with absolute values (|g| in place of g, |h e t|, |h e d d^T| / 2,
+ * |g e|) and the chain rule is applied with absolute values, so kappa_i >= |grad_i|; a
+ * relative perturbation delta of every summed term (fp32 rounding, atomic summation order)
+ * changes grad_i by at most delta kappa_i to first order. */
 int orc_grad_allowance(int L, const int64_t* goff, const double* P, double tau, double hdr_eps,
                        int mode, int64_t S, const double* x, const int32_t* len, const double* rgb,
                        const double* g_origin, const double* g_inv, const int32_t* g_dims,
-                       double amb_rel, double* allow_coef, double* allow_raw, int64_t* n_amb) {
+                       double amb_rel, int cond, double* allow_coef, double* allow_raw, int64_t* n_amb) {
   int64_t G = goff[L];
   orc_gauss* gs = orc_activate_all(G, P);
   orc_csr* csr = NULL;
@@ -761,8 +766,8 @@ int orc_grad_allowance(int L, const int64_t* goff, const double* P, double tau, 
       if (Q <= t2) for (int c = 0; c < 3; ++c) y[c] += gs[j].v[c] * e;
       if (fabs(Q - t2) <= amb_rel * t2) { amb = 1; for (int c = 0; c < 3; ++c) a[c] += gs[j].v[c] * e; }
     }
-    if (!amb) continue;
-    ++na;
+    if (!amb && !cond) continue;
+    na += amb;
     double k3 = 3.0 * (double)count[l], g[3], gam[3];
     for (int c = 0; c < 3; ++c) {
       double xh = rgb[3 * i + c], r = xh - y[c], dd = y[c] + hdr_eps;
@@ -779,10 +784,11 @@ int orc_grad_allowance(int L, const int64_t* goff, const double* P, double tau, 
       double d[3], t[3];
       double Q = orc_Q(&gs[j], xi, d, t);
       int isamb = fabs(Q - t2) <= amb_rel * t2;
-      if (!(Q <= t2) && !isamb) continue;
+      if (cond) { if (!(Q <= t2)) continue; }
+      else if (!(Q <= t2) && !isamb) continue;
       double e = exp(-0.5 * Q), H = 0.0, gg[3];
       for (int c = 0; c < 3; ++c) {
-        gg[c] = isamb ? fabs(g[c]) + gam[c] : gam[c];
+        gg[c] = cond ? fabs(g[c]) : (isamb ? fabs(g[c]) + gam[c] : gam[c]);
         H += gg[c] * gs[j].v[c];
       }
       double* aj = allow_coef + 15 * j;

@@ -27,7 +27,8 @@ EXPORTS = ["gc_default_hparams", "gc_create", "gc_destroy", "gc_reserve", "gc_fi
            "gc_query_radiance", "gc_fit_query", "gc_set_deferred_step", "gc_flush",
            "gc_params", "gc_set_params", "gc_reset_schedule", "gc_grid", "gc_info",
            "gc_nccl_unique_id", "gc_set_comm", "gc_debug_enable_grads", "gc_debug_grads",
-           "gc_debug_coef_grads", "gc_list_generation",
+           "gc_debug_coef_grads", "gc_list_generation", "gc_set_level_weights", "gc_level_plan",
+           "gc_comm_info",
            "gc_debug_cull", "gc_debug_levels", "gc_profile_enable", "gc_profile_read",
            "gc_last_error", "gc_status_string"]
 
@@ -107,6 +108,9 @@ def lib():
             "gc_info": (i32, [vp, vp, vp]),
             "gc_nccl_unique_id": (i32, [vp]),
             "gc_set_comm": (i32, [vp, vp, i32, i32, i32]),
+            "gc_set_level_weights": (i32, [vp, vp]),
+            "gc_level_plan": (i32, [i32, vp, i32, vp, vp, vp, vp]),
+            "gc_comm_info": (i32, [vp, vp, vp, vp, vp, vp]),
             "gc_debug_enable_grads": (i32, [vp, i32]),
             "gc_debug_grads": (i32, [vp, i32, vp, vp]),
             "gc_debug_coef_grads": (i32, [vp, i32, vp, vp]),
@@ -370,6 +374,18 @@ class GSCache:
         buf = C.create_string_buffer(uid, 128) if uid is not None else None
         _check(lib().gc_set_comm(self.h, buf, rank, world, mode))
 
+    def set_level_weights(self, weights=None):
+        """Level weights of the level-sharded plan (mode 1); None = per-level Gaussian share."""
+        w = None if weights is None else (C.c_double * self.L)(*[float(v) for v in weights])
+        _check(lib().gc_set_level_weights(self.h, w))
+
+    def comm_info(self):
+        v = [C.c_int() for _ in range(5)]
+        _check(lib().gc_comm_info(self.h, *[C.byref(x) for x in v]))
+        return dict(mode=v[0].value, rank=v[1].value, world=v[2].value,
+                    owned_levels=[l for l in range(self.L) if (v[3].value >> l) & 1],
+                    group_size=v[4].value)
+
     # ----------------------------------------------------------------- debug
     def debug_enable_grads(self, on=True, coef=False):
         """Bit 0 (on): raw 14-parameter gradients; bit 1 (coef): the coefficient-gradient
@@ -433,6 +449,20 @@ class GSCache:
                 torch.cuda.synchronize(self.device)
         except Exception:
             pass
+
+
+def level_plan(weights, world: int):
+    """gc_level_plan (pure host function): returns (group_of_level, [(first_rank, size)])."""
+    L = len(weights)
+    w = (C.c_double * L)(*[float(v) for v in weights])
+    gl = (C.c_int32 * L)()
+    fr = (C.c_int32 * L)()
+    gs = (C.c_int32 * L)()
+    ng = C.c_int()
+    st = lib().gc_level_plan(L, w, world, gl, fr, gs, C.byref(ng))
+    if st != 0:
+        raise GCError(st, "gc_level_plan: bad arguments")
+    return list(gl), [(fr[g], gs[g]) for g in range(ng.value)]
 
 
 def nccl_unique_id() -> bytes:

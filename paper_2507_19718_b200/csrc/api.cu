@@ -113,9 +113,6 @@ struct gc_cache_s {
   std::vector<StatsPayload*> payloads;    // all payloads (freed at destroy)
   std::vector<StatsPayload*> ring;        // the reusable ones of eager calls
   size_t payload_next = 0, captured_payloads = 0;
-  std::vector<void*> retired;             // culling lists replaced by a capacity growth: kept
-                                          // (not freed) until gc_destroy, because a CUDA graph
-                                          // captured earlier may still reference them
   uint64_t list_generation = 0;           // bumped by every reallocation of the culling lists
   CellRef cref{};                         // fp32 cell geometry of the evaluators (CellRef)
   int dbg_mode = 0;                       // gc_debug_enable_grads: bit 0 raw grads, bit 1 coef grads
@@ -123,6 +120,23 @@ struct gc_cache_s {
   Profiler prof;
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
+  // level-sharded mode (gc_set_comm mode 1): plan, the group communicator of this rank's
+  // levels, and the routing buffers (shard.cu)
+  int mode = 0;
+  RoutePlan plan{};
+  ncclComm_t gcomm = nullptr;
+  int glo = 0, ghi = 0, gsize = 1;        // this rank's group: levels [glo, ghi), gsize ranks
+  double lvl_w[kMaxL] = {0};
+  bool has_w = false;
+  uint32_t *r_count = nullptr, *r_all = nullptr, *r_base = nullptr, *r_cursor = nullptr;
+  uint32_t *h_all = nullptr, *h_base = nullptr;          // pinned
+  float4 *r_send = nullptr, *r_recv = nullptr;
+  int64_t r_send_cap = 0, r_recv_cap = 0;
+  float *r_pos = nullptr, *r_rgb = nullptr, *r_res = nullptr, *r_back = nullptr;
+  int32_t* r_len = nullptr;
+  uint32_t* r_perm = nullptr;
+  int64_t r_in_cap = 0, r_perm_cap = 0, r_send_cap_back = 0;
+  std::vector<int64_t> rt_send, rt_recv, rt_soff, rt_roff;   // last routing's per-peer counts/offsets
   float* pack_tmp = nullptr;
   int64_t pack_cap = 0;
   cudaStream_t side = nullptr;            // gc_fit_query: lookups run beside the fit samples' ingest
@@ -251,6 +265,15 @@ static gc_status rebuild_csr(gc_cache c, cudaStream_t s, bool recompute_records)
 // of their capacity (Gaussians growing, scale LR > 0) are reallocated to 4x their size; lists
 // that overflowed (entries past the capacity were dropped, so the lookups / fit that used them
 // were incomplete) are reallocated AND rebuilt, and the call reports GC_ERR_STATE once.
+// The culling-list buffers as the kernels see them (DevState::lrec / lovf / lcap / lovf_cap).
+static gc_status publish_lists(gc_cache c) {
+  CK(cudaMemcpy(&c->st->lrec, &c->csr_rec, sizeof(float4*), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(&c->st->lovf, &c->csr_ovf, sizeof(uint32_t*), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(&c->st->lcap, &c->csr_cap, sizeof(uint32_t), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(&c->st->lovf_cap, &c->csr_cap, sizeof(uint32_t), cudaMemcpyHostToDevice));
+  return GC_OK;
+}
+
 static gc_status csr_guard(gc_cache c, cudaStream_t s) {
   const uint32_t total = *(volatile uint32_t*)c->hcsr;
   if (total <= c->csr_cap / 2 || capturing(s)) return GC_OK;
@@ -262,8 +285,9 @@ static gc_status csr_guard(gc_cache c, cudaStream_t s) {
   CK(dalloc(&ovf, cap)); CK(dalloc(&lrec, 4 * cap));
   const uint64_t keep = std::min<uint64_t>(total, c->csr_cap);
   CK(cudaMemcpy(lrec, c->csr_rec, sizeof(float4) * 4 * keep, cudaMemcpyDeviceToDevice));
-  c->retired.push_back(c->csr_ovf); c->retired.push_back(c->csr_rec);   // a captured graph may
-  c->csr_ovf = ovf; c->csr_rec = lrec; c->csr_cap = (uint32_t)cap;       // still point at them
+  cudaFree(c->csr_ovf); cudaFree(c->csr_rec);     // (kernels reach the lists through DevState,
+  c->csr_ovf = ovf; c->csr_rec = lrec; c->csr_cap = (uint32_t)cap;   // captured graphs included)
+  if (gc_status e = publish_lists(c)) return e;
   c->list_generation += 1;
   if (!overflowed) return GC_OK;
   CK(cudaMemset(&c->st->csr_overflow, 0, sizeof(unsigned int)));
@@ -359,6 +383,89 @@ static gc_status emit_stats(gc_cache c, gc_fit_stats* user, cudaStream_t s) {
   return GC_OK;
 }
 
+// ------------------------------------------------------------ level-sharded routing (mode 1)
+static bool routed(gc_cache c) { return c->mode == 1 && c->comm != nullptr; }
+
+template <class T>
+static gc_status grow(T** p, int64_t* cap, int64_t n) {
+  if (*cap >= n && *p) return GC_OK;
+  if (*p) { CK(cudaDeviceSynchronize()); cudaFree(*p); *p = nullptr; }
+  const int64_t m = std::max<int64_t>(n + n / 4, 1024);
+  CK(dalloc(p, m));
+  *cap = m;
+  return GC_OK;
+}
+
+// Sends every valid sample (fit: rgb != NULL) or lookup of this rank to the rank owning its
+// level (RoutePlan) and receives the ones this rank owns: per-destination counts, one
+// all-gather of the W x W count matrix, a host synchronisation (NCCL point-to-point sizes are
+// host arguments: mode 1 is not graph-capturable), the pack pass, and one grouped
+// ncclSend/ncclRecv.  The received records are unpacked into c->r_pos / r_len / r_rgb (*R).
+static gc_status route_exchange(gc_cache c, cudaStream_t s, const float* pos, const int32_t* len, const float* rgb,
+                                int level_fixed, int64_t S, float* out_zero, int64_t* R) {
+  const int W = c->world, me = c->rank;
+  const bool fit = rgb != nullptr;
+  const int words = fit ? 2 : 1;                         // float4 per record
+  CK(cudaMemsetAsync(c->r_count, 0, sizeof(uint32_t) * W, s));
+  CK(cudaMemsetAsync(c->r_cursor, 0, sizeof(uint32_t) * W, s));
+  launch_route(pos, len, rgb, level_fixed, S, c->plan, 0, c->r_count, nullptr, nullptr, nullptr, nullptr, nullptr, s,
+               &c->prof);
+  NK(ncclAllGather(c->r_count, c->r_all, (size_t)W, ncclUint32, c->comm, s));
+  CK(cudaMemcpyAsync(c->h_all, c->r_all, sizeof(uint32_t) * W * W, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  c->rt_send.assign(W, 0); c->rt_recv.assign(W, 0); c->rt_soff.assign(W + 1, 0); c->rt_roff.assign(W + 1, 0);
+  for (int p = 0; p < W; ++p) {
+    c->rt_send[p] = c->h_all[(size_t)me * W + p];
+    c->rt_recv[p] = c->h_all[(size_t)p * W + me];
+    c->rt_soff[p + 1] = c->rt_soff[p] + c->rt_send[p];
+    c->rt_roff[p + 1] = c->rt_roff[p] + c->rt_recv[p];
+  }
+  const int64_t n_send = c->rt_soff[W], n_recv = c->rt_roff[W];
+  if (gc_status e = grow(&c->r_send, &c->r_send_cap, words * std::max<int64_t>(n_send, 1))) return e;
+  if (gc_status e = grow(&c->r_recv, &c->r_recv_cap, words * std::max<int64_t>(n_recv, 1))) return e;
+  if (!fit) { if (gc_status e = grow(&c->r_perm, &c->r_perm_cap, std::max<int64_t>(n_send, 1))) return e; }
+  if (c->r_in_cap < n_recv || !c->r_pos) {
+    CK(cudaDeviceSynchronize());
+    for (void* p : {(void*)c->r_pos, (void*)c->r_rgb, (void*)c->r_len, (void*)c->r_res}) if (p) cudaFree(p);
+    const int64_t m = std::max<int64_t>(n_recv + n_recv / 4, 1024);
+    CK(dalloc(&c->r_pos, 3 * m)); CK(dalloc(&c->r_rgb, 3 * m)); CK(dalloc(&c->r_len, m)); CK(dalloc(&c->r_res, 3 * m));
+    c->r_in_cap = m;
+  }
+  for (int p = 0; p < W; ++p) c->h_base[p] = (uint32_t)c->rt_soff[p];
+  CK(cudaMemcpyAsync(c->r_base, c->h_base, sizeof(uint32_t) * W, cudaMemcpyHostToDevice, s));
+  launch_route(pos, len, rgb, level_fixed, S, c->plan, 1, nullptr, c->r_base, c->r_cursor, c->r_send, c->r_perm,
+               out_zero, s, &c->prof);
+  const size_t rb = sizeof(float4) * words;
+  NK(ncclGroupStart());
+  for (int p = 0; p < W; ++p) {
+    if (c->rt_send[p]) NK(ncclSend(c->r_send + words * c->rt_soff[p], rb * c->rt_send[p], ncclUint8, p, c->comm, s));
+    if (c->rt_recv[p]) NK(ncclRecv(c->r_recv + words * c->rt_roff[p], rb * c->rt_recv[p], ncclUint8, p, c->comm, s));
+  }
+  NK(ncclGroupEnd());
+  launch_unpack_routed(c->r_recv, n_recv, fit, c->r_pos, c->r_len, c->r_rgb, s);
+  CK(cudaGetLastError());
+  *R = n_recv;
+  return GC_OK;
+}
+
+// Lookup results of the routed points (c->r_res, receive order) back to their source ranks,
+// then into caller order.
+static gc_status route_return(gc_cache c, cudaStream_t s, float* out) {
+  const int W = c->world;
+  const int64_t n_send = c->rt_soff[W];
+  if (gc_status e = grow(&c->r_back, &c->r_send_cap_back, 3 * std::max<int64_t>(n_send, 1))) return e;
+  NK(ncclGroupStart());
+  for (int p = 0; p < W; ++p) {
+    if (c->rt_recv[p]) NK(ncclSend(c->r_res + 3 * c->rt_roff[p], 3 * c->rt_recv[p], ncclFloat32, p, c->comm, s));
+    if (c->rt_send[p]) NK(ncclRecv(c->r_back + 3 * c->rt_soff[p], 3 * c->rt_send[p], ncclFloat32, p, c->comm, s));
+  }
+  NK(ncclGroupEnd());
+  launch_unroute(c->r_back, c->r_perm, n_send, out, s);
+  CK(cudaGetLastError());
+  return GC_OK;
+}
+
+
 // ---------------------------------------------------------------------------- ABI
 extern "C" {
 
@@ -428,6 +535,7 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
     DevState h0;
     memset(&h0, 0, sizeof h0);
     for (int l = 0; l < kMaxL; ++l) { h0.b1pow[l] = 1.0; h0.b2pow[l] = 1.0; }
+    h0.owned = 0xFFFFFFFFu;
     CK(cudaMemcpy(c->st, &h0, sizeof h0, cudaMemcpyHostToDevice));
   }
   CK(dalloc(&c->lvl, 1)); CK(dalloc(&c->dstats, 1)); CK(cudaMemset(c->dstats, 0, sizeof(gc_fit_stats)));
@@ -534,6 +642,7 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
   c->csr_cap = (uint32_t)cap;
   CK(dalloc(&c->csr_ovf, c->csr_cap));
   CK(dalloc(&c->csr_rec, 4 * (size_t)c->csr_cap));
+  if (gc_status e = publish_lists(c)) return e;
   CK(cudaMemset(&c->st->csr_overflow, 0, sizeof(unsigned int)));
   CK(cudaMemset(&c->st->ovf_next, 0, sizeof(unsigned int)));
   launch_record_cull(G, c->P, tau, c->geom, cull_bufs(c), c->st, s);
@@ -583,9 +692,15 @@ static void destroy_impl(gc_cache c) {
     if (p->done) cudaEventDestroy(p->done);
     delete p;
   }
-  for (void* p : c->retired) cudaFree(p);
   if (c->dbg_coef) cudaFree(c->dbg_coef);
+  if (c->gcomm) ncclCommDestroy(c->gcomm);
   if (c->comm) ncclCommDestroy(c->comm);
+  for (void* p : {(void*)c->r_count, (void*)c->r_all, (void*)c->r_base, (void*)c->r_cursor, (void*)c->r_send,
+                  (void*)c->r_recv, (void*)c->r_pos, (void*)c->r_rgb, (void*)c->r_res, (void*)c->r_back,
+                  (void*)c->r_len, (void*)c->r_perm})
+    if (p) cudaFree(p);
+  if (c->h_all) cudaFreeHost(c->h_all);
+  if (c->h_base) cudaFreeHost(c->h_base);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->side2) cudaStreamDestroy(c->side2);
   for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_fork2, c->ev_tail, c->ev_cpfork}) if (e) cudaEventDestroy(e);
@@ -664,6 +779,7 @@ struct Epilogue {
   }
 };
 
+
 // One optimisation step (gc_fit, and the fit half of gc_fit_query: `join`, if set, is waited
 // on before the optimizer step so that the lookups forked off beside it read pre-step
 // parameters).  `tail_ev`: a pending deferred step already forked by the caller (else this
@@ -683,6 +799,17 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
     if (gc_status e = csr_guard(c, s)) return e;
     if (gc_status e = fork_pending(c, s, &tail_ev)) return e;
   }
+  const int64_t S_in = S;             // this rank's input (n_in of the statistics)
+  if (routed(c)) {                    // level-sharded: fit the samples of this rank's levels
+    if (capturing(s)) return fail(GC_ERR_STATE, "level-sharded mode (gc_set_comm mode 1) is not graph-capturable");
+    int set0 = -1;
+    if (gc_status e = stage_inputs(c, c->fit, s, S, pos, path_len, rgb, set0)) return e;
+    int64_t R = 0;
+    if (gc_status e = route_exchange(c, s, pos, path_len, rgb, -1, S, nullptr, &R)) return e;
+    if (gc_status e = mark_staging_free(c->fit, s, set0)) return e;
+    pos = c->r_pos; path_len = c->r_len; rgb = c->r_rgb; S = R;
+    if (gc_status e = ensure_scratch(c, c->fit, std::max<int64_t>(S, 1), true, s)) return e;
+  }
   Scratch& F = c->fit;
   int set = -1;
   if (gc_status e = stage_inputs(c, F, s, S, pos, path_len, rgb, set)) return e;
@@ -693,7 +820,7 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
   if (gc_status e = mark_staging_free(F, s, set)) return e;
   if (tail_ev) CK(cudaStreamWaitEvent(s, tail_ev, 0));     // the previous step is complete
   FitArgs fa;
-  fa.work = F.work; fa.n_work = F.totals + 1; fa.csr_off = c->csr_off; fa.lrec = c->csr_rec; fa.cap = c->csr_cap;
+  fa.work = F.work; fa.n_work = F.totals + 1; fa.csr_off = c->csr_off; fa.st = c->st;
   fa.bin = F.bin;
   fa.grad = c->grad; fa.partial = c->partial;
   const float tau = c->hp.cutoff_sigma;
@@ -707,12 +834,20 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
   gc_fit_stats* out_stats = stats_in_place ? stats : c->dstats;
   launch_fwdbwd(fa, c->fb_grid, s, &c->prof);
   // single GPU: the step scalars ride in the statistics launch
-  launch_stats(c->partial, c->geom, S, c->lvl, !dp, c->st, c->hp, c->L, out_stats, s, &c->prof);
-  if (dp) {                         // data parallel: one sum over ranks of grads + level stats
+  launch_stats(c->partial, c->geom, S_in, c->lvl, !dp, c->st, c->hp, c->L, out_stats, s, &c->prof);
+  if (dp && c->mode == 0) {         // data parallel: one sum over ranks of grads + level stats
     NK(ncclGroupStart());
     NK(ncclAllReduce(c->grad, c->grad, (size_t)12 * c->G, ncclFloat32, ncclSum, c->comm, s));
     NK(ncclAllReduce(c->lvl, c->lvl, sizeof(LvlStats) / sizeof(double), ncclFloat64, ncclSum, c->comm, s));
     NK(ncclGroupEnd());
+    launch_step_scalars(c->lvl, c->st, c->hp, c->L, out_stats, s);
+  } else if (dp) {                  // level-sharded: gradients of the group's levels summed over
+    // the group (its members split those levels' samples); level statistics summed over all
+    // ranks, so every rank sees the global k_l and the same schedule step t
+    const int64_t g0 = c->geom.goff[c->glo], g1 = c->geom.goff[c->ghi];
+    if (c->gcomm && c->gsize > 1)
+      NK(ncclAllReduce(c->grad + 12 * g0, c->grad + 12 * g0, (size_t)12 * (g1 - g0), ncclFloat32, ncclSum, c->gcomm, s));
+    NK(ncclAllReduce(c->lvl, c->lvl, sizeof(LvlStats) / sizeof(double), ncclFloat64, ncclSum, c->comm, s));
     launch_step_scalars(c->lvl, c->st, c->hp, c->L, out_stats, s);
   }
   if (c->dbg_mode & 2)   // debug snapshot of the coefficient gradients the optimizer will read
@@ -725,7 +860,7 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
   }
   if (!stats_in_place) { if (gc_status e = emit_stats(c, stats, s)) return e; }
   CK(cudaGetLastError());
-  c->last_fit_S = S;
+  c->last_fit_S = routed(c) ? -1 : S;   // (gc_debug_levels: caller order only without routing)
   return GC_OK;
 }
 
@@ -750,6 +885,11 @@ gc_status gc_fit_query(gc_cache c, const float* pos, const int32_t* path_len, co
   if (S_q > 0 && (!qpos || !out_rgb)) return fail(GC_ERR_ARG, "NULL query pointer");
   if (S_q > 0 && !qlen && (qlevel < 0 || qlevel >= c->L)) return fail(GC_ERR_ARG, "qlevel %d not in [0, %d)", qlevel, c->L);
   if (S_q == 0) return fit_impl(c, pos, path_len, rgb, S, stream, stats);
+  if (routed(c)) {                    // level-sharded: lookups (routed), then the fit (routed)
+    if (gc_status e = query_impl(c, qpos, qlen, qlevel, S_q, attenuation, beta, unbiased_rgb, out_rgb, stream))
+      return e;
+    return fit_impl(c, pos, path_len, rgb, S, stream, stats);
+  }
   cudaStream_t s = (cudaStream_t)stream;
   CK(cudaSetDevice(c->device));
   cudaEvent_t tail_ev = nullptr;      // a deferred previous step overlaps both halves' ingest
@@ -786,15 +926,16 @@ static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_le
   if (S < 0 || S >= ((int64_t)1 << 31)) return fail(GC_ERR_ARG, "S out of range");
   if (S > 0 && (!pos || !out_rgb)) return fail(GC_ERR_ARG, "NULL pointer");
   if (!path_len && (level < 0 || level >= c->L)) return fail(GC_ERR_ARG, "level %d not in [0, %d)", level, c->L);
-  if (S == 0) return GC_OK;
+  if (S == 0 && !routed(c)) return GC_OK;      // (level-sharded calls are collective)
   cudaStream_t s = (cudaStream_t)stream;
   CK(cudaSetDevice(c->device));
   if (gc_status e = check_sticky(c)) return e;
-  if (gc_status e = ensure_scratch(c, c->qry, S, false, s)) return e;
+  if (gc_status e = ensure_scratch(c, c->qry, std::max<int64_t>(S, 1), false, s)) return e;
   if (!forked) {
     if (gc_status e = csr_guard(c, s)) return e;
     if (gc_status e = fork_pending(c, s, &tail_ev)) return e;
   }
+  const int64_t S_caller = S;
   Scratch& Q = c->qry;
   const bool hout = !is_device_ptr(out_rgb);
   if (hout) {
@@ -805,13 +946,26 @@ static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_le
   const float* no_rgb = nullptr;
   if (gc_status e = stage_inputs(c, Q, s, S, pos, path_len, no_rgb, set)) return e;
   float* dout = hout ? Q.out : out_rgb;
+  float* caller_out = nullptr;       // level-sharded: results come back into caller order here
+  if (routed(c)) {
+    if (capturing(s)) return fail(GC_ERR_STATE, "level-sharded mode (gc_set_comm mode 1) is not graph-capturable");
+    if (att || beta || unb) return fail(GC_ERR_UNSUPPORTED, "the gc_query_radiance epilogue is not available in level-sharded mode");
+    int64_t R = 0;
+    if (gc_status e = route_exchange(c, s, pos, path_len, nullptr, path_len ? -1 : level, S, dout, &R)) return e;
+    if (gc_status e = mark_staging_free(Q, s, set)) return e;
+    set = -1;
+    caller_out = dout;
+    pos = c->r_pos; path_len = c->r_len; level = -1; S = R;
+    dout = c->r_res;
+    if (gc_status e = ensure_scratch(c, c->qry, std::max<int64_t>(S, 1), false, s)) return e;
+  }
   IngestBufs b{Q.kr, Q.cell_count, Q.bin, c->NC};
   launch_keys_query(pos, path_len, path_len ? -1 : level, S, c->geom, b, dout, s, &c->prof);
   launch_scan(Q.cell_count, c->NC * kRep, kCH, Q.tiles, Q.totals, Q.cell_start, nullptr, Q.work, c->geom, s, &c->prof);
   launch_scatter(pos, nullptr, S, Q.cell_start, b, s, &c->prof);
   if (gc_status e = mark_staging_free(Q, s, set)) return e;
   QueryArgs qa;
-  qa.work = Q.work; qa.n_work = Q.totals + 1; qa.csr_off = c->csr_off; qa.lrec = c->csr_rec; qa.cap = c->csr_cap;
+  qa.work = Q.work; qa.n_work = Q.totals + 1; qa.csr_off = c->csr_off; qa.st = c->st;
   qa.bin = Q.bin; qa.out = dout;
   Epilogue ep;
   if (gc_status e = ep.stage(att, beta, unb, S, s)) return e;
@@ -821,6 +975,10 @@ static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_le
   qa.ref = c->cref;
   if (tail_ev) CK(cudaStreamWaitEvent(s, tail_ev, 0));     // a deferred step is complete
   launch_query(qa, c->q_grid, s, &c->prof);
+  if (caller_out) {
+    if (gc_status e = route_return(c, s, caller_out)) return e;
+    dout = caller_out; S = S_caller;
+  }
   if (hout) CK(cudaMemcpyAsync(out_rgb, dout, sizeof(float) * 3 * S, cudaMemcpyDeviceToHost, s));
   if (gc_status e = ep.release(s)) return e;
   CK(cudaGetLastError());
@@ -845,6 +1003,8 @@ static gc_status level_io(gc_cache c, int level, gc_level_params* p, bool out, c
   const int64_t off[5] = {0, 3 * n, 7 * n, 10 * n, 13 * n}, w[5] = {3, 4, 3, 3, 1};
   if (out) {
     launch_pack(planes, c->G, c->geom.goff[level], n, t, s);
+    if (routed(c) && planes == c->P && c->world > 1)   // level-sharded: the owner's copy (collective)
+      NK(ncclBroadcast(t, t, (size_t)kNP * n, ncclFloat32, c->plan.first[level], c->comm, s));
     for (int k = 0; k < 5; ++k) CK(cudaMemcpyAsync(f[k], t + off[k], sizeof(float) * w[k] * n, cudaMemcpyDefault, s));
   } else {
     for (int k = 0; k < 5; ++k) CK(cudaMemcpyAsync(t + off[k], f[k], sizeof(float) * w[k] * n, cudaMemcpyDefault, s));
@@ -925,13 +1085,29 @@ gc_status gc_nccl_unique_id(void* uid128) {
   return GC_OK;
 }
 
+gc_status gc_set_level_weights(gc_cache c, const double* weights) {
+  if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  if (!weights) { c->has_w = false; return GC_OK; }
+  for (int l = 0; l < c->L; ++l)
+    if (!(weights[l] >= 0.0) || !std::isfinite(weights[l])) return fail(GC_ERR_ARG, "weights[%d] not finite and >= 0", l);
+  for (int l = 0; l < c->L; ++l) c->lvl_w[l] = weights[l];
+  c->has_w = true;
+  return GC_OK;
+}
+
 gc_status gc_set_comm(gc_cache c, const void* nccl_uid, int rank, int world, int mode) {
   if (!c || world < 1 || rank < 0 || rank >= world) return fail(GC_ERR_ARG, "bad rank/world");
-  if (mode != 0) return fail(GC_ERR_UNSUPPORTED, "only mode 0 (data parallel) is implemented");
+  if (mode != 0 && mode != 1) return fail(GC_ERR_ARG, "mode must be 0 (data parallel) or 1 (level-sharded)");
+  if (mode == 1 && world > 1024) return fail(GC_ERR_ARG, "level-sharded mode supports at most 1024 ranks");
   CK(cudaSetDevice(c->device));
   CK(cudaDeviceSynchronize());
+  if (gc_status e = flush_pending(c, 0)) return e;
+  CK(cudaDeviceSynchronize());
+  if (c->gcomm) { ncclCommDestroy(c->gcomm); c->gcomm = nullptr; }
   if (c->comm) { ncclCommDestroy(c->comm); c->comm = nullptr; }
-  c->rank = rank; c->world = world;
+  c->rank = rank; c->world = world; c->mode = 0;
+  const unsigned int all = 0xFFFFFFFFu;
+  CK(cudaMemcpy(&c->st->owned, &all, sizeof all, cudaMemcpyHostToDevice));
   if (!nccl_uid) {
     if (world == 1) return GC_OK;     // detach
     return fail(GC_ERR_ARG, "NULL nccl_uid");
@@ -939,6 +1115,50 @@ gc_status gc_set_comm(gc_cache c, const void* nccl_uid, int rank, int world, int
   ncclUniqueId id;
   memcpy(&id, nccl_uid, sizeof id);
   NK(ncclCommInitRank(&c->comm, world, id, rank));
+  if (mode == 0) return GC_OK;
+  // level-sharded: the plan (identical on every rank: a function of L, the weights and W)
+  double w[kMaxL];
+  double G = 0.0;
+  for (int l = 0; l < c->L; ++l) G += (double)c->counts[l];
+  for (int l = 0; l < c->L; ++l) w[l] = c->has_w ? c->lvl_w[l] : (double)c->counts[l] / G;
+  int gl[kMaxL], fr[kMaxL], gs[kMaxL];
+  const int ng = level_plan(c->L, w, world, gl, fr, gs);
+  if (ng <= 0) return fail(GC_ERR_ARG, "level plan failed");
+  c->plan = RoutePlan{};
+  c->plan.world = world; c->plan.rank = rank; c->plan.L = c->L;
+  int mine = -1;
+  for (int g = 0; g < ng; ++g) if (rank >= fr[g] && rank < fr[g] + gs[g]) mine = g;
+  unsigned int owned = 0u;
+  c->glo = c->L; c->ghi = 0;
+  for (int l = 0; l < c->L; ++l) {
+    c->plan.first[l] = fr[gl[l]]; c->plan.size[l] = gs[gl[l]];
+    if (gl[l] == mine) { owned |= 1u << l; c->glo = std::min(c->glo, l); c->ghi = std::max(c->ghi, l + 1); }
+  }
+  c->gsize = gs[mine];
+  NK(ncclCommSplit(c->comm, mine, rank, &c->gcomm, nullptr));
+  CK(cudaMemcpy(&c->st->owned, &owned, sizeof owned, cudaMemcpyHostToDevice));
+  if (!c->r_count) {
+    CK(dalloc(&c->r_count, 1024)); CK(dalloc(&c->r_base, 1024)); CK(dalloc(&c->r_cursor, 1024));
+    CK(cudaHostAlloc((void**)&c->h_base, sizeof(uint32_t) * 1024, cudaHostAllocDefault));
+  }
+  if (c->r_all) cudaFree(c->r_all);
+  if (c->h_all) cudaFreeHost(c->h_all);
+  CK(dalloc(&c->r_all, (size_t)world * world));
+  CK(cudaHostAlloc((void**)&c->h_all, sizeof(uint32_t) * world * world, cudaHostAllocDefault));
+  c->mode = 1;
+  return GC_OK;
+}
+
+gc_status gc_comm_info(gc_cache c, int* mode, int* rank, int* world, int* owned_levels_mask, int* group_size) {
+  if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  unsigned int owned = 0u;
+  if (c->mode == 1) { for (int l = c->glo; l < c->ghi; ++l) owned |= 1u << l; }
+  else owned = (c->L >= 32) ? 0xFFFFFFFFu : ((1u << c->L) - 1u);
+  if (mode) *mode = c->comm ? c->mode : -1;
+  if (rank) *rank = c->rank;
+  if (world) *world = c->world;
+  if (owned_levels_mask) *owned_levels_mask = (int)owned;
+  if (group_size) *group_size = c->mode == 1 ? c->gsize : c->world;
   return GC_OK;
 }
 

@@ -48,6 +48,13 @@ struct DevState {
   unsigned int csr_overflow;         // a rebuild dropped entries past the list capacity (the
                                      // host guard detects it from the entry count, csr_guard)
   unsigned int ovf_next;             // bump allocator of the wide-range rank slots (per rebuild)
+  unsigned int owned;                // bit l: this rank steps level l (all ones unless level-sharded)
+  // the culling lists (entries [lcap][4] float4) and the wide-range rank slots [lovf_cap]: read
+  // by the kernels from here rather than from launch arguments, so that CUDA graphs captured
+  // before a capacity growth use the grown buffers
+  float4* lrec;
+  uint32_t* lovf;
+  uint32_t lcap, lovf_cap;
 };
 
 // Per-call level statistics; summed over ranks under data parallelism (all doubles so a

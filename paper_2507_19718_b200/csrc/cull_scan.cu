@@ -9,6 +9,7 @@ namespace gsc {
 __global__ void k_record_cull(int64_t G, const float* __restrict__ P, double tau, LevelGeom g, CullBufs cb,
                               DevState* st) {
   pdl_enter();
+  if (cb.ovf) { cb.ovf = st->lovf; cb.ovf_cap = st->lovf_cap; }   // current buffers (DevState)
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < G; j += (int64_t)gridDim.x * blockDim.x) {
     float p[kNP];
 #pragma unroll
@@ -23,6 +24,7 @@ __global__ void k_cull_emit(int64_t G, CullBufs cb, const float* __restrict__ P,
                             const uint32_t* __restrict__ off, uint32_t cap, DevState* st,
                             const uint32_t* total, uint32_t* host_total) {
   pdl_enter();
+  cb.lrec = st->lrec; cb.ovf = st->lovf; cb.ovf_cap = st->lovf_cap; cap = st->lcap;   // current buffers
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->ovf_next = 0u;                           // the counting pass is done
     if (host_total) *host_total = *total;        // entry count for the host's capacity guard

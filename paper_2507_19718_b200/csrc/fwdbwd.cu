@@ -500,6 +500,10 @@ __device__ __forceinline__ void query_out(float* out, const float* att, const fl
 
 __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
   pdl_enter();
+  // the culling lists are reached through DevState, so a CUDA graph captured before a capacity
+  // growth (csr_guard) reads the current lists
+  const float4* __restrict__ lrec = a.st->lrec;
+  const uint32_t lcap = a.st->lcap;
   extern __shared__ __align__(16) unsigned char dsm[];
   WarpSmem* sm = reinterpret_cast<WarpSmem*>(dsm);
   __shared__ double s_loss[kWarps][kMaxL];
@@ -527,8 +531,8 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
     const WorkItem wi = a.work[it];
     // clamped to the list capacity: after an overflowing rebuild the offsets run past it (the
     // entries there were dropped; the call reports GC_FLAG_LISTS_OVERFLOWED and skips its step)
-    const int lo = (int)min(__ldg(a.csr_off + wi.cell), a.cap);
-    const int C = (int)min(__ldg(a.csr_off + wi.cell + 1), a.cap) - lo;
+    const int lo = (int)min(__ldg(a.csr_off + wi.cell), lcap);
+    const int C = (int)min(__ldg(a.csr_off + wi.cell + 1), lcap) - lo;
     float xa[3], xb[3], ta[3] = {0.f, 0.f, 0.f}, tb[3] = {0.f, 0.f, 0.f};
     {                                            // one 32-byte load per sample: x y z r | g b - -
       const float kNaN = __int_as_float(0x7fffffff);   // inactive samples: never inside
@@ -554,7 +558,7 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
     const bool masked = C <= 32 * kMaskChunks;
     for (int cb = 0, c = 0; cb < C; cb += 32, ++c) {
       const int kc = min(32, C - cb);
-      iso = stage_chunk(w, a.lrec, lo + cb, kc, lane, xref, yref, zref, tau2);
+      iso = stage_chunk(w, lrec, lo + cb, kc, lane, xref, yref, zref, tau2);
       uint2 cm = make_uint2(0u, 0u);
       eval_any<true>(w, iso, wi.count > 32, kc, xa, xb, tau2, ya, yb, cm, lane);
       if (masked) w.u.mask[c][lane] = cm;
@@ -592,7 +596,7 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
         }
         const int P = __shfl_sync(0xffffffffu, incl, 31);
         if (P == 0) continue;
-        if (c != nch - 1) iso = stage_chunk(w, a.lrec, lo + cb, 32, lane, xref, yref, zref, tau2);
+        if (c != nch - 1) iso = stage_chunk(w, lrec, lo + cb, 32, lane, xref, yref, zref, tau2);
         w.offs[lane] = incl - nk;
         __syncwarp();
         if (wi.count > 32) {
@@ -609,7 +613,7 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
       const uint32_t lt = (1u << lane) - 1u;
       for (int cb = 0; cb < C; cb += 32) {
         const int kc = min(32, C - cb);
-        const bool ci = stage_chunk(w, a.lrec, lo + cb, kc, lane, xref, yref, zref, tau2);
+        const bool ci = stage_chunk(w, lrec, lo + cb, kc, lane, xref, yref, zref, tau2);
         int pb = 0;
         for (int k = 0; k < kc; ++k) {
           float Qa, Qb, ea, eb;                    // same arithmetic as eval_chunk[_iso]
@@ -669,6 +673,8 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
 
 __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
   pdl_enter();
+  const float4* __restrict__ lrec = a.st->lrec;
+  const uint32_t lcap = a.st->lcap;
   __shared__ ChunkSmem sm[kWarps];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   ChunkSmem& w = sm[wid];
@@ -689,8 +695,8 @@ __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
     const WorkItem wi = a.work[it];
     // clamped to the list capacity: after an overflowing rebuild the offsets run past it (the
     // entries there were dropped; the call reports GC_FLAG_LISTS_OVERFLOWED and skips its step)
-    const int lo = (int)min(__ldg(a.csr_off + wi.cell), a.cap);
-    const int C = (int)min(__ldg(a.csr_off + wi.cell + 1), a.cap) - lo;
+    const int lo = (int)min(__ldg(a.csr_off + wi.cell), lcap);
+    const int C = (int)min(__ldg(a.csr_off + wi.cell + 1), lcap) - lo;
     float xa[3], xb[3];
     float4 pa, pb4;
     load_pos(a.bin, 2, wi.start, wi.count, lane, xa, pa);
@@ -702,7 +708,7 @@ __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
     float ya[3] = {0.f, 0.f, 0.f}, yb[3] = {0.f, 0.f, 0.f};
     for (int cb = 0; cb < C; cb += 32) {
       const int kc = min(32, C - cb);
-      const bool iso = stage_chunk(w, a.lrec, lo + cb, kc, lane, xref, yref, zref, tau2);
+      const bool iso = stage_chunk(w, lrec, lo + cb, kc, lane, xref, yref, zref, tau2);
       uint2 cm;
       eval_any<false>(w, iso, wi.count > 32, kc, xa, xb, tau2, ya, yb, cm, lane);
     }

@@ -122,7 +122,7 @@ struct CellRef {
 CellRef cell_ref(const LevelGeom& g);
 struct FitArgs {
   const WorkItem* work; const uint32_t* n_work;
-  const uint32_t* csr_off; const float4* lrec; uint32_t cap;   // cap: list capacity (entries)
+  const uint32_t* csr_off; const DevState* st;   // st->lrec / st->lcap: the culling lists
   const float4* bin;
   float* grad;          // [G][12]
   double* partial;      // [grid][kMaxL + 2]: per-block loss sums, pairs, candidates
@@ -135,7 +135,7 @@ int fwdbwd_grid();
 void launch_fwdbwd(const FitArgs& a, int grid, cudaStream_t s, Profiler* prof);
 struct QueryArgs {
   const WorkItem* work; const uint32_t* n_work;
-  const uint32_t* csr_off; const float4* lrec; uint32_t cap;
+  const uint32_t* csr_off; const DevState* st;
   const float4* bin;
   float* out; float tau2;
   const float* att; const float* beta; const float* unb;   // optional f3 epilogue (caller order)
@@ -154,6 +154,23 @@ void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp
 void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, CullBufs cb, float* dbg_grad,
                   DevState* st, const gc_hparams& hp, const LevelGeom& g, unsigned long long* nonfinite,
                   cudaStream_t s, Profiler* prof);
+
+// shard.cu -- level-sharded mode (gc_set_comm mode 1)
+struct RoutePlan {
+  int world, rank, L;
+  int first[kMaxL];     // first rank of the group that owns level l
+  int size[kMaxL];      // ranks in that group (level l's samples split round-robin over them)
+};
+int level_plan(int L, const double* w, int W, int* group_of_level, int* first_rank, int* group_size);
+// pass 0: count[d] += samples routed to rank d; pass 1: pack them into sendbuf at base[d] +
+// (tile range reserved on cursor[d]); fit records 2 x float4 (x y z n | r g b 0) when rgb != NULL,
+// lookups 1 x float4 (x y z n) + perm[slot] = caller index, dropped lookups -> out_zero 0.
+void launch_route(const float* pos, const int32_t* len, const float* rgb, int level_fixed, int64_t S,
+                  const RoutePlan& p, int pass, uint32_t* count, const uint32_t* base, uint32_t* cursor,
+                  float4* sendbuf, uint32_t* perm, float* out_zero, cudaStream_t s, Profiler* prof);
+void launch_unpack_routed(const float4* recv, int64_t R, bool fit, float* pos, int32_t* len, float* rgb,
+                          cudaStream_t s);
+void launch_unroute(const float* res, const uint32_t* perm, int64_t n, float* out, cudaStream_t s);
 
 // create.cu
 void launch_gather_init(int64_t N0, const float* pos, const float* rgb, const float* log_scale,

@@ -1,0 +1,206 @@
+// shard.cu -- level-sharded multi-GPU mode (gc_set_comm mode 1, north star "the
+// level-sharded alternative"): the level plan (host), the routing of fit samples and lookups
+// to the ranks owning their level, and the return of lookup results to caller order.
+//
+// A level is owned by one group of consecutive ranks; inside a group its samples are split
+// round-robin (data parallel over the group, gradients summed over the group's communicator),
+// so level 0 -- most Gaussians and samples -- can be DP over a sub-group while the small levels
+// share one rank (the "hybrid" of SURVEY 8(e)).  No parameter replication is needed for the
+// math: a rank steps only the levels it owns (DevState::owned).
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace gsc {
+
+// ----------------------------------------------------------------------------- plan (host)
+// Level sharding uses as many groups as it can: K = min(L, W).
+//  W >= L: one group per level; the W - L extra ranks go, one at a time, to the level with the
+//    largest weight per rank (greedy, exact for min max w_l / n_l); level 0 -- most samples and
+//    Gaussians -- becomes data parallel over its group (the hybrid of SURVEY 8(e)).
+//  W < L: one rank per group; the levels are cut into W contiguous ranges minimising the
+//    largest range weight (exact dynamic programme, O(L^2 W)).
+// Ties resolve to the lowest level / earliest cut, so every rank computes the identical plan.
+int level_plan(int L, const double* w_in, int W, int* group_of_level, int* first_rank, int* group_size) {
+  if (L < 1 || W < 1 || L > kMaxL) return 0;
+  double w[kMaxL];
+  for (int l = 0; l < L; ++l) w[l] = w_in[l] > 0.0 ? w_in[l] : 0.0;
+  if (W >= L) {
+    int n[kMaxL];
+    for (int l = 0; l < L; ++l) n[l] = 1;
+    for (int extra = W - L; extra > 0; --extra) {
+      int best = 0;
+      for (int l = 1; l < L; ++l)
+        if (w[l] / n[l] > w[best] / n[best] * (1.0 + 1e-12)) best = l;
+      n[best] += 1;
+    }
+    int r = 0;
+    for (int l = 0; l < L; ++l) { group_of_level[l] = l; first_rank[l] = r; group_size[l] = n[l]; r += n[l]; }
+    return L;
+  }
+  const double inf = 1e300;
+  std::vector<double> pre(L + 1, 0.0);
+  for (int l = 0; l < L; ++l) pre[l + 1] = pre[l] + w[l];
+  // best[k][i]: levels [0, i) cut into k groups; cut[k][i]: start of the last group
+  std::vector<double> best((size_t)(W + 1) * (L + 1), inf);
+  std::vector<int> cut((size_t)(W + 1) * (L + 1), -1);
+  auto at = [&](int k, int i) { return (size_t)k * (L + 1) + i; };
+  best[at(0, 0)] = 0.0;
+  for (int k = 1; k <= W; ++k)
+    for (int i = k; i <= L; ++i)
+      for (int j = k - 1; j < i; ++j) {
+        if (best[at(k - 1, j)] >= inf) continue;
+        const double c = std::max(best[at(k - 1, j)], pre[i] - pre[j]);
+        if (c < best[at(k, i)] * (1.0 - 1e-12)) { best[at(k, i)] = c; cut[at(k, i)] = j; }
+      }
+  int i = L;
+  for (int k = W; k >= 1; --k) {
+    const int j = cut[at(k, i)];
+    if (j < 0) return 0;
+    for (int l = j; l < i; ++l) group_of_level[l] = k - 1;
+    first_rank[k - 1] = k - 1; group_size[k - 1] = 1;
+    i = j;
+  }
+  return W;
+}
+
+// ----------------------------------------------------------------------------- routing
+constexpr int kRouteThreads = 256, kRouteK = 8;            // 2048 samples per tile
+constexpr int kMaxWorld = 1024;
+
+// Destination rank of sample i, or -1 when it is dropped (same validity rule and level as
+// k_keys, C2): level l = min(n, L) - 1; the owning group's member (i + rank) mod size.
+__device__ __forceinline__ int route_dest(const RoutePlan& p, const float* pos, const int32_t* len,
+                                          const float* rgb, int level_fixed, int64_t i, int* lvl) {
+  const float x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
+  bool ok = isfinite(x) && isfinite(y) && isfinite(z);
+  int l = level_fixed;
+  if (level_fixed < 0) {
+    const int n = len[i];
+    ok = ok && n >= 1;
+    l = min(n, p.L) - 1;
+  }
+  if (rgb) ok = ok && isfinite(rgb[3 * i]) && isfinite(rgb[3 * i + 1]) && isfinite(rgb[3 * i + 2]);
+  *lvl = l;
+  if (!ok) return -1;
+  const int n = p.size[l];
+  return p.first[l] + (int)((i + p.rank) % n);
+}
+
+// pass 0: per-destination counts (tile histogram in shared memory, one global atomic per
+// (tile, destination)).  pass 1: packs every routed sample into the destination's segment of
+// the send buffer (segment base `base[d]`, a tile's range reserved with one atomic on
+// cursor[d]); fit records are 8 words (x y z n r g b 0), lookups 4 (x y z n) plus perm[slot]
+// = caller index; dropped lookups get out_zero = 0.
+__global__ void __launch_bounds__(kRouteThreads) k_route(const float* __restrict__ pos, const int32_t* __restrict__ len,
+                                                         const float* __restrict__ rgb, int level_fixed, int64_t S,
+                                                         RoutePlan p, int pass, uint32_t* count,
+                                                         const uint32_t* __restrict__ base, uint32_t* cursor,
+                                                         float4* sendbuf, uint32_t* perm, float* out_zero) {
+  __shared__ uint32_t hist[kMaxWorld], tbase[kMaxWorld];
+  const int W = p.world;
+  for (int64_t t0 = (int64_t)blockIdx.x * kRouteThreads * kRouteK; t0 < S;
+       t0 += (int64_t)gridDim.x * kRouteThreads * kRouteK) {
+    for (int d = threadIdx.x; d < W; d += kRouteThreads) hist[d] = 0u;
+    __syncthreads();
+    int dest[kRouteK], lv[kRouteK];
+    uint32_t lrank[kRouteK];
+#pragma unroll
+    for (int u = 0; u < kRouteK; ++u) {
+      const int64_t i = t0 + u * kRouteThreads + threadIdx.x;
+      dest[u] = -1; lv[u] = 0; lrank[u] = 0u;
+      if (i < S) {
+        dest[u] = route_dest(p, pos, len, rgb, level_fixed, i, &lv[u]);
+        if (dest[u] >= 0) lrank[u] = atomicAdd(&hist[dest[u]], 1u);
+        else if (pass == 1 && out_zero) { out_zero[3 * i] = 0.f; out_zero[3 * i + 1] = 0.f; out_zero[3 * i + 2] = 0.f; }
+      }
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < W; d += kRouteThreads) {
+      const uint32_t h = hist[d];
+      if (pass == 0) { if (h) atomicAdd(count + d, h); }
+      else tbase[d] = h ? base[d] + atomicAdd(cursor + d, h) : 0u;
+    }
+    __syncthreads();
+    if (pass == 1) {
+#pragma unroll
+      for (int u = 0; u < kRouteK; ++u) {
+        if (dest[u] < 0) continue;
+        const int64_t i = t0 + u * kRouteThreads + threadIdx.x;
+        const uint32_t slot = tbase[dest[u]] + lrank[u];
+        const int n = level_fixed < 0 ? len[i] : level_fixed + 1;
+        const float4 a = make_float4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], __int_as_float(n));
+        if (rgb) {
+          sendbuf[2 * (size_t)slot] = a;
+          sendbuf[2 * (size_t)slot + 1] = make_float4(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2], 0.f);
+        } else {
+          sendbuf[slot] = a;
+          perm[slot] = (uint32_t)i;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// received records -> the SoA inputs of the fit / lookup pipeline
+__global__ void k_unpack_routed(const float4* __restrict__ recv, int64_t R, int fit, float* pos, int32_t* len,
+                                float* rgb) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 a = fit ? recv[2 * i] : recv[i];
+    pos[3 * i] = a.x; pos[3 * i + 1] = a.y; pos[3 * i + 2] = a.z;
+    len[i] = __float_as_int(a.w);
+    if (fit) {
+      const float4 b = recv[2 * i + 1];
+      rgb[3 * i] = b.x; rgb[3 * i + 1] = b.y; rgb[3 * i + 2] = b.z;
+    }
+  }
+}
+
+// returned lookup results (slot order of the send buffer) -> caller order
+__global__ void k_unroute(const float* __restrict__ res, const uint32_t* __restrict__ perm, int64_t n, float* out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = perm[k];
+    out[3 * (size_t)i] = res[3 * k]; out[3 * (size_t)i + 1] = res[3 * k + 1]; out[3 * (size_t)i + 2] = res[3 * k + 2];
+  }
+}
+
+static int route_grid(int64_t S) {
+  const int64_t t = (S + kRouteThreads * kRouteK - 1) / (kRouteThreads * kRouteK);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(t, 148 * 8));
+}
+
+void launch_route(const float* pos, const int32_t* len, const float* rgb, int level_fixed, int64_t S,
+                  const RoutePlan& p, int pass, uint32_t* count, const uint32_t* base, uint32_t* cursor,
+                  float4* sendbuf, uint32_t* perm, float* out_zero, cudaStream_t s, Profiler* prof) {
+  ProfScope ps(prof, pass == 0 ? "route_count" : "route_pack", s);
+  if (S > 0)
+    k_route<<<route_grid(S), kRouteThreads, 0, s>>>(pos, len, rgb, level_fixed, S, p, pass, count, base, cursor,
+                                                    sendbuf, perm, out_zero);
+}
+
+void launch_unpack_routed(const float4* recv, int64_t R, bool fit, float* pos, int32_t* len, float* rgb,
+                          cudaStream_t s) {
+  if (R > 0) k_unpack_routed<<<route_grid(R), 256, 0, s>>>(recv, R, fit ? 1 : 0, pos, len, rgb);
+}
+
+void launch_unroute(const float* res, const uint32_t* perm, int64_t n, float* out, cudaStream_t s) {
+  if (n > 0) k_unroute<<<route_grid(n), 256, 0, s>>>(res, perm, n, out);
+}
+
+}  // namespace gsc
+
+extern "C" gc_status gc_level_plan(int levels, const double* weights, int world, int32_t* group_of_level,
+                                   int32_t* group_first_rank, int32_t* group_size, int* n_groups) {
+  if (levels < 1 || levels > GC_MAX_LEVELS || world < 1 || world > gsc::kMaxWorld || !weights ||
+      !group_of_level || !group_first_rank || !group_size || !n_groups)
+    return GC_ERR_ARG;
+  int gl[GC_MAX_LEVELS], fr[GC_MAX_LEVELS], gs[GC_MAX_LEVELS];
+  const int ng = gsc::level_plan(levels, weights, world, gl, fr, gs);
+  if (ng <= 0) return GC_ERR_ARG;
+  for (int l = 0; l < levels; ++l) group_of_level[l] = gl[l];
+  for (int g = 0; g < ng; ++g) { group_first_rank[g] = fr[g]; group_size[g] = gs[g]; }
+  *n_groups = ng;
+  return GC_OK;
+}

@@ -61,7 +61,7 @@ __device__ __forceinline__ void step_scalars_warp(const LvlStats* lvl, DevState*
   if (lane < kMaxL) {
     const int l = lane;
     const double k = l < hp.L ? lvl->count[l] : 0.0;
-    const int act = stepped && k > 0.0;
+    const int act = stepped && k > 0.0 && ((st->owned >> l) & 1u);   // level-sharded: own levels only
     st->active[l] = act;
     double p1 = st->b1pow[l], p2 = st->b2pow[l];
     if (act) {

@@ -1,10 +1,12 @@
-"""Multi-GPU data parallelism for the cache (north star; the paper runs on one GPU).
+"""Multi-GPU modes of the cache (north star; the paper runs on one GPU).
 
-One process per GPU.  Every rank holds a full replica of all levels, fits its own shard of
-the frame's samples, and the library performs ONE NCCL all-reduce (sum) per gc_fit of the
-per-level coefficient gradients and level statistics before the identical AdamW step
-(DESIGN.md "Multi-GPU").  torch.distributed is only plumbing: it carries the
-128-byte ncclUniqueId from rank 0 to the others (any backend, gloo included).
+One process per GPU.  Mode 0 (data parallel): every rank holds a full replica of all levels,
+fits its own shard of the frame's samples, and the library performs ONE NCCL all-reduce (sum)
+per gc_fit of the per-level coefficient gradients and level statistics before the identical
+AdamW step.  Mode 1 (level-sharded): the library routes each sample / lookup to the rank
+group owning its level (gc_level_plan), each group fits only its levels.  SURVEY 8(e);
+DESIGN.md "Multi-GPU".  torch.distributed is only plumbing: it carries the 128-byte
+ncclUniqueId from rank 0 to the others (any backend, gloo included).
 """
 from __future__ import annotations
 
@@ -27,6 +29,16 @@ def attach_data_parallel(cache, group=None, uid: bytes | None = None) -> None:
     if uid is None:
         uid = exchange_unique_id(group)
     cache.set_comm(uid, rank, world, 0)
+
+
+def attach_level_sharded(cache, group=None, uid: bytes | None = None, weights=None) -> None:
+    """Make `cache` one rank of a level-sharded cache (mode 1); every later gc_fit / gc_query /
+    gc_fit_query / gc_params call on it is collective over the group."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if uid is None:
+        uid = exchange_unique_id(group)
+    cache.set_level_weights(weights)
+    cache.set_comm(uid, rank, world, 1)
 
 
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:

@@ -92,6 +92,23 @@ def check_grad_group(a, b, what, scale=None, allow=None):
     return rel
 
 
+FP32_DELTA = 1e-6   # reading A21: relative perturbation of every summed term (~16 fp32 ulps)
+
+
+def grad_allow(c, P, x, ln, rgb, mode=0, max_amb_rate=5e-3):
+    """Per-element widening of the gradient bar (raw and coefficient layouts): reading A3's
+    boundary-flip allowance plus reading A21's summation-order floor FP32_DELTA * kappa
+    (kappa = the gradient summed and chained with absolute values; north star: "allowing for
+    atomic reordering").  kappa >= |g|, so well-conditioned elements gain 1e-6 |g| (nothing
+    next to 1e-4 |g|); only elements that are small differences of large terms gain more."""
+    kw = dict(mode=mode, grids=c.grids())
+    xd, rd = x.astype(np.float64), rgb.astype(np.float64)
+    a3 = oracle.grad_allowance(c.goff, P, xd, ln, rd, **kw)
+    assert a3["n_amb"] <= max(10, max_amb_rate * len(x)), a3["n_amb"]
+    kap = oracle.grad_allowance(c.goff, P, xd, ln, rd, cond=True, **kw)
+    return {k: a3[k] + FP32_DELTA * kap[k] for k in ("raw", "coef")}
+
+
 def check_grads(g, go, goff, what="", iso_levels=(), allow=None):
     """Both gradient bars on every (level, group) of raw 14-parameter gradients; levels in
     ``iso_levels`` hold isotropic Gaussians, whose rotation gradient is exactly 0 (C5).
@@ -303,8 +320,7 @@ def test_gradient_parity(gsc, mode):
     for l in range(3):
         assert st.count[l] == ro["count"][l]
         assert abs(st.loss[l] - ro["loss"][l]) <= 1e-4 * ro["loss"][l]
-    al = oracle.grad_allowance(c.goff, P, x.astype(np.float64), ln, rgb.astype(np.float64),
-                               mode=mode, grids=c.grids())
+    al = grad_allow(c, P, x, ln, rgb, mode=mode)
     check_grads(g, go, c.goff, f"cfg1 mode {mode}", iso_levels=(1, 2), allow=al["raw"])
     assert st.n_pairs == ro["npairs"] or abs(st.n_pairs - ro["npairs"]) <= 1e-4 * ro["npairs"]
 
@@ -700,8 +716,7 @@ def test_fit_query_lookups_and_gradients(gsc):
     for l in range(3):
         assert st.count[l] == ro["count"][l]
         assert abs(st.loss[l] - ro["loss"][l]) <= 1e-4 * ro["loss"][l]
-    al = oracle.grad_allowance(c.goff, P, x.astype(np.float64), ln, rgb.astype(np.float64),
-                               grids=c.grids())
+    al = grad_allow(c, P, x, ln, rgb)
     check_grads(g, ro["grad"], c.goff, "fit_query", iso_levels=(1, 2), allow=al["raw"])
     assert st.step == 1 and st.n_in == len(x)
 
@@ -866,8 +881,7 @@ def test_coherent_sample_order(gsc):
     ro = oracle.loss_grad(c.goff, P, x.astype(np.float64), ln, rgb.astype(np.float64), grids=c.grids())
     for l in range(3):
         assert st.count[l] == ro["count"][l]
-    al = oracle.grad_allowance(c.goff, P, x.astype(np.float64), ln, rgb.astype(np.float64),
-                               grids=c.grids())
+    al = grad_allow(c, P, x, ln, rgb)
     check_grads(g, ro["grad"], c.goff, "morton", iso_levels=(0, 1, 2), allow=al["raw"])
 
 

@@ -384,6 +384,30 @@ def test_grad_allowance_bounds_actual_cutoff_flips():
         assert np.abs(o["grad"] - base["grad"]).max() > 0      # some pair really flipped
 
 
+def test_grad_condition_magnitudes():
+    """Reading A21's kappa (oracle.grad_allowance(cond=True)): never below |grad| (raw and
+    coefficient layouts), and equal to it where every summed term has one sign -- with all
+    targets 0 every loss gradient g_i is positive (C5, mode 0: -2(0 - y)/(y+eps)^2 > 0), so the
+    colour-amplitude coefficient gradient sum_i g_i e_ij has no cancellation."""
+    r = np.random.default_rng(41)
+    G = 40
+    P = rand_params(G, r)
+    P[:, 0:3] *= 0.8
+    x = r.uniform(-0.6, 0.6, (5000, 3))
+    ln = np.ones(len(x), np.int32)
+    goff = [0, G]
+    for rgb, same_sign in ((r.uniform(0, 2, (len(x), 3)), False), (np.zeros((len(x), 3)), True)):
+        base = oracle.loss_grad(goff, P, x, ln, rgb, tau=3.0)
+        kap = oracle.grad_allowance(goff, P, x, ln, rgb, tau=3.0, cond=True)
+        for key in ("grad", "coef"):
+            k = kap["raw" if key == "grad" else key]
+            assert np.all(k >= np.abs(base[key]) * (1 - 1e-12) - 1e-300), key
+        if same_sign:
+            np.testing.assert_allclose(kap["coef"][:, 9:12], np.abs(base["coef"][:, 9:12]), rtol=1e-12)
+        else:
+            assert np.any(kap["coef"][:, 0:3] > 1.5 * np.abs(base["coef"][:, 0:3]))
+
+
 def _check_groups(g, fd, tol):
     for name, sl in oracle.GROUP_SLICES.items():
         a, b = g[:, sl], fd[:, sl]
