@@ -9,10 +9,16 @@ fit half on an internal stream; --separate times gc_query + gc_fit instead).  Wo
 Gaussians, one 1920x1080 frame = 2,073,600 samples per step), synthetic (workload.py).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+                  [--scaling weak|strong] [--parallelism dp|level]
 
-N > 1 runs under torchrun: one process per GPU, every rank fits its own frame (weak scaling)
-and one NCCL all-reduce of the level gradients per step keeps the replicas identical.
-Rank 0 prints ONE JSON line.
+--gpus N > 1 runs one process per GPU: launched by torchrun (the driver), or, when WORLD_SIZE is
+unset, bench.py re-executes itself under `python -m torch.distributed.run`.  --scaling weak
+(default): every rank fits its own full frame of the config; strong: the config's frame is
+split over the ranks (S/N samples and lookups each; cfg4's 16.8 M is the north star's case).
+--parallelism dp (default): mode 0, one NCCL all-reduce of the level gradients per step keeps
+the replicas identical; level: mode 1, samples and lookups are routed to the ranks owning
+their level (not graph-capturable: eager calls).  At N > 1 the other mode is timed too and
+reported under "alt".  Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
 
@@ -96,6 +102,34 @@ def dist_env():
         int(os.environ.get("LOCAL_RANK", 0))
 
 
+def relaunch_under_torchrun(n):
+    """--gpus N > 1 without a torchrun environment: re-execute this script as N ranks."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
+def cpu_info():
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except Exception:
+        usable = os.cpu_count()
+    return {"cpu_count": os.cpu_count(), "usable_cores": usable, "model": model}
+
+
 # ------------------------------------------------------------------ reference arm
 def run_reference(args):
     """The fp64 CPU oracle as it stands, on the host cores, bounded sample per step."""
@@ -168,6 +202,80 @@ def metric_name(cfg):
 
 
 # ------------------------------------------------------------------- our arm
+def make_frames(cfg, rank, world, R, strong, morton, dev):
+    """R rotating frames of device-resident inputs for this rank.  Weak scaling: the rank's
+    own full frame of the config; strong: its 1/world slice of a global frame (each slice an
+    independent seeded draw of the same distribution, S_global / world samples)."""
+    import torch
+    S = workload.CONFIGS[cfg]["S"]
+    S_local = -(-S // world) if strong else S
+    frames = []
+    for f in range(R):
+        fr = (f * 1000 + rank) if strong else (rank * R + f)
+        x, ln, rgb = workload.fit_batch(cfg, frame=fr, S=S_local, morton=morton)
+        xq, lq = workload.query_batch(cfg, frame=fr, S=S_local, morton=morton)
+        frames.append(tuple(torch.from_numpy(a).to(dev) for a in (x, ln, rgb, xq, lq)))
+    return frames, S_local
+
+
+def level_weights(cfg, frames):
+    """Mode-1 plan weights: each level's share of the frame's valid samples (the evaluator
+    work) averaged with its share of the Gaussians (the optimizer work)."""
+    counts = np.array(workload.CONFIGS[cfg]["counts"], np.float64)
+    L = len(counts)
+    ln = frames[0][1].cpu().numpy()
+    lv = np.minimum(ln[ln >= 1], L) - 1
+    share = np.bincount(lv, minlength=L) / max(len(lv), 1)
+    return 0.5 * share + 0.5 * counts / counts.sum()
+
+
+class Timer:
+    """CUDA-event time of `steps` frames on `stream`, barrier + synchronize on both sides, max
+    over ranks (the recipe's multi-GPU rule)."""
+
+    def __init__(self, dev, world):
+        import torch
+        self.torch, self.dev, self.world = torch, dev, world
+
+    def barrier(self):
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.barrier()
+        self.torch.cuda.synchronize(self.dev)
+
+    def run(self, fn, steps, stream):
+        import torch.distributed as dist
+        torch = self.torch
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        self.barrier()
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            for k in range(steps):
+                fn(k)
+        e1.record(stream)
+        self.barrier()
+        ms = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=self.dev)
+        if self.world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return float(ms.item())
+
+
+def build_cache(gsc, cfg, dev, local, args, rank, world, mode, frames, S_local):
+    import torch
+    c = workload.CONFIGS[cfg]
+    pos, alb = workload.init_cloud(cfg)
+    cache = gsc.GSCache(c["counts"], torch.from_numpy(pos).to(dev), torch.from_numpy(alb).to(dev),
+                        seed=cfg, device=local, hparams=dict(cell_edge_scale=args.cell_scale))
+    if world > 1:
+        from paper_2507_19718_b200 import dist as gdist
+        uid = gdist.exchange_unique_id()
+        if mode == 1:
+            cache.set_level_weights(level_weights(cfg, frames))
+        cache.set_comm(uid, rank, world, mode)
+    cache.reserve(S_local, S_local)
+    return cache
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -182,36 +290,28 @@ def run_ours(args):
     cfg = args.config
     c = workload.CONFIGS[cfg]
     counts = c["counts"]
-    S = c["S"]
-    pos, alb = workload.init_cloud(cfg)
-    cache = gsc.GSCache(counts, torch.from_numpy(pos).to(dev), torch.from_numpy(alb).to(dev),
-                        seed=cfg, device=local, hparams=dict(cell_edge_scale=args.cell_scale))
-    if world > 1:
-        uid = [gsc.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        cache.set_comm(uid[0], rank, world)
+    strong = args.scaling == "strong"
+    mode = 1 if args.parallelism == "level" else 0
     R = 4                                   # rotating frames: inputs of step k last used 4 steps ago
-    frames = []
-    for f in range(R):
-        x, ln, rgb = workload.fit_batch(cfg, frame=rank * R + f, morton=args.morton)
-        xq, lq = workload.query_batch(cfg, frame=rank * R + f, morton=args.morton)
-        frames.append(tuple(torch.from_numpy(a).to(dev) for a in (x, ln, rgb, xq, lq)))
+    frames, S = make_frames(cfg, rank, world, R, strong, args.morton, dev)
     in_bytes = sum(t.numel() * t.element_size() for t in frames[0])
     outq = torch.empty((S, 3), dtype=torch.float32, device=dev)
-    cache.reserve(S, S)
+    cache = build_cache(gsc, cfg, dev, local, args, rank, world, mode, frames, S)
     stream = torch.cuda.Stream(device=dev)
     if not args.no_defer:       # each frame's optimizer step overlaps the next frame's ingest
         cache.set_deferred_step(True)
+    use_graph = not args.no_graph and not (mode == 1 and world > 1)   # mode 1 is not capturable
+    timer = Timer(dev, world)
 
-    def frame_call(x, ln, rgb, xq, lq, out, s_, separate=args.separate):
+    def frame_call(cch, x, ln, rgb, xq, lq, out, s_, separate=args.separate):
         if separate:                        # two calls, serialised on one stream
-            cache.query(xq, lq, out=out, stream=s_)
-            return cache.fit(x, ln, rgb, stream=s_)
+            cch.query(xq, lq, out=out, stream=s_)
+            return cch.fit(x, ln, rgb, stream=s_)
         # one call: the lookups overlap the fit samples' ingest and fwd/bwd (internal stream)
-        return cache.fit_query(x, ln, rgb, xq, lq, out=out, stream=s_)[1]
+        return cch.fit_query(x, ln, rgb, xq, lq, out=out, stream=s_)[1]
 
     def step(f, s_):
-        return frame_call(*frames[f], outq, s_)
+        return frame_call(cache, *frames[f], outq, s_)
 
     # warm-up (eager), then capture one CUDA graph per rotating frame
     with torch.cuda.stream(stream):
@@ -219,7 +319,7 @@ def run_ours(args):
             step(w % R, stream)
     stream.synchronize()
     graphs = []
-    if not args.no_graph:
+    if use_graph:
         for f in range(R):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=stream):
@@ -230,32 +330,19 @@ def run_ours(args):
                 graphs[w % R].replay()
     stream.synchronize()
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
+    def timed(k):
+        if graphs:
+            graphs[k % R].replay()
+        else:
+            step(k % R, stream)
+        if k == args.steps - 1:
+            cache.flush(stream)        # the last frame's deferred step is inside the timed region
 
     # ---- timed region (device time, CUDA events on the launching stream)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
-        barrier()
-        e0.record(stream)
-        with torch.cuda.stream(stream):
-            for k in range(args.steps):
-                if graphs:
-                    graphs[k % R].replay()
-                else:
-                    step(k % R, stream)
-            cache.flush(stream)        # the last frame's deferred step is inside the timed region
-        e1.record(stream)
-        barrier()
-        ms_total = e0.elapsed_time(e1)
-        ms = torch.tensor([ms_total / args.steps], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-        ms_step = float(ms.item())
+        ms_step = timer.run(timed, args.steps, stream)
         if args.clock_window > 0:     # keep the GPU busy long enough for nvidia-smi samples;
-            # the same number of frames on every rank (each frame holds an NCCL all-reduce)
+            # the same number of frames on every rank (each frame holds collectives)
             rounds = max(1, int(args.clock_window * 1e3 / (ms_step * 20)))
             with torch.cuda.stream(stream):
                 for _ in range(rounds):
@@ -264,9 +351,34 @@ def run_ours(args):
                     stream.synchronize()
     st = cache._stats
     torch.cuda.synchronize(dev)
-    n_valid = int(st.n_valid)           # last step's valid samples (global under DP)
-    n_valid_local = n_valid // world if world > 1 else n_valid
-    value = n_valid_local * world / (ms_step * 1e-3)
+    n_valid = int(st.n_valid)           # last step's valid samples, global (summed over ranks)
+    value = n_valid / (ms_step * 1e-3)
+    S_q_total = S * world
+
+    # ---- the other multi-GPU mode, same frames (N > 1 only)
+    alt = None
+    if world > 1 and not args.no_alt:
+        alt_mode = 1 - mode
+        cache_b = build_cache(gsc, cfg, dev, local, args, rank, world, alt_mode, frames, S)
+        if not args.no_defer:
+            cache_b.set_deferred_step(True)
+
+        def alt_step(k):
+            frame_call(cache_b, *frames[k % R], outq, stream)
+            if k == args.steps - 1:
+                cache_b.flush(stream)
+        with torch.cuda.stream(stream):
+            for w in range(args.warmup):
+                frame_call(cache_b, *frames[w % R], outq, stream)
+        ms_alt = timer.run(alt_step, args.steps, stream)
+        nv = int(cache_b._stats.n_valid)
+        info = cache_b.comm_info()
+        alt = {"parallelism": ("level" if alt_mode == 1 else "dp") + str(world),
+               "value": nv / (ms_alt * 1e-3), "ms_per_step": ms_alt, "cuda_graph": alt_mode == 0,
+               "owned_levels_rank0": info["owned_levels"] if rank == 0 else None}
+        if alt_mode == 1:
+            alt["plan"] = gsc.level_plan(list(level_weights(cfg, frames)), world)
+        del cache_b
 
     # ---- per-kernel device time of the same steps, eager with events per kernel, the two
     # halves serialised (gc_query + gc_fit) so that no kernel's time includes an overlap
@@ -274,46 +386,55 @@ def run_ours(args):
     cache.flush(stream)
     cache.profile_enable(True)
     cache.profile_read(reset=True)
-    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    e2.record(stream)
-    with torch.cuda.stream(stream):
-        for k in range(args.steps):
-            frame_call(*frames[k % R], outq, stream, separate=True)
-    e3.record(stream)
-    torch.cuda.synchronize(dev)
+    ms_eager = timer.run(lambda k: frame_call(cache, *frames[k % R], outq, stream, separate=True),
+                         args.steps, stream)
     prof = cache.profile_read(reset=True)
     cache.profile_enable(False)
     cache.set_deferred_step(not args.no_defer)
-    ms_eager = e2.elapsed_time(e3) / args.steps
     launches_per_step = sum(v[1] for v in prof.values()) / args.steps
     kernel_ms = {k: v[0] / max(v[1], 1) for k, v in prof.items()}
     share = {k: v[0] / args.steps / ms_eager for k, v in prof.items()}
     top = max(prof, key=lambda k: prof[k][0])
     n_pairs, n_cand = int(st.n_pairs), int(st.n_candidates)
     pk, pk_kind = peaks()
-    traffic, traffic_src = None, None
-    try:   # per-launch DRAM bytes of the dominant kernel from the committed ncu launch list
+    traffic_all, traffic_src = {}, None
+    try:   # per-launch DRAM bytes of each kernel from the committed ncu launch list
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f)
-        traffic = next((v for k, v in tj["bytes_per_launch"].items() if k.endswith("k_" + top) or
-                        k.endswith("k_" + top + "<0>")), None)
+        traffic_all = {k.split("::")[-1].split("<")[0]: v for k, v in tj["bytes_per_launch"].items()}
         traffic_src = "profiles/traffic.json: " + tj["source"]
     except Exception:
         pass
-    issue = None
-    try:   # the kernel's issue rate from the committed ncu capture (its real limiter)
+    kmap = {"fwdbwd": "k_fwdbwd", "query_fwd": "k_query", "ingest_keys": "k_keys", "query_keys": "k_keys",
+            "ingest_scatter": "k_scatter", "query_scatter": "k_scatter", "scan": "k_scan",
+            "cull_emit": "k_cull_emit", "record_cull": "k_record_cull", "adamw": "k_adamw", "stats": "k_stats"}
+    traffic = traffic_all.get(kmap.get(top, "k_" + top))
+    issue_all = {}
+    try:   # issue rate / pipe utilisation per kernel from the committed ncu capture
         with open(os.path.join(ROOT, "profiles", "issue.json")) as f:
             ij = json.load(f)
-        m = ij["kernels"].get("k_" + top)
-        if m:
-            issue = {"ipc": m["ipc"], "peak_ipc": 4.0, "frac": m["ipc"] / 4.0,
-                     "fma_pipe_pct": m["fma_pipe_pct"], "xu_pipe_pct": m["xu_pipe_pct"],
-                     "source": "profiles/issue.json: " + ij["source"]}
+        issue_all, issue_src = ij["kernels"], "profiles/issue.json: " + ij["source"]
     except Exception:
-        pass
+        issue_src = None
+    per_kernel = {}
+    for k, ms_k in kernel_ms.items():
+        kk = kmap.get(k, "k_" + k)
+        e = {"ms": ms_k}
+        if kk in traffic_all and ms_k > 0:
+            gbs = traffic_all[kk] / (ms_k * 1e-3) / 1e9
+            e.update(dram_gbs=gbs, dram_frac=gbs / pk["hbm_gbs"])
+        if kk in issue_all:
+            e.update(ipc=issue_all[kk]["ipc"], issue_frac=issue_all[kk]["ipc"] / 4.0)
+        per_kernel[k] = e
+    issue = None
+    if "k_" + top in issue_all:
+        m = issue_all["k_" + top]
+        issue = {"ipc": m["ipc"], "peak_ipc": 4.0, "frac": m["ipc"] / 4.0, "fma_pipe_pct": m["fma_pipe_pct"],
+                 "xu_pipe_pct": m["xu_pipe_pct"], "source": issue_src}
+    n_valid_local = n_valid / world
+    pairs_local = n_pairs / world
     if top == "fwdbwd":
-        flops = (n_pairs / world) * FLOPS_PER_PAIR + n_valid_local * FLOPS_PER_SAMPLE
+        flops = pairs_local * FLOPS_PER_PAIR + n_valid_local * FLOPS_PER_SAMPLE
         achieved = flops / (kernel_ms[top] * 1e-3) / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic, "kernel": top,
@@ -323,28 +444,35 @@ def run_ours(args):
                 "issue_bound": issue}
     else:
         roof = {"bound": "hbm", "achieved": None, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": None, "traffic": None, "kernel": top}
+                "frac": None, "traffic": traffic, "kernel": top}
+    # whole-step roofline: algorithmic bytes 28/fit sample + 336/Gaussian +
+    # 28/lookup and flops 67/pair + 20/sample + 30/lookup pair (lookup pairs at the fit's P)
+    G = sum(counts)
+    pbar = n_pairs / max(n_valid, 1)
+    step_bytes = S * 28 + G * 336 + S * 28
+    step_flops = pairs_local * FLOPS_PER_PAIR + n_valid_local * FLOPS_PER_SAMPLE + S * pbar * FLOPS_PER_QPAIR
+    t_hbm = step_bytes / (pk["hbm_gbs"] * 1e9)
+    t_alu = step_flops / (FP32_PEAK_TFLOPS * 1e12)
+    roof["step"] = {"bytes": step_bytes, "flops": step_flops, "t_hbm_us": t_hbm * 1e6, "t_alu_us": t_alu * 1e6,
+                    "bound": "hbm" if t_hbm >= t_alu else "alu",
+                    "frac": max(t_hbm, t_alu) / (ms_step * 1e-3 / (1 if world == 1 else 1)),
+                    "per_gpu": True,
+                    "note": "max(B/BW, F/peak) / measured ms_per_step, per GPU; lookup pairs at the fit's mean P"}
+    roof["per_kernel"] = per_kernel
 
     # ---- end to end through the public API with pinned HOST buffers
     hx = [tuple(t.cpu().pin_memory() for t in fr) for fr in frames]
     hout = torch.empty((S, 3), dtype=torch.float32).pin_memory()
-    e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         for w in range(2):
-            frame_call(*hx[w % R], hout, stream)
-    barrier()
-    e4.record(stream)
-    with torch.cuda.stream(stream):
-        for k in range(args.steps):
-            frame_call(*hx[k % R], hout, stream)
-        cache.flush(stream)
-    e5.record(stream)
-    barrier()
-    ms_e2e = torch.tensor([e4.elapsed_time(e5) / args.steps], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms_e2e, op=dist.ReduceOp.MAX)
-    ms_e2e = float(ms_e2e.item())
-    e2e_val = n_valid_local * world / (ms_e2e * 1e-3)
+            frame_call(cache, *hx[w % R], hout, stream)
+
+    def e2e_step(k):
+        frame_call(cache, *hx[k % R], hout, stream)
+        if k == args.steps - 1:
+            cache.flush(stream)
+    ms_e2e = timer.run(e2e_step, args.steps, stream)
+    e2e_val = n_valid / (ms_e2e * 1e-3)
 
     # ---- CPU oracle baseline (rank 0, N = 1 only), bounded sample
     cpu = None
@@ -355,16 +483,18 @@ def run_ours(args):
         line = {
             "metric": metric_name(cfg), "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": c["name"], "levels": len(counts), "counts": counts,
-                       "S_fit_per_gpu": S, "S_query_per_gpu": S, "parallelism": f"dp{world}",
+                       "S_fit_per_gpu": S, "S_query_per_gpu": S,
+                       "S_fit_global": S * world,
+                       "parallelism": ("level" if mode == 1 else "dp") + str(world),
                        "l2": f"{R} rotating device-resident frames ({R * in_bytes / 1e6:.0f} MB) > 126 MB L2",
-                       "cuda_graph": not args.no_graph,
+                       "cuda_graph": bool(graphs),
                        "frame_call": "gc_query + gc_fit" if args.separate else "gc_fit_query",
                        "deferred_step": not args.no_defer,
                        "sample_order": "morton" if args.morton else "random"},
-            "queries_per_s": S * world / (ms_step * 1e-3),
+            "queries_per_s": S_q_total / (ms_step * 1e-3),
             "pairs_per_sample": n_pairs / max(n_valid, 1),
             "candidates_per_sample": n_cand / max(n_valid, 1),
             "roofline": roof,
@@ -375,6 +505,8 @@ def run_ours(args):
             "gpu_launches": int(round(launches_per_step * args.steps)),
             "clocks": clk.summary(), "peaks": pk_kind,
         }
+        if alt:
+            line["alt"] = alt
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
@@ -383,21 +515,100 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# CPU oracle baseline, multi-process leg: the oracle as it stands, one process per core over
+# contiguous sample shards (C9: per-shard sums add up; the shards' gradient sums are combined
+# with the per-level counts, then one AdamW step), set up before the pool forks.
+_MP = {}
+
+
+def _mp_shard(k):
+    import oracle
+    d = _MP
+    lo, hi = d["fit_cuts"][k], d["fit_cuts"][k + 1]
+    qlo, qhi = d["q_cuts"][k], d["q_cuts"][k + 1]
+    oracle.query(d["goff"], d["P"], d["xq"][qlo:qhi], d["lq"][qlo:qhi], grids=d["grids"])
+    r = oracle.loss_grad(d["goff"], d["P"], d["x"][lo:hi], d["ln"][lo:hi], d["rgb"][lo:hi], grids=d["grids"])
+    goff = d["goff"]
+    g = r["grad"].copy()
+    for l in range(len(goff) - 1):   # back to plain sums: the shard normalised by its own 3 k_l
+        g[goff[l]:goff[l + 1]] *= 3.0 * r["count"][l]
+    return g, r["count"]
+
+
 def cpu_baseline(cache, cfg, n):
-    """The fp64 oracle on this box's host cores (1 thread): one fit + query step on a bounded
-    sample of the same frame, starting from the same parameters and culling grids."""
+    """The fp64 oracle on this box's host cores: one fit + query step on a bounded sample of the
+    same frame, from the same parameters and culling grids -- single thread (the culled oracle
+    as it stands), all cores (one oracle process per core over sample shards), plus the
+    brute-force oracle (the definition, no culling) on cfg0 and on a cfg1 sample."""
+    import multiprocessing as mp
+
     import oracle
     P = np.concatenate([cache.params_rows(l) for l in range(cache.L)]).astype(np.float64)
-    oc = oracle.OracleCache(cache.counts, P, grids=cache.grids())
+    grids = cache.grids()
+    oc = oracle.OracleCache(cache.counts, P.copy(), grids=grids)
     x, ln, rgb = workload.fit_batch(cfg, frame=0, S=n)
     xq, lq = workload.query_batch(cfg, frame=0, S=n)
+    x, rgb, xq = x.astype(np.float64), rgb.astype(np.float64), xq.astype(np.float64)
     t0 = time.perf_counter()
-    oc.query(xq.astype(np.float64), lq)
-    r = oc.fit(x.astype(np.float64), ln, rgb.astype(np.float64))
+    oc.query(xq, lq)
+    r = oc.fit(x, ln, rgb)
     dt = time.perf_counter() - t0
-    return {"value": int(r["count"].sum()) / dt, "unit": "samples/s", "cores": 1, "kind": "oracle",
-            "sample": f"{n} fit samples + {n} queries of {workload.CONFIGS[cfg]['name']} frame 0 "
-                      f"(culled fp64 oracle, single thread, {dt:.1f} s)"}
+    nvalid = int(r["count"].sum())
+    info = cpu_info()
+    out = {"value": nvalid / dt, "unit": "samples/s", "cores": 1, "kind": "oracle",
+           "sample": f"{n} fit samples + {n} queries of {workload.CONFIGS[cfg]['name']} frame 0 "
+                     f"(culled fp64 oracle, single thread, {dt:.1f} s)",
+           "host": info}
+    # all cores
+    ncores = max(1, int(info["usable_cores"] or 1))
+    try:
+        goff = np.concatenate([[0], np.cumsum(cache.counts)]).astype(np.int64)
+        _MP.update(goff=goff, P=P, grids=grids, x=x, ln=ln, rgb=rgb, xq=xq, lq=lq,
+                   fit_cuts=np.linspace(0, n, ncores + 1).astype(np.int64),
+                   q_cuts=np.linspace(0, n, ncores + 1).astype(np.int64))
+        ctx = mp.get_context("fork")
+        with ctx.Pool(ncores) as pool:
+            pool.map(_mp_shard, range(ncores))              # warm (fork, library load)
+            t0 = time.perf_counter()
+            parts = pool.map(_mp_shard, range(ncores))
+            gsum = sum(p[0] for p in parts)
+            cnt = sum(p[1] for p in parts)
+            Pm = P.copy()
+            M, V = np.zeros_like(Pm), np.zeros_like(Pm)
+            for l in range(len(goff) - 1):
+                if cnt[l] > 0:
+                    gsum[goff[l]:goff[l + 1]] /= 3.0 * cnt[l]
+            oracle.adamw(Pm, M, V, gsum, 1e-3, 1e-2, 0.9, 0.999, 1e-8, 1)   # one step's AdamW work
+            dtm = time.perf_counter() - t0
+        out["all_cores"] = {"value": nvalid / dtm, "cores": ncores, "seconds": dtm}
+    except Exception as e:   # report, do not hide
+        out["all_cores"] = {"error": str(e)[:200]}
+    # brute force (no culling): cfg0 full step, cfg1 on a bounded sample
+    try:
+        c0 = workload.CONFIGS[0]
+        pos0, rgb0, ls0 = workload.cfg0_lattice()
+        P0 = oracle.create(c0["counts"], pos0.astype(np.float64), rgb0.astype(np.float64),
+                           ls0.astype(np.float64), seed=0)
+        xs, ls = workload.cfg0_samples(c0["S"])
+        t0 = time.perf_counter()
+        oracle.loss_grad([0, 64], P0, xs.astype(np.float64), ls, np.ones((len(xs), 3)))
+        b0 = time.perf_counter() - t0
+        c1 = workload.CONFIGS[1]
+        pos1, alb1 = workload.init_cloud(1)
+        P1 = oracle.create(c1["counts"], pos1.astype(np.float64), alb1.astype(np.float64), seed=1)
+        n1 = 8192
+        x1, l1, r1 = workload.fit_batch(1, frame=0, S=n1)
+        goff1 = np.concatenate([[0], np.cumsum(c1["counts"])])
+        t0 = time.perf_counter()
+        r1o = oracle.loss_grad(goff1, P1, x1.astype(np.float64), l1, r1.astype(np.float64))
+        b1 = time.perf_counter() - t0
+        out["brute_force"] = {"cfg0_step_s": b0, "cfg0_samples_per_s": c0["S"] / b0,
+                              "cfg1_samples_per_s": int(r1o["count"].sum()) / b1,
+                              "cfg1_sample": f"{n1} samples of cfg1 frame 0, every Gaussian of the level",
+                              "cores": 1}
+    except Exception as e:
+        out["brute_force"] = {"error": str(e)[:200]}
+    return out
 
 
 def main():
@@ -420,9 +631,14 @@ def main():
     ap.add_argument("--ref-samples", type=int, default=100_000)
     ap.add_argument("--clock-window", type=float, default=2.0)
     ap.add_argument("--cell-scale", type=float, default=1.0, help="culling-grid cell edge multiplier")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--parallelism", default="dp", choices=["dp", "level"])
+    ap.add_argument("--no-alt", action="store_true", help="N > 1: do not also time the other mode")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args.gpus)
     if args.impl == "reference":
         run_reference(args)
     else:

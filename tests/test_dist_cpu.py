@@ -117,3 +117,90 @@ def test_nccl_unique_id_exchange_over_gloo():
             pytest.skip(f"ncclGetUniqueId unavailable here: {e}")
         res = dict(out)
     assert len(res[0]) == 128 and res[0] == res[1] and any(res[0])
+
+
+def _ls_worker(rank, world, port, out):
+    """Level-sharded decomposition (gc_set_comm mode 1) on CPU: the library's plan
+    (gc_level_plan, a host function) and routing rule (a sample of level l goes to
+    first[l] + (i + rank) mod size[l], shard.cu route_dest), the exchange done here with gloo
+    instead of ncclSend/Recv, the group's gradient sum over a gloo sub-group (the library's
+    ncclCommSplit communicator) and the level statistics summed over all ranks."""
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2507_19718_b200 as gsc
+    goff, P, x, ln, rgb = _problem()
+    L = len(goff) - 1
+    gl, groups = gsc.level_plan([0.8, 0.2], world)
+    first = [groups[gl[l]][0] for l in range(L)]
+    size = [groups[gl[l]][1] for l in range(L)]
+    lo, hi = shard_range(len(x), rank, world)
+    dest = np.full(hi - lo, -1)
+    for i in range(hi - lo):
+        n = ln[lo + i]
+        if n >= 1:
+            l = min(n, L) - 1
+            dest[i] = first[l] + (i + rank) % size[l]
+    send = [np.nonzero(dest == d)[0] + lo for d in range(world)]
+    everyone = [None] * world
+    dist.all_gather_object(everyone, send)
+    mine = np.concatenate([everyone[s][rank] for s in range(world)]).astype(np.int64)
+    res = oracle.loss_grad(goff, P, x[mine], ln[mine], rgb[mine], mode=1)
+    k = res["count"].astype(np.float64)
+    g = res["grad"].copy()
+    for l in range(L):
+        g[goff[l]:goff[l + 1]] *= 3 * k[l]
+    my_group = [gi for gi, (f, s) in enumerate(groups) if f <= rank < f + s][0]
+    subgroups = [dist.new_group(list(range(f, f + s))) for f, s in groups]   # every rank creates all
+    owned = [l for l in range(L) if gl[l] == my_group]
+    gt = torch.from_numpy(g)
+    dist.all_reduce(gt, group=subgroups[my_group])        # the group's gradient sum
+    st = torch.from_numpy(np.concatenate([res["loss"] * 3 * k, k]))
+    dist.all_reduce(st)                                   # level statistics over all ranks
+    s = st.numpy()
+    lsum, ksum = s[:L], s[L:]
+    gsum = gt.numpy()
+    for l in range(L):
+        gsum[goff[l]:goff[l + 1]] /= 3 * ksum[l]
+    out[rank] = (owned, gsum, lsum / (3 * ksum), ksum, groups)
+    dist.destroy_process_group()
+
+
+def test_level_sharded_decomposition_equals_single_rank_gloo():
+    world = 3
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.start_processes(_ls_worker, args=(world, port, out), nprocs=world, join=True,
+                           start_method="fork")
+        res = dict(out)
+    goff, P, x, ln, rgb = _problem()
+    full = oracle.loss_grad(goff, P, x, ln, rgb, mode=1)
+    assert res[0][4] == [(0, 2), (2, 1)]                  # level 0 data parallel over 2 ranks
+    for r in range(world):
+        owned, g, loss, k, _ = res[r]
+        np.testing.assert_array_equal(k, full["count"])
+        np.testing.assert_allclose(loss, full["loss"], rtol=1e-12)
+        for l in owned:
+            sl = slice(goff[l], goff[l + 1])
+            np.testing.assert_allclose(g[sl], full["grad"][sl], rtol=1e-10, atol=1e-14)
+    np.testing.assert_array_equal(res[0][1][0:40], res[1][1][0:40])   # level-0 group agrees
+
+
+def test_level_plan_properties():
+    """gc_level_plan (host): K = min(L, W) groups, contiguous levels and ranks covering all,
+    the surplus ranks on the heaviest levels (hybrid), deterministic."""
+    import paper_2507_19718_b200 as gsc
+    w = [0.5, 0.25, 0.125, 0.125]
+    assert gsc.level_plan(w, 1) == ([0, 0, 0, 0], [(0, 1)])
+    assert gsc.level_plan(w, 2) == ([0, 1, 1, 1], [(0, 1), (1, 1)])
+    assert gsc.level_plan(w, 8) == ([0, 1, 2, 3], [(0, 4), (4, 2), (6, 1), (7, 1)])
+    for L in (1, 3, 6, 16):
+        ww = list(np.random.default_rng(L).uniform(0, 1, L))
+        for W in (1, 2, 5, 8, 33):
+            gl, groups = gsc.level_plan(ww, W)
+            assert len(groups) == min(L, W)
+            assert gl == sorted(gl) and set(gl) == set(range(len(groups)))
+            assert groups[0][0] == 0 and sum(s for _, s in groups) == W
+            assert all(groups[i][0] + groups[i][1] == groups[i + 1][0] for i in range(len(groups) - 1))
+            assert gsc.level_plan(ww, W) == (gl, groups)
