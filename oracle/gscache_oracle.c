@@ -764,7 +764,7 @@ int orc_grad_allowance(int L, const int64_t* goff, const double* P, double tau, 
       double Q = orc_Q(&gs[j], xi, d, t);
       double e = exp(-0.5 * Q);
       if (Q <= t2) for (int c = 0; c < 3; ++c) y[c] += gs[j].v[c] * e;
-      if (fabs(Q - t2) <= amb_rel * t2) { amb = 1; for (int c = 0; c < 3; ++c) a[c] += gs[j].v[c] * e; }
+      if (isfinite(t2) && fabs(Q - t2) <= amb_rel * t2) { amb = 1; for (int c = 0; c < 3; ++c) a[c] += gs[j].v[c] * e; }
     }
     if (!amb && !cond) continue;
     na += amb;
@@ -783,7 +783,7 @@ int orc_grad_allowance(int L, const int64_t* goff, const double* P, double tau, 
       int64_t j = csr ? goff[l] + csr[l].idx[k] : k;
       double d[3], t[3];
       double Q = orc_Q(&gs[j], xi, d, t);
-      int isamb = fabs(Q - t2) <= amb_rel * t2;
+      int isamb = isfinite(t2) && fabs(Q - t2) <= amb_rel * t2;   /* tau = inf: no boundary */
       if (cond) { if (!(Q <= t2)) continue; }
       else if (!(Q <= t2) && !isamb) continue;
       double e = exp(-0.5 * Q), H = 0.0, gg[3];
