@@ -169,6 +169,21 @@ gc_status gc_query_radiance(gc_cache c, const float* pos, const int32_t* path_le
                             int64_t S, const float* attenuation, const float* beta,
                             const float* unbiased_rgb, float* out_rgb, gc_stream stream);
 
+/* Early path termination, Algorithm 1 (sec.3.3.2; next-row f3), for P paths at once;
+ * each thread runs the device-callable gc_alg1 of include/gscache_device.cuh (the same helper
+ * a renderer kernel calls inline).  All arrays device memory:
+ *  sigma [P][nmax][3] f32: the RGB albedos sigma_1..sigma_n of each path's vertices so far;
+ *  n [P] i32: vertices of each path (clamped to [0, nmax]); C: termination coefficient;
+ *  beta [P] f32 or NULL (= 1): beta_n, the product of the earlier cache-miss probabilities
+ *  (sec.3.4.2); q [P] f32: one U(0,1) draw per path (the caller's random numbers);
+ *  eps: the guard of Tr_out / (Tr + eps) (unnamed in the paper; reading A22, e.g. 1e-6).
+ *  Outputs: terminate [P] i32 (1 = read the cache now), tr_out [P][3] f32 (throughput weight
+ *  of a continued path), beta_next [P] f32 (beta_{n+1}).  Returns GC_ERR_ARG on NULL arrays
+ *  or negative sizes, GC_ERR_CUDA if the launch fails; enqueued on `stream`. */
+gc_status gc_alg1_terminate(const float* sigma, const int32_t* n, int nmax, float C, const float* beta,
+                            const float* q, float eps, int64_t P, int32_t* terminate, float* tr_out,
+                            float* beta_next, gc_stream stream);
+
 /* Deferred optimizer step (enable != 0; off by default).  gc_fit / gc_fit_query then leave
  * their optimizer half -- the AdamW step with the next step's evaluation records, and the
  * culling-list rebuild -- pending, and the next call on the handle launches it on an internal
@@ -187,6 +202,24 @@ gc_status gc_flush(gc_cache c, gc_stream stream);
 gc_status gc_params(gc_cache c, int level, gc_level_params* dst, gc_stream stream);
 gc_status gc_set_params(gc_cache c, int level, const gc_level_params* src, int reset_adam,
                         gc_stream stream);
+
+/* Optimizer state for checkpoint / resume: the AdamW moments of one level in the
+ * gc_level_params layout (m: first, v: second moment; host or device arrays of the level's
+ * size), and, if ctr != NULL, the Eq. 5 schedule counter t and every level's AdamW step counter
+ * with its running beta powers (beta1^step, beta2^step, fp64 as kept on the device).
+ * gc_params + gc_adam_state of every level, restored into a cache created with the same
+ * arguments by gc_set_params(reset_adam = 0) + gc_set_adam_state, continue the run exactly
+ * (up to the fp32 atomic summation order of later steps).  gc_adam_state synchronises the
+ * stream when ctr != NULL; gc_set_adam_state with ctr synchronises it too. */
+typedef struct {
+  int64_t t;                             /* Eq. 5 counter (stepping fits since create / reset) */
+  int64_t adam_step[GC_MAX_LEVELS];      /* per-level AdamW steps (A12)                        */
+  double beta1_pow[GC_MAX_LEVELS], beta2_pow[GC_MAX_LEVELS];
+} gc_opt_counters;
+gc_status gc_adam_state(gc_cache c, int level, gc_level_params* m, gc_level_params* v,
+                        gc_opt_counters* ctr, gc_stream stream);
+gc_status gc_set_adam_state(gc_cache c, int level, const gc_level_params* m,
+                            const gc_level_params* v, const gc_opt_counters* ctr, gc_stream stream);
 
 /* Viewport / scene change: the next stepping gc_fit uses t = 1 again. */
 gc_status gc_reset_schedule(gc_cache c);

@@ -245,6 +245,32 @@ def query_radiance(yhat, attenuation=None, beta=None, unbiased_rgb=None):
     return y
 
 
+def alg1(sigma, n, C_, beta, q, eps=1e-6):
+    """Algorithm 1 (sec.3.3.2), early path termination, one path, as written:
+    Tr_out <- prod_k sigma_k; Tr <- clamp(C lum(Tr_out), 0, 1); if Tr < 0.9: p <- 1 - Tr,
+    terminate if q < p, else Tr_out <- Tr_out/(Tr + eps), beta_{n+1} <- beta_n Tr.
+    Readings A22: Rec. 709 luminance (0.2126, 0.7152, 0.0722); beta and Tr_out unchanged where
+    Alg. 1 assigns nothing.  The decision q < 1 - Tr is taken in fp32 with every operation
+    rounded in the written order (the device's precision, so both sides take the same branch);
+    returns (terminate, tr_out[3], beta_next) as fp32 values."""
+    f = np.float32
+    t = [f(1.0), f(1.0), f(1.0)]
+    for k in range(int(n)):
+        for c in range(3):
+            t[c] = f(t[c] * f(sigma[k][c]))
+    lum = f(f(f(0.2126) * t[0]) + f(f(0.7152) * t[1]))
+    lum = f(lum + f(f(0.0722) * t[2]))
+    tr = f(f(C_) * lum)
+    tr = f(min(max(tr, f(0.0)), f(1.0)))
+    if tr < f(0.9):
+        p = f(f(1.0) - tr)
+        if f(q) < p:
+            return 1, np.array(t, np.float32), f(beta)
+        d = f(tr + f(eps))
+        return 0, np.array([f(v / d) for v in t], np.float32), f(f(beta) * tr)
+    return 0, np.array(t, np.float32), f(beta)
+
+
 def level_of(length, L, x, rgb=None):
     x = _d(x).reshape(-1, 3)
     rgb = None if rgb is None else _d(rgb).reshape(-1, 3)

@@ -28,7 +28,7 @@ EXPORTS = ["gc_default_hparams", "gc_create", "gc_destroy", "gc_reserve", "gc_fi
            "gc_params", "gc_set_params", "gc_reset_schedule", "gc_grid", "gc_info",
            "gc_nccl_unique_id", "gc_set_comm", "gc_debug_enable_grads", "gc_debug_grads",
            "gc_debug_coef_grads", "gc_list_generation", "gc_set_level_weights", "gc_level_plan",
-           "gc_comm_info",
+           "gc_comm_info", "gc_adam_state", "gc_set_adam_state", "gc_alg1_terminate",
            "gc_debug_cull", "gc_debug_levels", "gc_profile_enable", "gc_profile_read",
            "gc_last_error", "gc_status_string"]
 
@@ -74,6 +74,11 @@ def pinned_stats() -> "gc_fit_stats":
         return gc_fit_stats()
 
 
+class gc_opt_counters(C.Structure):
+    _fields_ = [("t", C.c_int64), ("adam_step", C.c_int64 * MAX_LEVELS),
+                ("beta1_pow", C.c_double * MAX_LEVELS), ("beta2_pow", C.c_double * MAX_LEVELS)]
+
+
 class gc_level_params(C.Structure):
     _fields_ = [("count", C.c_int64), ("position", C.c_void_p), ("rotation", C.c_void_p),
                 ("color", C.c_void_p), ("log_scale", C.c_void_p), ("opacity_logit", C.c_void_p)]
@@ -111,6 +116,9 @@ def lib():
             "gc_set_level_weights": (i32, [vp, vp]),
             "gc_level_plan": (i32, [i32, vp, i32, vp, vp, vp, vp]),
             "gc_comm_info": (i32, [vp, vp, vp, vp, vp, vp]),
+            "gc_adam_state": (i32, [vp, i32, vp, vp, vp, vp]),
+            "gc_alg1_terminate": (i32, [vp, vp, i32, C.c_float, vp, vp, C.c_float, i64, vp, vp, vp, vp]),
+            "gc_set_adam_state": (i32, [vp, i32, vp, vp, vp, vp]),
             "gc_debug_enable_grads": (i32, [vp, i32]),
             "gc_debug_grads": (i32, [vp, i32, vp, vp]),
             "gc_debug_coef_grads": (i32, [vp, i32, vp, vp]),
@@ -349,6 +357,43 @@ class GSCache:
                                     color=rows[:, 7:10], log_scale=rows[:, 10:13],
                                     opacity_logit=rows[:, 13:14]), reset_adam)
 
+    @staticmethod
+    def _rows(a):
+        return np.concatenate([a["position"], a["rotation"], a["color"], a["log_scale"],
+                               a["opacity_logit"]], axis=1)
+
+    @staticmethod
+    def _split(rows):
+        rows = np.ascontiguousarray(np.asarray(rows, np.float32))
+        return {k: np.ascontiguousarray(rows[:, a:b]) for k, (a, b) in
+                dict(position=(0, 3), rotation=(3, 7), color=(7, 10), log_scale=(10, 13),
+                     opacity_logit=(13, 14)).items()}
+
+    def adam_state(self, level, stream=None):
+        """(m rows [N][14], v rows [N][14], counters) of one level (gc_adam_state)."""
+        m, v = self._empty_level(level), self._empty_level(level)
+        lm, lv = self._level_struct(level, m), self._level_struct(level, v)
+        ctr = gc_opt_counters()
+        _check(lib().gc_adam_state(self.h, level, C.byref(lm), C.byref(lv), C.byref(ctr), _stream_ptr(stream)))
+        self.synchronize(stream)
+        return self._rows(m), self._rows(v), dict(t=ctr.t, adam_step=list(ctr.adam_step),
+                                                  beta1_pow=list(ctr.beta1_pow), beta2_pow=list(ctr.beta2_pow))
+
+    def set_adam_state(self, level, m_rows, v_rows, counters=None, stream=None):
+        m, v = self._split(m_rows), self._split(v_rows)
+        lm, lv = self._level_struct(level, m), self._level_struct(level, v)
+        ctr = None
+        if counters is not None:
+            ctr = gc_opt_counters()
+            ctr.t = int(counters["t"])
+            for l in range(MAX_LEVELS):
+                ctr.adam_step[l] = int(counters["adam_step"][l])
+                ctr.beta1_pow[l] = float(counters["beta1_pow"][l])
+                ctr.beta2_pow[l] = float(counters["beta2_pow"][l])
+        _check(lib().gc_set_adam_state(self.h, level, C.byref(lm), C.byref(lv),
+                                       C.byref(ctr) if ctr is not None else None, _stream_ptr(stream)))
+        self.synchronize(stream)
+
     def set_deferred_step(self, on=True):
         """gc_set_deferred_step: leave each fit's optimizer half pending for the next call."""
         _check(lib().gc_set_deferred_step(self.h, 1 if on else 0))
@@ -449,6 +494,22 @@ class GSCache:
                 torch.cuda.synchronize(self.device)
         except Exception:
             pass
+
+
+def alg1_terminate(sigma, n, C_, q, beta=None, eps=1e-6, stream=None):
+    """gc_alg1_terminate on torch CUDA tensors: sigma [P][nmax][3] f32, n [P] i32, q [P] f32,
+    beta [P] f32 or None -> (terminate i32 [P], tr_out f32 [P][3], beta_next f32 [P])."""
+    import torch
+    P, nmax = int(sigma.shape[0]), int(sigma.shape[1])
+    dev = sigma.device
+    term = torch.empty(P, dtype=torch.int32, device=dev)
+    tr = torch.empty((P, 3), dtype=torch.float32, device=dev)
+    bn = torch.empty(P, dtype=torch.float32, device=dev)
+    _check(lib().gc_alg1_terminate(sigma.data_ptr(), n.data_ptr(), nmax, float(C_),
+                                   beta.data_ptr() if beta is not None else None, q.data_ptr(),
+                                   float(eps), P, term.data_ptr(), tr.data_ptr(), bn.data_ptr(),
+                                   _stream_ptr(stream)))
+    return term, tr, bn
 
 
 def level_plan(weights, world: int):

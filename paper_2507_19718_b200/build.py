@@ -24,7 +24,8 @@ def sources():
 
 def deps():
     return sources() + glob.glob(os.path.join(HERE, "csrc", "*.h")) + \
-        glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "gscache.h")]
+        glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + glob.glob(os.path.join(ROOT, "include", "*.h")) + \
+        glob.glob(os.path.join(ROOT, "include", "*.cuh"))
 
 
 def up_to_date() -> bool:

@@ -1008,7 +1008,7 @@ static gc_status level_io(gc_cache c, int level, gc_level_params* p, bool out, c
     for (int k = 0; k < 5; ++k) CK(cudaMemcpyAsync(f[k], t + off[k], sizeof(float) * w[k] * n, cudaMemcpyDefault, s));
   } else {
     for (int k = 0; k < 5; ++k) CK(cudaMemcpyAsync(t + off[k], f[k], sizeof(float) * w[k] * n, cudaMemcpyDefault, s));
-    launch_unpack(t, c->G, c->geom.goff[level], n, c->P, s);
+    launch_unpack(t, c->G, c->geom.goff[level], n, planes ? const_cast<float*>(planes) : c->P, s);
   }
   CK(cudaGetLastError());
   return GC_OK;
@@ -1198,6 +1198,50 @@ gc_status gc_debug_grads(gc_cache c, int level, gc_level_params* dst, gc_stream 
   CK(cudaSetDevice(c->device));
   if (gc_status e = flush_pending(c, (cudaStream_t)stream)) return e;
   return level_io(c, level, dst, true, c->dbg, (cudaStream_t)stream);
+}
+
+// AdamW state of one level (checkpoint / resume): moments in the gc_level_params
+// layout, plus the schedule counter and the per-level bias-correction state.
+gc_status gc_adam_state(gc_cache c, int level, gc_level_params* m, gc_level_params* v, gc_opt_counters* ctr,
+                        gc_stream stream) {
+  if (!c || !m || !v) return fail(GC_ERR_ARG, "NULL handle or moments");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->device));
+  if (gc_status e = flush_pending(c, s)) return e;
+  if (gc_status e = level_io(c, level, m, true, c->M, s)) return e;
+  if (gc_status e = level_io(c, level, v, true, c->V, s)) return e;
+  if (ctr) {
+    DevState h;
+    CK(cudaMemcpyAsync(&h, c->st, sizeof h, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    ctr->t = h.t;
+    for (int l = 0; l < GC_MAX_LEVELS; ++l) {
+      ctr->adam_step[l] = h.adam_step[l]; ctr->beta1_pow[l] = h.b1pow[l]; ctr->beta2_pow[l] = h.b2pow[l];
+    }
+  }
+  return GC_OK;
+}
+
+gc_status gc_set_adam_state(gc_cache c, int level, const gc_level_params* m, const gc_level_params* v,
+                            const gc_opt_counters* ctr, gc_stream stream) {
+  if (!c || !m || !v) return fail(GC_ERR_ARG, "NULL handle or moments");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->device));
+  if (gc_status e = flush_pending(c, s)) return e;
+  gc_level_params tm = *m, tv = *v;
+  if (gc_status e = level_io(c, level, &tm, false, c->M, s)) return e;
+  if (gc_status e = level_io(c, level, &tv, false, c->V, s)) return e;
+  if (ctr) {
+    CK(cudaStreamSynchronize(s));
+    DevState h;
+    CK(cudaMemcpy(&h, c->st, sizeof h, cudaMemcpyDeviceToHost));
+    h.t = ctr->t;
+    for (int l = 0; l < GC_MAX_LEVELS; ++l) {
+      h.adam_step[l] = ctr->adam_step[l]; h.b1pow[l] = ctr->beta1_pow[l]; h.b2pow[l] = ctr->beta2_pow[l];
+    }
+    CK(cudaMemcpy(c->st, &h, sizeof h, cudaMemcpyHostToDevice));
+  }
+  return GC_OK;
 }
 
 gc_status gc_debug_cull(gc_cache c, int level, int32_t* offsets, int32_t* idx, int64_t cap, int64_t* n,

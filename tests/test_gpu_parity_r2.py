@@ -302,3 +302,63 @@ def test_level_sharded_one_rank_routes_through_nccl(gsc):
             err = np.abs((P1 - P) - (oc.P - P))
             assert np.all(err[strong] <= 1e-3 * eta[np.nonzero(strong)[1]] + 4e-7 * (1 + np.abs(P[strong])))
             assert np.all(err <= 2.0 * eta[None, :] + 4e-7 * (1 + np.abs(P)))
+
+
+def test_checkpoint_resume_equals_continuous(gsc):
+    """gc_params + gc_adam_state after 3 fits, restored into a fresh cache (gc_set_params with
+    reset_adam = 0, gc_set_adam_state incl. t, AdamW step counters and beta powers): the next
+    3 fits reproduce the continuous run (up to float-atomic summation order), and
+    the restored state reads back bit-exactly."""
+    from test_gpu_parity import _close_up_to_atomic_order
+    a, _, _ = make_cfg1(gsc)
+    frames = [workload.fit_batch(1, S=60_000, frame=20 + f) for f in range(6)]
+    for f in range(3):
+        a.fit(*[cuda(v) for v in frames[f]])
+    torch.cuda.synchronize()
+    state = [(a.params_rows(l), *a.adam_state(l)) for l in range(3)]
+    assert state[0][3]["t"] == 3 and state[0][3]["adam_step"][:3] == [3, 3, 3]
+    b, _, _ = make_cfg1(gsc, seed=99)               # different init: everything must be restored
+    for l, (p, m, v, ctr) in enumerate(state):
+        b.set_params_rows(l, p)
+        b.set_adam_state(l, m, v, ctr)
+    for l, (p, m, v, ctr) in enumerate(state):
+        p2, m2, v2, c2 = b.params_rows(l), *b.adam_state(l)
+        np.testing.assert_array_equal(p2, p)
+        np.testing.assert_array_equal(m2, m)
+        np.testing.assert_array_equal(v2, v)
+        assert c2 == ctr
+    for f in range(3, 6):
+        sa = a.fit(*[cuda(v) for v in frames[f]])
+        sb = b.fit(*[cuda(v) for v in frames[f]])
+        torch.cuda.synchronize()
+        assert sa.step == sb.step == f + 1
+        np.testing.assert_allclose(list(sb.loss[:3]), list(sa.loss[:3]), rtol=1e-5)
+    _close_up_to_atomic_order(rows(b), rows(a))
+
+
+def test_alg1_device_helper_bit_exact(gsc):
+    """The device-callable Algorithm 1 helper (include/gscache_device.cuh, run by
+    gc_alg1_terminate) vs oracle.alg1 on 20,000 random paths (1-8 vertices, C in [0.1, 4], q
+    uniform, some q right at the 1 - Tr threshold): the termination decision, Tr_out and
+    beta_{n+1} are fp32 operations in the same order on both sides, hence bit-exact."""
+    r = np.random.default_rng(12)
+    P, nmax = 20_000, 8
+    sig = r.uniform(0.0, 1.0, (P, nmax, 3)).astype(np.float32)
+    n = r.integers(0, nmax + 1, P).astype(np.int32)
+    C_ = 1.7
+    beta = r.uniform(0.05, 1.0, P).astype(np.float32)
+    q = r.random(P).astype(np.float32)
+    want = [oracle.alg1(sig[i], n[i], C_, beta[i], q[i], eps=1e-6) for i in range(P)]
+    for i in range(0, P, 7):               # thresholds: q exactly 1 - Tr of the path
+        _, _, bn = want[i]
+        tr = np.float32(bn / beta[i]) if bn != beta[i] else None
+        if tr is not None:
+            q[i] = np.float32(1.0) - tr
+            want[i] = oracle.alg1(sig[i], n[i], C_, beta[i], q[i], eps=1e-6)
+    t, tro, bno = gsc.alg1_terminate(cuda(sig), cuda(n), C_, cuda(q), cuda(beta), eps=1e-6)
+    torch.cuda.synchronize()
+    t, tro, bno = t.cpu().numpy(), tro.cpu().numpy(), bno.cpu().numpy()
+    np.testing.assert_array_equal(t, np.array([w[0] for w in want]))
+    np.testing.assert_array_equal(tro, np.stack([w[1] for w in want]))
+    np.testing.assert_array_equal(bno, np.array([w[2] for w in want], np.float32))
+    assert 0.1 < t.mean() < 0.9

@@ -728,3 +728,48 @@ def test_query_radiance_epilogue_special_cases():
     np.testing.assert_allclose(out[0], y[0] * att[0] / 0.8)
     np.testing.assert_array_equal(out[1], unb[1])
     np.testing.assert_array_equal(out[2], unb[2])
+
+
+# ------------------------------------------------------------------ Algorithm 1 (f3)
+def test_alg1_hand_cases():
+    """Alg. 1 on hand-computed paths: a bright path (Tr >= 0.9) always continues
+    with its plain throughput and beta unchanged; a dark one terminates iff q < 1 - Tr, and
+    otherwise continues with Tr_out / Tr and beta * Tr (eps = 0 here)."""
+    # grey albedos 0.5, 0.5 -> Tr_out = 0.25 (all channels), lum = 0.25 (weights sum to 1)
+    sig = [[0.5, 0.5, 0.5], [0.5, 0.5, 0.5]]
+    for C_, q, term in ((1.0, 0.74, 1), (1.0, 0.76, 0), (4.0, 0.0, 0)):
+        t, tr, b = oracle.alg1(sig, 2, C_, 0.8, q, eps=0.0)
+        assert t == term
+        if C_ == 4.0:                      # Tr = clamp(1.0) >= 0.9: no roulette at all
+            np.testing.assert_allclose(tr, 0.25)
+            np.testing.assert_allclose(b, 0.8)
+        elif term == 0:                    # continued: 0.25 / 0.25 = 1, beta 0.8 * 0.25
+            np.testing.assert_allclose(tr, 1.0, rtol=1e-7)
+            np.testing.assert_allclose(b, 0.2, rtol=1e-7)
+    # luminance weights: a pure-green path of albedo 0.5 -> Tr = 0.7152 * 0.5
+    t, tr, b = oracle.alg1([[0.0, 0.5, 0.0]], 1, 1.0, 1.0, 0.99, eps=0.0)
+    assert t == 0 and abs(b - 0.3576) < 1e-6 and abs(tr[1] - 0.5 / 0.3576) < 1e-5
+    t, _, _ = oracle.alg1([[0.0, 0.5, 0.0]], 1, 1.0, 1.0, 0.6, eps=0.0)
+    assert t == 1                          # q = 0.6 < 1 - 0.3576
+
+
+def test_alg1_roulette_is_unbiased():
+    """Throughput importance sampling is unbiased: over q ~ U(0,1), E[continue *
+    Tr_out] = prod sigma (eps = 0), and the cascaded beta is the probability of
+    reaching the next vertex, E[1{reached} / beta_{n+1}] = 1 -- integrated exactly over q,
+    since the decision is a threshold at q = 1 - Tr."""
+    r = np.random.default_rng(3)
+    for _ in range(50):
+        n = int(r.integers(1, 6))
+        sig = r.uniform(0.05, 0.95, (n, 3))
+        C_ = float(r.uniform(0.2, 3.0))
+        beta = float(r.uniform(0.1, 1.0))
+        _, tr0, _ = oracle.alg1(sig, n, C_, beta, 1.0, eps=0.0)      # q = 1: never terminates
+        plain = np.prod(sig.astype(np.float32), axis=0)
+        _, _, bnext = oracle.alg1(sig, n, C_, beta, 1.0, eps=0.0)
+        Tr = bnext / beta                                                # the continue probability
+        if Tr >= 0.9 * (1 - 1e-6) and np.allclose(tr0, plain, rtol=1e-6):
+            continue                                                     # no roulette at this vertex
+        # P(continue) = P(q >= 1 - Tr) = Tr; E[continue * Tr_out] = Tr * plain / Tr = plain
+        np.testing.assert_allclose(Tr * tr0, plain, rtol=1e-5)
+        np.testing.assert_allclose(Tr * (beta / bnext), 1.0, rtol=1e-6)
