@@ -116,6 +116,18 @@ gc_status gc_create(int levels, const int64_t* counts, const float* init_pos,
 
 gc_status gc_destroy(gc_cache c);
 
+/* Re-initialisation for a change of the volume's morphology (sec.5: the design "requires
+ * re-initialization for cases that alter the overall morphology of the visible volume"; next
+ * row f2): rebuilds the cache in place from a new point cloud exactly as gc_create would with
+ * the same level counts and hyper-parameters -- parameters (Eq. 2 scales when init_log_scale is
+ * NULL), AdamW moments and counters, schedule t, culling grids and lists -- keeping the
+ * handle's communicator, multi-GPU mode, deferral setting, debug flags and level weights.
+ * init_pos / init_rgb / init_log_scale: [counts[0]][3], host or device.  Scratch is re-sized
+ * on the next call (call gc_reserve again before a CUDA-graph capture); graphs captured
+ * earlier must be re-captured.  Synchronises the device. */
+gc_status gc_reinit(gc_cache c, const float* init_pos, const float* init_rgb, const float* init_log_scale,
+                    uint64_t seed);
+
 /* Pre-size scratch for batches of up to S_fit fit samples and S_query query points, so that
  * later gc_fit / gc_query / gc_fit_query(S_fit, S_query) calls never allocate (required
  * before CUDA-graph capture). */

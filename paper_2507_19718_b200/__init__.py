@@ -28,7 +28,7 @@ EXPORTS = ["gc_default_hparams", "gc_create", "gc_destroy", "gc_reserve", "gc_fi
            "gc_params", "gc_set_params", "gc_reset_schedule", "gc_grid", "gc_info",
            "gc_nccl_unique_id", "gc_set_comm", "gc_debug_enable_grads", "gc_debug_grads",
            "gc_debug_coef_grads", "gc_list_generation", "gc_set_level_weights", "gc_level_plan",
-           "gc_comm_info", "gc_adam_state", "gc_set_adam_state", "gc_alg1_terminate",
+           "gc_comm_info", "gc_adam_state", "gc_set_adam_state", "gc_alg1_terminate", "gc_reinit",
            "gc_debug_cull", "gc_debug_levels", "gc_profile_enable", "gc_profile_read",
            "gc_last_error", "gc_status_string"]
 
@@ -117,6 +117,7 @@ def lib():
             "gc_level_plan": (i32, [i32, vp, i32, vp, vp, vp, vp]),
             "gc_comm_info": (i32, [vp, vp, vp, vp, vp, vp]),
             "gc_adam_state": (i32, [vp, i32, vp, vp, vp, vp]),
+            "gc_reinit": (i32, [vp, vp, vp, vp, C.c_uint64]),
             "gc_alg1_terminate": (i32, [vp, vp, i32, C.c_float, vp, vp, C.c_float, i64, vp, vp, vp, vp]),
             "gc_set_adam_state": (i32, [vp, i32, vp, vp, vp, vp]),
             "gc_debug_enable_grads": (i32, [vp, i32]),
@@ -240,6 +241,13 @@ class GSCache:
         self.device = device
         self.goff = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
         self._stats = pinned_stats()
+
+    def reinit(self, init_pos, init_rgb, init_log_scale=None, seed=0):
+        """gc_reinit: rebuild the cache in place from a new point cloud (morphology change)."""
+        p = _Buf(init_pos, np.float32)
+        r = _Buf(init_rgb, np.float32)
+        s = _Buf(init_log_scale, np.float32)
+        _check(lib().gc_reinit(self.h, p.ptr, r.ptr, s.ptr, C.c_uint64(seed)))
 
     def __del__(self):
         h = getattr(self, "h", None)

@@ -495,12 +495,6 @@ void gc_default_hparams(gc_hparams* hp) {
   hp->init_scale_factor = 0.5f; hp->init_zcap = 2.f; hp->cell_edge_scale = 1.f;
 }
 
-static uint64_t splitmix64(uint64_t x) {
-  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-  return z ^ (z >> 31);
-}
 
 static gc_status create_impl(gc_cache c, const int64_t* counts, const float* init_pos,
                              const float* init_rgb, const float* init_log_scale, uint64_t seed) {
@@ -516,14 +510,6 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
   for (int l = 0; l < L; ++l) { c->counts[l] = counts[l]; c->geom.goff[l + 1] = c->geom.goff[l] + counts[l]; }
   for (int l = L; l < kMaxL; ++l) c->geom.goff[l + 1] = c->geom.goff[L];
   const int64_t G = c->G = c->geom.goff[L];
-
-  // permutation pi = stable argsort(splitmix64(seed + i)) (C7), source index of every Gaussian
-  std::vector<std::pair<uint64_t, int64_t>> kv((size_t)N0);
-  for (int64_t i = 0; i < N0; ++i) kv[i] = {splitmix64(seed + (uint64_t)i), i};
-  std::stable_sort(kv.begin(), kv.end(), [](const std::pair<uint64_t, int64_t>& a, const std::pair<uint64_t, int64_t>& b) { return a.first < b.first; });
-  std::vector<int64_t> src((size_t)G);
-  for (int l = 0; l < L; ++l)
-    for (int64_t i = 0; i < counts[l]; ++i) src[c->geom.goff[l] + i] = (l == 0) ? i : kv[i].second;
 
   cudaStream_t s = 0;
   CK(dalloc(&c->P, kNP * G)); CK(dalloc(&c->M, kNP * G)); CK(dalloc(&c->V, kNP * G));
@@ -549,7 +535,9 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
   CK(cudaMemcpy(dpos, init_pos, sizeof(float) * 3 * N0, cudaMemcpyDefault));
   CK(cudaMemcpy(drgb, init_rgb, sizeof(float) * 3 * N0, cudaMemcpyDefault));
   if (init_log_scale) { CK(dalloc(&dls, 3 * N0)); CK(cudaMemcpy(dls, init_log_scale, sizeof(float) * 3 * N0, cudaMemcpyDefault)); }
-  CK(cudaMemcpy(dsrc, src.data(), sizeof(int64_t) * G, cudaMemcpyHostToDevice));
+  // permutation pi = stable argsort(splitmix64(seed + i)) (C7) and the source point of every
+  // Gaussian, on the device (next row f2)
+  CK(launch_level_sources(N0, seed, c->geom, dsrc, s));
   const double p0 = (double)c->hp.init_opacity;
   const float logit = (float)std::log(p0 / (1.0 - p0));
   launch_gather_init(N0, dpos, drgb, dls, dsrc, G, c->P, logit, s);
@@ -567,23 +555,22 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
   CK(cudaDeviceSynchronize());
   cudaFree(dpos); cudaFree(drgb); cudaFree(dsrc); if (dls) cudaFree(dls);
 
-  // culling grids (C8 auto rule, host fp64): level AABB + 5% of its diagonal; cell edge =
-  // 2 tau mean(e^s); dims = clamp(ceil(extent/edge), 1, 512), total cells <= 2^22 per level.
-  std::vector<float> hp_((size_t)kNP * G);
-  CK(cudaMemcpy(hp_.data(), c->P, sizeof(float) * kNP * G, cudaMemcpyDeviceToHost));
+  // culling grids (R1 auto rule): level AABB + 5% of its diagonal; cell edge = 2 tau mean(e^s);
+  // dims = clamp(ceil(extent/edge), 1, 512), total cells <= 2^22 per level.  The per-level
+  // AABB and mean e^s are reduced on the device (k_grid_stats, fixed order), 7 doubles per
+  // level come back; the rule's few flops run here in fp64.
+  double* dstat = nullptr;
+  CK(dalloc(&dstat, 7 * L));
+  CK(launch_grid_stats(c->P, G, c->geom, dstat, s));
+  std::vector<double> hstat(7 * (size_t)L);
+  CK(cudaMemcpy(hstat.data(), dstat, sizeof(double) * 7 * L, cudaMemcpyDeviceToHost));
+  cudaFree(dstat);
   c->geom.coff[0] = 0;
   const double tau = (double)c->hp.cutoff_sigma;
   for (int l = 0; l < L; ++l) {
-    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY}, ms = 0.0;
-    for (int64_t j = c->geom.goff[l]; j < c->geom.goff[l + 1]; ++j) {
-      for (int a = 0; a < 3; ++a) {
-        double v = hp_[(size_t)(P_MU + a) * G + j];
-        lo[a] = std::min(lo[a], v); hi[a] = std::max(hi[a], v);
-      }
-      ms += (std::exp((double)hp_[(size_t)P_S * G + j]) + std::exp((double)hp_[(size_t)(P_S + 1) * G + j]) +
-             std::exp((double)hp_[(size_t)(P_S + 2) * G + j])) / 3.0;
-    }
-    ms /= (double)std::max<int64_t>(1, counts[l]);
+    double lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) { lo[a] = hstat[7 * l + a]; hi[a] = hstat[7 * l + 3 + a]; }
+    const double ms = hstat[7 * l + 6];
     double diag = std::sqrt((hi[0] - lo[0]) * (hi[0] - lo[0]) + (hi[1] - lo[1]) * (hi[1] - lo[1]) + (hi[2] - lo[2]) * (hi[2] - lo[2]));
     double ext[3];
     for (int a = 0; a < 3; ++a) {
@@ -735,6 +722,59 @@ gc_status gc_create(int levels, const int64_t* counts, const float* init_pos, co
   gc_status st = create_impl(c, counts, init_pos, init_rgb, init_log_scale, seed);
   if (st != GC_OK) { std::string e = g_err; destroy_impl(c); g_err = e; return st; }
   *out = c;
+  return GC_OK;
+}
+
+// Re-initialisation on a morphology change (sec.5, next row f2): a new point cloud
+// for the same level counts, as gc_create would build it, on the existing handle -- its
+// communicator, mode, deferral, level weights and statistics ring are kept, everything the
+// point cloud determines (parameters, AdamW state, schedule, grids, culling lists, scratch)
+// is rebuilt.  Implemented as a fresh internal create whose state replaces the old one.
+gc_status gc_reinit(gc_cache c, const float* init_pos, const float* init_rgb, const float* init_log_scale,
+                    uint64_t seed) {
+  if (!c || !init_pos || !init_rgb) return fail(GC_ERR_ARG, "NULL handle or init points");
+  CK(cudaSetDevice(c->device));
+  if (gc_status e = flush_pending(c, 0)) return e;
+  CK(cudaDeviceSynchronize());
+  gc_cache n = new gc_cache_s();
+  n->device = c->device; n->L = c->L; n->hp = c->hp;
+  if (gc_status e = create_impl(n, c->counts, init_pos, init_rgb, init_log_scale, seed)) {
+    std::string msg = g_err; destroy_impl(n); g_err = msg; return e;
+  }
+  // release the old point-cloud state
+  for (void* p : {(void*)c->P, (void*)c->M, (void*)c->V, (void*)c->grad, (void*)c->dbg, (void*)c->dbg_coef,
+                  (void*)c->rec, (void*)c->range, (void*)c->rad2, (void*)c->csr_count, (void*)c->csr_off,
+                  (void*)c->csr_rank, (void*)c->csr_ovf, (void*)c->csr_totals, (void*)c->csr_rec, (void*)c->csr_tiles,
+                  (void*)c->st, (void*)c->lvl, (void*)c->dstats, (void*)c->partial})
+    if (p) cudaFree(p);
+  if (c->hcsr) cudaFreeHost(c->hcsr);
+  c->fit.release();
+  c->qry.release();
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->side2) cudaStreamDestroy(c->side2);
+  if (c->cp) cudaStreamDestroy(c->cp);
+  for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_fork2, c->ev_tail, c->ev_cpfork}) if (e) cudaEventDestroy(e);
+  // take the new one
+#define GSC_TAKE(f) do { c->f = n->f; n->f = decltype(n->f){}; } while (0)
+  GSC_TAKE(geom); GSC_TAKE(G); GSC_TAKE(NC); GSC_TAKE(sms);
+  GSC_TAKE(P); GSC_TAKE(M); GSC_TAKE(V); GSC_TAKE(grad); GSC_TAKE(rec); GSC_TAKE(range); GSC_TAKE(rad2);
+  GSC_TAKE(csr_count); GSC_TAKE(csr_off); GSC_TAKE(csr_totals); GSC_TAKE(csr_rank); GSC_TAKE(csr_ovf);
+  GSC_TAKE(csr_rec); GSC_TAKE(csr_tiles); GSC_TAKE(csr_cap); GSC_TAKE(st); GSC_TAKE(lvl); GSC_TAKE(dstats);
+  GSC_TAKE(hcsr); GSC_TAKE(partial); GSC_TAKE(fb_grid); GSC_TAKE(q_grid); GSC_TAKE(cref);
+  GSC_TAKE(side); GSC_TAKE(side2); GSC_TAKE(ev_fork); GSC_TAKE(ev_join); GSC_TAKE(ev_fork2); GSC_TAKE(ev_tail);
+  GSC_TAKE(cp); GSC_TAKE(ev_cpfork);
+#undef GSC_TAKE
+  delete n;
+  c->dbg = nullptr; c->dbg_coef = nullptr;
+  c->pending = false;
+  c->last_fit_S = -1;
+  c->list_generation += 1;
+  if (c->mode == 1) {                 // this rank's levels under the level-sharded plan
+    unsigned int owned = 0u;
+    for (int l = c->glo; l < c->ghi; ++l) owned |= 1u << l;
+    CK(cudaMemcpy(&c->st->owned, &owned, sizeof owned, cudaMemcpyHostToDevice));
+  }
+  if (c->dbg_mode) { const int m = c->dbg_mode; c->dbg_mode = 0; if (gc_status e = gc_debug_enable_grads(c, m)) return e; }
   return GC_OK;
 }
 

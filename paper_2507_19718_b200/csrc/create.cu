@@ -314,6 +314,145 @@ __global__ void k_unpack(const float* __restrict__ in, int64_t G, int64_t base, 
 
 static int blocks_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); }
 
+// ------------------------------------------------------------- permutation pi on the device
+// pi = stable argsort of splitmix64(seed + i), i < N0 (C7 / reading A9).  splitmix64 is a
+// bijection of its 64-bit input, so the N0 keys are distinct and any correct sort is the
+// stable one; a bitonic network over the next power of two (padding keys (2^64-1, 2^63-1)
+// sort last) sorts (key, index) pairs: global passes for strides >= 1024, then one
+// shared-memory kernel per 2048-element tile for every smaller stride of a merge level.
+__device__ __forceinline__ uint64_t splitmix64_d(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ bool kv_less(uint64_t ka, int64_t ia, uint64_t kb, int64_t ib) {
+  return ka < kb || (ka == kb && ia < ib);
+}
+
+__global__ void k_perm_keys(int64_t N0, int64_t Np, uint64_t seed, uint64_t* key, int64_t* idx) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < Np; i += (int64_t)gridDim.x * blockDim.x) {
+    key[i] = i < N0 ? splitmix64_d(seed + (uint64_t)i) : ~0ull;
+    idx[i] = i < N0 ? i : (int64_t)0x7FFFFFFFFFFFFFFFll;
+  }
+}
+
+__global__ void k_bitonic_global(uint64_t* key, int64_t* idx, int64_t Np, int64_t k, int64_t j) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < Np; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i ^ j;
+    if (p <= i) continue;
+    const bool up = (i & k) == 0;
+    const uint64_t ka = key[i], kb = key[p];
+    const int64_t ia = idx[i], ib = idx[p];
+    if (kv_less(kb, ib, ka, ia) == up) { key[i] = kb; key[p] = ka; idx[i] = ib; idx[p] = ia; }
+  }
+}
+
+constexpr int kBitTile = 2048;
+__global__ void __launch_bounds__(1024) k_bitonic_shared(uint64_t* key, int64_t* idx, int64_t k, int64_t j0) {
+  __shared__ uint64_t sk[kBitTile];
+  __shared__ int64_t si[kBitTile];
+  const int64_t base = (int64_t)blockIdx.x * kBitTile;
+  for (int t = threadIdx.x; t < kBitTile; t += blockDim.x) { sk[t] = key[base + t]; si[t] = idx[base + t]; }
+  __syncthreads();
+  for (int64_t j = j0; j > 0; j >>= 1) {
+    for (int t = threadIdx.x; t < kBitTile; t += blockDim.x) {
+      const int p = t ^ (int)j;
+      if (p > t) {
+        const bool up = ((base + t) & k) == 0;
+        if (kv_less(sk[p], si[p], sk[t], si[t]) == up) {
+          const uint64_t a = sk[t]; sk[t] = sk[p]; sk[p] = a;
+          const int64_t b = si[t]; si[t] = si[p]; si[p] = b;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < kBitTile; t += blockDim.x) { key[base + t] = sk[t]; idx[base + t] = si[t]; }
+}
+
+// src[goff[l] + i] = i on level 0 (caller order), pi[i] on level l >= 1 (nested prefixes)
+__global__ void k_level_src(const int64_t* __restrict__ pi, LevelGeom g, int64_t* src) {
+  const int64_t G = g.goff[g.L];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < G; j += (int64_t)gridDim.x * blockDim.x) {
+    const int l = level_of_gaussian(g, j);
+    const int64_t i = j - g.goff[l];
+    src[j] = l == 0 ? i : pi[i];
+  }
+}
+
+cudaError_t launch_level_sources(int64_t N0, uint64_t seed, const LevelGeom& g, int64_t* src, cudaStream_t s) {
+  int64_t Np = kBitTile;
+  while (Np < N0) Np <<= 1;
+  uint64_t* key = nullptr;
+  int64_t* idx = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&key, sizeof(uint64_t) * Np, s);
+  if (e != cudaSuccess) return e;
+  e = cudaMallocAsync((void**)&idx, sizeof(int64_t) * Np, s);
+  if (e != cudaSuccess) return e;
+  k_perm_keys<<<blocks_for(Np), 256, 0, s>>>(N0, Np, seed, key, idx);
+  for (int64_t k = 2; k <= Np; k <<= 1) {
+    int64_t j = k >> 1;
+    for (; j >= kBitTile; j >>= 1) k_bitonic_global<<<blocks_for(Np), 256, 0, s>>>(key, idx, Np, k, j);
+    k_bitonic_shared<<<(unsigned)(Np / kBitTile), 1024, 0, s>>>(key, idx, k, j);
+  }
+  k_level_src<<<blocks_for(g.goff[g.L]), 256, 0, s>>>(idx, g, src);
+  cudaFreeAsync(key, s);
+  cudaFreeAsync(idx, s);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------- culling-grid statistics per level
+// One CTA per level: the AABB of the means (fp32 values, exact min/max) and the mean over the
+// level of (e^{s0} + e^{s1} + e^{s2}) / 3 in fp64, summed in a fixed tree order -- the inputs of
+// the R1 grid rule, which the host finishes (a handful of flops per level).  out[l] = (lo[3],
+// hi[3], mean e^s).
+__global__ void __launch_bounds__(1024) k_grid_stats(const float* __restrict__ P, int64_t G, LevelGeom g,
+                                                     double* out) {
+  __shared__ double sh[1024];
+  __shared__ float sb[6][32];
+  const int l = blockIdx.x;
+  const int64_t base = g.goff[l], n = g.goff[l + 1] - base;
+  double acc = 0.0;
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const int64_t j = base + i;
+    const double e = __dadd_rn(__dadd_rn(exp((double)P[P_S * G + j]), exp((double)P[(P_S + 1) * G + j])),
+                               exp((double)P[(P_S + 2) * G + j]));
+    acc = __dadd_rn(acc, __ddiv_rn(e, 3.0));
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float v = P[(P_MU + a) * G + j];
+      lo[a] = fminf(lo[a], v); hi[a] = fmaxf(hi[a], v);
+    }
+  }
+  const double tot = eq2_block_sum(acc, sh);
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+      hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+    }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+    for (int a = 0; a < 3; ++a) { sb[a][w] = lo[a]; sb[3 + a][w] = hi[a]; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int a = 0; a < 3; ++a) {
+      float fl = INFINITY, fh = -INFINITY;
+      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { fl = fminf(fl, sb[a][k]); fh = fmaxf(fh, sb[3 + a][k]); }
+      out[7 * l + a] = fl; out[7 * l + 3 + a] = fh;
+    }
+    out[7 * l + 6] = __ddiv_rn(tot, (double)(n > 0 ? n : 1));
+  }
+}
+
+cudaError_t launch_grid_stats(const float* P, int64_t G, const LevelGeom& g, double* out, cudaStream_t s) {
+  k_grid_stats<<<g.L, 1024, 0, s>>>(P, G, g, out);
+  return cudaGetLastError();
+}
+
 void launch_gather_init(int64_t N0, const float* pos, const float* rgb, const float* log_scale,
                         const int64_t* src, int64_t G, float* P, float opacity_logit, cudaStream_t s) {
   k_gather_init<<<blocks_for(G), 256, 0, s>>>(N0, pos, rgb, log_scale, src, G, P, opacity_logit);

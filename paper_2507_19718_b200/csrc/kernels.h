@@ -178,6 +178,11 @@ void launch_gather_init(int64_t N0, const float* pos, const float* rgb, const fl
 cudaError_t launch_eq2_level(const float* P, int64_t G, int64_t base, int64_t n, double* dbar, double* capfl,
                              double zcap, double factor, float* Pw, cudaStream_t s);
 void launch_pack(const float* P, int64_t G, int64_t base, int64_t n, float* out14, cudaStream_t s);
+// src[j] of every Gaussian j: level 0 -> j (caller order), level l >= 1 -> pi[j - goff[l]], with
+// pi = argsort splitmix64(seed + i) computed on the device (C7)
+cudaError_t launch_level_sources(int64_t N0, uint64_t seed, const LevelGeom& g, int64_t* src, cudaStream_t s);
+// per level: lo[3], hi[3] of the means and mean (e^s0 + e^s1 + e^s2)/3 (fp64, fixed order)
+cudaError_t launch_grid_stats(const float* P, int64_t G, const LevelGeom& g, double* out7L, cudaStream_t s);
 void launch_unpack(const float* in14, int64_t G, int64_t base, int64_t n, float* P, cudaStream_t s);
 
 }  // namespace gsc

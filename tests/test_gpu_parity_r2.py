@@ -362,3 +362,37 @@ def test_alg1_device_helper_bit_exact(gsc):
     np.testing.assert_array_equal(tro, np.stack([w[1] for w in want]))
     np.testing.assert_array_equal(bno, np.array([w[2] for w in want], np.float32))
     assert 0.1 < t.mean() < 0.9
+
+
+def test_reinit_equals_fresh_create(gsc):
+    """gc_reinit (morphology change) on a cache that has been fitted: parameters,
+    AdamW state, schedule, culling grids and lists afterwards are those of a fresh gc_create
+    from the new cloud (bit-exact), and the caches then fit identically (up to atomic order)."""
+    a, _, _ = make_cfg1(gsc)
+    for f in range(2):
+        a.fit(*[cuda(v) for v in workload.fit_batch(1, S=30_000, frame=40 + f)])
+    torch.cuda.synchronize()
+    r = np.random.default_rng(8)
+    pos2 = (workload.init_cloud(1)[0][:4096] * 0.7 + r.normal(0, 0.02, (4096, 3))).astype(np.float32)
+    alb2 = r.uniform(0.1, 0.9, (4096, 3)).astype(np.float32)
+    a.reinit(cuda(pos2), alb2, seed=5)
+    b = gsc.GSCache([4096, 1024, 256], pos2, alb2, seed=5)
+    np.testing.assert_array_equal(rows(a), rows(b))
+    for l in range(3):
+        ma, va, ca = a.adam_state(l)
+        assert not ma.any() and not va.any() and ca["t"] == 0 and ca["adam_step"][l] == 0
+        for ga, gb in zip(a.grid(l), b.grid(l)):
+            np.testing.assert_array_equal(ga, gb)
+        oa, ia = a.debug_cull(l)
+        ob, ib = b.debug_cull(l)
+        np.testing.assert_array_equal(oa, ob)
+        np.testing.assert_array_equal(ia, ib)
+    Po = oracle.create([4096, 1024, 256], pos2.astype(np.float64), alb2.astype(np.float64), seed=5,
+                       init_opacity=float(np.float32(0.1)), zcap=2.0, factor=0.5)
+    np.testing.assert_array_equal(rows(a)[:, 0:10], Po.astype(np.float32).astype(np.float64)[:, 0:10])
+    x = workload.fit_batch(1, S=30_000, frame=50)
+    sa = a.fit(*[cuda(v) for v in x])
+    sb = b.fit(*[cuda(v) for v in x])
+    torch.cuda.synchronize()
+    assert sa.step == sb.step == 1
+    np.testing.assert_allclose(list(sa.loss[:3]), list(sb.loss[:3]), rtol=1e-6)
