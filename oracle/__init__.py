@@ -21,6 +21,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "gscache_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "screen_oracle.c"), os.path.join(_HERE, "gscache_oracle.h")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 NP = 14
@@ -36,9 +37,9 @@ DEFAULT_HP = dict(lr=[1.16e-3, 1e-3, 1.25e-2, 0.0, 1.5e-1],
 
 def build(force: bool = False) -> str:
     """Compile the oracle shared library with gcc (-ffp-contract=off, plain -O2)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(f) for f in _SRCS):
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
-                               "-shared", "-o", _LIB, _SRC, "-lm"])
+                               "-shared", "-o", _LIB, _SRCS[0], _SRCS[1], "-lm"])
     return _LIB
 
 
@@ -408,3 +409,93 @@ class OracleCache:
 def chi2_3_cdf(x: float) -> float:
     """F_{chi^2_3}(x) = erf(sqrt(x/2)) - sqrt(2x/pi) e^{-x/2} (closed form, textbook)."""
     return math.erf(math.sqrt(x / 2.0)) - math.sqrt(2.0 * x / math.pi) * math.exp(-x / 2.0)
+
+
+# ------------------------------------------------ screen-space evaluator (next row f1)
+class _Cam(C.Structure):
+    _fields_ = [("W", C.c_int), ("H", C.c_int), ("fx", C.c_double), ("fy", C.c_double),
+                ("cx", C.c_double), ("cy", C.c_double), ("view", C.c_double * 12),
+                ("znear", C.c_double)]
+
+
+def _cam(cam):
+    c = _Cam()
+    c.W, c.H = int(cam["width"]), int(cam["height"])
+    c.fx, c.fy, c.cx, c.cy = (float(cam[k]) for k in ("fx", "fy", "cx", "cy"))
+    for i, v in enumerate(np.asarray(cam["view"], np.float64).reshape(12)):
+        c.view[i] = float(v)
+    c.znear = float(cam.get("znear", 0.2))
+    return c
+
+
+def project(P, cam):
+    """orc_project of every row: [n][16] = ok, u, v, depth, conic(3), w, chat(3), x0, x1,
+    y0, y1, rect_amb (screen_oracle.c, reading A23)."""
+    P = _d(P).reshape(-1, NP)
+    out = np.empty((len(P), 16))
+    c = _cam(cam)
+    for j in range(len(P)):
+        lib().orc_project(_p(P[j].copy(), np.float64), C.byref(c), _p(out[j:j + 1], np.float64))
+    return out
+
+
+def render(P, cam, pix=None):
+    """One level's cache image (sec.3.1, front-to-back alpha compositing of the
+    projected Gaussians, reading A23): (rgb [H][W][3], T [H][W], amb [H][W]); with `pix`
+    (linear pixel indices) only those pixels are computed (the rest is NaN)."""
+    P = _d(P).reshape(-1, NP)
+    c = _cam(cam)
+    n = c.W * c.H
+    rgb = np.full((n, 3), np.nan)
+    T = np.full(n, np.nan)
+    amb = np.zeros(n, np.int32)
+    if pix is None:
+        lib().orc_render(C.c_int64(len(P)), _p(P, np.float64), C.byref(c), C.c_int64(-1), None,
+                         _p(rgb, np.float64), _p(T, np.float64), _p(amb, np.int32))
+    else:
+        pix = np.ascontiguousarray(pix, np.int64)
+        lib().orc_render(C.c_int64(len(P)), _p(P, np.float64), C.byref(c), C.c_int64(len(pix)),
+                         _p(pix, np.int64), _p(rgb, np.float64), _p(T, np.float64), _p(amb, np.int32))
+    return rgb.reshape(c.H, c.W, 3), T.reshape(c.H, c.W), amb.reshape(c.H, c.W)
+
+
+def image_loss(goff, P, cam, target, valid=None, denom=None, hdr_eps=0.01):
+    """Eq. 4 over the per-level cache images: (total, per_level).  `denom` freezes
+    the denominator images (reading A10's stop-gradient; its finite differences are the mode-0
+    gradient)."""
+    goff = _i64(goff)
+    L = len(goff) - 1
+    P = _d(P).reshape(-1, NP)
+    c = _cam(cam)
+    tgt = _d(target).reshape(-1)
+    va = None if valid is None else np.ascontiguousarray(valid, np.uint8).reshape(-1)
+    de = None if denom is None else _d(denom).reshape(-1)
+    per = np.empty(L)
+    lib().orc_image_loss.restype = C.c_double
+    tot = lib().orc_image_loss(C.c_int(L), _p(goff, np.int64), _p(P, np.float64), C.byref(c),
+                               _p(tgt, np.float64), None if va is None else _p(va, np.uint8),
+                               None if de is None else _p(de, np.float64), C.c_double(hdr_eps),
+                               _p(per, np.float64))
+    return tot, per
+
+
+def image_grad_fd(goff, P, cam, target, valid=None, hdr_eps=0.01, h=1e-6):
+    """Gradient of image_loss (mode 0: denominators frozen at the unperturbed render) by fp64
+    central finite differences over every raw parameter: [G][14].  Defines the screen-space
+    backward for the tests (the derivative of the forward above, "inverse splatting")."""
+    goff = _i64(goff)
+    P = _d(P).reshape(-1, NP).copy()
+    L = len(goff) - 1
+    den = np.concatenate([render(P[goff[l]:goff[l + 1]], cam)[0][None] for l in range(L)])
+    g = np.zeros_like(P)
+    for j in range(len(P)):
+        for k in range(NP):
+            v = P[j, k]
+            step = h * max(1.0, abs(v))
+            P[j, k] = v + step
+            lp, _ = image_loss(goff, P, cam, target, valid, den, hdr_eps)
+            P[j, k] = v - step
+            lm, _ = image_loss(goff, P, cam, target, valid, den, hdr_eps)
+            P[j, k] = v
+            g[j, k] = (lp - lm) / (2 * step)
+    return g

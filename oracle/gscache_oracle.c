@@ -166,10 +166,7 @@ int orc_create(int L, const int64_t* counts, const double* init_pos, const doubl
 
 /* ------------------------------------------------------------- activation (C1) */
 
-typedef struct {
-  double mu[3], qhat[4], qnorm, R[3][3], D[3], A[3][3], w, chat[3], v[3];
-  int degenerate;
-} orc_gauss;
+#include "gscache_oracle.h"
 
 /* R(q) for a unit quaternion (w,x,y,z), standard 3DGS formula, written order. */
 static void orc_rot(const double q[4], double R[3][3]) {
