@@ -196,6 +196,42 @@ gc_status gc_alg1_terminate(const float* sigma, const int32_t* n, int nmax, floa
                             const float* q, float eps, int64_t P, int32_t* terminate, float* tr_out,
                             float* beta_next, gc_stream stream);
 
+/* ---- screen-space cache images (next row f1: the paper's own read / train path) ----------
+ * Each level is rasterized into an image with the 3D Gaussian splatting rasterizer (P:68
+ * sec.3.1, after Kerbl et al.): EWA projection with a 0.3 px^2 low-pass, 16 x 16 tiles,
+ * depth-ordered front-to-back alpha compositing (alpha = min(0.99, w G), skipped below 1/255,
+ * stop below T = 1e-4), background 0.  All requested levels are rasterized in one pass over a
+ * joint (level, tile) list -- the paper's future-work joint multi-level rasterization.
+ * Readings A23; the oracle is oracle/screen_oracle.c.  Pixel (px, py) is sampled
+ * at (px + 0.5, py + 0.5); a Gaussian is culled when its camera depth is <= znear, its
+ * projected centre lies outside [-0.15 W, 1.15 W] x [-0.15 H, 1.15 H], or its 2D covariance
+ * is not positive definite. */
+typedef struct {
+  int width, height;               /* image size in pixels                                        */
+  float fx, fy, cx, cy;            /* pinhole intrinsics in pixels: u = fx x/z + cx, v = fy y/z + cy */
+  float view[12];                  /* world -> camera [R | t], row-major 3 x 4; camera looks down +z */
+  float znear;                     /* near plane (0.2 in 3DGS)                                     */
+} gc_camera;
+
+/* Cache images of level `level` (or of all L levels, jointly, when level == -1): out_rgb
+ * [Lr][H][W][3] f32 and out_T [Lr][H][W] f32 (final transmittance, nullable), device memory,
+ * Lr = 1 or L.  Synchronises the stream once (the number of (tile, Gaussian) pairs sizes the
+ * sort); not graph-capturable. */
+gc_status gc_render(gc_cache c, const gc_camera* cam, int level, float* out_rgb, float* out_T,
+                    gc_stream stream);
+
+/* One optimisation step of every level on screen-space samples (sec.3.5 "inverse
+ * splatting", Eq. 4): target [L][H][W][3] f32, the noisy per-level radiance images of
+ * the frame's paths; valid [L][H][W] u8 or NULL (all): pixels without a path of that length
+ * carry no sample.  Renders all levels, takes Eq. 4 per level over 3 k_l (k_l = valid pixels;
+ * loss_grad_mode as gc_fit), back-propagates through the compositing and the EWA projection
+ * into all 14 raw parameters, and takes the shared AdamW step (schedule, level skip, frozen
+ * groups as gc_fit), then rebuilds the evaluation records and culling lists so that the
+ * world-space calls see the new parameters.  stats as gc_fit (n_in = L H W pixel samples).
+ * Device buffers; single GPU (GC_ERR_UNSUPPORTED with a communicator); synchronises once. */
+gc_status gc_fit_image(gc_cache c, const gc_camera* cam, const float* target, const uint8_t* valid,
+                       gc_stream stream, gc_fit_stats* stats);
+
 /* Deferred optimizer step (enable != 0; off by default).  gc_fit / gc_fit_query then leave
  * their optimizer half -- the AdamW step with the next step's evaluation records, and the
  * culling-list rebuild -- pending, and the next call on the handle launches it on an internal

@@ -405,6 +405,19 @@ class OracleCache:
     def query(self, x, length=None, level=-1):
         return query(self.goff, self.P, x, length, level, tau=float(self.hp[14]), grids=self.grids)
 
+    def step_with_grad(self, grad, count=None):
+        """The optimizer half of a step (C6) on a given normalised raw gradient [G][14]
+        (e.g. the screen-space path's, next row f1); count: per-level sample counts (default:
+        every level stepped).  Returns False for a no-op step."""
+        g = _d(grad).reshape(-1, NP).copy()
+        cnt = _i64(np.ones(self.L) if count is None else count)
+        nonfinite = C.c_int64()
+        r = lib().orc_opt_step(C.c_int(self.L), _p(self.goff, np.int64), _p(self.P, np.float64),
+                               _p(self.M, np.float64), _p(self.V, np.float64),
+                               _p(self.adam_step, np.int64), C.byref(self.t), _p(self.hp, np.float64),
+                               _p(cnt, np.int64), _p(g, np.float64), C.byref(nonfinite))
+        return r == 0
+
 
 def chi2_3_cdf(x: float) -> float:
     """F_{chi^2_3}(x) = erf(sqrt(x/2)) - sqrt(2x/pi) e^{-x/2} (closed form, textbook)."""

@@ -663,6 +663,10 @@ double orc_lr_schedule(double eta0, int64_t t) { return eta0 / (1.0 + log((doubl
 /* group of raw parameter column k: 0 pos, 1 rot, 2 colour, 3 scale, 4 opacity */
 static int orc_group(int k) { return k < 3 ? 0 : (k < 7 ? 1 : (k < 10 ? 2 : (k < 13 ? 3 : 4))); }
 
+int orc_opt_step(int L, const int64_t* goff, double* P, double* M, double* V, int64_t* adam_step,
+                 int64_t* t_sched, const double* hp, const int64_t* count, const double* grad,
+                 int64_t* nonfinite);
+
 /* hp layout: lr[5], wd[5], beta1, beta2, adam_eps, hdr_eps, tau, mode, schedule (17 doubles)
  * One gc_fit step (C6): returns 0 = stepped, 1 = no valid sample (no-op, t not advanced). */
 int orc_fit_step(int L, const int64_t* goff, double* P, double* M, double* V, int64_t* adam_step,
@@ -675,6 +679,16 @@ int orc_fit_step(int L, const int64_t* goff, double* P, double* M, double* V, in
   orc_loss_grad(L, goff, P, hp[14], hp[13], (int)hp[15], S, x, len, rgb, g_origin, g_inv, g_dims,
                 lv, NULL, count, loss, grad, npairs, NULL);
   free(lv);
+  return orc_opt_step(L, goff, P, M, V, adam_step, t_sched, hp, count, grad, nonfinite);
+}
+
+/* The optimizer half of a step (C6) on a given normalised raw gradient grad [G][14] with the
+ * per-level sample counts `count` (a level with count 0 skips, A12; none at all: no-op).
+ * Shared by orc_fit_step and the screen-space fit of the tests (next row f1). */
+int orc_opt_step(int L, const int64_t* goff, double* P, double* M, double* V, int64_t* adam_step,
+                 int64_t* t_sched, const double* hp, const int64_t* count, const double* grad,
+                 int64_t* nonfinite) {
+  int64_t G = goff[L];
   int64_t tot = 0;
   for (int l = 0; l < L; ++l) tot += count[l];
   *nonfinite = 0;

@@ -29,6 +29,7 @@ EXPORTS = ["gc_default_hparams", "gc_create", "gc_destroy", "gc_reserve", "gc_fi
            "gc_nccl_unique_id", "gc_set_comm", "gc_debug_enable_grads", "gc_debug_grads",
            "gc_debug_coef_grads", "gc_list_generation", "gc_set_level_weights", "gc_level_plan",
            "gc_comm_info", "gc_adam_state", "gc_set_adam_state", "gc_alg1_terminate", "gc_reinit",
+           "gc_render", "gc_fit_image",
            "gc_debug_cull", "gc_debug_levels", "gc_profile_enable", "gc_profile_read",
            "gc_last_error", "gc_status_string"]
 
@@ -72,6 +73,20 @@ def pinned_stats() -> "gc_fit_stats":
         return st
     except Exception:
         return gc_fit_stats()
+
+
+class gc_camera(C.Structure):
+    _fields_ = [("width", C.c_int), ("height", C.c_int), ("fx", C.c_float), ("fy", C.c_float),
+                ("cx", C.c_float), ("cy", C.c_float), ("view", C.c_float * 12), ("znear", C.c_float)]
+
+
+def make_camera(width, height, fx, fy, cx, cy, view, znear=0.2) -> "gc_camera":
+    """gc_camera from a 3x4 (or 12) world->camera matrix [R | t]."""
+    c = gc_camera()
+    c.width, c.height, c.fx, c.fy, c.cx, c.cy, c.znear = int(width), int(height), fx, fy, cx, cy, znear
+    for i, v in enumerate(np.asarray(view, np.float64).reshape(12)):
+        c.view[i] = float(v)
+    return c
 
 
 class gc_opt_counters(C.Structure):
@@ -118,6 +133,8 @@ def lib():
             "gc_comm_info": (i32, [vp, vp, vp, vp, vp, vp]),
             "gc_adam_state": (i32, [vp, i32, vp, vp, vp, vp]),
             "gc_reinit": (i32, [vp, vp, vp, vp, C.c_uint64]),
+            "gc_render": (i32, [vp, vp, i32, vp, vp, vp]),
+            "gc_fit_image": (i32, [vp, vp, vp, vp, vp, vp]),
             "gc_alg1_terminate": (i32, [vp, vp, i32, C.c_float, vp, vp, C.c_float, i64, vp, vp, vp, vp]),
             "gc_set_adam_state": (i32, [vp, i32, vp, vp, vp, vp]),
             "gc_debug_enable_grads": (i32, [vp, i32]),
@@ -241,6 +258,26 @@ class GSCache:
         self.device = device
         self.goff = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
         self._stats = pinned_stats()
+
+    # ----------------------------------------------------- screen-space cache images (f1)
+    def render(self, cam: "gc_camera", level=-1, with_T=False, stream=None):
+        """gc_render: cache images [Lr][H][W][3] (torch CUDA tensor; Lr = L for level -1)."""
+        import torch
+        Lr = self.L if level < 0 else 1
+        out = torch.empty((Lr, cam.height, cam.width, 3), dtype=torch.float32, device=f"cuda:{self.device}")
+        T = torch.empty((Lr, cam.height, cam.width), dtype=torch.float32, device=out.device) if with_T else None
+        _check(lib().gc_render(self.h, C.byref(cam), int(level), out.data_ptr(),
+                               T.data_ptr() if T is not None else None, _stream_ptr(stream)))
+        return (out, T) if with_T else out
+
+    def fit_image(self, cam: "gc_camera", target, valid=None, stream=None, stats=None):
+        """gc_fit_image: one optimisation step on per-level radiance images target
+        [L][H][W][3] (CUDA f32) with optional valid [L][H][W] (CUDA u8)."""
+        st = stats if stats is not None else self._stats
+        _check(lib().gc_fit_image(self.h, C.byref(cam), target.data_ptr(),
+                                  valid.data_ptr() if valid is not None else None,
+                                  _stream_ptr(stream), C.addressof(st)))
+        return st
 
     def reinit(self, init_pos, init_rgb, init_log_scale=None, seed=0):
         """gc_reinit: rebuild the cache in place from a new point cloud (morphology change)."""

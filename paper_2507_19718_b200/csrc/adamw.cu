@@ -105,7 +105,8 @@ __device__ void chain_rule(const float p[kNP], const float cg[12], float out[kNP
 // k_record_cull right after (split so both kernels stay spill-free and latency-hidden).
 __global__ void __launch_bounds__(kAdamThreads, kAdamBlocksPerSM) k_adamw(
     int64_t G, float* __restrict__ P, float* __restrict__ M, float* __restrict__ V, float* __restrict__ grad,
-    float* __restrict__ dbg, DevState* st, AdamHP hp, LevelGeom g, unsigned long long* nonfinite) {
+    float* __restrict__ dbg, DevState* st, AdamHP hp, LevelGeom g, unsigned long long* nonfinite,
+    const float* __restrict__ rawg) {
   pdl_enter();
   // the culling rebuild that follows this kernel (k_record_cull -> scan -> k_cull_emit) sets the
   // overflow flag afresh; the previous rebuild's flag has been read by this call's k_stats
@@ -130,7 +131,12 @@ __global__ void __launch_bounds__(kAdamThreads, kAdamBlocksPerSM) k_adamw(
     const float cg[12] = {c0.x * s, c0.y * s, c0.z * s, c0.w * s, c1.x * s, c1.y * s,
                           c1.z * s, c1.w * s, c2.x * s, c2.y * s, c2.z * s, c2.w * s};
     float raw[kNP];
-    chain_rule(p, cg, raw);
+    if (rawg) {                      // screen-space path: raw gradients given (normalised here)
+#pragma unroll
+      for (int k = 0; k < kNP; ++k) raw[k] = rawg[k * G + j] * s;
+    } else {
+      chain_rule(p, cg, raw);
+    }
     if (dbg) {
 #pragma unroll
       for (int k = 0; k < kNP; ++k) dbg[k * G + j] = raw[k];
@@ -176,7 +182,8 @@ void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp
 
 void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, CullBufs cb, float* dbg_grad,
                   DevState* st, const gc_hparams& hp,
-                  const LevelGeom& g, unsigned long long* nonfinite, cudaStream_t s, Profiler* prof) {
+                  const LevelGeom& g, unsigned long long* nonfinite, cudaStream_t s, Profiler* prof,
+                  const float* raw_grad) {
   AdamHP h;
   for (int k = 0; k < GC_NGROUPS; ++k) h.wd[k] = hp.weight_decay[k];
   h.beta1 = hp.beta1; h.beta2 = hp.beta2; h.eps = hp.adam_eps; h.tau = (double)hp.cutoff_sigma;
@@ -185,7 +192,8 @@ void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, CullBufs
   {
     ProfScope ps(prof, "adamw", s);
     int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((G + kAdamThreads - 1) / kAdamThreads, 148 * kAdamBlocksPerSM));
-    launch_pdl(k_adamw, dim3(blocks), dim3(kAdamThreads), 0, s, G, P, M, V, grad, dbg_grad, st, h, g, nonfinite);
+    launch_pdl(k_adamw, dim3(blocks), dim3(kAdamThreads), 0, s, G, P, M, V, grad, dbg_grad, st, h, g, nonfinite,
+               raw_grad);
   }
   {
     ProfScope ps(prof, "record_cull", s);

@@ -137,6 +137,7 @@ struct gc_cache_s {
   uint32_t* r_perm = nullptr;
   int64_t r_in_cap = 0, r_perm_cap = 0, r_send_cap_back = 0;
   std::vector<int64_t> rt_send, rt_recv, rt_soff, rt_roff;   // last routing's per-peer counts/offsets
+  ScreenBufs scr;                         // screen-space evaluator buffers (gc_render / gc_fit_image)
   float* pack_tmp = nullptr;
   int64_t pack_cap = 0;
   cudaStream_t side = nullptr;            // gc_fit_query: lookups run beside the fit samples' ingest
@@ -663,6 +664,15 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
   return GC_OK;
 }
 
+static void free_screen(ScreenBufs& b) {
+  for (void* p : {(void*)b.pa, (void*)b.pb, (void*)b.pc, (void*)b.rect, (void*)b.touched, (void*)b.off,
+                  (void*)b.bsums, (void*)b.total, (void*)b.key, (void*)b.val, (void*)b.ranges, (void*)b.img,
+                  (void*)b.T, (void*)b.dLdC, (void*)b.last, (void*)b.g2d, (void*)b.raw})
+    if (p) cudaFree(p);
+  if (b.htotal) cudaFreeHost(b.htotal);
+  b = ScreenBufs();
+}
+
 static void destroy_impl(gc_cache c) {
   if (!c) return;
   cudaSetDevice(c->device);
@@ -680,6 +690,7 @@ static void destroy_impl(gc_cache c) {
     delete p;
   }
   if (c->dbg_coef) cudaFree(c->dbg_coef);
+  free_screen(c->scr);
   if (c->gcomm) ncclCommDestroy(c->gcomm);
   if (c->comm) ncclCommDestroy(c->comm);
   for (void* p : {(void*)c->r_count, (void*)c->r_all, (void*)c->r_base, (void*)c->r_cursor, (void*)c->r_send,
@@ -750,6 +761,7 @@ gc_status gc_reinit(gc_cache c, const float* init_pos, const float* init_rgb, co
   if (c->hcsr) cudaFreeHost(c->hcsr);
   c->fit.release();
   c->qry.release();
+  free_screen(c->scr);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->side2) cudaStreamDestroy(c->side2);
   if (c->cp) cudaStreamDestroy(c->cp);
@@ -1238,6 +1250,99 @@ gc_status gc_debug_grads(gc_cache c, int level, gc_level_params* dst, gc_stream 
   CK(cudaSetDevice(c->device));
   if (gc_status e = flush_pending(c, (cudaStream_t)stream)) return e;
   return level_io(c, level, dst, true, c->dbg, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------ screen-space evaluator (f1)
+// Projection of levels [lev0, lev1), the (tile, depth) sort and the joint raster into the
+// handle's image buffers (c->scr.img / T / last), or into out/outT when given.
+static gc_status screen_render(gc_cache c, const gc_camera* cam, int lev0, int lev1, float* out, float* outT,
+                               cudaStream_t s) {
+  if (!cam || cam->width < 1 || cam->height < 1 || cam->width > 16384 || cam->height > 16384 || !(cam->znear > 0.f))
+    return fail(GC_ERR_ARG, "bad camera");
+  ScreenBufs& b = c->scr;
+  const int64_t G = c->G;
+  if (!b.pa) {
+    CK(dalloc(&b.pa, G)); CK(dalloc(&b.pb, G)); CK(dalloc(&b.pc, G)); CK(dalloc(&b.rect, G));
+    CK(dalloc(&b.touched, G)); CK(dalloc(&b.off, G)); CK(dalloc(&b.bsums, G / 4096 + 2)); CK(dalloc(&b.total, 1));
+    CK(cudaHostAlloc((void**)&b.htotal, sizeof(uint32_t), cudaHostAllocDefault));
+    CK(dalloc(&b.g2d, 12 * G)); CK(cudaMemset(b.g2d, 0, sizeof(float) * 12 * G));
+    CK(dalloc(&b.raw, kNP * G));
+  }
+  const SCam sc = make_scam(*cam);
+  const int Lr = lev1 - lev0;
+  const int64_t npx = (int64_t)cam->width * cam->height;
+  const int64_t ntiles = (int64_t)sc.TX * sc.TY;
+  if (b.img_cap < Lr * npx) {
+    CK(cudaDeviceSynchronize());
+    for (void* p : {(void*)b.img, (void*)b.T, (void*)b.dLdC, (void*)b.last}) if (p) cudaFree(p);
+    CK(dalloc(&b.img, 3 * Lr * npx)); CK(dalloc(&b.T, Lr * npx)); CK(dalloc(&b.dLdC, 3 * Lr * npx));
+    CK(dalloc(&b.last, Lr * npx));
+    b.img_cap = Lr * npx;
+  }
+  if (b.range_cap < Lr * ntiles) {
+    CK(cudaDeviceSynchronize());
+    if (b.ranges) cudaFree(b.ranges);
+    CK(dalloc(&b.ranges, Lr * ntiles));
+    b.range_cap = Lr * ntiles;
+  }
+  if ((int64_t)Lr * ntiles >= ((int64_t)1 << 31)) return fail(GC_ERR_ARG, "image too large for the tile keys");
+  const int64_t g0 = c->geom.goff[lev0], g1 = c->geom.goff[lev1];
+  CK(launch_sproject(c->P, G, g0, g1, sc, b, s));
+  CK(cudaMemcpyAsync(b.htotal, b.total, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int64_t npairs = *b.htotal;
+  const int64_t Np = sort_kv_size(std::max<int64_t>(npairs, 1));
+  if (b.kv_cap < Np) {
+    if (b.key) cudaFree(b.key);
+    if (b.val) cudaFree(b.val);
+    CK(dalloc(&b.key, Np)); CK(dalloc(&b.val, Np));
+    b.kv_cap = Np;
+  }
+  CK(launch_skeys_sort(g0, g1, c->geom, lev0, Lr, sc, b, npairs, Np, s));
+  CK(launch_sraster(sc, Lr, b, out ? out : b.img, outT ? outT : b.T, b.last, s));
+  return GC_OK;
+}
+
+gc_status gc_render(gc_cache c, const gc_camera* cam, int level, float* out_rgb, float* out_T, gc_stream stream) {
+  if (!c || !cam || !out_rgb) return fail(GC_ERR_ARG, "NULL handle, camera or output");
+  if (level < -1 || level >= c->L) return fail(GC_ERR_ARG, "level %d not in [-1, %d)", level, c->L);
+  if (!is_device_ptr(out_rgb) || (out_T && !is_device_ptr(out_T))) return fail(GC_ERR_ARG, "gc_render outputs must be device memory");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->device));
+  if (gc_status e = check_sticky(c)) return e;
+  if (capturing(s)) return fail(GC_ERR_STATE, "gc_render is not graph-capturable");
+  if (gc_status e = flush_pending(c, s)) return e;
+  const int lev0 = level < 0 ? 0 : level, lev1 = level < 0 ? c->L : level + 1;
+  if (gc_status e = screen_render(c, cam, lev0, lev1, out_rgb, out_T, s)) return e;
+  CK(cudaGetLastError());
+  return GC_OK;
+}
+
+gc_status gc_fit_image(gc_cache c, const gc_camera* cam, const float* target, const uint8_t* valid, gc_stream stream,
+                       gc_fit_stats* stats) {
+  if (!c || !cam || !target) return fail(GC_ERR_ARG, "NULL handle, camera or target");
+  if (!is_device_ptr(target) || (valid && !is_device_ptr(valid))) return fail(GC_ERR_ARG, "gc_fit_image inputs must be device memory");
+  if (c->comm) return fail(GC_ERR_UNSUPPORTED, "gc_fit_image is single-GPU");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->device));
+  if (gc_status e = check_sticky(c)) return e;
+  if (capturing(s)) return fail(GC_ERR_STATE, "gc_fit_image is not graph-capturable");
+  if (gc_status e = flush_pending(c, s)) return e;
+  const int L = c->L;
+  if (gc_status e = screen_render(c, cam, 0, L, nullptr, nullptr, s)) return e;
+  ScreenBufs& b = c->scr;
+  const SCam sc = make_scam(*cam);
+  const int64_t npx = (int64_t)cam->width * cam->height;
+  CK(launch_sloss(b.img, target, valid, L, npx, c->hp.hdr_eps, c->hp.loss_grad_mode, b.dLdC, c->partial, s));
+  launch_stats(c->partial, c->geom, (int64_t)L * npx, c->lvl, true, c->st, c->hp, L, c->dstats, s, &c->prof);
+  CK(launch_sraster_bwd(sc, L, b, b.T, b.last, b.dLdC, b.g2d, s));
+  CK(launch_sproject_bwd(c->P, c->G, 0, c->G, sc, b, b.g2d, b.raw, s));
+  launch_adamw(c->G, c->P, c->M, c->V, c->grad, cull_bufs(c), c->dbg_on ? c->dbg : nullptr, c->st, c->hp, c->geom,
+               reinterpret_cast<unsigned long long*>(&c->dstats->nonfinite_grads), s, &c->prof, b.raw);
+  if (gc_status e = rebuild_csr(c, s, false)) return e;
+  if (gc_status e = emit_stats(c, stats, s)) return e;
+  CK(cudaGetLastError());
+  return GC_OK;
 }
 
 // AdamW state of one level (checkpoint / resume): moments in the gc_level_params

@@ -382,9 +382,22 @@ __global__ void k_level_src(const int64_t* __restrict__ pi, LevelGeom g, int64_t
   }
 }
 
-cudaError_t launch_level_sources(int64_t N0, uint64_t seed, const LevelGeom& g, int64_t* src, cudaStream_t s) {
+int64_t sort_kv_size(int64_t n) {
   int64_t Np = kBitTile;
-  while (Np < N0) Np <<= 1;
+  while (Np < n) Np <<= 1;
+  return Np;
+}
+
+void launch_sort_kv(uint64_t* key, int64_t* idx, int64_t Np, cudaStream_t s) {
+  for (int64_t k = 2; k <= Np; k <<= 1) {
+    int64_t j = k >> 1;
+    for (; j >= kBitTile; j >>= 1) k_bitonic_global<<<blocks_for(Np), 256, 0, s>>>(key, idx, Np, k, j);
+    k_bitonic_shared<<<(unsigned)(Np / kBitTile), 1024, 0, s>>>(key, idx, k, j);
+  }
+}
+
+cudaError_t launch_level_sources(int64_t N0, uint64_t seed, const LevelGeom& g, int64_t* src, cudaStream_t s) {
+  const int64_t Np = sort_kv_size(N0);
   uint64_t* key = nullptr;
   int64_t* idx = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&key, sizeof(uint64_t) * Np, s);
@@ -392,11 +405,7 @@ cudaError_t launch_level_sources(int64_t N0, uint64_t seed, const LevelGeom& g, 
   e = cudaMallocAsync((void**)&idx, sizeof(int64_t) * Np, s);
   if (e != cudaSuccess) return e;
   k_perm_keys<<<blocks_for(Np), 256, 0, s>>>(N0, Np, seed, key, idx);
-  for (int64_t k = 2; k <= Np; k <<= 1) {
-    int64_t j = k >> 1;
-    for (; j >= kBitTile; j >>= 1) k_bitonic_global<<<blocks_for(Np), 256, 0, s>>>(key, idx, Np, k, j);
-    k_bitonic_shared<<<(unsigned)(Np / kBitTile), 1024, 0, s>>>(key, idx, k, j);
-  }
+  launch_sort_kv(key, idx, Np, s);
   k_level_src<<<blocks_for(g.goff[g.L]), 256, 0, s>>>(idx, g, src);
   cudaFreeAsync(key, s);
   cudaFreeAsync(idx, s);

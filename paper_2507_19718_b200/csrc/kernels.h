@@ -151,9 +151,11 @@ void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp
                          gc_fit_stats* dev_stats, cudaStream_t s);
 // nonfinite: where the count of skipped non-finite gradient elements is added (the call's
 // gc_fit_stats, or DevState::nonfinite when the step is deferred into the next call)
+// raw_grad (nullable): [14][G] unnormalised raw-parameter gradients (the screen-space path, f1)
+// used instead of the chain rule from the 12 coefficient gradients
 void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, CullBufs cb, float* dbg_grad,
                   DevState* st, const gc_hparams& hp, const LevelGeom& g, unsigned long long* nonfinite,
-                  cudaStream_t s, Profiler* prof);
+                  cudaStream_t s, Profiler* prof, const float* raw_grad = nullptr);
 
 // shard.cu -- level-sharded mode (gc_set_comm mode 1)
 struct RoutePlan {
@@ -172,6 +174,35 @@ void launch_unpack_routed(const float4* recv, int64_t R, bool fit, float* pos, i
                           cudaStream_t s);
 void launch_unroute(const float* res, const uint32_t* perm, int64_t n, float* out, cudaStream_t s);
 
+// screen.cu -- screen-space evaluator (next row f1)
+struct SCam {
+  int W, H, TX, TY;
+  float fx, fy, cx, cy, znear;
+  float R[9], t[3];
+};
+SCam make_scam(const gc_camera& c);
+struct ScreenBufs {
+  float4 *pa = nullptr, *pb = nullptr, *pc = nullptr;   // [G] projection records
+  int4* rect = nullptr;                                  // [G] tile rectangles
+  uint32_t *touched = nullptr, *off = nullptr, *bsums = nullptr, *total = nullptr, *htotal = nullptr;
+  uint64_t* key = nullptr; int64_t* val = nullptr; int64_t kv_cap = 0;   // (tile, depth) -> Gaussian
+  uint2* ranges = nullptr; int64_t range_cap = 0;
+  float *img = nullptr, *T = nullptr, *dLdC = nullptr; uint32_t* last = nullptr; int64_t img_cap = 0;
+  float *g2d = nullptr, *raw = nullptr;                  // [G][12] partials, [14][G] raw gradients
+};
+cudaError_t launch_sproject(const float* P, int64_t G, int64_t g0, int64_t g1, const SCam& cam, ScreenBufs& b,
+                            cudaStream_t s);
+cudaError_t launch_skeys_sort(int64_t g0, int64_t g1, const LevelGeom& g, int lev0, int Lr, const SCam& cam,
+                              ScreenBufs& b, int64_t npairs, int64_t Np, cudaStream_t s);
+cudaError_t launch_sraster(const SCam& cam, int Lr, ScreenBufs& b, float* out, float* outT, uint32_t* last,
+                           cudaStream_t s);
+cudaError_t launch_sloss(const float* img, const float* target, const uint8_t* valid, int Lr, int64_t npx, float eps,
+                         int mode, float* dLdC, double* partial, cudaStream_t s);
+cudaError_t launch_sraster_bwd(const SCam& cam, int Lr, ScreenBufs& b, const float* outT, const uint32_t* last,
+                               const float* dLdC, float* g2d, cudaStream_t s);
+cudaError_t launch_sproject_bwd(const float* P, int64_t G, int64_t g0, int64_t g1, const SCam& cam,
+                                const ScreenBufs& b, float* g2d, float* raw, cudaStream_t s);
+
 // create.cu
 void launch_gather_init(int64_t N0, const float* pos, const float* rgb, const float* log_scale,
                         const int64_t* src, int64_t G, float* P, float opacity_logit, cudaStream_t s);
@@ -181,6 +212,9 @@ void launch_pack(const float* P, int64_t G, int64_t base, int64_t n, float* out1
 // src[j] of every Gaussian j: level 0 -> j (caller order), level l >= 1 -> pi[j - goff[l]], with
 // pi = argsort splitmix64(seed + i) computed on the device (C7)
 cudaError_t launch_level_sources(int64_t N0, uint64_t seed, const LevelGeom& g, int64_t* src, cudaStream_t s);
+// ascending sort of (key, idx) pairs, Np = sort_kv_size(n) entries (pad with (~0, INT64_MAX))
+int64_t sort_kv_size(int64_t n);
+void launch_sort_kv(uint64_t* key, int64_t* idx, int64_t Np, cudaStream_t s);
 // per level: lo[3], hi[3] of the means and mean (e^s0 + e^s1 + e^s2)/3 (fp64, fixed order)
 cudaError_t launch_grid_stats(const float* P, int64_t G, const LevelGeom& g, double* out7L, cudaStream_t s);
 void launch_unpack(const float* in14, int64_t G, int64_t base, int64_t n, float* P, cudaStream_t s);
