@@ -474,6 +474,12 @@ def run_ours(args):
     ms_e2e = timer.run(e2e_step, args.steps, stream)
     e2e_val = n_valid / (ms_e2e * 1e-3)
 
+    # ---- screen-space path (next row f1): gc_render of all levels and gc_fit_image on one
+    # 1920 x 1080 frame of per-level radiance images, rank 0 at N = 1, on a separate cache
+    screen = None
+    if rank == 0 and world == 1 and not args.no_screen:
+        screen = screen_bench(gsc, cfg, dev, local, args)
+
     # ---- CPU oracle baseline (rank 0, N = 1 only), bounded sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -507,12 +513,54 @@ def run_ours(args):
         }
         if alt:
             line["alt"] = alt
+        if screen:
+            line["screen"] = screen
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def screen_bench(gsc, cfg, dev, local, args, W=1920, H=1080):
+    """gc_render (all levels, one joint raster) and gc_fit_image (render + Eq. 4 + backward +
+    AdamW + culling rebuild) on the config's cache at 1920 x 1080; CUDA events on the calling
+    stream (each call synchronises the host once to size its sort)."""
+    import torch
+    c = workload.CONFIGS[cfg]
+    pos, alb = workload.init_cloud(cfg)
+    cache = gsc.GSCache(c["counts"], torch.from_numpy(pos).to(dev), torch.from_numpy(alb).to(dev),
+                        seed=cfg, device=local)
+    from scipy.spatial.transform import Rotation
+    view = np.hstack([Rotation.from_rotvec([0.15, -0.2, 0.05]).as_matrix(), [[0.02], [-0.03], [3.0]]])
+    cam = gsc.make_camera(W, H, 1400.0, 1470.0, W / 2, H / 2, view)
+    L = len(c["counts"])
+    r = np.random.default_rng(0)
+    tgt = torch.from_numpy(r.uniform(0, 1, (L, H, W, 3)).astype(np.float32)).to(dev)
+    valid = torch.from_numpy((r.random((L, H, W)) < 0.5).astype(np.uint8)).to(dev)
+    s = torch.cuda.current_stream(dev)
+    for _ in range(2):
+        cache.render(cam)
+        cache.fit_image(cam, tgt, valid)
+    torch.cuda.synchronize(dev)
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    n = max(3, args.steps // 4)
+    e[0].record(s)
+    for _ in range(n):
+        cache.render(cam)
+    e[1].record(s)
+    e[2].record(s)
+    for _ in range(n):
+        cache.fit_image(cam, tgt, valid)
+    e[3].record(s)
+    torch.cuda.synchronize(dev)
+    ms_r, ms_f = e[0].elapsed_time(e[1]) / n, e[2].elapsed_time(e[3]) / n
+    st = cache._stats
+    return {"image": [W, H], "levels": L, "render_ms": ms_r, "fit_image_ms": ms_f,
+            "pixel_samples_fitted_per_s": int(st.n_valid) / (ms_f * 1e-3),
+            "note": "gc_render of all levels in one joint raster; gc_fit_image = render + Eq. 4 + "
+                    "backward + AdamW + culling rebuild; valid pixels 50 % per level"}
 
 
 # CPU oracle baseline, multi-process leg: the oracle as it stands, one process per core over
@@ -634,6 +682,7 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--parallelism", default="dp", choices=["dp", "level"])
     ap.add_argument("--no-alt", action="store_true", help="N > 1: do not also time the other mode")
+    ap.add_argument("--no-screen", action="store_true", help="skip the screen-space (f1) timing")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
