@@ -10,7 +10,12 @@ of the lookups against the synthetic truth over all visible structure, averaged 
 64 frames of each phase, the largest Gaussian extent e^s and the largest |colour|, and
 whether anything became non-finite.
 
-  python tools/ablation.py [--config 1] [--frames 256] [--firefly Q] > profiles/r01_ablation.json
+  python tools/ablation.py [--config 1] [--frames 256] [--firefly Q] [--screen] > profiles/r01_ablation.json
+
+--screen: the paper's own setting -- the cache is fitted in SCREEN space (gc_fit_image, next
+row f1) to noisy per-level radiance images of a camera orbiting the scene once over `frames`
+frames, then still for `frames`; error = rendered cache images vs the noise-free images over
+the pixels whose primary ray hits the scene.
 
 --firefly Q: the paper's "unpredictably high variance ... gradients [that] can take on large
 values, which can occur very sparsely": each sample is additionally multiplied by
@@ -92,11 +97,64 @@ def run(cfg, frames, name, over, dev, firefly):
             "curve": errs}
 
 
+def look_at(theta, dist=3.0, elev=0.35):
+    C = dist * np.array([np.cos(theta), np.sin(theta), elev])
+    z = -C / np.linalg.norm(C)
+    x = np.cross(z, [0.0, 0.0, 1.0])
+    x /= np.linalg.norm(x)
+    y = np.cross(z, x)
+    R = np.stack([x, y, z])
+    return np.hstack([R, (-R @ C)[:, None]])
+
+
+def run_screen(cfg, frames, name, over, dev, W=128, H=96, f=110.0):
+    c = workload.CONFIGS[cfg]
+    hp = {}
+    if "weight_decay" in over:
+        hp["weight_decay"] = over["weight_decay"]
+    if "lr_scale" in over:
+        hp["lr"] = [1.16e-3, 1e-3, 1.25e-2, over["lr_scale"], 1.5e-1]
+    for k in ("init_zcap", "init_scale_factor"):
+        if k in over:
+            hp[k] = over[k]
+    pos, alb = workload.init_cloud(cfg)
+    cache = gsc.GSCache(c["counts"], torch.from_numpy(pos).to(dev), torch.from_numpy(alb).to(dev),
+                        seed=cfg, hparams=gsc.default_hparams(**hp))
+    L = len(c["counts"])
+    r = np.random.Generator(np.random.Philox(key=4242))
+    errs, bad = [], False
+    for fr in range(2 * frames):
+        theta = 2 * np.pi * min(fr, frames) / frames
+        view = look_at(theta)
+        cam = gsc.make_camera(W, H, f, f, W / 2, H / 2, view)
+        x, hit = workload.primary_hits(view, W, H, f, f, W / 2, H / 2)
+        tgt, valid = workload.screen_targets(x, hit, L, r)
+        st = cache.fit_image(cam, torch.from_numpy(tgt.astype(np.float32)).to(dev),
+                             torch.from_numpy(valid.astype(np.uint8)).to(dev))
+        if fr % 8 == 7:
+            img = cache.render(cam).cpu().numpy().astype(np.float64)
+            xs = np.where(hit[..., None], x, 0.0).reshape(-1, 3)
+            truth = np.stack([workload.radiance(xs, np.full(len(xs), l)).reshape(H, W, 3) for l in range(L)])
+            m = np.repeat(hit[None], L, 0)
+            e = np.abs(img[m] - truth[m]).sum() / max(np.abs(truth[m]).sum(), 1e-30)
+            errs.append((fr, float(e)))
+            bad = bad or not np.isfinite(img).all() or st.nonfinite_grads > 0
+    torch.cuda.synchronize()
+    P = np.concatenate([cache.params_rows(l) for l in range(L)])
+    e1 = [e for fr, e in errs if frames - 64 <= fr < frames]
+    e2 = [e for fr, e in errs if fr >= 2 * frames - 64]
+    return {"variant": name, "hparams": over, "path": "screen",
+            "rel_error_moving_last64": float(np.mean(e1)), "rel_error_still_last64": float(np.mean(e2)),
+            "max_extent_es": float(np.exp(P[:, 10:13]).max()), "max_abs_colour": float(np.abs(P[:, 7:10]).max()),
+            "nonfinite": bool(bad or not np.isfinite(P).all()), "curve": errs}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--frames", type=int, default=256)
     ap.add_argument("--firefly", type=float, default=0.0)
+    ap.add_argument("--screen", action="store_true")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     out = {"protocol": "viewport half-space turning once about z over `frames` frames, then still "
@@ -106,7 +164,10 @@ def main():
            "results": []}
     for n, o in VARIANTS.items():
         try:
-            out["results"].append(run(args.config, args.frames, n, o, dev, args.firefly))
+            if args.screen:
+                out["results"].append(run_screen(args.config, args.frames, n, o, dev))
+            else:
+                out["results"].append(run(args.config, args.frames, n, o, dev, args.firefly))
         except Exception as e:           # e.g. exploding Gaussians overflow the culling lists
             out["results"].append({"variant": n, "hparams": o, "failed": str(e)[:300]})
         torch.cuda.synchronize()

@@ -171,3 +171,52 @@ def cfg0_samples(S: int = 4096, seed: int = 1000):
     r = np.random.Generator(np.random.Philox(key=seed + 11))
     pos = r.uniform(-0.9, 0.9, size=(S, 3))
     return pos.astype(np.float32), np.ones(S, np.int32)
+
+
+def primary_hits(view, W, H, fx, fy, cx, cy, seed=1000):
+    """Screen-space samples (next row f1): the first structure each pixel's primary ray meets in
+    the synthetic scene -- the 8 shells as infinitely thin spheres, the slab as the plane
+    z = 0.1 inside |x|, |y| < 0.8 -- for a pinhole camera with world->camera view [R | t]
+    (pixel (px, py) through (px + 0.5, py + 0.5), u = fx x/z + cx).  Returns hit points [H][W][3]
+    (NaN where the ray misses) and a hit mask.  Geometry only (no method arithmetic)."""
+    sc = Scene(seed)
+    V = np.asarray(view, np.float64).reshape(3, 4)
+    R, t = V[:, :3], V[:, 3]
+    o = -R.T @ t                                               # camera centre in the world
+    py, px = np.mgrid[0:H, 0:W]
+    dc = np.stack([(px + 0.5 - cx) / fx, (py + 0.5 - cy) / fy, np.ones_like(px, np.float64)], -1)
+    d = dc @ R                                                 # R^T dc, per pixel
+    d /= np.linalg.norm(d, axis=-1, keepdims=True)
+    best = np.full((H, W), np.inf)
+    for c, r in zip(sc.centres, sc.radii):
+        oc = o - c
+        b = d @ oc
+        disc = b * b - (oc @ oc - r * r)
+        ok = disc >= 0
+        sq = np.sqrt(np.where(ok, disc, 0.0))
+        for tt in (-b - sq, -b + sq):
+            m = ok & (tt > 1e-6) & (tt < best)
+            best = np.where(m, tt, best)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        tz = (0.1 - o[2]) / d[..., 2]
+    hz = o + tz[..., None] * d
+    m = (tz > 1e-6) & (tz < best) & (np.abs(hz[..., 0]) < 0.8) & (np.abs(hz[..., 1]) < 0.8)
+    best = np.where(m, tz, best)
+    hit = np.isfinite(best)
+    x = np.where(hit[..., None], o + best[..., None] * d, np.nan)
+    return x, hit
+
+
+def screen_targets(x, hit, L, r: np.random.Generator, changed: bool = False):
+    """Noisy per-level radiance images of one frame's primary hits: target [L][H][W][3] =
+    L_l(x) B Z / p (the fit samples' noise model) and valid [L][H][W] (hit pixels)."""
+    H, W = hit.shape
+    tgt = np.zeros((L, H, W, 3))
+    xs = np.where(hit[..., None], x, 0.0).reshape(-1, 3)
+    for l in range(L):
+        Lx = radiance(xs, np.full(len(xs), l), changed).reshape(H, W, 3)
+        B = (r.random((H, W)) < 0.25).astype(np.float64)
+        Z = np.exp(0.5 * r.normal(size=(H, W)) - 0.125)
+        tgt[l] = Lx * (B * Z / 0.25)[..., None]
+    valid = np.repeat(hit[None], L, 0)
+    return np.where(valid[..., None], tgt, 0.0), valid
