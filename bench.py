@@ -480,6 +480,11 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_screen:
         screen = screen_bench(gsc, cfg, dev, local, args)
 
+    # ---- row A8: dense all-pairs lookups, tensor cores vs the CUDA-core evaluator (rank 0, N = 1)
+    dense = None
+    if rank == 0 and world == 1 and not args.no_dense:
+        dense = dense_bench(gsc, dev, local, args)
+
     # ---- CPU oracle baseline (rank 0, N = 1 only), bounded sample
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -515,6 +520,8 @@ def run_ours(args):
             line["alt"] = alt
         if screen:
             line["screen"] = screen
+        if dense:
+            line["dense_a8"] = dense
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
@@ -561,6 +568,54 @@ def screen_bench(gsc, cfg, dev, local, args, W=1920, H=1080):
             "pixel_samples_fitted_per_s": int(st.n_valid) / (ms_f * 1e-3),
             "note": "gc_render of all levels in one joint raster; gc_fit_image = render + Eq. 4 + "
                     "backward + AdamW + culling rebuild; valid pixels 50 % per level"}
+
+
+def dense_bench(gsc, dev, local, args, S=262_144):
+    """Row A8 on the dense case it is meant for: configs[1]'s 3 levels (4096/1024/256) with
+    tau = infinity (every Gaussian of a level contributes to every lookup) and a rotated
+    anisotropic level 0; 262,144 lookups per call.  gc_query_dense (tcgen05 3xTF32 Q + CUDA-core
+    exp/colour epilogue) vs gc_query (the packed fp32x2 CUDA-core evaluator over the one-cell
+    culling lists), device time per call with CUDA events; pairs = sum over lookups of the
+    level's Gaussian count; MUFU roofline = one ex2 per pair at 148 x 16 / clk."""
+    import torch
+    counts = workload.CONFIGS[1]["counts"]
+    pos, alb = workload.init_cloud(1)
+    c = gsc.GSCache(counts, torch.from_numpy(pos[:counts[0]]).to(dev), torch.from_numpy(alb[:counts[0]]).to(dev),
+                    seed=7, device=local, hparams=dict(cutoff_sigma=float("inf")))
+    r = np.random.default_rng(11)
+    P0 = c.params_rows(0)
+    P0[:, 3:7] = r.normal(size=(len(P0), 4)).astype(np.float32)
+    P0[:, 10:13] += r.uniform(-0.3, 0.3, (len(P0), 3)).astype(np.float32)
+    c.set_params_rows(0, P0)
+    xq, lq = workload.query_batch(1, S=S, frame=1)
+    xd, ld = torch.from_numpy(xq).to(dev), torch.from_numpy(lq).to(dev)
+    out = torch.empty((S, 3), dtype=torch.float32, device=dev)
+    c.reserve(0, S)
+    lv = np.minimum(lq, len(counts)) - 1
+    pairs = float(sum(np.sum(lv == l) * counts[l] for l in range(len(counts))))
+    s = torch.cuda.current_stream(dev)
+    res = {}
+    for name, fn in (("tensor_core", lambda: c.query_dense(xd, ld, out=out)),
+                     ("cuda_core", lambda: c.query(xd, ld, out=out))):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n = max(5, args.steps // 2)
+        e0.record(s)
+        for _ in range(n):
+            fn()
+        e1.record(s)
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / n
+        res[name] = {"ms": ms, "pairs_per_s": pairs / (ms * 1e-3)}
+    mufu = 148 * 16 * 1.965e9
+    for v in res.values():
+        v["mufu_frac"] = v["pairs_per_s"] / mufu
+    res.update(workload="cfg1 levels, tau = inf, rotated anisotropic level 0", lookups=S, pairs=pairs,
+               speedup=res["cuda_core"]["ms"] / res["tensor_core"]["ms"],
+               mufu_peak="148 SM x 16 ex2/clk x 1.965 GHz (one ex2 per pair)")
+    return res
 
 
 # CPU oracle baseline, multi-process leg: the oracle as it stands, one process per core over
@@ -683,6 +738,7 @@ def main():
     ap.add_argument("--parallelism", default="dp", choices=["dp", "level"])
     ap.add_argument("--no-alt", action="store_true", help="N > 1: do not also time the other mode")
     ap.add_argument("--no-screen", action="store_true", help="skip the screen-space (f1) timing")
+    ap.add_argument("--no-dense", action="store_true", help="skip the dense tensor-core (A8) timing")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -232,6 +232,18 @@ gc_status gc_render(gc_cache c, const gc_camera* cam, int level, float* out_rgb,
 gc_status gc_fit_image(gc_cache c, const gc_camera* cam, const float* target, const uint8_t* valid,
                        gc_stream stream, gc_fit_stats* stats);
 
+/* Dense all-pairs lookups on the tensor cores (row A8, optional in the north star): the same
+ * values as gc_query -- yhat_l(x) = sum over EVERY Gaussian of the level of v e^{-Q/2}
+ * [Q <= tau^2] (C3), no culling lists -- with Q evaluated as a GEMM of 10 monomial features
+ * of the sample against 10 coefficients per Gaussian (tcgen05.mma kind::tf32, 3xTF32 split,
+ * TMEM accumulators), both recentred on the centre of the sample's cell of a tile grid (the
+ * culling grid, or the same rule at tau = 3 when tau is infinite), and the exp / colour
+ * contraction on CUDA cores.  Meant for the dense case (tau = INFINITY) and small levels; cost
+ * grows with S x G.  pos [S][3], path_len [S] or NULL (then `level`), out_rgb [S][3]: DEVICE
+ * buffers, caller order; invalid lookups get 0. */
+gc_status gc_query_dense(gc_cache c, const float* pos, const int32_t* path_len, int level, int64_t S,
+                         float* out_rgb, gc_stream stream);
+
 /* Deferred optimizer step (enable != 0; off by default).  gc_fit / gc_fit_query then leave
  * their optimizer half -- the AdamW step with the next step's evaluation records, and the
  * culling-list rebuild -- pending, and the next call on the handle launches it on an internal

@@ -29,7 +29,7 @@ EXPORTS = ["gc_default_hparams", "gc_create", "gc_destroy", "gc_reserve", "gc_fi
            "gc_nccl_unique_id", "gc_set_comm", "gc_debug_enable_grads", "gc_debug_grads",
            "gc_debug_coef_grads", "gc_list_generation", "gc_set_level_weights", "gc_level_plan",
            "gc_comm_info", "gc_adam_state", "gc_set_adam_state", "gc_alg1_terminate", "gc_reinit",
-           "gc_render", "gc_fit_image",
+           "gc_render", "gc_fit_image", "gc_query_dense",
            "gc_debug_cull", "gc_debug_levels", "gc_profile_enable", "gc_profile_read",
            "gc_last_error", "gc_status_string"]
 
@@ -134,6 +134,7 @@ def lib():
             "gc_adam_state": (i32, [vp, i32, vp, vp, vp, vp]),
             "gc_reinit": (i32, [vp, vp, vp, vp, C.c_uint64]),
             "gc_render": (i32, [vp, vp, i32, vp, vp, vp]),
+            "gc_query_dense": (i32, [vp, vp, vp, i32, i64, vp, vp]),
             "gc_fit_image": (i32, [vp, vp, vp, vp, vp, vp]),
             "gc_alg1_terminate": (i32, [vp, vp, i32, C.c_float, vp, vp, C.c_float, i64, vp, vp, vp, vp]),
             "gc_set_adam_state": (i32, [vp, i32, vp, vp, vp, vp]),
@@ -341,6 +342,16 @@ class GSCache:
         n = _Buf(path_len, np.int32)
         _check(lib().gc_query(self.h, p.ptr, n.ptr, int(level), S, o.ptr, _stream_ptr(stream)))
         self._keep_q = (p, n, o)
+        return out
+
+    def query_dense(self, pos, path_len=None, level=-1, out=None, stream=None):
+        """gc_query_dense (tensor-core dense lookups, row A8) on CUDA tensors."""
+        import torch
+        S = int(pos.shape[0])
+        if out is None:
+            out = torch.empty((S, 3), dtype=torch.float32, device=pos.device)
+        _check(lib().gc_query_dense(self.h, pos.data_ptr(), path_len.data_ptr() if path_len is not None else None,
+                                    int(level), S, out.data_ptr(), _stream_ptr(stream)))
         return out
 
     def query_radiance(self, pos, path_len=None, level=-1, attenuation=None, beta=None,

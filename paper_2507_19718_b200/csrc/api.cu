@@ -138,6 +138,11 @@ struct gc_cache_s {
   int64_t r_in_cap = 0, r_perm_cap = 0, r_send_cap_back = 0;
   std::vector<int64_t> rt_send, rt_recv, rt_soff, rt_roff;   // last routing's per-peer counts/offsets
   ScreenBufs scr;                         // screen-space evaluator buffers (gc_render / gc_fit_image)
+  LevelGeom dgeom{};                      // dense tensor-core evaluator (A8): tile grid, its
+  CellRef dref{};                         // fp32 cell geometry and sample scratch
+  int64_t dNC = 0;
+  Scratch dns;
+  int dense_grid = 0;
   float* pack_tmp = nullptr;
   int64_t pack_cap = 0;
   cudaStream_t side = nullptr;            // gc_fit_query: lookups run beside the fit samples' ingest
@@ -174,14 +179,15 @@ static gc_status check_sticky(gc_cache c) {
   return GC_OK;
 }
 
-static gc_status ensure_scratch(gc_cache c, Scratch& sc, int64_t S, bool fit, cudaStream_t s) {
+static gc_status ensure_scratch(gc_cache c, Scratch& sc, int64_t S, bool fit, cudaStream_t s, int64_t nc = -1) {
   if (sc.cap >= S && sc.cell_count) return GC_OK;
   if (capturing(s)) return fail(GC_ERR_STATE, "scratch too small during graph capture; call gc_reserve first");
   CK(cudaDeviceSynchronize());
   sc.release();
+  if (nc < 0) nc = c->NC;
   int64_t cap = std::max<int64_t>(S, 1024);
-  const int64_t nbins = c->NC * kRep;                 // replicated per-cell counters
-  int64_t work_cap = cap / kCH + std::min<int64_t>(cap, c->NC) + 2;
+  const int64_t nbins = nc * kRep;                    // replicated per-cell counters
+  int64_t work_cap = cap / kCH + std::min<int64_t>(cap, nc) + 2;
   CK(dalloc(&sc.kr, cap));
   CK(dalloc(&sc.bin, 2 * cap));                       // 32-B bins (full sectors) for both
   CK(dalloc(&sc.cell_count, nbins)); CK(dalloc(&sc.cell_start, nbins + 1));
@@ -497,6 +503,52 @@ void gc_default_hparams(gc_hparams* hp) {
 }
 
 
+// The R1 grid rule (host fp64) from the per-level statistics of k_grid_stats (lo[3], hi[3],
+// mean e^s): level AABB + 5 % of its diagonal; cell edge = scale * 2 tau mean(e^s); dims =
+// clamp(ceil(extent / edge), 1, 512), total cells <= 2^22 per level.
+static void build_grid(LevelGeom& g, const std::vector<double>& hstat, int L, double tau, const gc_hparams& hp) {
+  g.coff[0] = 0;
+  for (int l = 0; l < L; ++l) {
+    double lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) { lo[a] = hstat[7 * l + a]; hi[a] = hstat[7 * l + 3 + a]; }
+    const double ms = hstat[7 * l + 6];
+    double diag = std::sqrt((hi[0] - lo[0]) * (hi[0] - lo[0]) + (hi[1] - lo[1]) * (hi[1] - lo[1]) + (hi[2] - lo[2]) * (hi[2] - lo[2]));
+    double ext[3];
+    for (int a = 0; a < 3; ++a) {
+      double pad = 0.05 * diag + 1e-6;
+      lo[a] -= pad; hi[a] += pad;
+      ext[a] = hi[a] - lo[a];
+    }
+    int32_t dims[3];
+    const int fixed = hp.cells_per_axis[l];
+    if (fixed > 0) {
+      for (int a = 0; a < 3; ++a) dims[a] = std::min(fixed, 4096);
+    } else {
+      const double esc = hp.cell_edge_scale > 0.f ? (double)hp.cell_edge_scale : 1.0;
+      double edge = std::isfinite(tau) ? esc * 2.0 * tau * ms : INFINITY;
+      if (!(edge > 0.0)) edge = INFINITY;
+      for (int it = 0; it < 200; ++it) {
+        int64_t prod = 1;
+        for (int a = 0; a < 3; ++a) {
+          double d = std::isfinite(edge) ? std::ceil(ext[a] / edge) : 1.0;
+          dims[a] = (int32_t)std::max(1.0, std::min(512.0, d));
+          prod *= dims[a];
+        }
+        if (prod <= (int64_t)1 << 22) break;
+        edge *= 1.25;
+      }
+    }
+    for (int a = 0; a < 3; ++a) {
+      g.origin[l][a] = lo[a];
+      g.dims[l][a] = dims[a];
+      g.inv_cell[l][a] = (double)dims[a] / ext[a];
+      g.edge[l][a] = 1.0 / g.inv_cell[l][a];
+    }
+    g.coff[l + 1] = g.coff[l] + (int64_t)dims[0] * dims[1] * dims[2];
+  }
+  for (int l = L; l < kMaxL; ++l) g.coff[l + 1] = g.coff[L];
+}
+
 static gc_status create_impl(gc_cache c, const int64_t* counts, const float* init_pos,
                              const float* init_rgb, const float* init_log_scale, uint64_t seed) {
   CK(cudaSetDevice(c->device));
@@ -566,48 +618,15 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
   std::vector<double> hstat(7 * (size_t)L);
   CK(cudaMemcpy(hstat.data(), dstat, sizeof(double) * 7 * L, cudaMemcpyDeviceToHost));
   cudaFree(dstat);
-  c->geom.coff[0] = 0;
   const double tau = (double)c->hp.cutoff_sigma;
-  for (int l = 0; l < L; ++l) {
-    double lo[3], hi[3];
-    for (int a = 0; a < 3; ++a) { lo[a] = hstat[7 * l + a]; hi[a] = hstat[7 * l + 3 + a]; }
-    const double ms = hstat[7 * l + 6];
-    double diag = std::sqrt((hi[0] - lo[0]) * (hi[0] - lo[0]) + (hi[1] - lo[1]) * (hi[1] - lo[1]) + (hi[2] - lo[2]) * (hi[2] - lo[2]));
-    double ext[3];
-    for (int a = 0; a < 3; ++a) {
-      double pad = 0.05 * diag + 1e-6;
-      lo[a] -= pad; hi[a] += pad;
-      ext[a] = hi[a] - lo[a];
-    }
-    int32_t dims[3];
-    const int fixed = c->hp.cells_per_axis[l];
-    if (fixed > 0) {
-      for (int a = 0; a < 3; ++a) dims[a] = std::min(fixed, 4096);
-    } else {
-      const double esc = c->hp.cell_edge_scale > 0.f ? (double)c->hp.cell_edge_scale : 1.0;
-      double edge = std::isfinite(tau) ? esc * 2.0 * tau * ms : INFINITY;
-      if (!(edge > 0.0)) edge = INFINITY;
-      for (int it = 0; it < 200; ++it) {
-        int64_t prod = 1;
-        for (int a = 0; a < 3; ++a) {
-          double d = std::isfinite(edge) ? std::ceil(ext[a] / edge) : 1.0;
-          dims[a] = (int32_t)std::max(1.0, std::min(512.0, d));
-          prod *= dims[a];
-        }
-        if (prod <= (int64_t)1 << 22) break;
-        edge *= 1.25;
-      }
-    }
-    for (int a = 0; a < 3; ++a) {
-      c->geom.origin[l][a] = lo[a];
-      c->geom.dims[l][a] = dims[a];
-      c->geom.inv_cell[l][a] = (double)dims[a] / ext[a];
-      c->geom.edge[l][a] = 1.0 / c->geom.inv_cell[l][a];
-    }
-    c->geom.coff[l + 1] = c->geom.coff[l] + (int64_t)dims[0] * dims[1] * dims[2];
-  }
-  for (int l = L; l < kMaxL; ++l) c->geom.coff[l + 1] = c->geom.coff[L];
+  build_grid(c->geom, hstat, L, tau, c->hp);
   c->NC = c->geom.coff[L];
+  // the dense tensor-core evaluator's tile grid (row A8): the same rule at tau = 3 whatever the
+  // cut-off, so that its tiles stay spatially compact (recentring) even for tau = infinity
+  c->dgeom = c->geom;
+  if (!std::isfinite(tau)) build_grid(c->dgeom, hstat, L, 3.0, c->hp);
+  c->dNC = c->dgeom.coff[L];
+  c->dref = cell_ref(c->dgeom);
   if (c->NC >= (int64_t)1 << 31) return fail(GC_ERR_ARG, "culling grid too large (%lld cells)", (long long)c->NC);
 
   // records + culling lists; exact size of the first CSR sets the list capacity
@@ -684,6 +703,7 @@ static void destroy_impl(gc_cache c) {
   if (c->hcsr) cudaFreeHost(c->hcsr);
   c->fit.release();
   c->qry.release();
+  c->dns.release();
   for (auto* p : c->payloads) {
     if (p->src) cudaFreeHost(p->src);
     if (p->done) cudaEventDestroy(p->done);
@@ -761,6 +781,7 @@ gc_status gc_reinit(gc_cache c, const float* init_pos, const float* init_rgb, co
   if (c->hcsr) cudaFreeHost(c->hcsr);
   c->fit.release();
   c->qry.release();
+  c->dns.release();
   free_screen(c->scr);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->side2) cudaStreamDestroy(c->side2);
@@ -768,7 +789,7 @@ gc_status gc_reinit(gc_cache c, const float* init_pos, const float* init_rgb, co
   for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_fork2, c->ev_tail, c->ev_cpfork}) if (e) cudaEventDestroy(e);
   // take the new one
 #define GSC_TAKE(f) do { c->f = n->f; n->f = decltype(n->f){}; } while (0)
-  GSC_TAKE(geom); GSC_TAKE(G); GSC_TAKE(NC); GSC_TAKE(sms);
+  GSC_TAKE(geom); GSC_TAKE(G); GSC_TAKE(NC); GSC_TAKE(sms); GSC_TAKE(dgeom); GSC_TAKE(dref); GSC_TAKE(dNC);
   GSC_TAKE(P); GSC_TAKE(M); GSC_TAKE(V); GSC_TAKE(grad); GSC_TAKE(rec); GSC_TAKE(range); GSC_TAKE(rad2);
   GSC_TAKE(csr_count); GSC_TAKE(csr_off); GSC_TAKE(csr_totals); GSC_TAKE(csr_rank); GSC_TAKE(csr_ovf);
   GSC_TAKE(csr_rec); GSC_TAKE(csr_tiles); GSC_TAKE(csr_cap); GSC_TAKE(st); GSC_TAKE(lvl); GSC_TAKE(dstats);
@@ -1341,6 +1362,39 @@ gc_status gc_fit_image(gc_cache c, const gc_camera* cam, const float* target, co
                reinterpret_cast<unsigned long long*>(&c->dstats->nonfinite_grads), s, &c->prof, b.raw);
   if (gc_status e = rebuild_csr(c, s, false)) return e;
   if (gc_status e = emit_stats(c, stats, s)) return e;
+  CK(cudaGetLastError());
+  return GC_OK;
+}
+
+// ------------------------------------------------------------ dense tensor-core lookups (A8)
+gc_status gc_query_dense(gc_cache c, const float* pos, const int32_t* path_len, int level, int64_t S, float* out_rgb,
+                         gc_stream stream) {
+  if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  if (S < 0 || S >= ((int64_t)1 << 31)) return fail(GC_ERR_ARG, "S out of range");
+  if (S > 0 && (!pos || !out_rgb)) return fail(GC_ERR_ARG, "NULL pointer");
+  if (!path_len && (level < 0 || level >= c->L)) return fail(GC_ERR_ARG, "level %d not in [0, %d)", level, c->L);
+  if (S == 0) return GC_OK;
+  if (!is_device_ptr(pos) || !is_device_ptr(out_rgb) || (path_len && !is_device_ptr(path_len)))
+    return fail(GC_ERR_ARG, "gc_query_dense takes device buffers");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->device));
+  if (gc_status e = check_sticky(c)) return e;
+  if (gc_status e = ensure_scratch(c, c->dns, S, false, s, c->dNC)) return e;
+  if (gc_status e = csr_guard(c, s)) return e;
+  if (gc_status e = flush_pending(c, s)) return e;
+  if (!c->dense_grid) c->dense_grid = dense_tc_grid();
+  Scratch& D = c->dns;
+  IngestBufs b{D.kr, D.cell_count, D.bin, c->dNC};
+  launch_keys_query(pos, path_len, path_len ? -1 : level, S, c->dgeom, b, out_rgb, s, &c->prof);
+  launch_scan(D.cell_count, c->dNC * kRep, 128, D.tiles, D.totals, D.cell_start, nullptr, D.work, c->dgeom, s, &c->prof);
+  launch_scatter(pos, nullptr, S, D.cell_start, b, s, &c->prof);
+  DenseArgs da;
+  da.work = D.work; da.n_work = D.totals + 1; da.bin = D.bin; da.rec = c->rec;
+  for (int l = 0; l <= kMaxL; ++l) da.goff[l] = c->geom.goff[l];
+  da.ref = c->dref; da.out = out_rgb;
+  const float tau = c->hp.cutoff_sigma;
+  da.tau2 = tau * tau;
+  launch_dense_tc(da, c->dense_grid, s, &c->prof);
   CK(cudaGetLastError());
   return GC_OK;
 }

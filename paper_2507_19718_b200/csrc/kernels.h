@@ -157,6 +157,18 @@ void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, CullBufs
                   DevState* st, const gc_hparams& hp, const LevelGeom& g, unsigned long long* nonfinite,
                   cudaStream_t s, Profiler* prof, const float* raw_grad = nullptr);
 
+// dense_tc.cu -- dense all-pairs evaluator on the tensor cores (row A8)
+struct DenseArgs {
+  const WorkItem* work; const uint32_t* n_work;   // items of <= 128 samples of one tile-grid cell
+  const float4* bin;                               // binned lookups (x, y, z, caller index), stride 2
+  const float4* rec;                               // [G][3] evaluation records
+  int64_t goff[kMaxL + 1];
+  CellRef ref;                                     // the tile grid's cell geometry (recentring)
+  float* out; float tau2;
+};
+int dense_tc_grid();
+void launch_dense_tc(const DenseArgs& a, int grid, cudaStream_t s, Profiler* prof);
+
 // shard.cu -- level-sharded mode (gc_set_comm mode 1)
 struct RoutePlan {
   int world, rank, L;
