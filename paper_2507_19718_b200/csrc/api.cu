@@ -1385,6 +1385,7 @@ gc_status gc_query_dense(gc_cache c, const float* pos, const int32_t* path_len, 
   if (!c->dense_grid) c->dense_grid = dense_tc_grid();
   Scratch& D = c->dns;
   IngestBufs b{D.kr, D.cell_count, D.bin, c->dNC};
+  CK(cudaMemsetAsync(out_rgb, 0, sizeof(float) * 3 * S, s));   // parts of a lookup add up (k_dense_tc)
   launch_keys_query(pos, path_len, path_len ? -1 : level, S, c->dgeom, b, out_rgb, s, &c->prof);
   launch_scan(D.cell_count, c->dNC * kRep, 128, D.tiles, D.totals, D.cell_start, nullptr, D.work, c->dgeom, s, &c->prof);
   launch_scatter(pos, nullptr, S, D.cell_start, b, s, &c->prof);

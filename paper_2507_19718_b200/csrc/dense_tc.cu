@@ -50,7 +50,7 @@ __device__ __forceinline__ void put_split(float* tile_hi, float* tile_lo, int r,
   *(float*)((char*)tile_lo + kmaj(r, k)) = l;
 }
 
-__global__ void __launch_bounds__(kTcThreads, 2) k_dense_tc(DenseArgs a) {
+__global__ void __launch_bounds__(kTcThreads, 4) k_dense_tc(DenseArgs a) {
   extern __shared__ __align__(1024) unsigned char dsm_raw[];
   DenseSmem& sm = *reinterpret_cast<DenseSmem*>(dsm_raw);
   const int t = threadIdx.x, warp = t >> 5;
@@ -69,7 +69,12 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_dense_tc(DenseArgs a) {
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   uint32_t phase = 0;
   const uint32_t n_work = a.n_work[0];
-  for (uint32_t it = blockIdx.x; it < n_work; it += gridDim.x) {
+  // tasks = (item, part of its level's Gaussian chunks): enough tasks for two per CTA even when
+  // the items are few (the dense case puts a level's samples in few cells); the parts' partial
+  // sums meet in red.global.add (output zeroed by the keys pass / the launcher)
+  const uint32_t nsplit = n_work ? max(1u, min(16u, (2u * gridDim.x + n_work - 1) / n_work)) : 1u;
+  for (uint32_t task = blockIdx.x; task < n_work * nsplit; task += gridDim.x) {
+    const uint32_t it = task / nsplit, part = task % nsplit;
     const WorkItem wi = a.work[it];
     const int l = wi.level;
     // cell centre of the item (dense tile grid)
@@ -95,7 +100,9 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_dense_tc(DenseArgs a) {
       }
     }
     float2 Y0 = make_float2(0.f, 0.f), Y1 = Y0, Y2 = Y0;
-    const int64_t g0 = a.goff[l], g1 = a.goff[l + 1];
+    const int64_t nch = (a.goff[l + 1] - a.goff[l] + 127) / 128;
+    const int64_t g0 = a.goff[l] + 128 * ((nch * part) / nsplit);
+    const int64_t g1 = min(a.goff[l + 1], a.goff[l] + 128 * ((nch * (part + 1)) / nsplit));
     for (int64_t cb = g0; cb < g1; cb += 128) {
       const int nj = (int)(g1 - cb < 128 ? g1 - cb : 128);
       {
@@ -156,7 +163,8 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_dense_tc(DenseArgs a) {
                    "@!P1 bra DWAIT;\n\t}\n" ::"r"(smem_addr(&sm.bar)), "r"(phase));
       phase ^= 1u;
       asm volatile("tcgen05.fence::after_thread_sync;");
-      for (int c0 = 0; c0 < nj; c0 += 32) {
+      const int nc_ep = (32 * warp < wi.count) ? nj : 0;     // warps without a valid row skip it
+      for (int c0 = 0; c0 < nc_ep; c0 += 32) {
         uint32_t q[32];
         const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c0;
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -184,10 +192,10 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_dense_tc(DenseArgs a) {
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncthreads();                             // TMEM and B are reused by the next chunk
     }
-    if (valid) {
-      a.out[3 * (size_t)idx] = Y0.x + Y0.y;
-      a.out[3 * (size_t)idx + 1] = Y1.x + Y1.y;
-      a.out[3 * (size_t)idx + 2] = Y2.x + Y2.y;
+    if (valid && g0 < g1) {
+      float* o = a.out + 3 * (size_t)idx;
+      if (nsplit == 1) { o[0] = Y0.x + Y0.y; o[1] = Y1.x + Y1.y; o[2] = Y2.x + Y2.y; }
+      else { atomicAdd(o, Y0.x + Y0.y); atomicAdd(o + 1, Y1.x + Y1.y); atomicAdd(o + 2, Y2.x + Y2.y); }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -195,20 +203,23 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_dense_tc(DenseArgs a) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
 }
 
+// 4 CTAs per SM exactly: each holds 128 TMEM columns (512 per SM), so the dynamic shared
+// memory request is sized to admit no fifth CTA (whose tcgen05.alloc would wait for a whole
+// persistent CTA to finish).
+constexpr size_t kDenseSmem = 52 * 1024;
+static_assert(sizeof(DenseSmem) <= kDenseSmem, "dense tile smem");
+
 int dense_tc_grid() {
-  static_assert(sizeof(DenseSmem) < 48 * 1024 + 16 * 1024, "dense tile smem");
-  const size_t smem = sizeof(DenseSmem) + 1024;
-  cudaFuncSetAttribute(k_dense_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int dev = 0, sms = 148, per = 1;
+  cudaFuncSetAttribute(k_dense_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDenseSmem);
+  int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dense_tc, kTcThreads, smem);
-  return sms * std::max(1, std::min(per, 2));
+  return sms * 4;
 }
 
 void launch_dense_tc(const DenseArgs& a, int grid, cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "dense_tc", s);
-  k_dense_tc<<<grid, kTcThreads, sizeof(DenseSmem) + 1024, s>>>(a);
+  k_dense_tc<<<grid, kTcThreads, kDenseSmem, s>>>(a);
 }
 
 }  // namespace gsc
