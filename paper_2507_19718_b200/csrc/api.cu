@@ -11,11 +11,20 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "stats.cuh"
 
 using namespace gsc;
+
+// NVTX range around every public entry point (header-only NVTX3: visible in Nsight Systems /
+// ncu --nvtx, free when no tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 static thread_local std::string g_err;
 
@@ -729,6 +738,7 @@ static void destroy_impl(gc_cache c) {
 gc_status gc_create(int levels, const int64_t* counts, const float* init_pos, const float* init_rgb,
                     const float* init_log_scale, uint64_t seed, const gc_hparams* hp, int device,
                     gc_cache* out) {
+  NvtxRange nvtx_("gc_create");
   if (!out) return fail(GC_ERR_ARG, "out is NULL");
   *out = nullptr;
   if (levels < 1 || levels > GC_MAX_LEVELS) return fail(GC_ERR_ARG, "levels must be in [1, %d]", GC_MAX_LEVELS);
@@ -763,6 +773,7 @@ gc_status gc_create(int levels, const int64_t* counts, const float* init_pos, co
 // is rebuilt.  Implemented as a fresh internal create whose state replaces the old one.
 gc_status gc_reinit(gc_cache c, const float* init_pos, const float* init_rgb, const float* init_log_scale,
                     uint64_t seed) {
+  NvtxRange nvtx_("gc_reinit");
   if (!c || !init_pos || !init_rgb) return fail(GC_ERR_ARG, "NULL handle or init points");
   CK(cudaSetDevice(c->device));
   if (gc_status e = flush_pending(c, 0)) return e;
@@ -939,6 +950,7 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
 
 gc_status gc_fit(gc_cache c, const float* pos, const int32_t* path_len, const float* rgb, int64_t S,
                  gc_stream stream, gc_fit_stats* stats) {
+  NvtxRange nvtx_("gc_fit");
   return fit_impl(c, pos, path_len, rgb, S, stream, stats);
 }
 
@@ -953,6 +965,7 @@ gc_status gc_fit_query(gc_cache c, const float* pos, const int32_t* path_len, co
                        const float* qpos, const int32_t* qlen, int qlevel, int64_t S_q, const float* attenuation,
                        const float* beta, const float* unbiased_rgb, float* out_rgb, gc_stream stream,
                        gc_fit_stats* stats) {
+  NvtxRange nvtx_("gc_fit_query");
   if (!c) return fail(GC_ERR_ARG, "NULL handle");
   if (S_q < 0 || S_q >= ((int64_t)1 << 31)) return fail(GC_ERR_ARG, "S_q out of range");
   if (S_q > 0 && (!qpos || !out_rgb)) return fail(GC_ERR_ARG, "NULL query pointer");
@@ -983,12 +996,14 @@ gc_status gc_fit_query(gc_cache c, const float* pos, const int32_t* path_len, co
 
 gc_status gc_query(gc_cache c, const float* pos, const int32_t* path_len, int level, int64_t S,
                    float* out_rgb, gc_stream stream) {
+  NvtxRange nvtx_("gc_query");
   return query_impl(c, pos, path_len, level, S, nullptr, nullptr, nullptr, out_rgb, stream);
 }
 
 gc_status gc_query_radiance(gc_cache c, const float* pos, const int32_t* path_len, int level,
                             int64_t S, const float* attenuation, const float* beta,
                             const float* unbiased_rgb, float* out_rgb, gc_stream stream) {
+  NvtxRange nvtx_("gc_query_radiance");
   return query_impl(c, pos, path_len, level, S, attenuation, beta, unbiased_rgb, out_rgb, stream);
 }
 
@@ -1088,6 +1103,7 @@ static gc_status level_io(gc_cache c, int level, gc_level_params* p, bool out, c
 }
 
 gc_status gc_params(gc_cache c, int level, gc_level_params* dst, gc_stream stream) {
+  NvtxRange nvtx_("gc_params");
   if (!c) return fail(GC_ERR_ARG, "NULL handle");
   CK(cudaSetDevice(c->device));
   if (gc_status e = flush_pending(c, (cudaStream_t)stream)) return e;
@@ -1101,12 +1117,14 @@ gc_status gc_set_deferred_step(gc_cache c, int enable) {
 }
 
 gc_status gc_flush(gc_cache c, gc_stream stream) {
+  NvtxRange nvtx_("gc_flush");
   if (!c) return fail(GC_ERR_ARG, "NULL handle");
   CK(cudaSetDevice(c->device));
   return flush_pending(c, (cudaStream_t)stream);
 }
 
 gc_status gc_set_params(gc_cache c, int level, const gc_level_params* src, int reset_adam, gc_stream stream) {
+  NvtxRange nvtx_("gc_set_params");
   if (!c || !src) return fail(GC_ERR_ARG, "NULL handle or src");
   cudaStream_t s = (cudaStream_t)stream;
   CK(cudaSetDevice(c->device));
@@ -1169,6 +1187,7 @@ gc_status gc_set_level_weights(gc_cache c, const double* weights) {
 }
 
 gc_status gc_set_comm(gc_cache c, const void* nccl_uid, int rank, int world, int mode) {
+  NvtxRange nvtx_("gc_set_comm");
   if (!c || world < 1 || rank < 0 || rank >= world) return fail(GC_ERR_ARG, "bad rank/world");
   if (mode != 0 && mode != 1) return fail(GC_ERR_ARG, "mode must be 0 (data parallel) or 1 (level-sharded)");
   if (mode == 1 && world > 1024) return fail(GC_ERR_ARG, "level-sharded mode supports at most 1024 ranks");
@@ -1325,6 +1344,7 @@ static gc_status screen_render(gc_cache c, const gc_camera* cam, int lev0, int l
 }
 
 gc_status gc_render(gc_cache c, const gc_camera* cam, int level, float* out_rgb, float* out_T, gc_stream stream) {
+  NvtxRange nvtx_("gc_render");
   if (!c || !cam || !out_rgb) return fail(GC_ERR_ARG, "NULL handle, camera or output");
   if (level < -1 || level >= c->L) return fail(GC_ERR_ARG, "level %d not in [-1, %d)", level, c->L);
   if (!is_device_ptr(out_rgb) || (out_T && !is_device_ptr(out_T))) return fail(GC_ERR_ARG, "gc_render outputs must be device memory");
@@ -1341,6 +1361,7 @@ gc_status gc_render(gc_cache c, const gc_camera* cam, int level, float* out_rgb,
 
 gc_status gc_fit_image(gc_cache c, const gc_camera* cam, const float* target, const uint8_t* valid, gc_stream stream,
                        gc_fit_stats* stats) {
+  NvtxRange nvtx_("gc_fit_image");
   if (!c || !cam || !target) return fail(GC_ERR_ARG, "NULL handle, camera or target");
   if (!is_device_ptr(target) || (valid && !is_device_ptr(valid))) return fail(GC_ERR_ARG, "gc_fit_image inputs must be device memory");
   if (c->comm) return fail(GC_ERR_UNSUPPORTED, "gc_fit_image is single-GPU");
@@ -1369,6 +1390,7 @@ gc_status gc_fit_image(gc_cache c, const gc_camera* cam, const float* target, co
 // ------------------------------------------------------------ dense tensor-core lookups (A8)
 gc_status gc_query_dense(gc_cache c, const float* pos, const int32_t* path_len, int level, int64_t S, float* out_rgb,
                          gc_stream stream) {
+  NvtxRange nvtx_("gc_query_dense");
   if (!c) return fail(GC_ERR_ARG, "NULL handle");
   if (S < 0 || S >= ((int64_t)1 << 31)) return fail(GC_ERR_ARG, "S out of range");
   if (S > 0 && (!pos || !out_rgb)) return fail(GC_ERR_ARG, "NULL pointer");
@@ -1404,6 +1426,7 @@ gc_status gc_query_dense(gc_cache c, const float* pos, const int32_t* path_len, 
 // layout, plus the schedule counter and the per-level bias-correction state.
 gc_status gc_adam_state(gc_cache c, int level, gc_level_params* m, gc_level_params* v, gc_opt_counters* ctr,
                         gc_stream stream) {
+  NvtxRange nvtx_("gc_adam_state");
   if (!c || !m || !v) return fail(GC_ERR_ARG, "NULL handle or moments");
   cudaStream_t s = (cudaStream_t)stream;
   CK(cudaSetDevice(c->device));
@@ -1424,6 +1447,7 @@ gc_status gc_adam_state(gc_cache c, int level, gc_level_params* m, gc_level_para
 
 gc_status gc_set_adam_state(gc_cache c, int level, const gc_level_params* m, const gc_level_params* v,
                             const gc_opt_counters* ctr, gc_stream stream) {
+  NvtxRange nvtx_("gc_set_adam_state");
   if (!c || !m || !v) return fail(GC_ERR_ARG, "NULL handle or moments");
   cudaStream_t s = (cudaStream_t)stream;
   CK(cudaSetDevice(c->device));

@@ -35,8 +35,12 @@ def main(csv_path, rep_path, tag):
     per = collections.defaultdict(lambda: [0, 0.0, 0.0])
     # everything launched before the first step's k_keys belongs to gc_create; torch fills too
     first = min((i for (i, name) in L if "k_keys" in name), default=0)
+    frame = ("k_keys", "k_scan", "k_scatter", "k_fwdbwd", "k_query", "k_stats", "k_step_scalars", "k_adamw",
+             "k_record_cull", "k_cull_emit")
     for (i, name), m in L.items():
         if i < first or name.startswith("at::") or "at::" in name:
+            continue
+        if not any(name.endswith(f) for f in frame):     # the bench's screen (f1) / dense (A8) legs
             continue
         p = per[name]
         p[0] += 1
@@ -47,7 +51,8 @@ def main(csv_path, rep_path, tag):
              "Cold-cache, serialised per-launch times from `ncu --metrics gpu__time_duration.sum,"
              "dram__bytes_read.sum,dram__bytes_write.sum --clock-control none` over the bench command "
              "(compare SHARES, not absolutes).  Launches before the first step (gc_create: Eq. 2 kNN, first "
-             "culling build) and torch fills are excluded: shares are of the fit+query steps.", "",
+             "culling build), torch fills and the bench's separate screen-space (f1) and dense (A8) legs are "
+             "excluded: shares are of the fit+query frame kernels.", "",
              "| kernel | launches | mean us | share | DRAM MB/launch |", "|---|---|---|---|---|"]
     traffic = {}
     for name, (n, t, b) in sorted(per.items(), key=lambda x: -x[1][1]):
