@@ -310,9 +310,20 @@ gc_status gc_info(gc_cache c, int* levels, int64_t* counts);
  *    level).  Each call synchronises the host once (the routed sizes are NCCL host
  *    arguments), so mode 1 is not graph-capturable (GC_ERR_STATE under capture), and the
  *    gc_query_radiance epilogue is not available (GC_ERR_UNSUPPORTED).
+ *  mode 2 = owner-computes (spatial; next row f4): every level's culling-grid columns (x cell
+ *    index) are cut into `world` contiguous slabs of about equal Gaussian counts
+ *    (gc_slab_plan); a Gaussian is owned by the rank of its mean's column (fixed at
+ *    gc_set_comm); samples and lookups are routed to the owner of their cell's column; a rank
+ *    evaluates against its owned Gaussians plus a HALO: the Gaussians of other ranks whose C8
+ *    cell range reaches its columns.  Instead of a dense all-reduce, only the gradients of the
+ *    boundary set B (Gaussians needed by more than their owner) are summed over ranks; every
+ *    owner steps its own Gaussians; the owners' fresh rows of B are then exchanged and the
+ *    culling lists rebuilt from owned + halo Gaussians.  Collective like mode 1 (one host
+ *    synchronisation per call for the routed sizes and one for |B|; not graph-capturable; no
+ *    deferred step; gc_params collective); world <= 32.
  * nccl_uid == NULL with world == 1 detaches; a uid with world == 1 builds a one-rank
- * communicator (mode 0: the all-reduce runs as an identity; mode 1: every sample is routed to
- * this rank through ncclSend/ncclRecv to itself -- both used to test the paths on one GPU). */
+ * communicator (mode 0: the all-reduce runs as an identity; modes 1 and 2: every sample is
+ * routed to this rank through ncclSend/ncclRecv to itself -- used to test the paths on one GPU). */
 gc_status gc_nccl_unique_id(void* uid128);
 gc_status gc_set_comm(gc_cache c, const void* nccl_uid, int rank, int world, int mode);
 
@@ -333,7 +344,15 @@ gc_status gc_set_level_weights(gc_cache c, const double* weights);
 gc_status gc_level_plan(int levels, const double* weights, int world, int32_t* group_of_level,
                         int32_t* group_first_rank, int32_t* group_size, int* n_groups);
 
-/* Communicator state: mode (-1 none, 0, 1), rank, world, the bit mask of levels this rank
+/* The mode-2 slab plan as a pure host function: for each level l, the grid columns c in
+ * [0, 512) get col_rank[l * 512 + c] in [0, world): the columns of the culling grid (origin,
+ * inv_cell, dims [levels][3], as gc_grid) are cut into `world` contiguous ranges holding about
+ * counts[l] / world of the level's means each (means_x [G]: x coordinates of every Gaussian,
+ * level-major); columns past dims_x map to world - 1.  world <= 32, dims_x <= 512. */
+gc_status gc_slab_plan(int levels, const int64_t* counts, const float* means_x, const double* origin,
+                       const double* inv_cell, const int32_t* dims, int world, int32_t* col_rank);
+
+/* Communicator state: mode (-1 none, 0, 1, 2), rank, world, the bit mask of levels this rank
  * steps, and the size of its level group (mode 0: world).  Each pointer nullable. */
 gc_status gc_comm_info(gc_cache c, int* mode, int* rank, int* world, int* owned_levels_mask,
                        int* group_size);

@@ -29,7 +29,7 @@ EXPORTS = ["gc_default_hparams", "gc_create", "gc_destroy", "gc_reserve", "gc_fi
            "gc_nccl_unique_id", "gc_set_comm", "gc_debug_enable_grads", "gc_debug_grads",
            "gc_debug_coef_grads", "gc_list_generation", "gc_set_level_weights", "gc_level_plan",
            "gc_comm_info", "gc_adam_state", "gc_set_adam_state", "gc_alg1_terminate", "gc_reinit",
-           "gc_render", "gc_fit_image", "gc_query_dense",
+           "gc_render", "gc_fit_image", "gc_query_dense", "gc_slab_plan",
            "gc_debug_cull", "gc_debug_levels", "gc_profile_enable", "gc_profile_read",
            "gc_last_error", "gc_status_string"]
 
@@ -135,6 +135,7 @@ def lib():
             "gc_reinit": (i32, [vp, vp, vp, vp, C.c_uint64]),
             "gc_render": (i32, [vp, vp, i32, vp, vp, vp]),
             "gc_query_dense": (i32, [vp, vp, vp, i32, i64, vp, vp]),
+            "gc_slab_plan": (i32, [i32, vp, vp, vp, vp, vp, i32, vp]),
             "gc_fit_image": (i32, [vp, vp, vp, vp, vp, vp]),
             "gc_alg1_terminate": (i32, [vp, vp, i32, C.c_float, vp, vp, C.c_float, i64, vp, vp, vp, vp]),
             "gc_set_adam_state": (i32, [vp, i32, vp, vp, vp, vp]),
@@ -566,6 +567,22 @@ def alg1_terminate(sigma, n, C_, q, beta=None, eps=1e-6, stream=None):
                                    float(eps), P, term.data_ptr(), tr.data_ptr(), bn.data_ptr(),
                                    _stream_ptr(stream)))
     return term, tr, bn
+
+
+def slab_plan(counts, means_x, grids, world: int):
+    """gc_slab_plan (host): [levels][512] column -> rank table of the owner-computes mode."""
+    counts = np.ascontiguousarray(counts, np.int64)
+    L = len(counts)
+    mx = np.ascontiguousarray(means_x, np.float32)
+    o = np.ascontiguousarray([g[0] for g in grids], np.float64)
+    ic = np.ascontiguousarray([g[1] for g in grids], np.float64)
+    dm = np.ascontiguousarray([g[2] for g in grids], np.int32)
+    out = np.empty((L, 512), np.int32)
+    st = lib().gc_slab_plan(L, counts.ctypes.data, mx.ctypes.data, o.ctypes.data, ic.ctypes.data,
+                            dm.ctypes.data, int(world), out.ctypes.data)
+    if st != 0:
+        raise GCError(st, "gc_slab_plan: bad arguments")
+    return out
 
 
 def level_plan(weights, world: int):

@@ -35,6 +35,8 @@ constexpr int kAdamThreads = 128, kAdamBlocksPerSM = 4;
 struct AdamHP {
   float wd[GC_NGROUPS]; float beta1, beta2, eps; double tau;
   int frozen;               // bit g: reading A16, lr 0 -> group g excluded from the optimizer
+  const uint8_t* owner;     // owner-computes (mode 2): step only Gaussians with owner[j] == me
+  int me;
 };
 
 __device__ __forceinline__ int group_of(int k) { return k < 3 ? 0 : (k < 7 ? 1 : (k < 10 ? 2 : (k < 13 ? 3 : 4))); }
@@ -123,7 +125,7 @@ __global__ void __launch_bounds__(kAdamThreads, kAdamBlocksPerSM) k_adamw(
 #pragma unroll
     for (int k = 0; k < kNP; ++k) { p[k] = P[k * G + j]; m[k] = M[k * G + j]; v[k] = V[k * G + j]; }
     const int l = level_of_gaussian(g, j);
-    const bool act = st->active[l] != 0;
+    const bool act = st->active[l] != 0 && (!hp.owner || hp.owner[j] == hp.me);
     const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
     gp[0] = zero; gp[1] = zero; gp[2] = zero;
     if (!act && !dbg) continue;
@@ -183,11 +185,12 @@ void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp
 void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, CullBufs cb, float* dbg_grad,
                   DevState* st, const gc_hparams& hp,
                   const LevelGeom& g, unsigned long long* nonfinite, cudaStream_t s, Profiler* prof,
-                  const float* raw_grad) {
+                  const float* raw_grad, const uint8_t* owner, int me, bool with_record) {
   AdamHP h;
   for (int k = 0; k < GC_NGROUPS; ++k) h.wd[k] = hp.weight_decay[k];
   h.beta1 = hp.beta1; h.beta2 = hp.beta2; h.eps = hp.adam_eps; h.tau = (double)hp.cutoff_sigma;
   h.frozen = 0;
+  h.owner = owner; h.me = me;
   for (int k = 0; k < GC_NGROUPS; ++k) h.frozen |= (hp.lr[k] == 0.f ? 1 : 0) << k;
   {
     ProfScope ps(prof, "adamw", s);
@@ -195,7 +198,7 @@ void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, CullBufs
     launch_pdl(k_adamw, dim3(blocks), dim3(kAdamThreads), 0, s, G, P, M, V, grad, dbg_grad, st, h, g, nonfinite,
                raw_grad);
   }
-  {
+  if (with_record) {
     ProfScope ps(prof, "record_cull", s);
     launch_record_cull(G, P, h.tau, g, cb, st, s);
   }

@@ -146,6 +146,13 @@ struct gc_cache_s {
   uint32_t* r_perm = nullptr;
   int64_t r_in_cap = 0, r_perm_cap = 0, r_send_cap_back = 0;
   std::vector<int64_t> rt_send, rt_recv, rt_soff, rt_roff;   // last routing's per-peer counts/offsets
+  // owner-computes (gc_set_comm mode 2): column slabs, Gaussian owners, need masks, boundary list B
+  int32_t* d_colrank = nullptr;
+  uint8_t* d_owner = nullptr;
+  uint32_t *d_need = nullptr, *d_flag = nullptr, *d_bsums = nullptr, *d_btotal = nullptr, *h_btotal = nullptr;
+  int32_t* d_idxB = nullptr;
+  float* xbuf = nullptr;
+  int64_t nB = 0;
   ScreenBufs scr;                         // screen-space evaluator buffers (gc_render / gc_fit_image)
   LevelGeom dgeom{};                      // dense tensor-core evaluator (A8): tile grid, its
   CellRef dref{};                         // fp32 cell geometry and sample scratch
@@ -260,7 +267,9 @@ static gc_status mark_staging_free(Scratch& sc, cudaStream_t s, int set) {
 }
 
 static CullBufs cull_bufs(gc_cache c) {
-  return CullBufs{c->rec, c->range, c->rad2, c->csr_count, c->csr_rank, c->csr_ovf, c->csr_cap, c->csr_rec};
+  CullBufs b{c->rec, c->range, c->rad2, c->csr_count, c->csr_rank, c->csr_ovf, c->csr_cap, c->csr_rec};
+  if (c->mode == 2) { b.need = c->d_need; b.me = c->rank; }   // owner-computes: owned + halo only
+  return b;
 }
 
 static gc_status rebuild_csr(gc_cache c, cudaStream_t s, bool recompute_records) {
@@ -338,9 +347,62 @@ static bool is_pinned_host(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
+// Owner-computes (mode 2) halo refresh after the owners' step: every owner marks which ranks
+// need each of its Gaussians (C8 range columns), the masks are summed over ranks (disjoint
+// owners: the sum is each owner's mask), the boundary list B = {needed by more than the owner}
+// is compacted in index order (identical on every rank), the owners' fresh parameter rows of B
+// are summed into every rank (non-owners contribute 0), and the culling lists are rebuilt from
+// the owned + halo Gaussians only.  One host synchronisation (|B| sizes the NCCL calls).
+static gc_status refresh_halo(gc_cache c, cudaStream_t s) {
+  const int64_t G = c->G;
+  launch_need(c->P, G, (double)c->hp.cutoff_sigma, c->geom, c->d_colrank, c->d_owner, c->rank, c->d_need, s);
+  NK(ncclAllReduce(c->d_need, c->d_need, (size_t)G, ncclUint32, ncclSum, c->comm, s));
+  launch_boundary(c->d_need, G, c->d_flag, c->d_bsums, c->d_btotal, c->d_idxB, s);
+  CK(cudaMemcpyAsync(c->h_btotal, c->d_btotal, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  c->nB = *c->h_btotal;
+  if (c->nB > 0) {
+    launch_rows_param(c->P, G, c->xbuf, c->d_idxB, c->nB, c->d_owner, c->rank, 0, s);
+    NK(ncclAllReduce(c->xbuf, c->xbuf, (size_t)kNP * c->nB, ncclFloat32, ncclSum, c->comm, s));
+    launch_rows_param(c->P, G, c->xbuf, c->d_idxB, c->nB, c->d_owner, c->rank, 1, s);
+  }
+  CK(cudaMemsetAsync(c->csr_count, 0, sizeof(uint32_t) * c->NC, s));
+  return rebuild_csr(c, s, true);
+}
+
+// Owner-computes set-up (gc_set_comm mode 2, and gc_reinit under it): column slabs from the
+// current means (identical on every rank: same create arguments), owners, first halo refresh.
+static gc_status setup_owner_computes(gc_cache c) {
+  const int64_t G = c->G;
+  std::vector<float> mx((size_t)G);
+  CK(cudaMemcpy(mx.data(), c->P + (size_t)P_MU * G, sizeof(float) * G, cudaMemcpyDeviceToHost));
+  std::vector<int32_t> cr((size_t)kMaxL * kMaxCols, 0);
+  slab_plan(c->L, c->geom.goff, mx.data(), c->geom, c->world, cr.data());
+  if (!c->d_colrank) {
+    CK(dalloc(&c->d_colrank, (size_t)kMaxL * kMaxCols)); CK(dalloc(&c->d_owner, G)); CK(dalloc(&c->d_need, G));
+    CK(dalloc(&c->d_flag, 2 * G)); CK(dalloc(&c->d_idxB, G)); CK(dalloc(&c->d_bsums, G / 4096 + 2));
+    CK(dalloc(&c->d_btotal, 1)); CK(dalloc(&c->xbuf, (size_t)kNP * G));
+    CK(cudaHostAlloc((void**)&c->h_btotal, sizeof(uint32_t), cudaHostAllocDefault));
+  }
+  CK(cudaMemcpy(c->d_colrank, cr.data(), sizeof(int32_t) * cr.size(), cudaMemcpyHostToDevice));
+  launch_owner(c->P, G, c->geom, c->d_colrank, c->d_owner, 0);
+  c->plan.colrank = c->d_colrank; c->plan.geom = c->geom;
+  c->glo = 0; c->ghi = c->L; c->gsize = c->world;
+  c->mode = 2;
+  if (gc_status e = refresh_halo(c, 0)) return e;
+  CK(cudaDeviceSynchronize());
+  return GC_OK;
+}
+
 // The optimizer half of a fit: AdamW (+ next-step records and culling counts) and the
-// culling-list rebuild.  `nonfinite` receives the skipped-gradient count.
+// culling-list rebuild.  `nonfinite` receives the skipped-gradient count.  Owner-computes: the
+// owners step their Gaussians, then the halo refresh rebuilds the lists.
 static gc_status launch_tail(gc_cache c, cudaStream_t s, unsigned long long* nonfinite) {
+  if (c->mode == 2 && c->comm) {
+    launch_adamw(c->G, c->P, c->M, c->V, c->grad, cull_bufs(c), c->dbg_on ? c->dbg : nullptr, c->st, c->hp, c->geom,
+                 nonfinite, s, &c->prof, nullptr, c->d_owner, c->rank, false);
+    return refresh_halo(c, s);
+  }
   launch_adamw(c->G, c->P, c->M, c->V, c->grad, cull_bufs(c), c->dbg_on ? c->dbg : nullptr, c->st, c->hp, c->geom,
                nonfinite, s, &c->prof);
   return rebuild_csr(c, s, false);
@@ -400,7 +462,7 @@ static gc_status emit_stats(gc_cache c, gc_fit_stats* user, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------ level-sharded routing (mode 1)
-static bool routed(gc_cache c) { return c->mode == 1 && c->comm != nullptr; }
+static bool routed(gc_cache c) { return (c->mode == 1 || c->mode == 2) && c->comm != nullptr; }
 
 template <class T>
 static gc_status grow(T** p, int64_t* cap, int64_t n) {
@@ -728,6 +790,10 @@ static void destroy_impl(gc_cache c) {
     if (p) cudaFree(p);
   if (c->h_all) cudaFreeHost(c->h_all);
   if (c->h_base) cudaFreeHost(c->h_base);
+  for (void* p : {(void*)c->d_colrank, (void*)c->d_owner, (void*)c->d_need, (void*)c->d_flag, (void*)c->d_idxB,
+                  (void*)c->d_bsums, (void*)c->d_btotal, (void*)c->xbuf})
+    if (p) cudaFree(p);
+  if (c->h_btotal) cudaFreeHost(c->h_btotal);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->side2) cudaStreamDestroy(c->side2);
   for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_fork2, c->ev_tail, c->ev_cpfork}) if (e) cudaEventDestroy(e);
@@ -819,6 +885,17 @@ gc_status gc_reinit(gc_cache c, const float* init_pos, const float* init_rgb, co
     CK(cudaMemcpy(&c->st->owned, &owned, sizeof owned, cudaMemcpyHostToDevice));
   }
   if (c->dbg_mode) { const int m = c->dbg_mode; c->dbg_mode = 0; if (gc_status e = gc_debug_enable_grads(c, m)) return e; }
+  if (c->mode == 2) {                 // owner-computes: slabs and owners of the new cloud (collective)
+    if (c->d_colrank) {
+      for (void* p : {(void*)c->d_colrank, (void*)c->d_owner, (void*)c->d_need, (void*)c->d_flag, (void*)c->d_idxB,
+                      (void*)c->d_bsums, (void*)c->d_btotal, (void*)c->xbuf})
+        if (p) cudaFree(p);
+      if (c->h_btotal) cudaFreeHost(c->h_btotal);
+      c->d_colrank = nullptr; c->d_owner = nullptr; c->d_need = nullptr; c->d_flag = nullptr; c->d_idxB = nullptr;
+      c->d_bsums = nullptr; c->d_btotal = nullptr; c->xbuf = nullptr; c->h_btotal = nullptr;
+    }
+    if (gc_status e = setup_owner_computes(c)) return e;
+  }
   return GC_OK;
 }
 
@@ -925,6 +1002,15 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
     NK(ncclAllReduce(c->lvl, c->lvl, sizeof(LvlStats) / sizeof(double), ncclFloat64, ncclSum, c->comm, s));
     NK(ncclGroupEnd());
     launch_step_scalars(c->lvl, c->st, c->hp, c->L, out_stats, s);
+  } else if (dp && c->mode == 2) {  // owner-computes: only the boundary Gaussians' gradients meet
+    // (an interior Gaussian is touched by its owner's samples alone); level statistics over all ranks
+    if (c->nB > 0) {
+      launch_rows_grad(c->grad, c->xbuf, c->d_idxB, c->nB, 0, s);
+      NK(ncclAllReduce(c->xbuf, c->xbuf, (size_t)12 * c->nB, ncclFloat32, ncclSum, c->comm, s));
+      launch_rows_grad(c->grad, c->xbuf, c->d_idxB, c->nB, 1, s);
+    }
+    NK(ncclAllReduce(c->lvl, c->lvl, sizeof(LvlStats) / sizeof(double), ncclFloat64, ncclSum, c->comm, s));
+    launch_step_scalars(c->lvl, c->st, c->hp, c->L, out_stats, s);
   } else if (dp) {                  // level-sharded: gradients of the group's levels summed over
     // the group (its members split those levels' samples); level statistics summed over all
     // ranks, so every rank sees the global k_l and the same schedule step t
@@ -937,7 +1023,7 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
   if (c->dbg_mode & 2)   // debug snapshot of the coefficient gradients the optimizer will read
     CK(cudaMemcpyAsync(c->dbg_coef, c->grad, sizeof(float) * 12 * c->G, cudaMemcpyDeviceToDevice, s));
   if (join) CK(cudaStreamWaitEvent(s, join, 0));
-  if (c->defer) {
+  if (c->defer && c->mode != 2) {     // (owner-computes: the tail holds collectives, never deferred)
     c->pending = true;                // AdamW + culling rebuild run at the start of the next call
   } else {
     if (gc_status e = launch_tail(c, s, reinterpret_cast<unsigned long long*>(&c->dstats->nonfinite_grads))) return e;
@@ -1091,8 +1177,12 @@ static gc_status level_io(gc_cache c, int level, gc_level_params* p, bool out, c
   const int64_t off[5] = {0, 3 * n, 7 * n, 10 * n, 13 * n}, w[5] = {3, 4, 3, 3, 1};
   if (out) {
     launch_pack(planes, c->G, c->geom.goff[level], n, t, s);
-    if (routed(c) && planes == c->P && c->world > 1)   // level-sharded: the owner's copy (collective)
+    if (routed(c) && c->mode == 1 && planes == c->P && c->world > 1)   // level-sharded: the owner's copy (collective)
       NK(ncclBroadcast(t, t, (size_t)kNP * n, ncclFloat32, c->plan.first[level], c->comm, s));
+    if (routed(c) && c->mode == 2 && planes == c->P && c->world > 1) {  // owner-computes: every row from its owner
+      launch_zero_nonowned(t, n, c->geom.goff[level], c->d_owner, c->rank, s);
+      NK(ncclAllReduce(t, t, (size_t)kNP * n, ncclFloat32, ncclSum, c->comm, s));
+    }
     for (int k = 0; k < 5; ++k) CK(cudaMemcpyAsync(f[k], t + off[k], sizeof(float) * w[k] * n, cudaMemcpyDefault, s));
   } else {
     for (int k = 0; k < 5; ++k) CK(cudaMemcpyAsync(t + off[k], f[k], sizeof(float) * w[k] * n, cudaMemcpyDefault, s));
@@ -1189,15 +1279,22 @@ gc_status gc_set_level_weights(gc_cache c, const double* weights) {
 gc_status gc_set_comm(gc_cache c, const void* nccl_uid, int rank, int world, int mode) {
   NvtxRange nvtx_("gc_set_comm");
   if (!c || world < 1 || rank < 0 || rank >= world) return fail(GC_ERR_ARG, "bad rank/world");
-  if (mode != 0 && mode != 1) return fail(GC_ERR_ARG, "mode must be 0 (data parallel) or 1 (level-sharded)");
+  if (mode < 0 || mode > 2) return fail(GC_ERR_ARG, "mode must be 0 (data parallel), 1 (level-sharded) or 2 (owner-computes)");
   if (mode == 1 && world > 1024) return fail(GC_ERR_ARG, "level-sharded mode supports at most 1024 ranks");
+  if (mode == 2 && world > 32) return fail(GC_ERR_ARG, "owner-computes mode supports at most 32 ranks");
   CK(cudaSetDevice(c->device));
   CK(cudaDeviceSynchronize());
   if (gc_status e = flush_pending(c, 0)) return e;
   CK(cudaDeviceSynchronize());
   if (c->gcomm) { ncclCommDestroy(c->gcomm); c->gcomm = nullptr; }
   if (c->comm) { ncclCommDestroy(c->comm); c->comm = nullptr; }
+  const int prev_mode = c->mode;
   c->rank = rank; c->world = world; c->mode = 0;
+  if (prev_mode == 2) {               // the lists were filtered to owned + halo: rebuild them all
+    CK(cudaMemset(c->csr_count, 0, sizeof(uint32_t) * c->NC));
+    if (gc_status e = rebuild_csr(c, 0, true)) return e;
+    CK(cudaDeviceSynchronize());
+  }
   const unsigned int all = 0xFFFFFFFFu;
   CK(cudaMemcpy(&c->st->owned, &all, sizeof all, cudaMemcpyHostToDevice));
   if (!nccl_uid) {
@@ -1208,6 +1305,20 @@ gc_status gc_set_comm(gc_cache c, const void* nccl_uid, int rank, int world, int
   memcpy(&id, nccl_uid, sizeof id);
   NK(ncclCommInitRank(&c->comm, world, id, rank));
   if (mode == 0) return GC_OK;
+  if (!c->r_count) {
+    CK(dalloc(&c->r_count, 1024)); CK(dalloc(&c->r_base, 1024)); CK(dalloc(&c->r_cursor, 1024));
+    CK(cudaHostAlloc((void**)&c->h_base, sizeof(uint32_t) * 1024, cudaHostAllocDefault));
+  }
+  if (c->r_all) cudaFree(c->r_all);
+  if (c->h_all) cudaFreeHost(c->h_all);
+  CK(dalloc(&c->r_all, (size_t)world * world));
+  CK(cudaHostAlloc((void**)&c->h_all, sizeof(uint32_t) * world * world, cudaHostAllocDefault));
+  if (mode == 2) {
+    c->plan = RoutePlan{};
+    c->plan.world = world; c->plan.rank = rank; c->plan.L = c->L;
+    if (gc_status e = setup_owner_computes(c)) { c->mode = 0; return e; }
+    return GC_OK;
+  }
   // level-sharded: the plan (identical on every rank: a function of L, the weights and W)
   double w[kMaxL];
   double G = 0.0;
@@ -1229,14 +1340,6 @@ gc_status gc_set_comm(gc_cache c, const void* nccl_uid, int rank, int world, int
   c->gsize = gs[mine];
   NK(ncclCommSplit(c->comm, mine, rank, &c->gcomm, nullptr));
   CK(cudaMemcpy(&c->st->owned, &owned, sizeof owned, cudaMemcpyHostToDevice));
-  if (!c->r_count) {
-    CK(dalloc(&c->r_count, 1024)); CK(dalloc(&c->r_base, 1024)); CK(dalloc(&c->r_cursor, 1024));
-    CK(cudaHostAlloc((void**)&c->h_base, sizeof(uint32_t) * 1024, cudaHostAllocDefault));
-  }
-  if (c->r_all) cudaFree(c->r_all);
-  if (c->h_all) cudaFreeHost(c->h_all);
-  CK(dalloc(&c->r_all, (size_t)world * world));
-  CK(cudaHostAlloc((void**)&c->h_all, sizeof(uint32_t) * world * world, cudaHostAllocDefault));
   c->mode = 1;
   return GC_OK;
 }
@@ -1244,13 +1347,13 @@ gc_status gc_set_comm(gc_cache c, const void* nccl_uid, int rank, int world, int
 gc_status gc_comm_info(gc_cache c, int* mode, int* rank, int* world, int* owned_levels_mask, int* group_size) {
   if (!c) return fail(GC_ERR_ARG, "NULL handle");
   unsigned int owned = 0u;
-  if (c->mode == 1) { for (int l = c->glo; l < c->ghi; ++l) owned |= 1u << l; }
+  if (c->mode >= 1) { for (int l = c->glo; l < c->ghi; ++l) owned |= 1u << l; }
   else owned = (c->L >= 32) ? 0xFFFFFFFFu : ((1u << c->L) - 1u);
   if (mode) *mode = c->comm ? c->mode : -1;
   if (rank) *rank = c->rank;
   if (world) *world = c->world;
   if (owned_levels_mask) *owned_levels_mask = (int)owned;
-  if (group_size) *group_size = c->mode == 1 ? c->gsize : c->world;
+  if (group_size) *group_size = c->mode >= 1 ? c->gsize : c->world;
   return GC_OK;
 }
 

@@ -85,6 +85,8 @@ void launch_scan(uint32_t* cnt, int64_t n, int ch, uint2* state, uint32_t* total
 struct CullBufs {
   float4* rec; uint4* range; double* rad2; uint32_t* count; uint32_t* rank; uint32_t* ovf; uint32_t ovf_cap;
   float4* lrec;         // [cap][4] the culling lists: per entry the record (3 x float4) + (gid, 0, 0, 0)
+  const uint32_t* need = nullptr;   // owner-computes: list Gaussian j only if bit `me` of need[j] is set
+  int me = 0;
 };
 void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& g, CullBufs cb, DevState* st,
                         cudaStream_t s);
@@ -155,7 +157,8 @@ void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp
 // used instead of the chain rule from the 12 coefficient gradients
 void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, CullBufs cb, float* dbg_grad,
                   DevState* st, const gc_hparams& hp, const LevelGeom& g, unsigned long long* nonfinite,
-                  cudaStream_t s, Profiler* prof, const float* raw_grad = nullptr);
+                  cudaStream_t s, Profiler* prof, const float* raw_grad = nullptr,
+                  const uint8_t* owner = nullptr, int me = 0, bool with_record = true);
 
 // dense_tc.cu -- dense all-pairs evaluator on the tensor cores (row A8)
 struct DenseArgs {
@@ -174,7 +177,10 @@ struct RoutePlan {
   int world, rank, L;
   int first[kMaxL];     // first rank of the group that owns level l
   int size[kMaxL];      // ranks in that group (level l's samples split round-robin over them)
+  const int32_t* colrank;   // owner-computes (mode 2): rank of each grid column [kMaxL][512], else NULL
+  LevelGeom geom;           // mode 2: the culling grids (a sample goes to the owner of its cell's column)
 };
+constexpr int kMaxCols = 512;
 int level_plan(int L, const double* w, int W, int* group_of_level, int* first_rank, int* group_size);
 // pass 0: count[d] += samples routed to rank d; pass 1: pack them into sendbuf at base[d] +
 // (tile range reserved on cursor[d]); fit records 2 x float4 (x y z n | r g b 0) when rgb != NULL,
@@ -185,6 +191,22 @@ void launch_route(const float* pos, const int32_t* len, const float* rgb, int le
 void launch_unpack_routed(const float4* recv, int64_t R, bool fit, float* pos, int32_t* len, float* rgb,
                           cudaStream_t s);
 void launch_unroute(const float* res, const uint32_t* perm, int64_t n, float* out, cudaStream_t s);
+// owner-computes (mode 2): column slabs per level (host), owner of every Gaussian (by the column of
+// its mean), the ranks that need each owned Gaussian (its C8 cell range's columns), the boundary
+// list B = {j : needed by more than its owner} (deterministic scan), and row exchanges over B
+void slab_plan(int L, const int64_t* goff, const float* means, const LevelGeom& g, int W, int32_t* colrank);
+void launch_owner(const float* P, int64_t G, const LevelGeom& g, const int32_t* colrank, uint8_t* owner, cudaStream_t s);
+void launch_need(const float* P, int64_t G, double tau, const LevelGeom& g, const int32_t* colrank,
+                 const uint8_t* owner, int rank, uint32_t* need, cudaStream_t s);
+void launch_boundary(const uint32_t* need, int64_t G, uint32_t* flag, uint32_t* bsums, uint32_t* total,
+                     int32_t* idx, cudaStream_t s);
+// mode 0: gather rows of AoS grads [G][12] into buf[n][12]; mode 1: scatter back.  params: planes
+// [14][G]; gather zeroes rows this rank does not own (the all-reduce then yields the owner's row)
+void launch_rows_grad(float* grad, float* buf, const int32_t* idx, int64_t n, int scatter, cudaStream_t s);
+void launch_rows_param(float* P, int64_t G, float* buf, const int32_t* idx, int64_t n, const uint8_t* owner, int rank,
+                       int scatter, cudaStream_t s);
+void launch_zero_nonowned(float* t, int64_t n, int64_t base, const uint8_t* owner, int me, cudaStream_t s);
+void launch_scan_u32(const uint32_t* in, int64_t n, uint32_t* bsums, uint32_t* total, uint32_t* out, cudaStream_t s);
 
 // screen.cu -- screen-space evaluator (next row f1)
 struct SCam {

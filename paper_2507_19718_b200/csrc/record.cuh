@@ -163,7 +163,9 @@ __device__ __forceinline__ void record_and_count(int64_t j, const float p[kNP], 
   const double m0 = p[P_MU], m1 = p[P_MU + 1], m2 = p[P_MU + 2];
   const int32_t nx = hi[0] - lo[0] + 1, ny = hi[1] - lo[1] + 1, nz = hi[2] - lo[2] + 1;
   uint32_t w;
-  if (nx <= 3 && ny <= 3 && nz <= 3) {
+  if (cb.need && !((cb.need[j] >> cb.me) & 1u)) {
+    w = 0u;                                       // owner-computes: not needed here, not listed
+  } else if (nx <= 3 && ny <= 3 && nz <= 3) {
     // common case: all counting atomics of the Gaussian in flight before any rank is stored
     const int64_t dx = g.dims[l][0], dy = g.dims[l][1];
     double tx[3], ty[3], tz[3];

@@ -163,6 +163,14 @@ __global__ void __launch_bounds__(kScanB) k_sscan_apply(const uint32_t* __restri
   for (int k = 0; k < kScanPer; ++k) if (base + k < n) { out[base + k] = off; off += v[k]; }
 }
 
+// exclusive scan of n u32 (bsums: >= n / 4096 + 2 words, total: 1 word), deterministic
+void launch_scan_u32(const uint32_t* in, int64_t n, uint32_t* bsums, uint32_t* total, uint32_t* out, cudaStream_t s) {
+  const int nb = (int)((n + kScanChunk - 1) / kScanChunk);
+  k_sscan_blocks<<<std::max(nb, 1), kScanB, 0, s>>>(in, n, bsums);
+  k_sscan_top<<<1, kScanB, 0, s>>>(bsums, nb, total);
+  k_sscan_apply<<<std::max(nb, 1), kScanB, 0, s>>>(in, n, bsums, out);
+}
+
 // --------------------------------------------------------------------------- keys / ranges
 __global__ void k_skeys(int64_t g0, int64_t g1, LevelGeom g, int lev0, int ntiles_img, int TX,
                         const float4* __restrict__ pa, const int4* __restrict__ rect,

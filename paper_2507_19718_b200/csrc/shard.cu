@@ -7,10 +7,13 @@
 // so level 0 -- most Gaussians and samples -- can be DP over a sub-group while the small levels
 // share one rank (the "hybrid" of SURVEY 8(e)).  No parameter replication is needed for the
 // math: a rank steps only the levels it owns (DevState::owned).
+#include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
+#include "record.cuh"
 
 namespace gsc {
 
@@ -84,6 +87,11 @@ __device__ __forceinline__ int route_dest(const RoutePlan& p, const float* pos, 
   if (rgb) ok = ok && isfinite(rgb[3 * i]) && isfinite(rgb[3 * i + 1]) && isfinite(rgb[3 * i + 2]);
   *lvl = l;
   if (!ok) return -1;
+  if (p.colrank) {                    // owner-computes: the owner of the sample's cell column (C8 cell)
+    const int32_t cx = clampcell(floor(__dmul_rn(__dsub_rn((double)x, p.geom.origin[l][0]), p.geom.inv_cell[l][0])),
+                                 p.geom.dims[l][0]);
+    return p.colrank[l * kMaxCols + cx];
+  }
   const int n = p.size[l];
   return p.first[l] + (int)((i + p.rank) % n);
 }
@@ -166,6 +174,66 @@ __global__ void k_unroute(const float* __restrict__ res, const uint32_t* __restr
   }
 }
 
+// ------------------------------------------------------------------ owner-computes (mode 2)
+// owner[j] = the rank of the column of the cell holding Gaussian j's mean (fixed at set_comm)
+__global__ void k_owner(const float* __restrict__ P, int64_t G, LevelGeom g, const int32_t* __restrict__ colrank,
+                        uint8_t* owner) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < G; j += (int64_t)gridDim.x * blockDim.x) {
+    const int l = level_of_gaussian(g, j);
+    const int32_t cx = clampcell(floor(__dmul_rn(__dsub_rn((double)P[P_MU * G + j], g.origin[l][0]), g.inv_cell[l][0])),
+                                 g.dims[l][0]);
+    owner[j] = (uint8_t)colrank[l * kMaxCols + cx];
+  }
+}
+
+// need[j] (owned j): bit r for every rank r owning a column of j's C8 cell range (its own bit
+// included); 0 for Gaussians owned elsewhere (the all-reduce then yields every owner's mask)
+__global__ void k_need(const float* __restrict__ P, int64_t G, double tau, LevelGeom g,
+                       const int32_t* __restrict__ colrank, const uint8_t* __restrict__ owner, int me, uint32_t* need) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < G; j += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t m = 0u;
+    if (owner[j] == me) {
+      float p[kNP];
+#pragma unroll
+      for (int k = 0; k < kNP; ++k) p[k] = P[k * G + j];
+      const int l = level_of_gaussian(g, j);
+      int32_t lo[3], hi[3];
+      double r2;
+      cull_range(p, tau, g, l, lo, hi, r2);
+      m = 1u << me;
+      for (int32_t cx = lo[0]; cx <= hi[0]; ++cx) m |= 1u << colrank[l * kMaxCols + cx];
+    }
+    need[j] = m;
+  }
+}
+
+__global__ void k_bflag(const uint32_t* __restrict__ need, int64_t G, uint32_t* flag) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < G; j += (int64_t)gridDim.x * blockDim.x)
+    flag[j] = __popc(need[j]) > 1 ? 1u : 0u;
+}
+
+__global__ void k_bcompact(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos, int64_t G, int32_t* idx) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < G; j += (int64_t)gridDim.x * blockDim.x)
+    if (flag[j]) idx[pos[j]] = (int32_t)j;
+}
+
+__global__ void k_rows_grad(float* grad, float* buf, const int32_t* __restrict__ idx, int64_t n, int scatter) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 12 * n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / 12, k = t % 12;
+    float* g = grad + 12 * (int64_t)idx[r] + k;
+    if (scatter) *g = buf[t]; else buf[t] = *g;
+  }
+}
+
+__global__ void k_rows_param(float* P, int64_t G, float* buf, const int32_t* __restrict__ idx, int64_t n,
+                             const uint8_t* __restrict__ owner, int me, int scatter) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < kNP * n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / kNP, k = t % kNP, j = idx[r];
+    if (scatter) P[k * G + j] = buf[t];
+    else buf[t] = owner[j] == me ? P[k * G + j] : 0.f;
+  }
+}
+
 static int route_grid(int64_t S) {
   const int64_t t = (S + kRouteThreads * kRouteK - 1) / (kRouteThreads * kRouteK);
   return (int)std::max<int64_t>(1, std::min<int64_t>(t, 148 * 8));
@@ -189,6 +257,71 @@ void launch_unroute(const float* res, const uint32_t* perm, int64_t n, float* ou
   if (n > 0) k_unroute<<<route_grid(n), 256, 0, s>>>(res, perm, n, out);
 }
 
+// gc_params under owner-computes: zero the rows of the packed level copy this rank does not own
+__global__ void k_zero_nonowned(float* t, int64_t n, int64_t base, const uint8_t* __restrict__ owner, int me) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (owner[base + i] == me) continue;
+    for (int a = 0; a < 3; ++a) { t[3 * i + a] = 0.f; t[7 * n + 3 * i + a] = 0.f; t[10 * n + 3 * i + a] = 0.f; }
+    for (int a = 0; a < 4; ++a) t[3 * n + 4 * i + a] = 0.f;
+    t[13 * n + i] = 0.f;
+  }
+}
+void launch_zero_nonowned(float* t, int64_t n, int64_t base, const uint8_t* owner, int me, cudaStream_t s) {
+  k_zero_nonowned<<<route_grid(n), 256, 0, s>>>(t, n, base, owner, me);
+}
+
+void launch_owner(const float* P, int64_t G, const LevelGeom& g, const int32_t* colrank, uint8_t* owner, cudaStream_t s) {
+  k_owner<<<route_grid(G), 256, 0, s>>>(P, G, g, colrank, owner);
+}
+void launch_need(const float* P, int64_t G, double tau, const LevelGeom& g, const int32_t* colrank,
+                 const uint8_t* owner, int rank, uint32_t* need, cudaStream_t s) {
+  k_need<<<route_grid(G), 256, 0, s>>>(P, G, tau, g, colrank, owner, rank, need);
+}
+void launch_boundary(const uint32_t* need, int64_t G, uint32_t* flag, uint32_t* bsums, uint32_t* total,
+                     int32_t* idx, cudaStream_t s) {
+  k_bflag<<<route_grid(G), 256, 0, s>>>(need, G, flag);
+  uint32_t* pos = flag + G;                        // flag buffer holds [G] flags + [G] positions
+  launch_scan_u32(flag, G, bsums, total, pos, s);
+  k_bcompact<<<route_grid(G), 256, 0, s>>>(flag, pos, G, idx);
+}
+void launch_rows_grad(float* grad, float* buf, const int32_t* idx, int64_t n, int scatter, cudaStream_t s) {
+  if (n > 0) k_rows_grad<<<route_grid(12 * n), 256, 0, s>>>(grad, buf, idx, n, scatter);
+}
+void launch_rows_param(float* P, int64_t G, float* buf, const int32_t* idx, int64_t n, const uint8_t* owner, int rank,
+                       int scatter, cudaStream_t s) {
+  if (n > 0) k_rows_param<<<route_grid(kNP * n), 256, 0, s>>>(P, G, buf, idx, n, owner, rank, scatter);
+}
+
+// Column slabs (host): per level, the grid columns (x cell index) are cut into W contiguous
+// ranges holding about G_l / W Gaussian means each (greedy on the prefix counts: rank r takes
+// the columns whose cumulative count lies in [r G_l / W, (r + 1) G_l / W)).  Deterministic.
+void slab_plan(int L, const int64_t* goff, const float* means, const LevelGeom& g, int W, int32_t* colrank) {
+  // means: the x coordinates of the Gaussian means [G]
+  const int64_t G = goff[L];
+  for (int l = 0; l < L; ++l) {
+    const int dx = g.dims[l][0];
+    std::vector<int64_t> cnt(dx, 0);
+    for (int64_t j = goff[l]; j < goff[l + 1]; ++j) {
+      const double f = std::floor(((double)means[j] - g.origin[l][0]) * g.inv_cell[l][0]);
+      int32_t cx = !(f >= 0.0) ? 0 : (f > (double)(dx - 1) ? dx - 1 : (int32_t)f);
+      cnt[cx] += 1;
+    }
+    const int64_t n = goff[l + 1] - goff[l];
+    int64_t acc = 0;
+    for (int c = 0; c < kMaxCols; ++c) {
+      int r = 0;
+      if (c < dx) {
+        r = n > 0 ? (int)std::min<int64_t>(W - 1, (acc * W) / n) : 0;   // owner of the column's first mean
+        acc += cnt[c];
+      } else {
+        r = W - 1;
+      }
+      colrank[l * kMaxCols + c] = r;
+    }
+  }
+  (void)G;
+}
+
 }  // namespace gsc
 
 extern "C" gc_status gc_level_plan(int levels, const double* weights, int world, int32_t* group_of_level,
@@ -202,5 +335,27 @@ extern "C" gc_status gc_level_plan(int levels, const double* weights, int world,
   for (int l = 0; l < levels; ++l) group_of_level[l] = gl[l];
   for (int g = 0; g < ng; ++g) { group_first_rank[g] = fr[g]; group_size[g] = gs[g]; }
   *n_groups = ng;
+  return GC_OK;
+}
+
+extern "C" gc_status gc_slab_plan(int levels, const int64_t* counts, const float* means_x, const double* origin,
+                                  const double* inv_cell, const int32_t* dims, int world, int32_t* col_rank) {
+  if (levels < 1 || levels > GC_MAX_LEVELS || world < 1 || world > 32 || !counts || !means_x || !origin ||
+      !inv_cell || !dims || !col_rank)
+    return GC_ERR_ARG;
+  gsc::LevelGeom g{};
+  g.L = levels;
+  g.goff[0] = 0;
+  for (int l = 0; l < levels; ++l) {
+    g.goff[l + 1] = g.goff[l] + counts[l];
+    for (int a = 0; a < 3; ++a) {
+      g.origin[l][a] = origin[3 * l + a]; g.inv_cell[l][a] = inv_cell[3 * l + a]; g.dims[l][a] = dims[3 * l + a];
+    }
+    if (dims[3 * l] < 1 || dims[3 * l] > gsc::kMaxCols) return GC_ERR_ARG;
+  }
+  std::vector<int32_t> cr((size_t)gsc::kMaxL * gsc::kMaxCols);
+  gsc::slab_plan(levels, g.goff, means_x, g, world, cr.data());
+  for (int l = 0; l < levels; ++l)
+    for (int c = 0; c < gsc::kMaxCols; ++c) col_rank[l * gsc::kMaxCols + c] = cr[(size_t)l * gsc::kMaxCols + c];
   return GC_OK;
 }

@@ -41,6 +41,16 @@ def attach_level_sharded(cache, group=None, uid: bytes | None = None, weights=No
     cache.set_comm(uid, rank, world, 1)
 
 
+def attach_owner_computes(cache, group=None, uid: bytes | None = None) -> None:
+    """Make `cache` one rank of a spatial owner-computes cache (mode 2, next row f4): samples and
+    lookups go to the owner of their cell column, only boundary Gaussians' gradients and rows
+    are exchanged.  Collective like mode 1."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if uid is None:
+        uid = exchange_unique_id(group)
+    cache.set_comm(uid, rank, world, 2)
+
+
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     """Contiguous shard [lo, hi) of n samples for `rank` (sizes differ by at most one)."""
     base, extra = divmod(n, world)

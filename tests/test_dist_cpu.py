@@ -204,3 +204,112 @@ def test_level_plan_properties():
             assert groups[0][0] == 0 and sum(s for _, s in groups) == W
             assert all(groups[i][0] + groups[i][1] == groups[i + 1][0] for i in range(len(groups) - 1))
             assert gsc.level_plan(ww, W) == (gl, groups)
+
+
+def _oc_problem():
+    """Two levels of spatially spread Gaussians (so that 3 column slabs have interiors and
+    boundaries), samples over the same box, a grid per level (C8 auto-rule stand-in)."""
+    r = np.random.default_rng(33)
+    G = (90, 30)
+    P = np.zeros((sum(G), 14))
+    P[:, 0:3] = r.uniform(-0.9, 0.9, (sum(G), 3))
+    P[:, 3:7] = r.normal(size=(sum(G), 4))
+    P[:, 7:10] = r.uniform(0.3, 2, (sum(G), 3))
+    P[:, 10:13] = np.log(r.uniform(0.04, 0.12, (sum(G), 3)))
+    P[:, 13] = r.uniform(-1, 1, sum(G))
+    x = r.uniform(-1.0, 1.0, (4001, 3))
+    ln = r.integers(0, 4, 4001).astype(np.int32)
+    rgb = r.uniform(0, 3, (4001, 3))
+    goff = [0, G[0], G[0] + G[1]]
+    grids = []
+    for l in range(2):
+        lo, hi = np.full(3, -1.05), np.full(3, 1.05)
+        dims = np.array([12, 10, 9], np.int32)
+        grids.append((lo, dims / (hi - lo), dims))
+    return goff, P, x, ln, rgb, grids
+
+
+def _oc_worker(rank, world, port, out):
+    """Owner-computes decomposition (gc_set_comm mode 2) on CPU: the library's slab plan
+    (gc_slab_plan), the routing rule (a sample goes to the owner of its cell's column,
+    shard.cu route_dest), need masks from the C8 cell ranges of owned Gaussians (k_need), the
+    boundary set B = needed by more than the owner, the gradient rows of B summed over ranks
+    (gloo here, ncclAllReduce in the library) -- and the owners' rows must equal the
+    single-rank gradients (interior rows are complete on their owner)."""
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2507_19718_b200 as gsc
+    goff, P, x, ln, rgb, grids = _oc_problem()
+    L = 2
+    colrank = gsc.slab_plan([goff[1], goff[2] - goff[1]], P[:, 0], grids, world)
+
+    def col(l, xx):
+        o, ic, dm = grids[l]
+        return np.clip(np.floor((xx - o[0]) * ic[0]), 0, dm[0] - 1).astype(np.int64)
+
+    owner = np.concatenate([colrank[l][col(l, P[goff[l]:goff[l + 1], 0])] for l in range(L)])
+    lo, hi = shard_range(len(x), rank, world)
+    dest = np.full(hi - lo, -1)
+    for i in range(hi - lo):
+        n = ln[lo + i]
+        if n >= 1:
+            l = min(n, L) - 1
+            dest[i] = colrank[l][col(l, x[lo + i:lo + i + 1, 0])[0]]
+    send = [np.nonzero(dest == d)[0] + lo for d in range(world)]
+    everyone = [None] * world
+    dist.all_gather_object(everyone, send)
+    mine = np.concatenate([everyone[s][rank] for s in range(world)]).astype(np.int64)
+    res = oracle.loss_grad(goff, P, x[mine], ln[mine], rgb[mine], mode=1, grids=grids)
+    k = res["count"].astype(np.float64)
+    g = res["grad"].copy()
+    for l in range(L):
+        g[goff[l]:goff[l + 1]] *= 3 * k[l]
+    # need masks of owned Gaussians from their C8 ranges, summed over ranks
+    need = np.zeros(len(P), np.int64)
+    for l in range(L):
+        o, ic, dm = grids[l]
+        rng, _ = oracle.cull_ranges(P[goff[l]:goff[l + 1]], 3.0, o, ic, dm)
+        for jj in range(goff[l + 1] - goff[l]):
+            j = goff[l] + jj
+            if owner[j] != rank:
+                continue
+            m = 1 << rank
+            for cx in range(rng[jj, 0], rng[jj, 3] + 1):
+                m |= 1 << int(colrank[l][cx])
+            need[j] = m
+    nt = torch.from_numpy(need)
+    dist.all_reduce(nt)
+    need = nt.numpy()
+    B = np.nonzero(np.array([bin(int(v)).count("1") for v in need]) > 1)[0]
+    gb = torch.from_numpy(np.ascontiguousarray(g[B]))
+    dist.all_reduce(gb)                                   # only the boundary rows meet
+    g[B] = gb.numpy()
+    st = torch.from_numpy(np.concatenate([res["loss"] * 3 * k, k]))
+    dist.all_reduce(st)
+    s = st.numpy()
+    ksum = s[L:]
+    for l in range(L):
+        g[goff[l]:goff[l + 1]] /= 3 * ksum[l]
+    out[rank] = (owner, g, ksum, len(B))
+    dist.destroy_process_group()
+
+
+def test_owner_computes_decomposition_equals_single_rank_gloo():
+    world = 3
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.start_processes(_oc_worker, args=(world, port, out), nprocs=world, join=True,
+                           start_method="fork")
+        res = dict(out)
+    goff, P, x, ln, rgb, grids = _oc_problem()
+    full = oracle.loss_grad(goff, P, x, ln, rgb, mode=1, grids=grids)
+    owner = res[0][0]
+    assert set(owner.tolist()) == {0, 1, 2}
+    assert 0 < res[0][3] < len(P)                         # a real boundary, not everything
+    for r in range(world):
+        o, g, k, _ = res[r]
+        np.testing.assert_array_equal(k, full["count"])
+        mine = o == r
+        np.testing.assert_allclose(g[mine], full["grad"][mine], rtol=1e-10, atol=1e-14)

@@ -252,16 +252,19 @@ def test_pageable_stats_ring_many_in_flight(gsc):
         assert stk.n_in == n and stk.step == k + 1, (k, stk.n_in, stk.step)
 
 
-def test_level_sharded_one_rank_routes_through_nccl(gsc):
-    """gc_set_comm mode 1 on a one-rank communicator: every sample and lookup goes through the
-    routing kernels (count, all-gather of the count matrix, pack, ncclSend/ncclRecv to itself,
-    unpack; lookups back through the return exchange into caller order).  Lookups (incl.
-    invalid ones, a fixed level, host buffers), fit statistics, gradients and parameters after
-    two steps are checked against the oracle on the caller's batch."""
+@pytest.mark.parametrize("mode", [1, 2])
+def test_routed_modes_one_rank_through_nccl(gsc, mode):
+    """gc_set_comm mode 1 (level-sharded) and mode 2 (owner-computes) on a one-rank
+    communicator: every sample and lookup goes through the routing kernels (count, all-gather
+    of the count matrix, pack, ncclSend/ncclRecv to itself, unpack; lookups back through the
+    return exchange into caller order); mode 2 also through the owner / need-mask / boundary
+    machinery (one slab: every Gaussian owned and interior) and the filtered list rebuild.
+    Lookups (incl. invalid ones, a fixed level, host buffers), fit statistics, gradients and the
+    first AdamW step are checked against the oracle on the caller's batch."""
     c, _, _ = make_cfg1(gsc)
-    c.set_comm(gsc.nccl_unique_id(), 0, 1, mode=1)
+    c.set_comm(gsc.nccl_unique_id(), 0, 1, mode=mode)
     info = c.comm_info()
-    assert info["mode"] == 1 and info["owned_levels"] == [0, 1, 2] and info["group_size"] == 1
+    assert info["mode"] == mode and info["owned_levels"] == [0, 1, 2] and info["group_size"] == 1
     P = rows(c)
     xq, lq = workload.query_batch(1, S=30_001, frame=2)
     lq[::11] = 0
@@ -270,13 +273,13 @@ def test_level_sharded_one_rank_routes_through_nccl(gsc):
     yo, lv, _ = oracle.query(c.goff, P, xq.astype(np.float64), lq, grids=c.grids())
     assert np.all(y[lv < 0] == 0) and (lv < 0).sum() > 0
     ok = lv >= 0
-    check_forward(y[ok], yo[ok], P, c.goff, xq[ok], lv[ok], what="mode-1 lookups")
+    check_forward(y[ok], yo[ok], P, c.goff, xq[ok], lv[ok], what=f"mode-{mode} lookups")
     y1 = c.query(xq[:5000], None, level=1)                          # host buffers, fixed level
     torch.cuda.synchronize()
     yo1, lv1, _ = oracle.query(c.goff, P, xq[:5000].astype(np.float64), np.full(5000, 2, np.int32),
                                grids=c.grids())
     ok1 = lv1 >= 0
-    check_forward(np.asarray(y1)[ok1], yo1[ok1], P, c.goff, xq[:5000][ok1], lv1[ok1], what="mode-1 level 1")
+    check_forward(np.asarray(y1)[ok1], yo1[ok1], P, c.goff, xq[:5000][ok1], lv1[ok1], what=f"mode-{mode} level 1")
     x, ln, rgb = workload.fit_batch(1, S=80_000, frame=3)
     x[::97, 2] = np.inf
     oc = oracle.OracleCache(c.counts, P, grids=c.grids())
@@ -293,7 +296,7 @@ def test_level_sharded_one_rank_routes_through_nccl(gsc):
             assert abs(st.loss[l] - ro["loss"][l]) <= 1e-4 * ro["loss"][l]
         g = np.concatenate([c.debug_grads_rows(l) for l in range(3)]).astype(np.float64)
         al = grad_allow(c, Pb, x, ln, rgb)
-        check_grads(g, ro["grad"], c.goff, f"mode-1 step {step}", iso_levels=(0, 1, 2), allow=al["raw"])
+        check_grads(g, ro["grad"], c.goff, f"mode-{mode} step {step}", iso_levels=(0, 1, 2), allow=al["raw"])
         if step == 0:                  # the first AdamW step vs the oracle's (criterion of
             go = oc.fit(x.astype(np.float64), ln, rgb.astype(np.float64))["grad"]   # test_first_step...)
             P1 = rows(c)
