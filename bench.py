@@ -17,8 +17,8 @@ unset, bench.py re-executes itself under `python -m torch.distributed.run`.  --s
 split over the ranks (S/N samples and lookups each; cfg4's 16.8 M is the north star's case).
 --parallelism dp (default): mode 0, one NCCL all-reduce of the level gradients per step keeps
 the replicas identical; level: mode 1, samples and lookups are routed to the ranks owning
-their level (not graph-capturable: eager calls).  At N > 1 the other mode is timed too and
-reported under "alt".  Rank 0 prints ONE JSON line.
+their level; oc: mode 2, spatial owner-computes with boundary-only exchanges (modes 1 and 2
+are eager calls, not graph-capturable).  At N > 1 the other modes are timed too ("alt").  Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
 
@@ -291,7 +291,9 @@ def run_ours(args):
     c = workload.CONFIGS[cfg]
     counts = c["counts"]
     strong = args.scaling == "strong"
-    mode = 1 if args.parallelism == "level" else 0
+    MODES = {"dp": 0, "level": 1, "oc": 2}
+    NAMES = {v: k for k, v in MODES.items()}
+    mode = MODES[args.parallelism]
     R = 4                                   # rotating frames: inputs of step k last used 4 steps ago
     frames, S = make_frames(cfg, rank, world, R, strong, args.morton, dev)
     in_bytes = sum(t.numel() * t.element_size() for t in frames[0])
@@ -300,7 +302,7 @@ def run_ours(args):
     stream = torch.cuda.Stream(device=dev)
     if not args.no_defer:       # each frame's optimizer step overlaps the next frame's ingest
         cache.set_deferred_step(True)
-    use_graph = not args.no_graph and not (mode == 1 and world > 1)   # mode 1 is not capturable
+    use_graph = not args.no_graph and not (mode >= 1 and world > 1)   # modes 1 and 2 are not capturable
     timer = Timer(dev, world)
 
     def frame_call(cch, x, ln, rgb, xq, lq, out, s_, separate=args.separate):
@@ -355,10 +357,8 @@ def run_ours(args):
     value = n_valid / (ms_step * 1e-3)
     S_q_total = S * world
 
-    # ---- the other multi-GPU mode, same frames (N > 1 only)
-    alt = None
-    if world > 1 and not args.no_alt:
-        alt_mode = 1 - mode
+    # ---- the other multi-GPU modes, same frames (N > 1 only)
+    def time_mode(alt_mode):
         cache_b = build_cache(gsc, cfg, dev, local, args, rank, world, alt_mode, frames, S)
         if not args.no_defer:
             cache_b.set_deferred_step(True)
@@ -373,12 +373,20 @@ def run_ours(args):
         ms_alt = timer.run(alt_step, args.steps, stream)
         nv = int(cache_b._stats.n_valid)
         info = cache_b.comm_info()
-        alt = {"parallelism": ("level" if alt_mode == 1 else "dp") + str(world),
-               "value": nv / (ms_alt * 1e-3), "ms_per_step": ms_alt, "cuda_graph": alt_mode == 0,
-               "owned_levels_rank0": info["owned_levels"] if rank == 0 else None}
+        a_ = {"parallelism": NAMES[alt_mode] + str(world), "value": nv / (ms_alt * 1e-3), "ms_per_step": ms_alt,
+              "cuda_graph": False, "owned_levels_rank0": info["owned_levels"] if rank == 0 else None}
         if alt_mode == 1:
-            alt["plan"] = gsc.level_plan(list(level_weights(cfg, frames)), world)
-        del cache_b
+            a_["plan"] = gsc.level_plan(list(level_weights(cfg, frames)), world)
+        return a_
+
+    alt = None
+    if world > 1 and not args.no_alt:
+        alt = []
+        for alt_mode in (m for m in (0, 1, 2) if m != mode):
+            try:                              # a failing alternative mode is reported, not fatal
+                alt.append(time_mode(alt_mode))
+            except Exception as e:
+                alt.append({"parallelism": NAMES[alt_mode] + str(world), "error": str(e)[:300]})
 
     # ---- per-kernel device time of the same steps, eager with events per kernel, the two
     # halves serialised (gc_query + gc_fit) so that no kernel's time includes an overlap
@@ -499,7 +507,7 @@ def run_ours(args):
             "config": {"workload": c["name"], "levels": len(counts), "counts": counts,
                        "S_fit_per_gpu": S, "S_query_per_gpu": S,
                        "S_fit_global": S * world,
-                       "parallelism": ("level" if mode == 1 else "dp") + str(world),
+                       "parallelism": NAMES[mode] + str(world),
                        "l2": f"{R} rotating device-resident frames ({R * in_bytes / 1e6:.0f} MB) > 126 MB L2",
                        "cuda_graph": bool(graphs),
                        "frame_call": "gc_query + gc_fit" if args.separate else "gc_fit_query",
@@ -735,7 +743,8 @@ def main():
     ap.add_argument("--clock-window", type=float, default=2.0)
     ap.add_argument("--cell-scale", type=float, default=1.0, help="culling-grid cell edge multiplier")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
-    ap.add_argument("--parallelism", default="dp", choices=["dp", "level"])
+    ap.add_argument("--parallelism", default="dp", choices=["dp", "level", "oc"],
+                    help="dp: data parallel (mode 0); level: level-sharded (mode 1); oc: spatial owner-computes (mode 2)")
     ap.add_argument("--no-alt", action="store_true", help="N > 1: do not also time the other mode")
     ap.add_argument("--no-screen", action="store_true", help="skip the screen-space (f1) timing")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense tensor-core (A8) timing")
