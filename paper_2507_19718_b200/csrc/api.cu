@@ -757,9 +757,11 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
 static void free_screen(ScreenBufs& b) {
   for (void* p : {(void*)b.pa, (void*)b.pb, (void*)b.pc, (void*)b.rect, (void*)b.touched, (void*)b.off,
                   (void*)b.bsums, (void*)b.total, (void*)b.key, (void*)b.val, (void*)b.ranges, (void*)b.img,
-                  (void*)b.T, (void*)b.dLdC, (void*)b.last, (void*)b.g2d, (void*)b.raw})
+                  (void*)b.T, (void*)b.dLdC, (void*)b.last, (void*)b.g2d, (void*)b.raw, (void*)b.tcount,
+                  (void*)b.tcursor, (void*)b.tstart, (void*)b.tbsums, (void*)b.ttotal, (void*)b.tbig})
     if (p) cudaFree(p);
   if (b.htotal) cudaFreeHost(b.htotal);
+  if (b.htbig) cudaFreeHost(b.htbig);
   b = ScreenBufs();
 }
 
@@ -1441,7 +1443,21 @@ static gc_status screen_render(gc_cache c, const gc_camera* cam, int lev0, int l
     CK(dalloc(&b.key, Np)); CK(dalloc(&b.val, Np));
     b.kv_cap = Np;
   }
-  CK(launch_skeys_sort(g0, g1, c->geom, lev0, Lr, sc, b, npairs, Np, s));
+  const int64_t nt = (int64_t)Lr * ntiles;
+  if (b.tile_cap < nt + 1) {
+    for (void* p : {(void*)b.tcount, (void*)b.tcursor, (void*)b.tstart, (void*)b.tbsums, (void*)b.ttotal, (void*)b.tbig})
+      if (p) cudaFree(p);
+    CK(dalloc(&b.tcount, nt + 1)); CK(dalloc(&b.tcursor, nt + 1)); CK(dalloc(&b.tstart, nt + 1));
+    CK(dalloc(&b.tbsums, nt / 4096 + 2)); CK(dalloc(&b.ttotal, 1)); CK(dalloc(&b.tbig, 1));
+    if (!b.htbig) CK(cudaHostAlloc((void**)&b.htbig, sizeof(uint32_t), cudaHostAllocDefault));
+    b.tile_cap = nt + 1;
+  }
+  // counting sort by tile + per-tile shared-memory sort; the global bitonic sort only when a
+  // tile holds more than 8192 Gaussians
+  CK(launch_tile_sort(g0, g1, c->geom, lev0, Lr, sc, b, b.tcount, b.tcursor, b.tstart, b.tbsums, b.ttotal, b.tbig, s));
+  CK(cudaMemcpyAsync(b.htbig, b.tbig, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (*b.htbig) CK(launch_skeys_sort(g0, g1, c->geom, lev0, Lr, sc, b, npairs, Np, s));
   CK(launch_sraster(sc, Lr, b, out ? out : b.img, outT ? outT : b.T, b.last, s));
   return GC_OK;
 }

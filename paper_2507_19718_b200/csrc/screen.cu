@@ -532,6 +532,87 @@ cudaError_t launch_skeys_sort(int64_t g0, int64_t g1, const LevelGeom& g, int le
   return cudaGetLastError();
 }
 
+// ---------------------------------------------- two-level sort: counting sort by tile, then
+// a per-tile sort of (depth bits << 32 | index) in shared memory.  The 64-bit key orders a
+// tile's Gaussians by depth with ties by index (the global sort's order, reading A23).
+__global__ void k_tile_count(int64_t g0, int64_t g1, LevelGeom g, int lev0, int ntiles_img, int TX,
+                             const int4* __restrict__ rect, uint32_t* count) {
+  for (int64_t j = g0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < g1; j += (int64_t)gridDim.x * blockDim.x) {
+    const int4 r = rect[j];
+    if (!(r.x < r.y && r.z < r.w)) continue;
+    const int l = level_of_gaussian(g, j) - lev0;
+    for (int ty = r.z; ty < r.w; ++ty)
+      for (int tx = r.x; tx < r.y; ++tx) atomicAdd(count + (size_t)l * ntiles_img + ty * TX + tx, 1u);
+  }
+}
+
+__global__ void k_tile_scatter(int64_t g0, int64_t g1, LevelGeom g, int lev0, int ntiles_img, int TX,
+                               const float4* __restrict__ pa, const int4* __restrict__ rect,
+                               const uint32_t* __restrict__ start, uint32_t* cursor, uint64_t* key) {
+  for (int64_t j = g0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < g1; j += (int64_t)gridDim.x * blockDim.x) {
+    const int4 r = rect[j];
+    if (!(r.x < r.y && r.z < r.w)) continue;
+    const int l = level_of_gaussian(g, j) - lev0;
+    const uint64_t k = ((uint64_t)__float_as_uint(pa[j].z) << 32) | (uint64_t)(uint32_t)j;
+    for (int ty = r.z; ty < r.w; ++ty)
+      for (int tx = r.x; tx < r.y; ++tx) {
+        const size_t t = (size_t)l * ntiles_img + ty * TX + tx;
+        key[start[t] + atomicAdd(cursor + t, 1u)] = k;
+      }
+  }
+}
+
+constexpr int kTileSortMax = 8192;           // items per tile sorted in shared memory (64 KB)
+
+// one CTA per (level, tile): bitonic sort of its segment in shared memory; segments over the
+// capacity flag `big` (the host then falls back to the global sort)
+__global__ void __launch_bounds__(1024) k_tile_sort(const uint32_t* __restrict__ start, const uint32_t* __restrict__ total,
+                                                    int nt, uint64_t* key, int64_t* val, uint2* ranges, uint32_t* big) {
+  extern __shared__ uint64_t sk[];
+  const int t = blockIdx.x;
+  const uint32_t b0 = start[t], b1 = t + 1 < nt ? start[t + 1] : *total;
+  const int n = (int)(b1 - b0);
+  if (threadIdx.x == 0) ranges[t] = make_uint2(b0, b1);
+  if (n <= 0) return;
+  if (n > kTileSortMax) { if (threadIdx.x == 0) atomicExch(big, 1u); return; }
+  int np = 1;
+  while (np < n) np <<= 1;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) sk[i] = i < n ? key[b0 + i] : ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= np; k <<= 1)
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      for (int i = threadIdx.x; i < np; i += blockDim.x) {
+        const int p = i ^ jj;
+        if (p > i) {
+          const bool up = (i & k) == 0;
+          const uint64_t a = sk[i], c = sk[p];
+          if ((c < a) == up) { sk[i] = c; sk[p] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) val[b0 + i] = (int64_t)(uint32_t)(sk[i] & 0xFFFFFFFFull);
+}
+
+// Returns in *big_host whether some tile exceeded kTileSortMax (then the caller uses the
+// global sort, launch_skeys_sort).  tile buffers: count/cursor/start [Lr * ntiles + 1].
+cudaError_t launch_tile_sort(int64_t g0, int64_t g1, const LevelGeom& g, int lev0, int Lr, const SCam& cam,
+                             ScreenBufs& b, uint32_t* tcount, uint32_t* tcursor, uint32_t* tstart, uint32_t* tbsums,
+                             uint32_t* ttotal, uint32_t* big, cudaStream_t s) {
+  const int ntiles = cam.TX * cam.TY;
+  const int nt = Lr * ntiles;
+  // (per call: the attribute belongs to the current device)
+  cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kTileSortMax * sizeof(uint64_t)));
+  cudaMemsetAsync(tcount, 0, sizeof(uint32_t) * nt, s);
+  cudaMemsetAsync(tcursor, 0, sizeof(uint32_t) * nt, s);
+  cudaMemsetAsync(big, 0, sizeof(uint32_t), s);
+  k_tile_count<<<sblocks(g1 - g0), 256, 0, s>>>(g0, g1, g, lev0, ntiles, cam.TX, b.rect, tcount);
+  launch_scan_u32(tcount, nt, tbsums, ttotal, tstart, s);
+  k_tile_scatter<<<sblocks(g1 - g0), 256, 0, s>>>(g0, g1, g, lev0, ntiles, cam.TX, b.pa, b.rect, tstart, tcursor, b.key);
+  k_tile_sort<<<nt, 1024, kTileSortMax * sizeof(uint64_t), s>>>(tstart, ttotal, nt, b.key, b.val, b.ranges, big);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sraster(const SCam& cam, int Lr, ScreenBufs& b, float* out, float* outT, uint32_t* last,
                            cudaStream_t s) {
   SRasterArgs a{b.ranges, b.val, b.pa, b.pb, b.pc, out, outT, last, cam};
