@@ -291,7 +291,7 @@ def run_ours(args):
     c = workload.CONFIGS[cfg]
     counts = c["counts"]
     strong = args.scaling == "strong"
-    MODES = {"dp": 0, "level": 1, "oc": 2}
+    MODES = {"dp": 0, "level": 1, "oc": 2, "zero": 3}
     NAMES = {v: k for k, v in MODES.items()}
     mode = MODES[args.parallelism]
     R = 4                                   # rotating frames: inputs of step k last used 4 steps ago
@@ -302,7 +302,7 @@ def run_ours(args):
     stream = torch.cuda.Stream(device=dev)
     if not args.no_defer:       # each frame's optimizer step overlaps the next frame's ingest
         cache.set_deferred_step(True)
-    use_graph = not args.no_graph and not (mode >= 1 and world > 1)   # modes 1 and 2 are not capturable
+    use_graph = not args.no_graph and not (mode in (1, 2) and world > 1)   # modes 1 and 2 are not capturable
     timer = Timer(dev, world)
 
     def frame_call(cch, x, ln, rgb, xq, lq, out, s_, separate=args.separate):
@@ -382,7 +382,7 @@ def run_ours(args):
     alt = None
     if world > 1 and not args.no_alt:
         alt = []
-        for alt_mode in (m for m in (0, 1, 2) if m != mode):
+        for alt_mode in (m for m in (0, 1, 2, 3) if m != mode):
             try:                              # a failing alternative mode is reported, not fatal
                 alt.append(time_mode(alt_mode))
             except Exception as e:
@@ -743,8 +743,9 @@ def main():
     ap.add_argument("--clock-window", type=float, default=2.0)
     ap.add_argument("--cell-scale", type=float, default=1.0, help="culling-grid cell edge multiplier")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
-    ap.add_argument("--parallelism", default="dp", choices=["dp", "level", "oc"],
-                    help="dp: data parallel (mode 0); level: level-sharded (mode 1); oc: spatial owner-computes (mode 2)")
+    ap.add_argument("--parallelism", default="dp", choices=["dp", "level", "oc", "zero"],
+                    help="dp: data parallel (mode 0); level: level-sharded (mode 1); oc: spatial owner-computes "
+                         "(mode 2); zero: data parallel with a reduce-scattered, sharded optimizer (mode 3)")
     ap.add_argument("--no-alt", action="store_true", help="N > 1: do not also time the other mode")
     ap.add_argument("--no-screen", action="store_true", help="skip the screen-space (f1) timing")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense tensor-core (A8) timing")

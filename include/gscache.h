@@ -321,8 +321,15 @@ gc_status gc_info(gc_cache c, int* levels, int64_t* counts);
  *    culling lists rebuilt from owned + halo Gaussians.  Collective like mode 1 (one host
  *    synchronisation per call for the routed sizes and one for |B|; not graph-capturable; no
  *    deferred step; gc_params collective); world <= 32.
+ *  mode 3 = ZeRO data parallel (SURVEY 8(e) "required upgrade" 1): as mode 0, but the per-level
+ *    gradients are REDUCE-SCATTERED (rank r sums Gaussians [r n, (r+1) n), n = ceil(G / world)),
+ *    every rank takes the AdamW step of its slice only (optimizer work and moment traffic / world),
+ *    and the updated parameter rows are ALL-GATHERED so every replica holds the full cache
+ *    before the (replicated) record / culling rebuild.  Same results as mode 0 up to summation
+ *    order; no deferred step (the tail holds a collective); gc_adam_state returns this rank's
+ *    slice of the moments (the other rows are not maintained here).  Graph-capturable.
  * nccl_uid == NULL with world == 1 detaches; a uid with world == 1 builds a one-rank
- * communicator (mode 0: the all-reduce runs as an identity; modes 1 and 2: every sample is
+ * communicator (modes 0 and 3: the collectives run as identities; modes 1 and 2: every sample is
  * routed to this rank through ncclSend/ncclRecv to itself -- used to test the paths on one GPU). */
 gc_status gc_nccl_unique_id(void* uid128);
 gc_status gc_set_comm(gc_cache c, const void* nccl_uid, int rank, int world, int mode);

@@ -37,6 +37,7 @@ struct AdamHP {
   int frozen;               // bit g: reading A16, lr 0 -> group g excluded from the optimizer
   const uint8_t* owner;     // owner-computes (mode 2): step only Gaussians with owner[j] == me
   int me;
+  int64_t gb, ge;           // ZeRO data parallel (mode 3): step only Gaussians in [gb, ge)
 };
 
 __device__ __forceinline__ int group_of(int k) { return k < 3 ? 0 : (k < 7 ? 1 : (k < 10 ? 2 : (k < 13 ? 3 : 4))); }
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(kAdamThreads, kAdamBlocksPerSM) k_adamw(
 #pragma unroll
     for (int k = 0; k < kNP; ++k) { p[k] = P[k * G + j]; m[k] = M[k * G + j]; v[k] = V[k * G + j]; }
     const int l = level_of_gaussian(g, j);
-    const bool act = st->active[l] != 0 && (!hp.owner || hp.owner[j] == hp.me);
+    const bool act = st->active[l] != 0 && (!hp.owner || hp.owner[j] == hp.me) && j >= hp.gb && j < hp.ge;
     const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
     gp[0] = zero; gp[1] = zero; gp[2] = zero;
     if (!act && !dbg) continue;
@@ -185,12 +186,14 @@ void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp
 void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, CullBufs cb, float* dbg_grad,
                   DevState* st, const gc_hparams& hp,
                   const LevelGeom& g, unsigned long long* nonfinite, cudaStream_t s, Profiler* prof,
-                  const float* raw_grad, const uint8_t* owner, int me, bool with_record) {
+                  const float* raw_grad, const uint8_t* owner, int me, bool with_record, int64_t g_begin,
+                  int64_t g_end) {
   AdamHP h;
   for (int k = 0; k < GC_NGROUPS; ++k) h.wd[k] = hp.weight_decay[k];
   h.beta1 = hp.beta1; h.beta2 = hp.beta2; h.eps = hp.adam_eps; h.tau = (double)hp.cutoff_sigma;
   h.frozen = 0;
   h.owner = owner; h.me = me;
+  h.gb = g_begin; h.ge = g_end < 0 ? G : g_end;
   for (int k = 0; k < GC_NGROUPS; ++k) h.frozen |= (hp.lr[k] == 0.f ? 1 : 0) << k;
   {
     ProfScope ps(prof, "adamw", s);

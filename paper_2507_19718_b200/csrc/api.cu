@@ -153,6 +153,9 @@ struct gc_cache_s {
   int32_t* d_idxB = nullptr;
   float* xbuf = nullptr;
   int64_t nB = 0;
+  // ZeRO data parallel (mode 3): slice of np Gaussians per rank, gather buffers
+  int64_t zp = 0;
+  float *zsend = nullptr, *zrecv = nullptr;
   ScreenBufs scr;                         // screen-space evaluator buffers (gc_render / gc_fit_image)
   LevelGeom dgeom{};                      // dense tensor-core evaluator (A8): tile grid, its
   CellRef dref{};                         // fp32 cell geometry and sample scratch
@@ -370,6 +373,25 @@ static gc_status refresh_halo(gc_cache c, cudaStream_t s) {
   return rebuild_csr(c, s, true);
 }
 
+// ZeRO data-parallel set-up (gc_set_comm mode 3, and gc_reinit under it): the gradient buffer
+// padded to `world` equal slices (ncclReduceScatter counts), the all-gather buffers.
+static gc_status setup_zero(gc_cache c) {
+  const int world = c->world;
+  const int64_t zp = (c->G + world - 1) / world;
+  float* g = nullptr;
+  CK(cudaDeviceSynchronize());
+  CK(dalloc(&g, (size_t)12 * zp * world));
+  CK(cudaMemset(g, 0, sizeof(float) * 12 * zp * world));
+  if (c->grad) cudaFree(c->grad);
+  c->grad = g;
+  if (c->zsend) cudaFree(c->zsend);
+  if (c->zrecv) cudaFree(c->zrecv);
+  CK(dalloc(&c->zsend, (size_t)kNP * zp)); CK(dalloc(&c->zrecv, (size_t)kNP * zp * world));
+  c->zp = zp;
+  c->mode = 3;
+  return GC_OK;
+}
+
 // Owner-computes set-up (gc_set_comm mode 2, and gc_reinit under it): column slabs from the
 // current means (identical on every rank: same create arguments), owners, first halo refresh.
 static gc_status setup_owner_computes(gc_cache c) {
@@ -398,6 +420,17 @@ static gc_status setup_owner_computes(gc_cache c) {
 // culling-list rebuild.  `nonfinite` receives the skipped-gradient count.  Owner-computes: the
 // owners step their Gaussians, then the halo refresh rebuilds the lists.
 static gc_status launch_tail(gc_cache c, cudaStream_t s, unsigned long long* nonfinite) {
+  if (c->mode == 3 && c->comm) {     // ZeRO: step this rank's slice, all-gather every slice's rows
+    const int64_t g0 = std::min<int64_t>(c->G, (int64_t)c->rank * c->zp);
+    const int64_t g1 = std::min<int64_t>(c->G, g0 + c->zp);
+    launch_adamw(c->G, c->P, c->M, c->V, c->grad, cull_bufs(c), c->dbg_on ? c->dbg : nullptr, c->st, c->hp, c->geom,
+                 nonfinite, s, &c->prof, nullptr, nullptr, 0, false, g0, g1);
+    launch_pack_slice(c->P, c->G, g0, g1 - g0, c->zp, c->zsend, s);
+    NK(ncclAllGather(c->zsend, c->zrecv, (size_t)kNP * c->zp, ncclFloat32, c->comm, s));
+    launch_unpack_slices(c->zrecv, c->world, c->zp, c->P, c->G, s);
+    launch_record_cull(c->G, c->P, (double)c->hp.cutoff_sigma, c->geom, cull_bufs(c), c->st, s);
+    return rebuild_csr(c, s, false);
+  }
   if (c->mode == 2 && c->comm) {
     launch_adamw(c->G, c->P, c->M, c->V, c->grad, cull_bufs(c), c->dbg_on ? c->dbg : nullptr, c->st, c->hp, c->geom,
                  nonfinite, s, &c->prof, nullptr, c->d_owner, c->rank, false);
@@ -796,6 +829,8 @@ static void destroy_impl(gc_cache c) {
                   (void*)c->d_bsums, (void*)c->d_btotal, (void*)c->xbuf})
     if (p) cudaFree(p);
   if (c->h_btotal) cudaFreeHost(c->h_btotal);
+  if (c->zsend) cudaFree(c->zsend);
+  if (c->zrecv) cudaFree(c->zrecv);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->side2) cudaStreamDestroy(c->side2);
   for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_fork2, c->ev_tail, c->ev_cpfork}) if (e) cudaEventDestroy(e);
@@ -887,6 +922,7 @@ gc_status gc_reinit(gc_cache c, const float* init_pos, const float* init_rgb, co
     CK(cudaMemcpy(&c->st->owned, &owned, sizeof owned, cudaMemcpyHostToDevice));
   }
   if (c->dbg_mode) { const int m = c->dbg_mode; c->dbg_mode = 0; if (gc_status e = gc_debug_enable_grads(c, m)) return e; }
+  if (c->mode == 3) { if (gc_status e = setup_zero(c)) return e; }   // the new gradient buffer, padded
   if (c->mode == 2) {                 // owner-computes: slabs and owners of the new cloud (collective)
     if (c->d_colrank) {
       for (void* p : {(void*)c->d_colrank, (void*)c->d_owner, (void*)c->d_need, (void*)c->d_flag, (void*)c->d_idxB,
@@ -1004,6 +1040,13 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
     NK(ncclAllReduce(c->lvl, c->lvl, sizeof(LvlStats) / sizeof(double), ncclFloat64, ncclSum, c->comm, s));
     NK(ncclGroupEnd());
     launch_step_scalars(c->lvl, c->st, c->hp, c->L, out_stats, s);
+  } else if (dp && c->mode == 3) {  // ZeRO data parallel: reduce-scatter, each rank sums its slice
+    NK(ncclGroupStart());
+    NK(ncclReduceScatter(c->grad, c->grad + (size_t)12 * c->rank * c->zp, (size_t)12 * c->zp, ncclFloat32, ncclSum,
+                         c->comm, s));
+    NK(ncclAllReduce(c->lvl, c->lvl, sizeof(LvlStats) / sizeof(double), ncclFloat64, ncclSum, c->comm, s));
+    NK(ncclGroupEnd());
+    launch_step_scalars(c->lvl, c->st, c->hp, c->L, out_stats, s);
   } else if (dp && c->mode == 2) {  // owner-computes: only the boundary Gaussians' gradients meet
     // (an interior Gaussian is touched by its owner's samples alone); level statistics over all ranks
     if (c->nB > 0) {
@@ -1025,7 +1068,7 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
   if (c->dbg_mode & 2)   // debug snapshot of the coefficient gradients the optimizer will read
     CK(cudaMemcpyAsync(c->dbg_coef, c->grad, sizeof(float) * 12 * c->G, cudaMemcpyDeviceToDevice, s));
   if (join) CK(cudaStreamWaitEvent(s, join, 0));
-  if (c->defer && c->mode != 2) {     // (owner-computes: the tail holds collectives, never deferred)
+  if (c->defer && c->mode != 2 && c->mode != 3) {   // (modes 2, 3: the tail holds collectives, never deferred)
     c->pending = true;                // AdamW + culling rebuild run at the start of the next call
   } else {
     if (gc_status e = launch_tail(c, s, reinterpret_cast<unsigned long long*>(&c->dstats->nonfinite_grads))) return e;
@@ -1281,7 +1324,8 @@ gc_status gc_set_level_weights(gc_cache c, const double* weights) {
 gc_status gc_set_comm(gc_cache c, const void* nccl_uid, int rank, int world, int mode) {
   NvtxRange nvtx_("gc_set_comm");
   if (!c || world < 1 || rank < 0 || rank >= world) return fail(GC_ERR_ARG, "bad rank/world");
-  if (mode < 0 || mode > 2) return fail(GC_ERR_ARG, "mode must be 0 (data parallel), 1 (level-sharded) or 2 (owner-computes)");
+  if (mode < 0 || mode > 3)
+    return fail(GC_ERR_ARG, "mode must be 0 (data parallel), 1 (level-sharded), 2 (owner-computes) or 3 (ZeRO data parallel)");
   if (mode == 1 && world > 1024) return fail(GC_ERR_ARG, "level-sharded mode supports at most 1024 ranks");
   if (mode == 2 && world > 32) return fail(GC_ERR_ARG, "owner-computes mode supports at most 32 ranks");
   CK(cudaSetDevice(c->device));
@@ -1307,6 +1351,7 @@ gc_status gc_set_comm(gc_cache c, const void* nccl_uid, int rank, int world, int
   memcpy(&id, nccl_uid, sizeof id);
   NK(ncclCommInitRank(&c->comm, world, id, rank));
   if (mode == 0) return GC_OK;
+  if (mode == 3) return setup_zero(c);
   if (!c->r_count) {
     CK(dalloc(&c->r_count, 1024)); CK(dalloc(&c->r_base, 1024)); CK(dalloc(&c->r_cursor, 1024));
     CK(cudaHostAlloc((void**)&c->h_base, sizeof(uint32_t) * 1024, cudaHostAllocDefault));

@@ -158,7 +158,8 @@ void launch_step_scalars(const LvlStats* lvl, DevState* st, const gc_hparams& hp
 void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, CullBufs cb, float* dbg_grad,
                   DevState* st, const gc_hparams& hp, const LevelGeom& g, unsigned long long* nonfinite,
                   cudaStream_t s, Profiler* prof, const float* raw_grad = nullptr,
-                  const uint8_t* owner = nullptr, int me = 0, bool with_record = true);
+                  const uint8_t* owner = nullptr, int me = 0, bool with_record = true, int64_t g_begin = 0,
+                  int64_t g_end = -1);
 
 // dense_tc.cu -- dense all-pairs evaluator on the tensor cores (row A8)
 struct DenseArgs {
@@ -205,6 +206,10 @@ void launch_boundary(const uint32_t* need, int64_t G, uint32_t* flag, uint32_t* 
 void launch_rows_grad(float* grad, float* buf, const int32_t* idx, int64_t n, int scatter, cudaStream_t s);
 void launch_rows_param(float* P, int64_t G, float* buf, const int32_t* idx, int64_t n, const uint8_t* owner, int rank,
                        int scatter, cudaStream_t s);
+// ZeRO data parallel (mode 3): this rank's slice [g0, g0 + n) of the 14 parameter planes into
+// buf [14][np] (np >= n, zero padded), and all ranks' gathered slices [W][14][np] back into P
+void launch_pack_slice(const float* P, int64_t G, int64_t g0, int64_t n, int64_t np, float* buf, cudaStream_t s);
+void launch_unpack_slices(const float* buf, int W, int64_t np, float* P, int64_t G, cudaStream_t s);
 void launch_zero_nonowned(float* t, int64_t n, int64_t base, const uint8_t* owner, int me, cudaStream_t s);
 void launch_scan_u32(const uint32_t* in, int64_t n, uint32_t* bsums, uint32_t* total, uint32_t* out, cudaStream_t s);
 

@@ -270,6 +270,27 @@ void launch_zero_nonowned(float* t, int64_t n, int64_t base, const uint8_t* owne
   k_zero_nonowned<<<route_grid(n), 256, 0, s>>>(t, n, base, owner, me);
 }
 
+__global__ void k_pack_slice(const float* __restrict__ P, int64_t G, int64_t g0, int64_t n, int64_t np, float* buf) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < kNP * np; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = t / np, i = t % np;
+    buf[t] = i < n ? P[k * G + g0 + i] : 0.f;
+  }
+}
+__global__ void k_unpack_slices(const float* __restrict__ buf, int W, int64_t np, float* P, int64_t G) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)W * kNP * np;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / (kNP * np), rem = t % (kNP * np), k = rem / np, i = rem % np;
+    const int64_t j = r * np + i;
+    if (j < G) P[k * G + j] = buf[t];
+  }
+}
+void launch_pack_slice(const float* P, int64_t G, int64_t g0, int64_t n, int64_t np, float* buf, cudaStream_t s) {
+  k_pack_slice<<<route_grid(kNP * np), 256, 0, s>>>(P, G, g0, n, np, buf);
+}
+void launch_unpack_slices(const float* buf, int W, int64_t np, float* P, int64_t G, cudaStream_t s) {
+  k_unpack_slices<<<route_grid((int64_t)W * kNP * np), 256, 0, s>>>(buf, W, np, P, G);
+}
+
 void launch_owner(const float* P, int64_t G, const LevelGeom& g, const int32_t* colrank, uint8_t* owner, cudaStream_t s) {
   k_owner<<<route_grid(G), 256, 0, s>>>(P, G, g, colrank, owner);
 }

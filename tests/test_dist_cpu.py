@@ -313,3 +313,61 @@ def test_owner_computes_decomposition_equals_single_rank_gloo():
         np.testing.assert_array_equal(k, full["count"])
         mine = o == r
         np.testing.assert_allclose(g[mine], full["grad"][mine], rtol=1e-10, atol=1e-14)
+
+
+def _zero_worker(rank, world, port, out):
+    """ZeRO data parallel (gc_set_comm mode 3) on CPU: unnormalised gradients reduce-scattered
+    into equal slices of ceil(G / world) Gaussians (padded), each rank runs the oracle's AdamW
+    (C6) on its slice only, the slices' rows are all-gathered -- the replicas must equal one
+    full AdamW step of the single-rank gradient."""
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    goff, P, x, ln, rgb = _problem()
+    G = len(P)
+    lo, hi = shard_range(len(x), rank, world)
+    res = oracle.loss_grad(goff, P, x[lo:hi], ln[lo:hi], rgb[lo:hi], mode=1)
+    k = res["count"].astype(np.float64)
+    g = res["grad"].copy()
+    for l in range(2):
+        g[goff[l]:goff[l + 1]] *= 3 * k[l]
+    zp = -(-G // world)
+    gp = np.zeros((zp * world, 14))
+    gp[:G] = g
+    mine = torch.zeros(zp * 14, dtype=torch.float64)
+    dist.reduce_scatter_tensor(mine, torch.from_numpy(gp.reshape(-1)))   # what ncclReduceScatter sums
+    kt = torch.from_numpy(k.copy())
+    dist.all_reduce(kt)
+    ksum = kt.numpy()
+    gs = mine.numpy().reshape(zp, 14)
+    g0, g1 = min(G, rank * zp), min(G, (rank + 1) * zp)
+    oc = oracle.OracleCache([goff[1], goff[2] - goff[1]], P)
+    gfull = np.zeros_like(P)                                               # only my slice is known
+    gfull[g0:g1] = gs[:g1 - g0]
+    for l in range(2):
+        gfull[goff[l]:goff[l + 1]] /= 3 * ksum[l]
+    oc.step_with_grad(gfull, ksum.astype(np.int64))
+    slab = np.zeros((zp, 14))
+    slab[:g1 - g0] = oc.P[g0:g1]
+    gathered = [torch.zeros(zp * 14, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(gathered, torch.from_numpy(slab.reshape(-1)))
+    Pnew = np.concatenate([t.numpy().reshape(zp, 14) for t in gathered])[:G]
+    out[rank] = Pnew
+    dist.destroy_process_group()
+
+
+def test_zero_data_parallel_equals_single_rank_gloo():
+    world = 3
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.start_processes(_zero_worker, args=(world, port, out), nprocs=world, join=True,
+                           start_method="fork")
+        res = dict(out)
+    goff, P, x, ln, rgb = _problem()
+    oc = oracle.OracleCache([goff[1], goff[2] - goff[1]], P)
+    full = oracle.loss_grad(goff, P, x, ln, rgb, mode=1)
+    oc.step_with_grad(full["grad"], full["count"])
+    for r in range(world):
+        np.testing.assert_allclose(res[r], oc.P, rtol=1e-12, atol=1e-14)
+    np.testing.assert_array_equal(res[0], res[1])

@@ -584,13 +584,15 @@ def _close_up_to_atomic_order(a, b):
     assert np.mean(d > 1e-6 + 1e-5 * np.abs(b)) <= 1e-3
 
 
-def test_data_parallel_one_rank_nccl_path_is_identity(gsc):
-    """The DP path (NCCL all-reduce of gradients + level stats inside gc_fit) on a one-rank
-    communicator must reproduce the plain path (sum over one rank; float atomics make the
-    gradient summation order, hence the last bits, run-dependent)."""
+@pytest.mark.parametrize("mode", [0, 3])
+def test_data_parallel_one_rank_nccl_path_is_identity(gsc, mode):
+    """The DP path (mode 0: NCCL all-reduce of gradients + level stats inside gc_fit; mode 3:
+    ZeRO -- reduce-scatter, AdamW on the rank's slice, all-gather of the updated rows) on a
+    one-rank communicator must reproduce the plain path (sum over one rank; float atomics make
+    the gradient summation order, hence the last bits, run-dependent)."""
     c1, _, _ = make_cfg1(gsc)
     c2, _, _ = make_cfg1(gsc)
-    c2.set_comm(gsc.nccl_unique_id(), 0, 1)
+    c2.set_comm(gsc.nccl_unique_id(), 0, 1, mode=mode)
     for f in range(3):
         x, ln, rgb = workload.fit_batch(1, frame=f, S=50_000)
         s1 = c1.fit(cuda(x), cuda(ln), cuda(rgb))
