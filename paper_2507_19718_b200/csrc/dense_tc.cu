@@ -27,7 +27,7 @@ constexpr float kTcNegHalfLog2e = -0.72134752044448170f;
 struct DenseSmem {
   float a[4][128 * 8];                                       // [kstep * 2 + (hi, lo)]
   float b[4][128 * 8];
-  float4 v[128];
+  float v[128 * 4];                 // pair-interleaved (r_j r_j+1 g_j g_j+1 b_j b_j+1 - -)
   uint64_t bar;
   uint32_t tbase;
 };
@@ -39,15 +39,45 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
   return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
          ((uint64_t)1 << 46);
 }
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+// tf32 rounding (to nearest, ties away from zero, as cvt.rna.tf32.f32) on the integer pipe --
+// the conversion instruction would compete with the epilogue's MUFU.EX2 for the XU pipe
+__device__ __forceinline__ float tf32_int(float x) {
+  return __int_as_float((__float_as_int(x) + 0x1000) & (int)0xFFFFE000);
 }
 __device__ __forceinline__ void put_split(float* tile_hi, float* tile_lo, int r, int k, float x) {
-  const float h = tf32_rna(x), l = tf32_rna(x - h);
+  const float h = tf32_int(x), l = tf32_int(x - h);
   *(float*)((char*)tile_hi + kmaj(r, k)) = h;
   *(float*)((char*)tile_lo + kmaj(r, k)) = l;
+}
+
+// the Gaussian amplitudes are stored pair-interleaved so that the packed epilogue reads each
+// operand pair of its FFMA2s with one shared load and no register moves
+__device__ __forceinline__ void put_v(float* v, int j, float4 c) {
+  float* p = v + 8 * (j >> 1) + (j & 1);
+  p[0] = c.x; p[2] = c.y; p[4] = c.z;
+}
+
+// one 32-column slice of the accumulator row: e = 2^(-Q/2 log2 e) (0 beyond the cut-off when
+// CUT), Y += e * colour; v points at the slice's first Gaussian
+template <bool CUT>
+__device__ __forceinline__ void epi32(const uint32_t (&qv)[32], const float* v, float tau2, float2& Y0, float2& Y1,
+                                      float2& Y2) {
+#pragma unroll
+  for (int k = 0; k < 32; k += 2) {
+    const float2 Q = make_float2(__uint_as_float(qv[k]), __uint_as_float(qv[k + 1]));
+    const float2 tt = __fmul2_rn(Q, make_float2(kTcNegHalfLog2e, kTcNegHalfLog2e));
+    float e0 = ex2_approx(tt.x), e1 = ex2_approx(tt.y);
+    if (CUT) {
+      e0 = Q.x <= tau2 ? e0 : 0.f;
+      e1 = Q.y <= tau2 ? e1 : 0.f;
+    }
+    const float4 P = *reinterpret_cast<const float4*>(v + 4 * k);
+    const float2 B = *reinterpret_cast<const float2*>(v + 4 * k + 4);
+    const float2 e = make_float2(e0, e1);
+    Y0 = __ffma2_rn(e, make_float2(P.x, P.y), Y0);
+    Y1 = __ffma2_rn(e, make_float2(P.z, P.w), Y1);
+    Y2 = __ffma2_rn(e, B, Y2);
+  }
 }
 
 __global__ void __launch_bounds__(kTcThreads, 4) k_dense_tc(DenseArgs a) {
@@ -133,7 +163,7 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_dense_tc(DenseArgs a) {
           const int s = k >> 3;
           put_split(sm.b[2 * s], sm.b[2 * s + 1], t, k & 7, k < 10 ? kap[k] : 0.f);
         }
-        sm.v[t] = v;
+        put_v(sm.v, t, v);
       }
       asm volatile("fence.proxy.async.shared::cta;");   // generic-proxy smem writes -> tensor core
       asm volatile("tcgen05.fence::before_thread_sync;");
@@ -176,18 +206,8 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_dense_tc(DenseArgs a) {
                        "=r"(q[29]), "=r"(q[30]), "=r"(q[31])
                      : "r"(ta));
         asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-        for (int k = 0; k < 32; k += 2) {
-          const float2 Q = make_float2(__uint_as_float(q[k]), __uint_as_float(q[k + 1]));
-          const float2 tt = __fmul2_rn(Q, make_float2(kTcNegHalfLog2e, kTcNegHalfLog2e));
-          const float e0 = Q.x <= a.tau2 ? ex2_approx(tt.x) : 0.f;
-          const float e1 = Q.y <= a.tau2 ? ex2_approx(tt.y) : 0.f;
-          const float4 va = sm.v[c0 + k], vb = sm.v[c0 + k + 1];      // zero beyond nj
-          const float2 e = make_float2(e0, e1);
-          Y0 = __ffma2_rn(e, make_float2(va.x, vb.x), Y0);
-          Y1 = __ffma2_rn(e, make_float2(va.y, vb.y), Y1);
-          Y2 = __ffma2_rn(e, make_float2(va.z, vb.z), Y2);
-        }
+        if (a.tau2 < INFINITY) epi32<true>(q, sm.v + 4 * c0, a.tau2, Y0, Y1, Y2);    // zero beyond nj
+        else epi32<false>(q, sm.v + 4 * c0, a.tau2, Y0, Y1, Y2);
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncthreads();                             // TMEM and B are reused by the next chunk
@@ -209,11 +229,12 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_dense_tc(DenseArgs a) {
 constexpr size_t kDenseSmem = 52 * 1024;
 static_assert(sizeof(DenseSmem) <= kDenseSmem, "dense tile smem");
 
+
 int dense_tc_grid() {
-  cudaFuncSetAttribute(k_dense_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDenseSmem);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncSetAttribute(k_dense_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDenseSmem);
   return sms * 4;
 }
 
