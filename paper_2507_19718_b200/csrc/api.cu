@@ -789,7 +789,7 @@ static gc_status create_impl(gc_cache c, const int64_t* counts, const float* ini
 
 static void free_screen(ScreenBufs& b) {
   for (void* p : {(void*)b.pa, (void*)b.pb, (void*)b.pc, (void*)b.rect, (void*)b.touched, (void*)b.off,
-                  (void*)b.bsums, (void*)b.total, (void*)b.key, (void*)b.val, (void*)b.ranges, (void*)b.img,
+                  (void*)b.bsums, (void*)b.total, (void*)b.key, (void*)b.val, (void*)b.ranges,
                   (void*)b.T, (void*)b.dLdC, (void*)b.last, (void*)b.g2d, (void*)b.raw, (void*)b.tcount,
                   (void*)b.tcursor, (void*)b.tstart, (void*)b.tbsums, (void*)b.ttotal, (void*)b.tbig})
     if (p) cudaFree(p);
@@ -1444,9 +1444,10 @@ gc_status gc_debug_grads(gc_cache c, int level, gc_level_params* dst, gc_stream 
 
 // ------------------------------------------------------------ screen-space evaluator (f1)
 // Projection of levels [lev0, lev1), the (tile, depth) sort and the joint raster into the
-// handle's image buffers (c->scr.img / T / last), or into out/outT when given.
+// caller's out (gc_render) or, with `loss` (gc_fit_image), into the handle's Eq. 4 gradient image
+// c->scr.dLdC; T and the last-contributor counts into c->scr.T / last (or outT when given).
 static gc_status screen_render(gc_cache c, const gc_camera* cam, int lev0, int lev1, float* out, float* outT,
-                               cudaStream_t s) {
+                               cudaStream_t s, const SLossArgs* loss = nullptr) {
   if (!cam || cam->width < 1 || cam->height < 1 || cam->width > 16384 || cam->height > 16384 || !(cam->znear > 0.f))
     return fail(GC_ERR_ARG, "bad camera");
   ScreenBufs& b = c->scr;
@@ -1464,8 +1465,8 @@ static gc_status screen_render(gc_cache c, const gc_camera* cam, int lev0, int l
   const int64_t ntiles = (int64_t)sc.TX * sc.TY;
   if (b.img_cap < Lr * npx) {
     CK(cudaDeviceSynchronize());
-    for (void* p : {(void*)b.img, (void*)b.T, (void*)b.dLdC, (void*)b.last}) if (p) cudaFree(p);
-    CK(dalloc(&b.img, 3 * Lr * npx)); CK(dalloc(&b.T, Lr * npx)); CK(dalloc(&b.dLdC, 3 * Lr * npx));
+    for (void* p : {(void*)b.T, (void*)b.dLdC, (void*)b.last}) if (p) cudaFree(p);
+    CK(dalloc(&b.T, Lr * npx)); CK(dalloc(&b.dLdC, 3 * Lr * npx));
     CK(dalloc(&b.last, Lr * npx));
     b.img_cap = Lr * npx;
   }
@@ -1493,7 +1494,7 @@ static gc_status screen_render(gc_cache c, const gc_camera* cam, int lev0, int l
     for (void* p : {(void*)b.tcount, (void*)b.tcursor, (void*)b.tstart, (void*)b.tbsums, (void*)b.ttotal, (void*)b.tbig})
       if (p) cudaFree(p);
     CK(dalloc(&b.tcount, nt + 1)); CK(dalloc(&b.tcursor, nt + 1)); CK(dalloc(&b.tstart, nt + 1));
-    CK(dalloc(&b.tbsums, nt / 4096 + 2)); CK(dalloc(&b.ttotal, 1)); CK(dalloc(&b.tbig, 1));
+    CK(dalloc(&b.tbsums, nt / 4096 + 2)); CK(dalloc(&b.ttotal, 1)); CK(dalloc(&b.tbig, 3));
     if (!b.htbig) CK(cudaHostAlloc((void**)&b.htbig, sizeof(uint32_t), cudaHostAllocDefault));
     b.tile_cap = nt + 1;
   }
@@ -1503,7 +1504,9 @@ static gc_status screen_render(gc_cache c, const gc_camera* cam, int lev0, int l
   CK(cudaMemcpyAsync(b.htbig, b.tbig, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (*b.htbig) CK(launch_skeys_sort(g0, g1, c->geom, lev0, Lr, sc, b, npairs, Np, s));
-  CK(launch_sraster(sc, Lr, b, out ? out : b.img, outT ? outT : b.T, b.last, s));
+  SLossArgs la{};
+  if (loss) { la = *loss; la.dLdC = b.dLdC; }
+  CK(launch_sraster(sc, Lr, b, out, outT ? outT : b.T, b.last, loss ? &la : nullptr, s));
   return GC_OK;
 }
 
@@ -1535,11 +1538,13 @@ gc_status gc_fit_image(gc_cache c, const gc_camera* cam, const float* target, co
   if (capturing(s)) return fail(GC_ERR_STATE, "gc_fit_image is not graph-capturable");
   if (gc_status e = flush_pending(c, s)) return e;
   const int L = c->L;
-  if (gc_status e = screen_render(c, cam, 0, L, nullptr, nullptr, s)) return e;
   ScreenBufs& b = c->scr;
+  // the raster writes each pixel's Eq. 4 gradient (and the loss partials) instead of its colour
+  // (b.dLdC is sized by screen_render before the raster runs)
+  SLossArgs loss{target, valid, c->hp.hdr_eps, c->hp.loss_grad_mode, nullptr, c->partial};
+  if (gc_status e = screen_render(c, cam, 0, L, nullptr, nullptr, s, &loss)) return e;
   const SCam sc = make_scam(*cam);
   const int64_t npx = (int64_t)cam->width * cam->height;
-  CK(launch_sloss(b.img, target, valid, L, npx, c->hp.hdr_eps, c->hp.loss_grad_mode, b.dLdC, c->partial, s));
   launch_stats(c->partial, c->geom, (int64_t)L * npx, c->lvl, true, c->st, c->hp, L, c->dstats, s, &c->prof);
   CK(launch_sraster_bwd(sc, L, b, b.T, b.last, b.dLdC, b.g2d, s));
   CK(launch_sproject_bwd(c->P, c->G, 0, c->G, sc, b, b.g2d, b.raw, s));

@@ -226,7 +226,7 @@ struct ScreenBufs {
   uint32_t *touched = nullptr, *off = nullptr, *bsums = nullptr, *total = nullptr, *htotal = nullptr;
   uint64_t* key = nullptr; int64_t* val = nullptr; int64_t kv_cap = 0;   // (tile, depth) -> Gaussian
   uint2* ranges = nullptr; int64_t range_cap = 0;
-  float *img = nullptr, *T = nullptr, *dLdC = nullptr; uint32_t* last = nullptr; int64_t img_cap = 0;
+  float *T = nullptr, *dLdC = nullptr; uint32_t* last = nullptr; int64_t img_cap = 0;
   float *g2d = nullptr, *raw = nullptr;                  // [G][12] partials, [14][G] raw gradients
   uint32_t *tcount = nullptr, *tcursor = nullptr, *tstart = nullptr, *tbsums = nullptr, *ttotal = nullptr,
            *tbig = nullptr, *htbig = nullptr;           // two-level tile sort
@@ -239,10 +239,11 @@ cudaError_t launch_skeys_sort(int64_t g0, int64_t g1, const LevelGeom& g, int le
 cudaError_t launch_tile_sort(int64_t g0, int64_t g1, const LevelGeom& g, int lev0, int Lr, const SCam& cam,
                              ScreenBufs& b, uint32_t* tcount, uint32_t* tcursor, uint32_t* tstart, uint32_t* tbsums,
                              uint32_t* ttotal, uint32_t* big, cudaStream_t s);
+struct SLossArgs {             // Eq. 4 fused into the forward raster (gc_fit_image)
+  const float* target; const uint8_t* valid; float eps; int mode; float* dLdC; double* partial;
+};
 cudaError_t launch_sraster(const SCam& cam, int Lr, ScreenBufs& b, float* out, float* outT, uint32_t* last,
-                           cudaStream_t s);
-cudaError_t launch_sloss(const float* img, const float* target, const uint8_t* valid, int Lr, int64_t npx, float eps,
-                         int mode, float* dLdC, double* partial, cudaStream_t s);
+                           const SLossArgs* loss, cudaStream_t s);
 cudaError_t launch_sraster_bwd(const SCam& cam, int Lr, ScreenBufs& b, const float* outT, const uint32_t* last,
                                const float* dLdC, float* g2d, cudaStream_t s);
 cudaError_t launch_sproject_bwd(const float* P, int64_t G, int64_t g0, int64_t g1, const SCam& cam,

@@ -10,15 +10,20 @@
 // Pipeline of gc_render / gc_fit_image:
 //   k_sproject   per Gaussian: EWA projection, conic, radius, tile rectangle, tiles touched
 //   scan         exclusive offsets of the tiles touched (3 small kernels)
-//   k_skeys      (level * tiles + tile) << 32 | depth bits  ->  Gaussian index
-//   sort         bitonic (key, index): per tile, depth order, ties by index
-//   k_sranges    [start, end) of every (level, tile)
+//   two-level sort: k_tile_count (per-(level, tile) counts) -> scan -> k_tile_scatter (keys
+//                depth bits << 32 | index into their tile's segment; rectangles over 16 tiles
+//                walked by the whole warp) -> k_tile_sort_warp (segment ranges; bitonic sort
+//                in registers, one warp per tile of <= 256 keys) -> k_tile_sort_warp16 (<= 512)
+//                -> k_tile_sort (shared memory, <= 8192); the global path (k_skeys, bitonic
+//                sort of (tile, depth) keys, k_sranges) only when a tile holds more
 //   k_sraster    one CTA per (tile, level), 16 x 16 threads, batches of 256 Gaussians staged in
-//                shared memory, front-to-back compositing; C, final T, last contributor
-//   gc_fit_image adds k_sloss (Eq. 4 terms + dL/dC, level statistics), k_sraster_bwd (back to
-//                front, per-Gaussian transposing warp reductions, then float reds) and
-//                k_sproject_bwd (EWA / projection chain rule to the 14 raw parameters), then
-//                the shared AdamW (raw-gradient mode) and the culling rebuild.
+//                shared memory, front-to-back compositing; C, final T, last contributor; for
+//                gc_fit_image Eq. 4 is fused in: dL/dC and the per-level loss statistics
+//                instead of C
+//   gc_fit_image then: k_sraster_bwd (back to front, per-Gaussian transposing warp
+//                reductions, then float reds) and k_sproject_bwd (EWA / projection chain rule
+//                to the 14 raw parameters), the shared AdamW (raw-gradient mode) and the
+//                culling rebuild.
 #include "common.cuh"
 #include "kernels.h"
 #include "stats.cuh"
@@ -207,25 +212,70 @@ struct SRasterArgs {
   float* outT;          // [Lr][H][W] (nullable)
   uint32_t* last;       // [Lr][H][W] last contributor count (nullable)
   SCam cam;
+  // fused Eq. 4 (gc_fit_image): with dLdC set, each pixel's loss gradient is written instead
+  // of its colour (out may be null) and the per-level loss sums / valid counts go to partial
+  const float* target; const uint8_t* valid; float eps; int mode;
+  float* dLdC; double* partial;
 };
 
-__global__ void __launch_bounds__(kTileThreads) k_sraster(SRasterArgs a) {
-  __shared__ float2 s_uv[kTileThreads];
-  __shared__ float4 s_co[kTileThreads];     // conic a, b, c, w
-  __shared__ float4 s_c[kTileThreads];
+// Eq. 4 at one pixel (reading A10: denominator frozen, mode 0, or the full quotient, mode 1):
+__device__ __forceinline__ void pixel_loss(const float* y, const float* x, float eps, int mode, double& ls, float* g) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const float r = x[c] - y[c], d = y[c] + eps;
+    ls += (double)(r * r / (d * d));
+    g[c] = mode == 0 ? -2.f * r / (d * d) : -2.f * r * (x[c] + eps) / (d * d * d);
+  }
+}
+
+// Two horizontally adjacent pixels per thread (128 threads per 16 x 16 tile): the staged
+// Gaussian is read from shared memory once per pixel pair and the pair's opacity chain runs in
+// packed fp32x2 (pix_alpha).  The forward and the backward evaluate a pixel's opacity through
+// this one function, so the backward's acceptance tests reproduce the forward's bit for bit.
+constexpr int kRasterThreads = kTileThreads / 2;
+constexpr float kL2E = 1.4426950408889634f;
+
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// power = -(a dx^2 + c dy^2)/2 - b dx dy at the pixel centres (nfx = -(px + 1/2) of the two
+// pixels, fy = py + 1/2), G = e^power, a0 = w G, alpha = min(0.99, a0) (reading A23)
+__device__ __forceinline__ void pix_alpha(float2 uv, float4 co, float2 nfx, float fy, float2& dx, float& dy,
+                                          float2& power, float2& G, float2& a0, float2& alpha) {
+  dx = __fadd2_rn(make_float2(uv.x, uv.x), nfx);
+  dy = __fadd_rn(uv.y, -fy);
+  const float cdd = __fmul_rn(__fmul_rn(co.z, dy), dy);
+  const float nbdy = -__fmul_rn(co.y, dy);
+  const float2 adx = __fmul2_rn(make_float2(co.x, co.x), dx);
+  const float2 q = __ffma2_rn(adx, dx, make_float2(cdd, cdd));
+  power = __ffma2_rn(make_float2(nbdy, nbdy), dx, __fmul2_rn(make_float2(-0.5f, -0.5f), q));
+  const float2 t = __fmul2_rn(power, make_float2(kL2E, kL2E));
+  G = make_float2(ex2_ftz(t.x), ex2_ftz(t.y));
+  a0 = __fmul2_rn(make_float2(co.w, co.w), G);
+  alpha = make_float2(fminf(0.99f, a0.x), fminf(0.99f, a0.y));
+}
+
+__global__ void __launch_bounds__(kRasterThreads) k_sraster(SRasterArgs a) {
+  __shared__ float2 s_uv[kRasterThreads];
+  __shared__ float4 s_co[kRasterThreads];     // conic a, b, c, w
+  __shared__ float4 s_c[kRasterThreads];
   const int tile = blockIdx.x, l = blockIdx.y;
   const int ntiles = a.cam.TX * a.cam.TY;
   const int tx = tile % a.cam.TX, ty = tile / a.cam.TX;
-  const int px = tx * kTile + (threadIdx.x % kTile), py = ty * kTile + (threadIdx.x / kTile);
-  const bool inside = px < a.cam.W && py < a.cam.H;
-  const float fx = px + 0.5f, fy = py + 0.5f;
+  const int px = tx * kTile + 2 * (threadIdx.x & 7), py = ty * kTile + (threadIdx.x >> 3);
+  const bool in0 = px < a.cam.W && py < a.cam.H, in1 = px + 1 < a.cam.W && py < a.cam.H;
+  const float2 nfx = make_float2(-(px + 0.5f), -(px + 1.5f));
+  const float fy = py + 0.5f;
   const uint2 rg = a.ranges[(size_t)l * ntiles + tile];
   const int n = rg.y > rg.x ? (int)(rg.y - rg.x) : 0;
-  bool done = !inside;
-  float T = 1.f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
-  uint32_t contributor = 0, last = 0;
-  for (int b0 = 0; b0 < n; b0 += kTileThreads) {
-    if (__syncthreads_count(done) == kTileThreads) break;
+  bool done0 = !in0, done1 = !in1;
+  float2 T = make_float2(1.f, 1.f), C0 = make_float2(0.f, 0.f), C1 = C0, C2 = C0;
+  uint32_t last0 = 0, last1 = 0;
+  for (int b0 = 0; b0 < n; b0 += kRasterThreads) {
+    if (__syncthreads_count(done0 && done1) == kRasterThreads) break;
     const int q = b0 + threadIdx.x;
     if (q < n) {
       const int64_t j = a.val[rg.x + q];
@@ -236,62 +286,65 @@ __global__ void __launch_bounds__(kTileThreads) k_sraster(SRasterArgs a) {
       s_c[threadIdx.x] = a.pc[j];
     }
     __syncthreads();
-    const int m = min(kTileThreads, n - b0);
-    for (int k = 0; !done && k < m; ++k) {
-      ++contributor;
-      const float2 uv = s_uv[k];
-      const float4 co = s_co[k];
-      const float dx = uv.x - fx, dy = uv.y - fy;
-      const float power = -0.5f * (co.x * dx * dx + co.z * dy * dy) - co.y * dx * dy;
-      if (power > 0.f) continue;
-      const float alpha = fminf(0.99f, co.w * __expf(power));
-      if (alpha < 1.f / 255.f) continue;
-      const float Tn = T * (1.f - alpha);
-      if (Tn < 1e-4f) { done = true; break; }
+    const int m = min(kRasterThreads, n - b0);
+    for (int k = 0; k < m && !(done0 && done1); ++k) {
+      float2 dx, power, G, a0, alpha;
+      float dy;
+      pix_alpha(s_uv[k], s_co[k], nfx, fy, dx, dy, power, G, a0, alpha);
+      const bool acc0 = !done0 && !(power.x > 0.f) && alpha.x >= 1.f / 255.f;
+      const bool acc1 = !done1 && !(power.y > 0.f) && alpha.y >= 1.f / 255.f;
+      if (!(acc0 || acc1)) continue;
+      const float2 Tn = __fmul2_rn(T, make_float2(1.f - alpha.x, 1.f - alpha.y));
+      const uint32_t cnt = (uint32_t)(b0 + k + 1);        // contributor count of this Gaussian
+      const bool ap0 = acc0 && !(Tn.x < 1e-4f), ap1 = acc1 && !(Tn.y < 1e-4f);
+      done0 |= acc0 && !ap0;
+      done1 |= acc1 && !ap1;
+      const float2 wgt = make_float2(ap0 ? alpha.x * T.x : 0.f, ap1 ? alpha.y * T.y : 0.f);
       const float4 c = s_c[k];
-      const float wgt = alpha * T;
-      C0 += c.x * wgt; C1 += c.y * wgt; C2 += c.z * wgt;
-      T = Tn;
-      last = contributor;
+      C0 = __ffma2_rn(wgt, make_float2(c.x, c.x), C0);
+      C1 = __ffma2_rn(wgt, make_float2(c.y, c.y), C1);
+      C2 = __ffma2_rn(wgt, make_float2(c.z, c.z), C2);
+      if (ap0) { T.x = Tn.x; last0 = cnt; }
+      if (ap1) { T.y = Tn.y; last1 = cnt; }
     }
   }
-  if (inside) {
-    const size_t pix = ((size_t)l * a.cam.H + py) * a.cam.W + px;
-    a.out[3 * pix] = C0; a.out[3 * pix + 1] = C1; a.out[3 * pix + 2] = C2;
-    if (a.outT) a.outT[pix] = T;
-    if (a.last) a.last[pix] = last;
-  }
-}
-
-// --------------------------------------------------------------------------- Eq. 4 on images
-// dLdC = d/dy of sum_ch (x - y)^2 / (y + eps)^2 with the denominator frozen (mode 0, reading
-// A10) or the full quotient (mode 1); the 1/(3 k_l) normalisation is applied by AdamW (inv3k).
-// Per-level loss sums and valid-pixel counts go to the kSlots fp64 partials (k_stats layout).
-__global__ void k_sloss(const float* __restrict__ img, const float* __restrict__ target,
-                        const uint8_t* __restrict__ valid, int Lr, int64_t npx, float eps, int mode,
-                        float* dLdC, double* partial) {
-  const int l = blockIdx.y;
+  const size_t pix = ((size_t)l * a.cam.H + min(py, a.cam.H - 1)) * a.cam.W + px;
+  const float Cp[2][3] = {{C0.x, C1.x, C2.x}, {C0.y, C1.y, C2.y}};
+  const float Tp[2] = {T.x, T.y};
+  const uint32_t Lp[2] = {last0, last1};
   double ls = 0.0, cnt = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npx; i += (int64_t)gridDim.x * blockDim.x) {
-    const size_t p = (size_t)l * npx + i;
-    const bool ok = !valid || valid[p];
-    float g[3] = {0.f, 0.f, 0.f};
-    if (ok) {
-      cnt += 1.0;
-      for (int c = 0; c < 3; ++c) {
-        const float y = img[3 * p + c], x = target[3 * p + c];
-        const float r = x - y, d = y + eps;
-        ls += (double)(r * r / (d * d));
-        g[c] = mode == 0 ? -2.f * r / (d * d) : -2.f * r * (x + eps) / (d * d * d);
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    if (!(i ? in1 : in0)) continue;
+    const size_t pi = pix + i;
+    if (a.out) { a.out[3 * pi] = Cp[i][0]; a.out[3 * pi + 1] = Cp[i][1]; a.out[3 * pi + 2] = Cp[i][2]; }
+    if (a.outT) a.outT[pi] = Tp[i];
+    if (a.last) a.last[pi] = Lp[i];
+    if (a.dLdC) {
+      float g[3] = {0.f, 0.f, 0.f};
+      if (!a.valid || a.valid[pi]) {
+        cnt += 1.0;
+        const float x[3] = {a.target[3 * pi], a.target[3 * pi + 1], a.target[3 * pi + 2]};
+        pixel_loss(Cp[i], x, a.eps, a.mode, ls, g);
+      }
+      a.dLdC[3 * pi] = g[0]; a.dLdC[3 * pi + 1] = g[1]; a.dLdC[3 * pi + 2] = g[2];
+    }
+  }
+  if (a.dLdC) {
+    __shared__ double s_red[2][kRasterThreads / 32];
+    for (int o = 16; o > 0; o >>= 1) { ls += __shfl_xor_sync(0xffffffffu, ls, o); cnt += __shfl_xor_sync(0xffffffffu, cnt, o); }
+    const int wid = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) { s_red[0][wid] = ls; s_red[1][wid] = cnt; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double L = 0.0, N = 0.0;
+      for (int w = 0; w < kRasterThreads / 32; ++w) { L += s_red[0][w]; N += s_red[1][w]; }
+      if (N > 0.0) {
+        double* slot = a.partial + (size_t)(tile % kSlots) * kPart;
+        atomicAdd(slot + l, L);
+        atomicAdd(slot + kMaxL + l, N);
       }
     }
-    dLdC[3 * p] = g[0]; dLdC[3 * p + 1] = g[1]; dLdC[3 * p + 2] = g[2];
-  }
-  for (int o = 16; o > 0; o >>= 1) { ls += __shfl_xor_sync(0xffffffffu, ls, o); cnt += __shfl_xor_sync(0xffffffffu, cnt, o); }
-  if ((threadIdx.x & 31) == 0) {
-    double* slot = partial + (size_t)(blockIdx.x % kSlots) * kPart;
-    atomicAdd(slot + l, ls);
-    atomicAdd(slot + kMaxL + l, cnt);
   }
 }
 
@@ -309,30 +362,61 @@ struct SBwdArgs {
   SCam cam;
 };
 
-__global__ void __launch_bounds__(kTileThreads) k_sraster_bwd(SBwdArgs a) {
-  __shared__ float2 s_uv[kTileThreads];
-  __shared__ float4 s_co[kTileThreads];
-  __shared__ float4 s_c[kTileThreads];
-  __shared__ int64_t s_j[kTileThreads];
+// One pixel's share of the backward at one accepted Gaussian (back to front): recovers T
+// before it, updates the colour behind, and adds the 9 partials into d.
+struct PixBwd {
+  float T, g0, g1, g2, acc0, acc1, acc2, la, lc0, lc1, lc2;
+};
+__device__ __forceinline__ void pix_bwd(PixBwd& p, float4 co, float4 c, float dx, float dy, float G, float a0,
+                                        float alpha, float (&d)[9]) {
+  p.T = p.T / (1.f - alpha);
+  const float wgt = alpha * p.T;
+  d[6] += wgt * p.g0; d[7] += wgt * p.g1; d[8] += wgt * p.g2;                  // dL/dchat
+  p.acc0 = p.la * p.lc0 + (1.f - p.la) * p.acc0;
+  p.acc1 = p.la * p.lc1 + (1.f - p.la) * p.acc1;
+  p.acc2 = p.la * p.lc2 + (1.f - p.la) * p.acc2;
+  p.la = alpha; p.lc0 = c.x; p.lc1 = c.y; p.lc2 = c.z;
+  const float dLda = p.T * ((c.x - p.acc0) * p.g0 + (c.y - p.acc1) * p.g1 + (c.z - p.acc2) * p.g2);
+  if (a0 < 0.99f) {
+    d[5] += dLda * G;                                                            // dL/dw
+    const float dLdp = dLda * co.w * G;                                          // dL/dpower
+    d[0] -= dLdp * (co.x * dx + co.y * dy);                                      // dL/du
+    d[1] -= dLdp * (co.z * dy + co.y * dx);                                      // dL/dv
+    d[2] -= 0.5f * dLdp * dx * dx;                                               // dL/dconic_a
+    d[3] -= dLdp * dx * dy;                                                      // dL/dconic_b
+    d[4] -= 0.5f * dLdp * dy * dy;                                               // dL/dconic_c
+  }
+}
+
+__global__ void __launch_bounds__(kRasterThreads) k_sraster_bwd(SBwdArgs a) {
+  __shared__ float2 s_uv[kRasterThreads];
+  __shared__ float4 s_co[kRasterThreads];
+  __shared__ float4 s_c[kRasterThreads];
+  __shared__ int64_t s_j[kRasterThreads];
   const int tile = blockIdx.x, l = blockIdx.y;
   const int ntiles = a.cam.TX * a.cam.TY;
   const int tx = tile % a.cam.TX, ty = tile / a.cam.TX;
-  const int px = tx * kTile + (threadIdx.x % kTile), py = ty * kTile + (threadIdx.x / kTile);
-  const bool inside = px < a.cam.W && py < a.cam.H;
-  const float fx = px + 0.5f, fy = py + 0.5f;
+  const int px = tx * kTile + 2 * (threadIdx.x & 7), py = ty * kTile + (threadIdx.x >> 3);
+  const bool in0 = px < a.cam.W && py < a.cam.H, in1 = px + 1 < a.cam.W && py < a.cam.H;
+  const float2 nfx = make_float2(-(px + 0.5f), -(px + 1.5f));
+  const float fy = py + 0.5f;
   const uint2 rg = a.ranges[(size_t)l * ntiles + tile];
   const int n = rg.y > rg.x ? (int)(rg.y - rg.x) : 0;
-  const size_t pix = ((size_t)l * a.cam.H + min(py, a.cam.H - 1)) * a.cam.W + min(px, a.cam.W - 1);
-  float T = inside ? a.outT[pix] : 1.f;
-  const uint32_t lastc = inside ? a.last[pix] : 0u;
-  const float g0 = inside ? a.dLdC[3 * pix] : 0.f, g1 = inside ? a.dLdC[3 * pix + 1] : 0.f,
-              g2 = inside ? a.dLdC[3 * pix + 2] : 0.f;
-  float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;        // colour behind (normalised)
-  float la = 0.f, lc0 = 0.f, lc1 = 0.f, lc2 = 0.f; // last processed (behind) Gaussian
-  uint32_t contributor = (uint32_t)n;
+  const size_t pix = ((size_t)l * a.cam.H + min(py, a.cam.H - 1)) * a.cam.W + px;
+  PixBwd p0{}, p1{};
+  int last0 = 0, last1 = 0;
+  if (in0) {
+    p0.T = a.outT[pix]; last0 = (int)a.last[pix];
+    p0.g0 = a.dLdC[3 * pix]; p0.g1 = a.dLdC[3 * pix + 1]; p0.g2 = a.dLdC[3 * pix + 2];
+  }
+  if (in1) {
+    p1.T = a.outT[pix + 1]; last1 = (int)a.last[pix + 1];
+    p1.g0 = a.dLdC[3 * pix + 3]; p1.g1 = a.dLdC[3 * pix + 4]; p1.g2 = a.dLdC[3 * pix + 5];
+  }
+  const int lastmax = max(last0, last1);                  // Gaussians at positions >= last were not accepted
   const int lane = threadIdx.x & 31;
-  for (int b1 = n; b1 > 0; b1 -= kTileThreads) {
-    const int b0 = max(0, b1 - kTileThreads);
+  for (int b1 = n; b1 > 0; b1 -= kRasterThreads) {
+    const int b0 = max(0, b1 - kRasterThreads);
     __syncthreads();
     const int q = b0 + threadIdx.x;
     if (q < b1) {
@@ -346,38 +430,21 @@ __global__ void __launch_bounds__(kTileThreads) k_sraster_bwd(SBwdArgs a) {
     }
     __syncthreads();
     for (int k = b1 - b0 - 1; k >= 0; --k) {
+      const int gpos = b0 + k;
       float d[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       bool use = false;
-      if (inside && contributor-- <= lastc) {
-        const float2 uv = s_uv[k];
+      if (gpos < lastmax) {
         const float4 co = s_co[k];
-        const float dx = uv.x - fx, dy = uv.y - fy;
-        const float power = -0.5f * (co.x * dx * dx + co.z * dy * dy) - co.y * dx * dy;
-        if (power <= 0.f) {
-          const float G = __expf(power);
-          const float a0 = co.w * G;
-          const float alpha = fminf(0.99f, a0);
-          if (alpha >= 1.f / 255.f) {
-            use = true;
-            T = T / (1.f - alpha);
-            const float4 c = s_c[k];
-            const float wgt = alpha * T;
-            d[6] = wgt * g0; d[7] = wgt * g1; d[8] = wgt * g2;                  // dL/dchat
-            acc0 = la * lc0 + (1.f - la) * acc0;
-            acc1 = la * lc1 + (1.f - la) * acc1;
-            acc2 = la * lc2 + (1.f - la) * acc2;
-            la = alpha; lc0 = c.x; lc1 = c.y; lc2 = c.z;
-            const float dLda = T * ((c.x - acc0) * g0 + (c.y - acc1) * g1 + (c.z - acc2) * g2);
-            if (a0 < 0.99f) {
-              d[5] = dLda * G;                                                  // dL/dw
-              const float dLdp = dLda * co.w * G;                               // dL/dpower
-              d[0] = -dLdp * (co.x * dx + co.y * dy);                           // dL/du
-              d[1] = -dLdp * (co.z * dy + co.y * dx);                           // dL/dv
-              d[2] = -0.5f * dLdp * dx * dx;                                    // dL/dconic_a
-              d[3] = -dLdp * dx * dy;                                           // dL/dconic_b
-              d[4] = -0.5f * dLdp * dy * dy;                                    // dL/dconic_c
-            }
-          }
+        float2 dx, power, G, a0, alpha;
+        float dy;
+        pix_alpha(s_uv[k], co, nfx, fy, dx, dy, power, G, a0, alpha);
+        const bool u0 = gpos < last0 && !(power.x > 0.f) && alpha.x >= 1.f / 255.f;
+        const bool u1 = gpos < last1 && !(power.y > 0.f) && alpha.y >= 1.f / 255.f;
+        if (u0 || u1) {
+          const float4 c = s_c[k];
+          if (u0) pix_bwd(p0, co, c, dx.x, dy, G.x, a0.x, alpha.x, d);
+          if (u1) pix_bwd(p1, co, c, dx.y, dy, G.y, a0.y, alpha.y, d);
+          use = true;
         }
       }
       // per-warp reduction, then one vector red per warp (skipped when no lane contributed)
@@ -554,8 +621,48 @@ cudaError_t launch_skeys_sort(int64_t g0, int64_t g1, const LevelGeom& g, int le
 // ---------------------------------------------- two-level sort: counting sort by tile, then
 // a per-tile sort of (depth bits << 32 | index) in shared memory.  The 64-bit key orders a
 // tile's Gaussians by depth with ties by index (the global sort's order, reading A23).
+// Rectangles larger than kCoopArea tiles are walked by the whole warp (lanes split the tiles)
+// instead of by their own thread: the top level's Gaussians cover up to ~200 tiles at 1080p
+// and a thread walking them one returning atomic at a time was the kernel's tail.
+constexpr int kCoopArea = 16;
+
+template <typename F>
+__device__ __forceinline__ void for_each_tile(int64_t g0, int64_t g1, const int4* __restrict__ rect, F&& f) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = g0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane; base < g1; base += stride) {
+    const int64_t j = base + lane;
+    int4 r = make_int4(0, 0, 0, 0);
+    if (j < g1) r = rect[j];
+    const int w = max(r.y - r.x, 0), h = max(r.w - r.z, 0), area = w * h;
+    const bool coop = area > kCoopArea;
+    if (!coop)
+      for (int ty = r.z; ty < r.w; ++ty)
+        for (int tx = r.x; tx < r.y; ++tx) f(j, tx, ty);
+    uint32_t m = __ballot_sync(0xffffffffu, coop);
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const int64_t js = __shfl_sync(0xffffffffu, j, src);
+      const int rx = __shfl_sync(0xffffffffu, r.x, src), rz = __shfl_sync(0xffffffffu, r.z, src);
+      const int ws = __shfl_sync(0xffffffffu, w, src), as = __shfl_sync(0xffffffffu, area, src);
+      // lane i walks tiles i, i + 32, ... of the row-major rectangle (one division per rectangle)
+      const int d32 = 32 / ws, r32 = 32 - d32 * ws;
+      int ty = lane / ws, tx = lane - ty * ws;
+      for (int i = lane; i < as; i += 32) {
+        f(js, rx + tx, rz + ty);
+        tx += r32; ty += d32;
+        if (tx >= ws) { tx -= ws; ++ty; }
+      }
+    }
+  }
+}
+
+// a per-tile sort of (depth bits << 32 | index).  The 64-bit key orders a tile's Gaussians by
+// depth with ties by index (the global sort's order, reading A23).
 __global__ void k_tile_count(int64_t g0, int64_t g1, LevelGeom g, int lev0, int ntiles_img, int TX,
                              const int4* __restrict__ rect, uint32_t* count) {
+  // (fire-and-forget reductions: a thread walks its own rectangle)
   for (int64_t j = g0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < g1; j += (int64_t)gridDim.x * blockDim.x) {
     const int4 r = rect[j];
     if (!(r.x < r.y && r.z < r.w)) continue;
@@ -568,49 +675,142 @@ __global__ void k_tile_count(int64_t g0, int64_t g1, LevelGeom g, int lev0, int 
 __global__ void k_tile_scatter(int64_t g0, int64_t g1, LevelGeom g, int lev0, int ntiles_img, int TX,
                                const float4* __restrict__ pa, const int4* __restrict__ rect,
                                const uint32_t* __restrict__ start, uint32_t* cursor, uint64_t* key) {
-  for (int64_t j = g0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < g1; j += (int64_t)gridDim.x * blockDim.x) {
-    const int4 r = rect[j];
-    if (!(r.x < r.y && r.z < r.w)) continue;
+  for_each_tile(g0, g1, rect, [&](int64_t j, int tx, int ty) {
     const int l = level_of_gaussian(g, j) - lev0;
     const uint64_t k = ((uint64_t)__float_as_uint(pa[j].z) << 32) | (uint64_t)(uint32_t)j;
-    for (int ty = r.z; ty < r.w; ++ty)
-      for (int tx = r.x; tx < r.y; ++tx) {
-        const size_t t = (size_t)l * ntiles_img + ty * TX + tx;
-        key[start[t] + atomicAdd(cursor + t, 1u)] = k;
+    const size_t t = (size_t)l * ntiles_img + ty * TX + tx;
+    key[start[t] + atomicAdd(cursor + t, 1u)] = k;
+  });
+}
+
+// Bitonic sort of one tile's n <= 32 E keys by one warp, E keys per lane in registers (lane
+// holds elements lane E .. lane E + E - 1): exchanges across lanes by shuffles, within a lane
+// by register compare-swaps.
+template <int E>
+__device__ __forceinline__ void warp_sort_tile(uint64_t* __restrict__ key, int64_t* __restrict__ val, uint32_t b0,
+                                               int n, int lane) {
+  uint64_t x[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = lane * E + e;
+    x[e] = i < n ? key[b0 + i] : ~0ull;
+  }
+  constexpr int NP = 32 * E;
+#pragma unroll
+  for (int k = 2; k <= NP; k <<= 1) {
+#pragma unroll
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      if (jj >= E) {
+        const int lm = jj / E;
+        const bool lower = (lane & lm) == 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const bool up = ((lane * E + e) & k) == 0;
+          const uint64_t y = __shfl_xor_sync(0xffffffffu, x[e], lm);
+          x[e] = (lower == up) ? (y < x[e] ? y : x[e]) : (y > x[e] ? y : x[e]);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if ((e & jj) == 0) {
+            const bool up = ((lane * E + e) & k) == 0;
+            const uint64_t a = x[e], c = x[e | jj];
+            const bool sw = (c < a) == up;
+            x[e] = sw ? c : a;
+            x[e | jj] = sw ? a : c;
+          }
+        }
       }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = lane * E + e;
+    if (i < n) val[b0 + i] = (int64_t)(uint32_t)(x[e] & 0xFFFFFFFFull);
   }
 }
 
+constexpr int kWarpSortMax = 256;            // tiles up to this many keys: one warp, registers
 constexpr int kTileSortMax = 8192;           // items per tile sorted in shared memory (64 KB)
 
-// one CTA per (level, tile): bitonic sort of its segment in shared memory; segments over the
-// capacity flag `big` (the host then falls back to the global sort)
-__global__ void __launch_bounds__(1024) k_tile_sort(const uint32_t* __restrict__ start, const uint32_t* __restrict__ total,
-                                                    int nt, uint64_t* key, int64_t* val, uint2* ranges, uint32_t* big) {
-  extern __shared__ uint64_t sk[];
-  const int t = blockIdx.x;
-  const uint32_t b0 = start[t], b1 = t + 1 < nt ? start[t + 1] : *total;
-  const int n = (int)(b1 - b0);
-  if (threadIdx.x == 0) ranges[t] = make_uint2(b0, b1);
-  if (n <= 0) return;
-  if (n > kTileSortMax) { if (threadIdx.x == 0) atomicExch(big, 1u); return; }
-  int np = 1;
-  while (np < n) np <<= 1;
-  for (int i = threadIdx.x; i < np; i += blockDim.x) sk[i] = i < n ? key[b0 + i] : ~0ull;
-  __syncthreads();
-  for (int k = 2; k <= np; k <<= 1)
-    for (int jj = k >> 1; jj > 0; jj >>= 1) {
-      for (int i = threadIdx.x; i < np; i += blockDim.x) {
-        const int p = i ^ jj;
-        if (p > i) {
-          const bool up = (i & k) == 0;
-          const uint64_t a = sk[i], c = sk[p];
-          if ((c < a) == up) { sk[i] = c; sk[p] = a; }
-        }
-      }
-      __syncthreads();
+// one warp per (level, tile): ranges, then the register sort; larger tiles are appended to
+// `list` (list_n = big[1]) for the shared-memory kernel
+__global__ void k_tile_sort_warp(const uint32_t* __restrict__ start, const uint32_t* __restrict__ total, int nt,
+                                 uint64_t* key, int64_t* val, uint2* ranges, uint32_t* list, uint32_t* big) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nt; t += nw) {
+    const uint32_t b0 = start[t], b1 = t + 1 < nt ? start[t + 1] : *total;
+    const int n = (int)(b1 - b0);
+    if (lane == 0) ranges[t] = make_uint2(b0, b1);
+    if (n <= 1) {
+      if (n == 1 && lane == 0) val[b0] = (int64_t)(uint32_t)(key[b0] & 0xFFFFFFFFull);
+      continue;
     }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) val[b0 + i] = (int64_t)(uint32_t)(sk[i] & 0xFFFFFFFFull);
+    if (n > kWarpSortMax) {
+      if (lane == 0) list[atomicAdd(big + 1, 1u)] = (uint32_t)t;
+      continue;
+    }
+    if (n <= 32) warp_sort_tile<1>(key, val, b0, n, lane);
+    else if (n <= 64) warp_sort_tile<2>(key, val, b0, n, lane);
+    else if (n <= 128) warp_sort_tile<4>(key, val, b0, n, lane);
+    else warp_sort_tile<8>(key, val, b0, n, lane);
+  }
+}
+
+// one warp per listed tile of (kWarpSortMax, 2 kWarpSortMax] keys (16 per lane: a kernel of
+// its own, so that the register budget of the 16-key sort does not limit the first pass);
+// larger tiles go on to list2 (big[2]) for the shared-memory kernel
+__global__ void k_tile_sort_warp16(const uint32_t* __restrict__ start, const uint32_t* __restrict__ total, int nt,
+                                   const uint32_t* __restrict__ list, uint64_t* key, int64_t* val, uint32_t* list2,
+                                   uint32_t* big) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t nlist = big[1];
+  for (uint32_t li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < nlist; li += nw) {
+    const int t = (int)list[li];
+    const uint32_t b0 = start[t], b1 = t + 1 < nt ? start[t + 1] : *total;
+    const int n = (int)(b1 - b0);
+    if (n > 2 * kWarpSortMax) {
+      if (lane == 0) list2[atomicAdd(big + 2, 1u)] = (uint32_t)t;
+      continue;
+    }
+    warp_sort_tile<16>(key, val, b0, n, lane);
+  }
+}
+
+// one CTA per listed (level, tile) of more than 2 kWarpSortMax keys: bitonic sort of its segment
+// in shared memory; segments over kTileSortMax flag big[0] (the host then falls back to the
+// global sort)
+__global__ void __launch_bounds__(1024) k_tile_sort(const uint32_t* __restrict__ start, const uint32_t* __restrict__ total,
+                                                    int nt, const uint32_t* __restrict__ list, uint64_t* key,
+                                                    int64_t* val, uint32_t* big) {
+  extern __shared__ uint64_t sk[];
+  const uint32_t nlist = big[2];
+  for (uint32_t li = blockIdx.x; li < nlist; li += gridDim.x) {
+    const int t = (int)list[li];
+    const uint32_t b0 = start[t], b1 = t + 1 < nt ? start[t + 1] : *total;
+    const int n = (int)(b1 - b0);
+    if (n > kTileSortMax) { if (threadIdx.x == 0) atomicExch(big, 1u); continue; }
+    int np = 1;
+    while (np < n) np <<= 1;
+    __syncthreads();
+    for (int i = threadIdx.x; i < np; i += blockDim.x) sk[i] = i < n ? key[b0 + i] : ~0ull;
+    __syncthreads();
+    for (int k = 2; k <= np; k <<= 1)
+      for (int jj = k >> 1; jj > 0; jj >>= 1) {
+        for (int i = threadIdx.x; i < np; i += blockDim.x) {
+          const int p = i ^ jj;
+          if (p > i) {
+            const bool up = (i & k) == 0;
+            const uint64_t a = sk[i], c = sk[p];
+            if ((c < a) == up) { sk[i] = c; sk[p] = a; }
+          }
+        }
+        __syncthreads();
+      }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) val[b0 + i] = (int64_t)(uint32_t)(sk[i] & 0xFFFFFFFFull);
+  }
 }
 
 // Returns in *big_host whether some tile exceeded kTileSortMax (then the caller uses the
@@ -624,32 +824,34 @@ cudaError_t launch_tile_sort(int64_t g0, int64_t g1, const LevelGeom& g, int lev
   cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kTileSortMax * sizeof(uint64_t)));
   cudaMemsetAsync(tcount, 0, sizeof(uint32_t) * nt, s);
   cudaMemsetAsync(tcursor, 0, sizeof(uint32_t) * nt, s);
-  cudaMemsetAsync(big, 0, sizeof(uint32_t), s);
+  cudaMemsetAsync(big, 0, 3 * sizeof(uint32_t), s);
   k_tile_count<<<sblocks(g1 - g0), 256, 0, s>>>(g0, g1, g, lev0, ntiles, cam.TX, b.rect, tcount);
   launch_scan_u32(tcount, nt, tbsums, ttotal, tstart, s);
   k_tile_scatter<<<sblocks(g1 - g0), 256, 0, s>>>(g0, g1, g, lev0, ntiles, cam.TX, b.pa, b.rect, tstart, tcursor, b.key);
-  k_tile_sort<<<nt, 1024, kTileSortMax * sizeof(uint64_t), s>>>(tstart, ttotal, nt, b.key, b.val, b.ranges, big);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // tcount / tcursor are free after the scatter: they hold the tile lists of the later passes
+  k_tile_sort_warp<<<(int)std::max<int64_t>((nt + 7) / 8, 1), 256, 0, s>>>(tstart, ttotal, nt, b.key, b.val, b.ranges,
+                                                                          tcount, big);
+  k_tile_sort_warp16<<<sms, 256, 0, s>>>(tstart, ttotal, nt, tcount, b.key, b.val, tcursor, big);
+  k_tile_sort<<<sms * 2, 1024, kTileSortMax * sizeof(uint64_t), s>>>(tstart, ttotal, nt, tcursor, b.key, b.val, big);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sraster(const SCam& cam, int Lr, ScreenBufs& b, float* out, float* outT, uint32_t* last,
-                           cudaStream_t s) {
-  SRasterArgs a{b.ranges, b.val, b.pa, b.pb, b.pc, out, outT, last, cam};
-  k_sraster<<<dim3(cam.TX * cam.TY, Lr), kTileThreads, 0, s>>>(a);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_sloss(const float* img, const float* target, const uint8_t* valid, int Lr, int64_t npx, float eps,
-                         int mode, float* dLdC, double* partial, cudaStream_t s) {
-  const int bx = (int)std::min<int64_t>((npx + 255) / 256, 256);
-  k_sloss<<<dim3(std::max(bx, 1), Lr), 256, 0, s>>>(img, target, valid, Lr, npx, eps, mode, dLdC, partial);
+                           const SLossArgs* loss, cudaStream_t s) {
+  SRasterArgs a{b.ranges, b.val, b.pa, b.pb, b.pc, out, outT, last, cam,
+                loss ? loss->target : nullptr, loss ? loss->valid : nullptr, loss ? loss->eps : 0.f,
+                loss ? loss->mode : 0, loss ? loss->dLdC : nullptr, loss ? loss->partial : nullptr};
+  k_sraster<<<dim3(cam.TX * cam.TY, Lr), kRasterThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sraster_bwd(const SCam& cam, int Lr, ScreenBufs& b, const float* outT, const uint32_t* last,
                                const float* dLdC, float* g2d, cudaStream_t s) {
   SBwdArgs a{b.ranges, b.val, b.pa, b.pb, b.pc, outT, last, dLdC, g2d, cam};
-  k_sraster_bwd<<<dim3(cam.TX * cam.TY, Lr), kTileThreads, 0, s>>>(a);
+  k_sraster_bwd<<<dim3(cam.TX * cam.TY, Lr), kRasterThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -10,7 +10,7 @@ import paper_2507_19718_b200 as gsc  # noqa: E402
 
 
 class A:
-    steps = 24
+    steps = int(os.environ.get("STEPS", "24"))
 
 
 if __name__ == "__main__":
