@@ -1478,7 +1478,16 @@ static gc_status screen_render(gc_cache c, const gc_camera* cam, int lev0, int l
   }
   if ((int64_t)Lr * ntiles >= ((int64_t)1 << 31)) return fail(GC_ERR_ARG, "image too large for the tile keys");
   const int64_t g0 = c->geom.goff[lev0], g1 = c->geom.goff[lev1];
-  CK(launch_sproject(c->P, G, g0, g1, sc, b, s));
+  const int64_t nt = (int64_t)Lr * ntiles;
+  if (b.tile_cap < nt + 1) {
+    for (void* p : {(void*)b.tcount, (void*)b.tcursor, (void*)b.tstart, (void*)b.tbsums, (void*)b.ttotal, (void*)b.tbig})
+      if (p) cudaFree(p);
+    CK(dalloc(&b.tcount, nt + 1)); CK(dalloc(&b.tcursor, nt + 1)); CK(dalloc(&b.tstart, nt + 1));
+    CK(dalloc(&b.tbsums, nt / 4096 + 2)); CK(dalloc(&b.ttotal, 1)); CK(dalloc(&b.tbig, 3));
+    if (!b.htbig) CK(cudaHostAlloc((void**)&b.htbig, sizeof(uint32_t), cudaHostAllocDefault));
+    b.tile_cap = nt + 1;
+  }
+  CK(launch_sproject(c->P, G, g0, g1, sc, b, c->geom, lev0, Lr, s));
   CK(cudaMemcpyAsync(b.htotal, b.total, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   const int64_t npairs = *b.htotal;
@@ -1488,15 +1497,6 @@ static gc_status screen_render(gc_cache c, const gc_camera* cam, int lev0, int l
     if (b.val) cudaFree(b.val);
     CK(dalloc(&b.key, Np)); CK(dalloc(&b.val, Np));
     b.kv_cap = Np;
-  }
-  const int64_t nt = (int64_t)Lr * ntiles;
-  if (b.tile_cap < nt + 1) {
-    for (void* p : {(void*)b.tcount, (void*)b.tcursor, (void*)b.tstart, (void*)b.tbsums, (void*)b.ttotal, (void*)b.tbig})
-      if (p) cudaFree(p);
-    CK(dalloc(&b.tcount, nt + 1)); CK(dalloc(&b.tcursor, nt + 1)); CK(dalloc(&b.tstart, nt + 1));
-    CK(dalloc(&b.tbsums, nt / 4096 + 2)); CK(dalloc(&b.ttotal, 1)); CK(dalloc(&b.tbig, 3));
-    if (!b.htbig) CK(cudaHostAlloc((void**)&b.htbig, sizeof(uint32_t), cudaHostAllocDefault));
-    b.tile_cap = nt + 1;
   }
   // counting sort by tile + per-tile shared-memory sort; the global bitonic sort only when a
   // tile holds more than 8192 Gaussians

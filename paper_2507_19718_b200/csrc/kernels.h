@@ -233,7 +233,7 @@ struct ScreenBufs {
   int64_t tile_cap = 0;
 };
 cudaError_t launch_sproject(const float* P, int64_t G, int64_t g0, int64_t g1, const SCam& cam, ScreenBufs& b,
-                            cudaStream_t s);
+                            const LevelGeom& g, int lev0, int Lr, cudaStream_t s);
 cudaError_t launch_skeys_sort(int64_t g0, int64_t g1, const LevelGeom& g, int lev0, int Lr, const SCam& cam,
                               ScreenBufs& b, int64_t npairs, int64_t Np, cudaStream_t s);
 cudaError_t launch_tile_sort(int64_t g0, int64_t g1, const LevelGeom& g, int lev0, int Lr, const SCam& cam,

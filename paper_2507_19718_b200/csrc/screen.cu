@@ -8,11 +8,11 @@
 // oracle/screen_oracle.c.
 //
 // Pipeline of gc_render / gc_fit_image:
-//   k_sproject   per Gaussian: EWA projection, conic, radius, tile rectangle, tiles touched
-//   scan         exclusive offsets of the tiles touched (3 small kernels)
-//   two-level sort: k_tile_count (per-(level, tile) counts) -> scan -> k_tile_scatter (keys
-//                depth bits << 32 | index into their tile's segment; rectangles over 16 tiles
-//                walked by the whole warp) -> k_tile_sort_warp (segment ranges; bitonic sort
+//   k_sproject   per Gaussian: EWA projection, conic, radius, tile rectangle, tiles touched,
+//                per-(level, tile) key counts, their total
+//   two-level sort: per-(level, tile) key counts (k_sproject) -> scan -> k_tile_scatter (keys
+//                depth bits << 32 | index into their tile's segment; a warp's (Gaussian, tile)
+//                pairs spread evenly over its lanes) -> k_tile_sort_warp (segment ranges; bitonic sort
 //                in registers, one warp per tile of <= 256 keys) -> k_tile_sort_warp16 (<= 512)
 //                -> k_tile_sort (shared memory, <= 8192); the global path (k_skeys, bitonic
 //                sort of (tile, depth) keys, k_sranges) only when a tile holds more
@@ -58,8 +58,12 @@ __device__ __forceinline__ int clamp_tile(float f, int n) {
 
 // --------------------------------------------------------------------------- projection
 // pa = (u, v, depth, w), pb = (conic a, b, c, -), pc = (chat, ok), rect = (x0, x1, y0, y1)
+// It also counts the keys of every (level, tile) (count, fire-and-forget reductions over the
+// rectangle) and their total (npairs, one warp-aggregated atomic).
 __global__ void k_sproject(const float* __restrict__ P, int64_t G, int64_t g0, int64_t g1, SCam cam,
-                           float4* pa, float4* pb, float4* pc, int4* rect, uint32_t* touched) {
+                           float4* pa, float4* pb, float4* pc, int4* rect, uint32_t* touched, LevelGeom lg,
+                           int lev0, uint32_t* count, uint32_t* npairs) {
+  const int ntiles_img = cam.TX * cam.TY;
   for (int64_t j = g0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < g1; j += (int64_t)gridDim.x * blockDim.x) {
     uint32_t n = 0;
     float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a, c = a;
@@ -111,6 +115,14 @@ __global__ void k_sproject(const float* __restrict__ P, int64_t G, int64_t g0, i
     }
     pa[j] = a; pb[j] = b; pc[j] = c; rect[j] = r;
     touched[j - g0] = n;
+    if (n) {
+      const size_t lbase = (size_t)(level_of_gaussian(lg, j) - lev0) * ntiles_img;
+      for (int ty = r.z; ty < r.w; ++ty)
+        for (int tx = r.x; tx < r.y; ++tx) atomicAdd(count + lbase + ty * cam.TX + tx, 1u);
+    }
+    const uint32_t m = __activemask();
+    const uint32_t tot = __reduce_add_sync(m, n);
+    if ((threadIdx.x & 31) == __ffs(m) - 1 && tot) atomicAdd(npairs, tot);
   }
 }
 
@@ -219,12 +231,14 @@ struct SRasterArgs {
 };
 
 // Eq. 4 at one pixel (reading A10: denominator frozen, mode 0, or the full quotient, mode 1):
-__device__ __forceinline__ void pixel_loss(const float* y, const float* x, float eps, int mode, double& ls, float* g) {
+// (one approximate reciprocal per channel; the pixel's 3 terms summed in fp32, the tile's in fp64)
+__device__ __forceinline__ void pixel_loss(const float* y, const float* x, float eps, int mode, float& ls, float* g) {
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     const float r = x[c] - y[c], d = y[c] + eps;
-    ls += (double)(r * r / (d * d));
-    g[c] = mode == 0 ? -2.f * r / (d * d) : -2.f * r * (x[c] + eps) / (d * d * d);
+    const float id2 = __fdividef(1.f, d * d);
+    ls += r * r * id2;
+    g[c] = mode == 0 ? -2.f * r * id2 : __fdividef(-2.f * r * (x[c] + eps) * id2, d);
   }
 }
 
@@ -232,7 +246,6 @@ __device__ __forceinline__ void pixel_loss(const float* y, const float* x, float
 // Gaussian is read from shared memory once per pixel pair and the pair's opacity chain runs in
 // packed fp32x2 (pix_alpha).  The forward and the backward evaluate a pixel's opacity through
 // this one function, so the backward's acceptance tests reproduce the forward's bit for bit.
-constexpr int kRasterThreads = kTileThreads / 2;
 constexpr float kL2E = 1.4426950408889634f;
 
 __device__ __forceinline__ float ex2_ftz(float x) {
@@ -257,6 +270,8 @@ __device__ __forceinline__ void pix_alpha(float2 uv, float4 co, float2 nfx, floa
   a0 = __fmul2_rn(make_float2(co.w, co.w), G);
   alpha = make_float2(fminf(0.99f, a0.x), fminf(0.99f, a0.y));
 }
+
+constexpr int kRasterThreads = kTileThreads / 2;
 
 __global__ void __launch_bounds__(kRasterThreads) k_sraster(SRasterArgs a) {
   __shared__ float2 s_uv[kRasterThreads];
@@ -325,7 +340,9 @@ __global__ void __launch_bounds__(kRasterThreads) k_sraster(SRasterArgs a) {
       if (!a.valid || a.valid[pi]) {
         cnt += 1.0;
         const float x[3] = {a.target[3 * pi], a.target[3 * pi + 1], a.target[3 * pi + 2]};
-        pixel_loss(Cp[i], x, a.eps, a.mode, ls, g);
+        float lp = 0.f;
+        pixel_loss(Cp[i], x, a.eps, a.mode, lp, g);
+        ls += (double)lp;
       }
       a.dLdC[3 * pi] = g[0]; a.dLdC[3 * pi + 1] = g[1]; a.dLdC[3 * pi + 2] = g[2];
     }
@@ -362,30 +379,51 @@ struct SBwdArgs {
   SCam cam;
 };
 
-// One pixel's share of the backward at one accepted Gaussian (back to front): recovers T
-// before it, updates the colour behind, and adds the 9 partials into d.
-struct PixBwd {
-  float T, g0, g1, g2, acc0, acc1, acc2, la, lc0, lc1, lc2;
+// The pixel pair's share of the backward at one Gaussian (back to front), in packed fp32x2:
+// for each pixel i with u_i (accepted by the forward), recover T before the Gaussian
+// (T / (1 - alpha), reciprocal refined by one Newton step), update the colour behind it and
+// set d[v] to the 9 partials summed over the pair; pixels without u_i keep their state and add 0.
+struct PixBwd2 {
+  float2 T, g0, g1, g2, acc0, acc1, acc2, la, lc0, lc1, lc2;
 };
-__device__ __forceinline__ void pix_bwd(PixBwd& p, float4 co, float4 c, float dx, float dy, float G, float a0,
-                                        float alpha, float (&d)[9]) {
-  p.T = p.T / (1.f - alpha);
-  const float wgt = alpha * p.T;
-  d[6] += wgt * p.g0; d[7] += wgt * p.g1; d[8] += wgt * p.g2;                  // dL/dchat
-  p.acc0 = p.la * p.lc0 + (1.f - p.la) * p.acc0;
-  p.acc1 = p.la * p.lc1 + (1.f - p.la) * p.acc1;
-  p.acc2 = p.la * p.lc2 + (1.f - p.la) * p.acc2;
-  p.la = alpha; p.lc0 = c.x; p.lc1 = c.y; p.lc2 = c.z;
-  const float dLda = p.T * ((c.x - p.acc0) * p.g0 + (c.y - p.acc1) * p.g1 + (c.z - p.acc2) * p.g2);
-  if (a0 < 0.99f) {
-    d[5] += dLda * G;                                                            // dL/dw
-    const float dLdp = dLda * co.w * G;                                          // dL/dpower
-    d[0] -= dLdp * (co.x * dx + co.y * dy);                                      // dL/du
-    d[1] -= dLdp * (co.z * dy + co.y * dx);                                      // dL/dv
-    d[2] -= 0.5f * dLdp * dx * dx;                                               // dL/dconic_a
-    d[3] -= dLdp * dx * dy;                                                      // dL/dconic_b
-    d[4] -= 0.5f * dLdp * dy * dy;                                               // dL/dconic_c
-  }
+__device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float2 sel2(bool u0, bool u1, float2 a, float2 b) {
+  return make_float2(u0 ? a.x : b.x, u1 ? a.y : b.y);
+}
+__device__ __forceinline__ void pix_bwd2(PixBwd2& p, bool u0, bool u1, float4 co, float4 c, float2 dx, float dy,
+                                         float2 G, float2 a0, float2 alpha, float (&d)[9]) {
+  const float2 oma = __fadd2_rn(f2(1.f), make_float2(-alpha.x, -alpha.y));          // 1 - alpha
+  float2 r = make_float2(rcp_ftz(oma.x), rcp_ftz(oma.y));
+  r = __ffma2_rn(r, __ffma2_rn(make_float2(-oma.x, -oma.y), r, f2(1.f)), r);          // Newton step
+  const float2 Tq = __fmul2_rn(p.T, r);
+  p.T = sel2(u0, u1, Tq, p.T);
+  const float2 wgt = sel2(u0, u1, __fmul2_rn(alpha, p.T), f2(0.f));
+  const float2 d6 = __fmul2_rn(wgt, p.g0), d7 = __fmul2_rn(wgt, p.g1), d8 = __fmul2_rn(wgt, p.g2);   // dL/dchat
+  const float2 oml = __fadd2_rn(f2(1.f), make_float2(-p.la.x, -p.la.y));
+  p.acc0 = sel2(u0, u1, __ffma2_rn(p.la, p.lc0, __fmul2_rn(oml, p.acc0)), p.acc0);
+  p.acc1 = sel2(u0, u1, __ffma2_rn(p.la, p.lc1, __fmul2_rn(oml, p.acc1)), p.acc1);
+  p.acc2 = sel2(u0, u1, __ffma2_rn(p.la, p.lc2, __fmul2_rn(oml, p.acc2)), p.acc2);
+  p.la = sel2(u0, u1, alpha, p.la);
+  p.lc0 = sel2(u0, u1, f2(c.x), p.lc0); p.lc1 = sel2(u0, u1, f2(c.y), p.lc1); p.lc2 = sel2(u0, u1, f2(c.z), p.lc2);
+  float2 s3 = __fmul2_rn(__fadd2_rn(f2(c.x), make_float2(-p.acc0.x, -p.acc0.y)), p.g0);
+  s3 = __ffma2_rn(__fadd2_rn(f2(c.y), make_float2(-p.acc1.x, -p.acc1.y)), p.g1, s3);
+  s3 = __ffma2_rn(__fadd2_rn(f2(c.z), make_float2(-p.acc2.x, -p.acc2.y)), p.g2, s3);
+  // the clamped alpha (a0 >= 0.99) has no gradient with respect to w and the power
+  const float2 dLda = sel2(u0 && a0.x < 0.99f, u1 && a0.y < 0.99f, __fmul2_rn(p.T, s3), f2(0.f));
+  const float2 d5 = __fmul2_rn(dLda, G);                                              // dL/dw
+  const float2 ndp = __fmul2_rn(__fmul2_rn(dLda, f2(-co.w)), G);                     // -dL/dpower
+  const float2 d0 = __fmul2_rn(ndp, __ffma2_rn(f2(co.x), dx, f2(co.y * dy)));          // dL/du
+  const float2 d1 = __fmul2_rn(ndp, __ffma2_rn(f2(co.y), dx, f2(co.z * dy)));          // dL/dv
+  const float2 d2 = __fmul2_rn(__fmul2_rn(f2(0.5f), ndp), __fmul2_rn(dx, dx));         // dL/dconic_a
+  const float2 d3 = __fmul2_rn(__fmul2_rn(ndp, dx), f2(dy));                           // dL/dconic_b
+  const float2 d4 = __fmul2_rn(f2(0.5f * dy * dy), ndp);                               // dL/dconic_c
+  d[0] = d0.x + d0.y; d[1] = d1.x + d1.y; d[2] = d2.x + d2.y; d[3] = d3.x + d3.y; d[4] = d4.x + d4.y;
+  d[5] = d5.x + d5.y; d[6] = d6.x + d6.y; d[7] = d7.x + d7.y; d[8] = d8.x + d8.y;
 }
 
 __global__ void __launch_bounds__(kRasterThreads) k_sraster_bwd(SBwdArgs a) {
@@ -403,15 +441,15 @@ __global__ void __launch_bounds__(kRasterThreads) k_sraster_bwd(SBwdArgs a) {
   const uint2 rg = a.ranges[(size_t)l * ntiles + tile];
   const int n = rg.y > rg.x ? (int)(rg.y - rg.x) : 0;
   const size_t pix = ((size_t)l * a.cam.H + min(py, a.cam.H - 1)) * a.cam.W + px;
-  PixBwd p0{}, p1{};
+  PixBwd2 pp{};
   int last0 = 0, last1 = 0;
   if (in0) {
-    p0.T = a.outT[pix]; last0 = (int)a.last[pix];
-    p0.g0 = a.dLdC[3 * pix]; p0.g1 = a.dLdC[3 * pix + 1]; p0.g2 = a.dLdC[3 * pix + 2];
+    pp.T.x = a.outT[pix]; last0 = (int)a.last[pix];
+    pp.g0.x = a.dLdC[3 * pix]; pp.g1.x = a.dLdC[3 * pix + 1]; pp.g2.x = a.dLdC[3 * pix + 2];
   }
   if (in1) {
-    p1.T = a.outT[pix + 1]; last1 = (int)a.last[pix + 1];
-    p1.g0 = a.dLdC[3 * pix + 3]; p1.g1 = a.dLdC[3 * pix + 4]; p1.g2 = a.dLdC[3 * pix + 5];
+    pp.T.y = a.outT[pix + 1]; last1 = (int)a.last[pix + 1];
+    pp.g0.y = a.dLdC[3 * pix + 3]; pp.g1.y = a.dLdC[3 * pix + 4]; pp.g2.y = a.dLdC[3 * pix + 5];
   }
   const int lastmax = max(last0, last1);                  // Gaussians at positions >= last were not accepted
   const int lane = threadIdx.x & 31;
@@ -441,9 +479,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_sraster_bwd(SBwdArgs a) {
         const bool u0 = gpos < last0 && !(power.x > 0.f) && alpha.x >= 1.f / 255.f;
         const bool u1 = gpos < last1 && !(power.y > 0.f) && alpha.y >= 1.f / 255.f;
         if (u0 || u1) {
-          const float4 c = s_c[k];
-          if (u0) pix_bwd(p0, co, c, dx.x, dy, G.x, a0.x, alpha.x, d);
-          if (u1) pix_bwd(p1, co, c, dx.y, dy, G.y, a0.y, alpha.y, d);
+          pix_bwd2(pp, u0, u1, co, s_c[k], dx, dy, G, a0, alpha, d);
           use = true;
         }
       }
@@ -596,19 +632,23 @@ __global__ void k_sproject_bwd(const float* __restrict__ P, int64_t G, int64_t g
 static int sblocks(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); }
 
 cudaError_t launch_sproject(const float* P, int64_t G, int64_t g0, int64_t g1, const SCam& cam, ScreenBufs& b,
-                            cudaStream_t s) {
-  k_sproject<<<sblocks(g1 - g0), 256, 0, s>>>(P, G, g0, g1, cam, b.pa, b.pb, b.pc, b.rect, b.touched);
-  const int64_t n = g1 - g0;
-  const int nb = (int)((n + kScanChunk - 1) / kScanChunk);
-  k_sscan_blocks<<<std::max(nb, 1), kScanB, 0, s>>>(b.touched, n, b.bsums);
-  k_sscan_top<<<1, kScanB, 0, s>>>(b.bsums, nb, b.total);
-  k_sscan_apply<<<std::max(nb, 1), kScanB, 0, s>>>(b.touched, n, b.bsums, b.off);
+                            const LevelGeom& g, int lev0, int Lr, cudaStream_t s) {
+  cudaMemsetAsync(b.tcount, 0, sizeof(uint32_t) * (size_t)Lr * cam.TX * cam.TY, s);
+  cudaMemsetAsync(b.total, 0, sizeof(uint32_t), s);
+  k_sproject<<<sblocks(g1 - g0), 256, 0, s>>>(P, G, g0, g1, cam, b.pa, b.pb, b.pc, b.rect, b.touched, g, lev0,
+                                              b.tcount, b.total);
   return cudaGetLastError();
 }
 
 cudaError_t launch_skeys_sort(int64_t g0, int64_t g1, const LevelGeom& g, int lev0, int Lr, const SCam& cam,
                               ScreenBufs& b, int64_t npairs, int64_t Np, cudaStream_t s) {
   const int ntiles = cam.TX * cam.TY;
+  // per-Gaussian key offsets: exclusive scan of the tiles touched
+  const int64_t n = g1 - g0;
+  const int nb = (int)((n + kScanChunk - 1) / kScanChunk);
+  k_sscan_blocks<<<std::max(nb, 1), kScanB, 0, s>>>(b.touched, n, b.bsums);
+  k_sscan_top<<<1, kScanB, 0, s>>>(b.bsums, nb, b.total);
+  k_sscan_apply<<<std::max(nb, 1), kScanB, 0, s>>>(b.touched, n, b.bsums, b.off);
   cudaMemsetAsync(b.key + npairs, 0xFF, sizeof(uint64_t) * (Np - npairs), s);
   cudaMemsetAsync(b.val + npairs, 0x7F, sizeof(int64_t) * (Np - npairs), s);
   k_skeys<<<sblocks(g1 - g0), 256, 0, s>>>(g0, g1, g, lev0, ntiles, cam.TX, b.pa, b.rect, b.off, b.key, b.val);
@@ -618,14 +658,14 @@ cudaError_t launch_skeys_sort(int64_t g0, int64_t g1, const LevelGeom& g, int le
   return cudaGetLastError();
 }
 
-// ---------------------------------------------- two-level sort: counting sort by tile, then
-// a per-tile sort of (depth bits << 32 | index) in shared memory.  The 64-bit key orders a
-// tile's Gaussians by depth with ties by index (the global sort's order, reading A23).
-// Rectangles larger than kCoopArea tiles are walked by the whole warp (lanes split the tiles)
-// instead of by their own thread: the top level's Gaussians cover up to ~200 tiles at 1080p
-// and a thread walking them one returning atomic at a time was the kernel's tail.
-constexpr int kCoopArea = 16;
-
+// ---------------------------------------------- two-level sort: counting sort by tile (counts
+// from k_sproject), then a per-tile sort of (depth bits << 32 | index).  The 64-bit key orders
+// a tile's Gaussians by depth with ties by index (the global sort's order, reading A23).
+//
+// The scatter spreads the (Gaussian, tile) pairs of a warp's 32 Gaussians evenly over its
+// lanes (warp prefix sum of the rectangle areas, then each lane finds its pair's Gaussian by a
+// 5-step binary search over the prefix): a lane issues ceil(pairs / 32) returning atomics in
+// sequence instead of its own rectangle's area (up to ~200 tiles for the top level at 1080p).
 template <typename F>
 __device__ __forceinline__ void for_each_tile(int64_t g0, int64_t g1, const int4* __restrict__ rect, F&& f) {
   const int lane = threadIdx.x & 31;
@@ -634,41 +674,30 @@ __device__ __forceinline__ void for_each_tile(int64_t g0, int64_t g1, const int4
     const int64_t j = base + lane;
     int4 r = make_int4(0, 0, 0, 0);
     if (j < g1) r = rect[j];
-    const int w = max(r.y - r.x, 0), h = max(r.w - r.z, 0), area = w * h;
-    const bool coop = area > kCoopArea;
-    if (!coop)
-      for (int ty = r.z; ty < r.w; ++ty)
-        for (int tx = r.x; tx < r.y; ++tx) f(j, tx, ty);
-    uint32_t m = __ballot_sync(0xffffffffu, coop);
-    while (m) {
-      const int src = __ffs(m) - 1;
-      m &= m - 1;
+    const int w = max(r.y - r.x, 0), area = w * max(r.w - r.z, 0);
+    int inc = area;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const int exc = inc - area, tot = __shfl_sync(0xffffffffu, inc, 31);
+    for (int p0 = 0; p0 < tot; p0 += 32) {
+      const int p = p0 + lane;
+      int src = 0;                                  // the last lane with exc <= p (its area > 0)
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int e = __shfl_sync(0xffffffffu, exc, src + step);
+        if (e <= p) src += step;
+      }
       const int64_t js = __shfl_sync(0xffffffffu, j, src);
       const int rx = __shfl_sync(0xffffffffu, r.x, src), rz = __shfl_sync(0xffffffffu, r.z, src);
-      const int ws = __shfl_sync(0xffffffffu, w, src), as = __shfl_sync(0xffffffffu, area, src);
-      // lane i walks tiles i, i + 32, ... of the row-major rectangle (one division per rectangle)
-      const int d32 = 32 / ws, r32 = 32 - d32 * ws;
-      int ty = lane / ws, tx = lane - ty * ws;
-      for (int i = lane; i < as; i += 32) {
-        f(js, rx + tx, rz + ty);
-        tx += r32; ty += d32;
-        if (tx >= ws) { tx -= ws; ++ty; }
+      const int ws = __shfl_sync(0xffffffffu, w, src), es = __shfl_sync(0xffffffffu, exc, src);
+      if (p < tot) {
+        const int i = p - es, ty = i / ws;
+        f(js, rx + (i - ty * ws), rz + ty);
       }
     }
-  }
-}
-
-// a per-tile sort of (depth bits << 32 | index).  The 64-bit key orders a tile's Gaussians by
-// depth with ties by index (the global sort's order, reading A23).
-__global__ void k_tile_count(int64_t g0, int64_t g1, LevelGeom g, int lev0, int ntiles_img, int TX,
-                             const int4* __restrict__ rect, uint32_t* count) {
-  // (fire-and-forget reductions: a thread walks its own rectangle)
-  for (int64_t j = g0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < g1; j += (int64_t)gridDim.x * blockDim.x) {
-    const int4 r = rect[j];
-    if (!(r.x < r.y && r.z < r.w)) continue;
-    const int l = level_of_gaussian(g, j) - lev0;
-    for (int ty = r.z; ty < r.w; ++ty)
-      for (int tx = r.x; tx < r.y; ++tx) atomicAdd(count + (size_t)l * ntiles_img + ty * TX + tx, 1u);
   }
 }
 
@@ -822,10 +851,9 @@ cudaError_t launch_tile_sort(int64_t g0, int64_t g1, const LevelGeom& g, int lev
   const int nt = Lr * ntiles;
   // (per call: the attribute belongs to the current device)
   cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kTileSortMax * sizeof(uint64_t)));
-  cudaMemsetAsync(tcount, 0, sizeof(uint32_t) * nt, s);
   cudaMemsetAsync(tcursor, 0, sizeof(uint32_t) * nt, s);
   cudaMemsetAsync(big, 0, 3 * sizeof(uint32_t), s);
-  k_tile_count<<<sblocks(g1 - g0), 256, 0, s>>>(g0, g1, g, lev0, ntiles, cam.TX, b.rect, tcount);
+  // tcount was filled by k_sproject
   launch_scan_u32(tcount, nt, tbsums, ttotal, tstart, s);
   k_tile_scatter<<<sblocks(g1 - g0), 256, 0, s>>>(g0, g1, g, lev0, ntiles, cam.TX, b.pa, b.rect, tstart, tcursor, b.key);
   int dev = 0, sms = 148;
