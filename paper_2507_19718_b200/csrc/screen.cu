@@ -13,8 +13,8 @@
 //   two-level sort: per-(level, tile) key counts (k_sproject) -> scan -> k_tile_scatter (keys
 //                depth bits << 32 | index into their tile's segment; a warp's (Gaussian, tile)
 //                pairs spread evenly over its lanes) -> k_tile_sort_warp (segment ranges; bitonic sort
-//                in registers, one warp per tile of <= 256 keys) -> k_tile_sort_warp16 (<= 512)
-//                -> k_tile_sort (shared memory, <= 8192); the global path (k_skeys, bitonic
+//                in registers, one warp per tile of <= 256 keys) -> k_tile_sort (shared
+//                memory, <= 8192); the global path (k_skeys, bitonic
 //                sort of (tile, depth) keys, k_sranges) only when a tile holds more
 //   k_sraster    one CTA per (tile, level), 16 x 16 threads, batches of 256 Gaussians staged in
 //                shared memory, front-to-back compositing; C, final T, last contributor; for
@@ -57,7 +57,17 @@ __device__ __forceinline__ int clamp_tile(float f, int n) {
 }
 
 // --------------------------------------------------------------------------- projection
-// pa = (u, v, depth, w), pb = (conic a, b, c, -), pc = (chat, ok), rect = (x0, x1, y0, y1)
+// true when some pixel centre of tile (tx, ty) lies within distance R of (u, v) (NaN: true)
+__device__ __forceinline__ bool tile_hit(float u, float v, float R, int tx, int ty) {
+  const float x0 = tx * kTile + 0.5f, y0 = ty * kTile + 0.5f;
+  const float dx = fmaxf(fmaxf(x0 - u, u - (x0 + (kTile - 1))), 0.f);
+  const float dy = fmaxf(fmaxf(y0 - v, v - (y0 + (kTile - 1))), 0.f);
+  return !(dx * dx + dy * dy > R * R);
+}
+
+// pa = (u, v, depth, w), pb = (conic a, b, c, R), pc = (chat, ok), rect = (x0, x1, y0, y1);
+// R bounds the pixels where alpha >= 1/255 can hold: only tiles of the rectangle with a pixel
+// centre within R of (u, v) get a key
 // It also counts the keys of every (level, tile) (count, fire-and-forget reductions over the
 // rectangle) and their total (npairs, one warp-aggregated atomic).
 __global__ void k_sproject(const float* __restrict__ P, int64_t G, int64_t g0, int64_t g1, SCam cam,
@@ -102,24 +112,45 @@ __global__ void k_sproject(const float* __restrict__ P, int64_t G, int64_t g0, i
           const float rad = ceilf(3.f * sqrtf(lam));
           r.x = clamp_tile(floorf((u - rad) / kTile), cam.TX); r.y = clamp_tile(floorf((u + rad + 15.f) / kTile), cam.TX);
           r.z = clamp_tile(floorf((v - rad) / kTile), cam.TY); r.w = clamp_tile(floorf((v + rad + 15.f) / kTile), cam.TY);
+          const float w = 1.f / (1.f + expf(-P[P_O * G + j]));
+          // opacity-aware tightening: alpha >= 1/255 needs d^T Sigma2^-1 d <= 2 ln(255 w), whose
+          // bounding box has half-extents sqrt(2 ln(255 w) Sigma2_xx), ..._yy (widened by 0.1 % +
+          // 0.01 px for fp32); tiles of the 3-sigma rectangle outside it hold no pixel the
+          // raster could accept, so dropping them changes no image (A23)
+          const float r2 = 2.f * logf(255.f * w);
+          float Ra = INFINITY;                           // radius of a circle around that ellipse
+          if (r2 < 0.f) {
+            r.y = r.x;                                   // w < 1/255: no pixel reaches the floor
+          } else {
+            const float hx = fmaf(sqrtf(r2 * A), 1.001f, 0.01f), hy = fmaf(sqrtf(r2 * Cc), 1.001f, 0.01f);
+            if (isfinite(hx) && isfinite(hy)) {
+              Ra = fmaf(sqrtf(r2 * lam), 1.001f, 0.01f);
+              r.x = max(r.x, clamp_tile(floorf((u - hx - 0.5f) / kTile), cam.TX));
+              r.y = min(r.y, clamp_tile(floorf((u + hx - 0.5f) / kTile) + 1.f, cam.TX));
+              r.z = max(r.z, clamp_tile(floorf((v - hy - 0.5f) / kTile), cam.TY));
+              r.w = min(r.w, clamp_tile(floorf((v + hy - 0.5f) / kTile) + 1.f, cam.TY));
+            }
+          }
           if (r.x < r.y && r.z < r.w) {
-            n = (uint32_t)((r.y - r.x) * (r.w - r.z));
+            n = 1;
             const float id = 1.f / det;
-            const float w = 1.f / (1.f + expf(-P[P_O * G + j]));
             a = make_float4(u, v, tz, w);
-            b = make_float4(Cc * id, -B * id, A * id, 0.f);
+            b = make_float4(Cc * id, -B * id, A * id, Ra);
             c = make_float4(fmaxf(P[P_C * G + j], 0.f), fmaxf(P[(P_C + 1) * G + j], 0.f), fmaxf(P[(P_C + 2) * G + j], 0.f), 1.f);
           }
         }
       }
     }
-    pa[j] = a; pb[j] = b; pc[j] = c; rect[j] = r;
-    touched[j - g0] = n;
     if (n) {
+      // keys only for the tiles within the circle (the same test in the scatter and k_skeys)
+      n = 0;
       const size_t lbase = (size_t)(level_of_gaussian(lg, j) - lev0) * ntiles_img;
       for (int ty = r.z; ty < r.w; ++ty)
-        for (int tx = r.x; tx < r.y; ++tx) atomicAdd(count + lbase + ty * cam.TX + tx, 1u);
+        for (int tx = r.x; tx < r.y; ++tx)
+          if (tile_hit(a.x, a.y, b.w, tx, ty)) { atomicAdd(count + lbase + ty * cam.TX + tx, 1u); ++n; }
     }
+    pa[j] = a; pb[j] = b; pc[j] = c; rect[j] = r;
+    touched[j - g0] = n;
     const uint32_t m = __activemask();
     const uint32_t tot = __reduce_add_sync(m, n);
     if ((threadIdx.x & 31) == __ffs(m) - 1 && tot) atomicAdd(npairs, tot);
@@ -190,7 +221,7 @@ void launch_scan_u32(const uint32_t* in, int64_t n, uint32_t* bsums, uint32_t* t
 
 // --------------------------------------------------------------------------- keys / ranges
 __global__ void k_skeys(int64_t g0, int64_t g1, LevelGeom g, int lev0, int ntiles_img, int TX,
-                        const float4* __restrict__ pa, const int4* __restrict__ rect,
+                        const float4* __restrict__ pa, const float4* __restrict__ pb, const int4* __restrict__ rect,
                         const uint32_t* __restrict__ off, uint64_t* key, int64_t* val) {
   for (int64_t j = g0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < g1; j += (int64_t)gridDim.x * blockDim.x) {
     const int4 r = rect[j];
@@ -200,6 +231,7 @@ __global__ void k_skeys(int64_t g0, int64_t g1, LevelGeom g, int lev0, int ntile
     uint32_t o = off[j - g0];
     for (int ty = r.z; ty < r.w; ++ty)
       for (int tx = r.x; tx < r.y; ++tx) {
+        if (!tile_hit(pa[j].x, pa[j].y, pb[j].w, tx, ty)) continue;
         const uint64_t tile = (uint64_t)l * ntiles_img + (uint64_t)ty * TX + tx;
         key[o] = (tile << 32) | dbits;
         val[o] = j;
@@ -651,7 +683,7 @@ cudaError_t launch_skeys_sort(int64_t g0, int64_t g1, const LevelGeom& g, int le
   k_sscan_apply<<<std::max(nb, 1), kScanB, 0, s>>>(b.touched, n, b.bsums, b.off);
   cudaMemsetAsync(b.key + npairs, 0xFF, sizeof(uint64_t) * (Np - npairs), s);
   cudaMemsetAsync(b.val + npairs, 0x7F, sizeof(int64_t) * (Np - npairs), s);
-  k_skeys<<<sblocks(g1 - g0), 256, 0, s>>>(g0, g1, g, lev0, ntiles, cam.TX, b.pa, b.rect, b.off, b.key, b.val);
+  k_skeys<<<sblocks(g1 - g0), 256, 0, s>>>(g0, g1, g, lev0, ntiles, cam.TX, b.pa, b.pb, b.rect, b.off, b.key, b.val);
   if (Np > 1) launch_sort_kv(b.key, b.val, Np, s);
   cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * (size_t)Lr * ntiles, s);
   if (npairs > 0) k_sranges<<<sblocks(npairs), 256, 0, s>>>(b.key, npairs, b.ranges);
@@ -702,11 +734,14 @@ __device__ __forceinline__ void for_each_tile(int64_t g0, int64_t g1, const int4
 }
 
 __global__ void k_tile_scatter(int64_t g0, int64_t g1, LevelGeom g, int lev0, int ntiles_img, int TX,
-                               const float4* __restrict__ pa, const int4* __restrict__ rect,
+                               const float4* __restrict__ pa, const float4* __restrict__ pb,
+                               const int4* __restrict__ rect,
                                const uint32_t* __restrict__ start, uint32_t* cursor, uint64_t* key) {
   for_each_tile(g0, g1, rect, [&](int64_t j, int tx, int ty) {
+    const float4 p = pa[j];
+    if (!tile_hit(p.x, p.y, pb[j].w, tx, ty)) return;
     const int l = level_of_gaussian(g, j) - lev0;
-    const uint64_t k = ((uint64_t)__float_as_uint(pa[j].z) << 32) | (uint64_t)(uint32_t)j;
+    const uint64_t k = ((uint64_t)__float_as_uint(p.z) << 32) | (uint64_t)(uint32_t)j;
     const size_t t = (size_t)l * ntiles_img + ty * TX + tx;
     key[start[t] + atomicAdd(cursor + t, 1u)] = k;
   });
@@ -787,35 +822,14 @@ __global__ void k_tile_sort_warp(const uint32_t* __restrict__ start, const uint3
   }
 }
 
-// one warp per listed tile of (kWarpSortMax, 2 kWarpSortMax] keys (16 per lane: a kernel of
-// its own, so that the register budget of the 16-key sort does not limit the first pass);
-// larger tiles go on to list2 (big[2]) for the shared-memory kernel
-__global__ void k_tile_sort_warp16(const uint32_t* __restrict__ start, const uint32_t* __restrict__ total, int nt,
-                                   const uint32_t* __restrict__ list, uint64_t* key, int64_t* val, uint32_t* list2,
-                                   uint32_t* big) {
-  const int lane = threadIdx.x & 31;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t nlist = big[1];
-  for (uint32_t li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; li < nlist; li += nw) {
-    const int t = (int)list[li];
-    const uint32_t b0 = start[t], b1 = t + 1 < nt ? start[t + 1] : *total;
-    const int n = (int)(b1 - b0);
-    if (n > 2 * kWarpSortMax) {
-      if (lane == 0) list2[atomicAdd(big + 2, 1u)] = (uint32_t)t;
-      continue;
-    }
-    warp_sort_tile<16>(key, val, b0, n, lane);
-  }
-}
-
-// one CTA per listed (level, tile) of more than 2 kWarpSortMax keys: bitonic sort of its segment
+// one CTA per listed (level, tile) of more than kWarpSortMax keys: bitonic sort of its segment
 // in shared memory; segments over kTileSortMax flag big[0] (the host then falls back to the
 // global sort)
 __global__ void __launch_bounds__(1024) k_tile_sort(const uint32_t* __restrict__ start, const uint32_t* __restrict__ total,
                                                     int nt, const uint32_t* __restrict__ list, uint64_t* key,
                                                     int64_t* val, uint32_t* big) {
   extern __shared__ uint64_t sk[];
-  const uint32_t nlist = big[2];
+  const uint32_t nlist = big[1];
   for (uint32_t li = blockIdx.x; li < nlist; li += gridDim.x) {
     const int t = (int)list[li];
     const uint32_t b0 = start[t], b1 = t + 1 < nt ? start[t + 1] : *total;
@@ -855,15 +869,14 @@ cudaError_t launch_tile_sort(int64_t g0, int64_t g1, const LevelGeom& g, int lev
   cudaMemsetAsync(big, 0, 3 * sizeof(uint32_t), s);
   // tcount was filled by k_sproject
   launch_scan_u32(tcount, nt, tbsums, ttotal, tstart, s);
-  k_tile_scatter<<<sblocks(g1 - g0), 256, 0, s>>>(g0, g1, g, lev0, ntiles, cam.TX, b.pa, b.rect, tstart, tcursor, b.key);
+  k_tile_scatter<<<sblocks(g1 - g0), 256, 0, s>>>(g0, g1, g, lev0, ntiles, cam.TX, b.pa, b.pb, b.rect, tstart, tcursor, b.key);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // tcount / tcursor are free after the scatter: they hold the tile lists of the later passes
+  // tcount is free after the scan: it holds the list of tiles for the shared-memory sort
   k_tile_sort_warp<<<(int)std::max<int64_t>((nt + 7) / 8, 1), 256, 0, s>>>(tstart, ttotal, nt, b.key, b.val, b.ranges,
                                                                           tcount, big);
-  k_tile_sort_warp16<<<sms, 256, 0, s>>>(tstart, ttotal, nt, tcount, b.key, b.val, tcursor, big);
-  k_tile_sort<<<sms * 2, 1024, kTileSortMax * sizeof(uint64_t), s>>>(tstart, ttotal, nt, tcursor, b.key, b.val, big);
+  k_tile_sort<<<sms * 2, 1024, kTileSortMax * sizeof(uint64_t), s>>>(tstart, ttotal, nt, tcount, b.key, b.val, big);
   return cudaGetLastError();
 }
 
