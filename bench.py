@@ -488,6 +488,12 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_screen:
         screen = screen_bench(gsc, cfg, dev, local, args)
 
+    # ---- the general path (rotated anisotropic Gaussians, scale LR > 0: the non-lite backward
+    # with the Cholesky test and the full dA chain), same frames and frame call, rank 0 at N = 1
+    general = None
+    if rank == 0 and world == 1 and not args.no_general:
+        general = general_bench(gsc, cfg, dev, local, args, frames, S, outq, stream, frame_call)
+
     # ---- row A8: dense all-pairs lookups, tensor cores vs the CUDA-core evaluator (rank 0, N = 1)
     dense = None
     if rank == 0 and world == 1 and not args.no_dense:
@@ -526,6 +532,8 @@ def run_ours(args):
         }
         if alt:
             line["alt"] = alt
+        if general:
+            line["general"] = general
         if screen:
             line["screen"] = screen
         if dense:
@@ -536,6 +544,60 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def general_bench(gsc, cfg, dev, local, args, frames, S, outq, stream, frame_call):
+    """The headline frame on the general path: every level of the config's cache rotated and
+    anisotropic (random quaternions, log-scales + U(-0.4, 0.2)), scale LR 0.0125 (the paper's
+    -CO variant), so the non-lite kernels run (9-FMA Cholesky test, the 12-term dA
+    backward, the scale group in AdamW); same frames, frame call, deferred step and CUDA
+    graphs as the headline; device time with CUDA events."""
+    import torch
+    c = workload.CONFIGS[cfg]
+    pos, alb = workload.init_cloud(cfg)
+    hp = gsc.default_hparams(lr=[1.16e-3, 1e-3, 1.25e-2, 1.25e-2, 1.5e-1], cell_edge_scale=args.cell_scale)
+    cache = gsc.GSCache(c["counts"], torch.from_numpy(pos).to(dev), torch.from_numpy(alb).to(dev),
+                        seed=cfg, device=local, hparams=hp)
+    r = np.random.default_rng(31)
+    for l in range(len(c["counts"])):
+        Pl = cache.params_rows(l)
+        Pl[:, 3:7] = r.normal(size=(len(Pl), 4)).astype(np.float32)
+        Pl[:, 10:13] += r.uniform(-0.4, 0.2, (len(Pl), 3)).astype(np.float32)
+        cache.set_params_rows(l, Pl)
+    cache.reserve(S, S)
+    if not args.no_defer:
+        cache.set_deferred_step(True)
+    R = len(frames)
+    with torch.cuda.stream(stream):
+        for w in range(max(args.warmup, 1)):
+            frame_call(cache, *frames[w % R], outq, stream)
+    stream.synchronize()
+    graphs = []
+    if not args.no_graph:
+        for f in range(R):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                frame_call(cache, *frames[f], outq, stream)
+            graphs.append(g)
+    n = max(5, args.steps)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        for w in range(args.warmup):
+            (graphs[w % R].replay() if graphs else frame_call(cache, *frames[w % R], outq, stream))
+        e0.record(stream)
+        for k in range(n):
+            (graphs[k % R].replay() if graphs else frame_call(cache, *frames[k % R], outq, stream))
+        cache.flush(stream)
+        e1.record(stream)
+    stream.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    st = cache._stats
+    nv = int(st.n_valid)
+    return {"ms_per_step": ms, "value": nv / (ms * 1e-3), "unit": "samples/s",
+            "pairs_per_sample": int(st.n_pairs) / max(nv, 1),
+            "candidates_per_sample": int(st.n_candidates) / max(nv, 1),
+            "cuda_graph": bool(graphs),
+            "workload": c["name"] + ", every level rotated + anisotropic, scale LR 0.0125 (non-lite path)"}
 
 
 def screen_bench(gsc, cfg, dev, local, args, W=1920, H=1080):
@@ -749,6 +811,8 @@ def main():
     ap.add_argument("--no-alt", action="store_true", help="N > 1: do not also time the other mode")
     ap.add_argument("--no-screen", action="store_true", help="skip the screen-space (f1) timing")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense tensor-core (A8) timing")
+    ap.add_argument("--no-general", action="store_true",
+                    help="skip the general-path (anisotropic, scale LR > 0) timing")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

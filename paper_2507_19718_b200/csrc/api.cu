@@ -1487,23 +1487,28 @@ static gc_status screen_render(gc_cache c, const gc_camera* cam, int lev0, int l
     if (!b.htbig) CK(cudaHostAlloc((void**)&b.htbig, sizeof(uint32_t), cudaHostAllocDefault));
     b.tile_cap = nt + 1;
   }
-  CK(launch_sproject(c->P, G, g0, g1, sc, b, c->geom, lev0, Lr, s));
-  CK(cudaMemcpyAsync(b.htotal, b.total, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  const int64_t npairs = *b.htotal;
-  const int64_t Np = sort_kv_size(std::max<int64_t>(npairs, 1));
-  if (b.kv_cap < Np) {
+  // One host round trip per call: the keys are scattered into the capacity of the previous
+  // calls; the number of keys and the over-8192-keys-per-tile flag come back together after
+  // the sorts.  Over capacity (the first call, a camera that sees more): grow, run again.
+  int64_t npairs = 0;
+  for (int attempt = 0;; ++attempt) {
+    CK(launch_sproject(c->P, G, g0, g1, sc, b, c->geom, lev0, Lr, s));
+    // counting sort by tile + per-tile register / shared-memory sorts; the global bitonic sort
+    // only when a tile holds more than 8192 Gaussians
+    CK(launch_tile_sort(g0, g1, c->geom, lev0, Lr, sc, b, b.tcount, b.tcursor, b.tstart, b.tbsums, b.ttotal, b.tbig, s));
+    CK(cudaMemcpyAsync(b.htbig, b.tbig, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(b.htotal, b.total, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    npairs = *b.htotal;
+    if (npairs <= b.kv_cap) break;
+    if (attempt > 0) return fail(GC_ERR_STATE, "screen keys over capacity after growing");
+    const int64_t Np = sort_kv_size(npairs + npairs / 4 + 1024);
     if (b.key) cudaFree(b.key);
     if (b.val) cudaFree(b.val);
     CK(dalloc(&b.key, Np)); CK(dalloc(&b.val, Np));
     b.kv_cap = Np;
   }
-  // counting sort by tile + per-tile shared-memory sort; the global bitonic sort only when a
-  // tile holds more than 8192 Gaussians
-  CK(launch_tile_sort(g0, g1, c->geom, lev0, Lr, sc, b, b.tcount, b.tcursor, b.tstart, b.tbsums, b.ttotal, b.tbig, s));
-  CK(cudaMemcpyAsync(b.htbig, b.tbig, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  if (*b.htbig) CK(launch_skeys_sort(g0, g1, c->geom, lev0, Lr, sc, b, npairs, Np, s));
+  if (*b.htbig) CK(launch_skeys_sort(g0, g1, c->geom, lev0, Lr, sc, b, npairs, b.kv_cap, s));
   SLossArgs la{};
   if (loss) { la = *loss; la.dLdC = b.dLdC; }
   CK(launch_sraster(sc, Lr, b, out, outT ? outT : b.T, b.last, loss ? &la : nullptr, s));

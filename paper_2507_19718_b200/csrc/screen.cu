@@ -304,6 +304,9 @@ __device__ __forceinline__ void pix_alpha(float2 uv, float4 co, float2 nfx, floa
 }
 
 constexpr int kRasterThreads = kTileThreads / 2;
+#ifndef GSC_BWD_DIRECT
+#define GSC_BWD_DIRECT 24
+#endif
 
 __global__ void __launch_bounds__(kRasterThreads) k_sraster(SRasterArgs a) {
   __shared__ float2 s_uv[kRasterThreads];
@@ -516,7 +519,22 @@ __global__ void __launch_bounds__(kRasterThreads) k_sraster_bwd(SBwdArgs a) {
         }
       }
       // per-warp reduction, then one vector red per warp (skipped when no lane contributed)
-      if (__any_sync(0xffffffffu, use)) {
+      const uint32_t users = __ballot_sync(0xffffffffu, use);
+#if GSC_BWD_DIRECT
+      // up to 24 contributing lanes: each adds its own 9 partials with 3 vector reductions
+      // (fewer instructions than the tree; the L2 takes one vector add per lane).  A/B of the
+      // threshold at 1080p: tree only 744 us per fit, 8: 739, 16: 726, 24: 722, 32 (never the
+      // tree): 1080 -- full warps of same-address vector adds serialise in the L2.
+      if (users && __popc(users) <= GSC_BWD_DIRECT) {
+        if (use) {
+          float* gj = a.g2d + 12 * s_j[k];
+          red_add_v4(gj, d[0], d[1], d[2], d[3]);
+          red_add_v4(gj + 4, d[4], d[5], d[6], d[7]);
+          atomicAdd(gj + 8, d[8]);
+        }
+      } else
+#endif
+      if (users) {
         // transposing reduction of d[0..7] (each level keeps half of the values and sends the
         // other half: 4 + 2 + 1 shuffles, then 2 plain levels) -- lane L ends with the sum of
         // value 4 bit4(L) + 2 bit3(L) + bit2(L) when L % 4 == 0; d[8] by a plain tree.
@@ -736,14 +754,15 @@ __device__ __forceinline__ void for_each_tile(int64_t g0, int64_t g1, const int4
 __global__ void k_tile_scatter(int64_t g0, int64_t g1, LevelGeom g, int lev0, int ntiles_img, int TX,
                                const float4* __restrict__ pa, const float4* __restrict__ pb,
                                const int4* __restrict__ rect,
-                               const uint32_t* __restrict__ start, uint32_t* cursor, uint64_t* key) {
+                               const uint32_t* __restrict__ start, uint32_t* cursor, uint64_t* key, uint32_t cap) {
   for_each_tile(g0, g1, rect, [&](int64_t j, int tx, int ty) {
     const float4 p = pa[j];
     if (!tile_hit(p.x, p.y, pb[j].w, tx, ty)) return;
     const int l = level_of_gaussian(g, j) - lev0;
     const uint64_t k = ((uint64_t)__float_as_uint(p.z) << 32) | (uint64_t)(uint32_t)j;
     const size_t t = (size_t)l * ntiles_img + ty * TX + tx;
-    key[start[t] + atomicAdd(cursor + t, 1u)] = k;
+    const uint32_t pos = start[t] + atomicAdd(cursor + t, 1u);
+    if (pos < cap) key[pos] = k;                  // (over capacity: the caller grows and re-runs)
   });
 }
 
@@ -800,7 +819,9 @@ constexpr int kTileSortMax = 8192;           // items per tile sorted in shared 
 // one warp per (level, tile): ranges, then the register sort; larger tiles are appended to
 // `list` (list_n = big[1]) for the shared-memory kernel
 __global__ void k_tile_sort_warp(const uint32_t* __restrict__ start, const uint32_t* __restrict__ total, int nt,
-                                 uint64_t* key, int64_t* val, uint2* ranges, uint32_t* list, uint32_t* big) {
+                                 uint64_t* key, int64_t* val, uint2* ranges, uint32_t* list, uint32_t* big,
+                                 uint32_t cap) {
+  if (*total > cap) return;                               // keys over capacity: re-run after growing
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nt; t += nw) {
@@ -827,8 +848,9 @@ __global__ void k_tile_sort_warp(const uint32_t* __restrict__ start, const uint3
 // global sort)
 __global__ void __launch_bounds__(1024) k_tile_sort(const uint32_t* __restrict__ start, const uint32_t* __restrict__ total,
                                                     int nt, const uint32_t* __restrict__ list, uint64_t* key,
-                                                    int64_t* val, uint32_t* big) {
+                                                    int64_t* val, uint32_t* big, uint32_t cap) {
   extern __shared__ uint64_t sk[];
+  if (*total > cap) return;
   const uint32_t nlist = big[1];
   for (uint32_t li = blockIdx.x; li < nlist; li += gridDim.x) {
     const int t = (int)list[li];
@@ -869,14 +891,16 @@ cudaError_t launch_tile_sort(int64_t g0, int64_t g1, const LevelGeom& g, int lev
   cudaMemsetAsync(big, 0, 3 * sizeof(uint32_t), s);
   // tcount was filled by k_sproject
   launch_scan_u32(tcount, nt, tbsums, ttotal, tstart, s);
-  k_tile_scatter<<<sblocks(g1 - g0), 256, 0, s>>>(g0, g1, g, lev0, ntiles, cam.TX, b.pa, b.pb, b.rect, tstart, tcursor, b.key);
+  const uint32_t cap = (uint32_t)std::min<int64_t>(b.kv_cap, 0xFFFFFFFFll);
+  k_tile_scatter<<<sblocks(g1 - g0), 256, 0, s>>>(g0, g1, g, lev0, ntiles, cam.TX, b.pa, b.pb, b.rect, tstart, tcursor,
+                                                  b.key, cap);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // tcount is free after the scan: it holds the list of tiles for the shared-memory sort
   k_tile_sort_warp<<<(int)std::max<int64_t>((nt + 7) / 8, 1), 256, 0, s>>>(tstart, ttotal, nt, b.key, b.val, b.ranges,
-                                                                          tcount, big);
-  k_tile_sort<<<sms * 2, 1024, kTileSortMax * sizeof(uint64_t), s>>>(tstart, ttotal, nt, tcount, b.key, b.val, big);
+                                                                          tcount, big, cap);
+  k_tile_sort<<<sms * 2, 1024, kTileSortMax * sizeof(uint64_t), s>>>(tstart, ttotal, nt, tcount, b.key, b.val, big, cap);
   return cudaGetLastError();
 }
 

@@ -5,6 +5,6 @@ timeout 2400 python -m pytest tests -q -m gpu > gpurun_out/gpu_tests.log 2>&1; e
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 600 --csv \
-  --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --clock-window 0 \
+  --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-general --clock-window 0 \
   > gpurun_out/ncu_list.log 2>&1; echo list rc=$?
 tail -n 3 gpurun_out/gpu_tests.log
