@@ -52,9 +52,9 @@ def scene(gsc, counts, seed=3, max_opacity=0.8):
     return c
 
 
-def check_image(y, yo, amb, what, max_amb=1e-3):
+def check_image(y, yo, amb, what, max_amb=1e-3, rel=1e-5):
     y, yo = np.asarray(y, np.float64), np.asarray(yo, np.float64)
-    tol = 1e-5 * np.abs(yo) + 1e-6 * max(np.abs(yo).max(), 1e-30)
+    tol = rel * np.abs(yo) + 1e-6 * max(np.abs(yo).max(), 1e-30)
     bad = (np.abs(y - yo) > tol).any(axis=-1)
     assert not np.any(bad & (amb == 0)), (what, np.argwhere(bad & (amb == 0))[:5],
                                           np.abs(y - yo)[bad & (amb == 0)][:5])
@@ -151,3 +151,44 @@ def test_fit_image_loss_curve_and_world_consistency(gsc):
     yo, lv, _ = oracle.query(c.goff, P1, x.astype(np.float64), ln, grids=c.grids())
     from test_gpu_parity import check_forward
     check_forward(y, yo, P1, c.goff, x, lv, what="world lookups after screen fit")
+
+
+def test_render_crowded_tiles_capacity_growth(gsc):
+    """The sort paths of the render: 10,000 of 12,000 Gaussians clustered into one tile at the
+    far camera (> 8192 keys in a tile: the global-sort fallback), spread over tiles of
+    257..8192 keys at the near camera (the shared-memory tile sort), opacities from 0.001
+    (< 1/255: culled by the opacity-aware bounds) to 0.999 (clamped alpha); the near camera
+    needs more keys than the far one (the grow-and-rerun path), and the far camera rendered
+    again reproduces its first image bit for bit.  Bar: a pixel of the cluster composites up
+    to ~500 layers (T falls to the 1e-4 stop through factors 1 - alpha with alpha <= 0.05), and
+    each layer's fp32 product T (1 - alpha) and accumulation c alpha T round once: the forward
+    error grows like n u (u = 2^-24), 500 u = 3e-5 relative, so this test uses 1e-4 instead of
+    the 1e-5 of shallow stacks (A23)."""
+    r = np.random.default_rng(21)
+    pos = np.concatenate([r.normal(0, 0.004, (10000, 3)), r.uniform(-0.5, 0.5, (2000, 3))]).astype(np.float32)
+    alb = r.uniform(0.1, 1.0, (12000, 3)).astype(np.float32)
+    counts = [12000, 300]
+    c = gsc.GSCache(counts, cuda(pos), cuda(alb), seed=4)
+    for l in range(2):
+        Pl = c.params_rows(l)
+        Pl[:, 3:7] = r.normal(size=(len(Pl), 4)).astype(np.float32)
+        Pl[:, 10:13] = np.log(r.uniform(0.002, 0.02, (len(Pl), 3))).astype(np.float32)
+        w = np.concatenate([r.uniform(0.001, 0.003, len(Pl) // 10), r.uniform(0.005, 0.05, len(Pl) - len(Pl) // 10 - 5),
+                            np.full(5, 0.999)])
+        r.shuffle(w)
+        Pl[:, 13] = np.log(w / (1 - w)).astype(np.float32)
+        c.set_params_rows(l, Pl)
+    P = rows(c)
+    far, ofar = camera(gsc, 48, 40, 40.0, dist=6.0)
+    near, onear = camera(gsc, 96, 80, 5000.0, dist=3.0)
+    first = c.render(far).cpu().numpy()
+    img = c.render(near).cpu().numpy()
+    again = c.render(far).cpu().numpy()
+    np.testing.assert_array_equal(again, first)
+    for l in range(2):
+        Pl = P[c.goff[l]:c.goff[l + 1]]
+        for y, oc, what in ((first[l], ofar, "far"), (img[l], onear, "near")):
+            yo, _, amb = oracle.render(Pl, oc)
+            assert (yo > 0).mean() > 0.01, what
+            check_image(y.reshape(-1, 3), yo.reshape(-1, 3), amb.reshape(-1), f"crowded {what} level {l}",
+                        rel=1e-4)
