@@ -488,7 +488,16 @@ __global__ void __launch_bounds__(kRasterThreads) k_sraster_bwd(SBwdArgs a) {
   }
   const int lastmax = max(last0, last1);                  // Gaussians at positions >= last were not accepted
   const int lane = threadIdx.x & 31;
-  for (int b1 = n; b1 > 0; b1 -= kRasterThreads) {
+  // the warp skips Gaussians behind all of its pixels' last contributors, the block starts at
+  // the last contributor of its tile (the forward stopped there: T fell below 1e-4)
+  const int warpmax = __reduce_max_sync(0xffffffffu, lastmax);
+  __shared__ int s_wmax[kRasterThreads / 32];
+  if (lane == 0) s_wmax[threadIdx.x >> 5] = warpmax;
+  __syncthreads();
+  int nb = 0;
+#pragma unroll
+  for (int w = 0; w < kRasterThreads / 32; ++w) nb = max(nb, s_wmax[w]);
+  for (int b1 = min(n, nb); b1 > 0; b1 -= kRasterThreads) {
     const int b0 = max(0, b1 - kRasterThreads);
     __syncthreads();
     const int q = b0 + threadIdx.x;
@@ -502,7 +511,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_sraster_bwd(SBwdArgs a) {
       s_j[threadIdx.x] = j;
     }
     __syncthreads();
-    for (int k = b1 - b0 - 1; k >= 0; --k) {
+    for (int k = min(b1, warpmax) - b0 - 1; k >= 0; --k) {
       const int gpos = b0 + k;
       float d[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       bool use = false;
