@@ -35,10 +35,14 @@ def main(csv_path, rep_path, tag):
     per = collections.defaultdict(lambda: [0, 0.0, 0.0])
     # everything launched before the first step's k_keys belongs to gc_create; torch fills too
     first = min((i for (i, name) in L if "k_keys" in name), default=0)
+    # the bench's later legs (screen space f1, general path, dense A8) launch some of the same
+    # kernels (k_stats, k_adamw, the culling rebuild): stop at the first launch of those legs
+    last = min((i for (i, name) in L if any(k in name for k in ("k_sproject", "k_dense_tc", "k_sraster"))),
+               default=1 << 60)
     frame = ("k_keys", "k_scan", "k_scatter", "k_fwdbwd", "k_query", "k_stats", "k_step_scalars", "k_adamw",
              "k_record_cull", "k_cull_emit")
     for (i, name), m in L.items():
-        if i < first or name.startswith("at::") or "at::" in name:
+        if i < first or i >= last or name.startswith("at::") or "at::" in name:
             continue
         if not any(name.endswith(f) for f in frame):     # the bench's screen (f1) / dense (A8) legs
             continue
