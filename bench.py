@@ -646,7 +646,9 @@ def dense_bench(gsc, dev, local, args, S=262_144):
     anisotropic level 0; 262,144 lookups per call.  gc_query_dense (tcgen05 3xTF32 Q + CUDA-core
     exp/colour epilogue) vs gc_query (the packed fp32x2 CUDA-core evaluator over the one-cell
     culling lists), device time per call with CUDA events; pairs = sum over lookups of the
-    level's Gaussian count; MUFU roofline = one ex2 per pair at 148 x 16 / clk."""
+    level's Gaussian count; MUFU roofline = one ex2 per pair at 148 x 16 / clk (the fit step:
+    two, forward and backward).  Also the fit step on the same case: gc_fit_dense (forward +
+    Eq. 4 + the two-product tensor-core backward + AdamW + rebuild) vs gc_fit."""
     import torch
     counts = workload.CONFIGS[1]["counts"]
     pos, alb = workload.init_cloud(1)
@@ -665,6 +667,25 @@ def dense_bench(gsc, dev, local, args, S=262_144):
     pairs = float(sum(np.sum(lv == l) * counts[l] for l in range(len(counts))))
     s = torch.cuda.current_stream(dev)
     res = {}
+    # the dense fit step on the same case: gc_fit_dense (tensor-core forward + backward) vs gc_fit
+    # (CUDA-core evaluators over the one-cell lists), each with AdamW and the list rebuild
+    r2 = np.random.default_rng(12)
+    rgbd = torch.from_numpy(r2.uniform(0, 2, (S, 3)).astype(np.float32)).to(dev)
+    c.reserve(S, S)
+    for name, fn in (("fit_tensor_core", lambda: c.fit_dense(xd, ld, rgbd)),
+                     ("fit_cuda_core", lambda: c.fit(xd, ld, rgbd))):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n = max(3, args.steps // 4)
+        e0.record(s)
+        for _ in range(n):
+            fn()
+        e1.record(s)
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / n
+        res[name] = {"ms": ms, "pairs_per_s": pairs / (ms * 1e-3)}
     for name, fn in (("tensor_core", lambda: c.query_dense(xd, ld, out=out)),
                      ("cuda_core", lambda: c.query(xd, ld, out=out))):
         for _ in range(3):
@@ -680,10 +701,11 @@ def dense_bench(gsc, dev, local, args, S=262_144):
         ms = e0.elapsed_time(e1) / n
         res[name] = {"ms": ms, "pairs_per_s": pairs / (ms * 1e-3)}
     mufu = 148 * 16 * 1.965e9
-    for v in res.values():
-        v["mufu_frac"] = v["pairs_per_s"] / mufu
+    for k, v in res.items():
+        v["mufu_frac"] = v["pairs_per_s"] / mufu * (2 if k.startswith("fit") else 1)   # fit: 2 ex2 per pair
     res.update(workload="cfg1 levels, tau = inf, rotated anisotropic level 0", lookups=S, pairs=pairs,
                speedup=res["cuda_core"]["ms"] / res["tensor_core"]["ms"],
+               fit_speedup=res["fit_cuda_core"]["ms"] / res["fit_tensor_core"]["ms"],
                mufu_peak="148 SM x 16 ex2/clk x 1.965 GHz (one ex2 per pair)")
     return res
 

@@ -244,6 +244,23 @@ gc_status gc_fit_image(gc_cache c, const gc_camera* cam, const float* target, co
 gc_status gc_query_dense(gc_cache c, const float* pos, const int32_t* path_len, int level, int64_t S,
                          float* out_rgb, gc_stream stream);
 
+/* Dense fit step on the tensor cores (row A8's backward): one gc_fit step -- Eq. 4 over the
+ * frame's samples (loss_grad_mode as gc_fit), the gradient of every parameter, the
+ * shared AdamW step with the Eq. 5 schedule, the records / culling lists rebuilt -- with the
+ * level mixture evaluated densely over EVERY Gaussian of the sample's level (as
+ * gc_query_dense; the same values as gc_fit with tau = INFINITY, or with the mask Q <= tau^2).
+ * Forward: gc_query_dense's product.  Backward, per (tile-grid cell item, 128-Gaussian chunk):
+ * Q^T as a product in the transposed orientation (tcgen05.mma kind::tf32, 3xTF32), e = e^{-Q/2}
+ * written back to tensor memory, then E^T times [g_i phi_i, g_i] (the per-sample loss gradient
+ * times the monomial features) as a second product with the A operand in TMEM: the sums over
+ * the item's samples of dL/dkappa and dL/dv for each Gaussian, chained to the 12 coefficient
+ * gradients (dmu, dA, dv) of gc_fit.  pos [S][3], path_len [S] or NULL (then `level`),
+ * rgb [S][3]: DEVICE buffers; samples with non-finite position or colour, or n < 1, are dropped
+ * (counted out of k_l).  Single GPU (GC_ERR_UNSUPPORTED with a communicator); not graph-
+ * capturable; completes a pending deferred step first.  stats as gc_fit. */
+gc_status gc_fit_dense(gc_cache c, const float* pos, const int32_t* path_len, int level, const float* rgb, int64_t S,
+                       gc_stream stream, gc_fit_stats* stats);
+
 /* Deferred optimizer step (enable != 0; off by default).  gc_fit / gc_fit_query then leave
  * their optimizer half -- the AdamW step with the next step's evaluation records, and the
  * culling-list rebuild -- pending, and the next call on the handle launches it on an internal

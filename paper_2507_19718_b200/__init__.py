@@ -29,7 +29,7 @@ EXPORTS = ["gc_default_hparams", "gc_create", "gc_destroy", "gc_reserve", "gc_fi
            "gc_nccl_unique_id", "gc_set_comm", "gc_debug_enable_grads", "gc_debug_grads",
            "gc_debug_coef_grads", "gc_list_generation", "gc_set_level_weights", "gc_level_plan",
            "gc_comm_info", "gc_adam_state", "gc_set_adam_state", "gc_alg1_terminate", "gc_reinit",
-           "gc_render", "gc_fit_image", "gc_query_dense", "gc_slab_plan",
+           "gc_render", "gc_fit_image", "gc_query_dense", "gc_fit_dense", "gc_slab_plan",
            "gc_debug_cull", "gc_debug_levels", "gc_profile_enable", "gc_profile_read",
            "gc_last_error", "gc_status_string"]
 
@@ -135,6 +135,7 @@ def lib():
             "gc_reinit": (i32, [vp, vp, vp, vp, C.c_uint64]),
             "gc_render": (i32, [vp, vp, i32, vp, vp, vp]),
             "gc_query_dense": (i32, [vp, vp, vp, i32, i64, vp, vp]),
+            "gc_fit_dense": (i32, [vp, vp, vp, i32, vp, i64, vp, vp]),
             "gc_slab_plan": (i32, [i32, vp, vp, vp, vp, vp, i32, vp]),
             "gc_fit_image": (i32, [vp, vp, vp, vp, vp, vp]),
             "gc_alg1_terminate": (i32, [vp, vp, i32, C.c_float, vp, vp, C.c_float, i64, vp, vp, vp, vp]),
@@ -344,6 +345,15 @@ class GSCache:
         _check(lib().gc_query(self.h, p.ptr, n.ptr, int(level), S, o.ptr, _stream_ptr(stream)))
         self._keep_q = (p, n, o)
         return out
+
+    def fit_dense(self, pos, path_len, rgb, level=-1, stream=None, stats=None):
+        """gc_fit_dense (dense fit step on the tensor cores, row A8's backward) on CUDA tensors:
+        pos [S][3] f32, path_len [S] i32 (or None with `level`), rgb [S][3] f32."""
+        S = int(pos.shape[0])
+        st = stats if stats is not None else self._stats
+        _check(lib().gc_fit_dense(self.h, pos.data_ptr(), path_len.data_ptr() if path_len is not None else None,
+                                  int(level), rgb.data_ptr(), S, _stream_ptr(stream), C.addressof(st)))
+        return st
 
     def query_dense(self, pos, path_len=None, level=-1, out=None, stream=None):
         """gc_query_dense (tensor-core dense lookups, row A8) on CUDA tensors."""

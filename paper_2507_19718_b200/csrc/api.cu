@@ -70,12 +70,13 @@ struct Scratch {
   // host-input staging, two sets: a call's upload may start while the previous call still
   // reads the other set (see stage_inputs)
   float *in_pos[2] = {nullptr, nullptr}, *in_rgb[2] = {nullptr, nullptr}, *out = nullptr;
+  float *y = nullptr, *g = nullptr;       // gc_fit_dense: per-sample y_hat and dL/dy_hat [cap][3]
   int32_t* in_len[2] = {nullptr, nullptr};
   int set = 0;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   bool free_rec[2] = {false, false};
   void release() {
-    void* ps[] = {kr, bin, cell_count, cell_start, totals, tiles, work, out,
+    void* ps[] = {kr, bin, cell_count, cell_start, totals, tiles, work, out, y, g,
                   in_pos[0], in_pos[1], in_rgb[0], in_rgb[1], in_len[0], in_len[1]};
     for (void* p : ps) if (p) cudaFree(p);
     for (cudaEvent_t e : {ev_copied[0], ev_copied[1], ev_free[0], ev_free[1]}) if (e) cudaEventDestroy(e);
@@ -1592,6 +1593,64 @@ gc_status gc_query_dense(gc_cache c, const float* pos, const int32_t* path_len, 
   const float tau = c->hp.cutoff_sigma;
   da.tau2 = tau * tau;
   launch_dense_tc(da, c->dense_grid, s, &c->prof);
+  CK(cudaGetLastError());
+  return GC_OK;
+}
+
+// ------------------------------------------------------------ dense fit on the tensor cores (A8)
+gc_status gc_fit_dense(gc_cache c, const float* pos, const int32_t* path_len, int level, const float* rgb, int64_t S,
+                       gc_stream stream, gc_fit_stats* stats) {
+  NvtxRange nvtx_("gc_fit_dense");
+  if (!c) return fail(GC_ERR_ARG, "NULL handle");
+  if (S < 0 || S >= ((int64_t)1 << 31)) return fail(GC_ERR_ARG, "S out of range");
+  if (S > 0 && (!pos || !rgb)) return fail(GC_ERR_ARG, "NULL pointer");
+  if (!path_len && (level < 0 || level >= c->L)) return fail(GC_ERR_ARG, "level %d not in [0, %d)", level, c->L);
+  if (c->comm) return fail(GC_ERR_UNSUPPORTED, "gc_fit_dense is single-GPU");
+  if (S > 0 && (!is_device_ptr(pos) || !is_device_ptr(rgb) || (path_len && !is_device_ptr(path_len))))
+    return fail(GC_ERR_ARG, "gc_fit_dense takes device buffers");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->device));
+  if (gc_status e = check_sticky(c)) return e;
+  if (capturing(s)) return fail(GC_ERR_STATE, "gc_fit_dense is not graph-capturable");
+  if (gc_status e = flush_pending(c, s)) return e;
+  if (gc_status e = ensure_scratch(c, c->dns, std::max<int64_t>(S, 1), false, s, c->dNC)) return e;
+  if (gc_status e = csr_guard(c, s)) return e;
+  Scratch& D = c->dns;
+  if (!D.y) { CK(dalloc(&D.y, 3 * D.cap)); CK(dalloc(&D.g, 3 * D.cap)); }
+  if (!c->dense_grid) c->dense_grid = dense_tc_grid();
+  const int fixed = path_len ? -1 : level;
+  if (S > 0) {
+    // forward: y_hat of every sample (gc_query_dense's product), caller order
+    IngestBufs b{D.kr, D.cell_count, D.bin, c->dNC};
+    CK(cudaMemsetAsync(D.y, 0, sizeof(float) * 3 * S, s));
+    launch_keys_query(pos, path_len, fixed, S, c->dgeom, b, D.y, s, &c->prof);
+    launch_scan(D.cell_count, c->dNC * kRep, 128, D.tiles, D.totals, D.cell_start, nullptr, D.work, c->dgeom, s, &c->prof);
+    launch_scatter(pos, nullptr, S, D.cell_start, b, s, &c->prof);
+    DenseArgs da;
+    da.work = D.work; da.n_work = D.totals + 1; da.bin = D.bin; da.rec = c->rec;
+    for (int l = 0; l <= kMaxL; ++l) da.goff[l] = c->geom.goff[l];
+    da.ref = c->dref; da.out = D.y;
+    const float tau = c->hp.cutoff_sigma;
+    da.tau2 = tau * tau;
+    launch_dense_tc(da, c->dense_grid, s, &c->prof);
+    // Eq. 4 per sample: dL/dy_hat and the per-level loss sums / counts
+    launch_dense_loss(pos, path_len, fixed, c->L, rgb, D.y, S, c->hp.hdr_eps, c->hp.loss_grad_mode, D.g, c->partial,
+                      s, &c->prof);
+  }
+  launch_stats(c->partial, c->geom, S, c->lvl, true, c->st, c->hp, c->L, c->dstats, s, &c->prof);
+  if (S > 0) {
+    DenseBwdArgs ba;
+    ba.work = D.work; ba.n_work = D.totals + 1; ba.bin = D.bin; ba.rec = c->rec;
+    for (int l = 0; l <= kMaxL; ++l) ba.goff[l] = c->geom.goff[l];
+    ba.ref = c->dref; ba.g = D.g; ba.grad = c->grad;
+    const float tau = c->hp.cutoff_sigma;
+    ba.tau2 = tau * tau;
+    launch_dense_bwd(ba, s, &c->prof);
+  }
+  launch_adamw(c->G, c->P, c->M, c->V, c->grad, cull_bufs(c), c->dbg_on ? c->dbg : nullptr, c->st, c->hp, c->geom,
+               reinterpret_cast<unsigned long long*>(&c->dstats->nonfinite_grads), s, &c->prof);
+  if (gc_status e = rebuild_csr(c, s, false)) return e;
+  if (gc_status e = emit_stats(c, stats, s)) return e;
   CK(cudaGetLastError());
   return GC_OK;
 }

@@ -17,6 +17,7 @@
 // padded second MMA.  MUFU (one ex2 per pair) is the binding unit.
 #include "common.cuh"
 #include "kernels.h"
+#include "stats.cuh"
 
 namespace gsc {
 
@@ -221,6 +222,322 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_dense_tc(DenseArgs a) {
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+}
+
+// --------------------------------------------------------------------------------------------
+// Dense fit (row A8 backward, gc_fit_dense): the gradient of Eq. 4 through the all-pairs
+// evaluator as two chained tensor-core products per (work item, 128-Gaussian chunk).
+//
+//   MMA 1   Q^T (128 Gaussians x 128 samples) = kappa (A, smem) . phi^T (B, smem)   [3xTF32]
+//   epi 1   thread j (a Gaussian, its TMEM lane): e_ji = 2^(-Q/2 log2 e) [Q <= tau^2], split
+//           into TF32 hi / lo and written back to tensor memory (tcgen05.st): E^T in TMEM
+//   MMA 2   D2 (128 Gaussians x 48) = E^T (A, TMEM) . W (B, smem)                    [3xTF32]
+//           with W[i][10 c + f] = g_ic phi_if and W[i][30 + c] = g_ic per sample i (built once
+//           per item; g = dL/dy_hat from the forward pass): the sums over the item's samples
+//           D2[j][10 c + f] = sum_i e_ji g_ic phi_if and D2[j][30 + c] = sum_i e_ji g_ic = dL/dv_jc
+//   epi 2   thread j: dL/dkappa_jf = -1/2 sum_c v_jc D2[j][10 c + f], then the chain to the 12
+//           coefficient gradients of the world-space fit (dmu, dA as a symmetric matrix, dv) with
+//           mu' = mu - (cell centre), one red.global.add.v4 x 3 per (Gaussian, item part).
+// No per-Gaussian reduction across threads: the sum over samples is the second product's K.
+// Tensor memory: [0, 128) Q^T then E_hi, [128, 256) E_lo, [256, 304) D2 -> 512 columns, 1 CTA/SM.
+struct DenseBwdSmem {
+  float a[4][128 * 8];                                       // kappa tiles  [kstep * 2 + (hi, lo)]
+  float b[4][128 * 8];                                       // phi tiles
+  float w[32][48 * 8];                                       // W tiles [kstep * 2 + (hi, lo)], 16 ksteps
+  uint64_t bar;
+  uint32_t tbase;
+};
+constexpr int kBwdN = 48;
+
+// A = U^T U, mu' = mu - centre, v, and kappa of one Gaussian from its evaluation record
+__device__ __forceinline__ void rec_kappa(const float4* __restrict__ rec, int64_t g, float xr, float yr, float zr,
+                                          float (&kap)[10], float (&A)[6], float (&m)[3], float (&v)[3]) {
+  const float4 r0 = __ldg(rec + 3 * g), r1 = __ldg(rec + 3 * g + 1), r2 = __ldg(rec + 3 * g + 2);
+  const float u00 = r0.x, u01 = r0.y, u02 = r0.z, u11 = r0.w, u12 = r1.x, u22 = r1.y;
+  A[0] = u00 * u00; A[3] = u00 * u01; A[4] = u00 * u02;                 // A00 A11 A22 A01 A02 A12
+  A[1] = fmaf(u11, u11, u01 * u01); A[5] = fmaf(u11, u12, u01 * u02);
+  A[2] = fmaf(u22, u22, fmaf(u12, u12, u02 * u02));
+  m[0] = r1.z - xr; m[1] = r1.w - yr; m[2] = r2.x - zr;
+  const float t0 = fmaf(A[4], m[2], fmaf(A[3], m[1], A[0] * m[0]));
+  const float t1 = fmaf(A[5], m[2], fmaf(A[1], m[1], A[3] * m[0]));
+  const float t2 = fmaf(A[2], m[2], fmaf(A[5], m[1], A[4] * m[0]));
+  kap[0] = A[0]; kap[1] = A[1]; kap[2] = A[2]; kap[3] = 2.f * A[3]; kap[4] = 2.f * A[4]; kap[5] = 2.f * A[5];
+  kap[6] = -2.f * t0; kap[7] = -2.f * t1; kap[8] = -2.f * t2;
+  kap[9] = fmaf(m[2], t2, fmaf(m[1], t1, m[0] * t0));
+  v[0] = r2.y; v[1] = r2.z; v[2] = r2.w;
+}
+
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t phase) {
+  asm volatile("{\n\t.reg .pred P1;\n\tBWAIT:\n\t"
+               "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+               "@!P1 bra BWAIT;\n\t}\n" ::"r"(smem_addr(bar)), "r"(phase));
+}
+
+#define GSC_TMEM_X32_REGS(q) "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), \
+  "=r"(q[7]), "=r"(q[8]), "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]), "=r"(q[13]), "=r"(q[14]), "=r"(q[15]),   \
+  "=r"(q[16]), "=r"(q[17]), "=r"(q[18]), "=r"(q[19]), "=r"(q[20]), "=r"(q[21]), "=r"(q[22]), "=r"(q[23]),            \
+  "=r"(q[24]), "=r"(q[25]), "=r"(q[26]), "=r"(q[27]), "=r"(q[28]), "=r"(q[29]), "=r"(q[30]), "=r"(q[31])
+#define GSC_TMEM_X32_IN(q) "r"(q[0]), "r"(q[1]), "r"(q[2]), "r"(q[3]), "r"(q[4]), "r"(q[5]), "r"(q[6]), "r"(q[7]), \
+  "r"(q[8]), "r"(q[9]), "r"(q[10]), "r"(q[11]), "r"(q[12]), "r"(q[13]), "r"(q[14]), "r"(q[15]), "r"(q[16]),          \
+  "r"(q[17]), "r"(q[18]), "r"(q[19]), "r"(q[20]), "r"(q[21]), "r"(q[22]), "r"(q[23]), "r"(q[24]), "r"(q[25]),        \
+  "r"(q[26]), "r"(q[27]), "r"(q[28]), "r"(q[29]), "r"(q[30]), "r"(q[31])
+#define GSC_X32_LIST "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}"
+#define GSC_X32_LIST1 "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32}"
+
+__device__ __forceinline__ void tmem_ld32(uint32_t ta, uint32_t (&q)[32]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 " GSC_X32_LIST ", [%32];" : GSC_TMEM_X32_REGS(q) : "r"(ta));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t ta, const uint32_t (&q)[32]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], " GSC_X32_LIST1 ";" ::"r"(ta), GSC_TMEM_X32_IN(q));
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) k_dense_bwd(DenseBwdArgs a) {
+  extern __shared__ __align__(1024) unsigned char dsm_raw[];
+  DenseBwdSmem& sm = *reinterpret_cast<DenseBwdSmem*>(dsm_raw);
+  const int t = threadIdx.x, warp = t >> 5;
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sm.bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(&sm.tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = sm.tbase;
+  const uint32_t lane_base = tmem + ((uint32_t)(32 * warp) << 16);
+  const uint32_t id1 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  const uint32_t id2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kBwdN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  uint32_t phase = 0;
+  const uint32_t n_work = a.n_work[0];
+  const uint32_t nsplit = n_work ? max(1u, min(16u, (2u * gridDim.x + n_work - 1) / n_work)) : 1u;
+  for (uint32_t task = blockIdx.x; task < n_work * nsplit; task += gridDim.x) {
+    const uint32_t it = task / nsplit, part = task % nsplit;
+    const WorkItem wi = a.work[it];
+    const int l = wi.level;
+    const int loc = wi.cell - a.ref.coff[l], dx = a.ref.dx[l], dy = a.ref.dy[l];
+    const int cx = loc % dx, tq = loc / dx, cy = tq % dy, cz = tq / dy;
+    const float xr = fmaf((float)cx + 0.5f, a.ref.edge[l][0], a.ref.org[l][0]);
+    const float yr = fmaf((float)cy + 0.5f, a.ref.edge[l][1], a.ref.org[l][1]);
+    const float zr = fmaf((float)cz + 0.5f, a.ref.edge[l][2], a.ref.org[l][2]);
+    // ---- per item: phi^T (B of MMA 1) and W (B of MMA 2), sample t of the item
+    float phi[10] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float g[3] = {0.f, 0.f, 0.f};
+    if (t < wi.count) {
+      const float4 p = __ldcs(a.bin + 2 * (int64_t)(wi.start + t));
+      const float x = p.x - xr, y = p.y - yr, z = p.z - zr;
+      const uint32_t idx = __float_as_uint(p.w);
+      phi[0] = x * x; phi[1] = y * y; phi[2] = z * z; phi[3] = x * y; phi[4] = x * z; phi[5] = y * z;
+      phi[6] = x; phi[7] = y; phi[8] = z; phi[9] = 1.f;
+      g[0] = a.g[3 * (size_t)idx]; g[1] = a.g[3 * (size_t)idx + 1]; g[2] = a.g[3 * (size_t)idx + 2];
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int s = k >> 3;
+      put_split(sm.b[2 * s], sm.b[2 * s + 1], t, k & 7, k < 10 ? phi[k] : 0.f);
+    }
+    {
+      const int ks = t >> 3, kk = t & 7;                     // W column k = t: K step t / 8
+      float* wh = sm.w[2 * ks];
+      float* wl = sm.w[2 * ks + 1];
+#pragma unroll
+      for (int n = 0; n < kBwdN; ++n) {
+        const float val = n < 30 ? g[n / 10] * phi[n % 10] : (n < 33 ? g[n - 30] : 0.f);
+        put_split(wh, wl, n, kk, val);
+      }
+    }
+    const int64_t nch = (a.goff[l + 1] - a.goff[l] + 127) / 128;
+    const int64_t g0 = a.goff[l] + 128 * ((nch * part) / nsplit);
+    const int64_t g1 = min(a.goff[l + 1], a.goff[l] + 128 * ((nch * (part + 1)) / nsplit));
+    for (int64_t cb = g0; cb < g1; cb += 128) {
+      const int nj = (int)(g1 - cb < 128 ? g1 - cb : 128);
+      // ---- kappa (A of MMA 1), Gaussian t of the chunk; its A, mu', v stay in registers
+      float kap[10], Am[6], mu[3], v[3];
+      if (t < nj) {
+        rec_kappa(a.rec, cb + t, xr, yr, zr, kap, Am, mu, v);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 10; ++k) kap[k] = 0.f;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) Am[k] = 0.f;
+        mu[0] = mu[1] = mu[2] = 0.f; v[0] = v[1] = v[2] = 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int s = k >> 3;
+        put_split(sm.a[2 * s], sm.a[2 * s + 1], t, k & 7, k < 10 ? kap[k] : 0.f);
+      }
+      asm volatile("fence.proxy.async.shared::cta;");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncthreads();
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (t == 0) {
+        int n = 0;
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const int pa[3] = {0, 0, 1}, pb[3] = {0, 1, 0};
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            const uint64_t da = smem_desc(smem_addr(sm.a[2 * s + pa[q]]));
+            const uint64_t db = smem_desc(smem_addr(sm.b[2 * s + pb[q]]));
+            const uint32_t acc = n++ > 0;
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
+                         ::"r"(tmem), "l"(da), "l"(db), "r"(id1), "r"(acc));
+          }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                     ::"r"(smem_addr(&sm.bar)) : "memory");
+      }
+      mbar_wait_parity(&sm.bar, phase);
+      phase ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      // ---- epilogue 1: E^T row t (its TMEM lane) = masked exponentials, TF32 hi / lo
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t q[32], lo[32];
+        tmem_ld32(lane_base + (uint32_t)c0, q);
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const float Q = __uint_as_float(q[k]);
+          const float e = Q <= a.tau2 ? ex2_approx(Q * kTcNegHalfLog2e) : 0.f;
+          const float h = tf32_int(e);
+          q[k] = __float_as_uint(h);
+          lo[k] = __float_as_uint(tf32_int(e - h));
+        }
+        tmem_st32(lane_base + (uint32_t)c0, q);
+        tmem_st32(lane_base + 128u + (uint32_t)c0, lo);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncthreads();
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (t == 0) {
+        const uint32_t d2 = tmem + 256u;
+#pragma unroll 1
+        for (int s = 0; s < 16; ++s) {
+          const uint64_t bh = smem_desc(smem_addr(sm.w[2 * s])), bl = smem_desc(smem_addr(sm.w[2 * s + 1]));
+          const uint32_t ah = tmem + 8u * s, al = tmem + 128u + 8u * s;
+          const uint32_t acc0 = s > 0;
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
+                       ::"r"(d2), "r"(ah), "l"(bh), "r"(id2), "r"(acc0));
+          asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, 1;"
+                       ::"r"(d2), "r"(ah), "l"(bl), "r"(id2));
+          asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, 1;"
+                       ::"r"(d2), "r"(al), "l"(bh), "r"(id2));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                     ::"r"(smem_addr(&sm.bar)) : "memory");
+      }
+      mbar_wait_parity(&sm.bar, phase);
+      phase ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      // ---- epilogue 2: thread t = Gaussian cb + t
+      {
+        uint32_t q[32], r[16];
+        tmem_ld32(lane_base + 256u, q);
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                       "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                       "=r"(r[15])
+                     : "r"(lane_base + 288u));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        if (t < nj) {
+          float D[33];
+#pragma unroll
+          for (int k = 0; k < 32; ++k) D[k] = __uint_as_float(q[k]);
+          D[32] = __uint_as_float(r[0]);
+          float Gk[10];
+#pragma unroll
+          for (int f = 0; f < 10; ++f) Gk[f] = -0.5f * (v[0] * D[f] + v[1] * D[10 + f] + v[2] * D[20 + f]);
+          // A (symmetric, per element) and mu through kappa's dependence on A and mu' = mu - c
+          const float G00 = Gk[0] - 2.f * Gk[6] * mu[0] + Gk[9] * mu[0] * mu[0];
+          const float G11 = Gk[1] - 2.f * Gk[7] * mu[1] + Gk[9] * mu[1] * mu[1];
+          const float G22 = Gk[2] - 2.f * Gk[8] * mu[2] + Gk[9] * mu[2] * mu[2];
+          const float G01 = Gk[3] - (Gk[6] * mu[1] + Gk[7] * mu[0]) + Gk[9] * mu[0] * mu[1];
+          const float G02 = Gk[4] - (Gk[6] * mu[2] + Gk[8] * mu[0]) + Gk[9] * mu[0] * mu[2];
+          const float G12 = Gk[5] - (Gk[7] * mu[2] + Gk[8] * mu[1]) + Gk[9] * mu[1] * mu[2];
+          const float t0 = Am[0] * mu[0] + Am[3] * mu[1] + Am[4] * mu[2];
+          const float t1 = Am[3] * mu[0] + Am[1] * mu[1] + Am[5] * mu[2];
+          const float t2 = Am[4] * mu[0] + Am[5] * mu[1] + Am[2] * mu[2];
+          const float dm0 = -2.f * (Am[0] * Gk[6] + Am[3] * Gk[7] + Am[4] * Gk[8]) + 2.f * Gk[9] * t0;
+          const float dm1 = -2.f * (Am[3] * Gk[6] + Am[1] * Gk[7] + Am[5] * Gk[8]) + 2.f * Gk[9] * t1;
+          const float dm2 = -2.f * (Am[4] * Gk[6] + Am[5] * Gk[7] + Am[2] * Gk[8]) + 2.f * Gk[9] * t2;
+          float* gp = a.grad + 12 * (cb + t);
+          red_add_v4(gp, dm0, dm1, dm2, G00);
+          red_add_v4(gp + 4, G11, G22, G01, G02);
+          red_add_v4(gp + 8, G12, D[30], D[31], D[32]);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+    }
+  }
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// Eq. 4 per sample of the dense fit (caller order): y_hat from the forward pass, the target,
+// the level of the sample (dropped: non-finite position or colour, n < 1 without a fixed
+// level) -> g = dL/dy_hat (reading A10: mode 0 frozen denominator, mode 1 full quotient) and the
+// per-level loss sums / counts into the k_stats partial slots
+__global__ void k_dense_loss(const float* __restrict__ pos, const int32_t* __restrict__ len, int fixed_level, int L,
+                             const float* __restrict__ rgb, const float* __restrict__ yhat, int64_t S, float eps,
+                             int mode, float* g, double* partial) {
+  __shared__ double s_l[kMaxL], s_n[kMaxL];
+  if (threadIdx.x < kMaxL) { s_l[threadIdx.x] = 0.0; s_n[threadIdx.x] = 0.0; }
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x) {
+    float gi[3] = {0.f, 0.f, 0.f};
+    const float px = pos[3 * i], py = pos[3 * i + 1], pz = pos[3 * i + 2];
+    const float x0 = rgb[3 * i], x1 = rgb[3 * i + 1], x2 = rgb[3 * i + 2];
+    int l = fixed_level;
+    if (len) { const int n = len[i]; l = n >= 1 ? min(n, L) - 1 : -1; }
+    const bool ok = l >= 0 && isfinite(px) && isfinite(py) && isfinite(pz) && isfinite(x0) && isfinite(x1) &&
+                    isfinite(x2);
+    if (ok) {
+      double ls = 0.0;
+      const float xs[3] = {x0, x1, x2};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float y = yhat[3 * i + c], r = xs[c] - y, d = y + eps;
+        ls += (double)(r * r / (d * d));
+        gi[c] = mode == 0 ? -2.f * r / (d * d) : -2.f * r * (xs[c] + eps) / (d * d * d);
+      }
+      atomicAdd(&s_l[l], ls);
+      atomicAdd(&s_n[l], 1.0);
+    }
+    g[3 * i] = gi[0]; g[3 * i + 1] = gi[1]; g[3 * i + 2] = gi[2];
+  }
+  __syncthreads();
+  if (threadIdx.x < kMaxL && s_n[threadIdx.x] > 0.0) {
+    double* slot = partial + (size_t)(blockIdx.x % kSlots) * kPart;
+    atomicAdd(slot + threadIdx.x, s_l[threadIdx.x]);
+    atomicAdd(slot + kMaxL + threadIdx.x, s_n[threadIdx.x]);
+  }
+}
+
+constexpr size_t kBwdSmem = sizeof(DenseBwdSmem) + 1024;
+
+void launch_dense_bwd(const DenseBwdArgs& a, cudaStream_t s, Profiler* prof) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncSetAttribute(k_dense_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem);
+  ProfScope ps(prof, "dense_bwd", s);
+  k_dense_bwd<<<sms, kTcThreads, kBwdSmem, s>>>(a);            // 512 TMEM columns: one CTA per SM
+}
+
+void launch_dense_loss(const float* pos, const int32_t* len, int fixed_level, int L, const float* rgb,
+                       const float* yhat, int64_t S, float eps, int mode, float* g, double* partial, cudaStream_t s,
+                       Profiler* prof) {
+  ProfScope ps(prof, "dense_loss", s);
+  const int blocks = (int)std::min<int64_t>((S + 255) / 256, 148 * 8);
+  k_dense_loss<<<std::max(blocks, 1), 256, 0, s>>>(pos, len, fixed_level, L, rgb, yhat, S, eps, mode, g, partial);
 }
 
 // 4 CTAs per SM exactly: each holds 128 TMEM columns (512 per SM), so the dynamic shared

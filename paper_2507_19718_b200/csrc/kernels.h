@@ -172,6 +172,19 @@ struct DenseArgs {
 };
 int dense_tc_grid();
 void launch_dense_tc(const DenseArgs& a, int grid, cudaStream_t s, Profiler* prof);
+struct DenseBwdArgs {                              // gc_fit_dense's backward (k_dense_bwd)
+  const WorkItem* work; const uint32_t* n_work;
+  const float4* bin; const float4* rec;
+  int64_t goff[kMaxL + 1];
+  CellRef ref;
+  const float* g;        // [S][3] dL/dy_hat per sample (caller order), 0 for dropped samples
+  float* grad;           // [G][12] coefficient gradients (dmu, dA00 dA11 dA22 dA01 dA02 dA12, dv)
+  float tau2;
+};
+void launch_dense_bwd(const DenseBwdArgs& a, cudaStream_t s, Profiler* prof);
+void launch_dense_loss(const float* pos, const int32_t* len, int fixed_level, int L, const float* rgb,
+                       const float* yhat, int64_t S, float eps, int mode, float* g, double* partial, cudaStream_t s,
+                       Profiler* prof);
 
 // shard.cu -- level-sharded mode (gc_set_comm mode 1)
 struct RoutePlan {

@@ -57,3 +57,67 @@ def test_dense_tc_fixed_level_and_ragged(gsc):
         y = c.query_dense(cuda(xq), None, level=2).cpu().numpy()
         yo, lv, _ = oracle.query(c.goff, P, xq.astype(np.float64), None, level=2, tau=float("inf"))
         check_forward(y, yo, P, c.goff, xq, lv, tau=float("inf"), what=f"dense tc S={S}")
+
+
+def _dense_fit_case(gsc, n0, S, seed):
+    r = np.random.default_rng(seed)
+    pos = r.uniform(-0.8, 0.8, (n0, 3)).astype(np.float32)
+    alb = r.uniform(0.2, 0.9, (n0, 3)).astype(np.float32)
+    ls = np.full((n0, 3), np.log(0.3), np.float32)
+    hp = gsc.default_hparams(cutoff_sigma=float("inf"))
+    c = gsc.GSCache([n0, max(n0 // 4, 1)], pos, alb, init_log_scale=ls, seed=1, hparams=hp)
+    P0 = c.params_rows(0)
+    P0[:, 3:7] = r.normal(size=(n0, 4)).astype(np.float32)
+    P0[:, 10:13] += r.uniform(-0.3, 0.3, (n0, 3)).astype(np.float32)
+    c.set_params_rows(0, P0)
+    x = r.uniform(-0.9, 0.9, (S, 3)).astype(np.float32)
+    ln = r.integers(1, 3, S).astype(np.int32)
+    rgb = r.uniform(0, 2, (S, 3)).astype(np.float32)
+    return c, x, ln, rgb
+
+
+@pytest.mark.parametrize("n0,S", [(64, 3000), (448, 3000), (1000, 9000)])
+def test_dense_fit_gradients_match_oracle(gsc, n0, S):
+    """gc_fit_dense (row A8's backward: Q^T and E^T . [g phi, g] as two chained tcgen05
+    products, the second with its A operand in tensor memory) against the fp64 oracle's
+    loss_grad at tau = infinity: per-level loss and valid counts, and all 14 raw gradients
+    under both gradient bars (with reading A21's summation-order allowance); sizes span one
+    and several 128-Gaussian chunks, ragged work items and both levels."""
+    from test_gpu_parity import check_grads, grad_allow
+    c, x, ln, rgb = _dense_fit_case(gsc, n0, S, seed=n0)
+    x[::97] = np.nan                                          # dropped samples
+    rgb[5::89] = np.inf
+    P = rows(c)
+    c.debug_enable_grads(True)
+    c.profile_enable(True)
+    st = c.fit_dense(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    prof = c.profile_read()
+    c.profile_enable(False)
+    assert {"dense_tc", "dense_loss", "dense_bwd", "adamw"} <= set(prof) and "fwdbwd" not in prof, prof
+    keep = np.isfinite(x).all(1) & np.isfinite(rgb).all(1)
+    xo, lo_, ro_ = x[keep], ln[keep], rgb[keep]
+    ro = oracle.loss_grad(c.goff, P, xo.astype(np.float64), lo_, ro_.astype(np.float64), tau=np.inf)
+    for l in range(2):
+        assert st.count[l] == ro["count"][l]
+        assert abs(st.loss[l] - ro["loss"][l]) <= 1e-4 * ro["loss"][l]
+    g = np.concatenate([c.debug_grads_rows(l) for l in range(2)]).astype(np.float64)
+    al = grad_allow(c, P, xo, lo_, ro_, tau=np.inf, brute=True)
+    check_grads(g, ro["grad"], c.goff, f"dense fit n0={n0}", iso_levels=(1,), allow=al["raw"])
+
+
+def test_dense_fit_steps_track_world_fit(gsc):
+    """Five gc_fit_dense steps and five gc_fit steps (tau = infinity, same frames) from the same
+    cache: per-level losses agree at every step (the same method, two evaluators) and the
+    parameters stay within Adam's amplification of last-bit gradient differences."""
+    from test_gpu_parity import _close_up_to_atomic_order
+    c1, x, ln, rgb = _dense_fit_case(gsc, 300, 4000, seed=3)
+    c2, _, _, _ = _dense_fit_case(gsc, 300, 4000, seed=3)
+    for k in range(5):
+        s1 = c1.fit_dense(cuda(x), cuda(ln), cuda(rgb))
+        torch.cuda.synchronize()
+        l1 = list(s1.loss[:2])
+        s2 = c2.fit(cuda(x), cuda(ln), cuda(rgb))
+        torch.cuda.synchronize()
+        np.testing.assert_allclose(l1, list(s2.loss[:2]), rtol=1e-4)
+    _close_up_to_atomic_order(rows(c1), rows(c2))
