@@ -239,20 +239,20 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_dense_tc(DenseArgs a) {
 //           coefficient gradients of the world-space fit (dmu, dA as a symmetric matrix, dv) with
 //           mu' = mu - (cell centre), one red.global.add.v4 x 3 per (Gaussian, item part).
 // No per-Gaussian reduction across threads: the sum over samples is the second product's K.
-// Tensor memory: [0, 128) Q^T then E_hi, [128, 256) E_lo, [256, 304) D2 -> 512 columns, 1 CTA/SM.
+// Tensor memory: Q^T [0, 128), E_hi [128, 256), E_lo [256, 384), D2 [384, 432) -> 512 columns, 1 CTA/SM.
 struct DenseBwdSmem {
   float a[4][128 * 8];                                       // kappa tiles  [kstep * 2 + (hi, lo)]
   float b[4][128 * 8];                                       // phi tiles
   float w[32][48 * 8];                                       // W tiles [kstep * 2 + (hi, lo)], 16 ksteps
-  uint64_t bar;
+  uint64_t bar, bar2;                                        // MMA 1 / MMA 2 commits
   uint32_t tbase;
 };
 constexpr int kBwdN = 48;
 
 // A = U^T U, mu' = mu - centre, v, and kappa of one Gaussian from its evaluation record
-__device__ __forceinline__ void rec_kappa(const float4* __restrict__ rec, int64_t g, float xr, float yr, float zr,
+__device__ __forceinline__ void rec_kappa(const float4 (&rv)[3], float xr, float yr, float zr,
                                           float (&kap)[10], float (&A)[6], float (&m)[3], float (&v)[3]) {
-  const float4 r0 = __ldg(rec + 3 * g), r1 = __ldg(rec + 3 * g + 1), r2 = __ldg(rec + 3 * g + 2);
+  const float4 r0 = rv[0], r1 = rv[1], r2 = rv[2];
   const float u00 = r0.x, u01 = r0.y, u02 = r0.z, u11 = r0.w, u12 = r1.x, u22 = r1.y;
   A[0] = u00 * u00; A[3] = u00 * u01; A[4] = u00 * u02;                 // A00 A11 A22 A01 A02 A12
   A[1] = fmaf(u11, u11, u01 * u01); A[5] = fmaf(u11, u12, u01 * u02);
@@ -291,12 +291,95 @@ __device__ __forceinline__ void tmem_st32(uint32_t ta, const uint32_t (&q)[32]) 
   asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], " GSC_X32_LIST1 ";" ::"r"(ta), GSC_TMEM_X32_IN(q));
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1) k_dense_bwd(DenseBwdArgs a) {
+// 8 warps: two per TMEM lane quarter; thread (t, half) handles row t (sample / Gaussian) and
+// half of each row-parallel job (K steps of the phi / kappa tiles, columns of W, columns of E^T)
+constexpr int kBwdThreads = 256;
+
+// Per (item, chunk k) the threads run a software pipeline on two mbarriers: build kappa(k)
+// and issue MMA 1(k) while MMA 2(k-1) still runs, then the chain of chunk k-1 (wait MMA 2),
+// then epilogue 1(k) (wait MMA 1) and MMA 2(k).  Tensor memory: Q [0, 128), E_hi [128, 256),
+// E_lo [256, 384), D2 [384, 432).
+__device__ __forceinline__ void bwd_mma1(uint32_t tmem, const DenseBwdSmem& sm, uint32_t id1) {
+  int n = 0;
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int pa[3] = {0, 0, 1}, pb[3] = {0, 1, 0};
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const uint64_t da = smem_desc(smem_addr(sm.a[2 * s + pa[q]]));
+      const uint64_t db = smem_desc(smem_addr(sm.b[2 * s + pb[q]]));
+      const uint32_t acc = n++ > 0;
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                   "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
+                   ::"r"(tmem), "l"(da), "l"(db), "r"(id1), "r"(acc));
+    }
+  }
+}
+
+__device__ __forceinline__ void bwd_mma2(uint32_t tmem, const DenseBwdSmem& sm, uint32_t id2) {
+  const uint32_t d2 = tmem + 384u;
+#pragma unroll 1
+  for (int s = 0; s < 16; ++s) {
+    const uint64_t bh = smem_desc(smem_addr(sm.w[2 * s])), bl = smem_desc(smem_addr(sm.w[2 * s + 1]));
+    const uint32_t ah = tmem + 128u + 8u * s, al = tmem + 256u + 8u * s;
+    const uint32_t acc0 = s > 0;
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
+                 ::"r"(d2), "r"(ah), "l"(bh), "r"(id2), "r"(acc0));
+    asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, 1;" ::"r"(d2), "r"(ah), "l"(bl), "r"(id2));
+    asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, 1;" ::"r"(d2), "r"(al), "l"(bh), "r"(id2));
+  }
+}
+
+__device__ __forceinline__ void mma_commit_to(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
+               : "memory");
+}
+
+// the chain of one Gaussian: D2 row (33 values) -> 12 coefficient gradients, added into grad
+__device__ __forceinline__ void bwd_chain(uint32_t lane_base, float* gp, const float (&Am)[6], const float (&mu)[3],
+                                          const float (&v)[3], bool live) {
+  uint32_t q[32], r[16];
+  tmem_ld32(lane_base + 384u, q);
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+               : "r"(lane_base + 416u));
+  asm volatile("tcgen05.wait::ld.sync.aligned;");
+  if (!live) return;
+  float D[33];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) D[k] = __uint_as_float(q[k]);
+  D[32] = __uint_as_float(r[0]);
+  float Gk[10];
+#pragma unroll
+  for (int f = 0; f < 10; ++f) Gk[f] = -0.5f * (v[0] * D[f] + v[1] * D[10 + f] + v[2] * D[20 + f]);
+  // A (symmetric, per element) and mu through kappa's dependence on A and mu' = mu - c
+  const float G00 = Gk[0] - 2.f * Gk[6] * mu[0] + Gk[9] * mu[0] * mu[0];
+  const float G11 = Gk[1] - 2.f * Gk[7] * mu[1] + Gk[9] * mu[1] * mu[1];
+  const float G22 = Gk[2] - 2.f * Gk[8] * mu[2] + Gk[9] * mu[2] * mu[2];
+  const float G01 = Gk[3] - (Gk[6] * mu[1] + Gk[7] * mu[0]) + Gk[9] * mu[0] * mu[1];
+  const float G02 = Gk[4] - (Gk[6] * mu[2] + Gk[8] * mu[0]) + Gk[9] * mu[0] * mu[2];
+  const float G12 = Gk[5] - (Gk[7] * mu[2] + Gk[8] * mu[1]) + Gk[9] * mu[1] * mu[2];
+  const float t0 = Am[0] * mu[0] + Am[3] * mu[1] + Am[4] * mu[2];
+  const float t1 = Am[3] * mu[0] + Am[1] * mu[1] + Am[5] * mu[2];
+  const float t2 = Am[4] * mu[0] + Am[5] * mu[1] + Am[2] * mu[2];
+  const float dm0 = -2.f * (Am[0] * Gk[6] + Am[3] * Gk[7] + Am[4] * Gk[8]) + 2.f * Gk[9] * t0;
+  const float dm1 = -2.f * (Am[3] * Gk[6] + Am[1] * Gk[7] + Am[5] * Gk[8]) + 2.f * Gk[9] * t1;
+  const float dm2 = -2.f * (Am[4] * Gk[6] + Am[5] * Gk[7] + Am[2] * Gk[8]) + 2.f * Gk[9] * t2;
+  red_add_v4(gp, dm0, dm1, dm2, G00);
+  red_add_v4(gp + 4, G11, G22, G01, G02);
+  red_add_v4(gp + 8, G12, D[30], D[31], D[32]);
+}
+
+__global__ void __launch_bounds__(kBwdThreads, 1) k_dense_bwd(DenseBwdArgs a) {
   extern __shared__ __align__(1024) unsigned char dsm_raw[];
   DenseBwdSmem& sm = *reinterpret_cast<DenseBwdSmem*>(dsm_raw);
-  const int t = threadIdx.x, warp = t >> 5;
-  if (t == 0) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int t = tid & 127, half = tid >> 7;
+  if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sm.bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sm.bar2)));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   if (warp == 0) {
@@ -307,10 +390,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_dense_bwd(DenseBwdArgs a) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = sm.tbase;
-  const uint32_t lane_base = tmem + ((uint32_t)(32 * warp) << 16);
+  const uint32_t lane_base = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
   const uint32_t id1 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   const uint32_t id2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kBwdN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-  uint32_t phase = 0;
+  uint32_t ph1 = 0, ph2 = 0;
   const uint32_t n_work = a.n_work[0];
   const uint32_t nsplit = n_work ? max(1u, min(16u, (2u * gridDim.x + n_work - 1) / n_work)) : 1u;
   for (uint32_t task = blockIdx.x; task < n_work * nsplit; task += gridDim.x) {
@@ -322,81 +405,89 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_dense_bwd(DenseBwdArgs a) {
     const float xr = fmaf((float)cx + 0.5f, a.ref.edge[l][0], a.ref.org[l][0]);
     const float yr = fmaf((float)cy + 0.5f, a.ref.edge[l][1], a.ref.org[l][1]);
     const float zr = fmaf((float)cz + 0.5f, a.ref.edge[l][2], a.ref.org[l][2]);
-    // ---- per item: phi^T (B of MMA 1) and W (B of MMA 2), sample t of the item
-    float phi[10] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    float g[3] = {0.f, 0.f, 0.f};
-    if (t < wi.count) {
-      const float4 p = __ldcs(a.bin + 2 * (int64_t)(wi.start + t));
-      const float x = p.x - xr, y = p.y - yr, z = p.z - zr;
-      const uint32_t idx = __float_as_uint(p.w);
-      phi[0] = x * x; phi[1] = y * y; phi[2] = z * z; phi[3] = x * y; phi[4] = x * z; phi[5] = y * z;
-      phi[6] = x; phi[7] = y; phi[8] = z; phi[9] = 1.f;
-      g[0] = a.g[3 * (size_t)idx]; g[1] = a.g[3 * (size_t)idx + 1]; g[2] = a.g[3 * (size_t)idx + 2];
-    }
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const int s = k >> 3;
-      put_split(sm.b[2 * s], sm.b[2 * s + 1], t, k & 7, k < 10 ? phi[k] : 0.f);
-    }
+    const int64_t nch = (a.goff[l + 1] - a.goff[l] + 127) / 128;
+    const int64_t g0 = a.goff[l] + 128 * ((nch * part) / nsplit);
+    const int64_t g1 = min(a.goff[l + 1], a.goff[l] + 128 * ((nch * (part + 1)) / nsplit));
+    if (g0 >= g1) continue;
+    float4 rv[3];
+    if (g0 + t < g1)
+      for (int w = 0; w < 3; ++w) rv[w] = __ldg(a.rec + 3 * (g0 + t) + w);
+    // ---- per item: phi^T (B of MMA 1) and W (B of MMA 2), sample t of the item (the previous
+    // item's products have completed: every thread waited on their last commits)
     {
+      float phi[10] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      float g[3] = {0.f, 0.f, 0.f};
+      if (t < wi.count) {
+        const float4 p = __ldcs(a.bin + 2 * (int64_t)(wi.start + t));
+        const float x = p.x - xr, y = p.y - yr, z = p.z - zr;
+        const uint32_t idx = __float_as_uint(p.w);
+        phi[0] = x * x; phi[1] = y * y; phi[2] = z * z; phi[3] = x * y; phi[4] = x * z; phi[5] = y * z;
+        phi[6] = x; phi[7] = y; phi[8] = z; phi[9] = 1.f;
+        g[0] = a.g[3 * (size_t)idx]; g[1] = a.g[3 * (size_t)idx + 1]; g[2] = a.g[3 * (size_t)idx + 2];
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int s = k >> 3;
+        if (s != half) continue;
+        put_split(sm.b[2 * s], sm.b[2 * s + 1], t, k & 7, k < 10 ? phi[k] : 0.f);
+      }
       const int ks = t >> 3, kk = t & 7;                     // W column k = t: K step t / 8
       float* wh = sm.w[2 * ks];
       float* wl = sm.w[2 * ks + 1];
 #pragma unroll
       for (int n = 0; n < kBwdN; ++n) {
+        if ((n >= kBwdN / 2) != (half == 1)) continue;
         const float val = n < 30 ? g[n / 10] * phi[n % 10] : (n < 33 ? g[n - 30] : 0.f);
         put_split(wh, wl, n, kk, val);
       }
     }
-    const int64_t nch = (a.goff[l + 1] - a.goff[l] + 127) / 128;
-    const int64_t g0 = a.goff[l] + 128 * ((nch * part) / nsplit);
-    const int64_t g1 = min(a.goff[l + 1], a.goff[l] + 128 * ((nch * (part + 1)) / nsplit));
-    for (int64_t cb = g0; cb < g1; cb += 128) {
-      const int nj = (int)(g1 - cb < 128 ? g1 - cb : 128);
-      // ---- kappa (A of MMA 1), Gaussian t of the chunk; its A, mu', v stay in registers
-      float kap[10], Am[6], mu[3], v[3];
-      if (t < nj) {
-        rec_kappa(a.rec, cb + t, xr, yr, zr, kap, Am, mu, v);
-      } else {
+    float pAm[6], pmu[3], pv[3];                             // the previous chunk's Gaussian t
+    bool plive = false;
+    float* pgp = nullptr;
+    for (int64_t cb = g0; cb < g1 + 128; cb += 128) {
+      const bool have = cb < g1;                             // (the last round only drains)
+      const int nj = have ? (int)(g1 - cb < 128 ? g1 - cb : 128) : 0;
+      float Am[6], mu[3], v[3];
+      if (have) {
+        // ---- kappa(k) (A of MMA 1); MMA 1(k) runs beside MMA 2(k-1)
+        float kap[10];
+        if (t < nj) {
+          rec_kappa(rv, xr, yr, zr, kap, Am, mu, v);
+        } else {
 #pragma unroll
-        for (int k = 0; k < 10; ++k) kap[k] = 0.f;
+          for (int k = 0; k < 10; ++k) kap[k] = 0.f;
 #pragma unroll
-        for (int k = 0; k < 6; ++k) Am[k] = 0.f;
-        mu[0] = mu[1] = mu[2] = 0.f; v[0] = v[1] = v[2] = 0.f;
-      }
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const int s = k >> 3;
-        put_split(sm.a[2 * s], sm.a[2 * s + 1], t, k & 7, k < 10 ? kap[k] : 0.f);
-      }
-      asm volatile("fence.proxy.async.shared::cta;");
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncthreads();
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      if (t == 0) {
-        int n = 0;
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          const int pa[3] = {0, 0, 1}, pb[3] = {0, 1, 0};
-#pragma unroll
-          for (int q = 0; q < 3; ++q) {
-            const uint64_t da = smem_desc(smem_addr(sm.a[2 * s + pa[q]]));
-            const uint64_t db = smem_desc(smem_addr(sm.b[2 * s + pb[q]]));
-            const uint32_t acc = n++ > 0;
-            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
-                         ::"r"(tmem), "l"(da), "l"(db), "r"(id1), "r"(acc));
-          }
+          for (int k = 0; k < 6; ++k) Am[k] = 0.f;
+          mu[0] = mu[1] = mu[2] = 0.f; v[0] = v[1] = v[2] = 0.f;
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                     ::"r"(smem_addr(&sm.bar)) : "memory");
+        if (cb + 128 + t < g1)
+          for (int w = 0; w < 3; ++w) rv[w] = __ldg(a.rec + 3 * (cb + 128 + t) + w);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int s = k >> 3;
+          if (s != half) continue;
+          put_split(sm.a[2 * s], sm.a[2 * s + 1], t, k & 7, k < 10 ? kap[k] : 0.f);
+        }
+        asm volatile("fence.proxy.async.shared::cta;");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (tid == 0) { bwd_mma1(tmem, sm, id1); mma_commit_to(&sm.bar); }
       }
-      mbar_wait_parity(&sm.bar, phase);
-      phase ^= 1u;
+      if (cb > g0) {
+        // ---- chain of chunk k-1 (its MMA 2 done)
+        mbar_wait_parity(&sm.bar2, ph2);
+        ph2 ^= 1u;
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (half == 0) bwd_chain(lane_base, pgp, pAm, pmu, pv, plive);
+      }
+      if (!have) break;
+      // ---- epilogue 1(k): E^T row t (its TMEM lane), TF32 hi / lo, into [128, 384)
+      mbar_wait_parity(&sm.bar, ph1);
+      ph1 ^= 1u;
       asm volatile("tcgen05.fence::after_thread_sync;");
-      // ---- epilogue 1: E^T row t (its TMEM lane) = masked exponentials, TF32 hi / lo
 #pragma unroll 1
-      for (int c0 = 0; c0 < 128; c0 += 32) {
+      for (int c0 = 64 * half; c0 < 64 * half + 64; c0 += 32) {
         uint32_t q[32], lo[32];
         tmem_ld32(lane_base + (uint32_t)c0, q);
         asm volatile("tcgen05.wait::ld.sync.aligned;");
@@ -408,74 +499,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_dense_bwd(DenseBwdArgs a) {
           q[k] = __float_as_uint(h);
           lo[k] = __float_as_uint(tf32_int(e - h));
         }
-        tmem_st32(lane_base + (uint32_t)c0, q);
-        tmem_st32(lane_base + 128u + (uint32_t)c0, lo);
+        tmem_st32(lane_base + 128u + (uint32_t)c0, q);
+        tmem_st32(lane_base + 256u + (uint32_t)c0, lo);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;");
       asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncthreads();
+      __syncthreads();                                       // (also: all chains of k-1 read D2)
       asm volatile("tcgen05.fence::after_thread_sync;");
-      if (t == 0) {
-        const uint32_t d2 = tmem + 256u;
-#pragma unroll 1
-        for (int s = 0; s < 16; ++s) {
-          const uint64_t bh = smem_desc(smem_addr(sm.w[2 * s])), bl = smem_desc(smem_addr(sm.w[2 * s + 1]));
-          const uint32_t ah = tmem + 8u * s, al = tmem + 128u + 8u * s;
-          const uint32_t acc0 = s > 0;
-          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
-                       ::"r"(d2), "r"(ah), "l"(bh), "r"(id2), "r"(acc0));
-          asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, 1;"
-                       ::"r"(d2), "r"(ah), "l"(bl), "r"(id2));
-          asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, 1;"
-                       ::"r"(d2), "r"(al), "l"(bh), "r"(id2));
-        }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                     ::"r"(smem_addr(&sm.bar)) : "memory");
-      }
-      mbar_wait_parity(&sm.bar, phase);
-      phase ^= 1u;
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      // ---- epilogue 2: thread t = Gaussian cb + t
-      {
-        uint32_t q[32], r[16];
-        tmem_ld32(lane_base + 256u, q);
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                       "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                       "=r"(r[15])
-                     : "r"(lane_base + 288u));
-        asm volatile("tcgen05.wait::ld.sync.aligned;");
-        if (t < nj) {
-          float D[33];
+      if (tid == 0) { bwd_mma2(tmem, sm, id2); mma_commit_to(&sm.bar2); }
 #pragma unroll
-          for (int k = 0; k < 32; ++k) D[k] = __uint_as_float(q[k]);
-          D[32] = __uint_as_float(r[0]);
-          float Gk[10];
+      for (int k = 0; k < 6; ++k) pAm[k] = Am[k];
 #pragma unroll
-          for (int f = 0; f < 10; ++f) Gk[f] = -0.5f * (v[0] * D[f] + v[1] * D[10 + f] + v[2] * D[20 + f]);
-          // A (symmetric, per element) and mu through kappa's dependence on A and mu' = mu - c
-          const float G00 = Gk[0] - 2.f * Gk[6] * mu[0] + Gk[9] * mu[0] * mu[0];
-          const float G11 = Gk[1] - 2.f * Gk[7] * mu[1] + Gk[9] * mu[1] * mu[1];
-          const float G22 = Gk[2] - 2.f * Gk[8] * mu[2] + Gk[9] * mu[2] * mu[2];
-          const float G01 = Gk[3] - (Gk[6] * mu[1] + Gk[7] * mu[0]) + Gk[9] * mu[0] * mu[1];
-          const float G02 = Gk[4] - (Gk[6] * mu[2] + Gk[8] * mu[0]) + Gk[9] * mu[0] * mu[2];
-          const float G12 = Gk[5] - (Gk[7] * mu[2] + Gk[8] * mu[1]) + Gk[9] * mu[1] * mu[2];
-          const float t0 = Am[0] * mu[0] + Am[3] * mu[1] + Am[4] * mu[2];
-          const float t1 = Am[3] * mu[0] + Am[1] * mu[1] + Am[5] * mu[2];
-          const float t2 = Am[4] * mu[0] + Am[5] * mu[1] + Am[2] * mu[2];
-          const float dm0 = -2.f * (Am[0] * Gk[6] + Am[3] * Gk[7] + Am[4] * Gk[8]) + 2.f * Gk[9] * t0;
-          const float dm1 = -2.f * (Am[3] * Gk[6] + Am[1] * Gk[7] + Am[5] * Gk[8]) + 2.f * Gk[9] * t1;
-          const float dm2 = -2.f * (Am[4] * Gk[6] + Am[5] * Gk[7] + Am[2] * Gk[8]) + 2.f * Gk[9] * t2;
-          float* gp = a.grad + 12 * (cb + t);
-          red_add_v4(gp, dm0, dm1, dm2, G00);
-          red_add_v4(gp + 4, G11, G22, G01, G02);
-          red_add_v4(gp + 8, G12, D[30], D[31], D[32]);
-        }
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;");
+      for (int k = 0; k < 3; ++k) { pmu[k] = mu[k]; pv[k] = v[k]; }
+      plive = t < nj;
+      pgp = a.grad + 12 * (cb + t);
     }
   }
+  asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -529,7 +569,7 @@ void launch_dense_bwd(const DenseBwdArgs& a, cudaStream_t s, Profiler* prof) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaFuncSetAttribute(k_dense_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem);
   ProfScope ps(prof, "dense_bwd", s);
-  k_dense_bwd<<<sms, kTcThreads, kBwdSmem, s>>>(a);            // 512 TMEM columns: one CTA per SM
+  k_dense_bwd<<<sms, kBwdThreads, kBwdSmem, s>>>(a);           // 512 TMEM columns: one CTA per SM
 }
 
 void launch_dense_loss(const float* pos, const int32_t* len, int fixed_level, int L, const float* rgb,
