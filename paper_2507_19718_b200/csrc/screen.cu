@@ -16,7 +16,7 @@
 //                in registers, one warp per tile of <= 256 keys) -> k_tile_sort (shared
 //                memory, <= 8192); the global path (k_skeys, bitonic
 //                sort of (tile, depth) keys, k_sranges) only when a tile holds more
-//   k_sraster    one CTA per (tile, level), 16 x 16 threads, batches of 256 Gaussians staged in
+//   k_sraster    one CTA per (tile, level), 128 threads x 2 pixels, batches of 128 Gaussians staged in
 //                shared memory, front-to-back compositing; C, final T, last contributor; for
 //                gc_fit_image Eq. 4 is fused in: dL/dC and the per-level loss statistics
 //                instead of C
@@ -404,8 +404,9 @@ __global__ void __launch_bounds__(kRasterThreads) k_sraster(SRasterArgs a) {
 // Back to front over each pixel's accepted Gaussians (T recovered by division, alpha <= 0.99):
 //   dC/dchat = alpha T, dC/dalpha = T (chat - behind), alpha = min(0.99, w G), G = e^power,
 //   power = -(a dx^2 + c dy^2)/2 - b dx dy, dx = u - px, dy = v - py.
-// Per Gaussian and warp the 9 partials (du, dv, da, db, dc, dw, dchat) are summed with
-// shuffles, then one red.global.add.v4.f32 x 3 per warp into g2d[j] (12 floats).
+// Per Gaussian and warp the 9 partials (du, dv, da, db, dc, dw, dchat) go into g2d[j] (12
+// floats): with at most 24 contributing lanes each adds its own (3 vector reductions), else
+// the warp sums them with a transposing shuffle reduction first (9 reductions per warp).
 struct SBwdArgs {
   const uint2* ranges; const int64_t* val;
   const float4 *pa, *pb, *pc;
