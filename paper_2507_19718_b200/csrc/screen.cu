@@ -286,21 +286,24 @@ __device__ __forceinline__ float ex2_ftz(float x) {
   return y;
 }
 
-// power = -(a dx^2 + c dy^2)/2 - b dx dy at the pixel centres (nfx = -(px + 1/2) of the two
-// pixels, fy = py + 1/2), G = e^power, a0 = w G, alpha = min(0.99, a0) (reading A23)
-__device__ __forceinline__ void pix_alpha(float2 uv, float4 co, float2 nfx, float fy, float2& dx, float& dy,
-                                          float2& power, float2& G, float2& a0, float2& alpha) {
+// The staged conic is pre-scaled into log2 units, cs = (-a/2, -b, -c/2) log2(e), so that
+// t = power log2(e) = cs.x dx^2 + cs.z dy^2 + cs.y dx dy at the pixel centres (nfx = -(px + 1/2)
+// of the two pixels, fy = py + 1/2); G = 2^t = e^power, a0 = w G.  A pixel accepts the Gaussian
+// iff t <= 0 and a0 >= 1/255 (alpha = min(0.99, a0) >= 1/255 exactly then; reading A23).
+__device__ __forceinline__ float4 scaled_conic(float a, float b, float c, float w) {
+  return make_float4(a * (-0.5f * kL2E), b * -kL2E, c * (-0.5f * kL2E), w);
+}
+__device__ __forceinline__ void pix_alpha(float2 uv, float4 cs, float2 nfx, float fy, float2& dx, float& dy,
+                                          float2& t, float2& G, float2& a0) {
   dx = __fadd2_rn(make_float2(uv.x, uv.x), nfx);
   dy = __fadd_rn(uv.y, -fy);
-  const float cdd = __fmul_rn(__fmul_rn(co.z, dy), dy);
-  const float nbdy = -__fmul_rn(co.y, dy);
-  const float2 adx = __fmul2_rn(make_float2(co.x, co.x), dx);
-  const float2 q = __ffma2_rn(adx, dx, make_float2(cdd, cdd));
-  power = __ffma2_rn(make_float2(nbdy, nbdy), dx, __fmul2_rn(make_float2(-0.5f, -0.5f), q));
-  const float2 t = __fmul2_rn(power, make_float2(kL2E, kL2E));
+  const float cdd = __fmul_rn(__fmul_rn(cs.z, dy), dy);
+  const float bdy = __fmul_rn(cs.y, dy);
+  const float2 adx = __fmul2_rn(make_float2(cs.x, cs.x), dx);
+  t = __ffma2_rn(adx, dx, make_float2(cdd, cdd));
+  t = __ffma2_rn(make_float2(bdy, bdy), dx, t);
   G = make_float2(ex2_ftz(t.x), ex2_ftz(t.y));
-  a0 = __fmul2_rn(make_float2(co.w, co.w), G);
-  alpha = make_float2(fminf(0.99f, a0.x), fminf(0.99f, a0.y));
+  a0 = __fmul2_rn(make_float2(cs.w, cs.w), G);
 }
 
 constexpr int kRasterThreads = kTileThreads / 2;
@@ -310,7 +313,7 @@ constexpr int kRasterThreads = kTileThreads / 2;
 
 __global__ void __launch_bounds__(kRasterThreads) k_sraster(SRasterArgs a) {
   __shared__ float2 s_uv[kRasterThreads];
-  __shared__ float4 s_co[kRasterThreads];     // conic a, b, c, w
+  __shared__ float4 s_co[kRasterThreads];     // scaled conic (scaled_conic), w
   __shared__ float4 s_c[kRasterThreads];
   const int tile = blockIdx.x, l = blockIdx.y;
   const int ntiles = a.cam.TX * a.cam.TY;
@@ -332,18 +335,19 @@ __global__ void __launch_bounds__(kRasterThreads) k_sraster(SRasterArgs a) {
       const float4 p = a.pa[j];
       s_uv[threadIdx.x] = make_float2(p.x, p.y);
       const float4 b = a.pb[j];
-      s_co[threadIdx.x] = make_float4(b.x, b.y, b.z, p.w);
+      s_co[threadIdx.x] = scaled_conic(b.x, b.y, b.z, p.w);
       s_c[threadIdx.x] = a.pc[j];
     }
     __syncthreads();
     const int m = min(kRasterThreads, n - b0);
     for (int k = 0; k < m && !(done0 && done1); ++k) {
-      float2 dx, power, G, a0, alpha;
+      float2 dx, tp, G, a0;
       float dy;
-      pix_alpha(s_uv[k], s_co[k], nfx, fy, dx, dy, power, G, a0, alpha);
-      const bool acc0 = !done0 && !(power.x > 0.f) && alpha.x >= 1.f / 255.f;
-      const bool acc1 = !done1 && !(power.y > 0.f) && alpha.y >= 1.f / 255.f;
+      pix_alpha(s_uv[k], s_co[k], nfx, fy, dx, dy, tp, G, a0);
+      const bool acc0 = !done0 && !(tp.x > 0.f) && a0.x >= 1.f / 255.f;
+      const bool acc1 = !done1 && !(tp.y > 0.f) && a0.y >= 1.f / 255.f;
       if (!(acc0 || acc1)) continue;
+      const float2 alpha = make_float2(fminf(0.99f, a0.x), fminf(0.99f, a0.y));
       const float2 Tn = __fmul2_rn(T, make_float2(1.f - alpha.x, 1.f - alpha.y));
       const uint32_t cnt = (uint32_t)(b0 + k + 1);        // contributor count of this Gaussian
       const bool ap0 = acc0 && !(Tn.x < 1e-4f), ap1 = acc1 && !(Tn.y < 1e-4f);
@@ -507,7 +511,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_sraster_bwd(SBwdArgs a) {
       const float4 p = a.pa[j];
       s_uv[threadIdx.x] = make_float2(p.x, p.y);
       const float4 b = a.pb[j];
-      s_co[threadIdx.x] = make_float4(b.x, b.y, b.z, p.w);
+      s_co[threadIdx.x] = scaled_conic(b.x, b.y, b.z, p.w);
       s_c[threadIdx.x] = a.pc[j];
       s_j[threadIdx.x] = j;
     }
@@ -517,13 +521,16 @@ __global__ void __launch_bounds__(kRasterThreads) k_sraster_bwd(SBwdArgs a) {
       float d[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       bool use = false;
       if (gpos < lastmax) {
-        const float4 co = s_co[k];
-        float2 dx, power, G, a0, alpha;
+        const float4 cs = s_co[k];
+        float2 dx, tp, G, a0;
         float dy;
-        pix_alpha(s_uv[k], co, nfx, fy, dx, dy, power, G, a0, alpha);
-        const bool u0 = gpos < last0 && !(power.x > 0.f) && alpha.x >= 1.f / 255.f;
-        const bool u1 = gpos < last1 && !(power.y > 0.f) && alpha.y >= 1.f / 255.f;
+        pix_alpha(s_uv[k], cs, nfx, fy, dx, dy, tp, G, a0);
+        const bool u0 = gpos < last0 && !(tp.x > 0.f) && a0.x >= 1.f / 255.f;
+        const bool u1 = gpos < last1 && !(tp.y > 0.f) && a0.y >= 1.f / 255.f;
         if (u0 || u1) {
+          const float2 alpha = make_float2(fminf(0.99f, a0.x), fminf(0.99f, a0.y));
+          // the conic in pixel units for the gradient formulas
+          const float4 co = make_float4(cs.x * (-2.f / kL2E), cs.y * (-1.f / kL2E), cs.z * (-2.f / kL2E), cs.w);
           pix_bwd2(pp, u0, u1, co, s_c[k], dx, dy, G, a0, alpha, d);
           use = true;
         }
