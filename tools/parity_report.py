@@ -1,5 +1,5 @@
 """Measured parity of the CUDA path against the fp64 oracle (what the -m gpu tests assert,
-with the numbers written down): python tools/parity_report.py > profiles/r01_parity.json
+with the numbers written down): python tools/parity_report.py > profiles/r02_parity.json
 
 * forward: cfg1 full frame of lookups -- max relative error per element, samples with an A3
   boundary-ambiguous pair;
@@ -7,7 +7,10 @@ with the numbers written down): python tools/parity_report.py > profiles/r01_par
   (level, group);
 * culling lists and level assignment: mismatching entries (must be 0);
 * 100 fit steps: cfg1 noisy and cfg0 clean -- largest relative loss difference over the curve;
-* cfg2 full frame through the bench's frame call: sampled lookups.
+* cfg2 full frame through the bench's frame call: sampled lookups;
+* (round 2) screen-space render (all levels, 200 x 150) and fit_image gradients (fp64 central
+  differences of the oracle's Eq. 4 image loss); dense tensor-core lookups (gc_query_dense) and
+  the dense fit step's gradients (gc_fit_dense) at tau = infinity.
 """
 import json
 import os
@@ -125,6 +128,62 @@ def main():
     mx, med, nbad = fwd_err(y.cpu().numpy()[idx], yo)
     out["forward_cfg2_frame_call_sampled"] = {"points": 3000, "max_rel_err": mx, "median_rel_err": med,
                                               "points_over_1e-5": nbad}
+    # ---- round 2: screen space (f1)
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+    import test_gpu_screen as ts
+    c = ts.scene(gsc, [1500, 400, 100])
+    cam, ocam = ts.camera(gsc, 200, 150, 180.0)
+    img = c.render(cam).cpu().numpy()
+    P = rows(c)
+    errs, namb = [], 0
+    for l in range(3):
+        yo, _, amb = oracle.render(P[c.goff[l]:c.goff[l + 1]], ocam)
+        okp = (amb == 0)
+        d = np.abs(img[l] - yo)[okp] / (np.abs(yo)[okp] + 1e-6 * np.abs(yo).max())
+        errs.append(float(d.max()))
+        namb += int((amb != 0).sum())
+    out["screen_render_200x150"] = {"max_rel_err_per_level": errs, "ambiguous_pixels": namb,
+                                    "pixels": 3 * 200 * 150, "tolerance": "1e-5 |y| + 1e-6 max|y|"}
+    c, cam, ocam, P, target, valid = ts._tiny(gsc)
+    c.debug_enable_grads(True)
+    c.fit_image(cam, cuda(target.astype(np.float32)), cuda(valid))
+    torch.cuda.synchronize()
+    g = np.concatenate([c.debug_grads_rows(l) for l in range(2)]).astype(np.float64)
+    go = oracle.image_grad_fd(c.goff, P, ocam, target, valid)
+    res = {}
+    for l in range(2):
+        sl = slice(c.goff[l], c.goff[l + 1])
+        for name, cs in oracle.GROUP_SLICES.items():
+            a, b = g[sl, cs], go[sl, cs]
+            res[f"L{l}/{name}"] = float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+    out["screen_fit_image_gradients"] = {"rel_l2_err": res, "reference": "fp64 central differences of the oracle's Eq. 4 image loss"}
+    # ---- round 2: dense tensor cores (A8)
+    import test_gpu_dense_tc as td
+    c = td.dense_cache(gsc, float("inf"), True)
+    P = rows(c)
+    xq, lq = workload.query_batch(1, S=12_001, frame=6)
+    y = c.query_dense(cuda(xq), cuda(lq)).cpu().numpy()
+    yo, lv, _ = oracle.query(c.goff, P, xq.astype(np.float64), lq, tau=float("inf"))
+    mx, med, nbad = fwd_err(y[lv >= 0], yo[lv >= 0])
+    out["dense_tc_lookups_tau_inf"] = {"points": int((lv >= 0).sum()), "max_rel_err": mx, "median_rel_err": med,
+                                       "points_over_1e-5": nbad}
+    c, x, ln, rgb = td._dense_fit_case(gsc, 1000, 9000, seed=1000)
+    P = rows(c)
+    c.debug_enable_grads(True)
+    st = c.fit_dense(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    g = np.concatenate([c.debug_grads_rows(l) for l in range(2)]).astype(np.float64)
+    ro = oracle.loss_grad(c.goff, P, x.astype(np.float64), ln, rgb.astype(np.float64), tau=np.inf)
+    res = {}
+    for l in range(2):
+        sl = slice(c.goff[l], c.goff[l + 1])
+        for name, cs in oracle.GROUP_SLICES.items():
+            a, b = g[sl, cs], ro["grad"][sl, cs]
+            if name == "rotation" and l > 0:
+                continue
+            res[f"L{l}/{name}"] = float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+    out["dense_fit_gradients_tau_inf"] = {"rel_l2_err": res, "loss_rel_err": [
+        float(abs(st.loss[l] - ro["loss"][l]) / ro["loss"][l]) for l in range(2)], "tolerance": "1e-4"}
     print(json.dumps(out, indent=1))
 
 
