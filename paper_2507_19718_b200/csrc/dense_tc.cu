@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kTcThreads, 4) k_dense_tc(DenseArgs a) {
 //           coefficient gradients of the world-space fit (dmu, dA as a symmetric matrix, dv) with
 //           mu' = mu - (cell centre), one red.global.add.v4 x 3 per (Gaussian, item part).
 // No per-Gaussian reduction across threads: the sum over samples is the second product's K.
-// Tensor memory: Q^T [0, 128), E_hi [128, 256), E_lo [256, 384), D2 [384, 432) -> 512 columns, 1 CTA/SM.
+// Tensor memory: Q^T, E_hi, E_lo of one sample half (64 columns each) and D2 (48) -> 256 columns, 2 CTAs/SM.
 struct DenseBwdSmem {
   float a[4][128 * 8];                                       // kappa tiles  [kstep * 2 + (hi, lo)]
   float b[4][128 * 8];                                       // phi tiles
@@ -294,12 +294,16 @@ __device__ __forceinline__ void tmem_st32(uint32_t ta, const uint32_t (&q)[32]) 
 // 8 warps: two per TMEM lane quarter; thread (t, half) handles row t (sample / Gaussian) and
 // half of each row-parallel job (K steps of the phi / kappa tiles, columns of W, columns of E^T)
 constexpr int kBwdThreads = 256;
+// Each chunk is processed in two halves of the item's samples (64 each): MMA 1 with N = 64,
+// epilogue 1 on 64 columns, MMA 2 over K = 64 samples accumulating into D2.  Tensor memory
+// per CTA: Q^T [0, 64), E_hi [64, 128), E_lo [128, 192), D2 [192, 240) -> 256 columns, so two
+// CTAs share an SM and overlap each other's product waits.
+constexpr uint32_t kColQ = 0, kColEh = 64, kColEl = 128, kColD2 = 192, kBwdCols = 256;
 
 // Per (item, chunk k) the threads run a software pipeline on two mbarriers: build kappa(k)
-// and issue MMA 1(k) while MMA 2(k-1) still runs, then the chain of chunk k-1 (wait MMA 2),
-// then epilogue 1(k) (wait MMA 1) and MMA 2(k).  Tensor memory: Q [0, 128), E_hi [128, 256),
-// E_lo [256, 384), D2 [384, 432).
-__device__ __forceinline__ void bwd_mma1(uint32_t tmem, const DenseBwdSmem& sm, uint32_t id1) {
+// and issue MMA 1(k, 0) while MMA 2(k-1, 1) still runs, then the chain of chunk k-1 (wait
+// MMA 2), then per sample half h: epilogue 1(k, h) (wait MMA 1) and MMA 2(k, h) (+ MMA 1(k, 1)).
+__device__ __forceinline__ void bwd_mma1(uint32_t tmem, const DenseBwdSmem& sm, uint32_t id1, int h) {
   int n = 0;
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
@@ -307,7 +311,8 @@ __device__ __forceinline__ void bwd_mma1(uint32_t tmem, const DenseBwdSmem& sm, 
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
       const uint64_t da = smem_desc(smem_addr(sm.a[2 * s + pa[q]]));
-      const uint64_t db = smem_desc(smem_addr(sm.b[2 * s + pb[q]]));
+      // samples 64 h .. 64 h + 63: eight 8-row core-matrix groups (256 B each) into the tile
+      const uint64_t db = smem_desc(smem_addr(sm.b[2 * s + pb[q]]) + 2048u * (uint32_t)h);
       const uint32_t acc = n++ > 0;
       asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
@@ -316,12 +321,13 @@ __device__ __forceinline__ void bwd_mma1(uint32_t tmem, const DenseBwdSmem& sm, 
   }
 }
 
-__device__ __forceinline__ void bwd_mma2(uint32_t tmem, const DenseBwdSmem& sm, uint32_t id2) {
-  const uint32_t d2 = tmem + 384u;
+__device__ __forceinline__ void bwd_mma2(uint32_t tmem, const DenseBwdSmem& sm, uint32_t id2, int h) {
+  const uint32_t d2 = tmem + kColD2;
 #pragma unroll 1
-  for (int s = 0; s < 16; ++s) {
+  for (int sl = 0; sl < 8; ++sl) {
+    const int s = 8 * h + sl;                                // K step of the item's samples
     const uint64_t bh = smem_desc(smem_addr(sm.w[2 * s])), bl = smem_desc(smem_addr(sm.w[2 * s + 1]));
-    const uint32_t ah = tmem + 128u + 8u * s, al = tmem + 256u + 8u * s;
+    const uint32_t ah = tmem + kColEh + 8u * sl, al = tmem + kColEl + 8u * sl;
     const uint32_t acc0 = s > 0;
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                  "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n"
@@ -340,11 +346,11 @@ __device__ __forceinline__ void mma_commit_to(uint64_t* bar) {
 __device__ __forceinline__ void bwd_chain(uint32_t lane_base, float* gp, const float (&Am)[6], const float (&mu)[3],
                                           const float (&v)[3], bool live) {
   uint32_t q[32], r[16];
-  tmem_ld32(lane_base + 384u, q);
+  tmem_ld32(lane_base + kColD2, q);
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-               : "r"(lane_base + 416u));
+               : "r"(lane_base + kColD2 + 32u));
   asm volatile("tcgen05.wait::ld.sync.aligned;");
   if (!live) return;
   float D[33];
@@ -372,7 +378,7 @@ __device__ __forceinline__ void bwd_chain(uint32_t lane_base, float* gp, const f
   red_add_v4(gp + 8, G12, D[30], D[31], D[32]);
 }
 
-__global__ void __launch_bounds__(kBwdThreads, 1) k_dense_bwd(DenseBwdArgs a) {
+__global__ void __launch_bounds__(kBwdThreads, 2) k_dense_bwd(DenseBwdArgs a) {
   extern __shared__ __align__(1024) unsigned char dsm_raw[];
   DenseBwdSmem& sm = *reinterpret_cast<DenseBwdSmem*>(dsm_raw);
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -383,7 +389,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_dense_bwd(DenseBwdArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(&sm.tbase)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&sm.tbase)),
+                 "n"(kBwdCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -391,7 +398,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_dense_bwd(DenseBwdArgs a) {
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = sm.tbase;
   const uint32_t lane_base = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-  const uint32_t id1 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  const uint32_t id1 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   const uint32_t id2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kBwdN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   uint32_t ph1 = 0, ph2 = 0;
   const uint32_t n_work = a.n_work[0];
@@ -472,7 +479,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_dense_bwd(DenseBwdArgs a) {
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;");
-        if (tid == 0) { bwd_mma1(tmem, sm, id1); mma_commit_to(&sm.bar); }
+        if (tid == 0) { bwd_mma1(tmem + kColQ, sm, id1, 0); mma_commit_to(&sm.bar); }
       }
       if (cb > g0) {
         // ---- chain of chunk k-1 (its MMA 2 done)
@@ -482,31 +489,55 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_dense_bwd(DenseBwdArgs a) {
         if (half == 0) bwd_chain(lane_base, pgp, pAm, pmu, pv, plive);
       }
       if (!have) break;
-      // ---- epilogue 1(k): E^T row t (its TMEM lane), TF32 hi / lo, into [128, 384)
-      mbar_wait_parity(&sm.bar, ph1);
-      ph1 ^= 1u;
-      asm volatile("tcgen05.fence::after_thread_sync;");
+      // ---- the two sample halves: epilogue 1(k, h) -> E^T (64 columns) -> MMA 2(k, h)
 #pragma unroll 1
-      for (int c0 = 64 * half; c0 < 64 * half + 64; c0 += 32) {
-        uint32_t q[32], lo[32];
-        tmem_ld32(lane_base + (uint32_t)c0, q);
-        asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const float Q = __uint_as_float(q[k]);
-          const float e = Q <= a.tau2 ? ex2_approx(Q * kTcNegHalfLog2e) : 0.f;
-          const float h = tf32_int(e);
-          q[k] = __float_as_uint(h);
-          lo[k] = __float_as_uint(tf32_int(e - h));
+      for (int h = 0; h < 2; ++h) {
+        mbar_wait_parity(&sm.bar, ph1);                      // MMA 1(k, h)
+        ph1 ^= 1u;
+        if (h == 1) {                                        // MMA 2(k, 0) has read E
+          mbar_wait_parity(&sm.bar2, ph2);
+          ph2 ^= 1u;
         }
-        tmem_st32(lane_base + 128u + (uint32_t)c0, q);
-        tmem_st32(lane_base + 256u + (uint32_t)c0, lo);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        {
+          const uint32_t c0 = 32u * (uint32_t)half;          // this warp's 32 of the 64 columns
+#pragma unroll
+          for (int c1 = 0; c1 < 32; c1 += 16) {
+            uint32_t q[16], lo[16];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                         : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]), "=r"(q[7]),
+                           "=r"(q[8]), "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]), "=r"(q[13]), "=r"(q[14]),
+                           "=r"(q[15])
+                         : "r"(lane_base + kColQ + c0 + c1));
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const float Q = __uint_as_float(q[k]);
+              const float e = Q <= a.tau2 ? ex2_approx(Q * kTcNegHalfLog2e) : 0.f;
+              const float hi = tf32_int(e);
+              q[k] = __float_as_uint(hi);
+              lo[k] = __float_as_uint(tf32_int(e - hi));
+            }
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                         ::"r"(lane_base + kColEh + c0 + c1), "r"(q[0]), "r"(q[1]), "r"(q[2]), "r"(q[3]), "r"(q[4]),
+                           "r"(q[5]), "r"(q[6]), "r"(q[7]), "r"(q[8]), "r"(q[9]), "r"(q[10]), "r"(q[11]), "r"(q[12]),
+                           "r"(q[13]), "r"(q[14]), "r"(q[15]));
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                         ::"r"(lane_base + kColEl + c0 + c1), "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]), "r"(lo[4]),
+                           "r"(lo[5]), "r"(lo[6]), "r"(lo[7]), "r"(lo[8]), "r"(lo[9]), "r"(lo[10]), "r"(lo[11]),
+                           "r"(lo[12]), "r"(lo[13]), "r"(lo[14]), "r"(lo[15]));
+          }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();                                     // (h = 0: all chains of k-1 read D2)
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (tid == 0) {
+          bwd_mma2(tmem, sm, id2, h);
+          mma_commit_to(&sm.bar2);
+          if (h == 0) { bwd_mma1(tmem + kColQ, sm, id1, 1); mma_commit_to(&sm.bar); }
+        }
       }
-      asm volatile("tcgen05.wait::st.sync.aligned;");
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncthreads();                                       // (also: all chains of k-1 read D2)
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      if (tid == 0) { bwd_mma2(tmem, sm, id2); mma_commit_to(&sm.bar2); }
 #pragma unroll
       for (int k = 0; k < 6; ++k) pAm[k] = Am[k];
 #pragma unroll
@@ -518,7 +549,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_dense_bwd(DenseBwdArgs a) {
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kBwdCols));
 }
 
 // Eq. 4 per sample of the dense fit (caller order): y_hat from the forward pass, the target,
@@ -561,7 +592,7 @@ __global__ void k_dense_loss(const float* __restrict__ pos, const int32_t* __res
   }
 }
 
-constexpr size_t kBwdSmem = sizeof(DenseBwdSmem) + 1024;
+constexpr size_t kBwdSmem = sizeof(DenseBwdSmem) + 1024;     // ~82 KB: two CTAs per SM
 
 void launch_dense_bwd(const DenseBwdArgs& a, cudaStream_t s, Profiler* prof) {
   int dev = 0, sms = 148;
@@ -569,7 +600,7 @@ void launch_dense_bwd(const DenseBwdArgs& a, cudaStream_t s, Profiler* prof) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaFuncSetAttribute(k_dense_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem);
   ProfScope ps(prof, "dense_bwd", s);
-  k_dense_bwd<<<sms, kBwdThreads, kBwdSmem, s>>>(a);           // 512 TMEM columns: one CTA per SM
+  k_dense_bwd<<<2 * sms, kBwdThreads, kBwdSmem, s>>>(a);       // 2 x 256 TMEM columns per SM
 }
 
 void launch_dense_loss(const float* pos, const int32_t* len, int fixed_level, int L, const float* rgb,
