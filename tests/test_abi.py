@@ -60,6 +60,11 @@ def test_arg_errors_have_no_side_effects(built):
     assert L.gc_create(0, counts.ctypes.data, pos.ctypes.data, pos.ctypes.data, None, 0, None, 0,
                        C.byref(h)) == 1
     assert L.gc_fit(None, None, None, None, 0, None, None) == 1
+    # the round-2 entry points: a NULL handle is GC_ERR_ARG before any device work
+    assert L.gc_fit_dense(None, None, None, 0, None, 0, None, None) == 1
+    assert L.gc_query_dense(None, None, None, 0, 0, None, None) == 1
+    assert L.gc_render(None, None, -1, None, None, None) == 1
+    assert L.gc_fit_image(None, None, None, None, None, None) == 1
 
 
 def test_sources_are_sm100a_only():
