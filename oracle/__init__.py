@@ -492,14 +492,16 @@ def image_loss(goff, P, cam, target, valid=None, denom=None, hdr_eps=0.01):
     return tot, per
 
 
-def image_grad_fd(goff, P, cam, target, valid=None, hdr_eps=0.01, h=1e-6):
-    """Gradient of image_loss (mode 0: denominators frozen at the unperturbed render) by fp64
-    central finite differences over every raw parameter: [G][14].  Defines the screen-space
-    backward for the tests (the derivative of the forward above, "inverse splatting")."""
+def image_grad_fd(goff, P, cam, target, valid=None, hdr_eps=0.01, h=1e-6, mode=0):
+    """Gradient of image_loss by fp64 central finite differences over every raw parameter:
+    [G][14].  mode 0: denominators frozen at the unperturbed render (reading A10's stop-gradient);
+    mode 1: the full quotient of Eq. 4 as written, denominators perturbed with the
+    render.  Defines the screen-space backward for the tests (the derivative of the forward
+    above, P:189 "inverse splatting")."""
     goff = _i64(goff)
     P = _d(P).reshape(-1, NP).copy()
     L = len(goff) - 1
-    den = np.concatenate([render(P[goff[l]:goff[l + 1]], cam)[0][None] for l in range(L)])
+    den = None if mode == 1 else np.concatenate([render(P[goff[l]:goff[l + 1]], cam)[0][None] for l in range(L)])
     g = np.zeros_like(P)
     for j in range(len(P)):
         for k in range(NP):

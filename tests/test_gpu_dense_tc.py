@@ -121,3 +121,38 @@ def test_dense_fit_steps_track_world_fit(gsc):
         torch.cuda.synchronize()
         np.testing.assert_allclose(l1, list(s2.loss[:2]), rtol=1e-4)
     _close_up_to_atomic_order(rows(c1), rows(c2))
+
+
+def test_dense_fit_fixed_level_and_cutoff(gsc):
+    """gc_fit_dense with a fixed level (path_len NULL: every sample on level 0) and with the
+    cut-off tau = 3 (the backward masks e by Q <= tau^2 like the forward): gradients against the
+    oracle's loss_grad under both bars, with reading A3's boundary allowance for tau = 3."""
+    from test_gpu_parity import check_grads, grad_allow
+    c, x, ln, rgb = _dense_fit_case(gsc, 448, 3000, seed=77)
+    P = rows(c)
+    c.debug_enable_grads(True)
+    c.fit_dense(cuda(x), None, cuda(rgb), level=0)
+    torch.cuda.synchronize()
+    ln0 = np.ones(len(x), np.int32)
+    g = np.concatenate([c.debug_grads_rows(l) for l in range(2)]).astype(np.float64)
+    ro = oracle.loss_grad(c.goff, P, x.astype(np.float64), ln0, rgb.astype(np.float64), tau=np.inf)
+    assert np.abs(g[c.goff[1]:]).max() == 0.0                 # level 1 untouched
+    al = grad_allow(c, P, x, ln0, rgb, tau=np.inf, brute=True)
+    n0 = c.goff[1]
+    check_grads(g[:n0], ro["grad"][:n0], [0, n0], "dense fit fixed level", allow=al["raw"][:n0])
+    # tau = 3
+    r = np.random.default_rng(5)
+    pos = r.uniform(-0.8, 0.8, (448, 3)).astype(np.float32)
+    alb = r.uniform(0.2, 0.9, (448, 3)).astype(np.float32)
+    ls = np.full((448, 3), np.log(0.3), np.float32)
+    c3 = gsc.GSCache([448, 112], pos, alb, init_log_scale=ls, seed=1, hparams=dict(cutoff_sigma=3.0))
+    P3 = rows(c3)
+    c3.debug_enable_grads(True)
+    c3.fit_dense(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    g3 = np.concatenate([c3.debug_grads_rows(l) for l in range(2)]).astype(np.float64)
+    ro3 = oracle.loss_grad(c3.goff, P3, x.astype(np.float64), ln, rgb.astype(np.float64), tau=3.0, grids=c3.grids())
+    # every sample meets ~100 Gaussians inside 3 sigma, so ~2 % of the samples hold a pair within
+    # 1e-4 tau^2 of the cut-off (reading A3); those get the allowance
+    al3 = grad_allow(c3, P3, x, ln, rgb, tau=3.0, max_amb_rate=0.05)
+    check_grads(g3, ro3["grad"], c3.goff, "dense fit tau=3", iso_levels=(0, 1), allow=al3["raw"])

@@ -37,10 +37,10 @@ def camera(gsc, W, H, f, dist=3.0, rot=(0.15, -0.2, 0.05)):
     return cam, ocam
 
 
-def scene(gsc, counts, seed=3, max_opacity=0.8):
+def scene(gsc, counts, seed=3, max_opacity=0.8, hparams=None):
     pos, alb = workload.init_cloud(1)
     pos, alb = pos[:counts[0]], alb[:counts[0]]
-    c = gsc.GSCache(counts, cuda(pos), cuda(alb), seed=seed)
+    c = gsc.GSCache(counts, cuda(pos), cuda(alb), seed=seed, hparams=hparams)
     r = np.random.default_rng(seed)
     for l in range(len(counts)):
         Pl = c.params_rows(l)
@@ -95,8 +95,8 @@ def test_render_full_hd_sampled(gsc):
         assert (yo.reshape(-1, 3)[pix] > 0).mean() > 0.05
 
 
-def _tiny(gsc, seed=5):
-    c = scene(gsc, [24, 8], seed=seed, max_opacity=0.7)
+def _tiny(gsc, seed=5, hparams=None):
+    c = scene(gsc, [24, 8], seed=seed, max_opacity=0.7, hparams=hparams)
     cam, ocam = camera(gsc, 48, 40, 40.0)
     P = rows(c)
     r = np.random.default_rng(seed)
@@ -127,6 +127,22 @@ def test_fit_image_gradients_match_finite_differences(gsc):
         sl = slice(c.goff[l], c.goff[l + 1])
         for name, cs in oracle.GROUP_SLICES.items():
             check_grad_group(g[sl, cs], go[sl, cs], f"screen level {l} {name}")
+
+
+def test_fit_image_gradients_full_quotient(gsc):
+    """loss_grad_mode 1 (Eq. 4's full quotient as written; reading A10): the gradient
+    written by the fused forward raster and back-propagated through the compositing and the
+    projection, against fp64 central differences of the oracle's live-denominator image loss."""
+    c, cam, ocam, P, target, valid = _tiny(gsc, seed=6, hparams=dict(loss_grad_mode=1))
+    c.debug_enable_grads(True)
+    c.fit_image(cam, cuda(target.astype(np.float32)), cuda(valid))
+    torch.cuda.synchronize()
+    g = np.concatenate([c.debug_grads_rows(l) for l in range(2)]).astype(np.float64)
+    go = oracle.image_grad_fd(c.goff, P, ocam, target, valid, mode=1)
+    for l in range(2):
+        sl = slice(c.goff[l], c.goff[l + 1])
+        for name, cs in oracle.GROUP_SLICES.items():
+            check_grad_group(g[sl, cs], go[sl, cs], f"screen mode 1 level {l} {name}")
 
 
 def test_fit_image_loss_curve_and_world_consistency(gsc):

@@ -143,3 +143,22 @@ def test_fd_gradient_of_colour_matches_closed_form():
     want = [np.sum(-2 * (tgt[0, ..., ch] - img[..., ch]) * alpha / (img[..., ch] + 0.01) ** 2) / (3 * k)
             for ch in range(3)]
     np.testing.assert_allclose(g[0, 7:10], want, rtol=1e-6)
+
+
+def test_fd_gradient_of_colour_full_quotient_closed_form():
+    """mode 1 (Eq. 4's full quotient, reading A10): the finite-difference colour gradient
+    of a single Gaussian equals the closed form d/dy (x - y)^2 / (y + eps)^2 = -2 (x - y)(x + eps)
+    / (y + eps)^3, chained through y = c alpha, summed over pixels and divided by 3k."""
+    c = cam(W=32, H=32)
+    P = row((0.02, 0.01, 2.0), c=(0.4, 0.8, 1.1), w=0.7)[None]
+    img = oracle.render(P, c)[0]
+    r = np.random.default_rng(3)
+    tgt = img[None] * r.uniform(0.5, 1.5, img.shape)[None]
+    g = oracle.image_grad_fd([0, 1], P, c, tgt, mode=1)
+    alpha = img[..., 0] / 0.4
+    k = 32 * 32
+    want = [np.sum(-2 * (tgt[0, ..., ch] - img[..., ch]) * (tgt[0, ..., ch] + 0.01) * alpha
+                   / (img[..., ch] + 0.01) ** 3) / (3 * k) for ch in range(3)]
+    np.testing.assert_allclose(g[0, 7:10], want, rtol=1e-6)
+    g0 = oracle.image_grad_fd([0, 1], P, c, tgt)              # differs from the frozen mode
+    assert np.abs(g0[0, 7:10] - g[0, 7:10]).max() > 1e-3 * np.abs(g[0, 7:10]).max()
