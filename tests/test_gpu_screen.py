@@ -208,3 +208,27 @@ def test_render_crowded_tiles_capacity_growth(gsc):
             assert (yo > 0).mean() > 0.01, what
             check_image(y.reshape(-1, 3), yo.reshape(-1, 3), amb.reshape(-1), f"crowded {what} level {l}",
                         rel=1e-4)
+
+
+def test_render_degenerate_cameras_and_empty_fit(gsc):
+    """Edge cases of the screen path: a camera that sees no Gaussian (no keys: every pixel
+    C = 0, T = 1), a 1 x 1 image and a 17 x 9 image (partial tiles) against the oracle, and a
+    fit_image step with no valid pixel (k_l = 0 on every level: no optimizer step, parameters
+    unchanged, finite statistics)."""
+    c = scene(gsc, [300, 60], seed=12)
+    P = rows(c)
+    away, _ = camera(gsc, 40, 30, 40.0, dist=-3.0)            # the scene behind the camera
+    img, T = c.render(away, with_T=True)
+    assert np.all(img.cpu().numpy() == 0.0) and np.all(T.cpu().numpy() == 1.0)
+    for W, H in ((1, 1), (17, 9)):
+        cam, ocam = camera(gsc, W, H, 12.0)
+        img = c.render(cam).cpu().numpy()
+        for l in range(2):
+            yo, _, amb = oracle.render(P[c.goff[l]:c.goff[l + 1]], ocam)
+            check_image(img[l].reshape(-1, 3), yo.reshape(-1, 3), amb.reshape(-1), f"{W}x{H} level {l}")
+    cam, _ = camera(gsc, 40, 30, 40.0)
+    tgt = cuda(np.ones((2, 30, 40, 3), np.float32))
+    st = c.fit_image(cam, tgt, cuda(np.zeros((2, 30, 40), np.uint8)))
+    torch.cuda.synchronize()
+    assert st.count[0] == 0 and st.count[1] == 0 and np.isfinite(st.loss[0]) and st.loss[0] == 0.0
+    np.testing.assert_array_equal(rows(c), P)
