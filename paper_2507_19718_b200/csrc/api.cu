@@ -1569,8 +1569,8 @@ gc_status gc_query_dense(gc_cache c, const float* pos, const int32_t* path_len, 
   if (!c) return fail(GC_ERR_ARG, "NULL handle");
   if (S < 0 || S >= ((int64_t)1 << 31)) return fail(GC_ERR_ARG, "S out of range");
   if (S > 0 && (!pos || !out_rgb)) return fail(GC_ERR_ARG, "NULL pointer");
-  if (!path_len && (level < 0 || level >= c->L)) return fail(GC_ERR_ARG, "level %d not in [0, %d)", level, c->L);
   if (S == 0) return GC_OK;
+  if (!path_len && (level < 0 || level >= c->L)) return fail(GC_ERR_ARG, "level %d not in [0, %d)", level, c->L);
   if (!is_device_ptr(pos) || !is_device_ptr(out_rgb) || (path_len && !is_device_ptr(path_len)))
     return fail(GC_ERR_ARG, "gc_query_dense takes device buffers");
   cudaStream_t s = (cudaStream_t)stream;
@@ -1604,7 +1604,8 @@ gc_status gc_fit_dense(gc_cache c, const float* pos, const int32_t* path_len, in
   if (!c) return fail(GC_ERR_ARG, "NULL handle");
   if (S < 0 || S >= ((int64_t)1 << 31)) return fail(GC_ERR_ARG, "S out of range");
   if (S > 0 && (!pos || !rgb)) return fail(GC_ERR_ARG, "NULL pointer");
-  if (!path_len && (level < 0 || level >= c->L)) return fail(GC_ERR_ARG, "level %d not in [0, %d)", level, c->L);
+  if (S > 0 && !path_len && (level < 0 || level >= c->L))
+    return fail(GC_ERR_ARG, "level %d not in [0, %d)", level, c->L);
   if (c->comm) return fail(GC_ERR_UNSUPPORTED, "gc_fit_dense is single-GPU");
   if (S > 0 && (!is_device_ptr(pos) || !is_device_ptr(rgb) || (path_len && !is_device_ptr(path_len))))
     return fail(GC_ERR_ARG, "gc_fit_dense takes device buffers");

@@ -156,3 +156,20 @@ def test_dense_fit_fixed_level_and_cutoff(gsc):
     # 1e-4 tau^2 of the cut-off (reading A3); those get the allowance
     al3 = grad_allow(c3, P3, x, ln, rgb, tau=3.0, max_amb_rate=0.05)
     check_grads(g3, ro3["grad"], c3.goff, "dense fit tau=3", iso_levels=(0, 1), allow=al3["raw"])
+
+
+def test_dense_fit_empty_and_all_invalid(gsc):
+    """gc_fit_dense with no samples and with only dropped samples (non-finite positions, n < 1,
+    non-finite colours): k_l = 0 on every level, so no optimizer step -- parameters unchanged."""
+    c, x, ln, rgb = _dense_fit_case(gsc, 200, 300, seed=9)
+    P = rows(c)
+    st = c.fit_dense(cuda(x[:0]), cuda(ln[:0]), cuda(rgb[:0]))
+    torch.cuda.synchronize()
+    assert st.count[0] == 0 and st.count[1] == 0
+    x[:100] = np.nan
+    ln[100:200] = 0
+    rgb[200:] = np.nan
+    st = c.fit_dense(cuda(x), cuda(ln), cuda(rgb))
+    torch.cuda.synchronize()
+    assert st.count[0] == 0 and st.count[1] == 0 and st.loss[0] == 0.0
+    np.testing.assert_array_equal(rows(c), P)
