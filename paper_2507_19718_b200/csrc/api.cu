@@ -1145,8 +1145,8 @@ static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_le
   if (!c) return fail(GC_ERR_ARG, "NULL handle");
   if (S < 0 || S >= ((int64_t)1 << 31)) return fail(GC_ERR_ARG, "S out of range");
   if (S > 0 && (!pos || !out_rgb)) return fail(GC_ERR_ARG, "NULL pointer");
-  if (!path_len && (level < 0 || level >= c->L)) return fail(GC_ERR_ARG, "level %d not in [0, %d)", level, c->L);
   if (S == 0 && !routed(c)) return GC_OK;      // (level-sharded calls are collective)
+  if (!path_len && (level < 0 || level >= c->L)) return fail(GC_ERR_ARG, "level %d not in [0, %d)", level, c->L);
   cudaStream_t s = (cudaStream_t)stream;
   CK(cudaSetDevice(c->device));
   if (gc_status e = check_sticky(c)) return e;
