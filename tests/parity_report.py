@@ -1,5 +1,6 @@
 """Measured parity of the CUDA path against the fp64 oracle (what the -m gpu tests assert,
-with the numbers written down): python tools/parity_report.py > profiles/r02_parity.json
+with the numbers written down; test infrastructure, it calls the oracle):
+  python tests/parity_report.py > profiles/r02_parity.json
 
 * forward: cfg1 full frame of lookups -- max relative error per element, samples with an A3
   boundary-ambiguous pair;
@@ -129,7 +130,7 @@ def main():
     out["forward_cfg2_frame_call_sampled"] = {"points": 3000, "max_rel_err": mx, "median_rel_err": med,
                                               "points_over_1e-5": nbad}
     # ---- round 2: screen space (f1)
-    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     import test_gpu_screen as ts
     c = ts.scene(gsc, [1500, 400, 100])
     cam, ocam = ts.camera(gsc, 200, 150, 180.0)
