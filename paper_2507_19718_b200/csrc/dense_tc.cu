@@ -22,7 +22,6 @@
 namespace gsc {
 
 constexpr int kTcThreads = 128;
-constexpr int kTcTile = 128 * 8 * 4;                         // bytes of one 128-row x 8 tf32 K-major tile
 constexpr float kTcNegHalfLog2e = -0.72134752044448170f;
 
 struct DenseSmem {
