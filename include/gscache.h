@@ -226,8 +226,9 @@ gc_status gc_render(gc_cache c, const gc_camera* cam, int level, float* out_rgb,
  * carry no sample.  Renders all levels, takes Eq. 4 per level over 3 k_l (k_l = valid pixels;
  * loss_grad_mode as gc_fit), back-propagates through the compositing and the EWA projection
  * into all 14 raw parameters, and takes the shared AdamW step (schedule, level skip, frozen
- * groups as gc_fit), then rebuilds the evaluation records and culling lists so that the
- * world-space calls see the new parameters.  stats as gc_fit (n_in = L H W pixel samples).
+ * groups as gc_fit).  The world-space calls see the new parameters: their evaluation records
+ * and culling lists are rebuilt by the next call that reads them (consecutive gc_fit_image /
+ * gc_render calls skip that rebuild).  stats as gc_fit (n_in = L H W pixel samples).
  * Device buffers; single GPU (GC_ERR_UNSUPPORTED with a communicator); synchronises once. */
 gc_status gc_fit_image(gc_cache c, const gc_camera* cam, const float* target, const uint8_t* valid,
                        gc_stream stream, gc_fit_stats* stats);

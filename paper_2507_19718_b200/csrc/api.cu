@@ -124,6 +124,10 @@ struct gc_cache_s {
   std::vector<StatsPayload*> ring;        // the reusable ones of eager calls
   size_t payload_next = 0, captured_payloads = 0;
   uint64_t list_generation = 0;           // bumped by every reallocation of the culling lists
+  // gc_fit_image leaves the evaluation records and culling lists of the world-space calls
+  // stale (the screen path reads the parameters directly); the next call that reads them
+  // rebuilds first (refresh_stale), so consecutive image steps skip the rebuild
+  bool lists_stale = false;
   CellRef cref{};                         // fp32 cell geometry of the evaluators (CellRef)
   int dbg_mode = 0;                       // gc_debug_enable_grads: bit 0 raw grads, bit 1 coef grads
   float* dbg_coef = nullptr;              // [G][12] coefficient-gradient snapshot (bit 1)
@@ -277,6 +281,7 @@ static CullBufs cull_bufs(gc_cache c) {
 }
 
 static gc_status rebuild_csr(gc_cache c, cudaStream_t s, bool recompute_records) {
+  if (recompute_records) c->lists_stale = false;
   if (recompute_records) CK(cudaMemsetAsync(&c->st->csr_overflow, 0, sizeof(unsigned int), s));
   if (recompute_records)
     launch_record_cull(c->G, c->P, (double)c->hp.cutoff_sigma, c->geom, cull_bufs(c), c->st, s);
@@ -303,7 +308,14 @@ static gc_status publish_lists(gc_cache c) {
   return GC_OK;
 }
 
+static gc_status refresh_stale(gc_cache c, cudaStream_t s) {
+  if (!c->lists_stale) return GC_OK;
+  CK(cudaMemsetAsync(c->csr_count, 0, sizeof(uint32_t) * c->NC, s));
+  return rebuild_csr(c, s, true);
+}
+
 static gc_status csr_guard(gc_cache c, cudaStream_t s) {
+  if (gc_status e = refresh_stale(c, s)) return e;
   const uint32_t total = *(volatile uint32_t*)c->hcsr;
   if (total <= c->csr_cap / 2 || capturing(s)) return GC_OK;
   const bool overflowed = total > c->csr_cap;
@@ -1330,6 +1342,7 @@ gc_status gc_set_comm(gc_cache c, const void* nccl_uid, int rank, int world, int
   if (mode == 1 && world > 1024) return fail(GC_ERR_ARG, "level-sharded mode supports at most 1024 ranks");
   if (mode == 2 && world > 32) return fail(GC_ERR_ARG, "owner-computes mode supports at most 32 ranks");
   CK(cudaSetDevice(c->device));
+  if (gc_status e = refresh_stale(c, 0)) return e;
   CK(cudaDeviceSynchronize());
   if (gc_status e = flush_pending(c, 0)) return e;
   CK(cudaDeviceSynchronize());
@@ -1555,8 +1568,9 @@ gc_status gc_fit_image(gc_cache c, const gc_camera* cam, const float* target, co
   CK(launch_sraster_bwd(sc, L, b, b.T, b.last, b.dLdC, b.g2d, s));
   CK(launch_sproject_bwd(c->P, c->G, 0, c->G, sc, b, b.g2d, b.raw, s));
   launch_adamw(c->G, c->P, c->M, c->V, c->grad, cull_bufs(c), c->dbg_on ? c->dbg : nullptr, c->st, c->hp, c->geom,
-               reinterpret_cast<unsigned long long*>(&c->dstats->nonfinite_grads), s, &c->prof, b.raw);
-  if (gc_status e = rebuild_csr(c, s, false)) return e;
+               reinterpret_cast<unsigned long long*>(&c->dstats->nonfinite_grads), s, &c->prof, b.raw, nullptr, 0,
+               /*with_record=*/false);
+  c->lists_stale = true;             // records + culling lists rebuilt by the next world-space call
   if (gc_status e = emit_stats(c, stats, s)) return e;
   CK(cudaGetLastError());
   return GC_OK;
@@ -1708,6 +1722,7 @@ gc_status gc_debug_cull(gc_cache c, int level, int32_t* offsets, int32_t* idx, i
   cudaStream_t s = (cudaStream_t)stream;
   CK(cudaSetDevice(c->device));
   if (gc_status e = flush_pending(c, s)) return e;
+  if (gc_status e = refresh_stale(c, s)) return e;
   const int64_t c0 = c->geom.coff[level], nc = c->geom.coff[level + 1] - c0;
   std::vector<uint32_t> off((size_t)nc + 1);
   CK(cudaMemcpyAsync(off.data(), c->csr_off + c0, sizeof(uint32_t) * (nc + 1), cudaMemcpyDeviceToHost, s));

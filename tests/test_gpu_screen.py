@@ -167,6 +167,16 @@ def test_fit_image_loss_curve_and_world_consistency(gsc):
     yo, lv, _ = oracle.query(c.goff, P1, x.astype(np.float64), ln, grids=c.grids())
     from test_gpu_parity import check_forward
     check_forward(y, yo, P1, c.goff, x, lv, what="world lookups after screen fit")
+    # the culling lists the image steps left stale are rebuilt for the new parameters (C8,
+    # bit-exact), also when the first reader is gc_debug_cull
+    c.fit_image(cam, tg, va)
+    torch.cuda.synchronize()
+    P2 = rows(c)
+    for l in range(2):
+        off_o, idx_o = oracle.csr_for(P2[c.goff[l]:c.goff[l + 1]], 3.0, c.grid(l))
+        off_g, idx_g = c.debug_cull(l)
+        np.testing.assert_array_equal(off_g.astype(np.int64), off_o)
+        np.testing.assert_array_equal(idx_g, idx_o)
 
 
 def test_render_crowded_tiles_capacity_growth(gsc):
