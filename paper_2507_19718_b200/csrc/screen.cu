@@ -480,6 +480,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_sraster_bwd(SBwdArgs a) {
   const float fy = py + 0.5f;
   const uint2 rg = a.ranges[(size_t)l * ntiles + tile];
   const int n = rg.y > rg.x ? (int)(rg.y - rg.x) : 0;
+  if (n == 0) return;                                      // (uniform: an empty tile has no gradient)
   const size_t pix = ((size_t)l * a.cam.H + min(py, a.cam.H - 1)) * a.cam.W + px;
   PixBwd2 pp{};
   int last0 = 0, last1 = 0;
