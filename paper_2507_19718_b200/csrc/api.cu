@@ -1025,7 +1025,7 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
   Scratch& F = c->fit;
   int set = -1;
   if (gc_status e = stage_inputs(c, F, s, S, pos, path_len, rgb, set)) return e;
-  IngestBufs b{F.kr, F.cell_count, F.bin, c->NC};
+  IngestBufs b{F.kr, F.cell_count, F.bin, c->NC, F.cap};
   if (S > 0) launch_keys(pos, path_len, rgb, -1, S, c->geom, b, s, &c->prof);
   launch_scan(F.cell_count, c->NC * kRep, kCH, F.tiles, F.totals, F.cell_start, nullptr, F.work, c->geom, s, &c->prof);
   if (S > 0) launch_scatter(pos, rgb, S, F.cell_start, b, s, &c->prof);
@@ -1039,6 +1039,7 @@ static gc_status fit_impl(gc_cache c, const float* pos, const int32_t* path_len,
   fa.tau2 = tau * tau; fa.hdr_eps = c->hp.hdr_eps; fa.mode = c->hp.loss_grad_mode; fa.L = c->L;
   fa.lite = (c->hp.lr[GC_SCALE] == 0.f && !c->dbg_on) ? 1 : 0;
   fa.ref = c->cref;
+  fa.bin_cap = F.cap; fa.G = c->G;
   const bool dp = c->comm != nullptr;
   // with the step deferred nothing after the statistics launch touches the call's stats, so a
   // page-locked caller struct is written by the kernel itself (mapped through UVA): no copy
@@ -1191,7 +1192,7 @@ static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_le
     dout = c->r_res;
     if (gc_status e = ensure_scratch(c, c->qry, std::max<int64_t>(S, 1), false, s)) return e;
   }
-  IngestBufs b{Q.kr, Q.cell_count, Q.bin, c->NC};
+  IngestBufs b{Q.kr, Q.cell_count, Q.bin, c->NC, Q.cap};
   launch_keys_query(pos, path_len, path_len ? -1 : level, S, c->geom, b, dout, s, &c->prof);
   launch_scan(Q.cell_count, c->NC * kRep, kCH, Q.tiles, Q.totals, Q.cell_start, nullptr, Q.work, c->geom, s, &c->prof);
   launch_scatter(pos, nullptr, S, Q.cell_start, b, s, &c->prof);
@@ -1205,6 +1206,7 @@ static gc_status query_impl(gc_cache c, const float* pos, const int32_t* path_le
   const float tau = c->hp.cutoff_sigma;
   qa.tau2 = tau * tau;
   qa.ref = c->cref;
+  qa.bin_cap = Q.cap; qa.G = c->G; qa.S = S;
   if (tail_ev) CK(cudaStreamWaitEvent(s, tail_ev, 0));     // a deferred step is complete
   launch_query(qa, c->q_grid, s, &c->prof);
   if (caller_out) {
@@ -1595,7 +1597,7 @@ gc_status gc_query_dense(gc_cache c, const float* pos, const int32_t* path_len, 
   if (gc_status e = flush_pending(c, s)) return e;
   if (!c->dense_grid) c->dense_grid = dense_tc_grid();
   Scratch& D = c->dns;
-  IngestBufs b{D.kr, D.cell_count, D.bin, c->dNC};
+  IngestBufs b{D.kr, D.cell_count, D.bin, c->dNC, D.cap};
   CK(cudaMemsetAsync(out_rgb, 0, sizeof(float) * 3 * S, s));   // parts of a lookup add up (k_dense_tc)
   launch_keys_query(pos, path_len, path_len ? -1 : level, S, c->dgeom, b, out_rgb, s, &c->prof);
   launch_scan(D.cell_count, c->dNC * kRep, 128, D.tiles, D.totals, D.cell_start, nullptr, D.work, c->dgeom, s, &c->prof);
@@ -1636,7 +1638,7 @@ gc_status gc_fit_dense(gc_cache c, const float* pos, const int32_t* path_len, in
   const int fixed = path_len ? -1 : level;
   if (S > 0) {
     // forward: y_hat of every sample (gc_query_dense's product), caller order
-    IngestBufs b{D.kr, D.cell_count, D.bin, c->dNC};
+    IngestBufs b{D.kr, D.cell_count, D.bin, c->dNC, D.cap};
     CK(cudaMemsetAsync(D.y, 0, sizeof(float) * 3 * S, s));
     launch_keys_query(pos, path_len, fixed, S, c->dgeom, b, D.y, s, &c->prof);
     launch_scan(D.cell_count, c->dNC * kRep, 128, D.tiles, D.totals, D.cell_start, nullptr, D.work, c->dgeom, s, &c->prof);

@@ -6,12 +6,38 @@
 
 #include "../../include/gscache.h"
 
+// Checked build (-DGSC_CHECKED, tools/build_variant.py): device-side bounds checks on the
+// index arithmetic of the hot kernels (bins, work items, list entries, gradient rows, outputs,
+// screen-space key / range / image buffers).  A failed check prints the site and traps, so
+// the call fails with a sticky CUDA error.  The GPU pool refuses compute-sanitizer; the
+// whole `-m gpu` suite runs against this build instead.  Compiled out of
+// the product build.
+#include <cstdio>
+#ifdef GSC_CHECKED
+#define GSC_CHECK(cond, what)                                                                  \
+  do {                                                                                         \
+    if (!(cond)) {                                                                             \
+      printf("GSC_CHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__,   \
+             (int)blockIdx.x, (int)threadIdx.x);                                               \
+      __trap();                                                                                \
+    }                                                                                          \
+  } while (0)
+#else
+#define GSC_CHECK(cond, what) do { } while (0)
+#endif
+
 namespace gsc {
 
 constexpr int kMaxL = GC_MAX_LEVELS;
 constexpr int kNP = 14;              // raw floats per Gaussian
 constexpr int kCH = 64;              // samples per work item: one warp, two samples per lane
-constexpr int kScanThreads = 1024;   // one scan tile per CTA: 1024 threads x 8 items
+#ifndef GSC_SCAN_THREADS
+#define GSC_SCAN_THREADS 1024
+#endif
+#ifndef GSC_SCAN_MINB
+#define GSC_SCAN_MINB 1
+#endif
+constexpr int kScanThreads = GSC_SCAN_THREADS;   // one scan tile per CTA: kScanThreads threads x 8 items
 constexpr int kScanTile = 8 * kScanThreads;
 #ifndef GSC_KREP
 #define GSC_KREP 4

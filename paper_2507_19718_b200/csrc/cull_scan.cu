@@ -181,7 +181,7 @@ __device__ __forceinline__ uint2 st_val(unsigned long long w) {
   return make_uint2((uint32_t)(w & 0x7FFFFFFFu), (uint32_t)((w >> 31) & 0x7FFFFFFFu));
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_scan(uint32_t* __restrict__ cnt, int64_t n, int ch,
+__global__ void __launch_bounds__(kScanThreads, GSC_SCAN_MINB) k_scan(uint32_t* __restrict__ cnt, int64_t n, int ch,
                                               unsigned long long* state, uint32_t* ctl, int ntiles,
                                               uint32_t* totals, uint32_t* excl, uint32_t* excl_copy,
                                               WorkItem* work, LevelGeom g) {

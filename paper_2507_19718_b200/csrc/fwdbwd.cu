@@ -76,7 +76,7 @@ __device__ __forceinline__ float cand_q(const Cand& g, float x, float y, float z
 // general chunks r0..r2 as documented on ChunkSmem.  (The expanded form g|x'|^2 + g|m|^2 -
 // 2g x'.m saves 2 ops per test but its cancellation costs ~1e-5 relative: measured, rejected.)
 __device__ __forceinline__ bool stage_chunk(ChunkSmem& w, const float4* __restrict__ lrec, int base, int kc, int lane,
-                                            float xr, float yr, float zr, float tau2) {
+                                            float xr, float yr, float zr, float tau2, int64_t G) {
   __syncwarp();
   float4 p = make_float4(0.f, 0.f, 0.f, 0.f), q = p, r = p;
   int gid = 0;
@@ -85,6 +85,7 @@ __device__ __forceinline__ bool stage_chunk(ChunkSmem& w, const float4* __restri
     ld_v8_nc(lrec + 4 * (int64_t)(base + lane), p, q);
     ld_v8_nc(lrec + 4 * (int64_t)(base + lane) + 2, r, t);
     gid = __float_as_int(t.x);
+    GSC_CHECK(gid >= 0 && gid < G, "list entry Gaussian index");
   }
   const bool iso = __all_sync(0xffffffffu, lane >= kc || (p.y == 0.f && p.z == 0.f && q.x == 0.f &&
                                                            p.x == p.w && p.w == q.y));
@@ -529,6 +530,8 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
     --left;
     if (it >= n_work) break;
     const WorkItem wi = a.work[it];
+    GSC_CHECK(wi.start >= 0 && wi.count >= 1 && wi.count <= kCH && (int64_t)wi.start + wi.count <= a.bin_cap &&
+              wi.level >= 0 && wi.level < a.L && wi.cell >= 0, "fit work item");
     // clamped to the list capacity: after an overflowing rebuild the offsets run past it (the
     // entries there were dropped; the call reports GC_FLAG_LISTS_OVERFLOWED and skips its step)
     const int lo = (int)min(__ldg(a.csr_off + wi.cell), lcap);
@@ -558,7 +561,7 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
     const bool masked = C <= 32 * kMaskChunks;
     for (int cb = 0, c = 0; cb < C; cb += 32, ++c) {
       const int kc = min(32, C - cb);
-      iso = stage_chunk(w, lrec, lo + cb, kc, lane, xref, yref, zref, tau2);
+      iso = stage_chunk(w, lrec, lo + cb, kc, lane, xref, yref, zref, tau2, a.G);
       uint2 cm = make_uint2(0u, 0u);
       eval_any<true>(w, iso, wi.count > 32, kc, xa, xb, tau2, ya, yb, cm, lane);
       if (masked) w.u.mask[c][lane] = cm;
@@ -596,7 +599,7 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
         }
         const int P = __shfl_sync(0xffffffffu, incl, 31);
         if (P == 0) continue;
-        if (c != nch - 1) iso = stage_chunk(w, lrec, lo + cb, 32, lane, xref, yref, zref, tau2);
+        if (c != nch - 1) iso = stage_chunk(w, lrec, lo + cb, 32, lane, xref, yref, zref, tau2, a.G);
         w.offs[lane] = incl - nk;
         __syncwarp();
         if (wi.count > 32) {
@@ -613,7 +616,7 @@ __global__ void __launch_bounds__(256, 4) k_fwdbwd(FitArgs a) {
       const uint32_t lt = (1u << lane) - 1u;
       for (int cb = 0; cb < C; cb += 32) {
         const int kc = min(32, C - cb);
-        const bool ci = stage_chunk(w, lrec, lo + cb, kc, lane, xref, yref, zref, tau2);
+        const bool ci = stage_chunk(w, lrec, lo + cb, kc, lane, xref, yref, zref, tau2, a.G);
         int pb = 0;
         for (int k = 0; k < kc; ++k) {
           float Qa, Qb, ea, eb;                    // same arithmetic as eval_chunk[_iso]
@@ -693,6 +696,8 @@ __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
     --left;
     if (it >= n_work) break;
     const WorkItem wi = a.work[it];
+    GSC_CHECK(wi.start >= 0 && wi.count >= 1 && wi.count <= kCH && (int64_t)wi.start + wi.count <= a.bin_cap &&
+              wi.cell >= 0, "lookup work item");
     // clamped to the list capacity: after an overflowing rebuild the offsets run past it (the
     // entries there were dropped; the call reports GC_FLAG_LISTS_OVERFLOWED and skips its step)
     const int lo = (int)min(__ldg(a.csr_off + wi.cell), lcap);
@@ -708,10 +713,12 @@ __global__ void __launch_bounds__(256, 4) k_query(QueryArgs a) {
     float ya[3] = {0.f, 0.f, 0.f}, yb[3] = {0.f, 0.f, 0.f};
     for (int cb = 0; cb < C; cb += 32) {
       const int kc = min(32, C - cb);
-      const bool iso = stage_chunk(w, lrec, lo + cb, kc, lane, xref, yref, zref, tau2);
+      const bool iso = stage_chunk(w, lrec, lo + cb, kc, lane, xref, yref, zref, tau2, a.G);
       uint2 cm;
       eval_any<false>(w, iso, wi.count > 32, kc, xa, xb, tau2, ya, yb, cm, lane);
     }
+    GSC_CHECK(lane >= wi.count || __float_as_uint(pa.w) < (uint64_t)a.S, "lookup output index");
+    GSC_CHECK(lane + 32 >= wi.count || __float_as_uint(pb4.w) < (uint64_t)a.S, "lookup output index");
     if (lane < wi.count) query_out(a.out, a.att, a.beta, a.unb, __float_as_uint(pa.w), ya);
     if (lane + 32 < wi.count) query_out(a.out, a.att, a.beta, a.unb, __float_as_uint(pb4.w), yb);
   }

@@ -25,6 +25,7 @@ __global__ void __launch_bounds__(256, 4) k_keys(const float* __restrict__ pos, 
     if (a == 0) s_coff[l] = g.coff[l];
   }
   __syncthreads();
+  GSC_CHECK(S <= b.cap, "keys: samples past the scratch capacity");
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -80,7 +81,11 @@ __global__ void __launch_bounds__(256, 4) k_keys(const float* __restrict__ pos, 
       rank[u] = 0u;
       const uint32_t r = (uint32_t)(((i0 + u * 32) >> 5) & (kRep - 1));
       if (key[u] != kInvalidKey && lane == __ffs(peers[u]) - 1)
+#ifdef GSC_EXP_KEYS_NOATOMIC   // timing experiment only: ranks are wrong
+        rank[u] = r;
+#else
         rank[u] = atomicAdd(b.cell_count + (size_t)r * b.nc + key[u], (uint32_t)__popc(peers[u]));
+#endif
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
@@ -128,6 +133,7 @@ __global__ void __launch_bounds__(256, 4) k_scatter(const float* __restrict__ po
     for (int u = 0; u < kU; ++u) {
       if (key[u] == kInvalidKey) continue;
       const int64_t i = i0 + u * 32;
+      GSC_CHECK(d[u] < b.cap, "scatter: bin slot past the capacity");
       if (rgb) {
         st_v8(b.bin + 2 * (int64_t)d[u], make_float4(v[u][0], v[u][1], v[u][2], v[u][3]),
               make_float4(v[u][4], v[u][5], 0.f, 0.f));

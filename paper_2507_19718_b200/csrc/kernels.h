@@ -102,6 +102,7 @@ struct IngestBufs {
   float4* bin;          // binned samples, cell-major, one 32-B sector each: fit (x,y,z,r | g,b,-,-),
                         // query (x,y,z, original index as bits | -)
   int64_t nc;           // cells (counters are replica-major [kRep][nc])
+  int64_t cap;          // samples the bins hold (GSC_CHECKED bounds)
 };
 void launch_keys(const float* pos, const int32_t* len, const float* rgb, int level_fixed,
                  int64_t S, const LevelGeom& g, IngestBufs b, cudaStream_t s, Profiler* prof);
@@ -131,6 +132,7 @@ struct FitArgs {
   float tau2, hdr_eps; int mode; int L;
   int lite;             // scale group frozen (lr 0) and no gradient export: skip dA on isotropic chunks
   CellRef ref;
+  int64_t bin_cap, G;   // GSC_CHECKED bounds: binned samples, gradient rows
 
 };
 int fwdbwd_grid();
@@ -142,6 +144,7 @@ struct QueryArgs {
   float* out; float tau2;
   const float* att; const float* beta; const float* unb;   // optional f3 epilogue (caller order)
   CellRef ref;
+  int64_t bin_cap, G, S;   // GSC_CHECKED bounds: binned lookups, Gaussians, outputs
 };
 int query_grid();
 void launch_query(const QueryArgs& a, int grid, cudaStream_t s, Profiler* prof);

@@ -260,6 +260,7 @@ struct SRasterArgs {
   // of its colour (out may be null) and the per-level loss sums / valid counts go to partial
   const float* target; const uint8_t* valid; float eps; int mode;
   float* dLdC; double* partial;
+  int64_t kv_cap = 0;   // GSC_CHECKED bounds of the sorted (tile, depth) -> Gaussian list
 };
 
 // Eq. 4 at one pixel (reading A10: denominator frozen, mode 0, or the full quotient, mode 1):
@@ -332,6 +333,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_sraster(SRasterArgs a) {
     const int q = b0 + threadIdx.x;
     if (q < n) {
       const int64_t j = a.val[rg.x + q];
+      GSC_CHECK(rg.y <= (uint64_t)a.kv_cap && j >= 0, "raster: tile range / Gaussian index");
       const float4 p = a.pa[j];
       s_uv[threadIdx.x] = make_float2(p.x, p.y);
       const float4 b = a.pb[j];
@@ -417,6 +419,7 @@ struct SBwdArgs {
   const float* outT; const uint32_t* last; const float* dLdC;
   float* g2d;           // [G][12]: du dv da db | dc dw dc0 dc1 | dc2 - - -
   SCam cam;
+  int64_t kv_cap = 0;   // GSC_CHECKED bounds
 };
 
 // The pixel pair's share of the backward at one Gaussian (back to front), in packed fp32x2:
@@ -509,6 +512,7 @@ __global__ void __launch_bounds__(kRasterThreads) k_sraster_bwd(SBwdArgs a) {
     const int q = b0 + threadIdx.x;
     if (q < b1) {
       const int64_t j = a.val[rg.x + q];
+      GSC_CHECK(rg.y <= (uint64_t)a.kv_cap && j >= 0, "raster: tile range / Gaussian index");
       const float4 p = a.pa[j];
       s_uv[threadIdx.x] = make_float2(p.x, p.y);
       const float4 b = a.pb[j];
@@ -927,6 +931,7 @@ cudaError_t launch_sraster(const SCam& cam, int Lr, ScreenBufs& b, float* out, f
   SRasterArgs a{b.ranges, b.val, b.pa, b.pb, b.pc, out, outT, last, cam,
                 loss ? loss->target : nullptr, loss ? loss->valid : nullptr, loss ? loss->eps : 0.f,
                 loss ? loss->mode : 0, loss ? loss->dLdC : nullptr, loss ? loss->partial : nullptr};
+  a.kv_cap = b.kv_cap;
   k_sraster<<<dim3(cam.TX * cam.TY, Lr), kRasterThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
@@ -934,6 +939,7 @@ cudaError_t launch_sraster(const SCam& cam, int Lr, ScreenBufs& b, float* out, f
 cudaError_t launch_sraster_bwd(const SCam& cam, int Lr, ScreenBufs& b, const float* outT, const uint32_t* last,
                                const float* dLdC, float* g2d, cudaStream_t s) {
   SBwdArgs a{b.ranges, b.val, b.pa, b.pb, b.pc, outT, last, dLdC, g2d, cam};
+  a.kv_cap = b.kv_cap;
   k_sraster_bwd<<<dim3(cam.TX * cam.TY, Lr), kRasterThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
