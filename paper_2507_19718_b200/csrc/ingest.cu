@@ -9,8 +9,11 @@
 namespace gsc {
 
 constexpr int kU = 4;   // samples per thread per iteration
+#ifndef GSC_INGEST_MINB
+#define GSC_INGEST_MINB 4   // resident CTAs per SM the register budget is sized for
+#endif
 
-__global__ void __launch_bounds__(256, 4) k_keys(const float* __restrict__ pos, const int32_t* __restrict__ len,
+__global__ void __launch_bounds__(256, GSC_INGEST_MINB) k_keys(const float* __restrict__ pos, const int32_t* __restrict__ len,
                                                  const float* __restrict__ rgb, int level_fixed, int64_t S,
                                                  LevelGeom g, IngestBufs b, float* out_zero) {
   pdl_enter();
@@ -102,7 +105,7 @@ __global__ void __launch_bounds__(256, 4) k_keys(const float* __restrict__ pos, 
   }
 }
 
-__global__ void __launch_bounds__(256, 4) k_scatter(const float* __restrict__ pos, const float* __restrict__ rgb,
+__global__ void __launch_bounds__(256, GSC_INGEST_MINB) k_scatter(const float* __restrict__ pos, const float* __restrict__ rgb,
                                                  int64_t S, const uint32_t* __restrict__ cell_start, IngestBufs b) {
   pdl_enter();
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
