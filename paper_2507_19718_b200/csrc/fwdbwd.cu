@@ -462,11 +462,22 @@ __device__ __forceinline__ void load_pos(const float4* __restrict__ bin, int str
   }
 }
 
+// n / d for n >= 0, d >= 1 (n < 2^22): a float quotient estimate (off by at most one) corrected
+// exactly -- a few instructions instead of the integer division routine.
+__device__ __forceinline__ int div_small(int n, int d, float inv_d) {
+  if (n >= (1 << 22)) return n / d;              // (estimate error could exceed one)
+  int q = __float2int_rz(__int2float_rn(n) * inv_d);
+  const int r = n - q * d;
+  q += (r >= d) - (r < 0);
+  return q;
+}
+
 // Centre of a work item's cell (fp32; any point of the cell would do as long as every pass
 // of the item uses the same one).
 __device__ __forceinline__ void cell_centre(const CellRef& r, int cell, int l, float& x, float& y, float& z) {
   const int loc = cell - r.coff[l], dx = r.dx[l], dy = r.dy[l];
-  const int cx = loc % dx, t = loc / dx, cy = t % dy, cz = t / dy;
+  const int t = div_small(loc, dx, r.idx[l]), cz = div_small(t, dy, r.idy[l]);
+  const int cx = loc - t * dx, cy = t - cz * dy;
   x = fmaf((float)cx + 0.5f, r.edge[l][0], r.org[l][0]);
   y = fmaf((float)cy + 0.5f, r.edge[l][1], r.org[l][1]);
   z = fmaf((float)cz + 0.5f, r.edge[l][2], r.org[l][2]);
@@ -729,6 +740,7 @@ CellRef cell_ref(const LevelGeom& g) {
   for (int l = 0; l < g.L; ++l) {
     for (int a = 0; a < 3; ++a) { r.org[l][a] = (float)g.origin[l][a]; r.edge[l][a] = (float)g.edge[l][a]; }
     r.dx[l] = g.dims[l][0]; r.dy[l] = g.dims[l][1]; r.coff[l] = (int)g.coff[l];
+    r.idx[l] = 1.f / (float)r.dx[l]; r.idy[l] = 1.f / (float)r.dy[l];
   }
   return r;
 }

@@ -121,6 +121,7 @@ void launch_levels_of(const uint2* kr, int64_t S, const LevelGeom& g, int32_t* o
 struct CellRef {
   float org[kMaxL][3], edge[kMaxL][3];
   int dx[kMaxL], dy[kMaxL], coff[kMaxL];
+  float idx[kMaxL], idy[kMaxL];   // 1 / dx, 1 / dy (quotient estimates, corrected exactly)
 };
 CellRef cell_ref(const LevelGeom& g);
 struct FitArgs {
