@@ -734,58 +734,69 @@ cudaError_t launch_skeys_sort(int64_t g0, int64_t g1, const LevelGeom& g, int le
 // from k_sproject), then a per-tile sort of (depth bits << 32 | index).  The 64-bit key orders
 // a tile's Gaussians by depth with ties by index (the global sort's order, reading A23).
 //
-// The scatter spreads the (Gaussian, tile) pairs of a warp's 32 Gaussians evenly over its
-// lanes (warp prefix sum of the rectangle areas, then each lane finds its pair's Gaussian by a
-// 5-step binary search over the prefix): a lane issues ceil(pairs / 32) returning atomics in
-// sequence instead of its own rectangle's area (up to ~200 tiles for the top level at 1080p).
-template <typename F>
-__device__ __forceinline__ void for_each_tile(int64_t g0, int64_t g1, const int4* __restrict__ rect, F&& f) {
-  const int lane = threadIdx.x & 31;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = g0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane; base < g1; base += stride) {
-    const int64_t j = base + lane;
-    int4 r = make_int4(0, 0, 0, 0);
-    if (j < g1) r = rect[j];
-    const int w = max(r.y - r.x, 0), area = w * max(r.w - r.z, 0);
-    int inc = area;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += y;
-    }
-    const int exc = inc - area, tot = __shfl_sync(0xffffffffu, inc, 31);
-    for (int p0 = 0; p0 < tot; p0 += 32) {
-      const int p = p0 + lane;
-      int src = 0;                                  // the last lane with exc <= p (its area > 0)
-#pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int e = __shfl_sync(0xffffffffu, exc, src + step);
-        if (e <= p) src += step;
-      }
-      const int64_t js = __shfl_sync(0xffffffffu, j, src);
-      const int rx = __shfl_sync(0xffffffffu, r.x, src), rz = __shfl_sync(0xffffffffu, r.z, src);
-      const int ws = __shfl_sync(0xffffffffu, w, src), es = __shfl_sync(0xffffffffu, exc, src);
-      if (p < tot) {
-        const int i = p - es, ty = i / ws;
-        f(js, rx + (i - ty * ws), rz + ty);
-      }
-    }
-  }
-}
+// The scatter spreads the (Gaussian, tile) pairs of a warp's Gaussians evenly over its lanes:
+// a lane issues ceil(pairs / 32) returning atomics in sequence instead of its own rectangle's
+// area (up to ~200 tiles for the top level at 1080p).
+// Tile scatter: each warp owns kScatterGW Gaussians (lanes 0 .. kScatterGW-1 load their
+// projection record, level and rectangle once), the warp's (Gaussian, tile) pairs are spread
+// over all 32 lanes (prefix over the rectangles' areas, a binary search for a pair's owner),
+// and a pair's record fields arrive by shuffles instead of per-pair dependent loads.  Few
+// Gaussians per warp keep many warps in flight: the pass is a chain of dependent round trips
+// (rectangle -> cursor atomic -> key store), not bandwidth.
+constexpr int kScatterGW = 8;
 
 __global__ void k_tile_scatter(int64_t g0, int64_t g1, LevelGeom g, int lev0, int ntiles_img, int TX,
                                const float4* __restrict__ pa, const float4* __restrict__ pb,
                                const int4* __restrict__ rect,
                                const uint32_t* __restrict__ start, uint32_t* cursor, uint64_t* key, uint32_t cap) {
-  for_each_tile(g0, g1, rect, [&](int64_t j, int tx, int ty) {
-    const float4 p = pa[j];
-    if (!tile_hit(p.x, p.y, pb[j].w, tx, ty)) return;
-    const int l = level_of_gaussian(g, j) - lev0;
-    const uint64_t k = ((uint64_t)__float_as_uint(p.z) << 32) | (uint64_t)(uint32_t)j;
-    const size_t t = (size_t)l * ntiles_img + ty * TX + tx;
-    const uint32_t pos = start[t] + atomicAdd(cursor + t, 1u);
-    if (pos < cap) key[pos] = k;                  // (over capacity: the caller grows and re-runs)
-  });
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = g0 + warp * kScatterGW; base < g1; base += nwarps * kScatterGW) {
+    const int64_t j = base + lane;
+    int4 r = make_int4(0, 0, 0, 0);
+    float u = 0.f, v = 0.f, R = 0.f;
+    uint32_t dbits = 0u;
+    int l = 0;
+    if (lane < kScatterGW && j < g1) {
+      r = rect[j];
+      const float4 p = pa[j];
+      u = p.x; v = p.y; dbits = __float_as_uint(p.z); R = pb[j].w;
+      l = level_of_gaussian(g, j) - lev0;
+    }
+    const int w = max(r.y - r.x, 0), area = w * max(r.w - r.z, 0);
+    int inc = area;
+#pragma unroll
+    for (int o = 1; o < kScatterGW; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const int exc = inc - area, tot = __shfl_sync(0xffffffffu, inc, kScatterGW - 1);
+    for (int p0 = 0; p0 < tot; p0 += 32) {
+      const int q = p0 + lane;
+      int src = 0;                                  // the last owner lane with exc <= q (its area > 0)
+#pragma unroll
+      for (int step = kScatterGW / 2; step > 0; step >>= 1) {
+        const int e = __shfl_sync(0xffffffffu, exc, src + step);
+        if (e <= q) src += step;
+      }
+      const int rx = __shfl_sync(0xffffffffu, r.x, src), rz = __shfl_sync(0xffffffffu, r.z, src);
+      const int ws = __shfl_sync(0xffffffffu, w, src), es = __shfl_sync(0xffffffffu, exc, src);
+      const float us = __shfl_sync(0xffffffffu, u, src), vs = __shfl_sync(0xffffffffu, v, src);
+      const float Rs = __shfl_sync(0xffffffffu, R, src);
+      const uint32_t ds = __shfl_sync(0xffffffffu, dbits, src);
+      const int ls = __shfl_sync(0xffffffffu, l, src);
+      if (q < tot) {
+        const int i = q - es, ty = rz + i / ws, tx = rx + (i - (i / ws) * ws);
+        if (tile_hit(us, vs, Rs, tx, ty)) {
+          const uint64_t k = ((uint64_t)ds << 32) | (uint64_t)(uint32_t)(base + src);
+          const size_t t = (size_t)ls * ntiles_img + ty * TX + tx;
+          const uint32_t pos = start[t] + atomicAdd(cursor + t, 1u);
+          if (pos < cap) key[pos] = k;              // (over capacity: the caller grows and re-runs)
+        }
+      }
+    }
+  }
 }
 
 // Bitonic sort of one tile's n <= 32 E keys by one warp, E keys per lane in registers (lane
@@ -914,7 +925,8 @@ cudaError_t launch_tile_sort(int64_t g0, int64_t g1, const LevelGeom& g, int lev
   // tcount was filled by k_sproject
   launch_scan_u32(tcount, nt, tbsums, ttotal, tstart, s);
   const uint32_t cap = (uint32_t)std::min<int64_t>(b.kv_cap, 0xFFFFFFFFll);
-  k_tile_scatter<<<sblocks(g1 - g0), 256, 0, s>>>(g0, g1, g, lev0, ntiles, cam.TX, b.pa, b.pb, b.rect, tstart, tcursor,
+  const int scatter_blocks = (int)std::max<int64_t>(1, std::min<int64_t>((g1 - g0 + 8 * kScatterGW - 1) / (8 * kScatterGW), 148 * 16));
+  k_tile_scatter<<<scatter_blocks, 256, 0, s>>>(g0, g1, g, lev0, ntiles, cam.TX, b.pa, b.pb, b.rect, tstart, tcursor,
                                                   b.key, cap);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
