@@ -211,8 +211,46 @@ __global__ void __launch_bounds__(kScanB) k_sscan_apply(const uint32_t* __restri
   for (int k = 0; k < kScanPer; ++k) if (base + k < n) { out[base + k] = off; off += v[k]; }
 }
 
+// Up to kScanSingleMax entries: one CTA scans them all (one launch instead of three, which
+// at these sizes -- 32 k tile counters at 1080p -- are a chain of fixed latencies).  Thread t
+// owns 32 consecutive entries, loaded as 8 x uint4 all in flight before any is summed.
+constexpr int kScanSinglePer = 32, kScanSingleMax = kScanB * kScanSinglePer;
+__global__ void __launch_bounds__(kScanB) k_sscan_single(const uint32_t* __restrict__ in, int n, uint32_t* total,
+                                                        uint32_t* out) {
+  const int b = threadIdx.x * kScanSinglePer;
+  uint4 v[kScanSinglePer / 4];
+#pragma unroll
+  for (int k = 0; k < kScanSinglePer / 4; ++k) {
+    const int i = b + 4 * k;
+    if (i + 4 <= n) v[k] = *reinterpret_cast<const uint4*>(in + i);
+    else v[k] = make_uint4(i < n ? in[i] : 0u, i + 1 < n ? in[i + 1] : 0u, i + 2 < n ? in[i + 2] : 0u, 0u);
+  }
+  uint32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanSinglePer / 4; ++k) s += v[k].x + v[k].y + v[k].z + v[k].w;
+  uint32_t tot;
+  uint32_t off = block_scan_excl(s, &tot);
+#pragma unroll
+  for (int k = 0; k < kScanSinglePer / 4; ++k) {
+    const int i = b + 4 * k;
+    uint4 o;
+    o.x = off; off += v[k].x; o.y = off; off += v[k].y; o.z = off; off += v[k].z; o.w = off; off += v[k].w;
+    if (i + 4 <= n) *reinterpret_cast<uint4*>(out + i) = o;
+    else {
+      if (i < n) out[i] = o.x;
+      if (i + 1 < n) out[i + 1] = o.y;
+      if (i + 2 < n) out[i + 2] = o.z;
+    }
+  }
+  if (threadIdx.x == 0) *total = tot;
+}
+
 // exclusive scan of n u32 (bsums: >= n / 4096 + 2 words, total: 1 word), deterministic
 void launch_scan_u32(const uint32_t* in, int64_t n, uint32_t* bsums, uint32_t* total, uint32_t* out, cudaStream_t s) {
+  if (n <= kScanSingleMax && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
+    k_sscan_single<<<1, kScanB, 0, s>>>(in, (int)n, total, out);
+    return;
+  }
   const int nb = (int)((n + kScanChunk - 1) / kScanChunk);
   k_sscan_blocks<<<std::max(nb, 1), kScanB, 0, s>>>(in, n, bsums);
   k_sscan_top<<<1, kScanB, 0, s>>>(bsums, nb, total);
