@@ -31,6 +31,9 @@ __global__ void k_step_scalars(const LvlStats* __restrict__ lvl, DevState* st, S
 }
 
 constexpr int kAdamThreads = 128, kAdamBlocksPerSM = 4;
+#ifndef GSC_ADAM_GRID
+#define GSC_ADAM_GRID kAdamBlocksPerSM   // CTAs per SM of the grid (A/B: fewer leave the ingest room)
+#endif
 
 struct AdamHP {
   float wd[GC_NGROUPS]; float beta1, beta2, eps; double tau;
@@ -197,7 +200,7 @@ void launch_adamw(int64_t G, float* P, float* M, float* V, float* grad, CullBufs
   for (int k = 0; k < GC_NGROUPS; ++k) h.frozen |= (hp.lr[k] == 0.f ? 1 : 0) << k;
   {
     ProfScope ps(prof, "adamw", s);
-    int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((G + kAdamThreads - 1) / kAdamThreads, 148 * kAdamBlocksPerSM));
+    int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((G + kAdamThreads - 1) / kAdamThreads, 148 * GSC_ADAM_GRID));
     launch_pdl(k_adamw, dim3(blocks), dim3(kAdamThreads), 0, s, G, P, M, V, grad, dbg_grad, st, h, g, nonfinite,
                raw_grad);
   }

@@ -79,6 +79,25 @@ __global__ void k_cull_emit(int64_t G, CullBufs cb, const float* __restrict__ P,
   }
 }
 
+// Grid of the record / emit passes of the culling rebuild.  They run beside the next call's
+// sample ingest (deferred optimizer step), one latency-bound Gaussian per thread; a grid that
+// fills every SM's register file (the old 4-5 CTAs per SM at cfg2) starves the ingest on the
+// frame's critical path, so the grid is capped at GSC_CULL_GRID CTAs per SM unless that would
+// give a thread more than GSC_CULL_PER_THREAD Gaussians (large caches keep their parallelism).
+// Measured at cfg2 (same-box A/B, frame): 32 (no cap) 0.380 ms, 4: 0.378, 3: 0.374, 2: 0.372,
+// 1: 0.414.
+#ifndef GSC_CULL_GRID
+#define GSC_CULL_GRID 2
+#endif
+#ifndef GSC_CULL_PER_THREAD
+#define GSC_CULL_PER_THREAD 2     // cfg4 (1.4 M Gaussians): 4.288 -> 4.285 ms, i.e. unchanged
+#endif
+static int cull_blocks(int64_t G) {
+  const int64_t need = (G + 127) / 128;
+  const int64_t floor_ = (G + 128 * GSC_CULL_PER_THREAD - 1) / (128 * GSC_CULL_PER_THREAD);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(need, std::max<int64_t>(148 * GSC_CULL_GRID, floor_)));
+}
+
 // ---------------------------------------------------------------------------- scan
 // Block-wide exclusive scan of (a, b) pairs, kScanThreads threads.
 __device__ __forceinline__ uint2 block_excl_scan(uint2 v, uint2& total) {
@@ -312,8 +331,7 @@ void launch_scan(uint32_t* cnt, int64_t n, int ch, uint2* state, uint32_t* total
 
 void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& g, CullBufs cb, DevState* st,
                         cudaStream_t s) {
-  int blocks = (int)std::min<int64_t>((G + 127) / 128, 148 * 32);
-  if (blocks < 1) blocks = 1;
+  const int blocks = cull_blocks(G);
   launch_pdl(k_record_cull, dim3(blocks), dim3(128), 0, s, G, P, tau, g, cb, st);
 }
 
@@ -321,8 +339,7 @@ void launch_cull_emit(int64_t G, CullBufs cb, const float* P, const LevelGeom& g
                       uint32_t cap, DevState* st, const uint32_t* total, uint32_t* host_total,
                       cudaStream_t s, Profiler* prof) {
   ProfScope ps(prof, "cull_emit", s);
-  int blocks = (int)std::min<int64_t>((G + 127) / 128, 148 * 32);
-  if (blocks < 1) blocks = 1;
+  const int blocks = cull_blocks(G);
   launch_pdl(k_cull_emit, dim3(blocks), dim3(128), 0, s, G, cb, P, g, off, cap, st, total, host_total);
 }
 
