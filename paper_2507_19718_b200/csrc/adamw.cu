@@ -109,7 +109,10 @@ __device__ void chain_rule(const float p[kNP], const float cg[12], float out[kNP
 // Fused normalise + chain rule + AdamW of one Gaussian per thread (A6); zeroes the gradient
 // slots it consumes.  The next step's evaluation record and culling counts are emitted by
 // k_record_cull right after (split so both kernels stay spill-free and latency-hidden).
-__global__ void __launch_bounds__(kAdamThreads, kAdamBlocksPerSM) k_adamw(
+#ifndef GSC_ADAM_MINB
+#define GSC_ADAM_MINB kAdamBlocksPerSM
+#endif
+__global__ void __launch_bounds__(kAdamThreads, GSC_ADAM_MINB) k_adamw(
     int64_t G, float* __restrict__ P, float* __restrict__ M, float* __restrict__ V, float* __restrict__ grad,
     float* __restrict__ dbg, DevState* st, AdamHP hp, LevelGeom g, unsigned long long* nonfinite,
     const float* __restrict__ rawg) {

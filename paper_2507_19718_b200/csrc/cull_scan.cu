@@ -6,7 +6,10 @@
 
 namespace gsc {
 
-__global__ void k_record_cull(int64_t G, const float* __restrict__ P, double tau, LevelGeom g, CullBufs cb,
+#ifndef GSC_REC_MINB
+#define GSC_REC_MINB 1
+#endif
+__global__ void __launch_bounds__(128, GSC_REC_MINB) k_record_cull(int64_t G, const float* __restrict__ P, double tau, LevelGeom g, CullBufs cb,
                               DevState* st) {
   pdl_enter();
   if (cb.ovf) { cb.ovf = st->lovf; cb.ovf_cap = st->lovf_cap; }   // current buffers (DevState)
