@@ -289,7 +289,7 @@ static gc_status rebuild_csr(gc_cache c, cudaStream_t s, bool recompute_records)
               &c->prof);
   // (the rebuild's entry count goes to pinned memory for the capacity guard of later calls)
   launch_cull_emit(c->G, cull_bufs(c), c->P, c->geom, c->csr_off, c->csr_cap, c->st, c->csr_totals, c->hcsr,
-                   s, &c->prof);
+                   s, &c->prof, c->hp.lr[GC_SCALE] == 0.f);
   CK(cudaGetLastError());
   return GC_OK;
 }

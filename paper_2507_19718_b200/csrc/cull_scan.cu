@@ -88,15 +88,19 @@ __global__ void k_cull_emit(int64_t G, CullBufs cb, const float* __restrict__ P,
 // frame's critical path, so the grid is capped at GSC_CULL_GRID CTAs per SM unless that would
 // give a thread more than GSC_CULL_PER_THREAD Gaussians (large caches keep their parallelism).
 // Measured at cfg2 (same-box A/B, frame): 32 (no cap) 0.380 ms, 4: 0.378, 3: 0.374, 2: 0.372,
-// 1: 0.414.
+// 1: 0.414.  The emit pass is capped only while the scale group is frozen (lr 0, the paper's
+// setting): with scales training (rotated anisotropic caches, the bench's general leg) the
+// rebuild chain is longer and a capped emit delays the evaluators (general frame: both capped
+// 0.455 ms, record only 0.445, neither 0.447).
 #ifndef GSC_CULL_GRID
 #define GSC_CULL_GRID 2
 #endif
 #ifndef GSC_CULL_PER_THREAD
 #define GSC_CULL_PER_THREAD 2     // cfg4 (1.4 M Gaussians): 4.288 -> 4.285 ms, i.e. unchanged
 #endif
-static int cull_blocks(int64_t G) {
+static int cull_blocks(int64_t G, bool capped = true) {
   const int64_t need = (G + 127) / 128;
+  if (!capped) return (int)std::max<int64_t>(1, std::min<int64_t>(need, 148 * 32));
   const int64_t floor_ = (G + 128 * GSC_CULL_PER_THREAD - 1) / (128 * GSC_CULL_PER_THREAD);
   return (int)std::max<int64_t>(1, std::min<int64_t>(need, std::max<int64_t>(148 * GSC_CULL_GRID, floor_)));
 }
@@ -340,9 +344,9 @@ void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& 
 
 void launch_cull_emit(int64_t G, CullBufs cb, const float* P, const LevelGeom& g, const uint32_t* off,
                       uint32_t cap, DevState* st, const uint32_t* total, uint32_t* host_total,
-                      cudaStream_t s, Profiler* prof) {
+                      cudaStream_t s, Profiler* prof, bool capped) {
   ProfScope ps(prof, "cull_emit", s);
-  const int blocks = cull_blocks(G);
+  const int blocks = cull_blocks(G, capped);
   launch_pdl(k_cull_emit, dim3(blocks), dim3(128), 0, s, G, cb, P, g, off, cap, st, total, host_total);
 }
 

@@ -93,7 +93,7 @@ void launch_record_cull(int64_t G, const float* P, double tau, const LevelGeom& 
 // host_total (page-locked, nullable): receives the rebuild's entry count (written by the kernel)
 void launch_cull_emit(int64_t G, CullBufs cb, const float* P, const LevelGeom& g, const uint32_t* off,
                       uint32_t cap, DevState* st, const uint32_t* total, uint32_t* host_total,
-                      cudaStream_t s, Profiler* prof);
+                      cudaStream_t s, Profiler* prof, bool capped = true);
 
 // ingest.cu
 struct IngestBufs {

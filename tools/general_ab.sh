@@ -1,0 +1,6 @@
+cp paper_2507_19718_b200/libgscache.so gpurun_var_base.so
+for rep in 1 2; do for v in $VARIANTS; do
+  cp gpurun_var_$v.so paper_2507_19718_b200/libgscache.so
+  echo "$v $(timeout 300 python tools/general_case.py 2>&1 | head -3 | tr '\n' ' ')"
+done; done
+cp gpurun_var_base.so paper_2507_19718_b200/libgscache.so
