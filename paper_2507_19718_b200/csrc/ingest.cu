@@ -155,7 +155,10 @@ __global__ void k_levels_of(const uint2* kr, int64_t S, LevelGeom g, int32_t* ou
   }
 }
 
-static int grid_for(int64_t n, int per_sm = 12) {
+#ifndef GSC_INGEST_GRID
+#define GSC_INGEST_GRID 12   // CTAs per SM of the keys / scatter grids (A/B knob)
+#endif
+static int grid_for(int64_t n, int per_sm = GSC_INGEST_GRID) {
   int64_t b = (n + 256 * kU - 1) / (256 * kU);
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * per_sm));
 }
