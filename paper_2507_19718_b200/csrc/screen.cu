@@ -889,7 +889,10 @@ constexpr int kTileSortMax = 8192;           // items per tile sorted in shared 
 
 // one warp per (level, tile): ranges, then the register sort; larger tiles are appended to
 // `list` (list_n = big[1]) for the shared-memory kernel
-__global__ void k_tile_sort_warp(const uint32_t* __restrict__ start, const uint32_t* __restrict__ total, int nt,
+#ifndef GSC_TSW_MINB
+#define GSC_TSW_MINB 6   // 40 registers (a little spill in the rare 256-key sort): 3 -> 6 CTAs per SM; render 277 -> 273 us, fit_image 626 -> 621 us
+#endif
+__global__ void __launch_bounds__(256, GSC_TSW_MINB) k_tile_sort_warp(const uint32_t* __restrict__ start, const uint32_t* __restrict__ total, int nt,
                                  uint64_t* key, int64_t* val, uint2* ranges, uint32_t* list, uint32_t* big,
                                  uint32_t cap) {
   if (*total > cap) return;                               // keys over capacity: re-run after growing
