@@ -350,7 +350,11 @@ constexpr int kRasterThreads = kTileThreads / 2;
 #define GSC_BWD_DIRECT 24
 #endif
 
+#ifdef GSC_SFWD_MINB
+__global__ void __launch_bounds__(kRasterThreads, GSC_SFWD_MINB) k_sraster(SRasterArgs a) {
+#else
 __global__ void __launch_bounds__(kRasterThreads) k_sraster(SRasterArgs a) {
+#endif
   __shared__ float2 s_uv[kRasterThreads];
   __shared__ float4 s_co[kRasterThreads];     // scaled conic (scaled_conic), w
   __shared__ float4 s_c[kRasterThreads];
@@ -507,7 +511,11 @@ __device__ __forceinline__ void pix_bwd2(PixBwd2& p, bool u0, bool u1, float4 co
   d[5] = d5.x + d5.y; d[6] = d6.x + d6.y; d[7] = d7.x + d7.y; d[8] = d8.x + d8.y;
 }
 
+#ifdef GSC_SBWD_MINB
+__global__ void __launch_bounds__(kRasterThreads, GSC_SBWD_MINB) k_sraster_bwd(SBwdArgs a) {
+#else
 __global__ void __launch_bounds__(kRasterThreads) k_sraster_bwd(SBwdArgs a) {
+#endif
   __shared__ float2 s_uv[kRasterThreads];
   __shared__ float4 s_co[kRasterThreads];
   __shared__ float4 s_c[kRasterThreads];
